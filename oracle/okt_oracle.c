@@ -1,0 +1,550 @@
+/*
+ * okt_oracle.c — plain-C restatement of the reference's Ok-Topk hot path.
+ * TEST INFRASTRUCTURE ONLY (see okt_oracle.h).  Paths are relative to
+ * /root/reference/proj.  Compiled with -ffp-contract=off so every double
+ * operation rounds exactly as the reference's (non-FMA) build does.
+ */
+#include "okt_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define GAMMA 0x9e3779b97f4a7c15ULL
+
+/* ---- rng.hpp:11-49 ------------------------------------------------------- */
+uint64_t orc_splitmix64(uint64_t x) {
+  x += GAMMA;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+uint64_t orc_mix64(uint64_t a, uint64_t b) {
+  return orc_splitmix64(a ^ (GAMMA + b + (a << 6) + (a >> 2)));
+}
+
+static double unit_from_bits(uint64_t bits) { return (double)(bits >> 11) * 0x1.0p-53; }
+
+/* SplitMix64::next (rng.hpp:33-39) */
+static uint64_t sm_next(uint64_t* state) {
+  *state += GAMMA;
+  uint64_t z = *state;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+/* tests/test_util.hpp:135-140 */
+void orc_random_dense(uint64_t seed, size_t n, double* out) {
+  uint64_t s = seed;
+  for (size_t i = 0; i < n; ++i) out[i] = 2.0 * unit_from_bits(sm_next(&s)) - 1.0;
+}
+
+/* tests/test_util.hpp:144-153 */
+void orc_random_int_dense(uint64_t seed, size_t n, int hi, double* out) {
+  uint64_t s = seed;
+  const uint64_t span = 2 * (uint64_t)hi + 1;
+  for (size_t i = 0; i < n; ++i) out[i] = (double)((int64_t)(sm_next(&s) % span) - hi);
+}
+
+/* trainer.cpp:338-388 */
+int orc_drift(int64_t t, uint64_t seed, size_t n, uint64_t rank_key, int fixed_positions, double* g) {
+  if (t < 1) return -1;
+  const uint64_t epoch = (uint64_t)((t - 1) / 1024);
+  const double scale = pow(0.95, (double)epoch);
+  if (n == 0) return 0;
+  const uint64_t stream = orc_mix64(seed, orc_mix64(0x72616e6bu, rank_key));
+  const uint64_t pair = (uint64_t)((t + 1) / 2);
+  const double noise_sign = (t % 2 == 1) ? 1.0 : -1.0;
+  const uint64_t noise_key = orc_mix64(orc_mix64(stream, 0x6e6f6973u), pair);
+  for (size_t i = 0; i < n; ++i) {
+    const double u = unit_from_bits(orc_mix64(noise_key, i));
+    g[i] = noise_sign * 0.04 * scale * (2.0 * u - 1.0);
+  }
+  const uint64_t heavy_epoch = fixed_positions ? 0 : epoch;
+  const uint64_t pos_key = orc_mix64(orc_mix64(seed, 0x65706f73u), heavy_epoch);
+  const uint64_t mag_key = orc_mix64(orc_mix64(stream, 0x656d6167u), heavy_epoch);
+  const uint64_t jit_key = orc_mix64(stream, 0x6a697474u);
+  const size_t slots = n / 100 > 1 ? n / 100 : 1;
+  unsigned char* taken = (unsigned char*)calloc(n, 1);
+  if (!taken) return -3;
+  for (size_t h = 0; h < slots; ++h) {
+    size_t pos = (size_t)(orc_mix64(pos_key, h) % n);
+    while (taken[pos]) pos = (pos + 1) % n;
+    taken[pos] = 1;
+    const uint64_t mag_bits = orc_mix64(mag_key, h);
+    double mag = (1.0 + unit_from_bits(mag_bits)) * scale;
+    if (!fixed_positions) {
+      const double u = unit_from_bits(orc_mix64(orc_mix64(jit_key, (uint64_t)t), h));
+      mag *= 1.0 + 0.08 * (2.0 * u - 1.0);
+    }
+    g[pos] = (mag_bits & 1u) ? mag : -mag;
+  }
+  free(taken);
+  return 0;
+}
+
+void orc_state_init(orc_state* s) {
+  memset(s, 0, sizeof(*s));
+  s->tau = 64;            /* sparse.hpp:59 */
+  s->tau_prime = 32;      /* sparse.hpp:60 */
+  s->last_local_eval = -1;
+  s->last_global_eval = -1;
+  s->regions = -1;
+  s->bucket_size = 4;     /* oktopk.hpp:34 */
+}
+
+/* ---- selection ----------------------------------------------------------- */
+/* k-th smallest of a[0..n) (0-based kth), in place (quickselect). */
+static double kth_smallest(double* a, ptrdiff_t n, ptrdiff_t kth) {
+  ptrdiff_t lo = 0, hi = n - 1;
+  while (lo < hi) {
+    double x = a[lo], y = a[lo + (hi - lo) / 2], z = a[hi];
+    double pivot = (x < y) ? ((y < z) ? y : ((x < z) ? z : x)) : ((x < z) ? x : ((y < z) ? z : y));
+    ptrdiff_t i = lo, j = hi;
+    while (i <= j) {
+      while (a[i] < pivot) ++i;
+      while (a[j] > pivot) --j;
+      if (i <= j) {
+        double tmp = a[i];
+        a[i] = a[j];
+        a[j] = tmp;
+        ++i;
+        --j;
+      }
+    }
+    if (kth <= j) hi = j;
+    else if (kth >= i) lo = i;
+    else return a[kth];
+  }
+  return a[lo];
+}
+
+/* topk_from's threshold (sparse.cpp:43-71): for take = min(k, count) < count
+ * the magnitude at position take-1 of the magnitude-descending order, else
+ * the smallest magnitude present — in both cases the take-th largest |v|. */
+double orc_kth_largest_mag(const double* v, size_t count, size_t k) {
+  if (count == 0 || k == 0) return NAN;
+  const size_t take = k < count ? k : count;
+  double* a = (double*)malloc(count * sizeof(double));
+  for (size_t i = 0; i < count; ++i) a[i] = fabs(v[i]);
+  const double th = kth_smallest(a, (ptrdiff_t)count, (ptrdiff_t)(count - take));
+  free(a);
+  return th;
+}
+
+/* sparse.cpp:94-120 (inclusive >=) */
+size_t orc_select(const double* g, size_t n, double th, uint32_t* idx, double* val) {
+  size_t m = 0;
+  for (size_t i = 0; i < n; ++i) {
+    if (fabs(g[i]) >= th) {
+      if (idx) idx[m] = (uint32_t)i;
+      if (val) val[m] = g[i];
+      ++m;
+    }
+  }
+  return m;
+}
+
+static size_t select_sparse(const uint32_t* idx, const double* val, size_t nnz, double th, uint32_t* oi,
+                            double* ov) {
+  size_t m = 0;
+  for (size_t i = 0; i < nnz; ++i)
+    if (fabs(val[i]) >= th) {
+      oi[m] = idx[i];
+      ov[m] = val[i];
+      ++m;
+    }
+  return m;
+}
+
+/* collectives.cpp:79-87 */
+void orc_equal_slice_ends(uint64_t n, int P, uint64_t* ends) {
+  const uint64_t base = n / (uint64_t)P, rem = n % (uint64_t)P;
+  ends[0] = 0;
+  for (int r = 0; r < P; ++r) ends[r + 1] = ends[r] + base + ((uint64_t)r < rem ? 1 : 0);
+}
+
+/* ---- sparse_sum (sparse.cpp:206-257) ---------------------------------------- */
+typedef struct {
+  uint32_t* idx;
+  double* val;
+  size_t nnz;
+} part_t;
+
+/* merge_two (sparse.cpp:206-236): union in ascending index order, a + b on ties. */
+static part_t merge_two(part_t a, part_t b) {
+  part_t o;
+  o.idx = (uint32_t*)malloc((a.nnz + b.nnz + 1) * sizeof(uint32_t));
+  o.val = (double*)malloc((a.nnz + b.nnz + 1) * sizeof(double));
+  size_t i = 0, j = 0, m = 0;
+  while (i < a.nnz && j < b.nnz) {
+    if (a.idx[i] < b.idx[j]) {
+      o.idx[m] = a.idx[i];
+      o.val[m++] = a.val[i++];
+    } else if (b.idx[j] < a.idx[i]) {
+      o.idx[m] = b.idx[j];
+      o.val[m++] = b.val[j++];
+    } else {
+      o.idx[m] = a.idx[i];
+      o.val[m++] = a.val[i] + b.val[j];
+      ++i;
+      ++j;
+    }
+  }
+  for (; i < a.nnz; ++i) {
+    o.idx[m] = a.idx[i];
+    o.val[m++] = a.val[i];
+  }
+  for (; j < b.nnz; ++j) {
+    o.idx[m] = b.idx[j];
+    o.val[m++] = b.val[j];
+  }
+  o.nnz = m;
+  return o;
+}
+
+static part_t copy_part(part_t p) {
+  part_t o;
+  o.idx = (uint32_t*)malloc((p.nnz + 1) * sizeof(uint32_t));
+  o.val = (double*)malloc((p.nnz + 1) * sizeof(double));
+  memcpy(o.idx, p.idx, p.nnz * sizeof(uint32_t));
+  memcpy(o.val, p.val, p.nnz * sizeof(double));
+  o.nnz = p.nnz;
+  return o;
+}
+
+/* stride_sum (sparse.cpp:238-245): sum(q, s) = sum(q, 2s) + sum(q+s, 2s). */
+static part_t stride_sum(const part_t* parts, int P, int q, int s) {
+  if (q + s >= P) return copy_part(parts[q]);
+  part_t a = stride_sum(parts, P, q, 2 * s);
+  part_t b = stride_sum(parts, P, q + s, 2 * s);
+  part_t o = merge_two(a, b);
+  free(a.idx);
+  free(a.val);
+  free(b.idx);
+  free(b.val);
+  return o;
+}
+
+size_t orc_sparse_sum(int P, const uint32_t* const* idx, const double* const* val, const size_t* nnz,
+                      uint32_t* out_idx, double* out_val) {
+  if (P <= 0) return 0;
+  part_t parts[ORC_MAX_P];
+  for (int q = 0; q < P; ++q) {
+    parts[q].idx = (uint32_t*)idx[q];
+    parts[q].val = (double*)val[q];
+    parts[q].nnz = nnz[q];
+  }
+  part_t o = stride_sum(parts, P, 0, 1);
+  memcpy(out_idx, o.idx, o.nnz * sizeof(uint32_t));
+  memcpy(out_val, o.val, o.nnz * sizeof(double));
+  const size_t m = o.nnz;
+  free(o.idx);
+  free(o.val);
+  return m;
+}
+
+/* ---- ledger helpers (transport.cpp:71-93, 103-160; collectives.cpp:30-77) ---- */
+static int log2i(int p) {
+  int l = 0;
+  while ((1 << l) < p) ++l;
+  return l;
+}
+
+static void credit(orc_counters* L, int P, int r, int ph, int send, uint64_t words) {
+  (void)P;
+  if (!L) return;
+  orc_counters* c = &L[r * ORC_PHASES + ph];
+  if (send) {
+    c->words_sent += words;
+    c->msgs_sent += 1;
+  } else {
+    c->words_recv += words;
+    c->msgs_recv += 1;
+  }
+}
+
+/* sparse_allgatherv's recursive doubling accounting over part sizes. */
+static void credit_allgatherv(orc_counters* L, int P, int ph, const uint64_t* parts) {
+  const int rounds = log2i(P);
+  for (int r = 0; r < P; ++r)
+    for (int j = 0; j < rounds; ++j) {
+      const int width = 1 << j, partner = r ^ width;
+      const int mb = r & ~(width - 1), pb = partner & ~(width - 1);
+      uint64_t ms = 0, ps = 0;
+      for (int q = 0; q < width; ++q) {
+        ms += parts[mb + q];
+        ps += parts[pb + q];
+      }
+      credit(L, P, r, ph, 1, 2 * ms);
+      credit(L, P, r, ph, 0, 2 * ps);
+    }
+}
+
+/* ---- space_repartition (oktopk.cpp:28-61) -------------------------------------- */
+void orc_space_repartition(int P, const uint32_t* const* sel, const size_t* m, uint64_t n, uint64_t* cuts,
+                           orc_counters* ledger) {
+  double vec[ORC_MAX_P][ORC_MAX_P + 1], nxt[ORC_MAX_P][ORC_MAX_P + 1];
+  for (int r = 0; r < P; ++r) {
+    vec[r][0] = 0.0;
+    vec[r][P] = (double)n;
+    for (int q = 1; q < P; ++q) {
+      uint64_t cut;
+      if (m[r] == 0) cut = (uint64_t)q * n / (uint64_t)P;
+      else {
+        const uint64_t pos = (uint64_t)q * m[r] / (uint64_t)P;
+        cut = pos < m[r] ? sel[r][pos] : n;
+      }
+      vec[r][q] = (double)cut;
+    }
+  }
+  /* small_allreduce_avg: recursive doubling, lower-rank block first. */
+  const int rounds = log2i(P);
+  for (int j = 0; j < rounds; ++j) {
+    for (int r = 0; r < P; ++r) {
+      const int partner = r ^ (1 << j);
+      for (int q = 0; q <= P; ++q)
+        nxt[r][q] = partner < r ? vec[partner][q] + vec[r][q] : vec[r][q] + vec[partner][q];
+      credit(ledger, P, r, 3, 1, (uint64_t)(P + 1));
+      credit(ledger, P, r, 3, 0, (uint64_t)(P + 1));
+    }
+    memcpy(vec, nxt, sizeof(vec));
+  }
+  cuts[0] = 0;
+  cuts[P] = n;
+  for (int q = 1; q < P; ++q) {
+    const double avg = vec[0][q] / (double)P;
+    uint64_t rounded = (uint64_t)llround(avg > 0.0 ? avg : 0.0);
+    if (rounded > n) rounded = n;
+    cuts[q] = rounded > cuts[q - 1] ? rounded : cuts[q - 1];
+  }
+}
+
+static size_t lower_bound_u32(const uint32_t* a, size_t n, uint64_t key) {
+  size_t lo = 0, hi = n;
+  while (lo < hi) {
+    size_t mid = (lo + hi) / 2;
+    if ((uint64_t)a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+static uint64_t bucket_count(uint64_t nnz, uint32_t bucket) {
+  if (bucket == 0 || nnz <= bucket) return 1;
+  return (nnz + bucket - 1) / bucket;
+}
+
+/* ---- ok_sparse_allreduce (oktopk.cpp:246-307) ------------------------------------ */
+int orc_ok_sparse_allreduce(int P, orc_state* st, const double* const* g, size_t n, int64_t t, size_t k,
+                            orc_counters* ledger, uint32_t* u_idx, double* u_val, size_t* U,
+                            uint32_t* const* indexes, size_t* n_indexes, size_t* local_selected) {
+  if (n == 0 || k < 1 || t < 1) return -1;
+  if (P < 1 || P > ORC_MAX_P || (P & (P - 1))) return -5;
+  for (int r = 0; r < P; ++r)
+    for (size_t i = 0; i < n; ++i)
+      if (!isfinite(g[r][i])) return -2;
+
+  const int thr = (t - 1) % (int64_t)st[0].tau_prime == 0;
+  const int bnd = (t - 1) % (int64_t)st[0].tau == 0;
+  uint32_t* sel_idx[ORC_MAX_P];
+  double* sel_val[ORC_MAX_P];
+  size_t m[ORC_MAX_P];
+  for (int r = 0; r < P; ++r) {
+    if (thr) {
+      st[r].local_th = orc_kth_largest_mag(g[r], n, k);
+      st[r].last_local_eval = t;
+    }
+    sel_idx[r] = (uint32_t*)malloc((n + 1) * sizeof(uint32_t));
+    sel_val[r] = (double*)malloc((n + 1) * sizeof(double));
+    m[r] = orc_select(g[r], n, st[r].local_th, sel_idx[r], sel_val[r]);
+  }
+  uint64_t cuts[ORC_MAX_P + 1];
+  if (bnd) {
+    orc_space_repartition(P, (const uint32_t* const*)sel_idx, m, n, cuts, ledger);
+    for (int r = 0; r < P; ++r) {
+      memcpy(st[r].cuts, cuts, sizeof(uint64_t) * (P + 1));
+      st[r].regions = P;
+    }
+  } else if (st[0].regions != P) {
+    orc_equal_slice_ends(n, P, cuts);
+    for (int r = 0; r < P; ++r) {
+      memcpy(st[r].cuts, cuts, sizeof(uint64_t) * (P + 1));
+      st[r].regions = P;
+    }
+  } else {
+    memcpy(cuts, st[0].cuts, sizeof(uint64_t) * (P + 1));
+  }
+
+  /* split_and_reduce (oktopk.cpp:95-163) */
+  size_t off[ORC_MAX_P][ORC_MAX_P + 1];
+  for (int r = 0; r < P; ++r) {
+    for (int q = 0; q < P; ++q) off[r][q] = lower_bound_u32(sel_idx[r], m[r], cuts[q]);
+    off[r][P] = m[r];
+  }
+  for (int r = 0; r < P; ++r)
+    for (int s = 1; s < P; ++s) {
+      const int dst = (r + s) % P, src = (r - s + P) % P;
+      const uint64_t out_n = off[r][dst + 1] - off[r][dst];
+      const uint64_t in_n = off[src][r + 1] - off[src][r];
+      const uint64_t ob = bucket_count(out_n, st[r].bucket_size);
+      const uint64_t ib = bucket_count(in_n, st[r].bucket_size);
+      if (ledger) {
+        ledger[r * ORC_PHASES + 0].words_sent += 2 * out_n;
+        ledger[r * ORC_PHASES + 0].msgs_sent += ob;
+        ledger[r * ORC_PHASES + 0].words_recv += 2 * in_n;
+        ledger[r * ORC_PHASES + 0].msgs_recv += ib;
+      }
+    }
+  uint32_t* reg_idx[ORC_MAX_P];
+  double* reg_val[ORC_MAX_P];
+  size_t R[ORC_MAX_P];
+  for (int o = 0; o < P; ++o) {
+    const uint32_t* pi[ORC_MAX_P];
+    const double* pv[ORC_MAX_P];
+    size_t pn[ORC_MAX_P], tot = 0;
+    for (int q = 0; q < P; ++q) {
+      pi[q] = sel_idx[q] + off[q][o];
+      pv[q] = sel_val[q] + off[q][o];
+      pn[q] = off[q][o + 1] - off[q][o];
+      tot += pn[q];
+    }
+    reg_idx[o] = (uint32_t*)malloc((tot + 1) * sizeof(uint32_t));
+    reg_val[o] = (double*)malloc((tot + 1) * sizeof(double));
+    R[o] = orc_sparse_sum(P, pi, pv, pn, reg_idx[o], reg_val[o]);
+  }
+
+  /* global threshold refresh (oktopk.cpp:277-293) */
+  if (thr) {
+    size_t tot = 0;
+    for (int o = 0; o < P; ++o) tot += R[o];
+    if (P > 1) {
+      uint64_t parts[ORC_MAX_P];
+      for (int o = 0; o < P; ++o) parts[o] = R[o];
+      credit_allgatherv(ledger, P, 5, parts);
+    }
+    if (tot > 0) {
+      double* all = (double*)malloc(tot * sizeof(double));
+      size_t w = 0;
+      for (int o = 0; o < P; ++o) {
+        memcpy(all + w, reg_val[o], R[o] * sizeof(double));
+        w += R[o];
+      }
+      const double gth = orc_kth_largest_mag(all, tot, k);
+      free(all);
+      for (int r = 0; r < P; ++r) st[r].global_th = gth;
+    }
+    for (int r = 0; r < P; ++r) st[r].last_global_eval = t;
+  }
+
+  /* balance_and_allgatherv (oktopk.cpp:165-244) */
+  size_t c[ORC_MAX_P], total = 0, maxs = 0;
+  uint32_t* mi[ORC_MAX_P];
+  double* mv[ORC_MAX_P];
+  for (int r = 0; r < P; ++r) {
+    mi[r] = (uint32_t*)malloc((R[r] + 1) * sizeof(uint32_t));
+    mv[r] = (double*)malloc((R[r] + 1) * sizeof(double));
+    c[r] = select_sparse(reg_idx[r], reg_val[r], R[r], st[r].global_th, mi[r], mv[r]);
+    total += c[r];
+    if (c[r] > maxs) maxs = c[r];
+  }
+  if (P > 1) {
+    const int rounds = log2i(P);
+    for (int r = 0; r < P; ++r)
+      for (int j = 0; j < rounds; ++j) {
+        credit(ledger, P, r, 3, 1, (uint64_t)1 << j);
+        credit(ledger, P, r, 3, 0, (uint64_t)1 << j);
+      }
+    uint64_t parts[ORC_MAX_P];
+    for (int r = 0; r < P; ++r) parts[r] = c[r];
+    if (total > 0 && (uint64_t)maxs * (uint64_t)P >= 4 * (uint64_t)total) {
+      uint64_t o[ORC_MAX_P + 1], block[ORC_MAX_P + 1];
+      o[0] = 0;
+      for (int r = 0; r < P; ++r) o[r + 1] = o[r] + c[r];
+      orc_equal_slice_ends(total, P, block);
+      for (int src = 0; src < P; ++src)
+        for (int dst = 0; dst < P; ++dst) {
+          if (src == dst) continue;
+          const uint64_t a = o[src] > block[dst] ? o[src] : block[dst];
+          const uint64_t b = o[src + 1] < block[dst + 1] ? o[src + 1] : block[dst + 1];
+          if (a < b) {
+            credit(ledger, P, src, 1, 1, 2 * (b - a));
+            credit(ledger, P, dst, 1, 0, 2 * (b - a));
+          }
+        }
+      for (int r = 0; r < P; ++r) parts[r] = block[r + 1] - block[r];
+    }
+    credit_allgatherv(ledger, P, 2, parts);
+  }
+  size_t uw = 0;
+  for (int r = 0; r < P; ++r) {
+    memcpy(u_idx + uw, mi[r], c[r] * sizeof(uint32_t));
+    memcpy(u_val + uw, mv[r], c[r] * sizeof(double));
+    uw += c[r];
+  }
+  *U = uw;
+
+  /* indexes = local selection ∩ u (oktopk.cpp:299-302) */
+  for (int r = 0; r < P; ++r) {
+    size_t i = 0, j = 0, w = 0;
+    while (i < m[r] && j < uw) {
+      if (sel_idx[r][i] < u_idx[j]) ++i;
+      else if (u_idx[j] < sel_idx[r][i]) ++j;
+      else {
+        if (indexes && indexes[r]) indexes[r][w] = sel_idx[r][i];
+        ++w;
+        ++i;
+        ++j;
+      }
+    }
+    if (n_indexes) n_indexes[r] = w;
+    if (local_selected) local_selected[r] = m[r];
+    st[r].t = t;
+  }
+  for (int r = 0; r < P; ++r) {
+    free(sel_idx[r]);
+    free(sel_val[r]);
+    free(reg_idx[r]);
+    free(reg_val[r]);
+    free(mi[r]);
+    free(mv[r]);
+  }
+  return 0;
+}
+
+/* ---- oktopk_sgd_step (trainer.cpp:466-488) ---------------------------------------- */
+int orc_sgd_step(int P, orc_state* st, const double* const* grad, double* const* eps, double* const* w,
+                 size_t n, double alpha, int64_t t, size_t k, orc_counters* ledger, uint32_t* u_idx,
+                 double* u_val, size_t* U) {
+  for (int r = 0; r < P; ++r)
+    for (size_t i = 0; i < n; ++i)
+      if (!isfinite(grad[r][i])) return -2;
+  double* acc[ORC_MAX_P];
+  uint32_t* ix[ORC_MAX_P];
+  size_t nix[ORC_MAX_P], sel[ORC_MAX_P];
+  for (int r = 0; r < P; ++r) {
+    acc[r] = (double*)malloc((n + 1) * sizeof(double));
+    ix[r] = (uint32_t*)malloc((n + 1) * sizeof(uint32_t));
+    for (size_t i = 0; i < n; ++i) acc[r][i] = eps[r][i] + alpha * grad[r][i];
+  }
+  const int rc = orc_ok_sparse_allreduce(P, st, (const double* const*)acc, n, t, k, ledger, u_idx, u_val, U, ix,
+                                         nix, sel);
+  if (rc == 0) {
+    for (int r = 0; r < P; ++r) {
+      memcpy(eps[r], acc[r], n * sizeof(double));
+      for (size_t j = 0; j < nix[r]; ++j) eps[r][ix[r][j]] = 0.0;
+      for (size_t j = 0; j < *U; ++j) w[r][u_idx[j]] -= u_val[j] / (double)P;
+    }
+  }
+  for (int r = 0; r < P; ++r) {
+    free(acc[r]);
+    free(ix[r]);
+  }
+  if (rc) return rc;
+  for (int r = 0; r < P; ++r)
+    for (size_t i = 0; i < n; ++i)
+      if (!isfinite(w[r][i])) return -2;
+  return 0;
+}

@@ -1,0 +1,1274 @@
+// okt_core.cpp — host orchestration of the Ok-Topk sparse allreduce and the
+// C-ABI entry points declared in include/okt.h.
+//
+// One okt_comm per rank.  A step (ok_sparse_allreduce, oktopk.cpp:246-307)
+// runs these device phases on the comm's stream:
+//   K1  fused accumulate + select + compact           (every iteration)
+//   K2  radix select of local_th                      (t-1 ≡ 0 mod tau')
+//   K8  proposals + cuts consensus                    (t-1 ≡ 0 mod tau)
+//       slice offsets; counts allgather    <- host sync #1 (P > 1)
+//       rotated slice exchange (split)
+//   K3  scatter + ordered bracket scan of the owned region (fused survivor
+//       filter on steady iterations)
+//   K4  gather + radix select of global_th + filter  (t-1 ≡ 0 mod tau')
+//       survivor-count allgather             <- host sync #2 (P > 1)
+//   K5/K6 balance moves + allgatherv into u
+//   K7  apply: indexes, residual zero, model update  <- host sync #3
+// Thresholds live on the device during a step; the host mirror (okt_state)
+// is committed only when the step succeeds, so a failing step leaves the
+// state, the residual and the model as the reference leaves them.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "../../include/okt.h"
+#include "okt_kernels.hpp"
+#include "okt_transport.hpp"
+
+using okt::Launch;
+using okt::Xfer;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+// ---- device buffers ---------------------------------------------------------
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  bool zero_init = false;
+  ~Buf() {
+    if (p) cudaFree(p);
+  }
+  // Grow-only.  Rare (capacities track the largest n / counts seen).
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    size_t want = std::max<size_t>(bytes, 256);
+    if (p) want = std::max(want, cap + cap / 2);
+    if (p) {
+      cudaError_t e = cudaFree(p);
+      if (e != cudaSuccess) return e;
+      p = nullptr;
+      cap = 0;
+    }
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) return e;
+    cap = want;
+    if (zero_init) return cudaMemset(p, 0, want);
+    return cudaSuccess;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Device-resident scalars of one comm; mirrored to pinned host memory at sync
+// points with a single D2H copy.
+struct DevScalars {
+  double local_th;
+  double global_th;
+  double th_arg;  // threshold argument of the sub-phase entry points
+  double pad0;
+  uint64_t m, R, S, U, nidx;
+  uint32_t flags;  // bit0 non-finite input, bit1 out-of-region entry, bit2 non-finite iterate
+  uint32_t pad1;
+  uint64_t cuts[OKT_MAX_WORLD + 1];
+  uint64_t off[OKT_MAX_WORLD + 1];
+  uint64_t prop[OKT_MAX_WORLD + 1];
+  uint64_t prop_all[OKT_MAX_WORLD * (OKT_MAX_WORLD + 1)];
+  uint32_t cnt[OKT_MAX_WORLD + 1];
+  uint32_t cnt_all[OKT_MAX_WORLD * (OKT_MAX_WORLD + 1)];
+  uint32_t small[2];
+  uint32_t small_all[2 * OKT_MAX_WORLD];
+  okt::RadixState rs;
+};
+
+bool is_pow2(int v) { return v >= 1 && (v & (v - 1)) == 0; }
+int log2i(int p) {
+  int l = 0;
+  while ((1 << l) < p) ++l;
+  return l;
+}
+
+// equal_slice_ends (collectives.cpp:79-87): ceil-sized blocks first.
+std::vector<uint64_t> equal_slice_ends(uint64_t n, int P) {
+  std::vector<uint64_t> e(P + 1, 0);
+  const uint64_t base = n / uint64_t(P), rem = n % uint64_t(P);
+  for (int r = 0; r < P; ++r) e[r + 1] = e[r] + base + (uint64_t(r) < rem ? 1 : 0);
+  return e;
+}
+
+// bucket_count (oktopk.cpp:88-91): at least one message per destination.
+uint64_t bucket_count(uint64_t nnz, uint32_t bucket) {
+  if (bucket == 0 || nnz <= bucket) return 1;
+  return (nnz + bucket - 1) / bucket;
+}
+
+okt_state default_state() {
+  okt_state s;
+  std::memset(&s, 0, sizeof(s));
+  s.local_th = 0.0;
+  s.global_th = 0.0;
+  s.tau = 64;
+  s.tau_prime = 32;
+  s.last_local_eval = -1;
+  s.last_global_eval = -1;
+  s.regions = -1;
+  s.bucket_size = 4;
+  s.t = 0;
+  return s;
+}
+
+}  // namespace
+
+// =============================================================================
+// okt_comm
+// =============================================================================
+struct okt_comm {
+  int rank = 0, P = 1, device = 0;
+  okt_world* world = nullptr;
+  std::unique_ptr<okt::Transport> tr;
+  cudaStream_t own = nullptr;
+  cudaEvent_t ready_ev = nullptr;
+  Launch L;
+  okt_state st = default_state();
+  bool dev_stale = true;  // device thresholds / cuts must be re-uploaded
+  okt_counters ledger[OKT_PHASE_COUNT] = {};
+
+  // buffers
+  Buf coo;                 // local selection, AoS (u32 idx | f32 val << 32)
+  Buf rbuf;                // split receive windows
+  Buf mask, stage;         // region presence bytes / coordinate-major staging
+  Buf reg_idx, reg_val;    // reduced region (refresh iterations)
+  Buf sur_idx, sur_val;    // survivors of the global threshold
+  Buf gval;                // gathered region values (refresh)
+  Buf u_idx, u_val;        // allgathered result
+  Buf sel_idx, sel_val;    // sub-phase outputs
+  Buf indexes;
+  Buf eps[2];
+  Buf hgrad;               // staging for the host-buffer entry points
+  Buf status, ctr, hist, scal;
+  DevScalars* h = nullptr;   // pinned download mirror
+  DevScalars* hup = nullptr; // pinned upload staging
+  size_t cap_n = 0;
+  int eps_cur = 0;
+  size_t eps_n = 0;
+
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Span { int id; cudaEvent_t a, b; };
+  std::vector<Span> spans;
+  int open_id = -1;
+  cudaEvent_t open_ev = nullptr;
+  double t_ms[OKT_T_COUNT] = {};
+  uint64_t t_calls[OKT_T_COUNT] = {};
+
+  DevScalars* d() const { return scal.as<DevScalars>(); }
+  cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : own; }
+
+  // ---- ledger ---------------------------------------------------------------
+  void credit_send(int ph, uint64_t words, uint64_t msgs, uint64_t bytes) {
+    ledger[ph].words_sent += words;
+    ledger[ph].msgs_sent += msgs;
+    ledger[ph].bytes_sent += bytes;
+  }
+  void credit_recv(int ph, uint64_t words, uint64_t msgs, uint64_t bytes) {
+    ledger[ph].words_recv += words;
+    ledger[ph].msgs_recv += msgs;
+    ledger[ph].bytes_recv += bytes;
+  }
+  // small_allreduce_avg of P+1 reals (transport.cpp:103-128): log2 P rounds.
+  void credit_avg(uint64_t len, uint64_t bytes_moved) {
+    const int rounds = log2i(P);
+    credit_send(OKT_PHASE_CONSENSUS, len * rounds, rounds, bytes_moved * (P - 1));
+    credit_recv(OKT_PHASE_CONSENSUS, len * rounds, rounds, bytes_moved * (P - 1));
+  }
+  // small_allgather_u32 of one word (transport.cpp:130-160).
+  void credit_allgather_u32() {
+    const int rounds = log2i(P);
+    for (int j = 0; j < rounds; ++j) {
+      credit_send(OKT_PHASE_CONSENSUS, uint64_t(1) << j, 1, 0);
+      credit_recv(OKT_PHASE_CONSENSUS, uint64_t(1) << j, 1, 0);
+    }
+    ledger[OKT_PHASE_CONSENSUS].bytes_sent += 4ull * (P - 1);
+    ledger[OKT_PHASE_CONSENSUS].bytes_recv += 4ull * (P - 1);
+  }
+  // sparse_allgatherv (collectives.cpp:30-77): recursive doubling; round j
+  // moves the parts of a 2^j-wide block, 2 words per entry.
+  void credit_allgatherv(int ph, const std::vector<uint64_t>& parts, uint64_t bytes_per_entry) {
+    const int rounds = log2i(P);
+    for (int j = 0; j < rounds; ++j) {
+      const int width = 1 << j;
+      const int partner = rank ^ width;
+      const int mb = rank & ~(width - 1), pb = partner & ~(width - 1);
+      uint64_t ms = 0, ps = 0;
+      for (int q = 0; q < width; ++q) {
+        ms += parts[mb + q];
+        ps += parts[pb + q];
+      }
+      credit_send(ph, 2 * ms, 1, 0);
+      credit_recv(ph, 2 * ps, 1, 0);
+    }
+    uint64_t others = 0;
+    for (int q = 0; q < P; ++q)
+      if (q != rank) others += parts[q];
+    ledger[ph].bytes_sent += parts[rank] * bytes_per_entry * (P - 1);
+    ledger[ph].bytes_recv += others * bytes_per_entry;
+  }
+
+  // ---- profiling --------------------------------------------------------------
+  cudaEvent_t ev_get() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+  void tmark(int id, cudaStream_t s) {
+    if (!prof) return;
+    cudaEvent_t e = ev_get();
+    cudaEventRecord(e, s);
+    if (open_id >= 0) spans.push_back({open_id, open_ev, e});
+    open_id = id;
+    open_ev = e;
+  }
+  void tstop(cudaStream_t s) {
+    if (!prof || open_id < 0) return;
+    cudaEvent_t e = ev_get();
+    cudaEventRecord(e, s);
+    spans.push_back({open_id, open_ev, e});
+    open_id = -1;
+  }
+  // Called after the stream was synchronised.
+  void tcollect() {
+    if (!prof) return;
+    for (const Span& sp : spans) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, sp.a, sp.b) == cudaSuccess) {
+        t_ms[sp.id] += ms;
+        t_calls[sp.id] += 1;
+      }
+    }
+    cudaGetLastError();
+    spans.clear();
+    ev_used = 0;
+    open_id = -1;
+  }
+
+  // ---- capacity -----------------------------------------------------------------
+  int reserve(size_t n) {
+    if (n <= cap_n) return OKT_OK;
+    const size_t tiles = n / 4096 + 8;
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = coo.ensure(8 * n);
+    if (e == cudaSuccess) e = status.ensure(8 * tiles);
+    if (e == cudaSuccess && P == 1) {
+      // P = 1 runs without host syncs: survivors/indexes sized for the worst case.
+      e = sur_idx.ensure(4 * n);
+      if (e == cudaSuccess) e = sur_val.ensure(8 * n);
+      if (e == cudaSuccess) e = indexes.ensure(4 * n);
+    }
+    L.status = status.as<uint64_t>();
+    if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("reserve: ") + cudaGetErrorString(e));
+    cap_n = n;
+    return OKT_OK;
+  }
+  int ensure(Buf& b, size_t bytes) {
+    const cudaError_t e = b.ensure(bytes);
+    if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return OKT_OK;
+  }
+
+  int sync(cudaStream_t s) {
+    cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s);
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("device: ") + cudaGetErrorString(e));
+    return OKT_OK;
+  }
+  int ck(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return OKT_OK;
+    cudaGetLastError();
+    return set_err(OKT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+
+  // Upload the host mirror's thresholds (and cuts) when the device copy is stale.
+  int upload_state(cudaStream_t s) {
+    if (!dev_stale) return OKT_OK;
+    hup->local_th = st.local_th;
+    hup->global_th = st.global_th;
+    std::memcpy(hup->cuts, st.cuts, sizeof(st.cuts));
+    int rc = ck(cudaMemcpyAsync(&d()->local_th, &hup->local_th, 2 * sizeof(double),
+                                cudaMemcpyHostToDevice, s), "upload");
+    if (rc) return rc;
+    rc = ck(cudaMemcpyAsync(d()->cuts, hup->cuts, sizeof(hup->cuts), cudaMemcpyHostToDevice, s),
+            "upload");
+    if (rc) return rc;
+    dev_stale = false;
+    return OKT_OK;
+  }
+  int upload_u64(uint64_t* dst, uint64_t v, uint64_t* staging, cudaStream_t s) {
+    *staging = v;
+    return ck(cudaMemcpyAsync(dst, staging, 8, cudaMemcpyHostToDevice, s), "upload");
+  }
+  int upload_f64(double* dst, double v, double* staging, cudaStream_t s) {
+    *staging = v;
+    return ck(cudaMemcpyAsync(dst, staging, 8, cudaMemcpyHostToDevice, s), "upload");
+  }
+
+  int comm_err(int rc, const std::string& err) {
+    if (rc == OKT_ERR_TRANSPORT && world) return set_err(rc, "TransportError: " + err);
+    return set_err(rc, err);
+  }
+
+  // ---- phases -----------------------------------------------------------------------
+  // space_repartition from a selected index list (oktopk.cpp:28-61).  Cuts land
+  // in d()->cuts; no host sync.
+  int repartition_dev(const uint32_t* idx, int stride, const uint64_t* d_m, uint64_t m_host,
+                      uint64_t n, cudaStream_t s) {
+    int rc = ck(okt::launch_proposals(L, idx, stride, d_m, m_host, n, P, d()->prop), "proposals");
+    if (rc) return rc;
+    if (P > 1) {
+      std::string err;
+      rc = tr->allgather(d()->prop, d()->prop_all, sizeof(uint64_t) * (P + 1), s, err);
+      if (rc) return comm_err(rc, err);
+      credit_avg(uint64_t(P + 1), sizeof(uint64_t) * (P + 1));
+      rc = ck(okt::launch_cuts(L, d()->prop_all, P, n, d()->cuts), "cuts");
+    } else {
+      rc = ck(cudaMemcpyAsync(d()->cuts, d()->prop, 2 * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s),
+              "cuts");
+    }
+    return rc;
+  }
+
+  // split_and_reduce (oktopk.cpp:95-163) given the local selection in coo/d->m
+  // and cuts in d->cuts.  Region (filter=false) or survivors of *d_gth
+  // (filter=true) land in out_idx/out_val with count *d_out_cnt.  Host sync #1.
+  // On return h->cnt_all / h->cuts are valid.
+  int split_reduce_dev(uint64_t n, uint32_t bucket, bool filter, const double* d_gth, Buf& out_idx,
+                       Buf& out_val, uint64_t* d_out_cnt, uint64_t& bound_out, cudaStream_t s) {
+    int rc = ck(okt::launch_slice_offsets(L, coo.as<uint64_t>(), &d()->m, d()->cuts, P, d()->off,
+                                          d()->cnt, &d()->flags),
+                "slice_offsets");
+    if (rc) return rc;
+    std::string err;
+    tmark(OKT_T_SPLIT, s);
+    rc = tr->allgather(d()->cnt, d()->cnt_all, sizeof(uint32_t) * (P + 1), s, err);
+    if (rc) return comm_err(rc, err);
+    if ((rc = sync(s))) return rc;
+    // Any rank with a non-finite accumulator aborts the step everywhere.
+    for (int q = 0; q < P; ++q) {
+      if (h->cnt_all[q * (P + 1) + P] & 1u) {
+        if (q == rank) return set_err(OKT_ERR_NUMERIC, "ok_sparse_allreduce: non-finite input");
+        return set_err(OKT_ERR_TRANSPORT, "TransportError: rank " + std::to_string(q) +
+                                              " failed (non-finite input)");
+      }
+    }
+    const uint64_t lo = h->cuts[rank], hi = h->cuts[rank + 1];
+    const uint64_t W = hi > lo ? hi - lo : 0;
+    std::vector<uint64_t> scnt(P), rcnt(P), roff(P + 1, 0);
+    for (int q = 0; q < P; ++q) {
+      scnt[q] = h->cnt_all[rank * (P + 1) + q];
+      rcnt[q] = h->cnt_all[q * (P + 1) + rank];
+    }
+    // Ledger: rotated schedule dst = (r+s)%P, src = (r-s+P)%P (oktopk.cpp:113-157).
+    uint64_t in_total = 0;
+    for (int step = 1; step < P; ++step) {
+      const int dst = (rank + step) % P, src = (rank - step + P) % P;
+      credit_send(OKT_PHASE_SPLIT, 2 * scnt[dst], bucket_count(scnt[dst], bucket), 8 * scnt[dst]);
+      credit_recv(OKT_PHASE_SPLIT, 2 * rcnt[src], bucket_count(rcnt[src], bucket), 8 * rcnt[src]);
+    }
+    for (int q = 0; q < P; ++q) {
+      roff[q + 1] = roff[q] + (q == rank ? 0 : rcnt[q]);
+      if (q != rank) in_total += rcnt[q];
+    }
+    if ((rc = ensure(rbuf, 8 * std::max<uint64_t>(in_total, 1)))) return rc;
+    std::vector<Xfer> sends, recvs;
+    uint64_t* cooP = coo.as<uint64_t>();
+    uint64_t* rb = rbuf.as<uint64_t>();
+    for (int step = 1; step < P; ++step) {
+      const int dst = (rank + step) % P, src = (rank - step + P) % P;
+      sends.push_back({dst, cooP + h->off[dst], 8 * scnt[dst]});
+      recvs.push_back({src, rb + roff[src], 8 * rcnt[src]});
+    }
+    rc = tr->exchange(sends, recvs, s, err);
+    if (rc) return comm_err(rc, err);
+
+    // K3: region merge.
+    tmark(OKT_T_MERGE, s);
+    const uint64_t bound = in_total + scnt[rank];
+    if ((rc = ensure(mask, ((W + 15) / 16) * 16 + 16))) return rc;
+    if ((rc = ensure(stage, 4 * std::max<uint64_t>(W, 1) * P))) return rc;
+    if ((rc = ensure(out_idx, 4 * std::max<uint64_t>(bound, 1)))) return rc;
+    if ((rc = ensure(out_val, 8 * std::max<uint64_t>(bound, 1)))) return rc;
+    okt::Segs segs{};
+    segs.nseg = 0;
+    segs.start[0] = 0;
+    for (int q = 0; q < P; ++q) {
+      const uint64_t c = q == rank ? scnt[rank] : rcnt[q];
+      segs.ptr[segs.nseg] = q == rank ? cooP + h->off[rank] : rb + roff[q];
+      segs.src[segs.nseg] = q;
+      segs.start[segs.nseg + 1] = segs.start[segs.nseg] + c;
+      ++segs.nseg;
+    }
+    rc = ck(okt::launch_scatter(L, segs, lo, W, P, mask.as<uint32_t>(), stage.as<float>(), &d()->flags),
+            "scatter");
+    if (rc) return rc;
+    rc = ck(okt::launch_region_scan(L, P, filter, lo, W, mask.as<uint32_t>(), stage.as<float>(), d_gth,
+                                    out_idx.as<uint32_t>(), out_val.as<double>(), d_out_cnt),
+            "region_scan");
+    bound_out = bound;
+    return rc;
+  }
+
+  // Global threshold refresh (oktopk.cpp:277-293): gather all regions, k-th
+  // largest fp64 magnitude; unchanged when everything is empty.
+  int refresh_global_dev(uint64_t k, uint64_t R_bound, cudaStream_t s) {
+    (void)R_bound;
+    int rc;
+    std::string err;
+    if (P == 1) {
+      return ck(okt::launch_radix_select(L, okt::RadixSrc::kF64, reg_val.p, 0, &d()->R, R_bound, k,
+                                         &d()->rs, hist.as<uint32_t>(), &d()->global_th, false),
+                "radix");
+    }
+    rc = ck(cudaMemcpyAsync(&d()->small[0], &d()->R, 4, cudaMemcpyDeviceToDevice, s), "copy");
+    if (rc) return rc;
+    rc = tr->allgather(&d()->small[0], d()->small_all, 4, s, err);
+    if (rc) return comm_err(rc, err);
+    if ((rc = sync(s))) return rc;
+    std::vector<uint64_t> parts(P), goff(P + 1, 0);
+    for (int q = 0; q < P; ++q) {
+      parts[q] = h->small_all[q];
+      goff[q + 1] = goff[q] + parts[q];
+    }
+    const uint64_t total = goff[P];
+    if ((rc = ensure(gval, 8 * std::max<uint64_t>(total, 1)))) return rc;
+    double* gv = gval.as<double>();
+    if (parts[rank]) {
+      rc = ck(cudaMemcpyAsync(gv + goff[rank], reg_val.p, 8 * parts[rank], cudaMemcpyDeviceToDevice, s),
+              "copy");
+      if (rc) return rc;
+    }
+    std::vector<Xfer> sends, recvs;
+    for (int q = 0; q < P; ++q) {
+      if (q == rank) continue;
+      sends.push_back({q, reg_val.p, 8 * parts[rank]});
+      recvs.push_back({q, gv + goff[q], 8 * parts[q]});
+    }
+    rc = tr->exchange(sends, recvs, s, err);
+    if (rc) return comm_err(rc, err);
+    credit_allgatherv(OKT_PHASE_GATHER, parts, 8);
+    return ck(okt::launch_radix_select(L, okt::RadixSrc::kF64, gv, total, nullptr, total, k, &d()->rs,
+                                       hist.as<uint32_t>(), &d()->global_th, false),
+              "radix");
+  }
+
+  // balance_and_allgatherv (oktopk.cpp:165-244) on survivors already in
+  // sur_idx/sur_val with count d->S.  u lands in u_idx/u_val; returns U.
+  int balance_allgatherv_dev(cudaStream_t s, uint64_t& U) {
+    int rc;
+    std::string err;
+    rc = ck(cudaMemcpyAsync(&d()->small[0], &d()->S, 4, cudaMemcpyDeviceToDevice, s), "copy");
+    if (rc) return rc;
+    rc = tr->allgather(&d()->small[0], d()->small_all, 4, s, err);
+    if (rc) return comm_err(rc, err);
+    if ((rc = sync(s))) return rc;
+    credit_allgather_u32();
+    std::vector<uint64_t> sizes(P), off(P + 1, 0);
+    uint64_t total = 0, maxs = 0;
+    for (int q = 0; q < P; ++q) {
+      sizes[q] = h->small_all[q];
+      off[q + 1] = off[q] + sizes[q];
+      total += sizes[q];
+      maxs = std::max(maxs, sizes[q]);
+    }
+    U = total;
+    if ((rc = ensure(u_idx, 4 * std::max<uint64_t>(total, 1)))) return rc;
+    if ((rc = ensure(u_val, 8 * std::max<uint64_t>(total, 1)))) return rc;
+    uint32_t* ui = u_idx.as<uint32_t>();
+    double* uv = u_val.as<double>();
+    const uint32_t* si = sur_idx.as<uint32_t>();
+    const double* sv = sur_val.as<double>();
+    std::vector<uint64_t> part_off = off, part_sz = sizes;
+    const bool balance = total > 0 && maxs * uint64_t(P) >= 4 * total;
+    if (balance) {
+      // Re-cut the rank-concatenated survivor stream into P equal blocks and
+      // move every overlap to its block owner.  Pieces land directly at their
+      // final position in u (the stream order is the result order).
+      const std::vector<uint64_t> block = equal_slice_ends(total, P);
+      auto overlap = [&](int src, int dst, uint64_t& a, uint64_t& b) {
+        a = std::max(off[src], block[dst]);
+        b = std::min(off[src + 1], block[dst + 1]);
+        return a < b;
+      };
+      std::vector<Xfer> sends, recvs;
+      uint64_t a, b;
+      for (int dst = 0; dst < P; ++dst) {
+        if (dst == rank || !overlap(rank, dst, a, b)) continue;
+        sends.push_back({dst, const_cast<uint32_t*>(si) + (a - off[rank]), 4 * (b - a)});
+        sends.push_back({dst, const_cast<double*>(sv) + (a - off[rank]), 8 * (b - a)});
+        credit_send(OKT_PHASE_BALANCE, 2 * (b - a), 1, 12 * (b - a));
+      }
+      for (int src = 0; src < P; ++src) {
+        if (!overlap(src, rank, a, b)) continue;
+        if (src == rank) {
+          rc = ck(cudaMemcpyAsync(ui + a, si + (a - off[rank]), 4 * (b - a), cudaMemcpyDeviceToDevice, s),
+                  "copy");
+          if (!rc)
+            rc = ck(cudaMemcpyAsync(uv + a, sv + (a - off[rank]), 8 * (b - a), cudaMemcpyDeviceToDevice, s),
+                    "copy");
+          if (rc) return rc;
+        } else {
+          recvs.push_back({src, ui + a, 4 * (b - a)});
+          recvs.push_back({src, uv + a, 8 * (b - a)});
+          credit_recv(OKT_PHASE_BALANCE, 2 * (b - a), 1, 12 * (b - a));
+        }
+      }
+      rc = tr->exchange(sends, recvs, s, err);
+      if (rc) return comm_err(rc, err);
+      for (int q = 0; q < P; ++q) {
+        part_off[q] = block[q];
+        part_sz[q] = block[q + 1] - block[q];
+      }
+    } else if (sizes[rank]) {
+      rc = ck(cudaMemcpyAsync(ui + off[rank], si, 4 * sizes[rank], cudaMemcpyDeviceToDevice, s), "copy");
+      if (!rc) rc = ck(cudaMemcpyAsync(uv + off[rank], sv, 8 * sizes[rank], cudaMemcpyDeviceToDevice, s), "copy");
+      if (rc) return rc;
+    }
+    // allgatherv: every rank's part to every peer, straight into u.
+    std::vector<Xfer> sends, recvs;
+    for (int q = 0; q < P; ++q) {
+      if (q == rank) continue;
+      sends.push_back({q, ui + part_off[rank], 4 * part_sz[rank]});
+      sends.push_back({q, uv + part_off[rank], 8 * part_sz[rank]});
+      recvs.push_back({q, ui + part_off[q], 4 * part_sz[q]});
+      recvs.push_back({q, uv + part_off[q], 8 * part_sz[q]});
+    }
+    rc = tr->exchange(sends, recvs, s, err);
+    if (rc) return comm_err(rc, err);
+    credit_allgatherv(OKT_PHASE_ALLGATHERV, part_sz, 12);
+    return OKT_OK;
+  }
+
+  // ---- the step ---------------------------------------------------------------------
+  int step(const float* g, float* w, size_t n, double alpha, int64_t t, size_t k, bool sgd,
+           okt_result* out, cudaStream_t s) {
+    if (n == 0 || k < 1 || t < 1)
+      return set_err(OKT_ERR_INVALID_ARGUMENT, "ok_sparse_allreduce: empty input, k < 1, or t < 1");
+    if (n > 0xffffffffull) return set_err(OKT_ERR_INVALID_ARGUMENT, "n exceeds the u32 index space");
+    if (st.tau == 0 || st.tau_prime == 0)
+      return set_err(OKT_ERR_INVALID_ARGUMENT, "tau and tau_prime must be >= 1");
+    if (!g) return set_err(OKT_ERR_INVALID_ARGUMENT, "null gradient");
+    int rc;
+    if ((rc = reserve(n))) return rc;
+    if (sgd) {
+      if (eps_n == 0) {
+        if ((rc = residual_reset(n, nullptr, s))) return rc;
+      } else if (eps_n != n) {
+        return set_err(OKT_ERR_INVALID_ARGUMENT, "oktopk_sgd_step: residual size does not match problem");
+      }
+    }
+    L.s = s;
+    cudaEvent_t step_begin = nullptr;
+    if (prof) {
+      step_begin = ev_get();
+      cudaEventRecord(step_begin, s);
+    }
+    if ((rc = upload_state(s))) return rc;
+    if ((rc = ck(cudaMemsetAsync(&d()->flags, 0, 4, s), "memset"))) return rc;
+
+    const bool thr = (t - 1) % int64_t(st.tau_prime) == 0;
+    const bool bnd = (t - 1) % int64_t(st.tau) == 0;
+    const float* acc = g;
+    const float* eps_in = nullptr;
+    float* eps_out = nullptr;
+    if (sgd) {
+      eps_in = eps[eps_cur].as<float>();
+      eps_out = eps[eps_cur ^ 1].as<float>();
+      acc = eps_out;
+    }
+    uint32_t* hp = hist.as<uint32_t>();
+    const float fa = float(alpha);
+
+    // ---- K1 / K2 ----
+    if (thr) {
+      if (sgd) {
+        tmark(OKT_T_SELECT, s);
+        rc = ck(okt::launch_radix_init(L, &d()->rs, k, n, nullptr), "radix_init");
+        if (!rc) rc = ck(okt::launch_k1(L, okt::K1Mode::kAccumHist, g, eps_in, eps_out, fa, n, nullptr, nullptr,
+                                        nullptr, &d()->flags, hp), "k1");
+        tmark(OKT_T_THRESHOLD, s);
+        if (!rc) rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kDenseF32, acc, n, nullptr, n, k, &d()->rs,
+                                                  hp, &d()->local_th, true), "radix");
+      } else {
+        tmark(OKT_T_THRESHOLD, s);
+        rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kDenseF32, acc, n, nullptr, n, k, &d()->rs, hp,
+                                         &d()->local_th, false), "radix");
+      }
+      tmark(OKT_T_SELECT, s);
+      if (!rc) rc = ck(okt::launch_k1(L, okt::K1Mode::kSelect, acc, nullptr, nullptr, 0.f, n, &d()->local_th,
+                                      coo.as<uint64_t>(), &d()->m, &d()->flags, nullptr), "k1");
+    } else {
+      tmark(OKT_T_SELECT, s);
+      rc = ck(okt::launch_k1(L, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, g, eps_in, eps_out, fa,
+                             n, &d()->local_th, coo.as<uint64_t>(), &d()->m, &d()->flags, nullptr), "k1");
+    }
+    if (rc) return abort_step(rc);
+
+    uint64_t U_bound = n;
+    const uint64_t* d_U = nullptr;
+    const uint32_t* ui = nullptr;
+    const double* uv = nullptr;
+    std::vector<uint64_t> new_cuts(P + 1, 0);
+
+    if (P == 1) {
+      tmark(OKT_T_GLOBAL, s);
+      if (thr) {
+        // The region is the local selection itself (fp32 values, exact in fp64).
+        rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kAosF32, coo.p, 0, &d()->m, n, k, &d()->rs, hp,
+                                         &d()->global_th, false), "radix");
+        if (rc) return abort_step(rc);
+      }
+      rc = ck(okt::launch_filter(L, true, coo.as<uint64_t>(), nullptr, nullptr, &d()->m, n, &d()->global_th,
+                                 sur_idx.as<uint32_t>(), sur_val.as<double>(), &d()->S), "filter");
+      if (rc) return abort_step(rc);
+      ui = sur_idx.as<uint32_t>();
+      uv = sur_val.as<double>();
+      d_U = &d()->S;
+      new_cuts[0] = 0;
+      new_cuts[1] = n;
+    } else {
+      if (!is_pow2(P)) return set_err(OKT_ERR_CONFIG, "world size must be a power of two");
+      // ---- boundaries ----
+      if (bnd) {
+        tmark(OKT_T_SPLIT, s);
+        rc = repartition_dev(coo.as<uint32_t>(), 2, &d()->m, 0, n, s);
+        if (rc) return abort_step(rc);
+      } else if (st.regions != P) {
+        const std::vector<uint64_t> eq = equal_slice_ends(n, P);
+        std::memcpy(hup->cuts, eq.data(), sizeof(uint64_t) * (P + 1));
+        rc = ck(cudaMemcpyAsync(d()->cuts, hup->cuts, sizeof(uint64_t) * (P + 1), cudaMemcpyHostToDevice, s),
+                "upload");
+        if (rc) return abort_step(rc);
+      }
+      uint64_t bound = 0;
+      Buf& oi = thr ? reg_idx : sur_idx;
+      Buf& ov = thr ? reg_val : sur_val;
+      rc = split_reduce_dev(n, st.bucket_size, !thr, &d()->global_th, oi, ov, thr ? &d()->R : &d()->S, bound, s);
+      if (rc) return abort_step(rc);
+      for (int q = 0; q <= P; ++q) new_cuts[q] = h->cuts[q];
+      if (thr) {
+        tmark(OKT_T_GLOBAL, s);
+        rc = refresh_global_dev(k, bound, s);
+        if (!rc) {
+          if ((rc = ensure(sur_idx, 4 * std::max<uint64_t>(bound, 1))) ||
+              (rc = ensure(sur_val, 8 * std::max<uint64_t>(bound, 1))))
+            return abort_step(rc);
+          rc = ck(okt::launch_filter(L, false, nullptr, reg_idx.as<uint32_t>(), reg_val.as<double>(), &d()->R,
+                                     bound, &d()->global_th, sur_idx.as<uint32_t>(), sur_val.as<double>(),
+                                     &d()->S), "filter");
+        }
+        if (rc) return abort_step(rc);
+      }
+      tmark(OKT_T_ALLGATHER, s);
+      uint64_t U = 0;
+      rc = balance_allgatherv_dev(s, U);
+      if (rc) return abort_step(rc);
+      if ((rc = ensure(indexes, 4 * std::max<uint64_t>(U, 1)))) return abort_step(rc);
+      if ((rc = upload_u64(&d()->U, U, &hup->U, s))) return abort_step(rc);
+      U_bound = U;
+      d_U = &d()->U;
+      ui = u_idx.as<uint32_t>();
+      uv = u_val.as<double>();
+    }
+
+    // ---- K7 ----
+    tmark(OKT_T_APPLY, s);
+    rc = ck(okt::launch_apply(L, ui, uv, d_U, U_bound, const_cast<float*>(acc), sgd, sgd ? w : nullptr, P,
+                              &d()->local_th, indexes.as<uint32_t>(), &d()->nidx, &d()->flags), "apply");
+    if (rc) return abort_step(rc);
+    tstop(s);
+    if (prof) {
+      cudaEvent_t e = ev_get();
+      cudaEventRecord(e, s);
+      spans.push_back({OKT_T_STEP, step_begin, e});
+    }
+    if ((rc = sync(s))) return abort_step(rc);
+    tcollect();
+
+    if (h->flags & 1u) {
+      dev_stale = true;
+      return set_err(OKT_ERR_NUMERIC, "ok_sparse_allreduce: non-finite input");
+    }
+    if (h->flags & 2u) {
+      dev_stale = true;
+      return set_err(OKT_ERR_PROTOCOL, "split_and_reduce: entries outside my region");
+    }
+    // Commit.
+    st.local_th = h->local_th;
+    st.global_th = h->global_th;
+    if (thr) {
+      st.last_local_eval = t;
+      st.last_global_eval = t;
+    }
+    st.regions = P;
+    for (int q = 0; q <= P; ++q) st.cuts[q] = new_cuts[q];
+    st.t = t;
+    if (sgd) eps_cur ^= 1;
+    if (out) {
+      out->u.d_idx = ui;
+      out->u.d_val = uv;
+      out->u.nnz = P == 1 ? h->S : h->U;
+      out->u.n = n;
+      out->d_indexes = indexes.as<uint32_t>();
+      out->n_indexes = h->nidx;
+      out->local_selected = h->m;
+    }
+    if (h->flags & 4u) return set_err(OKT_ERR_NUMERIC, "oktopk_sgd_step: non-finite iterate");
+    return OKT_OK;
+  }
+
+  int abort_step(int rc) {
+    dev_stale = true;
+    cudaStreamSynchronize(L.s);
+    cudaGetLastError();
+    spans.clear();
+    ev_used = 0;
+    open_id = -1;
+    return rc;
+  }
+
+  int residual_reset(size_t n, const float* init, cudaStream_t s) {
+    int rc;
+    if ((rc = ensure(eps[0], 4 * std::max<size_t>(n, 1)))) return rc;
+    if ((rc = ensure(eps[1], 4 * std::max<size_t>(n, 1)))) return rc;
+    eps_cur = 0;
+    eps_n = n;
+    if (init)
+      rc = ck(cudaMemcpyAsync(eps[0].p, init, 4 * n, cudaMemcpyDeviceToDevice, s), "residual");
+    else
+      rc = ck(cudaMemsetAsync(eps[0].p, 0, 4 * n, s), "residual");
+    if (rc) return rc;
+    return ck(cudaStreamSynchronize(s), "residual");
+  }
+};
+
+// =============================================================================
+// C-ABI
+// =============================================================================
+namespace {
+
+int init_comm(okt_comm* c) {
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+  c->L.sms = dev_sms;
+  if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ready_ev, cudaEventDisableTiming) != cudaSuccess) {
+    return set_err(OKT_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(cudaGetLastError()));
+  }
+  c->L.s = c->own;
+  c->ctr.zero_init = true;
+  c->hist.zero_init = true;
+  c->scal.zero_init = true;
+  c->status.zero_init = true;
+  c->mask.zero_init = true;
+  cudaError_t e = c->ctr.ensure(64);
+  if (e == cudaSuccess) e = c->hist.ensure(2048 * 4);
+  if (e == cudaSuccess) e = c->scal.ensure(sizeof(DevScalars));
+  if (e == cudaSuccess) e = cudaMallocHost(&c->h, sizeof(DevScalars));
+  if (e == cudaSuccess) e = cudaMallocHost(&c->hup, sizeof(DevScalars));
+  if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("init: ") + cudaGetErrorString(e));
+  std::memset(c->h, 0, sizeof(DevScalars));
+  std::memset(c->hup, 0, sizeof(DevScalars));
+  c->L.status = nullptr;
+  c->L.ctr = c->ctr.as<uint32_t>();
+  const int rc = c->reserve(4096);
+  c->L.status = c->status.as<uint64_t>();
+  return rc;
+}
+
+struct DeviceGuard {
+  explicit DeviceGuard(int dev) { cudaSetDevice(dev); }
+};
+
+#define OKT_COMM_CHECK(c)                                               \
+  do {                                                                  \
+    if (!(c)) return set_err(OKT_ERR_INVALID_ARGUMENT, "null comm");    \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+int okt_abi_version(void) { return OKT_ABI_VERSION; }
+
+const char* okt_status_string(int s) {
+  switch (s) {
+    case OKT_OK: return "ok";
+    case OKT_ERR_INVALID_ARGUMENT: return "invalid_argument";
+    case OKT_ERR_NUMERIC: return "NumericError";
+    case OKT_ERR_PROTOCOL: return "ProtocolError";
+    case OKT_ERR_TRANSPORT: return "TransportError";
+    case OKT_ERR_CONFIG: return "ConfigError";
+    case OKT_ERR_CUDA: return "cuda";
+    case OKT_ERR_NCCL: return "nccl";
+    default: return "internal";
+  }
+}
+
+const char* okt_last_error(void) { return g_err.c_str(); }
+
+int okt_world_create_local(okt_world** out, int P, const int* devices) {
+  if (!out) return set_err(OKT_ERR_INVALID_ARGUMENT, "null out");
+  if (P < 1) return set_err(OKT_ERR_INVALID_ARGUMENT, "P must be >= 1");
+  if (!is_pow2(P) || P > OKT_MAX_WORLD)
+    return set_err(OKT_ERR_CONFIG, "world size must be a power of two <= 8");
+  auto* w = new okt_world();
+  w->P = P;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int r = 0; r < P; ++r) w->devices.push_back(devices ? devices[r] : cur);
+  w->sends.assign(P, std::vector<std::vector<Xfer>>(P));
+  w->ready.assign(P, nullptr);
+  *out = w;
+  return OKT_OK;
+}
+
+int okt_world_close(okt_world* w) {
+  if (!w) return set_err(OKT_ERR_INVALID_ARGUMENT, "null world");
+  w->close();
+  return OKT_OK;
+}
+
+int okt_world_destroy(okt_world* w) {
+  delete w;
+  return OKT_OK;
+}
+
+int okt_comm_init_local(okt_comm** out, okt_world* w, int rank) {
+  if (!out || !w) return set_err(OKT_ERR_INVALID_ARGUMENT, "null argument");
+  if (rank < 0 || rank >= w->P) return set_err(OKT_ERR_INVALID_ARGUMENT, "rank out of range");
+  auto* c = new okt_comm();
+  c->rank = rank;
+  c->P = w->P;
+  c->device = w->devices[rank];
+  c->world = w;
+  DeviceGuard g(c->device);
+  int rc = init_comm(c);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  c->tr.reset(new okt::LocalTransport(w, rank, c->device, c->ready_ev));
+  *out = c;
+  return OKT_OK;
+}
+
+int okt_nccl_unique_id(void* out, size_t len) {
+  if (!out || len < sizeof(ncclUniqueId)) return set_err(OKT_ERR_INVALID_ARGUMENT, "buffer too small");
+  ncclUniqueId id;
+  const ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return set_err(OKT_ERR_NCCL, ncclGetErrorString(r));
+  std::memcpy(out, &id, sizeof(id));
+  return OKT_OK;
+}
+
+int okt_comm_init_nccl(okt_comm** out, int rank, int P, int device, const void* uid, size_t len) {
+  if (!out || !uid || len < sizeof(ncclUniqueId)) return set_err(OKT_ERR_INVALID_ARGUMENT, "bad argument");
+  if (P < 1 || rank < 0 || rank >= P) return set_err(OKT_ERR_INVALID_ARGUMENT, "bad rank/world");
+  if (!is_pow2(P) || P > OKT_MAX_WORLD)
+    return set_err(OKT_ERR_CONFIG, "world size must be a power of two <= 8");
+  auto* c = new okt_comm();
+  c->rank = rank;
+  c->P = P;
+  c->device = device;
+  DeviceGuard g(device);
+  int rc = init_comm(c);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  ncclComm_t nc = nullptr;
+  const ncclResult_t r = ncclCommInitRank(&nc, P, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return set_err(OKT_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  c->tr.reset(new okt::NcclTransport(nc));
+  *out = c;
+  return OKT_OK;
+}
+
+int okt_comm_destroy(okt_comm* c) {
+  if (!c) return OKT_OK;
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->own);
+  c->tr.reset();
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->ready_ev) cudaEventDestroy(c->ready_ev);
+  if (c->h) cudaFreeHost(c->h);
+  if (c->hup) cudaFreeHost(c->hup);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+  return OKT_OK;
+}
+
+int okt_comm_info(const okt_comm* c, int* rank, int* P, int* device) {
+  OKT_COMM_CHECK(c);
+  if (rank) *rank = c->rank;
+  if (P) *P = c->P;
+  if (device) *device = c->device;
+  return OKT_OK;
+}
+
+int okt_comm_reserve(okt_comm* c, size_t n) {
+  OKT_COMM_CHECK(c);
+  DeviceGuard g(c->device);
+  const int rc = c->reserve(n);
+  c->L.status = c->status.as<uint64_t>();
+  return rc;
+}
+
+int okt_get_state(const okt_comm* c, okt_state* out) {
+  OKT_COMM_CHECK(c);
+  if (!out) return set_err(OKT_ERR_INVALID_ARGUMENT, "null out");
+  *out = c->st;
+  return OKT_OK;
+}
+
+int okt_set_state(okt_comm* c, const okt_state* in) {
+  OKT_COMM_CHECK(c);
+  if (!in) return set_err(OKT_ERR_INVALID_ARGUMENT, "null state");
+  c->st = *in;
+  c->dev_stale = true;
+  return OKT_OK;
+}
+
+int okt_set_params(okt_comm* c, uint32_t tau, uint32_t tau_prime, uint32_t bucket) {
+  OKT_COMM_CHECK(c);
+  if (tau == 0 || tau_prime == 0) return set_err(OKT_ERR_INVALID_ARGUMENT, "tau and tau_prime must be >= 1");
+  c->st.tau = tau;
+  c->st.tau_prime = tau_prime;
+  c->st.bucket_size = bucket;
+  return OKT_OK;
+}
+
+int okt_ledger(const okt_comm* c, int phase, okt_counters* out) {
+  OKT_COMM_CHECK(c);
+  if (phase < 0 || phase >= OKT_PHASE_COUNT || !out) return set_err(OKT_ERR_INVALID_ARGUMENT, "bad phase");
+  *out = c->ledger[phase];
+  return OKT_OK;
+}
+
+int okt_ledger_reset(okt_comm* c) {
+  OKT_COMM_CHECK(c);
+  std::memset(c->ledger, 0, sizeof(c->ledger));
+  return OKT_OK;
+}
+
+int okt_sparse_allreduce(okt_comm* c, const float* d_acc, size_t n, int64_t t, size_t k, okt_result* out,
+                         void* stream) {
+  OKT_COMM_CHECK(c);
+  DeviceGuard g(c->device);
+  int rc = c->reserve(n);
+  c->L.status = c->status.as<uint64_t>();
+  if (rc) return rc;
+  return c->step(d_acc, nullptr, n, 0.0, t, k, false, out, c->pick(stream));
+}
+
+int okt_residual_reset(okt_comm* c, size_t n, const float* d_init, void* stream) {
+  OKT_COMM_CHECK(c);
+  DeviceGuard g(c->device);
+  return c->residual_reset(n, d_init, c->pick(stream));
+}
+
+int okt_residual(okt_comm* c, float** d_eps, size_t* n) {
+  OKT_COMM_CHECK(c);
+  if (d_eps) *d_eps = c->eps_n ? c->eps[c->eps_cur].as<float>() : nullptr;
+  if (n) *n = c->eps_n;
+  return OKT_OK;
+}
+
+int okt_sgd_step(okt_comm* c, const float* d_grad, float* d_w, size_t n, double alpha, int64_t t, size_t k,
+                 okt_result* out, void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!d_w) return set_err(OKT_ERR_INVALID_ARGUMENT, "null model");
+  DeviceGuard g(c->device);
+  int rc = c->reserve(n);
+  c->L.status = c->status.as<uint64_t>();
+  if (rc) return rc;
+  return c->step(d_grad, d_w, n, alpha, t, k, true, out, c->pick(stream));
+}
+
+// ---- host-buffer entry points --------------------------------------------------------
+static int copy_result_to_host(okt_comm* c, const okt_result& r, uint32_t* h_idx, double* h_val,
+                               uint32_t* h_indexes, size_t cap, cudaStream_t s) {
+  if (r.u.nnz > cap) return set_err(OKT_ERR_INVALID_ARGUMENT, "u does not fit the host buffers");
+  cudaError_t e = cudaSuccess;
+  if (r.u.nnz && h_idx) e = cudaMemcpyAsync(h_idx, r.u.d_idx, 4 * r.u.nnz, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && r.u.nnz && h_val)
+    e = cudaMemcpyAsync(h_val, r.u.d_val, 8 * r.u.nnz, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && r.n_indexes && h_indexes)
+    e = cudaMemcpyAsync(h_indexes, r.d_indexes, 4 * r.n_indexes, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return c->ck(e, "copy result");
+}
+
+int okt_sparse_allreduce_host(okt_comm* c, const float* h_acc, size_t n, int64_t t, size_t k, uint32_t* h_u_idx,
+                              double* h_u_val, uint32_t* h_indexes, size_t u_cap, okt_result* out, void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!h_acc) return set_err(OKT_ERR_INVALID_ARGUMENT, "null gradient");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  int rc = c->ensure(c->hgrad, 4 * std::max<size_t>(n, 1));
+  if (rc) return rc;
+  if (n && (rc = c->ck(cudaMemcpyAsync(c->hgrad.p, h_acc, 4 * n, cudaMemcpyHostToDevice, s), "h2d"))) return rc;
+  okt_result r{};
+  if ((rc = c->reserve(n))) return rc;
+  rc = c->step(c->hgrad.as<float>(), nullptr, n, 0.0, t, k, false, &r, s);
+  if (rc) return rc;
+  if (out) *out = r;
+  return copy_result_to_host(c, r, h_u_idx, h_u_val, h_indexes, u_cap, s);
+}
+
+int okt_sgd_step_host(okt_comm* c, const float* h_grad, float* d_w, size_t n, double alpha, int64_t t, size_t k,
+                      uint32_t* h_u_idx, double* h_u_val, size_t u_cap, okt_result* out, void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!h_grad || !d_w) return set_err(OKT_ERR_INVALID_ARGUMENT, "null argument");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  int rc = c->ensure(c->hgrad, 4 * std::max<size_t>(n, 1));
+  if (rc) return rc;
+  if (n && (rc = c->ck(cudaMemcpyAsync(c->hgrad.p, h_grad, 4 * n, cudaMemcpyHostToDevice, s), "h2d"))) return rc;
+  okt_result r{};
+  if ((rc = c->reserve(n))) return rc;
+  rc = c->step(c->hgrad.as<float>(), d_w, n, alpha, t, k, true, &r, s);
+  if (rc) return rc;
+  if (out) *out = r;
+  return copy_result_to_host(c, r, h_u_idx, h_u_val, nullptr, u_cap, s);
+}
+
+int okt_memcpy_h2d(void* d_dst, const void* h_src, size_t bytes, void* stream) {
+  cudaError_t e = stream ? cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream))
+                         : cudaMemcpy(d_dst, h_src, bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, cudaGetErrorString(e));
+  return OKT_OK;
+}
+
+int okt_memcpy_d2h(void* h_dst, const void* d_src, size_t bytes, void* stream) {
+  cudaError_t e = stream ? cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream))
+                         : cudaMemcpy(h_dst, d_src, bytes, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && stream) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, cudaGetErrorString(e));
+  return OKT_OK;
+}
+
+// ---- sub-phases ----------------------------------------------------------------------
+int okt_th_re_evaluate_dense(okt_comm* c, const float* d_g, size_t n, size_t k, double* th, void* stream) {
+  OKT_COMM_CHECK(c);
+  if (n == 0) return set_err(OKT_ERR_INVALID_ARGUMENT, "th_re_evaluate: empty gradient");
+  if (k < 1) return set_err(OKT_ERR_INVALID_ARGUMENT, "th_re_evaluate: k must be >= 1");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  int rc = c->ck(okt::launch_radix_select(c->L, okt::RadixSrc::kDenseF32, d_g, n, nullptr, n, k, &c->d()->rs,
+                                          c->hist.as<uint32_t>(), &c->d()->th_arg, false), "radix");
+  if (rc || (rc = c->sync(s))) return rc;
+  *th = c->h->th_arg;
+  return OKT_OK;
+}
+
+int okt_th_re_evaluate_sparse(okt_comm* c, const double* d_val, size_t nnz, size_t k, double* th, void* stream) {
+  OKT_COMM_CHECK(c);
+  if (nnz == 0) return set_err(OKT_ERR_INVALID_ARGUMENT, "th_re_evaluate: empty gradient");
+  if (k < 1) return set_err(OKT_ERR_INVALID_ARGUMENT, "th_re_evaluate: k must be >= 1");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  int rc = c->ck(okt::launch_radix_select(c->L, okt::RadixSrc::kF64, d_val, nnz, nullptr, nnz, k, &c->d()->rs,
+                                          c->hist.as<uint32_t>(), &c->d()->th_arg, false), "radix");
+  if (rc || (rc = c->sync(s))) return rc;
+  *th = c->h->th_arg;
+  return OKT_OK;
+}
+
+int okt_select_by_threshold(okt_comm* c, const float* d_g, size_t n, double th, okt_sparse* out, void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!(th >= 0.0)) return set_err(OKT_ERR_INVALID_ARGUMENT, "select_by_threshold: th must be >= 0");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  int rc = c->reserve(std::max<size_t>(n, 1));
+  c->L.status = c->status.as<uint64_t>();
+  if (rc) return rc;
+  if ((rc = c->ensure(c->sel_idx, 4 * std::max<size_t>(n, 1))) ||
+      (rc = c->ensure(c->sel_val, 8 * std::max<size_t>(n, 1))))
+    return rc;
+  if ((rc = c->upload_f64(&c->d()->th_arg, th, &c->hup->th_arg, s))) return rc;
+  if (n) {
+    rc = c->ck(okt::launch_k1(c->L, okt::K1Mode::kSelect, d_g, nullptr, nullptr, 0.f, n, &c->d()->th_arg,
+                              c->coo.as<uint64_t>(), &c->d()->m, &c->d()->flags, nullptr), "k1");
+    if (!rc) rc = c->ck(okt::launch_extract(c->L, c->coo.as<uint64_t>(), &c->d()->m, n, c->sel_idx.as<uint32_t>(),
+                                            c->sel_val.as<double>()), "extract");
+  } else {
+    rc = c->ck(cudaMemsetAsync(&c->d()->m, 0, 8, s), "memset");
+  }
+  if (rc || (rc = c->sync(s))) return rc;
+  out->d_idx = c->sel_idx.as<uint32_t>();
+  out->d_val = c->sel_val.as<double>();
+  out->nnz = c->h->m;
+  out->n = n;
+  return OKT_OK;
+}
+
+int okt_space_repartition(okt_comm* c, const uint32_t* d_sel_idx, size_t m, size_t n, uint64_t* cuts_out,
+                          void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!cuts_out) return set_err(OKT_ERR_INVALID_ARGUMENT, "null cuts");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  int rc = c->repartition_dev(d_sel_idx, 1, nullptr, m, n, s);
+  if (rc || (rc = c->sync(s))) return rc;
+  for (int q = 0; q <= c->P; ++q) cuts_out[q] = c->h->cuts[q];
+  c->dev_stale = true;  // device cuts no longer mirror the state
+  return OKT_OK;
+}
+
+int okt_split_and_reduce(okt_comm* c, const float* d_g, size_t n, double local_th, const uint64_t* cuts,
+                         uint32_t bucket, okt_sparse* region, okt_sparse* local, void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!cuts) return set_err(OKT_ERR_INVALID_ARGUMENT, "split_and_reduce: boundaries do not match P");
+  if (!(local_th >= 0.0)) return set_err(OKT_ERR_INVALID_ARGUMENT, "select_by_threshold: th must be >= 0");
+  if (n == 0 || n > 0xffffffffull) return set_err(OKT_ERR_INVALID_ARGUMENT, "bad n");
+  for (int q = 0; q < c->P; ++q)
+    if (cuts[q] > cuts[q + 1] || cuts[c->P] > n)
+      return set_err(OKT_ERR_INVALID_ARGUMENT, "split_and_reduce: bad boundaries");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  int rc = c->reserve(n);
+  c->L.status = c->status.as<uint64_t>();
+  if (rc) return rc;
+  if ((rc = c->ensure(c->sel_idx, 4 * n)) || (rc = c->ensure(c->sel_val, 8 * n))) return rc;
+  if ((rc = c->upload_f64(&c->d()->th_arg, local_th, &c->hup->th_arg, s))) return rc;
+  std::memcpy(c->hup->cuts, cuts, sizeof(uint64_t) * (c->P + 1));
+  if ((rc = c->ck(cudaMemcpyAsync(c->d()->cuts, c->hup->cuts, sizeof(uint64_t) * (c->P + 1),
+                                  cudaMemcpyHostToDevice, s), "upload")))
+    return rc;
+  c->dev_stale = true;
+  if ((rc = c->ck(cudaMemsetAsync(&c->d()->flags, 0, 4, s), "memset"))) return rc;
+  rc = c->ck(okt::launch_k1(c->L, okt::K1Mode::kSelect, d_g, nullptr, nullptr, 0.f, n, &c->d()->th_arg,
+                            c->coo.as<uint64_t>(), &c->d()->m, &c->d()->flags, nullptr), "k1");
+  if (rc) return rc;
+  // The reference's split_and_reduce does not test finiteness; keep the
+  // collective non-finite abort of the full step out of this entry point.
+  if ((rc = c->ck(cudaMemsetAsync(&c->d()->flags, 0, 4, s), "memset"))) return rc;
+  if (c->P == 1) {
+    if ((rc = c->ensure(c->reg_idx, 4 * n)) || (rc = c->ensure(c->reg_val, 8 * n))) return rc;
+    rc = c->ck(okt::launch_extract(c->L, c->coo.as<uint64_t>(), &c->d()->m, n, c->reg_idx.as<uint32_t>(),
+                                   c->reg_val.as<double>()), "extract");
+    if (rc) return rc;
+    rc = c->ck(cudaMemcpyAsync(&c->d()->R, &c->d()->m, 8, cudaMemcpyDeviceToDevice, s), "copy");
+  } else {
+    uint64_t bound = 0;
+    rc = c->split_reduce_dev(n, bucket, false, nullptr, c->reg_idx, c->reg_val, &c->d()->R, bound, s);
+  }
+  if (rc) return c->abort_step(rc);
+  rc = c->ck(okt::launch_extract(c->L, c->coo.as<uint64_t>(), &c->d()->m, n, c->sel_idx.as<uint32_t>(),
+                                 c->sel_val.as<double>()), "extract");
+  if (rc || (rc = c->sync(s))) return rc;
+  if (c->h->flags & 2u) return set_err(OKT_ERR_PROTOCOL, "split_and_reduce: entries outside my region");
+  region->d_idx = c->reg_idx.as<uint32_t>();
+  region->d_val = c->reg_val.as<double>();
+  region->nnz = c->h->R;
+  region->n = n;
+  local->d_idx = c->sel_idx.as<uint32_t>();
+  local->d_val = c->sel_val.as<double>();
+  local->nnz = c->h->m;
+  local->n = n;
+  return OKT_OK;
+}
+
+int okt_balance_and_allgatherv(okt_comm* c, const uint32_t* d_idx, const double* d_val, size_t nnz, size_t n,
+                               double global_th, okt_sparse* u, void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!(global_th >= 0.0)) return set_err(OKT_ERR_INVALID_ARGUMENT, "select_by_threshold: th must be >= 0");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  int rc;
+  if ((rc = c->ensure(c->sur_idx, 4 * std::max<size_t>(nnz, 1))) ||
+      (rc = c->ensure(c->sur_val, 8 * std::max<size_t>(nnz, 1))))
+    return rc;
+  if ((rc = c->upload_f64(&c->d()->th_arg, global_th, &c->hup->th_arg, s))) return rc;
+  if ((rc = c->upload_u64(&c->d()->R, nnz, &c->hup->R, s))) return rc;
+  rc = c->ck(okt::launch_filter(c->L, false, nullptr, d_idx, d_val, &c->d()->R, nnz, &c->d()->th_arg,
+                                c->sur_idx.as<uint32_t>(), c->sur_val.as<double>(), &c->d()->S), "filter");
+  if (rc) return rc;
+  if (c->P == 1) {
+    if ((rc = c->sync(s))) return rc;
+    u->d_idx = c->sur_idx.as<uint32_t>();
+    u->d_val = c->sur_val.as<double>();
+    u->nnz = c->h->S;
+    u->n = n;
+    return OKT_OK;
+  }
+  uint64_t U = 0;
+  rc = c->balance_allgatherv_dev(s, U);
+  if (rc || (rc = c->sync(s))) return rc;
+  u->d_idx = c->u_idx.as<uint32_t>();
+  u->d_val = c->u_val.as<double>();
+  u->nnz = U;
+  u->n = n;
+  return OKT_OK;
+}
+
+// ---- instrumentation --------------------------------------------------------------------
+int okt_set_profiling(okt_comm* c, int on) {
+  OKT_COMM_CHECK(c);
+  c->prof = on != 0;
+  return OKT_OK;
+}
+
+int okt_phase_times(okt_comm* c, double* ms, uint64_t* calls) {
+  OKT_COMM_CHECK(c);
+  for (int i = 0; i < OKT_T_COUNT; ++i) {
+    if (ms) ms[i] = c->t_ms[i];
+    if (calls) calls[i] = c->t_calls[i];
+  }
+  return OKT_OK;
+}
+
+int okt_reset_phase_times(okt_comm* c) {
+  OKT_COMM_CHECK(c);
+  std::memset(c->t_ms, 0, sizeof(c->t_ms));
+  std::memset(c->t_calls, 0, sizeof(c->t_calls));
+  return OKT_OK;
+}
+
+int okt_kernel_launches(const okt_comm* c, uint64_t* out) {
+  OKT_COMM_CHECK(c);
+  if (out) *out = c->L.launches;
+  return OKT_OK;
+}
+
+}  // extern "C"

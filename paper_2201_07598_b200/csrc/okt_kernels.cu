@@ -1,0 +1,865 @@
+// okt_kernels.cu — sm_100a kernels of the Ok-Topk sparse allreduce.
+//
+// Everything here is HBM- or latency-bound integer/byte work: 128-bit
+// coalesced streaming loads, warp-ballot + decoupled look-back compaction, and
+// O(k) scatters.  No tensor cores: nothing on this path is a contraction.
+//
+// Reference functions each kernel replaces (proj/core/src/...):
+//   k1_kernel          trainer.cpp:423-435 make_accumulator, sparse.cpp:14-19
+//                      all_finite, sparse.cpp:94-106 select_by_threshold(Dense)
+//   radix_*            oktopk.cpp:12-26 th_re_evaluate -> sparse.cpp:43-80 topk_from
+//   scatter/region_scan sparse.cpp:206-257 sparse_sum (stride-doubling bracket)
+//   filter_kernel      sparse.cpp:108-120 select_by_threshold(Sparse)
+//   apply_kernel       oktopk.cpp:299-302 set_intersection, trainer.cpp:478-479
+//                      residual zero, trainer.cpp:437-442 apply_sparse_update
+//   proposals/cuts     oktopk.cpp:28-61 space_repartition
+//   slice_offsets      sparse.cpp:190-202 sparse_slice (lower_bound)
+#include "okt_device.cuh"
+#include "okt_kernels.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+namespace okt {
+
+namespace {
+
+template <typename K>
+int resident_ctas(K kernel, int threads, int sms) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  return per_sm * sms;
+}
+
+__device__ __forceinline__ bool nonfinite(float a) {
+  return (__float_as_uint(a) & 0x7f800000u) == 0x7f800000u;
+}
+
+}  // namespace
+
+// =============================================================================
+// K1: fused accumulate / select / compact
+// =============================================================================
+template <bool ACCUM, bool SELECT, bool HIST, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    k1_kernel(const float* __restrict__ g, const float* eps_in, float* eps_out, float alpha,
+              uint64_t n, uint32_t num_tiles, const double* __restrict__ d_th,
+              uint64_t* __restrict__ out, uint64_t* d_m, uint64_t* status, uint32_t epoch,
+              uint32_t* ctr, uint32_t* d_flags, uint32_t* d_hist) {
+  __shared__ TileScanSmem s;
+  __shared__ uint32_t s_hist[HIST ? 2048 : 1];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  float tf = 0.f;
+  if (SELECT) tf = ceil_to_float(*d_th);
+  if (HIST) {
+    for (int i = tid; i < 2048; i += kThreads) s_hist[i] = 0;
+  }
+  bool bad = false;
+  for (;;) {
+    const uint32_t tile = fetch_tile(ctr, s.tile);
+    if (tile >= num_tiles) break;
+    const uint64_t base = uint64_t(tile) * kTile;
+    float a[kJ][kC];
+    bool valid[kJ][kC];
+    if (VEC && base + kTile <= n) {
+      float4 gv[kJ], ev[kJ];
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const uint64_t e0 = base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC;
+        gv[j] = __ldg(reinterpret_cast<const float4*>(g + e0));
+        if (ACCUM) ev[j] = *reinterpret_cast<const float4*>(eps_in + e0);
+      }
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        if (ACCUM) {
+          a[j][0] = fmaf(alpha, gv[j].x, ev[j].x);
+          a[j][1] = fmaf(alpha, gv[j].y, ev[j].y);
+          a[j][2] = fmaf(alpha, gv[j].z, ev[j].z);
+          a[j][3] = fmaf(alpha, gv[j].w, ev[j].w);
+          const uint64_t e0 = base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC;
+          *reinterpret_cast<float4*>(eps_out + e0) = make_float4(a[j][0], a[j][1], a[j][2], a[j][3]);
+        } else {
+          a[j][0] = gv[j].x;
+          a[j][1] = gv[j].y;
+          a[j][2] = gv[j].z;
+          a[j][3] = gv[j].w;
+        }
+#pragma unroll
+        for (int c = 0; c < kC; ++c) {
+          valid[j][c] = true;
+          bad |= nonfinite(a[j][c]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+#pragma unroll
+        for (int c = 0; c < kC; ++c) {
+          const uint64_t e = base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC + c;
+          valid[j][c] = e < n;
+          float x = 0.f;
+          if (valid[j][c]) {
+            x = g[e];
+            if (ACCUM) {
+              x = fmaf(alpha, x, eps_in[e]);
+              eps_out[e] = x;
+            }
+            bad |= nonfinite(x);
+          }
+          a[j][c] = x;
+        }
+      }
+    }
+    if (HIST) {
+#pragma unroll
+      for (int j = 0; j < kJ; ++j)
+#pragma unroll
+        for (int c = 0; c < kC; ++c)
+          if (valid[j][c]) atomicAdd(&s_hist[(__float_as_uint(a[j][c]) & 0x7fffffffu) >> 20], 1u);
+    }
+    if (SELECT) {
+      unsigned bal[kJ][kC];
+      bool pred[kJ][kC];
+#pragma unroll
+      for (int j = 0; j < kJ; ++j)
+#pragma unroll
+        for (int c = 0; c < kC; ++c) {
+          pred[j][c] = valid[j][c] && fabsf(a[j][c]) >= tf;
+          bal[j][c] = __ballot_sync(0xffffffffu, pred[j][c]);
+        }
+      tile_scan<kC>(s, bal, tile, num_tiles, status, epoch, d_m);
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const uint32_t gbase = s.base + s.cnt[j * kWarps + warp];
+#pragma unroll
+        for (int c = 0; c < kC; ++c) {
+          if (pred[j][c]) {
+            const uint32_t pos = gbase + rank_in_group<kC>(bal, j, c);
+            const uint64_t e = base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC + c;
+            out[pos] = coo_pack(uint32_t(e), a[j][c]);
+          }
+        }
+      }
+    }
+  }
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(d_flags, 1u);
+  if (HIST) {
+    for (int i = tid; i < 2048; i += kThreads)
+      if (s_hist[i]) atomicAdd(&d_hist[i], s_hist[i]);
+  }
+  retire_cta(ctr);
+}
+
+template <bool ACCUM, bool SELECT, bool HIST>
+static cudaError_t k1_dispatch(Launch& L, bool vec, const float* g, const float* eps_in,
+                               float* eps_out, float alpha, uint64_t n, const double* d_th,
+                               uint64_t* out, uint64_t* d_m, uint32_t* d_flags, uint32_t* d_hist) {
+  const uint32_t tiles = uint32_t((n + kTile - 1) / kTile);
+  auto kern = vec ? k1_kernel<ACCUM, SELECT, HIST, true> : k1_kernel<ACCUM, SELECT, HIST, false>;
+  static int cap_v = 0, cap_s = 0;
+  int& cap = vec ? cap_v : cap_s;
+  if (!cap) cap = resident_ctas(kern, kThreads, L.sms);
+  const int grid = int(std::min<uint64_t>(tiles, uint64_t(cap)));
+  const uint32_t ep = SELECT ? L.next_epoch() : 0;
+  kern<<<grid, kThreads, 0, L.s>>>(g, eps_in, eps_out, alpha, n, tiles, d_th, out, d_m, L.status,
+                                   ep, L.ctr, d_flags, d_hist);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k1(Launch& L, K1Mode mode, const float* g, const float* eps_in, float* eps_out,
+                      float alpha, uint64_t n, const double* d_th, uint64_t* out, uint64_t* d_m,
+                      uint32_t* d_flags, uint32_t* d_hist) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  bool vec = al(g);
+  if (mode != K1Mode::kSelect) vec = vec && al(eps_in) && al(eps_out);
+  switch (mode) {
+    case K1Mode::kSelect:
+      return k1_dispatch<false, true, false>(L, vec, g, eps_in, eps_out, alpha, n, d_th, out, d_m,
+                                             d_flags, d_hist);
+    case K1Mode::kAccumSelect:
+      return k1_dispatch<true, true, false>(L, vec, g, eps_in, eps_out, alpha, n, d_th, out, d_m,
+                                            d_flags, d_hist);
+    case K1Mode::kAccumHist:
+      return k1_dispatch<true, false, true>(L, vec, g, eps_in, eps_out, alpha, n, d_th, out, d_m,
+                                            d_flags, d_hist);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// =============================================================================
+// K2 / K4: radix select of the k-th largest magnitude
+// =============================================================================
+template <int SRC>  // 0: dense f32, 1: AoS (u32 idx | f32 val << 32), 2: f64
+__device__ __forceinline__ uint64_t mag_key(const void* data, uint64_t i) {
+  if (SRC == 0) return uint64_t(__float_as_uint(static_cast<const float*>(data)[i]) & 0x7fffffffu);
+  if (SRC == 1) return (static_cast<const uint64_t*>(data)[i] >> 32) & 0x7fffffffull;
+  return uint64_t(__double_as_longlong(static_cast<const double*>(data)[i])) & 0x7fffffffffffffffull;
+}
+
+__global__ void radix_init_kernel(RadixState* rs, uint64_t k, uint64_t n_host, const uint64_t* d_n) {
+  const uint64_t cnt = d_n ? *d_n : n_host;
+  rs->prefix = 0;
+  rs->kk = k < cnt ? k : cnt;
+  rs->active = cnt > 0 ? 1u : 0u;
+  rs->pad = 0;
+}
+
+template <int SRC>
+__global__ void __launch_bounds__(kThreads)
+    radix_hist_kernel(const void* __restrict__ data, uint64_t n_host, const uint64_t* d_n,
+                      const RadixState* rs, int shift, int bits, uint32_t* hist) {
+  __shared__ uint32_t sh[2048];
+  const int nb = 1 << bits;
+  for (int i = threadIdx.x; i < nb; i += kThreads) sh[i] = 0;
+  __syncthreads();
+  if (!rs->active) return;
+  const uint64_t n = d_n ? *d_n : n_host;
+  const uint64_t prefix = rs->prefix;
+  const int hi = shift + bits;
+  const uint64_t want = prefix >> hi;
+  const uint64_t stride = uint64_t(gridDim.x) * kThreads;
+  uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    uint64_t k0 = mag_key<SRC>(data, i), k1 = mag_key<SRC>(data, i + stride);
+    uint64_t k2 = mag_key<SRC>(data, i + 2 * stride), k3 = mag_key<SRC>(data, i + 3 * stride);
+    if ((k0 >> hi) == want) atomicAdd(&sh[(k0 >> shift) & (nb - 1)], 1u);
+    if ((k1 >> hi) == want) atomicAdd(&sh[(k1 >> shift) & (nb - 1)], 1u);
+    if ((k2 >> hi) == want) atomicAdd(&sh[(k2 >> shift) & (nb - 1)], 1u);
+    if ((k3 >> hi) == want) atomicAdd(&sh[(k3 >> shift) & (nb - 1)], 1u);
+  }
+  for (; i < n; i += stride) {
+    const uint64_t k0 = mag_key<SRC>(data, i);
+    if ((k0 >> hi) == want) atomicAdd(&sh[(k0 >> shift) & (nb - 1)], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += kThreads)
+    if (sh[b]) atomicAdd(&hist[b], sh[b]);
+}
+
+// One CTA of 1024 threads: find the bin holding the kk-th largest key, update
+// the prefix, clear the histogram for the next pass.
+__global__ void __launch_bounds__(1024)
+    radix_pick_kernel(RadixState* rs, uint32_t* hist, int shift, int bits, int last, int f64,
+                      double* th_out) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t s_bin, s_above;
+  const int nb = 1 << bits;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const bool active = rs->active != 0;
+  // Bins in descending order: position q holds bin nb-1-q.
+  const int q0 = 2 * t, q1 = 2 * t + 1;
+  const uint32_t c0 = (active && q0 < nb) ? hist[nb - 1 - q0] : 0u;
+  const uint32_t c1 = (active && q1 < nb) ? hist[nb - 1 - q1] : 0u;
+  uint32_t v = c0 + c1, incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  if (lane == 31) warp_sums[w] = incl;
+  if (t == 0) { s_bin = 0xffffffffu; s_above = 0; }
+  __syncthreads();
+  if (w == 0) {
+    uint32_t ws = warp_sums[lane], wi = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += x;
+    }
+    warp_sums[lane] = wi - ws;
+  }
+  __syncthreads();
+  const uint32_t excl = warp_sums[w] + incl - v;
+  if (active) {
+    const uint64_t kk = rs->kk;
+    if (excl < kk && uint64_t(excl) + c0 >= kk) {
+      s_bin = uint32_t(nb - 1 - q0);
+      s_above = excl;
+    } else if (uint64_t(excl) + c0 < kk && uint64_t(excl) + c0 + c1 >= kk) {
+      s_bin = uint32_t(nb - 1 - q1);
+      s_above = excl + c0;
+    }
+  }
+  __syncthreads();
+  for (int b = t; b < nb; b += 1024) hist[b] = 0;
+  if (t == 0 && active && s_bin != 0xffffffffu) {
+    const uint64_t prefix = rs->prefix | (uint64_t(s_bin) << shift);
+    rs->prefix = prefix;
+    rs->kk = rs->kk - s_above;
+    if (last) {
+      *th_out = f64 ? __longlong_as_double(static_cast<long long>(prefix))
+                    : double(__uint_as_float(uint32_t(prefix)));
+    }
+  }
+}
+
+cudaError_t launch_radix_init(Launch& L, RadixState* d_rs, uint64_t k, uint64_t n_host,
+                              const uint64_t* d_n) {
+  radix_init_kernel<<<1, 1, 0, L.s>>>(d_rs, k, n_host, d_n);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_radix_select(Launch& L, RadixSrc src, const void* data, uint64_t n_host,
+                                const uint64_t* d_n, uint64_t n_bound, uint64_t k,
+                                RadixState* d_rs, uint32_t* d_hist, double* d_th_out,
+                                bool hist0_done) {
+  static const int f32_pass[3][2] = {{20, 11}, {10, 10}, {0, 10}};
+  static const int f64_pass[6][2] = {{52, 11}, {41, 11}, {30, 11}, {19, 11}, {8, 11}, {0, 8}};
+  const bool f64 = src == RadixSrc::kF64;
+  const int npass = f64 ? 6 : 3;
+  cudaError_t e;
+  if (!hist0_done) {
+    if ((e = launch_radix_init(L, d_rs, k, n_host, d_n)) != cudaSuccess) return e;
+  }
+  const uint64_t bound = d_n ? n_bound : n_host;
+  const int grid = int(std::max<uint64_t>(
+      1, std::min<uint64_t>((bound + kThreads * 8 - 1) / (kThreads * 8), uint64_t(L.sms) * 8)));
+  for (int p = 0; p < npass; ++p) {
+    const int shift = f64 ? f64_pass[p][0] : f32_pass[p][0];
+    const int bits = f64 ? f64_pass[p][1] : f32_pass[p][1];
+    if (!(p == 0 && hist0_done)) {
+      switch (src) {
+        case RadixSrc::kDenseF32:
+          radix_hist_kernel<0><<<grid, kThreads, 0, L.s>>>(data, n_host, d_n, d_rs, shift, bits, d_hist);
+          break;
+        case RadixSrc::kAosF32:
+          radix_hist_kernel<1><<<grid, kThreads, 0, L.s>>>(data, n_host, d_n, d_rs, shift, bits, d_hist);
+          break;
+        case RadixSrc::kF64:
+          radix_hist_kernel<2><<<grid, kThreads, 0, L.s>>>(data, n_host, d_n, d_rs, shift, bits, d_hist);
+          break;
+      }
+      ++L.launches;
+    }
+    radix_pick_kernel<<<1, 1024, 0, L.s>>>(d_rs, d_hist, shift, bits, p == npass - 1, f64 ? 1 : 0,
+                                           d_th_out);
+    ++L.launches;
+  }
+  return cudaGetLastError();
+}
+
+// =============================================================================
+// Survivor filter and K7 apply (COO lists with device-resident lengths)
+// =============================================================================
+template <bool AOS>
+__device__ __forceinline__ void load_coo4(const uint64_t* in_aos, const uint32_t* in_idx,
+                                          const double* in_val, uint64_t e0, uint64_t cnt,
+                                          uint32_t (&idx)[kC], double (&val)[kC],
+                                          bool (&valid)[kC]) {
+  if (e0 + kC <= cnt) {
+    if (AOS) {
+      const ulonglong2 p0 = *reinterpret_cast<const ulonglong2*>(in_aos + e0);
+      const ulonglong2 p1 = *reinterpret_cast<const ulonglong2*>(in_aos + e0 + 2);
+      const uint64_t ev[4] = {p0.x, p0.y, p1.x, p1.y};
+#pragma unroll
+      for (int c = 0; c < kC; ++c) {
+        idx[c] = coo_idx(ev[c]);
+        val[c] = double(coo_val(ev[c]));
+      }
+    } else {
+      const uint4 iv = *reinterpret_cast<const uint4*>(in_idx + e0);
+      const double2 v0 = *reinterpret_cast<const double2*>(in_val + e0);
+      const double2 v1 = *reinterpret_cast<const double2*>(in_val + e0 + 2);
+      idx[0] = iv.x; idx[1] = iv.y; idx[2] = iv.z; idx[3] = iv.w;
+      val[0] = v0.x; val[1] = v0.y; val[2] = v1.x; val[3] = v1.y;
+    }
+#pragma unroll
+    for (int c = 0; c < kC; ++c) valid[c] = true;
+  } else {
+#pragma unroll
+    for (int c = 0; c < kC; ++c) {
+      const uint64_t e = e0 + c;
+      valid[c] = e < cnt;
+      idx[c] = 0;
+      val[c] = 0.0;
+      if (valid[c]) {
+        if (AOS) {
+          idx[c] = coo_idx(in_aos[e]);
+          val[c] = double(coo_val(in_aos[e]));
+        } else {
+          idx[c] = in_idx[e];
+          val[c] = in_val[e];
+        }
+      }
+    }
+  }
+}
+
+template <bool AOS>
+__global__ void __launch_bounds__(kThreads)
+    filter_kernel(const uint64_t* __restrict__ in_aos, const uint32_t* __restrict__ in_idx,
+                  const double* __restrict__ in_val, const uint64_t* d_cnt_in,
+                  const double* d_th, uint32_t* __restrict__ out_idx,
+                  double* __restrict__ out_val, uint64_t* d_cnt_out, uint64_t* status,
+                  uint32_t epoch, uint32_t* ctr) {
+  __shared__ TileScanSmem s;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint64_t cnt = *d_cnt_in;
+  const double th = *d_th;
+  const uint32_t num_tiles = uint32_t((cnt + kTile - 1) / kTile);
+  if (num_tiles == 0 && blockIdx.x == 0 && tid == 0) *d_cnt_out = 0;
+  for (;;) {
+    const uint32_t tile = fetch_tile(ctr, s.tile);
+    if (tile >= num_tiles) break;
+    const uint64_t base = uint64_t(tile) * kTile;
+    uint32_t idx[kJ][kC];
+    double val[kJ][kC];
+    bool pred[kJ][kC];
+    unsigned bal[kJ][kC];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      bool valid[kC];
+      load_coo4<AOS>(in_aos, in_idx, in_val, base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC,
+                     cnt, idx[j], val[j], valid);
+#pragma unroll
+      for (int c = 0; c < kC; ++c) {
+        pred[j][c] = valid[c] && fabs(val[j][c]) >= th;
+        bal[j][c] = __ballot_sync(0xffffffffu, pred[j][c]);
+      }
+    }
+    tile_scan<kC>(s, bal, tile, num_tiles, status, epoch, d_cnt_out);
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const uint32_t gbase = s.base + s.cnt[j * kWarps + warp];
+#pragma unroll
+      for (int c = 0; c < kC; ++c)
+        if (pred[j][c]) {
+          const uint32_t pos = gbase + rank_in_group<kC>(bal, j, c);
+          out_idx[pos] = idx[j][c];
+          out_val[pos] = val[j][c];
+        }
+    }
+  }
+  retire_cta(ctr);
+}
+
+cudaError_t launch_filter(Launch& L, bool aos, const uint64_t* in_aos, const uint32_t* in_idx,
+                          const double* in_val, const uint64_t* d_cnt_in, uint64_t bound,
+                          const double* d_th, uint32_t* out_idx, double* out_val,
+                          uint64_t* d_cnt_out) {
+  const uint64_t tiles = std::max<uint64_t>(1, (bound + kTile - 1) / kTile);
+  static int cap_a = 0, cap_s = 0;
+  int& cap = aos ? cap_a : cap_s;
+  if (!cap) cap = aos ? resident_ctas(filter_kernel<true>, kThreads, L.sms)
+                      : resident_ctas(filter_kernel<false>, kThreads, L.sms);
+  const int grid = int(std::min<uint64_t>(tiles, uint64_t(cap)));
+  const uint32_t ep = L.next_epoch();
+  if (aos)
+    filter_kernel<true><<<grid, kThreads, 0, L.s>>>(in_aos, in_idx, in_val, d_cnt_in, d_th, out_idx,
+                                                    out_val, d_cnt_out, L.status, ep, L.ctr);
+  else
+    filter_kernel<false><<<grid, kThreads, 0, L.s>>>(in_aos, in_idx, in_val, d_cnt_in, d_th, out_idx,
+                                                     out_val, d_cnt_out, L.status, ep, L.ctr);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(kThreads)
+    apply_kernel(const uint32_t* __restrict__ u_idx, const double* __restrict__ u_val,
+                 const uint64_t* d_U, float* acc, int zero_eps, float* w, int P,
+                 const double* d_local_th, uint32_t* __restrict__ out_indexes, uint64_t* d_nidx,
+                 uint32_t* d_flags, uint64_t* status, uint32_t epoch, uint32_t* ctr) {
+  __shared__ TileScanSmem s;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  // A step whose input was non-finite applies nothing (the reference throws
+  // before touching the residual or the model).
+  const bool skip = (*d_flags & 1u) != 0;
+  const uint64_t cnt = skip ? 0 : *d_U;
+  const float tf = ceil_to_float(*d_local_th);
+  const double dP = double(P);
+  const uint32_t num_tiles = uint32_t((cnt + kTile - 1) / kTile);
+  if (num_tiles == 0 && blockIdx.x == 0 && tid == 0) *d_nidx = 0;
+  bool bad = false;
+  for (;;) {
+    const uint32_t tile = fetch_tile(ctr, s.tile);
+    if (tile >= num_tiles) break;
+    const uint64_t base = uint64_t(tile) * kTile;
+    uint32_t idx[kJ][kC];
+    double val[kJ][kC];
+    bool pred[kJ][kC];
+    unsigned bal[kJ][kC];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      bool valid[kC];
+      load_coo4<false>(nullptr, u_idx, u_val, base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC,
+                       cnt, idx[j], val[j], valid);
+#pragma unroll
+      for (int c = 0; c < kC; ++c) {
+        bool sel = false;
+        if (valid[c]) {
+          const uint32_t i = idx[j][c];
+          sel = fabsf(acc[i]) >= tf;
+          if (w) {
+            const float nw = float(double(w[i]) - val[j][c] / dP);
+            w[i] = nw;
+            bad |= nonfinite(nw);
+          }
+          if (zero_eps && sel) acc[i] = 0.f;
+        }
+        pred[j][c] = sel;
+        bal[j][c] = __ballot_sync(0xffffffffu, sel);
+      }
+    }
+    tile_scan<kC>(s, bal, tile, num_tiles, status, epoch, d_nidx);
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const uint32_t gbase = s.base + s.cnt[j * kWarps + warp];
+#pragma unroll
+      for (int c = 0; c < kC; ++c)
+        if (pred[j][c]) out_indexes[gbase + rank_in_group<kC>(bal, j, c)] = idx[j][c];
+    }
+  }
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(d_flags, 4u);
+  retire_cta(ctr);
+}
+
+cudaError_t launch_apply(Launch& L, const uint32_t* u_idx, const double* u_val, const uint64_t* d_U,
+                         uint64_t bound, float* acc, bool zero_eps, float* w, int P,
+                         const double* d_local_th, uint32_t* out_indexes, uint64_t* d_nidx,
+                         uint32_t* d_flags) {
+  const uint64_t tiles = std::max<uint64_t>(1, (bound + kTile - 1) / kTile);
+  static int cap = 0;
+  if (!cap) cap = resident_ctas(apply_kernel, kThreads, L.sms);
+  const int grid = int(std::min<uint64_t>(tiles, uint64_t(cap)));
+  const uint32_t ep = L.next_epoch();
+  apply_kernel<<<grid, kThreads, 0, L.s>>>(u_idx, u_val, d_U, acc, zero_eps ? 1 : 0, w, P, d_local_th,
+                                           out_indexes, d_nidx, d_flags, L.status, ep, L.ctr);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+// =============================================================================
+// K3: region merge — scatter (M1) + ordered bracket scan (M2)
+// =============================================================================
+__global__ void __launch_bounds__(kThreads)
+    scatter_kernel(Segs segs, uint64_t lo, uint64_t W, int P, uint32_t* mask, float* stage,
+                   uint32_t* d_flags) {
+  const uint64_t total = segs.start[segs.nseg];
+  const uint64_t stride = uint64_t(gridDim.x) * kThreads;
+  for (uint64_t e = uint64_t(blockIdx.x) * kThreads + threadIdx.x; e < total; e += stride) {
+    int sg = 0;
+    while (sg + 1 < segs.nseg && e >= segs.start[sg + 1]) ++sg;
+    const uint64_t entry = segs.ptr[sg][e - segs.start[sg]];
+    const uint64_t idx = coo_idx(entry);
+    if (idx < lo || idx - lo >= W) {
+      atomicOr(d_flags, 2u);
+      continue;
+    }
+    const uint64_t i = idx - lo;
+    const int src = segs.src[sg];
+    stage[i * uint64_t(P) + src] = coo_val(entry);
+    atomicOr(&mask[i >> 2], 1u << (unsigned(i & 3u) * 8u + unsigned(src)));
+  }
+}
+
+cudaError_t launch_scatter(Launch& L, const Segs& segs, uint64_t lo, uint64_t W, int P,
+                           uint32_t* mask, float* stage, uint32_t* d_flags) {
+  const uint64_t total = segs.start[segs.nseg];
+  if (total == 0) return cudaSuccess;
+  const int grid = int(std::min<uint64_t>((total + kThreads - 1) / kThreads, uint64_t(L.sms) * 16));
+  scatter_kernel<<<grid, kThreads, 0, L.s>>>(segs, lo, W, P, mask, stage, d_flags);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+// Fixed stride-doubling bracket over source ranks with absent pass-through
+// (sparse.cpp:238-245, tests/test_util.hpp:124-132):
+//   P=8: ((p0+p4)+(p2+p6)) + ((p1+p5)+(p3+p7))
+template <int P>
+__device__ __forceinline__ double bracket_sum(const float* st, uint32_t bits) {
+  double a[P];
+  bool h[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) {
+    h[q] = (bits >> q) & 1u;
+    a[q] = h[q] ? double(st[q]) : 0.0;
+  }
+#pragma unroll
+  for (int s = P >> 1; s >= 1; s >>= 1) {
+#pragma unroll
+    for (int q = 0; q < s; ++q) {
+      if (h[q] && h[q + s]) a[q] = a[q] + a[q + s];
+      else if (h[q + s]) a[q] = a[q + s];
+      h[q] = h[q] || h[q + s];
+    }
+  }
+  return a[0];
+}
+
+template <int P, bool FILTER>
+__global__ void __launch_bounds__(kThreads)
+    region_scan_kernel(uint64_t lo, uint64_t W, uint32_t num_tiles, uint32_t* mask,
+                       const float* __restrict__ stage, const double* d_gth,
+                       uint32_t* __restrict__ out_idx, double* __restrict__ out_val,
+                       uint64_t* d_count, uint64_t* status, uint32_t epoch, uint32_t* ctr) {
+  __shared__ TileScanSmem s;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const double gth = FILTER ? *d_gth : 0.0;
+  const uint64_t nwords = (W + 3) / 4;
+  for (;;) {
+    const uint32_t tile = fetch_tile(ctr, s.tile);
+    if (tile >= num_tiles) break;
+    const uint64_t base = uint64_t(tile) * kTile;
+    double val[kJ][kC];
+    bool pred[kJ][kC];
+    unsigned bal[kJ][kC];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const uint64_t wi = (base >> 2) + uint64_t(j) * kThreads + tid;
+      const uint32_t mw = wi < nwords ? mask[wi] : 0u;
+#pragma unroll
+      for (int c = 0; c < kC; ++c) {
+        const uint32_t bits = (mw >> (8 * c)) & 0xffu;
+        val[j][c] = 0.0;
+        bool p = false;
+        if (bits) {
+          val[j][c] = bracket_sum<P>(stage + (wi * 4 + c) * P, bits);
+          p = !FILTER || fabs(val[j][c]) >= gth;
+        }
+        pred[j][c] = p;
+        bal[j][c] = __ballot_sync(0xffffffffu, p);
+      }
+      if (mw) mask[wi] = 0u;
+    }
+    tile_scan<kC>(s, bal, tile, num_tiles, status, epoch, d_count);
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const uint32_t gbase = s.base + s.cnt[j * kWarps + warp];
+#pragma unroll
+      for (int c = 0; c < kC; ++c)
+        if (pred[j][c]) {
+          const uint32_t pos = gbase + rank_in_group<kC>(bal, j, c);
+          out_idx[pos] = uint32_t(lo + base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC + c);
+          out_val[pos] = val[j][c];
+        }
+    }
+  }
+  retire_cta(ctr);
+}
+
+template <int P, bool FILTER>
+static cudaError_t region_scan_dispatch(Launch& L, uint64_t lo, uint64_t W, uint32_t* mask,
+                                        const float* stage, const double* d_gth, uint32_t* out_idx,
+                                        double* out_val, uint64_t* d_count) {
+  const uint32_t tiles = uint32_t((W + kTile - 1) / kTile);
+  if (tiles == 0) {
+    cudaMemsetAsync(d_count, 0, sizeof(uint64_t), L.s);
+    return cudaGetLastError();
+  }
+  static int cap = 0;
+  if (!cap) cap = resident_ctas(region_scan_kernel<P, FILTER>, kThreads, L.sms);
+  const int grid = int(std::min<uint64_t>(tiles, uint64_t(cap)));
+  const uint32_t ep = L.next_epoch();
+  region_scan_kernel<P, FILTER><<<grid, kThreads, 0, L.s>>>(lo, W, tiles, mask, stage, d_gth, out_idx,
+                                                            out_val, d_count, L.status, ep, L.ctr);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_region_scan(Launch& L, int P, bool filter, uint64_t lo, uint64_t W,
+                               uint32_t* mask, const float* stage, const double* d_gth,
+                               uint32_t* out_idx, double* out_val, uint64_t* d_count) {
+#define OKT_RS(PP)                                                                              \
+  return filter ? region_scan_dispatch<PP, true>(L, lo, W, mask, stage, d_gth, out_idx, out_val, \
+                                                 d_count)                                       \
+                : region_scan_dispatch<PP, false>(L, lo, W, mask, stage, d_gth, out_idx, out_val, \
+                                                  d_count)
+  switch (P) {
+    case 1: OKT_RS(1);
+    case 2: OKT_RS(2);
+    case 4: OKT_RS(4);
+    case 8: OKT_RS(8);
+  }
+#undef OKT_RS
+  return cudaErrorInvalidValue;
+}
+
+// =============================================================================
+// Control kernels
+// =============================================================================
+__global__ void slice_offsets_kernel(const uint64_t* coo, const uint64_t* d_m, const uint64_t* cuts,
+                                     int P, uint64_t* off, uint32_t* cnt_out, const uint32_t* d_flags) {
+  __shared__ uint64_t s_off[kMaxP + 1];
+  const int d = threadIdx.x;
+  const uint64_t m = *d_m;
+  if (d <= P) {
+    // lower_bound of cuts[d] over the ascending indices of the local selection
+    const uint64_t key = cuts[d];
+    uint64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (uint64_t(coo_idx(coo[mid])) < key) lo = mid + 1;
+      else hi = mid;
+    }
+    s_off[d] = (d == P) ? m : lo;
+    off[d] = s_off[d];
+  }
+  __syncthreads();
+  if (d < P) cnt_out[d] = uint32_t(s_off[d + 1] - s_off[d]);
+  if (d == 0) cnt_out[P] = *d_flags;
+}
+
+cudaError_t launch_slice_offsets(Launch& L, const uint64_t* coo, const uint64_t* d_m,
+                                 const uint64_t* d_cuts, int P, uint64_t* d_off, uint32_t* d_cnt_out,
+                                 const uint32_t* d_flags) {
+  slice_offsets_kernel<<<1, 32, 0, L.s>>>(coo, d_m, d_cuts, P, d_off, d_cnt_out, d_flags);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+// space_repartition proposal (oktopk.cpp:39-49): cut_r = sel[floor(r*m/P)], or
+// r*n/P when nothing was selected.
+__global__ void proposals_kernel(const uint32_t* idx, int stride, const uint64_t* d_m, uint64_t m_host,
+                                 uint64_t n, int P, uint64_t* prop) {
+  const int r = threadIdx.x;
+  if (r > P) return;
+  const uint64_t m = d_m ? *d_m : m_host;
+  uint64_t cut;
+  if (r == 0) cut = 0;
+  else if (r == P) cut = n;
+  else if (m == 0) cut = uint64_t(r) * n / uint64_t(P);
+  else {
+    const uint64_t pos = uint64_t(r) * m / uint64_t(P);
+    cut = pos < m ? uint64_t(idx[pos * uint64_t(stride)]) : n;
+  }
+  prop[r] = cut;
+}
+
+cudaError_t launch_proposals(Launch& L, const uint32_t* idx, int stride, const uint64_t* d_m,
+                             uint64_t m_host, uint64_t n, int P, uint64_t* d_prop) {
+  proposals_kernel<<<1, 32, 0, L.s>>>(idx, stride, d_m, m_host, n, P, d_prop);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+// Consensus cuts (oktopk.cpp:51-61): the element-wise mean of P integer
+// proposals is exact in fp64 (sums < 2^53, P a power of two), so
+// llround(max(0, S/P)) == floor((2S + P) / 2P) in integers.
+__global__ void cuts_kernel(const uint64_t* allprop, int P, uint64_t n, uint64_t* cuts) {
+  if (threadIdx.x != 0) return;
+  cuts[0] = 0;
+  uint64_t prev = 0;
+  for (int r = 1; r < P; ++r) {
+    uint64_t S = 0;
+    for (int q = 0; q < P; ++q) S += allprop[uint64_t(q) * (P + 1) + r];
+    uint64_t rounded = (2 * S + uint64_t(P)) / (2 * uint64_t(P));
+    if (rounded > n) rounded = n;
+    if (rounded < prev) rounded = prev;
+    cuts[r] = rounded;
+    prev = rounded;
+  }
+  cuts[P] = n;
+}
+
+cudaError_t launch_cuts(Launch& L, const uint64_t* d_allprop, int P, uint64_t n, uint64_t* d_cuts) {
+  cuts_kernel<<<1, 32, 0, L.s>>>(d_allprop, P, n, d_cuts);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+__global__ void extract_kernel(const uint64_t* coo, const uint64_t* d_m, uint32_t* idx, double* val) {
+  const uint64_t m = *d_m;
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < m;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t x = coo[e];
+    idx[e] = coo_idx(x);
+    val[e] = double(coo_val(x));
+  }
+}
+
+cudaError_t launch_extract(Launch& L, const uint64_t* coo, const uint64_t* d_m, uint64_t bound,
+                           uint32_t* idx, double* val) {
+  const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>((bound + kThreads - 1) / kThreads,
+                                                              uint64_t(L.sms) * 8)));
+  extract_kernel<<<grid, kThreads, 0, L.s>>>(coo, d_m, idx, val);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+__global__ void widen_kernel(const float* in, uint64_t n, double* out) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += uint64_t(gridDim.x) * blockDim.x)
+    out[e] = double(in[e]);
+}
+
+cudaError_t launch_widen_f32(Launch& L, const float* in, uint64_t n, double* out) {
+  if (!n) return cudaSuccess;
+  const int grid = int(std::min<uint64_t>((n + kThreads - 1) / kThreads, uint64_t(L.sms) * 8));
+  widen_kernel<<<grid, kThreads, 0, L.s>>>(in, n, out);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+// =============================================================================
+// Generators: SplitMix64 streams of proj/core/include/oklab/rng.hpp
+// =============================================================================
+__device__ __forceinline__ uint64_t d_splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t d_mix64(uint64_t a, uint64_t b) {
+  return d_splitmix64(a ^ (0x9e3779b97f4a7c15ull + b + (a << 6) + (a >> 2)));
+}
+__device__ __forceinline__ double d_unit(uint64_t bits) {
+  return double(bits >> 11) * 0x1.0p-53;
+}
+
+// The i-th draw of SplitMix64(seed) is splitmix64(seed + i*gamma), so the
+// sequential stream parallelises exactly.
+__global__ void gen_random_dense_kernel(float* out, uint64_t n, uint64_t seed) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const double u = d_unit(d_splitmix64(seed + i * 0x9e3779b97f4a7c15ull));
+    out[i] = float(__dsub_rn(__dmul_rn(2.0, u), 1.0));
+  }
+}
+
+__global__ void gen_noise_kernel(float* out, uint64_t n, uint64_t noise_key, double coef) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const double u = d_unit(d_mix64(noise_key, i));
+    out[i] = float(__dmul_rn(coef, __dsub_rn(__dmul_rn(2.0, u), 1.0)));
+  }
+}
+
+__global__ void scatter_heavy_kernel(const uint32_t* pos, const float* val, uint64_t count, float* out) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[pos[i]] = val[i];
+}
+
+cudaError_t launch_gen_random_dense(Launch& L, float* out, uint64_t n, uint64_t seed) {
+  if (!n) return cudaSuccess;
+  const int grid = int(std::min<uint64_t>((n + kThreads - 1) / kThreads, uint64_t(L.sms) * 16));
+  gen_random_dense_kernel<<<grid, kThreads, 0, L.s>>>(out, n, seed);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_noise(Launch& L, float* out, uint64_t n, uint64_t noise_key, double coef) {
+  if (!n) return cudaSuccess;
+  const int grid = int(std::min<uint64_t>((n + kThreads - 1) / kThreads, uint64_t(L.sms) * 16));
+  gen_noise_kernel<<<grid, kThreads, 0, L.s>>>(out, n, noise_key, coef);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_heavy(Launch& L, const uint32_t* pos, const float* val, uint64_t count,
+                                 float* out) {
+  if (!count) return cudaSuccess;
+  const int grid = int(std::min<uint64_t>((count + kThreads - 1) / kThreads, uint64_t(L.sms) * 8));
+  scatter_heavy_kernel<<<grid, kThreads, 0, L.s>>>(pos, val, count, out);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+}  // namespace okt

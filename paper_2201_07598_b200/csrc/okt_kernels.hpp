@@ -1,0 +1,104 @@
+// okt_kernels.hpp — host launchers for the sm_100a Ok-Topk kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace okt {
+
+// Per-comm launch context: stream, look-back scratch, launch accounting.
+struct Launch {
+  cudaStream_t s = nullptr;
+  uint64_t* status = nullptr;   // look-back status words (one per tile)
+  uint32_t* ctr = nullptr;      // dynamic tile counter pair
+  uint32_t epoch = 0;           // bumped per look-back launch
+  uint64_t launches = 0;        // kernels launched through this context
+  int sms = 148;
+  uint32_t next_epoch() { epoch = (epoch + 1) & 0x3fffffffu; if (!epoch) epoch = 1; return epoch; }
+};
+
+struct RadixState {
+  uint64_t prefix;
+  uint64_t kk;
+  uint32_t active;
+  uint32_t pad;
+};
+
+enum class K1Mode { kSelect, kAccumSelect, kAccumHist };
+enum class RadixSrc { kDenseF32, kAosF32, kF64 };
+
+// Split-phase receive segments for the region scatter (M1): one per source.
+struct Segs {
+  const uint64_t* ptr[8];
+  uint64_t start[9];
+  int src[8];
+  int nseg;
+};
+
+// K1: fused residual accumulate + threshold select + order-preserving COO
+// compaction over n fp32 elements.  Modes:
+//   kSelect       acc = g,                       emit {|acc| >= th}
+//   kAccumSelect  acc = fma(alpha, g, eps_in) -> eps_out, emit {|acc| >= th}
+//   kAccumHist    acc = fma(alpha, g, eps_in) -> eps_out, radix pass-0 histogram
+// Sets bit 0 of *d_flags on any non-finite accumulator.
+cudaError_t launch_k1(Launch& L, K1Mode mode, const float* g, const float* eps_in,
+                      float* eps_out, float alpha, uint64_t n, const double* d_th,
+                      uint64_t* out, uint64_t* d_m, uint32_t* d_flags, uint32_t* d_hist);
+
+// K2/K4: exact k-th largest magnitude (k clamped to the element count) by MSD
+// radix select on the IEEE bit patterns; writes the threshold to *d_th_out
+// unless the input is empty.  `hist0_done`: pass 0's histogram was already
+// accumulated into d_hist (fused into K1).
+cudaError_t launch_radix_select(Launch& L, RadixSrc src, const void* data,
+                                uint64_t n_host, const uint64_t* d_n, uint64_t n_bound,
+                                uint64_t k, RadixState* d_rs, uint32_t* d_hist,
+                                double* d_th_out, bool hist0_done);
+// Zero-initialises the radix state before a fused pass-0 histogram.
+cudaError_t launch_radix_init(Launch& L, RadixState* d_rs, uint64_t k, uint64_t n_host,
+                              const uint64_t* d_n);
+
+// Survivor filter: {(i, v) : |v| >= *d_th} of a COO list whose length lives in
+// device memory.  Input is AoS (u32 idx, f32 val) or SoA (u32, f64).
+cudaError_t launch_filter(Launch& L, bool aos, const uint64_t* in_aos,
+                          const uint32_t* in_idx, const double* in_val,
+                          const uint64_t* d_cnt_in, uint64_t bound, const double* d_th,
+                          uint32_t* out_idx, double* out_val, uint64_t* d_cnt_out);
+
+// K7: for each (i, v) of u: sel = |acc[i]| >= local_th; if w: w[i] -= v / P;
+// if zero_eps && sel: acc[i] = 0; emit i into indexes when sel.
+cudaError_t launch_apply(Launch& L, const uint32_t* u_idx, const double* u_val,
+                         const uint64_t* d_U, uint64_t bound, float* acc, bool zero_eps,
+                         float* w, int P, const double* d_local_th, uint32_t* out_indexes,
+                         uint64_t* d_nidx, uint32_t* d_flags);
+
+// K3 (M1): scatter split-phase entries into the owner's presence mask and
+// coordinate-major staging [W][P]; out-of-region entries set bit 1 of flags.
+cudaError_t launch_scatter(Launch& L, const Segs& segs, uint64_t lo, uint64_t W, int P,
+                           uint32_t* mask, float* stage, uint32_t* d_flags);
+// K3 (M2): ordered scan of the owned region: bracket-sum the present sources in
+// fp64, keep explicit zeros, optionally filter by |sum| >= *d_gth, clear mask.
+cudaError_t launch_region_scan(Launch& L, int P, bool filter, uint64_t lo, uint64_t W,
+                               uint32_t* mask, const float* stage, const double* d_gth,
+                               uint32_t* out_idx, double* out_val, uint64_t* d_count);
+
+// Small control kernels.
+cudaError_t launch_slice_offsets(Launch& L, const uint64_t* coo, const uint64_t* d_m,
+                                 const uint64_t* d_cuts, int P, uint64_t* d_off,
+                                 uint32_t* d_cnt_out, const uint32_t* d_flags);
+cudaError_t launch_proposals(Launch& L, const uint32_t* idx, int stride,
+                             const uint64_t* d_m, uint64_t m_host, uint64_t n, int P,
+                             uint64_t* d_prop);
+cudaError_t launch_cuts(Launch& L, const uint64_t* d_allprop, int P, uint64_t n,
+                        uint64_t* d_cuts);
+cudaError_t launch_extract(Launch& L, const uint64_t* coo, const uint64_t* d_m,
+                           uint64_t bound, uint32_t* idx, double* val);
+cudaError_t launch_widen_f32(Launch& L, const float* in, uint64_t n, double* out);
+
+// Input generators (bit-exact with proj/core/include/oklab/rng.hpp streams).
+cudaError_t launch_gen_random_dense(Launch& L, float* out, uint64_t n, uint64_t seed);
+cudaError_t launch_gen_noise(Launch& L, float* out, uint64_t n, uint64_t noise_key,
+                             double coef);
+cudaError_t launch_scatter_heavy(Launch& L, const uint32_t* pos, const float* val,
+                                 uint64_t count, float* out);
+
+}  // namespace okt

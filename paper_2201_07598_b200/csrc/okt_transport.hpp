@@ -1,0 +1,206 @@
+// okt_transport.hpp — the communication boundary of the path.
+//
+// Replaces the reference's Transport/WorkerCtx (proj/core/include/oklab/
+// transport.hpp:91-122) with device-to-device movement:
+//   LocalTransport  P ranks as host threads of one process (the reference's
+//                   InprocTransport + run_ranks model); a rank pulls each peer's
+//                   published device buffer with a peer copy (NVLink when the
+//                   ranks sit on different GPUs, an HBM copy when they share one).
+//   NcclTransport   one process per GPU; grouped ncclSend/ncclRecv and
+//                   ncclAllGather over NVLink / NVSwitch.
+// Both expose the same two collectives the Ok-Topk phases need.
+#pragma once
+
+#include <condition_variable>
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "../../include/okt.h"
+
+namespace okt {
+
+struct Xfer {
+  int peer;
+  void* ptr;
+  size_t bytes;
+};
+
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  // Group of point-to-point transfers, matched per (src, dst) pair in posting
+  // order.  All ranks call it collectively.
+  virtual int exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs,
+                       cudaStream_t s, std::string& err) = 0;
+  // recv holds P slots of `bytes`; slot r receives rank r's send buffer.
+  virtual int allgather(const void* send, void* recv, size_t bytes, cudaStream_t s,
+                        std::string& err) = 0;
+};
+
+}  // namespace okt
+
+// Single-process world shared by P rank threads.
+struct okt_world {
+  int P = 1;
+  std::vector<int> devices;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool closed = false;
+  // Published per exchange: sends[src][dst] in posting order + readiness event.
+  std::vector<std::vector<std::vector<okt::Xfer>>> sends;
+  std::vector<cudaEvent_t> ready;
+
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (closed) return false;
+    const uint64_t g = gen;
+    if (++arrived == P) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    cv.wait(lk, [&] { return gen != g || closed; });
+    return gen != g;
+  }
+  void close() {
+    std::lock_guard<std::mutex> lk(mu);
+    closed = true;
+    cv.notify_all();
+  }
+};
+
+namespace okt {
+
+class LocalTransport final : public Transport {
+ public:
+  LocalTransport(okt_world* w, int rank, int device, cudaEvent_t ev)
+      : w_(w), rank_(rank), device_(device), ev_(ev) {}
+
+  int exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s,
+               std::string& err) override {
+    const int P = w_->P;
+    if (cudaEventRecord(ev_, s) != cudaSuccess) return fail_cuda(err, "cudaEventRecord");
+    {
+      std::lock_guard<std::mutex> lk(w_->mu);
+      auto& mine = w_->sends[rank_];
+      for (auto& v : mine) v.clear();
+      for (const Xfer& x : sends) mine[x.peer].push_back(x);
+      w_->ready[rank_] = ev_;
+    }
+    if (!w_->barrier()) {
+      err = "transport closed";
+      return OKT_ERR_TRANSPORT;
+    }
+    std::vector<size_t> next(P, 0);
+    std::vector<char> waited(P, 0);
+    for (const Xfer& r : recvs) {
+      const auto& from = w_->sends[r.peer][rank_];
+      if (next[r.peer] >= from.size() || from[next[r.peer]].bytes != r.bytes) {
+        err = "exchange: unmatched or mis-sized message from rank " + std::to_string(r.peer);
+        w_->close();
+        return OKT_ERR_PROTOCOL;
+      }
+      const Xfer& snd = from[next[r.peer]++];
+      if (!waited[r.peer]) {
+        if (cudaStreamWaitEvent(s, w_->ready[r.peer], 0) != cudaSuccess) {
+          w_->close();
+          return fail_cuda(err, "cudaStreamWaitEvent");
+        }
+        waited[r.peer] = 1;
+      }
+      if (r.bytes &&
+          cudaMemcpyPeerAsync(r.ptr, device_, snd.ptr, w_->devices[r.peer], r.bytes, s) !=
+              cudaSuccess) {
+        w_->close();
+        return fail_cuda(err, "cudaMemcpyPeerAsync");
+      }
+    }
+    for (int p = 0; p < P; ++p) {
+      if (p != rank_ && next[p] != w_->sends[p][rank_].size()) {
+        err = "exchange: rank " + std::to_string(p) + " sent messages this rank did not expect";
+        w_->close();
+        return OKT_ERR_PROTOCOL;
+      }
+    }
+    // Peers may reuse their send buffers once this rank's pulls have landed.
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+      w_->close();
+      return fail_cuda(err, "cudaStreamSynchronize");
+    }
+    if (!w_->barrier()) {
+      err = "transport closed";
+      return OKT_ERR_TRANSPORT;
+    }
+    return OKT_OK;
+  }
+
+  int allgather(const void* send, void* recv, size_t bytes, cudaStream_t s,
+                std::string& err) override {
+    char* out = static_cast<char*>(recv);
+    if (bytes && cudaMemcpyAsync(out + bytes * rank_, send, bytes, cudaMemcpyDeviceToDevice, s) !=
+                     cudaSuccess)
+      return fail_cuda(err, "cudaMemcpyAsync");
+    std::vector<Xfer> sends, recvs;
+    for (int p = 0; p < w_->P; ++p) {
+      if (p == rank_) continue;
+      sends.push_back({p, const_cast<void*>(send), bytes});
+      recvs.push_back({p, out + bytes * p, bytes});
+    }
+    return exchange(sends, recvs, s, err);
+  }
+
+ private:
+  static int fail_cuda(std::string& err, const char* what) {
+    err = std::string(what) + ": " + cudaGetErrorString(cudaGetLastError());
+    return OKT_ERR_CUDA;
+  }
+  okt_world* w_;
+  int rank_;
+  int device_;
+  cudaEvent_t ev_;
+};
+
+class NcclTransport final : public Transport {
+ public:
+  explicit NcclTransport(ncclComm_t c) : c_(c) {}
+  ~NcclTransport() override {
+    if (c_) ncclCommDestroy(c_);
+  }
+  int exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s,
+               std::string& err) override {
+    ncclResult_t r = ncclGroupStart();
+    for (const Xfer& x : sends)
+      if (r == ncclSuccess && x.bytes) r = ncclSend(x.ptr, x.bytes, ncclUint8, x.peer, c_, s);
+    for (const Xfer& x : recvs)
+      if (r == ncclSuccess && x.bytes) r = ncclRecv(x.ptr, x.bytes, ncclUint8, x.peer, c_, s);
+    const ncclResult_t r2 = ncclGroupEnd();
+    if (r == ncclSuccess) r = r2;
+    if (r != ncclSuccess) {
+      err = std::string("nccl send/recv: ") + ncclGetErrorString(r);
+      return OKT_ERR_NCCL;
+    }
+    return OKT_OK;
+  }
+  int allgather(const void* send, void* recv, size_t bytes, cudaStream_t s,
+                std::string& err) override {
+    const ncclResult_t r = ncclAllGather(send, recv, bytes, ncclUint8, c_, s);
+    if (r != ncclSuccess) {
+      err = std::string("ncclAllGather: ") + ncclGetErrorString(r);
+      return OKT_ERR_NCCL;
+    }
+    return OKT_OK;
+  }
+
+ private:
+  ncclComm_t c_;
+};
+
+}  // namespace okt
