@@ -1,0 +1,366 @@
+#!/usr/bin/env python3
+"""Ok-Topk sparse-allreduce benchmark (BASELINE.json metric) on B200.
+
+One step = one Ok-Topk error-feedback SGD iteration through the C-ABI
+(okt_sgd_step: acc = eps + alpha*g fused with threshold selection, split and
+reduce, global threshold, balance + allgatherv, residual / model scatter) on a
+VGG-16-sized fp32 gradient (n = 14,728,266, density 1%, BASELINE.json
+configs[1]), tau = 64, tau' = 32, bucket 4 — refresh iterations included in
+the timed window in their natural 1-in-32 proportion.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl okt|reference]
+
+N > 1 runs under torchrun, one process per GPU; the data path is the library's
+own NCCL communicator (NVLink), torch.distributed (gloo) is only plumbing for
+the id broadcast, barriers and the max-over-ranks reduction.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+VGG_N = 14_728_266
+
+
+def k_for(n: int, density: float) -> int:
+    """ExperimentConfig::k (harness.cpp:82-86)."""
+    raw = density * float(n) * (1.0 - 1e-12)
+    return max(1, min(n, int(math.ceil(raw))))
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="okt", choices=["okt", "reference"])
+    ap.add_argument("--n", type=int, default=VGG_N)
+    ap.add_argument("--density", type=float, default=0.01)
+    ap.add_argument("--tau", type=int, default=64)
+    ap.add_argument("--tau-prime", type=int, default=32)
+    ap.add_argument("--bucket", type=int, default=4)
+    ap.add_argument("--ring", type=int, default=8, help="distinct gradient snapshots cycled per rank")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=32)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(args, P):
+    return {"workload": "vgg16-sized fp32 gradient, Ok-Topk EF-SGD step" if args.n == VGG_N
+            else f"n={args.n} fp32 gradient, Ok-Topk EF-SGD step",
+            "n": args.n, "density": args.density, "k": k_for(args.n, args.density), "P": P,
+            "tau": args.tau, "tau_prime": args.tau_prime, "bucket": args.bucket,
+            "inputs": f"drifting_gradient_process(t, seed=1, rank_key=r+1), ring of {args.ring} snapshots",
+            "parallelism": f"dp{P} (one process per GPU, NCCL/NVLink)" if P > 1 else "single GPU",
+            "l2": "flushed (256 MiB write) before every timed step"}
+
+
+# ---- clocks ----------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- reference arm -------------------------------------------------------------------
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0  # rank 0 alone times the reference's CPU path with P = N threads
+    P = max(args.gpus, world)
+    k = k_for(args.n, args.density)
+    line = {"metric": "Ok-Topk sparse allreduce ms/iter", "unit": "ms/iter", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload(args, P)}
+    try:
+        from oracle import Reference
+        ref = Reference()
+    except Exception as e:  # the reference .so is built in the dev container and travels
+        line["unavailable"] = f"oracle/_ref/libokref.so not loadable: {e}"
+        print(json.dumps(line))
+        return 0
+    steps = args.steps
+    t0 = time.time()
+    ms = ref.bench_sgd(P, args.n, k, args.warmup, steps, args.tau, args.tau_prime, args.bucket, 1.0, 1, True)
+    wall = time.time() - t0
+    v = float(ms.mean())
+    line.update({"value": v, "ms_per_step": v,
+                 "cpu_baseline": {"value": v, "unit": "ms/iter", "cores": P, "kind": "reference",
+                                  "sample": f"{steps} timed iterations after {args.warmup} warm-up, "
+                                            f"P={P} rank threads (InprocTransport), one core each",
+                                  "cpu": _cpu_model(), "nproc": os.cpu_count(), "wall_s": round(wall, 1)},
+                 "e2e": {"value": v, "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                 "ms_min": float(ms.min()), "ms_max": float(ms.max())})
+    print(json.dumps(line))
+    return 0
+
+
+def _cpu_model() -> str:
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---- our arm ------------------------------------------------------------------------
+def run_okt(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2201_07598_b200 import lib
+    from paper_2201_07598_b200._lib import OktResult
+
+    rank, world, local = dist_env()
+    P = world
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    L = lib()
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    # ---- comm: NCCL over NVLink for P > 1, a local single-rank world for P = 1
+    comm = ctypes.c_void_p()
+    if P > 1:
+        uid = (ctypes.c_char * 128)()
+        if rank == 0:
+            assert L.okt_nccl_unique_id(uid, 128) == 0
+        obj = [bytes(uid)] if rank == 0 else [None]
+        dist.broadcast_object_list(obj, src=0)
+        ctypes.memmove(uid, obj[0], 128)
+        rc = L.okt_comm_init_nccl(ctypes.byref(comm), rank, P, local, uid, 128)
+    else:
+        w = ctypes.c_void_p()
+        dev = (ctypes.c_int * 1)(local)
+        rc = L.okt_world_create_local(ctypes.byref(w), 1, dev)
+        rc = rc or L.okt_comm_init_local(ctypes.byref(comm), w, 0)
+    if rc:
+        raise SystemExit(f"comm init failed: {L.okt_last_error().decode()}")
+    n, k = args.n, k_for(args.n, args.density)
+    assert L.okt_set_params(comm, args.tau, args.tau_prime, args.bucket) == 0
+    assert L.okt_comm_reserve(comm, n) == 0
+    stream = torch.cuda.Stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    # ---- inputs: a ring of drift snapshots per rank, generated on the device
+    ring = [torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(args.ring)]
+    for i, buf in enumerate(ring):
+        assert L.okt_gen_drift(ctypes.c_void_p(buf.data_ptr()), n, i + 1, 1, rank + 1, 0, sp) == 0
+    wmodel = torch.zeros(n, dtype=torch.float32, device="cuda")
+    assert L.okt_residual_reset(comm, n, None, sp) == 0
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    res = OktResult()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def step(t):
+        g = ring[(t - 1) % args.ring]
+        rc = L.okt_sgd_step(comm, ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(wmodel.data_ptr()), n, 1.0, t, k,
+                            ctypes.byref(res), sp)
+        if rc:
+            raise SystemExit(f"okt_sgd_step failed: {L.okt_last_error().decode()}")
+
+    # ---- warm-up
+    t = 0
+    for _ in range(args.warmup):
+        t += 1
+        step(t)
+    barrier()
+    # ---- timed device-resident run
+    L.okt_set_profiling(comm, 1)
+    L.okt_reset_phase_times(comm)
+    launches0 = ctypes.c_uint64()
+    L.okt_kernel_launches(comm, ctypes.byref(launches0))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = Clocks(local)
+    clocks.start()
+    barrier()
+    U_sum, m_sum = 0, 0
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        t += 1
+        with torch.cuda.stream(stream):
+            flush.fill_(i & 0xff)  # evict L2 between timed steps (outside the events)
+            ev[i][0].record(stream)
+        step(t)
+        with torch.cuda.stream(stream):
+            ev[i][1].record(stream)
+        U_sum += res.u.nnz
+        m_sum += res.local_selected
+    barrier()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    launches1 = ctypes.c_uint64()
+    L.okt_kernel_launches(comm, ctypes.byref(launches1))
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    ms_t = (ctypes.c_double * 8)()
+    calls = (ctypes.c_uint64 * 8)()
+    byts = (ctypes.c_double * 8)()
+    L.okt_phase_times(comm, ms_t, calls)
+    L.okt_phase_bytes(comm, byts)
+    L.okt_set_profiling(comm, 0)
+    phases = {nm: round(ms_t[i] / max(1, args.steps), 4) for i, nm in
+              enumerate(("select", "threshold", "split", "merge", "global", "allgather", "apply", "step"))}
+    # ---- end-to-end through the host-buffer C-ABI call (H2D gradient, D2H u)
+    hbuf = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(min(args.ring, 4))]
+    for i, hb in enumerate(hbuf):
+        hb.copy_(ring[i].cpu())
+    cap = n
+    h_uidx = torch.empty(cap, dtype=torch.int32).pin_memory()
+    h_uval = torch.empty(cap, dtype=torch.float64).pin_memory()
+    e2e_steps = max(4, min(args.steps, 32))
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e2e_steps)]
+    barrier()
+    d2h = 0
+    for i in range(e2e_steps):
+        t += 1
+        with torch.cuda.stream(stream):
+            flush.fill_(i & 0xff)
+            e2e_ev[i][0].record(stream)
+        rc = L.okt_sgd_step_host(comm, ctypes.c_void_p(hbuf[i % len(hbuf)].data_ptr()),
+                                 ctypes.c_void_p(wmodel.data_ptr()), n, 1.0, t, k,
+                                 ctypes.c_void_p(h_uidx.data_ptr()), ctypes.c_void_p(h_uval.data_ptr()), cap,
+                                 ctypes.byref(res), sp)
+        if rc:
+            raise SystemExit(f"okt_sgd_step_host failed: {L.okt_last_error().decode()}")
+        with torch.cuda.stream(stream):
+            e2e_ev[i][1].record(stream)
+        d2h += 12 * res.u.nnz
+    barrier()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev) / e2e_steps
+    # ---- max over ranks
+    mine = torch.tensor([total_ms, e2e_ms, wall], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(mine, op=dist.ReduceOp.MAX)
+    total_ms, e2e_ms, wall = mine.tolist()
+    ms_per_step = total_ms / args.steps
+    sel_ms = ms_t[0]
+    sel_bytes = byts[0]
+    achieved = sel_bytes / (sel_ms * 1e-3) / 1e9 if sel_ms > 0 else None
+    peak = None
+    try:
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        peak_src = "measured"
+    except Exception:
+        peak, peak_src = 6650.0, "fallback"
+    line = None
+    if rank == 0:
+        traffic = None
+        try:
+            prof = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))
+            traffic = prof.get("bytes_per_launch")
+        except Exception:
+            pass
+        line = {"metric": "Ok-Topk sparse allreduce ms/iter", "value": ms_per_step, "unit": "ms/iter",
+                "n_gpus": P, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": workload(args, P),
+                "e2e": {"value": e2e_ms, "unit": "ms/iter", "h2d_bytes_per_step": 4 * n,
+                        "d2h_bytes_per_step": int(d2h / e2e_steps)},
+                "gpu_launches": int(launches1.value - launches0.value),
+                "roofline": {"bound": "hbm", "kernel": "k1 fused accumulate+select+compact",
+                             "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                             "peak_source": peak_src,
+                             "bytes_per_step": sel_bytes / args.steps,
+                             "ms_per_step": sel_ms / args.steps},
+                "phases_ms_per_step": phases,
+                "avg_U": U_sum / args.steps, "avg_local_selected": m_sum / args.steps,
+                "wall_ms_per_step": 1e3 * wall / args.steps,
+                "clocks": clk}
+    # ---- CPU baseline (rank 0, N = 1 only): the reference itself, bounded sample
+    if rank == 0 and P == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import Reference
+            ref = Reference()
+            t0 = time.time()
+            ms = ref.bench_sgd(1, n, k, 1, args.cpu_iters, args.tau, args.tau_prime, args.bucket, 1.0, 1, True)
+            line["cpu_baseline"] = {"value": float(ms.mean()), "unit": "ms/iter", "cores": 1, "kind": "reference",
+                                    "sample": f"{args.cpu_iters} iterations t=2..{args.cpu_iters + 1} "
+                                              f"(one tau' refresh) of the reference's EF-SGD step, same n/k/tau",
+                                    "cpu": _cpu_model(), "wall_s": round(time.time() - t0, 1)}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    L.okt_comm_destroy(comm)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_okt(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

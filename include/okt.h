@@ -232,6 +232,8 @@ enum okt_timer {
 int okt_set_profiling(okt_comm* comm, int on);
 int okt_phase_times(okt_comm* comm, double* ms_out /* OKT_T_COUNT */,
                     uint64_t* calls_out /* OKT_T_COUNT, nullable */);
+/* Algorithmic HBM bytes the timed phases were charged. */
+int okt_phase_bytes(okt_comm* comm, double* bytes_out /* OKT_T_COUNT */);
 int okt_reset_phase_times(okt_comm* comm);
 /* Number of kernels this comm has launched since creation. */
 int okt_kernel_launches(const okt_comm* comm, uint64_t* out);

@@ -32,7 +32,7 @@ EXPORTS = (
     "okt_th_re_evaluate_dense", "okt_th_re_evaluate_sparse",
     "okt_select_by_threshold", "okt_space_repartition",
     "okt_split_and_reduce", "okt_balance_and_allgatherv",
-    "okt_set_profiling", "okt_phase_times", "okt_reset_phase_times",
+    "okt_set_profiling", "okt_phase_times", "okt_phase_bytes", "okt_reset_phase_times",
     "okt_kernel_launches", "okt_gen_random_dense", "okt_gen_drift",
 )
 
@@ -127,6 +127,7 @@ def lib() -> ctypes.CDLL:
                                                c_double, P(OktSparse), c_void_p]),
         "okt_set_profiling": (c_int, [c_void_p, c_int]),
         "okt_phase_times": (c_int, [c_void_p, P(c_double), P(c_uint64)]),
+        "okt_phase_bytes": (c_int, [c_void_p, P(c_double)]),
         "okt_reset_phase_times": (c_int, [c_void_p]),
         "okt_kernel_launches": (c_int, [c_void_p, P(c_uint64)]),
         "okt_gen_random_dense": (c_int, [c_void_p, c_size_t, c_uint64, c_void_p]),

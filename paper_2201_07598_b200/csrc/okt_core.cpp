@@ -177,6 +177,7 @@ struct okt_comm {
   cudaEvent_t open_ev = nullptr;
   double t_ms[OKT_T_COUNT] = {};
   uint64_t t_calls[OKT_T_COUNT] = {};
+  double t_bytes[OKT_T_COUNT] = {};  // algorithmic HBM bytes per phase
 
   DevScalars* d() const { return scal.as<DevScalars>(); }
   cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : own; }
@@ -711,6 +712,18 @@ struct okt_comm {
     }
     if ((rc = sync(s))) return abort_step(rc);
     tcollect();
+    if (prof) {
+      // Algorithmic bytes: K1 reads g (+ eps) and writes eps and
+      // the m COO entries; refresh iterations add the radix passes over acc.
+      const double nn = double(n), mm = double(h->m);
+      const double uu = double(P == 1 ? h->S : h->U);
+      double sel = (sgd ? 12.0 * nn : 4.0 * nn) + 8.0 * mm;
+      if (thr && sgd) sel += 4.0 * nn;  // the select-only K1 after the fused accumulate+histogram
+      t_bytes[OKT_T_SELECT] += sel;
+      if (thr) t_bytes[OKT_T_THRESHOLD] += (sgd ? 2.0 : 3.0) * 4.0 * nn;
+      // K7: read u (12 B), gather acc (4 B), w read+write (8 B), eps zero (4 B).
+      t_bytes[OKT_T_APPLY] += uu * (sgd ? 28.0 : 16.0);
+    }
 
     if (h->flags & 1u) {
       dev_stale = true;
@@ -1258,8 +1271,16 @@ int okt_phase_times(okt_comm* c, double* ms, uint64_t* calls) {
   return OKT_OK;
 }
 
+int okt_phase_bytes(okt_comm* c, double* bytes) {
+  OKT_COMM_CHECK(c);
+  for (int i = 0; i < OKT_T_COUNT; ++i)
+    if (bytes) bytes[i] = c->t_bytes[i];
+  return OKT_OK;
+}
+
 int okt_reset_phase_times(okt_comm* c) {
   OKT_COMM_CHECK(c);
+  std::memset(c->t_bytes, 0, sizeof(c->t_bytes));
   std::memset(c->t_ms, 0, sizeof(c->t_ms));
   std::memset(c->t_calls, 0, sizeof(c->t_calls));
   return OKT_OK;
