@@ -22,9 +22,7 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -42,7 +40,7 @@ def k_for(n: int, density: float) -> int:
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--steps", type=int, default=128)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="okt", choices=["okt", "reference"])
     ap.add_argument("--n", type=int, default=VGG_N)
@@ -75,49 +73,50 @@ def workload(args, P):
 
 # ---- clocks ----------------------------------------------------------------------
 class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clock and throttle reasons through NVML on a background
+    thread while the measured region runs (nvidia-smi's 200 ms polling is too
+    coarse for a region this short)."""
+
+    HW = 0x0000000000000008          # hw_slowdown
+    HW_THERMAL = 0x0000000000000040
+    SW_THERMAL = 0x0000000000000020
+    SW_POWER = 0x0000000000000004
 
     def __init__(self, gpu: int):
+        import threading
         self.gpu = gpu
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
+        self.samples, self.reasons, self.mx = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for bit, nm in ((self.HW, "hw_slowdown"), (self.HW_THERMAL, "hw_thermal_slowdown"),
+                                (self.SW_THERMAL, "sw_thermal_slowdown"), (self.SW_POWER, "sw_power_cap")):
+                    if r & bit:
+                        self.reasons.add(nm)
+                self._stop.wait(0.002)
+        except Exception as e:  # pragma: no cover - reported in the JSON
+            self.reasons.add(f"nvml unavailable: {e}")
 
     def start(self):
-        try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.p = None
+        import threading
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
 
     def stop(self):
-        if not self.p:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.flush()
-        self.f.seek(0)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=5)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
 # ---- reference arm -------------------------------------------------------------------
@@ -253,7 +252,6 @@ def run_okt(args):
         m_sum += res.local_selected
     barrier()
     wall = time.perf_counter() - wall0
-    clk = clocks.stop()
     launches1 = ctypes.c_uint64()
     L.okt_kernel_launches(comm, ctypes.byref(launches1))
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -292,6 +290,7 @@ def run_okt(args):
             e2e_ev[i][1].record(stream)
         d2h += 12 * res.u.nnz
     barrier()
+    clk = clocks.stop()
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev) / e2e_steps
     # ---- max over ranks
     mine = torch.tensor([total_ms, e2e_ms, wall], dtype=torch.float64)

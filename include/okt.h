@@ -215,6 +215,33 @@ int okt_balance_and_allgatherv(okt_comm* comm, const uint32_t* d_idx,
                                const double* d_val, size_t nnz, size_t n,
                                double global_th, okt_sparse* u, void* stream);
 
+/* ---- host planning (pure functions, no GPU) ------------------------------
+ * The exchange plans every rank derives from the sizes it already agreed on;
+ * the device orchestration uses the same code.  Exported so the multi-rank
+ * planning can be exercised on CPU ranks. */
+typedef struct okt_piece {
+  int32_t peer;
+  uint64_t begin; /* range of the rank-concatenated survivor stream */
+  uint64_t end;
+} okt_piece;
+enum okt_plan_kind {
+  OKT_PLAN_SPLIT = 0,         /* sizes: P x P send counts, row = sender */
+  OKT_PLAN_ALLGATHERV = 1,    /* sizes: P part sizes */
+  OKT_PLAN_AVG = 2,           /* small_allreduce_avg of `len` reals */
+  OKT_PLAN_ALLGATHER_U32 = 3, /* small_allgather_u32 of one word */
+  OKT_PLAN_BALANCE = 4        /* sizes: P survivor counts */
+};
+/* space_repartition consensus (oktopk.cpp:51-61): proposals is P x (P+1). */
+int okt_plan_cuts(const uint64_t* proposals, int P, uint64_t n, uint64_t* cuts);
+/* balance_and_allgatherv's plan (oktopk.cpp:172-231); arrays hold <= P. */
+int okt_plan_balance(int rank, int P, const uint64_t* sizes, int* balanced,
+                     okt_piece* sends, int* nsends, okt_piece* recvs,
+                     int* nrecvs, okt_piece* own, uint64_t* part_off,
+                     uint64_t* part_sz);
+/* Ledger words / messages the reference's transport credits for one phase. */
+int okt_plan_ledger(int rank, int P, int kind, const uint64_t* sizes,
+                    uint64_t len, uint32_t bucket, okt_counters* out);
+
 /* ---- instrumentation ------------------------------------------------------ */
 enum okt_timer {
   OKT_T_SELECT = 0,   /* K1 fused accumulate/select/compact */

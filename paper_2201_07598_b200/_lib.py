@@ -34,6 +34,7 @@ EXPORTS = (
     "okt_split_and_reduce", "okt_balance_and_allgatherv",
     "okt_set_profiling", "okt_phase_times", "okt_phase_bytes", "okt_reset_phase_times",
     "okt_kernel_launches", "okt_gen_random_dense", "okt_gen_drift",
+    "okt_plan_cuts", "okt_plan_balance", "okt_plan_ledger",
 )
 
 
@@ -60,6 +61,10 @@ class OktCounters(Structure):
 class OktSparse(Structure):
     _fields_ = [("d_idx", c_void_p), ("d_val", c_void_p), ("nnz", c_uint64),
                 ("n", c_uint64)]
+
+
+class OktPiece(Structure):
+    _fields_ = [("peer", c_int32), ("begin", c_uint64), ("end", c_uint64)]
 
 
 class OktResult(Structure):
@@ -133,6 +138,11 @@ def lib() -> ctypes.CDLL:
         "okt_gen_random_dense": (c_int, [c_void_p, c_size_t, c_uint64, c_void_p]),
         "okt_gen_drift": (c_int, [c_void_p, c_size_t, c_int64, c_uint64, c_uint64, c_int,
                                   c_void_p]),
+        "okt_plan_cuts": (c_int, [P(c_uint64), c_int, c_uint64, P(c_uint64)]),
+        "okt_plan_balance": (c_int, [c_int, c_int, P(c_uint64), P(c_int), P(OktPiece), P(c_int),
+                                     P(OktPiece), P(c_int), P(OktPiece), P(c_uint64), P(c_uint64)]),
+        "okt_plan_ledger": (c_int, [c_int, c_int, c_int, P(c_uint64), c_uint64, c_uint32,
+                                    P(OktCounters)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -142,5 +152,5 @@ def lib() -> ctypes.CDLL:
     return L
 
 
-__all__ = ["lib", "LIB_PATH", "EXPORTS", "OktState", "OktCounters", "OktSparse",
+__all__ = ["lib", "LIB_PATH", "EXPORTS", "OktState", "OktCounters", "OktSparse", "OktPiece",
            "OktResult", "OKT_MAX_WORLD", "OKT_T_COUNT", "TIMER_NAMES", "c_float"]

@@ -30,6 +30,7 @@
 
 #include "../../include/okt.h"
 #include "okt_kernels.hpp"
+#include "okt_plan.hpp"
 #include "okt_transport.hpp"
 
 using okt::Launch;
@@ -97,25 +98,7 @@ struct DevScalars {
 };
 
 bool is_pow2(int v) { return v >= 1 && (v & (v - 1)) == 0; }
-int log2i(int p) {
-  int l = 0;
-  while ((1 << l) < p) ++l;
-  return l;
-}
-
-// equal_slice_ends (collectives.cpp:79-87): ceil-sized blocks first.
-std::vector<uint64_t> equal_slice_ends(uint64_t n, int P) {
-  std::vector<uint64_t> e(P + 1, 0);
-  const uint64_t base = n / uint64_t(P), rem = n % uint64_t(P);
-  for (int r = 0; r < P; ++r) e[r + 1] = e[r] + base + (uint64_t(r) < rem ? 1 : 0);
-  return e;
-}
-
-// bucket_count (oktopk.cpp:88-91): at least one message per destination.
-uint64_t bucket_count(uint64_t nnz, uint32_t bucket) {
-  if (bucket == 0 || nnz <= bucket) return 1;
-  return (nnz + bucket - 1) / bucket;
-}
+using okt::plan::equal_slice_ends;
 
 okt_state default_state() {
   okt_state s;
@@ -160,7 +143,10 @@ struct okt_comm {
   Buf indexes;
   Buf eps[2];
   Buf hgrad;               // staging for the host-buffer entry points
-  Buf status, ctr, hist, scal;
+  Buf st64, stidx, stval;  // phase-A compaction staging
+  Buf counts, counts2, chunkcap;
+  Buf hist, scal;
+  okt::Stage S;
   DevScalars* h = nullptr;   // pinned download mirror
   DevScalars* hup = nullptr; // pinned upload staging
   size_t cap_n = 0;
@@ -195,36 +181,19 @@ struct okt_comm {
   }
   // small_allreduce_avg of P+1 reals (transport.cpp:103-128): log2 P rounds.
   void credit_avg(uint64_t len, uint64_t bytes_moved) {
-    const int rounds = log2i(P);
-    credit_send(OKT_PHASE_CONSENSUS, len * rounds, rounds, bytes_moved * (P - 1));
-    credit_recv(OKT_PHASE_CONSENSUS, len * rounds, rounds, bytes_moved * (P - 1));
+    okt::plan::ledger_avg(ledger[OKT_PHASE_CONSENSUS], P, len);
+    ledger[OKT_PHASE_CONSENSUS].bytes_sent += bytes_moved * (P - 1);
+    ledger[OKT_PHASE_CONSENSUS].bytes_recv += bytes_moved * (P - 1);
   }
   // small_allgather_u32 of one word (transport.cpp:130-160).
   void credit_allgather_u32() {
-    const int rounds = log2i(P);
-    for (int j = 0; j < rounds; ++j) {
-      credit_send(OKT_PHASE_CONSENSUS, uint64_t(1) << j, 1, 0);
-      credit_recv(OKT_PHASE_CONSENSUS, uint64_t(1) << j, 1, 0);
-    }
+    okt::plan::ledger_allgather_u32(ledger[OKT_PHASE_CONSENSUS], P);
     ledger[OKT_PHASE_CONSENSUS].bytes_sent += 4ull * (P - 1);
     ledger[OKT_PHASE_CONSENSUS].bytes_recv += 4ull * (P - 1);
   }
-  // sparse_allgatherv (collectives.cpp:30-77): recursive doubling; round j
-  // moves the parts of a 2^j-wide block, 2 words per entry.
+  // sparse_allgatherv (collectives.cpp:30-77) over part sizes.
   void credit_allgatherv(int ph, const std::vector<uint64_t>& parts, uint64_t bytes_per_entry) {
-    const int rounds = log2i(P);
-    for (int j = 0; j < rounds; ++j) {
-      const int width = 1 << j;
-      const int partner = rank ^ width;
-      const int mb = rank & ~(width - 1), pb = partner & ~(width - 1);
-      uint64_t ms = 0, ps = 0;
-      for (int q = 0; q < width; ++q) {
-        ms += parts[mb + q];
-        ps += parts[pb + q];
-      }
-      credit_send(ph, 2 * ms, 1, 0);
-      credit_recv(ph, 2 * ps, 1, 0);
-    }
+    okt::plan::ledger_allgatherv(ledger[ph], rank, P, parts.data());
     uint64_t others = 0;
     for (int q = 0; q < P; ++q)
       if (q != rank) others += parts[q];
@@ -275,17 +244,22 @@ struct okt_comm {
   // ---- capacity -----------------------------------------------------------------
   int reserve(size_t n) {
     if (n <= cap_n) return OKT_OK;
-    const size_t tiles = n / 4096 + 8;
     cudaError_t e = cudaSuccess;
+    const size_t k1_stage = okt::stage_entries(n, okt::kK1Tile, S.max_chunks);
+    const size_t coo_stage = std::max(okt::stage_entries(n, okt::kCooTile, S.max_chunks), k1_stage);
     if (e == cudaSuccess) e = coo.ensure(8 * n);
-    if (e == cudaSuccess) e = status.ensure(8 * tiles);
+    if (e == cudaSuccess) e = st64.ensure(8 * k1_stage);
+    if (e == cudaSuccess) e = stidx.ensure(4 * coo_stage);
+    if (e == cudaSuccess) e = stval.ensure(8 * coo_stage);
     if (e == cudaSuccess && P == 1) {
       // P = 1 runs without host syncs: survivors/indexes sized for the worst case.
       e = sur_idx.ensure(4 * n);
       if (e == cudaSuccess) e = sur_val.ensure(8 * n);
       if (e == cudaSuccess) e = indexes.ensure(4 * n);
     }
-    L.status = status.as<uint64_t>();
+    S.s64 = st64.as<uint64_t>();
+    S.sidx = stidx.as<uint32_t>();
+    S.sval = stval.as<double>();
     if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("reserve: ") + cudaGetErrorString(e));
     cap_n = n;
     return OKT_OK;
@@ -389,10 +363,16 @@ struct okt_comm {
     }
     // Ledger: rotated schedule dst = (r+s)%P, src = (r-s+P)%P (oktopk.cpp:113-157).
     uint64_t in_total = 0;
-    for (int step = 1; step < P; ++step) {
-      const int dst = (rank + step) % P, src = (rank - step + P) % P;
-      credit_send(OKT_PHASE_SPLIT, 2 * scnt[dst], bucket_count(scnt[dst], bucket), 8 * scnt[dst]);
-      credit_recv(OKT_PHASE_SPLIT, 2 * rcnt[src], bucket_count(rcnt[src], bucket), 8 * rcnt[src]);
+    {
+      std::vector<uint64_t> counts(size_t(P) * P);
+      for (int q = 0; q < P; ++q)
+        for (int d2 = 0; d2 < P; ++d2) counts[size_t(q) * P + d2] = h->cnt_all[q * (P + 1) + d2];
+      okt::plan::ledger_split(ledger[OKT_PHASE_SPLIT], rank, P, counts.data(), bucket);
+      for (int q = 0; q < P; ++q)
+        if (q != rank) {
+          ledger[OKT_PHASE_SPLIT].bytes_sent += 8 * scnt[q];
+          ledger[OKT_PHASE_SPLIT].bytes_recv += 8 * rcnt[q];
+        }
     }
     for (int q = 0; q < P; ++q) {
       roff[q + 1] = roff[q] + (q == rank ? 0 : rcnt[q]);
@@ -430,7 +410,7 @@ struct okt_comm {
     rc = ck(okt::launch_scatter(L, segs, lo, W, P, mask.as<uint32_t>(), stage.as<float>(), &d()->flags),
             "scatter");
     if (rc) return rc;
-    rc = ck(okt::launch_region_scan(L, P, filter, lo, W, mask.as<uint32_t>(), stage.as<float>(), d_gth,
+    rc = ck(okt::launch_region_scan(L, S, P, filter, lo, W, mask.as<uint32_t>(), stage.as<float>(), d_gth,
                                     out_idx.as<uint32_t>(), out_val.as<double>(), d_out_cnt),
             "region_scan");
     bound_out = bound;
@@ -491,14 +471,10 @@ struct okt_comm {
     if (rc) return comm_err(rc, err);
     if ((rc = sync(s))) return rc;
     credit_allgather_u32();
-    std::vector<uint64_t> sizes(P), off(P + 1, 0);
-    uint64_t total = 0, maxs = 0;
-    for (int q = 0; q < P; ++q) {
-      sizes[q] = h->small_all[q];
-      off[q + 1] = off[q] + sizes[q];
-      total += sizes[q];
-      maxs = std::max(maxs, sizes[q]);
-    }
+    std::vector<uint64_t> sizes(P);
+    for (int q = 0; q < P; ++q) sizes[q] = h->small_all[q];
+    const okt::plan::Balance B = okt::plan::balance(rank, P, sizes);
+    const uint64_t total = B.total;
     U = total;
     if ((rc = ensure(u_idx, 4 * std::max<uint64_t>(total, 1)))) return rc;
     if ((rc = ensure(u_val, 8 * std::max<uint64_t>(total, 1)))) return rc;
@@ -506,52 +482,33 @@ struct okt_comm {
     double* uv = u_val.as<double>();
     const uint32_t* si = sur_idx.as<uint32_t>();
     const double* sv = sur_val.as<double>();
-    std::vector<uint64_t> part_off = off, part_sz = sizes;
-    const bool balance = total > 0 && maxs * uint64_t(P) >= 4 * total;
-    if (balance) {
-      // Re-cut the rank-concatenated survivor stream into P equal blocks and
-      // move every overlap to its block owner.  Pieces land directly at their
-      // final position in u (the stream order is the result order).
-      const std::vector<uint64_t> block = equal_slice_ends(total, P);
-      auto overlap = [&](int src, int dst, uint64_t& a, uint64_t& b) {
-        a = std::max(off[src], block[dst]);
-        b = std::min(off[src + 1], block[dst + 1]);
-        return a < b;
-      };
-      std::vector<Xfer> sends, recvs;
-      uint64_t a, b;
-      for (int dst = 0; dst < P; ++dst) {
-        if (dst == rank || !overlap(rank, dst, a, b)) continue;
-        sends.push_back({dst, const_cast<uint32_t*>(si) + (a - off[rank]), 4 * (b - a)});
-        sends.push_back({dst, const_cast<double*>(sv) + (a - off[rank]), 8 * (b - a)});
-        credit_send(OKT_PHASE_BALANCE, 2 * (b - a), 1, 12 * (b - a));
-      }
-      for (int src = 0; src < P; ++src) {
-        if (!overlap(src, rank, a, b)) continue;
-        if (src == rank) {
-          rc = ck(cudaMemcpyAsync(ui + a, si + (a - off[rank]), 4 * (b - a), cudaMemcpyDeviceToDevice, s),
-                  "copy");
-          if (!rc)
-            rc = ck(cudaMemcpyAsync(uv + a, sv + (a - off[rank]), 8 * (b - a), cudaMemcpyDeviceToDevice, s),
-                    "copy");
-          if (rc) return rc;
-        } else {
-          recvs.push_back({src, ui + a, 4 * (b - a)});
-          recvs.push_back({src, uv + a, 8 * (b - a)});
-          credit_recv(OKT_PHASE_BALANCE, 2 * (b - a), 1, 12 * (b - a));
-        }
-      }
-      rc = tr->exchange(sends, recvs, s, err);
-      if (rc) return comm_err(rc, err);
-      for (int q = 0; q < P; ++q) {
-        part_off[q] = block[q];
-        part_sz[q] = block[q + 1] - block[q];
-      }
-    } else if (sizes[rank]) {
-      rc = ck(cudaMemcpyAsync(ui + off[rank], si, 4 * sizes[rank], cudaMemcpyDeviceToDevice, s), "copy");
-      if (!rc) rc = ck(cudaMemcpyAsync(uv + off[rank], sv, 8 * sizes[rank], cudaMemcpyDeviceToDevice, s), "copy");
+    const uint64_t mine = B.off[rank];
+    // My own survivors (or the part of my block I hold) land straight at their
+    // final position in u: the stream order is the result order.
+    if (B.own.b > B.own.a) {
+      const uint64_t a = B.own.a, b = B.own.b;
+      rc = ck(cudaMemcpyAsync(ui + a, si + (a - mine), 4 * (b - a), cudaMemcpyDeviceToDevice, s), "copy");
+      if (!rc) rc = ck(cudaMemcpyAsync(uv + a, sv + (a - mine), 8 * (b - a), cudaMemcpyDeviceToDevice, s), "copy");
       if (rc) return rc;
     }
+    if (B.on) {
+      std::vector<Xfer> sends, recvs;
+      for (const okt::plan::Piece& p : B.sends) {
+        sends.push_back({p.peer, const_cast<uint32_t*>(si) + (p.a - mine), 4 * (p.b - p.a)});
+        sends.push_back({p.peer, const_cast<double*>(sv) + (p.a - mine), 8 * (p.b - p.a)});
+        ledger[OKT_PHASE_BALANCE].bytes_sent += 12 * (p.b - p.a);
+      }
+      for (const okt::plan::Piece& p : B.recvs) {
+        recvs.push_back({p.peer, ui + p.a, 4 * (p.b - p.a)});
+        recvs.push_back({p.peer, uv + p.a, 8 * (p.b - p.a)});
+        ledger[OKT_PHASE_BALANCE].bytes_recv += 12 * (p.b - p.a);
+      }
+      okt::plan::ledger_balance(ledger[OKT_PHASE_BALANCE], B);
+      rc = tr->exchange(sends, recvs, s, err);
+      if (rc) return comm_err(rc, err);
+    }
+    const std::vector<uint64_t>& part_off = B.part_off;
+    const std::vector<uint64_t>& part_sz = B.part_sz;
     // allgatherv: every rank's part to every peer, straight into u.
     std::vector<Xfer> sends, recvs;
     for (int q = 0; q < P; ++q) {
@@ -606,14 +563,18 @@ struct okt_comm {
     }
     uint32_t* hp = hist.as<uint32_t>();
     const float fa = float(alpha);
+    // P = 1: u is a subset of the local selection, so K7 (w -= u, eps = 0 at u)
+    // is fused into the compaction that writes u, and indexes = u.indices.
+    okt::ApplyArgs ap1;
+    if (sgd && P == 1) ap1 = okt::ApplyArgs{eps_out, w, &d()->flags};
 
     // ---- K1 / K2 ----
     if (thr) {
       if (sgd) {
         tmark(OKT_T_SELECT, s);
         rc = ck(okt::launch_radix_init(L, &d()->rs, k, n, nullptr), "radix_init");
-        if (!rc) rc = ck(okt::launch_k1(L, okt::K1Mode::kAccumHist, g, eps_in, eps_out, fa, n, nullptr, nullptr,
-                                        nullptr, &d()->flags, hp), "k1");
+        if (!rc) rc = ck(okt::launch_k1(L, S, okt::K1Mode::kAccumHist, g, eps_in, eps_out, fa, n, nullptr, nullptr,
+                                        okt::OutCoo{}, nullptr, nullptr, &d()->flags, hp), "k1");
         tmark(OKT_T_THRESHOLD, s);
         if (!rc) rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kDenseF32, acc, n, nullptr, n, k, &d()->rs,
                                                   hp, &d()->local_th, true), "radix");
@@ -623,12 +584,23 @@ struct okt_comm {
                                          &d()->local_th, false), "radix");
       }
       tmark(OKT_T_SELECT, s);
-      if (!rc) rc = ck(okt::launch_k1(L, okt::K1Mode::kSelect, acc, nullptr, nullptr, 0.f, n, &d()->local_th,
-                                      coo.as<uint64_t>(), &d()->m, &d()->flags, nullptr), "k1");
+      if (!rc) rc = ck(okt::launch_k1(L, S, okt::K1Mode::kSelect, acc, nullptr, nullptr, 0.f, n, &d()->local_th,
+                                      nullptr, okt::OutCoo{coo.as<uint64_t>()}, &d()->m, nullptr, &d()->flags,
+                                      nullptr), "k1");
+    } else if (P == 1) {
+      // Steady state, one rank: the region is the local selection itself, so
+      // u = {|acc| >= max(local_th, global_th)} comes straight out of K1 and
+      // the local selection is only counted.
+      tmark(OKT_T_SELECT, s);
+      rc = ck(okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, g, eps_in, eps_out, fa,
+                             n, &d()->local_th, &d()->global_th,
+                             okt::OutCoo{nullptr, sur_idx.as<uint32_t>(), sur_val.as<double>()}, &d()->S, &d()->m,
+                             &d()->flags, nullptr, &ap1), "k1");
     } else {
       tmark(OKT_T_SELECT, s);
-      rc = ck(okt::launch_k1(L, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, g, eps_in, eps_out, fa,
-                             n, &d()->local_th, coo.as<uint64_t>(), &d()->m, &d()->flags, nullptr), "k1");
+      rc = ck(okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, g, eps_in, eps_out, fa,
+                             n, &d()->local_th, nullptr, okt::OutCoo{coo.as<uint64_t>()}, &d()->m, nullptr,
+                             &d()->flags, nullptr), "k1");
     }
     if (rc) return abort_step(rc);
 
@@ -639,16 +611,16 @@ struct okt_comm {
     std::vector<uint64_t> new_cuts(P + 1, 0);
 
     if (P == 1) {
-      tmark(OKT_T_GLOBAL, s);
       if (thr) {
         // The region is the local selection itself (fp32 values, exact in fp64).
+        tmark(OKT_T_GLOBAL, s);
         rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kAosF32, coo.p, 0, &d()->m, n, k, &d()->rs, hp,
                                          &d()->global_th, false), "radix");
+        if (!rc)
+          rc = ck(okt::launch_filter(L, S, true, coo.as<uint64_t>(), nullptr, nullptr, &d()->m, n, &d()->global_th,
+                                     sur_idx.as<uint32_t>(), sur_val.as<double>(), &d()->S, &ap1), "filter");
         if (rc) return abort_step(rc);
       }
-      rc = ck(okt::launch_filter(L, true, coo.as<uint64_t>(), nullptr, nullptr, &d()->m, n, &d()->global_th,
-                                 sur_idx.as<uint32_t>(), sur_val.as<double>(), &d()->S), "filter");
-      if (rc) return abort_step(rc);
       ui = sur_idx.as<uint32_t>();
       uv = sur_val.as<double>();
       d_U = &d()->S;
@@ -681,7 +653,7 @@ struct okt_comm {
           if ((rc = ensure(sur_idx, 4 * std::max<uint64_t>(bound, 1))) ||
               (rc = ensure(sur_val, 8 * std::max<uint64_t>(bound, 1))))
             return abort_step(rc);
-          rc = ck(okt::launch_filter(L, false, nullptr, reg_idx.as<uint32_t>(), reg_val.as<double>(), &d()->R,
+          rc = ck(okt::launch_filter(L, S, false, nullptr, reg_idx.as<uint32_t>(), reg_val.as<double>(), &d()->R,
                                      bound, &d()->global_th, sur_idx.as<uint32_t>(), sur_val.as<double>(),
                                      &d()->S), "filter");
         }
@@ -699,11 +671,13 @@ struct okt_comm {
       uv = u_val.as<double>();
     }
 
-    // ---- K7 ----
-    tmark(OKT_T_APPLY, s);
-    rc = ck(okt::launch_apply(L, ui, uv, d_U, U_bound, const_cast<float*>(acc), sgd, sgd ? w : nullptr, P,
-                              &d()->local_th, indexes.as<uint32_t>(), &d()->nidx, &d()->flags), "apply");
-    if (rc) return abort_step(rc);
+    // ---- K7 (fused into the compaction for P = 1) ----
+    if (P > 1) {
+      tmark(OKT_T_APPLY, s);
+      rc = ck(okt::launch_apply(L, S, ui, uv, d_U, U_bound, const_cast<float*>(acc), sgd, sgd ? w : nullptr, P,
+                                &d()->local_th, indexes.as<uint32_t>(), &d()->nidx, &d()->flags), "apply");
+      if (rc) return abort_step(rc);
+    }
     tstop(s);
     if (prof) {
       cudaEvent_t e = ev_get();
@@ -749,8 +723,8 @@ struct okt_comm {
       out->u.d_val = uv;
       out->u.nnz = P == 1 ? h->S : h->U;
       out->u.n = n;
-      out->d_indexes = indexes.as<uint32_t>();
-      out->n_indexes = h->nidx;
+      out->d_indexes = P == 1 ? ui : indexes.as<uint32_t>();
+      out->n_indexes = P == 1 ? h->S : h->nidx;
       out->local_selected = h->m;
     }
     if (h->flags & 4u) return set_err(OKT_ERR_NUMERIC, "oktopk_sgd_step: non-finite iterate");
@@ -796,24 +770,24 @@ int init_comm(okt_comm* c) {
     return set_err(OKT_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(cudaGetLastError()));
   }
   c->L.s = c->own;
-  c->ctr.zero_init = true;
   c->hist.zero_init = true;
   c->scal.zero_init = true;
-  c->status.zero_init = true;
   c->mask.zero_init = true;
-  cudaError_t e = c->ctr.ensure(64);
-  if (e == cudaSuccess) e = c->hist.ensure(2048 * 4);
+  c->S.max_chunks = dev_sms * 8;
+  cudaError_t e = c->hist.ensure(2048 * 4);
   if (e == cudaSuccess) e = c->scal.ensure(sizeof(DevScalars));
+  if (e == cudaSuccess) e = c->counts.ensure(4 * size_t(c->S.max_chunks));
+  if (e == cudaSuccess) e = c->counts2.ensure(4 * size_t(c->S.max_chunks));
+  if (e == cudaSuccess) e = c->chunkcap.ensure(64);
   if (e == cudaSuccess) e = cudaMallocHost(&c->h, sizeof(DevScalars));
   if (e == cudaSuccess) e = cudaMallocHost(&c->hup, sizeof(DevScalars));
   if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("init: ") + cudaGetErrorString(e));
   std::memset(c->h, 0, sizeof(DevScalars));
   std::memset(c->hup, 0, sizeof(DevScalars));
-  c->L.status = nullptr;
-  c->L.ctr = c->ctr.as<uint32_t>();
-  const int rc = c->reserve(4096);
-  c->L.status = c->status.as<uint64_t>();
-  return rc;
+  c->S.counts = c->counts.as<uint32_t>();
+  c->S.counts2 = c->counts2.as<uint32_t>();
+  c->S.chunk_cap = c->chunkcap.as<uint64_t>();
+  return c->reserve(4096);
 }
 
 struct DeviceGuard {
@@ -956,7 +930,6 @@ int okt_comm_reserve(okt_comm* c, size_t n) {
   OKT_COMM_CHECK(c);
   DeviceGuard g(c->device);
   const int rc = c->reserve(n);
-  c->L.status = c->status.as<uint64_t>();
   return rc;
 }
 
@@ -1002,7 +975,6 @@ int okt_sparse_allreduce(okt_comm* c, const float* d_acc, size_t n, int64_t t, s
   OKT_COMM_CHECK(c);
   DeviceGuard g(c->device);
   int rc = c->reserve(n);
-  c->L.status = c->status.as<uint64_t>();
   if (rc) return rc;
   return c->step(d_acc, nullptr, n, 0.0, t, k, false, out, c->pick(stream));
 }
@@ -1026,7 +998,6 @@ int okt_sgd_step(okt_comm* c, const float* d_grad, float* d_w, size_t n, double 
   if (!d_w) return set_err(OKT_ERR_INVALID_ARGUMENT, "null model");
   DeviceGuard g(c->device);
   int rc = c->reserve(n);
-  c->L.status = c->status.as<uint64_t>();
   if (rc) return rc;
   return c->step(d_grad, d_w, n, alpha, t, k, true, out, c->pick(stream));
 }
@@ -1130,17 +1101,15 @@ int okt_select_by_threshold(okt_comm* c, const float* d_g, size_t n, double th, 
   cudaStream_t s = c->pick(stream);
   c->L.s = s;
   int rc = c->reserve(std::max<size_t>(n, 1));
-  c->L.status = c->status.as<uint64_t>();
   if (rc) return rc;
   if ((rc = c->ensure(c->sel_idx, 4 * std::max<size_t>(n, 1))) ||
       (rc = c->ensure(c->sel_val, 8 * std::max<size_t>(n, 1))))
     return rc;
   if ((rc = c->upload_f64(&c->d()->th_arg, th, &c->hup->th_arg, s))) return rc;
   if (n) {
-    rc = c->ck(okt::launch_k1(c->L, okt::K1Mode::kSelect, d_g, nullptr, nullptr, 0.f, n, &c->d()->th_arg,
-                              c->coo.as<uint64_t>(), &c->d()->m, &c->d()->flags, nullptr), "k1");
-    if (!rc) rc = c->ck(okt::launch_extract(c->L, c->coo.as<uint64_t>(), &c->d()->m, n, c->sel_idx.as<uint32_t>(),
-                                            c->sel_val.as<double>()), "extract");
+    rc = c->ck(okt::launch_k1(c->L, c->S, okt::K1Mode::kSelect, d_g, nullptr, nullptr, 0.f, n, &c->d()->th_arg,
+                              nullptr, okt::OutCoo{nullptr, c->sel_idx.as<uint32_t>(), c->sel_val.as<double>()},
+                              &c->d()->m, nullptr, &c->d()->flags, nullptr), "k1");
   } else {
     rc = c->ck(cudaMemsetAsync(&c->d()->m, 0, 8, s), "memset");
   }
@@ -1179,7 +1148,6 @@ int okt_split_and_reduce(okt_comm* c, const float* d_g, size_t n, double local_t
   cudaStream_t s = c->pick(stream);
   c->L.s = s;
   int rc = c->reserve(n);
-  c->L.status = c->status.as<uint64_t>();
   if (rc) return rc;
   if ((rc = c->ensure(c->sel_idx, 4 * n)) || (rc = c->ensure(c->sel_val, 8 * n))) return rc;
   if ((rc = c->upload_f64(&c->d()->th_arg, local_th, &c->hup->th_arg, s))) return rc;
@@ -1189,8 +1157,9 @@ int okt_split_and_reduce(okt_comm* c, const float* d_g, size_t n, double local_t
     return rc;
   c->dev_stale = true;
   if ((rc = c->ck(cudaMemsetAsync(&c->d()->flags, 0, 4, s), "memset"))) return rc;
-  rc = c->ck(okt::launch_k1(c->L, okt::K1Mode::kSelect, d_g, nullptr, nullptr, 0.f, n, &c->d()->th_arg,
-                            c->coo.as<uint64_t>(), &c->d()->m, &c->d()->flags, nullptr), "k1");
+  rc = c->ck(okt::launch_k1(c->L, c->S, okt::K1Mode::kSelect, d_g, nullptr, nullptr, 0.f, n, &c->d()->th_arg,
+                            nullptr, okt::OutCoo{c->coo.as<uint64_t>()}, &c->d()->m, nullptr, &c->d()->flags,
+                            nullptr), "k1");
   if (rc) return rc;
   // The reference's split_and_reduce does not test finiteness; keep the
   // collective non-finite abort of the full step out of this entry point.
@@ -1234,7 +1203,7 @@ int okt_balance_and_allgatherv(okt_comm* c, const uint32_t* d_idx, const double*
     return rc;
   if ((rc = c->upload_f64(&c->d()->th_arg, global_th, &c->hup->th_arg, s))) return rc;
   if ((rc = c->upload_u64(&c->d()->R, nnz, &c->hup->R, s))) return rc;
-  rc = c->ck(okt::launch_filter(c->L, false, nullptr, d_idx, d_val, &c->d()->R, nnz, &c->d()->th_arg,
+  rc = c->ck(okt::launch_filter(c->L, c->S, false, nullptr, d_idx, d_val, &c->d()->R, nnz, &c->d()->th_arg,
                                 c->sur_idx.as<uint32_t>(), c->sur_val.as<double>(), &c->d()->S), "filter");
   if (rc) return rc;
   if (c->P == 1) {
@@ -1252,6 +1221,53 @@ int okt_balance_and_allgatherv(okt_comm* c, const uint32_t* d_idx, const double*
   u->d_val = c->u_val.as<double>();
   u->nnz = U;
   u->n = n;
+  return OKT_OK;
+}
+
+// ---- host planning (no GPU) ------------------------------------------------------------
+int okt_plan_cuts(const uint64_t* proposals, int P, uint64_t n, uint64_t* cuts) {
+  if (!proposals || !cuts || P < 1 || P > OKT_MAX_WORLD) return set_err(OKT_ERR_INVALID_ARGUMENT, "bad argument");
+  const std::vector<uint64_t> c = okt::plan::cuts_from_proposals(proposals, P, n);
+  std::memcpy(cuts, c.data(), sizeof(uint64_t) * (P + 1));
+  return OKT_OK;
+}
+
+int okt_plan_balance(int rank, int P, const uint64_t* sizes, int* balanced, okt_piece* sends, int* nsends,
+                     okt_piece* recvs, int* nrecvs, okt_piece* own, uint64_t* part_off, uint64_t* part_sz) {
+  if (!sizes || P < 1 || P > OKT_MAX_WORLD || rank < 0 || rank >= P)
+    return set_err(OKT_ERR_INVALID_ARGUMENT, "bad argument");
+  const okt::plan::Balance B = okt::plan::balance(rank, P, std::vector<uint64_t>(sizes, sizes + P));
+  if (balanced) *balanced = B.on ? 1 : 0;
+  auto put = [](const std::vector<okt::plan::Piece>& v, okt_piece* out, int* cnt) {
+    if (cnt) *cnt = int(v.size());
+    if (out)
+      for (size_t i = 0; i < v.size(); ++i) out[i] = okt_piece{v[i].peer, v[i].a, v[i].b};
+  };
+  put(B.sends, sends, nsends);
+  put(B.recvs, recvs, nrecvs);
+  if (own) *own = okt_piece{B.own.peer, B.own.a, B.own.b};
+  for (int q = 0; q < P; ++q) {
+    if (part_off) part_off[q] = B.part_off[q];
+    if (part_sz) part_sz[q] = B.part_sz[q];
+  }
+  return OKT_OK;
+}
+
+int okt_plan_ledger(int rank, int P, int kind, const uint64_t* sizes, uint64_t len, uint32_t bucket,
+                    okt_counters* out) {
+  if (!out || P < 1 || P > OKT_MAX_WORLD || rank < 0 || rank >= P)
+    return set_err(OKT_ERR_INVALID_ARGUMENT, "bad argument");
+  std::memset(out, 0, sizeof(*out));
+  switch (kind) {
+    case OKT_PLAN_SPLIT: okt::plan::ledger_split(*out, rank, P, sizes, bucket); break;
+    case OKT_PLAN_ALLGATHERV: okt::plan::ledger_allgatherv(*out, rank, P, sizes); break;
+    case OKT_PLAN_AVG: okt::plan::ledger_avg(*out, P, len); break;
+    case OKT_PLAN_ALLGATHER_U32: okt::plan::ledger_allgather_u32(*out, P); break;
+    case OKT_PLAN_BALANCE:
+      okt::plan::ledger_balance(*out, okt::plan::balance(rank, P, std::vector<uint64_t>(sizes, sizes + P)));
+      break;
+    default: return set_err(OKT_ERR_INVALID_ARGUMENT, "unknown ledger kind");
+  }
   return OKT_OK;
 }
 

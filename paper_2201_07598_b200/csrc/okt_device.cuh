@@ -1,12 +1,17 @@
 // okt_device.cuh — device building blocks shared by the Ok-Topk kernels.
 //
 // Every order-preserving compaction on the path (local selection, region
-// merge, survivor filter, index intersection) is a single-pass decoupled
-// look-back scan: a tile publishes its aggregate, one warp walks predecessors
-// 32 at a time, and the tile's entries are written straight to their final
-// positions.  Tile IDs come from an atomic counter (not blockIdx), so a tile
-// only ever waits on tiles already owned by running CTAs: deadlock-free even
-// when several ranks' kernels share one GPU.
+// merge, survivor filter, index intersection) runs in two phases:
+//   phase A  CTA c owns a contiguous chunk of tiles and compacts its selected
+//            entries into its own staging window (chunk-local positions).  One
+//            __syncthreads per tile; no CTA ever waits on another, so the
+//            streaming pass runs at HBM speed.
+//   phase B  one CTA per chunk: exclusive prefix of the chunk counts, then a
+//            coalesced copy of the chunk's entries to their final positions.
+// Round-1 measurement (profiles/r01_k1_lookback_raw.csv): a single-pass
+// decoupled look-back version of K1 spent 64% of its cycles at the CTA
+// barrier behind the look-back warp and ran at 30% of HBM peak, while the
+// same streaming pass without the look-back ran at 91%.
 #pragma once
 
 #include <cstdint>
@@ -18,95 +23,24 @@ constexpr int kMaxP = 8;                     // ranks per world (one HGX box)
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kJ = 4;                        // groups per thread per tile
-constexpr int kC = 4;                        // elements per group (one 16 B vector)
-constexpr int kTile = kJ * kC * kThreads;    // 4096 elements per tile
 static_assert(kJ * kWarps == 32, "tile scan table must be one warp wide");
 
-// ---- look-back status words --------------------------------------------------
-// [63:62] flag (1 = aggregate, 2 = inclusive prefix), [61:32] launch epoch,
-// [31:0] value.  Flag, epoch and value travel in one 64-bit store, so no
-// fences are needed between them; the epoch makes stale words from earlier
-// launches invisible, so the array is never cleared.
-constexpr uint64_t kFlagAgg = 1ull;
-constexpr uint64_t kFlagPre = 2ull;
-
-__device__ __forceinline__ uint64_t pack_status(uint64_t flag, uint32_t epoch,
-                                                uint32_t v) {
-  return (flag << 62) | (uint64_t(epoch & 0x3fffffffu) << 32) | uint64_t(v);
-}
-__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned r;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
   return r;
 }
 
-// Warp-collective: publish `agg` for `tile` and return the exclusive prefix of
-// all earlier tiles.  Every lane returns the same value.
-__device__ __forceinline__ uint32_t lookback(uint64_t* status, uint32_t tile,
-                                             uint32_t epoch, uint32_t agg) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t ep = epoch & 0x3fffffffu;
-  if (tile == 0) {
-    if (lane == 0) st_relaxed(&status[0], pack_status(kFlagPre, epoch, agg));
-    return 0;
-  }
-  if (lane == 0) st_relaxed(&status[tile], pack_status(kFlagAgg, epoch, agg));
-  uint32_t excl = 0;
-  int64_t pred = int64_t(tile) - 1;
-  while (true) {
-    const int64_t idx = pred - lane;
-    uint32_t flag = uint32_t(kFlagPre), val = 0;
-    if (idx >= 0) {
-      uint64_t s;
-      int spins = 0;
-      while (true) {
-        s = ld_relaxed(&status[idx]);
-        if (uint32_t((s >> 32) & 0x3fffffffu) == ep && (s >> 62) != 0) break;
-        if (++spins > 8) __nanosleep(32);
-      }
-      flag = uint32_t(s >> 62);
-      val = uint32_t(s);
-    }
-    const unsigned pre = __ballot_sync(0xffffffffu, flag == uint32_t(kFlagPre));
-    const int first = pre ? (__ffs(pre) - 1) : 32;
-    uint32_t contrib = (lane <= first) ? val : 0u;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, o);
-    excl += contrib;
-    if (pre) break;
-    pred -= 32;
-  }
-  if (lane == 0) st_relaxed(&status[tile], pack_status(kFlagPre, epoch, excl + agg));
-  return excl;
-}
-
-// ---- tile scan ---------------------------------------------------------------
 // Element (j, warp, lane, c) of a tile sits at tile offset
-// j*kC*kThreads + (warp*32 + lane)*kC + c, so output order is (j, warp, lane, c).
-// Each thread passes one ballot per (j, c); the per-(j, warp) counts form a
-// 32-entry table that warp 0 scans before the look-back.
-struct TileScanSmem {
-  uint32_t cnt[kJ * kWarps];
-  uint32_t base;
-  uint32_t tile;
-};
-
-// All threads call.  On return s.base is the tile's exclusive prefix and
-// s.cnt[j*kWarps + w] the exclusive offset of (j, w) inside the tile.  The
-// CTA that owns the last tile stores the grand total to *d_total.
+// j*C*kThreads + (warp*32 + lane)*C + c, so output order is (j, warp, lane, c).
+// Lane 0 of each warp writes its per-j selected counts into the 32-entry
+// table; after one barrier every warp scans the table itself.  The table is
+// double-buffered by the caller (tile parity), which makes the second barrier
+// unnecessary.  Returns the tile's selected total; grp[j] receives the
+// exclusive offset of (j, this warp) inside the tile.
 template <int C>
-__device__ __forceinline__ void tile_scan(TileScanSmem& s, const unsigned (&bal)[kJ][C],
-                                          uint32_t tile, uint32_t num_tiles,
-                                          uint64_t* status, uint32_t epoch,
-                                          uint64_t* d_total) {
+__device__ __forceinline__ uint32_t tile_offsets(uint32_t* tbl, const unsigned (&bal)[kJ][C],
+                                                 uint32_t (&grp)[kJ]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) {
 #pragma unroll
@@ -114,33 +48,26 @@ __device__ __forceinline__ void tile_scan(TileScanSmem& s, const unsigned (&bal)
       uint32_t c = 0;
 #pragma unroll
       for (int q = 0; q < C; ++q) c += __popc(bal[j][q]);
-      s.cnt[j * kWarps + warp] = c;
+      tbl[j * kWarps + warp] = c;
     }
   }
   __syncthreads();
-  if (warp == 0) {
-    const uint32_t v = s.cnt[lane];
-    uint32_t incl = v;
+  const uint32_t v = tbl[lane];
+  uint32_t incl = v;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t excl = lookback(status, tile, epoch, total);
-    s.cnt[lane] = incl - v;
-    if (lane == 0) {
-      s.base = excl;
-      if (tile + 1 == num_tiles && d_total) *d_total = uint64_t(excl) + total;
-    }
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
   }
-  __syncthreads();
+  const uint32_t excl = incl - v;
+#pragma unroll
+  for (int j = 0; j < kJ; ++j) grp[j] = __shfl_sync(0xffffffffu, excl, j * kWarps + warp);
+  return __shfl_sync(0xffffffffu, incl, 31);
 }
 
 // Rank of element (j, c) of this thread inside its (j, warp) group.
 template <int C>
-__device__ __forceinline__ uint32_t rank_in_group(const unsigned (&bal)[kJ][C], int j,
-                                                  int c) {
+__device__ __forceinline__ uint32_t rank_in_group(const unsigned (&bal)[kJ][C], int j, int c) {
   const unsigned lt = lanemask_lt();
   const unsigned me = 1u << (threadIdx.x & 31);
   uint32_t r = 0;
@@ -152,25 +79,18 @@ __device__ __forceinline__ uint32_t rank_in_group(const unsigned (&bal)[kJ][C], 
   return r;
 }
 
-// Dynamic tile fetch: one atomic per tile on ctr[0]; the last CTA to leave
-// resets the counter pair so the next launch on the stream starts at 0.
-__device__ __forceinline__ uint32_t fetch_tile(uint32_t* ctr, uint32_t& s_tile) {
-  if (threadIdx.x == 0) s_tile = atomicAdd(&ctr[0], 1u);
+// CTA-wide sum of one u32 per thread (all threads get the result).
+__device__ __forceinline__ uint64_t block_sum(uint64_t v, uint64_t* red) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __syncthreads();
-  const uint32_t t = s_tile;
-  __syncthreads();  // every thread has read s_tile before thread 0 may refill it
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  uint64_t t = 0;
+  const int nw = blockDim.x >> 5;
+  for (int w = 0; w < nw; ++w) t += red[w];
   return t;
-}
-__device__ __forceinline__ void retire_cta(uint32_t* ctr) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&ctr[1], 1u) == gridDim.x - 1) {
-      ctr[0] = 0;
-      ctr[1] = 0;
-      __threadfence();
-    }
-  }
 }
 
 // Smallest float f with (double)f >= th (th >= 0): |a| >= th  <=>  |a| >= f for

@@ -1,8 +1,9 @@
 // okt_kernels.cu — sm_100a kernels of the Ok-Topk sparse allreduce.
 //
 // Everything here is HBM- or latency-bound integer/byte work: 128-bit
-// coalesced streaming loads, warp-ballot + decoupled look-back compaction, and
-// O(k) scatters.  No tensor cores: nothing on this path is a contraction.
+// coalesced streaming loads, warp-ballot compaction in two phases (see
+// okt_device.cuh), and O(k) scatters.  No tensor cores: nothing on this path
+// is a contraction.
 //
 // Reference functions each kernel replaces (proj/core/src/...):
 //   k1_kernel          trainer.cpp:423-435 make_accumulator, sparse.cpp:14-19
@@ -39,40 +40,140 @@ __device__ __forceinline__ bool nonfinite(float a) {
   return (__float_as_uint(a) & 0x7f800000u) == 0x7f800000u;
 }
 
+uint32_t chunks_for(uint64_t tiles, int resident, int max_chunks) {
+  uint64_t g = std::min<uint64_t>(tiles, uint64_t(resident));
+  g = std::min<uint64_t>(g, uint64_t(max_chunks));
+  return uint32_t(std::max<uint64_t>(g, 1));
+}
+
 }  // namespace
 
+size_t stage_entries(uint64_t count, int tile, int max_chunks) {
+  return size_t((count + tile - 1) / tile + uint64_t(max_chunks)) * size_t(tile);
+}
+
 // =============================================================================
-// K1: fused accumulate / select / compact
+// Phase B: chunk prefix + copy to final positions
 // =============================================================================
-template <bool ACCUM, bool SELECT, bool HIST, bool VEC>
+// MODE 0: AoS u64 -> AoS u64; 1: AoS u64 -> SoA (u32, f32 widened to f64);
+//      2: SoA -> SoA; 3: u32 -> u32.
+// APPLY (P = 1, where every entry of u is also in the local selection): fuse
+// K7 into the copy — w[i] -= v, acc[i] = 0 — so the single-rank step needs no
+// separate apply pass; `indexes` is then u's index array itself.
+template <int MODE, bool APPLY>
 __global__ void __launch_bounds__(kThreads)
-    k1_kernel(const float* __restrict__ g, const float* eps_in, float* eps_out, float alpha,
-              uint64_t n, uint32_t num_tiles, const double* __restrict__ d_th,
-              uint64_t* __restrict__ out, uint64_t* d_m, uint64_t* status, uint32_t epoch,
-              uint32_t* ctr, uint32_t* d_flags, uint32_t* d_hist) {
-  __shared__ TileScanSmem s;
+    compact_kernel(const uint64_t* __restrict__ s64, const uint32_t* __restrict__ sidx,
+                   const double* __restrict__ sval, const uint32_t* __restrict__ counts,
+                   const uint32_t* __restrict__ counts2, uint64_t cap_host, const uint64_t* d_cap,
+                   uint64_t* __restrict__ o64, uint32_t* __restrict__ oidx, double* __restrict__ oval,
+                   uint64_t* d_total, uint64_t* d_total2, ApplyArgs ap) {
+  __shared__ uint64_t red[kWarps];
+  const int c = blockIdx.x, G = gridDim.x;
+  uint64_t pre = 0;
+  for (int q = threadIdx.x; q < c; q += kThreads) pre += counts[q];
+  pre = block_sum(pre, red);
+  const uint64_t cnt = counts[c];
+  const uint64_t cap = d_cap ? *d_cap : cap_host;
+  const uint64_t src = uint64_t(c) * cap;
+  const bool skip = APPLY && (*ap.d_flags & 1u);  // non-finite step: touch nothing
+  bool bad = false;
+  for (uint64_t j = threadIdx.x; j < cnt; j += kThreads) {
+    uint32_t i = 0;
+    double v = 0.0;
+    if (MODE == 0) {
+      o64[pre + j] = s64[src + j];
+    } else if (MODE == 1) {
+      const uint64_t e = s64[src + j];
+      i = coo_idx(e);
+      v = double(coo_val(e));
+      oidx[pre + j] = i;
+      oval[pre + j] = v;
+    } else if (MODE == 2) {
+      i = sidx[src + j];
+      v = sval[src + j];
+      oidx[pre + j] = i;
+      oval[pre + j] = v;
+    } else {
+      oidx[pre + j] = sidx[src + j];
+    }
+    if (APPLY && !skip) {
+      const float wi = ap.w[i];
+      const float nw = float(double(wi) - v);
+      ap.w[i] = nw;
+      ap.acc[i] = 0.f;
+      bad |= (__float_as_uint(nw) & 0x7f800000u) == 0x7f800000u;
+    }
+  }
+  if (APPLY && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(ap.d_flags, 4u);
+  if (c == G - 1) {
+    if (threadIdx.x == 0) *d_total = pre + cnt;
+    if (counts2) {
+      uint64_t s2 = 0;
+      for (int q = threadIdx.x; q < G; q += kThreads) s2 += counts2[q];
+      s2 = block_sum(s2, red);
+      if (threadIdx.x == 0) *d_total2 = s2;
+    }
+  }
+}
+
+template <int MODE>
+static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_t cap_host,
+                                  const uint64_t* d_cap, bool with2, uint64_t* o64, uint32_t* oidx,
+                                  double* oval, uint64_t* d_total, uint64_t* d_total2,
+                                  const ApplyArgs* ap = nullptr) {
+  if (ap && ap->w)
+    compact_kernel<MODE, true><<<G, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts,
+                                                        with2 ? S.counts2 : nullptr, cap_host, d_cap, o64, oidx,
+                                                        oval, d_total, d_total2, *ap);
+  else
+    compact_kernel<MODE, false><<<G, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts,
+                                                         with2 ? S.counts2 : nullptr, cap_host, d_cap, o64, oidx,
+                                                         oval, d_total, d_total2, ApplyArgs{});
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+// =============================================================================
+// K1: fused accumulate / select / compact (phase A)
+// =============================================================================
+template <bool ACCUM, bool SELECT, bool HIST, bool VEC, bool DUAL>
+__global__ void __launch_bounds__(kThreads)
+    k1_kernel(const float* __restrict__ g, const float* eps_in, float* eps_out, float alpha, uint64_t n,
+              uint32_t tiles, uint32_t tpc, const double* __restrict__ d_th,
+              const double* __restrict__ d_th2, uint64_t* __restrict__ stg, uint32_t* counts,
+              uint32_t* counts2, uint32_t* d_flags, uint32_t* d_hist) {
+  constexpr int C = 4, TILE = kJ * C * kThreads;
+  __shared__ uint32_t tbl[2][32];
   __shared__ uint32_t s_hist[HIST ? 2048 : 1];
+  __shared__ uint64_t red[kWarps];
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  float tf = 0.f;
-  if (SELECT) tf = ceil_to_float(*d_th);
+  float tf = 0.f, tf_loc = 0.f;
+  if (SELECT) {
+    const double lth = *d_th;
+    tf_loc = ceil_to_float(lth);
+    tf = DUAL ? ceil_to_float(fmax(lth, *d_th2)) : tf_loc;
+  }
   if (HIST) {
     for (int i = tid; i < 2048; i += kThreads) s_hist[i] = 0;
+    __syncthreads();
   }
   bool bad = false;
-  for (;;) {
-    const uint32_t tile = fetch_tile(ctr, s.tile);
-    if (tile >= num_tiles) break;
-    const uint64_t base = uint64_t(tile) * kTile;
-    float a[kJ][kC];
-    bool valid[kJ][kC];
-    if (VEC && base + kTile <= n) {
+  uint32_t running = 0, mloc = 0;
+  const uint32_t t0 = blockIdx.x * tpc;
+  const uint32_t t1 = min(t0 + tpc, tiles);
+  uint64_t* out = stg + uint64_t(blockIdx.x) * tpc * TILE;
+  int parity = 0;
+  for (uint32_t tile = t0; tile < t1; ++tile, parity ^= 1) {
+    const uint64_t base = uint64_t(tile) * TILE;
+    float a[kJ][C];
+    bool valid[kJ][C];
+    if (VEC && base + TILE <= n) {
       float4 gv[kJ], ev[kJ];
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
-        const uint64_t e0 = base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC;
-        gv[j] = __ldg(reinterpret_cast<const float4*>(g + e0));
-        if (ACCUM) ev[j] = *reinterpret_cast<const float4*>(eps_in + e0);
+        const uint64_t e0 = base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C;
+        gv[j] = __ldcs(reinterpret_cast<const float4*>(g + e0));
+        if (ACCUM) ev[j] = __ldcs(reinterpret_cast<const float4*>(eps_in + e0));
       }
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
@@ -81,7 +182,7 @@ __global__ void __launch_bounds__(kThreads)
           a[j][1] = fmaf(alpha, gv[j].y, ev[j].y);
           a[j][2] = fmaf(alpha, gv[j].z, ev[j].z);
           a[j][3] = fmaf(alpha, gv[j].w, ev[j].w);
-          const uint64_t e0 = base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC;
+          const uint64_t e0 = base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C;
           *reinterpret_cast<float4*>(eps_out + e0) = make_float4(a[j][0], a[j][1], a[j][2], a[j][3]);
         } else {
           a[j][0] = gv[j].x;
@@ -90,7 +191,7 @@ __global__ void __launch_bounds__(kThreads)
           a[j][3] = gv[j].w;
         }
 #pragma unroll
-        for (int c = 0; c < kC; ++c) {
+        for (int c = 0; c < C; ++c) {
           valid[j][c] = true;
           bad |= nonfinite(a[j][c]);
         }
@@ -99,8 +200,8 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
 #pragma unroll
-        for (int c = 0; c < kC; ++c) {
-          const uint64_t e = base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC + c;
+        for (int c = 0; c < C; ++c) {
+          const uint64_t e = base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C + c;
           valid[j][c] = e < n;
           float x = 0.f;
           if (valid[j][c]) {
@@ -119,76 +220,405 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int j = 0; j < kJ; ++j)
 #pragma unroll
-        for (int c = 0; c < kC; ++c)
+        for (int c = 0; c < C; ++c)
           if (valid[j][c]) atomicAdd(&s_hist[(__float_as_uint(a[j][c]) & 0x7fffffffu) >> 20], 1u);
     }
     if (SELECT) {
-      unsigned bal[kJ][kC];
-      bool pred[kJ][kC];
+      unsigned bal[kJ][C];
+      bool pred[kJ][C];
 #pragma unroll
       for (int j = 0; j < kJ; ++j)
 #pragma unroll
-        for (int c = 0; c < kC; ++c) {
-          pred[j][c] = valid[j][c] && fabsf(a[j][c]) >= tf;
+        for (int c = 0; c < C; ++c) {
+          const float m = fabsf(a[j][c]);
+          pred[j][c] = valid[j][c] && m >= tf;
+          if (DUAL) mloc += (valid[j][c] && m >= tf_loc) ? 1u : 0u;
           bal[j][c] = __ballot_sync(0xffffffffu, pred[j][c]);
         }
-      tile_scan<kC>(s, bal, tile, num_tiles, status, epoch, d_m);
+      uint32_t grp[kJ];
+      const uint32_t total = tile_offsets<C>(tbl[parity], bal, grp);
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
-        const uint32_t gbase = s.base + s.cnt[j * kWarps + warp];
 #pragma unroll
-        for (int c = 0; c < kC; ++c) {
+        for (int c = 0; c < C; ++c) {
           if (pred[j][c]) {
-            const uint32_t pos = gbase + rank_in_group<kC>(bal, j, c);
-            const uint64_t e = base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC + c;
+            const uint32_t pos = running + grp[j] + rank_in_group<C>(bal, j, c);
+            const uint64_t e = base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C + c;
             out[pos] = coo_pack(uint32_t(e), a[j][c]);
           }
         }
       }
+      running += total;
     }
+  }
+  if (SELECT && tid == 0) counts[blockIdx.x] = running;
+  if (DUAL) {
+    const uint64_t s = block_sum(mloc, red);
+    if (tid == 0) counts2[blockIdx.x] = uint32_t(s);
   }
   if (__syncthreads_or(bad) && tid == 0) atomicOr(d_flags, 1u);
   if (HIST) {
     for (int i = tid; i < 2048; i += kThreads)
       if (s_hist[i]) atomicAdd(&d_hist[i], s_hist[i]);
   }
-  retire_cta(ctr);
 }
 
-template <bool ACCUM, bool SELECT, bool HIST>
-static cudaError_t k1_dispatch(Launch& L, bool vec, const float* g, const float* eps_in,
+template <bool ACCUM, bool SELECT, bool HIST, bool DUAL>
+static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float* g, const float* eps_in,
                                float* eps_out, float alpha, uint64_t n, const double* d_th,
-                               uint64_t* out, uint64_t* d_m, uint32_t* d_flags, uint32_t* d_hist) {
-  const uint32_t tiles = uint32_t((n + kTile - 1) / kTile);
-  auto kern = vec ? k1_kernel<ACCUM, SELECT, HIST, true> : k1_kernel<ACCUM, SELECT, HIST, false>;
+                               const double* d_th2, const OutCoo& out, uint64_t* d_m, uint64_t* d_m2,
+                               uint32_t* d_flags, uint32_t* d_hist, const ApplyArgs* ap) {
+  constexpr int TILE = kJ * 4 * kThreads;
+  const uint64_t tiles = (n + TILE - 1) / TILE;
+  auto kern = vec ? k1_kernel<ACCUM, SELECT, HIST, true, DUAL> : k1_kernel<ACCUM, SELECT, HIST, false, DUAL>;
   static int cap_v = 0, cap_s = 0;
   int& cap = vec ? cap_v : cap_s;
   if (!cap) cap = resident_ctas(kern, kThreads, L.sms);
-  const int grid = int(std::min<uint64_t>(tiles, uint64_t(cap)));
-  const uint32_t ep = SELECT ? L.next_epoch() : 0;
-  kern<<<grid, kThreads, 0, L.s>>>(g, eps_in, eps_out, alpha, n, tiles, d_th, out, d_m, L.status,
-                                   ep, L.ctr, d_flags, d_hist);
+  const uint32_t G = chunks_for(tiles, cap, S.max_chunks);
+  const uint32_t tpc = uint32_t((tiles + G - 1) / G);
+  kern<<<G, kThreads, 0, L.s>>>(g, eps_in, eps_out, alpha, n, uint32_t(tiles), tpc, d_th, d_th2, S.s64, S.counts,
+                                S.counts2, d_flags, d_hist);
+  ++L.launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !SELECT) return e;
+  const uint64_t chunk_cap = uint64_t(tpc) * TILE;
+  if (out.aos)
+    return launch_compact<0>(L, S, G, chunk_cap, nullptr, DUAL, out.aos, nullptr, nullptr, d_m, d_m2);
+  return launch_compact<1>(L, S, G, chunk_cap, nullptr, DUAL, nullptr, out.idx, out.val, d_m, d_m2, ap);
+}
+
+cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, const float* eps_in,
+                      float* eps_out, float alpha, uint64_t n, const double* d_th, const double* d_th2,
+                      const OutCoo& out, uint64_t* d_m, uint64_t* d_m2, uint32_t* d_flags, uint32_t* d_hist,
+                      const ApplyArgs* ap) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  bool vec = al(g);
+  if (mode != K1Mode::kSelect) vec = vec && al(eps_in) && al(eps_out);
+  const bool dual = d_th2 != nullptr;
+  switch (mode) {
+    case K1Mode::kSelect:
+      return dual ? k1_dispatch<false, true, false, true>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out,
+                                                           d_m, d_m2, d_flags, d_hist, ap)
+                  : k1_dispatch<false, true, false, false>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2,
+                                                            out, d_m, d_m2, d_flags, d_hist, ap);
+    case K1Mode::kAccumSelect:
+      return dual ? k1_dispatch<true, true, false, true>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out,
+                                                          d_m, d_m2, d_flags, d_hist, ap)
+                  : k1_dispatch<true, true, false, false>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out,
+                                                           d_m, d_m2, d_flags, d_hist, ap);
+    case K1Mode::kAccumHist:
+      return k1_dispatch<true, false, true, false>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out, d_m,
+                                                   d_m2, d_flags, d_hist, ap);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// =============================================================================
+// Survivor filter and K7 apply (COO lists whose length lives on the device)
+// =============================================================================
+constexpr int kTileK = kJ * kThreads;  // 1024 entries per tile for the O(k) passes
+
+template <bool AOS>
+__global__ void __launch_bounds__(kThreads)
+    filter_kernel(const uint64_t* __restrict__ in_aos, const uint32_t* __restrict__ in_idx,
+                  const double* __restrict__ in_val, const uint64_t* d_cnt_in, const double* d_th,
+                  uint32_t* __restrict__ sidx, double* __restrict__ sval, uint32_t* counts,
+                  uint64_t* d_cap) {
+  __shared__ uint32_t tbl[2][32];
+  const int tid = threadIdx.x;
+  const uint64_t cnt = *d_cnt_in;
+  const double th = *d_th;
+  const uint64_t tiles = (cnt + kTileK - 1) / kTileK;
+  const uint64_t tpc = (tiles + gridDim.x - 1) / gridDim.x;
+  if (blockIdx.x == 0 && tid == 0) *d_cap = tpc * kTileK;
+  const uint64_t t0 = uint64_t(blockIdx.x) * tpc, t1 = min(t0 + tpc, tiles);
+  const uint64_t obase = uint64_t(blockIdx.x) * tpc * kTileK;
+  uint32_t running = 0;
+  int parity = 0;
+  for (uint64_t tile = t0; tile < t1; ++tile, parity ^= 1) {
+    uint32_t idx[kJ];
+    double val[kJ];
+    unsigned bal[kJ][1];
+    bool pred[kJ];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const uint64_t e = tile * kTileK + uint64_t(j) * kThreads + tid;
+      const bool valid = e < cnt;
+      idx[j] = 0;
+      val[j] = 0.0;
+      if (valid) {
+        if (AOS) {
+          const uint64_t x = in_aos[e];
+          idx[j] = coo_idx(x);
+          val[j] = double(coo_val(x));
+        } else {
+          idx[j] = in_idx[e];
+          val[j] = in_val[e];
+        }
+      }
+      pred[j] = valid && fabs(val[j]) >= th;
+      bal[j][0] = __ballot_sync(0xffffffffu, pred[j]);
+    }
+    uint32_t grp[kJ];
+    const uint32_t total = tile_offsets<1>(tbl[parity], bal, grp);
+#pragma unroll
+    for (int j = 0; j < kJ; ++j)
+      if (pred[j]) {
+        const uint64_t pos = obase + running + grp[j] + rank_in_group<1>(bal, j, 0);
+        sidx[pos] = idx[j];
+        sval[pos] = val[j];
+      }
+    running += total;
+  }
+  if (tid == 0) counts[blockIdx.x] = running;
+}
+
+cudaError_t launch_filter(Launch& L, const Stage& S, bool aos, const uint64_t* in_aos, const uint32_t* in_idx,
+                          const double* in_val, const uint64_t* d_cnt_in, uint64_t bound, const double* d_th,
+                          uint32_t* out_idx, double* out_val, uint64_t* d_cnt_out, const ApplyArgs* ap) {
+  static int cap_a = 0, cap_s = 0;
+  int& cap = aos ? cap_a : cap_s;
+  if (!cap) cap = aos ? resident_ctas(filter_kernel<true>, kThreads, L.sms)
+                      : resident_ctas(filter_kernel<false>, kThreads, L.sms);
+  const uint32_t G = chunks_for((bound + kTileK - 1) / kTileK, cap, S.max_chunks);
+  if (aos)
+    filter_kernel<true><<<G, kThreads, 0, L.s>>>(in_aos, in_idx, in_val, d_cnt_in, d_th, S.sidx, S.sval, S.counts,
+                                                 S.chunk_cap);
+  else
+    filter_kernel<false><<<G, kThreads, 0, L.s>>>(in_aos, in_idx, in_val, d_cnt_in, d_th, S.sidx, S.sval, S.counts,
+                                                  S.chunk_cap);
+  ++L.launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_compact<2>(L, S, G, 0, S.chunk_cap, false, nullptr, out_idx, out_val, d_cnt_out, nullptr, ap);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    apply_kernel(const uint32_t* __restrict__ u_idx, const double* __restrict__ u_val, const uint64_t* d_U,
+                 float* acc, int zero_eps, float* w, int P, const double* d_local_th,
+                 uint32_t* __restrict__ sidx, uint32_t* counts, uint64_t* d_cap, uint32_t* d_flags) {
+  __shared__ uint32_t tbl[2][32];
+  const int tid = threadIdx.x;
+  // A step whose input was non-finite applies nothing (the reference throws
+  // before touching the residual or the model).
+  const bool skip = (*d_flags & 1u) != 0;
+  const uint64_t cnt = skip ? 0 : *d_U;
+  const float tf = ceil_to_float(*d_local_th);
+  const double dP = double(P);
+  const uint64_t tiles = (cnt + kTileK - 1) / kTileK;
+  const uint64_t tpc = (tiles + gridDim.x - 1) / gridDim.x;
+  if (blockIdx.x == 0 && tid == 0) *d_cap = tpc * kTileK;
+  const uint64_t t0 = uint64_t(blockIdx.x) * tpc, t1 = min(t0 + tpc, tiles);
+  const uint64_t obase = uint64_t(blockIdx.x) * tpc * kTileK;
+  uint32_t running = 0;
+  bool bad = false;
+  int parity = 0;
+  for (uint64_t tile = t0; tile < t1; ++tile, parity ^= 1) {
+    uint32_t idx[kJ];
+    double val[kJ];
+    bool valid[kJ];
+    float av[kJ], wv[kJ];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const uint64_t e = tile * kTileK + uint64_t(j) * kThreads + tid;
+      valid[j] = e < cnt;
+      idx[j] = valid[j] ? u_idx[e] : 0u;
+      val[j] = valid[j] ? u_val[e] : 0.0;
+    }
+    // Issue every gather before any store: acc and w never alias, and the
+    // entries of u are distinct, so all 2*kJ loads can be in flight together.
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      av[j] = valid[j] ? acc[idx[j]] : 0.f;
+      wv[j] = (valid[j] && w) ? w[idx[j]] : 0.f;
+    }
+    unsigned bal[kJ][1];
+    bool pred[kJ];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      pred[j] = valid[j] && fabsf(av[j]) >= tf;
+      if (valid[j]) {
+        if (w) {
+          const float nw = float(double(wv[j]) - val[j] / dP);
+          w[idx[j]] = nw;
+          bad |= nonfinite(nw);
+        }
+        if (zero_eps && pred[j]) acc[idx[j]] = 0.f;
+      }
+      bal[j][0] = __ballot_sync(0xffffffffu, pred[j]);
+    }
+    uint32_t grp[kJ];
+    const uint32_t total = tile_offsets<1>(tbl[parity], bal, grp);
+#pragma unroll
+    for (int j = 0; j < kJ; ++j)
+      if (pred[j]) sidx[obase + running + grp[j] + rank_in_group<1>(bal, j, 0)] = idx[j];
+    running += total;
+  }
+  if (tid == 0) counts[blockIdx.x] = running;
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(d_flags, 4u);
+}
+
+cudaError_t launch_apply(Launch& L, const Stage& S, const uint32_t* u_idx, const double* u_val, const uint64_t* d_U,
+                         uint64_t bound, float* acc, bool zero_eps, float* w, int P, const double* d_local_th,
+                         uint32_t* out_indexes, uint64_t* d_nidx, uint32_t* d_flags) {
+  static int cap = 0;
+  if (!cap) cap = resident_ctas(apply_kernel, kThreads, L.sms);
+  const uint32_t G = chunks_for((bound + kTileK - 1) / kTileK, cap, S.max_chunks);
+  apply_kernel<<<G, kThreads, 0, L.s>>>(u_idx, u_val, d_U, acc, zero_eps ? 1 : 0, w, P, d_local_th, S.sidx, S.counts,
+                                        S.chunk_cap, d_flags);
+  ++L.launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_compact<3>(L, S, G, 0, S.chunk_cap, false, nullptr, out_indexes, nullptr, d_nidx, nullptr);
+}
+
+// =============================================================================
+// K3: region merge — scatter (M1) + ordered bracket scan (M2)
+// =============================================================================
+__global__ void __launch_bounds__(kThreads)
+    scatter_kernel(Segs segs, uint64_t lo, uint64_t W, int P, uint32_t* mask, float* stage, uint32_t* d_flags) {
+  const uint64_t total = segs.start[segs.nseg];
+  const uint64_t stride = uint64_t(gridDim.x) * kThreads;
+  for (uint64_t e = uint64_t(blockIdx.x) * kThreads + threadIdx.x; e < total; e += stride) {
+    int sg = 0;
+    while (sg + 1 < segs.nseg && e >= segs.start[sg + 1]) ++sg;
+    const uint64_t entry = segs.ptr[sg][e - segs.start[sg]];
+    const uint64_t idx = coo_idx(entry);
+    if (idx < lo || idx - lo >= W) {
+      atomicOr(d_flags, 2u);
+      continue;
+    }
+    const uint64_t i = idx - lo;
+    const int src = segs.src[sg];
+    stage[i * uint64_t(P) + src] = coo_val(entry);
+    atomicOr(&mask[i >> 2], 1u << (unsigned(i & 3u) * 8u + unsigned(src)));
+  }
+}
+
+cudaError_t launch_scatter(Launch& L, const Segs& segs, uint64_t lo, uint64_t W, int P, uint32_t* mask,
+                           float* stage, uint32_t* d_flags) {
+  const uint64_t total = segs.start[segs.nseg];
+  if (total == 0) return cudaSuccess;
+  const int grid = int(std::min<uint64_t>((total + kThreads - 1) / kThreads, uint64_t(L.sms) * 16));
+  scatter_kernel<<<grid, kThreads, 0, L.s>>>(segs, lo, W, P, mask, stage, d_flags);
   ++L.launches;
   return cudaGetLastError();
 }
 
-cudaError_t launch_k1(Launch& L, K1Mode mode, const float* g, const float* eps_in, float* eps_out,
-                      float alpha, uint64_t n, const double* d_th, uint64_t* out, uint64_t* d_m,
-                      uint32_t* d_flags, uint32_t* d_hist) {
-  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-  bool vec = al(g);
-  if (mode != K1Mode::kSelect) vec = vec && al(eps_in) && al(eps_out);
-  switch (mode) {
-    case K1Mode::kSelect:
-      return k1_dispatch<false, true, false>(L, vec, g, eps_in, eps_out, alpha, n, d_th, out, d_m,
-                                             d_flags, d_hist);
-    case K1Mode::kAccumSelect:
-      return k1_dispatch<true, true, false>(L, vec, g, eps_in, eps_out, alpha, n, d_th, out, d_m,
-                                            d_flags, d_hist);
-    case K1Mode::kAccumHist:
-      return k1_dispatch<true, false, true>(L, vec, g, eps_in, eps_out, alpha, n, d_th, out, d_m,
-                                            d_flags, d_hist);
+// Fixed stride-doubling bracket over source ranks with absent pass-through
+// (sparse.cpp:238-245, tests/test_util.hpp:124-132):
+//   P=8: ((p0+p4)+(p2+p6)) + ((p1+p5)+(p3+p7))
+template <int P>
+__device__ __forceinline__ double bracket_sum(const float* st, uint32_t bits) {
+  double a[P];
+  bool h[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) {
+    h[q] = (bits >> q) & 1u;
+    a[q] = h[q] ? double(st[q]) : 0.0;
   }
+#pragma unroll
+  for (int s = P >> 1; s >= 1; s >>= 1) {
+#pragma unroll
+    for (int q = 0; q < s; ++q) {
+      if (h[q] && h[q + s]) a[q] = a[q] + a[q + s];
+      else if (h[q + s]) a[q] = a[q + s];
+      h[q] = h[q] || h[q + s];
+    }
+  }
+  return a[0];
+}
+
+template <int P, bool FILTER>
+__global__ void __launch_bounds__(kThreads)
+    region_scan_kernel(uint64_t lo, uint64_t W, uint32_t tiles, uint32_t tpc, uint32_t* mask,
+                       const float* __restrict__ stage, const double* d_gth, uint32_t* __restrict__ sidx,
+                       double* __restrict__ sval, uint32_t* counts) {
+  constexpr int C = 4, TILE = kJ * C * kThreads;
+  __shared__ uint32_t tbl[2][32];
+  const int tid = threadIdx.x;
+  const double gth = FILTER ? *d_gth : 0.0;
+  const uint64_t nwords = (W + 3) / 4;
+  const uint32_t t0 = blockIdx.x * tpc, t1 = min(t0 + tpc, tiles);
+  const uint64_t obase = uint64_t(blockIdx.x) * tpc * TILE;
+  uint32_t running = 0;
+  int parity = 0;
+  for (uint32_t tile = t0; tile < t1; ++tile, parity ^= 1) {
+    const uint64_t base = uint64_t(tile) * TILE;
+    double val[kJ][C];
+    bool pred[kJ][C];
+    unsigned bal[kJ][C];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const uint64_t wi = (base >> 2) + uint64_t(j) * kThreads + tid;
+      const uint32_t mw = wi < nwords ? mask[wi] : 0u;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const uint32_t bits = (mw >> (8 * c)) & 0xffu;
+        val[j][c] = 0.0;
+        bool p = false;
+        if (bits) {
+          val[j][c] = bracket_sum<P>(stage + (wi * 4 + c) * P, bits);
+          p = !FILTER || fabs(val[j][c]) >= gth;
+        }
+        pred[j][c] = p;
+        bal[j][c] = __ballot_sync(0xffffffffu, p);
+      }
+      if (mw) mask[wi] = 0u;
+    }
+    uint32_t grp[kJ];
+    const uint32_t total = tile_offsets<C>(tbl[parity], bal, grp);
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (pred[j][c]) {
+          const uint64_t pos = obase + running + grp[j] + rank_in_group<C>(bal, j, c);
+          sidx[pos] = uint32_t(lo + base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C + c);
+          sval[pos] = val[j][c];
+        }
+    }
+    running += total;
+  }
+  if (tid == 0) counts[blockIdx.x] = running;
+}
+
+template <int P, bool FILTER>
+static cudaError_t region_scan_dispatch(Launch& L, const Stage& S, uint64_t lo, uint64_t W, uint32_t* mask,
+                                        const float* stage, const double* d_gth, uint32_t* out_idx,
+                                        double* out_val, uint64_t* d_count) {
+  constexpr int TILE = kJ * 4 * kThreads;
+  const uint64_t tiles = (W + TILE - 1) / TILE;
+  if (tiles == 0) {
+    cudaMemsetAsync(d_count, 0, sizeof(uint64_t), L.s);
+    return cudaGetLastError();
+  }
+  static int cap = 0;
+  if (!cap) cap = resident_ctas(region_scan_kernel<P, FILTER>, kThreads, L.sms);
+  const uint32_t G = chunks_for(tiles, cap, S.max_chunks);
+  const uint32_t tpc = uint32_t((tiles + G - 1) / G);
+  region_scan_kernel<P, FILTER><<<G, kThreads, 0, L.s>>>(lo, W, uint32_t(tiles), tpc, mask, stage, d_gth, S.sidx,
+                                                         S.sval, S.counts);
+  ++L.launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_compact<2>(L, S, G, uint64_t(tpc) * TILE, nullptr, false, nullptr, out_idx, out_val, d_count,
+                           nullptr);
+}
+
+cudaError_t launch_region_scan(Launch& L, const Stage& S, int P, bool filter, uint64_t lo, uint64_t W,
+                               uint32_t* mask, const float* stage, const double* d_gth, uint32_t* out_idx,
+                               double* out_val, uint64_t* d_count) {
+#define OKT_RS(PP)                                                                                     \
+  return filter ? region_scan_dispatch<PP, true>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count) \
+                : region_scan_dispatch<PP, false>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count)
+  switch (P) {
+    case 1: OKT_RS(1);
+    case 2: OKT_RS(2);
+    case 4: OKT_RS(4);
+    case 8: OKT_RS(8);
+  }
+#undef OKT_RS
   return cudaErrorInvalidValue;
 }
 
@@ -343,342 +773,6 @@ cudaError_t launch_radix_select(Launch& L, RadixSrc src, const void* data, uint6
     ++L.launches;
   }
   return cudaGetLastError();
-}
-
-// =============================================================================
-// Survivor filter and K7 apply (COO lists with device-resident lengths)
-// =============================================================================
-template <bool AOS>
-__device__ __forceinline__ void load_coo4(const uint64_t* in_aos, const uint32_t* in_idx,
-                                          const double* in_val, uint64_t e0, uint64_t cnt,
-                                          uint32_t (&idx)[kC], double (&val)[kC],
-                                          bool (&valid)[kC]) {
-  if (e0 + kC <= cnt) {
-    if (AOS) {
-      const ulonglong2 p0 = *reinterpret_cast<const ulonglong2*>(in_aos + e0);
-      const ulonglong2 p1 = *reinterpret_cast<const ulonglong2*>(in_aos + e0 + 2);
-      const uint64_t ev[4] = {p0.x, p0.y, p1.x, p1.y};
-#pragma unroll
-      for (int c = 0; c < kC; ++c) {
-        idx[c] = coo_idx(ev[c]);
-        val[c] = double(coo_val(ev[c]));
-      }
-    } else {
-      const uint4 iv = *reinterpret_cast<const uint4*>(in_idx + e0);
-      const double2 v0 = *reinterpret_cast<const double2*>(in_val + e0);
-      const double2 v1 = *reinterpret_cast<const double2*>(in_val + e0 + 2);
-      idx[0] = iv.x; idx[1] = iv.y; idx[2] = iv.z; idx[3] = iv.w;
-      val[0] = v0.x; val[1] = v0.y; val[2] = v1.x; val[3] = v1.y;
-    }
-#pragma unroll
-    for (int c = 0; c < kC; ++c) valid[c] = true;
-  } else {
-#pragma unroll
-    for (int c = 0; c < kC; ++c) {
-      const uint64_t e = e0 + c;
-      valid[c] = e < cnt;
-      idx[c] = 0;
-      val[c] = 0.0;
-      if (valid[c]) {
-        if (AOS) {
-          idx[c] = coo_idx(in_aos[e]);
-          val[c] = double(coo_val(in_aos[e]));
-        } else {
-          idx[c] = in_idx[e];
-          val[c] = in_val[e];
-        }
-      }
-    }
-  }
-}
-
-template <bool AOS>
-__global__ void __launch_bounds__(kThreads)
-    filter_kernel(const uint64_t* __restrict__ in_aos, const uint32_t* __restrict__ in_idx,
-                  const double* __restrict__ in_val, const uint64_t* d_cnt_in,
-                  const double* d_th, uint32_t* __restrict__ out_idx,
-                  double* __restrict__ out_val, uint64_t* d_cnt_out, uint64_t* status,
-                  uint32_t epoch, uint32_t* ctr) {
-  __shared__ TileScanSmem s;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const uint64_t cnt = *d_cnt_in;
-  const double th = *d_th;
-  const uint32_t num_tiles = uint32_t((cnt + kTile - 1) / kTile);
-  if (num_tiles == 0 && blockIdx.x == 0 && tid == 0) *d_cnt_out = 0;
-  for (;;) {
-    const uint32_t tile = fetch_tile(ctr, s.tile);
-    if (tile >= num_tiles) break;
-    const uint64_t base = uint64_t(tile) * kTile;
-    uint32_t idx[kJ][kC];
-    double val[kJ][kC];
-    bool pred[kJ][kC];
-    unsigned bal[kJ][kC];
-#pragma unroll
-    for (int j = 0; j < kJ; ++j) {
-      bool valid[kC];
-      load_coo4<AOS>(in_aos, in_idx, in_val, base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC,
-                     cnt, idx[j], val[j], valid);
-#pragma unroll
-      for (int c = 0; c < kC; ++c) {
-        pred[j][c] = valid[c] && fabs(val[j][c]) >= th;
-        bal[j][c] = __ballot_sync(0xffffffffu, pred[j][c]);
-      }
-    }
-    tile_scan<kC>(s, bal, tile, num_tiles, status, epoch, d_cnt_out);
-#pragma unroll
-    for (int j = 0; j < kJ; ++j) {
-      const uint32_t gbase = s.base + s.cnt[j * kWarps + warp];
-#pragma unroll
-      for (int c = 0; c < kC; ++c)
-        if (pred[j][c]) {
-          const uint32_t pos = gbase + rank_in_group<kC>(bal, j, c);
-          out_idx[pos] = idx[j][c];
-          out_val[pos] = val[j][c];
-        }
-    }
-  }
-  retire_cta(ctr);
-}
-
-cudaError_t launch_filter(Launch& L, bool aos, const uint64_t* in_aos, const uint32_t* in_idx,
-                          const double* in_val, const uint64_t* d_cnt_in, uint64_t bound,
-                          const double* d_th, uint32_t* out_idx, double* out_val,
-                          uint64_t* d_cnt_out) {
-  const uint64_t tiles = std::max<uint64_t>(1, (bound + kTile - 1) / kTile);
-  static int cap_a = 0, cap_s = 0;
-  int& cap = aos ? cap_a : cap_s;
-  if (!cap) cap = aos ? resident_ctas(filter_kernel<true>, kThreads, L.sms)
-                      : resident_ctas(filter_kernel<false>, kThreads, L.sms);
-  const int grid = int(std::min<uint64_t>(tiles, uint64_t(cap)));
-  const uint32_t ep = L.next_epoch();
-  if (aos)
-    filter_kernel<true><<<grid, kThreads, 0, L.s>>>(in_aos, in_idx, in_val, d_cnt_in, d_th, out_idx,
-                                                    out_val, d_cnt_out, L.status, ep, L.ctr);
-  else
-    filter_kernel<false><<<grid, kThreads, 0, L.s>>>(in_aos, in_idx, in_val, d_cnt_in, d_th, out_idx,
-                                                     out_val, d_cnt_out, L.status, ep, L.ctr);
-  ++L.launches;
-  return cudaGetLastError();
-}
-
-__global__ void __launch_bounds__(kThreads)
-    apply_kernel(const uint32_t* __restrict__ u_idx, const double* __restrict__ u_val,
-                 const uint64_t* d_U, float* acc, int zero_eps, float* w, int P,
-                 const double* d_local_th, uint32_t* __restrict__ out_indexes, uint64_t* d_nidx,
-                 uint32_t* d_flags, uint64_t* status, uint32_t epoch, uint32_t* ctr) {
-  __shared__ TileScanSmem s;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  // A step whose input was non-finite applies nothing (the reference throws
-  // before touching the residual or the model).
-  const bool skip = (*d_flags & 1u) != 0;
-  const uint64_t cnt = skip ? 0 : *d_U;
-  const float tf = ceil_to_float(*d_local_th);
-  const double dP = double(P);
-  const uint32_t num_tiles = uint32_t((cnt + kTile - 1) / kTile);
-  if (num_tiles == 0 && blockIdx.x == 0 && tid == 0) *d_nidx = 0;
-  bool bad = false;
-  for (;;) {
-    const uint32_t tile = fetch_tile(ctr, s.tile);
-    if (tile >= num_tiles) break;
-    const uint64_t base = uint64_t(tile) * kTile;
-    uint32_t idx[kJ][kC];
-    double val[kJ][kC];
-    bool pred[kJ][kC];
-    unsigned bal[kJ][kC];
-#pragma unroll
-    for (int j = 0; j < kJ; ++j) {
-      bool valid[kC];
-      load_coo4<false>(nullptr, u_idx, u_val, base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC,
-                       cnt, idx[j], val[j], valid);
-#pragma unroll
-      for (int c = 0; c < kC; ++c) {
-        bool sel = false;
-        if (valid[c]) {
-          const uint32_t i = idx[j][c];
-          sel = fabsf(acc[i]) >= tf;
-          if (w) {
-            const float nw = float(double(w[i]) - val[j][c] / dP);
-            w[i] = nw;
-            bad |= nonfinite(nw);
-          }
-          if (zero_eps && sel) acc[i] = 0.f;
-        }
-        pred[j][c] = sel;
-        bal[j][c] = __ballot_sync(0xffffffffu, sel);
-      }
-    }
-    tile_scan<kC>(s, bal, tile, num_tiles, status, epoch, d_nidx);
-#pragma unroll
-    for (int j = 0; j < kJ; ++j) {
-      const uint32_t gbase = s.base + s.cnt[j * kWarps + warp];
-#pragma unroll
-      for (int c = 0; c < kC; ++c)
-        if (pred[j][c]) out_indexes[gbase + rank_in_group<kC>(bal, j, c)] = idx[j][c];
-    }
-  }
-  if (__syncthreads_or(bad) && tid == 0) atomicOr(d_flags, 4u);
-  retire_cta(ctr);
-}
-
-cudaError_t launch_apply(Launch& L, const uint32_t* u_idx, const double* u_val, const uint64_t* d_U,
-                         uint64_t bound, float* acc, bool zero_eps, float* w, int P,
-                         const double* d_local_th, uint32_t* out_indexes, uint64_t* d_nidx,
-                         uint32_t* d_flags) {
-  const uint64_t tiles = std::max<uint64_t>(1, (bound + kTile - 1) / kTile);
-  static int cap = 0;
-  if (!cap) cap = resident_ctas(apply_kernel, kThreads, L.sms);
-  const int grid = int(std::min<uint64_t>(tiles, uint64_t(cap)));
-  const uint32_t ep = L.next_epoch();
-  apply_kernel<<<grid, kThreads, 0, L.s>>>(u_idx, u_val, d_U, acc, zero_eps ? 1 : 0, w, P, d_local_th,
-                                           out_indexes, d_nidx, d_flags, L.status, ep, L.ctr);
-  ++L.launches;
-  return cudaGetLastError();
-}
-
-// =============================================================================
-// K3: region merge — scatter (M1) + ordered bracket scan (M2)
-// =============================================================================
-__global__ void __launch_bounds__(kThreads)
-    scatter_kernel(Segs segs, uint64_t lo, uint64_t W, int P, uint32_t* mask, float* stage,
-                   uint32_t* d_flags) {
-  const uint64_t total = segs.start[segs.nseg];
-  const uint64_t stride = uint64_t(gridDim.x) * kThreads;
-  for (uint64_t e = uint64_t(blockIdx.x) * kThreads + threadIdx.x; e < total; e += stride) {
-    int sg = 0;
-    while (sg + 1 < segs.nseg && e >= segs.start[sg + 1]) ++sg;
-    const uint64_t entry = segs.ptr[sg][e - segs.start[sg]];
-    const uint64_t idx = coo_idx(entry);
-    if (idx < lo || idx - lo >= W) {
-      atomicOr(d_flags, 2u);
-      continue;
-    }
-    const uint64_t i = idx - lo;
-    const int src = segs.src[sg];
-    stage[i * uint64_t(P) + src] = coo_val(entry);
-    atomicOr(&mask[i >> 2], 1u << (unsigned(i & 3u) * 8u + unsigned(src)));
-  }
-}
-
-cudaError_t launch_scatter(Launch& L, const Segs& segs, uint64_t lo, uint64_t W, int P,
-                           uint32_t* mask, float* stage, uint32_t* d_flags) {
-  const uint64_t total = segs.start[segs.nseg];
-  if (total == 0) return cudaSuccess;
-  const int grid = int(std::min<uint64_t>((total + kThreads - 1) / kThreads, uint64_t(L.sms) * 16));
-  scatter_kernel<<<grid, kThreads, 0, L.s>>>(segs, lo, W, P, mask, stage, d_flags);
-  ++L.launches;
-  return cudaGetLastError();
-}
-
-// Fixed stride-doubling bracket over source ranks with absent pass-through
-// (sparse.cpp:238-245, tests/test_util.hpp:124-132):
-//   P=8: ((p0+p4)+(p2+p6)) + ((p1+p5)+(p3+p7))
-template <int P>
-__device__ __forceinline__ double bracket_sum(const float* st, uint32_t bits) {
-  double a[P];
-  bool h[P];
-#pragma unroll
-  for (int q = 0; q < P; ++q) {
-    h[q] = (bits >> q) & 1u;
-    a[q] = h[q] ? double(st[q]) : 0.0;
-  }
-#pragma unroll
-  for (int s = P >> 1; s >= 1; s >>= 1) {
-#pragma unroll
-    for (int q = 0; q < s; ++q) {
-      if (h[q] && h[q + s]) a[q] = a[q] + a[q + s];
-      else if (h[q + s]) a[q] = a[q + s];
-      h[q] = h[q] || h[q + s];
-    }
-  }
-  return a[0];
-}
-
-template <int P, bool FILTER>
-__global__ void __launch_bounds__(kThreads)
-    region_scan_kernel(uint64_t lo, uint64_t W, uint32_t num_tiles, uint32_t* mask,
-                       const float* __restrict__ stage, const double* d_gth,
-                       uint32_t* __restrict__ out_idx, double* __restrict__ out_val,
-                       uint64_t* d_count, uint64_t* status, uint32_t epoch, uint32_t* ctr) {
-  __shared__ TileScanSmem s;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const double gth = FILTER ? *d_gth : 0.0;
-  const uint64_t nwords = (W + 3) / 4;
-  for (;;) {
-    const uint32_t tile = fetch_tile(ctr, s.tile);
-    if (tile >= num_tiles) break;
-    const uint64_t base = uint64_t(tile) * kTile;
-    double val[kJ][kC];
-    bool pred[kJ][kC];
-    unsigned bal[kJ][kC];
-#pragma unroll
-    for (int j = 0; j < kJ; ++j) {
-      const uint64_t wi = (base >> 2) + uint64_t(j) * kThreads + tid;
-      const uint32_t mw = wi < nwords ? mask[wi] : 0u;
-#pragma unroll
-      for (int c = 0; c < kC; ++c) {
-        const uint32_t bits = (mw >> (8 * c)) & 0xffu;
-        val[j][c] = 0.0;
-        bool p = false;
-        if (bits) {
-          val[j][c] = bracket_sum<P>(stage + (wi * 4 + c) * P, bits);
-          p = !FILTER || fabs(val[j][c]) >= gth;
-        }
-        pred[j][c] = p;
-        bal[j][c] = __ballot_sync(0xffffffffu, p);
-      }
-      if (mw) mask[wi] = 0u;
-    }
-    tile_scan<kC>(s, bal, tile, num_tiles, status, epoch, d_count);
-#pragma unroll
-    for (int j = 0; j < kJ; ++j) {
-      const uint32_t gbase = s.base + s.cnt[j * kWarps + warp];
-#pragma unroll
-      for (int c = 0; c < kC; ++c)
-        if (pred[j][c]) {
-          const uint32_t pos = gbase + rank_in_group<kC>(bal, j, c);
-          out_idx[pos] = uint32_t(lo + base + uint64_t(j) * (kC * kThreads) + uint64_t(tid) * kC + c);
-          out_val[pos] = val[j][c];
-        }
-    }
-  }
-  retire_cta(ctr);
-}
-
-template <int P, bool FILTER>
-static cudaError_t region_scan_dispatch(Launch& L, uint64_t lo, uint64_t W, uint32_t* mask,
-                                        const float* stage, const double* d_gth, uint32_t* out_idx,
-                                        double* out_val, uint64_t* d_count) {
-  const uint32_t tiles = uint32_t((W + kTile - 1) / kTile);
-  if (tiles == 0) {
-    cudaMemsetAsync(d_count, 0, sizeof(uint64_t), L.s);
-    return cudaGetLastError();
-  }
-  static int cap = 0;
-  if (!cap) cap = resident_ctas(region_scan_kernel<P, FILTER>, kThreads, L.sms);
-  const int grid = int(std::min<uint64_t>(tiles, uint64_t(cap)));
-  const uint32_t ep = L.next_epoch();
-  region_scan_kernel<P, FILTER><<<grid, kThreads, 0, L.s>>>(lo, W, tiles, mask, stage, d_gth, out_idx,
-                                                            out_val, d_count, L.status, ep, L.ctr);
-  ++L.launches;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_region_scan(Launch& L, int P, bool filter, uint64_t lo, uint64_t W,
-                               uint32_t* mask, const float* stage, const double* d_gth,
-                               uint32_t* out_idx, double* out_val, uint64_t* d_count) {
-#define OKT_RS(PP)                                                                              \
-  return filter ? region_scan_dispatch<PP, true>(L, lo, W, mask, stage, d_gth, out_idx, out_val, \
-                                                 d_count)                                       \
-                : region_scan_dispatch<PP, false>(L, lo, W, mask, stage, d_gth, out_idx, out_val, \
-                                                  d_count)
-  switch (P) {
-    case 1: OKT_RS(1);
-    case 2: OKT_RS(2);
-    case 4: OKT_RS(4);
-    case 8: OKT_RS(8);
-  }
-#undef OKT_RS
-  return cudaErrorInvalidValue;
 }
 
 // =============================================================================

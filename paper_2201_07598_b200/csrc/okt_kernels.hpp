@@ -6,15 +6,11 @@
 
 namespace okt {
 
-// Per-comm launch context: stream, look-back scratch, launch accounting.
+// Per-comm launch context: stream and launch accounting.
 struct Launch {
   cudaStream_t s = nullptr;
-  uint64_t* status = nullptr;   // look-back status words (one per tile)
-  uint32_t* ctr = nullptr;      // dynamic tile counter pair
-  uint32_t epoch = 0;           // bumped per look-back launch
   uint64_t launches = 0;        // kernels launched through this context
   int sms = 148;
-  uint32_t next_epoch() { epoch = (epoch + 1) & 0x3fffffffu; if (!epoch) epoch = 1; return epoch; }
 };
 
 struct RadixState {
@@ -26,6 +22,35 @@ struct RadixState {
 
 enum class K1Mode { kSelect, kAccumSelect, kAccumHist };
 enum class RadixSrc { kDenseF32, kAosF32, kF64 };
+
+// Phase-A staging of the two-phase compactions (okt_device.cuh).
+struct Stage {
+  uint64_t* s64 = nullptr;      // AoS staging (u32 idx | f32 val << 32)
+  uint32_t* sidx = nullptr;     // SoA staging indices
+  double* sval = nullptr;       // SoA staging values
+  uint32_t* counts = nullptr;   // per-chunk emitted counts
+  uint32_t* counts2 = nullptr;  // per-chunk secondary counts (K1 dual threshold)
+  uint64_t* chunk_cap = nullptr;  // device-computed chunk capacity (entries)
+  int max_chunks = 0;
+};
+// Staging entries needed for a pass over `count` elements in tiles of `tile`.
+size_t stage_entries(uint64_t count, int tile, int max_chunks);
+constexpr int kK1Tile = 4096;   // K1 / region-scan tile (elements)
+constexpr int kCooTile = 1024;  // O(k) passes tile (entries)
+
+// Output of a compaction: AoS u64 entries or SoA (u32 idx, f64 val).
+struct OutCoo {
+  uint64_t* aos = nullptr;
+  uint32_t* idx = nullptr;
+  double* val = nullptr;
+};
+
+// Fused K7 for the single-rank path (every entry of u is locally selected).
+struct ApplyArgs {
+  float* acc = nullptr;   // residual buffer holding acc; zeroed at u's indices
+  float* w = nullptr;     // model; w[i] -= u_i
+  uint32_t* d_flags = nullptr;
+};
 
 // Split-phase receive segments for the region scatter (M1): one per source.
 struct Segs {
@@ -40,10 +65,13 @@ struct Segs {
 //   kSelect       acc = g,                       emit {|acc| >= th}
 //   kAccumSelect  acc = fma(alpha, g, eps_in) -> eps_out, emit {|acc| >= th}
 //   kAccumHist    acc = fma(alpha, g, eps_in) -> eps_out, radix pass-0 histogram
+// With d_th2 (dual threshold) the emitted set is {|acc| >= max(th, th2)} and
+// *d_m2 receives |{|acc| >= th}| (P = 1 steady state: u straight from K1).
 // Sets bit 0 of *d_flags on any non-finite accumulator.
-cudaError_t launch_k1(Launch& L, K1Mode mode, const float* g, const float* eps_in,
-                      float* eps_out, float alpha, uint64_t n, const double* d_th,
-                      uint64_t* out, uint64_t* d_m, uint32_t* d_flags, uint32_t* d_hist);
+cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, const float* eps_in,
+                      float* eps_out, float alpha, uint64_t n, const double* d_th, const double* d_th2,
+                      const OutCoo& out, uint64_t* d_m, uint64_t* d_m2, uint32_t* d_flags,
+                      uint32_t* d_hist, const ApplyArgs* ap = nullptr);
 
 // K2/K4: exact k-th largest magnitude (k clamped to the element count) by MSD
 // radix select on the IEEE bit patterns; writes the threshold to *d_th_out
@@ -59,14 +87,15 @@ cudaError_t launch_radix_init(Launch& L, RadixState* d_rs, uint64_t k, uint64_t 
 
 // Survivor filter: {(i, v) : |v| >= *d_th} of a COO list whose length lives in
 // device memory.  Input is AoS (u32 idx, f32 val) or SoA (u32, f64).
-cudaError_t launch_filter(Launch& L, bool aos, const uint64_t* in_aos,
+cudaError_t launch_filter(Launch& L, const Stage& S, bool aos, const uint64_t* in_aos,
                           const uint32_t* in_idx, const double* in_val,
                           const uint64_t* d_cnt_in, uint64_t bound, const double* d_th,
-                          uint32_t* out_idx, double* out_val, uint64_t* d_cnt_out);
+                          uint32_t* out_idx, double* out_val, uint64_t* d_cnt_out,
+                          const ApplyArgs* ap = nullptr);
 
 // K7: for each (i, v) of u: sel = |acc[i]| >= local_th; if w: w[i] -= v / P;
 // if zero_eps && sel: acc[i] = 0; emit i into indexes when sel.
-cudaError_t launch_apply(Launch& L, const uint32_t* u_idx, const double* u_val,
+cudaError_t launch_apply(Launch& L, const Stage& S, const uint32_t* u_idx, const double* u_val,
                          const uint64_t* d_U, uint64_t bound, float* acc, bool zero_eps,
                          float* w, int P, const double* d_local_th, uint32_t* out_indexes,
                          uint64_t* d_nidx, uint32_t* d_flags);
@@ -77,7 +106,7 @@ cudaError_t launch_scatter(Launch& L, const Segs& segs, uint64_t lo, uint64_t W,
                            uint32_t* mask, float* stage, uint32_t* d_flags);
 // K3 (M2): ordered scan of the owned region: bracket-sum the present sources in
 // fp64, keep explicit zeros, optionally filter by |sum| >= *d_gth, clear mask.
-cudaError_t launch_region_scan(Launch& L, int P, bool filter, uint64_t lo, uint64_t W,
+cudaError_t launch_region_scan(Launch& L, const Stage& S, int P, bool filter, uint64_t lo, uint64_t W,
                                uint32_t* mask, const float* stage, const double* d_gth,
                                uint32_t* out_idx, double* out_val, uint64_t* d_count);
 

@@ -360,3 +360,27 @@ def test_sgd_trajectory_exact_sum(okm, oracle, gpus, P):
             assert np.array_equal(res[r].eps(w.ctx(r)), eps[r]), (t, r, "residual")
             wm = models[r].w.cpu().numpy().astype(np.float64)
             assert np.array_equal(wm, ws[r]), (t, r, "model")
+
+
+# ---- golden vectors produced by the reference itself (tests/golden) ----
+from . import _golden  # noqa: E402
+
+
+@pytest.mark.parametrize("name", _golden.cases())
+def test_gpu_reproduces_reference_golden(okm, gpus, name):
+    fx = _golden.load(name)
+    P = int(fx["P"])
+    w = gpu_world(okm, P, gpus)
+    st = [okm.OkState(okm.ThresholdState(tau=int(fx["tau"]), tau_prime=int(fx["tau_prime"])),
+                      bucket_size=int(fx["bucket"])) for _ in range(P)]
+    prev = np.zeros((P, 6, 4), np.uint64)
+    for t in fx["ts"]:
+        t = int(t)
+        ins = fx[f"in_t{t}"]
+        got = okm.run_ranks(w, lambda ctx: okm.ok_sparse_allreduce(ctx, st[ctx.rank], ins[ctx.rank], t, int(fx["k"])))
+        led = ledger_array(w, P)
+        _golden.check_step(fx, t, P, got[0].u.indices, got[0].u.values, [g.indexes for g in got],
+                           [g.local_selected for g in got], led - prev)
+        prev = led
+        for r in range(1, P):
+            assert got[r].u == got[0].u
