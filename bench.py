@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--ring", type=int, default=8, help="distinct gradient snapshots cycled per rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=32)
+    ap.add_argument("--trace", default="", help="directory: dump a CUPTI timeline (torch.profiler) of 16 steps")
     return ap.parse_args()
 
 
@@ -163,6 +164,32 @@ def _cpu_model() -> str:
     return "unknown"
 
 
+def trace_steps(args, rank, stream, step, t0):
+    """CUPTI timeline of 16 steps: per-kernel device time and the idle gaps
+    between them (host launch / sync latency), written next to a chrome trace."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    os.makedirs(args.trace, exist_ok=True)
+    with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+        for i in range(16):
+            step(t0 + 1 + i)
+        torch.cuda.synchronize()
+    prof.export_chrome_trace(os.path.join(args.trace, f"trace_rank{rank}.json"))
+    ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    ev.sort(key=lambda e: e.time_range.start)
+    per = {}
+    for e in ev:
+        d = per.setdefault(e.name[:60], [0, 0.0])
+        d[0] += 1
+        d[1] += e.time_range.elapsed_us()
+    span = (ev[-1].time_range.end - ev[0].time_range.start) if ev else 0
+    busy = sum(e.time_range.elapsed_us() for e in ev)
+    with open(os.path.join(args.trace, f"summary_rank{rank}.txt"), "w") as f:
+        f.write(f"16 steps: device span {span:.1f} us, kernel+copy busy {busy:.1f} us\n")
+        for k, (c, us) in sorted(per.items(), key=lambda kv: -kv[1][1]):
+            f.write(f"{c:5d} {us / 16:9.2f} us/step  {k}\n")
+
+
 # ---- our arm ------------------------------------------------------------------------
 def run_okt(args):
     import torch
@@ -229,6 +256,9 @@ def run_okt(args):
         t += 1
         step(t)
     barrier()
+    if args.trace:
+        trace_steps(args, rank, stream, step, t)
+        t += 16
     # ---- timed device-resident run
     L.okt_set_profiling(comm, 1)
     L.okt_reset_phase_times(comm)

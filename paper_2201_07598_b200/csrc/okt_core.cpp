@@ -1005,6 +1005,7 @@ int okt_sgd_step(okt_comm* c, const float* d_grad, float* d_w, size_t n, double 
 // ---- host-buffer entry points --------------------------------------------------------
 static int copy_result_to_host(okt_comm* c, const okt_result& r, uint32_t* h_idx, double* h_val,
                                uint32_t* h_indexes, size_t cap, cudaStream_t s) {
+  if (!h_idx && !h_val && !h_indexes) return OKT_OK;  // result stays on the device
   if (r.u.nnz > cap) return set_err(OKT_ERR_INVALID_ARGUMENT, "u does not fit the host buffers");
   cudaError_t e = cudaSuccess;
   if (r.u.nnz && h_idx) e = cudaMemcpyAsync(h_idx, r.u.d_idx, 4 * r.u.nnz, cudaMemcpyDeviceToHost, s);

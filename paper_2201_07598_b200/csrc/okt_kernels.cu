@@ -60,6 +60,8 @@ size_t stage_entries(uint64_t count, int tile, int max_chunks) {
 // APPLY (P = 1, where every entry of u is also in the local selection): fuse
 // K7 into the copy — w[i] -= v, acc[i] = 0 — so the single-rank step needs no
 // separate apply pass; `indexes` is then u's index array itself.
+constexpr int kCompactBatch = 2;
+
 template <int MODE, bool APPLY>
 __global__ void __launch_bounds__(kThreads)
     compact_kernel(const uint64_t* __restrict__ s64, const uint32_t* __restrict__ sidx,
@@ -69,40 +71,71 @@ __global__ void __launch_bounds__(kThreads)
                    uint64_t* d_total, uint64_t* d_total2, ApplyArgs ap) {
   __shared__ uint64_t red[kWarps];
   const int c = blockIdx.x, G = gridDim.x;
-  uint64_t pre = 0;
-  for (int q = threadIdx.x; q < c; q += kThreads) pre += counts[q];
-  pre = block_sum(pre, red);
   const uint64_t cnt = counts[c];
   const uint64_t cap = d_cap ? *d_cap : cap_host;
   const uint64_t src = uint64_t(c) * cap;
+  // The first kCompactBatch entries of each thread are loaded (and, for the
+  // fused apply, their model / residual words gathered) before the chunk
+  // prefix is known: only the output positions depend on it.
+  constexpr int B = kCompactBatch;
+  uint64_t e64[B];
+  uint32_t ei[B];
+  double ev[B];
+  float wv[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const uint64_t j = threadIdx.x + uint64_t(b) * kThreads;
+    e64[b] = 0;
+    ei[b] = 0;
+    ev[b] = 0.0;
+    wv[b] = 0.f;
+    if (j < cnt) {
+      if (MODE == 0 || MODE == 1) e64[b] = s64[src + j];
+      if (MODE == 2 || MODE == 3) ei[b] = sidx[src + j];
+      if (MODE == 2) ev[b] = sval[src + j];
+      if (MODE == 1) {
+        ei[b] = coo_idx(e64[b]);
+        ev[b] = double(coo_val(e64[b]));
+      }
+      if (APPLY) wv[b] = ap.w[ei[b]];
+    }
+  }
+  uint64_t pre = 0;
+  for (int q = threadIdx.x; q < c; q += kThreads) pre += counts[q];
+  pre = block_sum(pre, red);
   const bool skip = APPLY && (*ap.d_flags & 1u);  // non-finite step: touch nothing
   bool bad = false;
-  for (uint64_t j = threadIdx.x; j < cnt; j += kThreads) {
-    uint32_t i = 0;
-    double v = 0.0;
-    if (MODE == 0) {
-      o64[pre + j] = s64[src + j];
-    } else if (MODE == 1) {
-      const uint64_t e = s64[src + j];
-      i = coo_idx(e);
-      v = double(coo_val(e));
+  auto emit = [&](uint64_t j, uint64_t e, uint32_t i, double v, float w_old) {
+    if (MODE == 0) o64[pre + j] = e;
+    else if (MODE == 3) oidx[pre + j] = i;
+    else {
       oidx[pre + j] = i;
       oval[pre + j] = v;
-    } else if (MODE == 2) {
-      i = sidx[src + j];
-      v = sval[src + j];
-      oidx[pre + j] = i;
-      oval[pre + j] = v;
-    } else {
-      oidx[pre + j] = sidx[src + j];
     }
     if (APPLY && !skip) {
-      const float wi = ap.w[i];
-      const float nw = float(double(wi) - v);
+      const float nw = float(double(w_old) - v);
       ap.w[i] = nw;
       ap.acc[i] = 0.f;
       bad |= (__float_as_uint(nw) & 0x7f800000u) == 0x7f800000u;
     }
+  };
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const uint64_t j = threadIdx.x + uint64_t(b) * kThreads;
+    if (j < cnt) emit(j, e64[b], ei[b], ev[b], wv[b]);
+  }
+  for (uint64_t j = threadIdx.x + uint64_t(B) * kThreads; j < cnt; j += kThreads) {
+    uint64_t e = 0;
+    uint32_t i = 0;
+    double v = 0.0;
+    if (MODE == 0 || MODE == 1) e = s64[src + j];
+    if (MODE == 1) {
+      i = coo_idx(e);
+      v = double(coo_val(e));
+    }
+    if (MODE == 2 || MODE == 3) i = sidx[src + j];
+    if (MODE == 2) v = sval[src + j];
+    emit(j, e, i, v, APPLY ? ap.w[i] : 0.f);
   }
   if (APPLY && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(ap.d_flags, 4u);
   if (c == G - 1) {
