@@ -53,6 +53,7 @@ inline void check(int status) {
 }
 
 struct Binding {
+  int P = 0;
   okt_world* world = nullptr;
   std::vector<okt_comm*> comms;
   std::vector<okt_counters> seen;  // ledger already credited, per rank * phase
@@ -74,8 +75,10 @@ inline std::map<const oklab::Transport*, std::unique_ptr<Binding>>& bindings() {
 inline okt_comm* comm_for(const oklab::WorkerCtx& ctx, Binding** out) {
   std::lock_guard<std::mutex> lk(mu());
   auto& slot = bindings()[ctx.transport];
+  if (slot && slot->P != ctx.world) slot.reset();  // a new transport reused the address
   if (!slot) {
     slot.reset(new Binding());
+    slot->P = ctx.world;
     int ndev = 1;
     cudaGetDeviceCount(&ndev);
     std::vector<int> dev(ctx.world);
@@ -150,6 +153,14 @@ inline oklab::OkAllreduceResult to_result(const okt_result& r, std::size_t n) {
 }
 
 }  // namespace detail
+
+// Releases the device comms bound to `transport` (call before destroying it;
+// otherwise a later transport allocated at the same address would inherit
+// them).
+inline void release(const oklab::Transport* transport) {
+  std::lock_guard<std::mutex> lk(detail::mu());
+  detail::bindings().erase(transport);
+}
 
 // Drop-in for oklab::ok_sparse_allreduce (oktopk.hpp:118-120).
 inline oklab::OkAllreduceResult ok_sparse_allreduce(const oklab::WorkerCtx& ctx, oklab::OkState& state,

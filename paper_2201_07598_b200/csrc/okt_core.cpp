@@ -25,6 +25,8 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -115,6 +117,35 @@ okt_state default_state() {
   return s;
 }
 
+// Symmetric P2P window layout (identical on every rank for a given n).
+struct WinLayout {
+  size_t L[2], sidx[2], sval[2], uidx[2], uval[2], bytes;
+};
+WinLayout win_layout(size_t n) {
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  WinLayout w;
+  size_t o = al(sizeof(okt::P2PHdr));
+  for (int p = 0; p < 2; ++p) { w.L[p] = o; o += al(8 * n); }
+  for (int p = 0; p < 2; ++p) { w.sidx[p] = o; o += al(4 * n); }
+  for (int p = 0; p < 2; ++p) { w.sval[p] = o; o += al(8 * n); }
+  for (int p = 0; p < 2; ++p) { w.uidx[p] = o; o += al(4 * n); }
+  for (int p = 0; p < 2; ++p) { w.uval[p] = o; o += al(8 * n); }
+  w.bytes = o;
+  return w;
+}
+
+// What every rank contributes to the P2P bootstrap allgather.
+struct WinInfo {
+  uint64_t pid;
+  uint64_t base;
+  cudaIpcMemHandle_t handle;
+  unsigned char uuid[16];
+  int32_t device;
+  int32_t ok;
+};
+
+constexpr uint64_t kP2PTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
 }  // namespace
 
 // =============================================================================
@@ -147,6 +178,14 @@ struct okt_comm {
   Buf counts, counts2, chunkcap;
   Buf hist, scal;
   okt::Stage S;
+  // device-driven multi-GPU exchange (okt_p2p.cuh)
+  bool p2p_checked = false, p2p = false;
+  Buf win, planb, boot, tabd, pdone, plt;
+  size_t win_n = 0;
+  okt::PeerTab tab{};
+  std::vector<void*> ipc_open;
+  uint64_t p2p_epoch = 0;
+  okt::P2PPlan* hplan = nullptr;  // pinned mirror of the device plan
   DevScalars* h = nullptr;   // pinned download mirror
   DevScalars* hup = nullptr; // pinned upload staging
   size_t cap_n = 0;
@@ -246,7 +285,8 @@ struct okt_comm {
     if (n <= cap_n) return OKT_OK;
     cudaError_t e = cudaSuccess;
     const size_t k1_stage = okt::stage_entries(n, okt::kK1Tile, S.max_chunks);
-    const size_t coo_stage = std::max(okt::stage_entries(n, okt::kCooTile, S.max_chunks), k1_stage);
+    const size_t coo_stage = std::max({okt::stage_entries(n, okt::kCooTile, S.max_chunks), k1_stage,
+                                       okt::stage_entries(n, okt::kRegionTileHost, S.max_chunks)});
     if (e == cudaSuccess) e = coo.ensure(8 * n);
     if (e == cudaSuccess) e = st64.ensure(8 * k1_stage);
     if (e == cudaSuccess) e = stidx.ensure(4 * coo_stage);
@@ -524,6 +564,190 @@ struct okt_comm {
     return OKT_OK;
   }
 
+  // ---- P2P window bootstrap (collective) ---------------------------------------------------
+  int allgather_host(const void* mine, void* all, size_t bytes, cudaStream_t s) {
+    int rc;
+    if ((rc = ensure(boot, bytes * (P + 1)))) return rc;
+    char* b = boot.as<char>();
+    if ((rc = ck(cudaMemcpyAsync(b + bytes * P, mine, bytes, cudaMemcpyHostToDevice, s), "h2d"))) return rc;
+    std::string err;
+    rc = tr->allgather(b + bytes * P, b, bytes, s, err);
+    if (rc) return comm_err(rc, err);
+    if ((rc = ck(cudaMemcpyAsync(all, b, bytes * P, cudaMemcpyDeviceToHost, s), "d2h"))) return rc;
+    return ck(cudaStreamSynchronize(s), "sync");
+  }
+
+  void close_peers() {
+    for (void* p : ipc_open) cudaIpcCloseMemHandle(p);
+    ipc_open.clear();
+  }
+
+  // Maps every peer's window when all ranks sit on distinct, peer-accessible
+  // GPUs; otherwise the exchanges stay on the host-synchronised transport.
+  // Collective: every rank calls it with the same n.
+  int setup_p2p(size_t n, cudaStream_t s) {
+    if (P == 1 || (p2p_checked && !p2p) || (p2p && win_n >= n)) return OKT_OK;
+    if (std::getenv("OKT_DISABLE_P2P")) {
+      p2p_checked = true;
+      return OKT_OK;
+    }
+    int rc;
+    int one = 1;
+    std::vector<int> ones(P);
+    close_peers();
+    if ((rc = allgather_host(&one, ones.data(), sizeof(int), s))) return rc;  // peers closed my old window
+    const WinLayout lay = win_layout(n);
+    win.zero_init = false;
+    if (win.p) {
+      cudaFree(win.p);
+      win.p = nullptr;
+      win.cap = 0;
+    }
+    if ((rc = ensure(win, lay.bytes))) return rc;
+    if ((rc = ck(cudaMemset(win.p, 0, sizeof(okt::P2PHdr)), "memset"))) return rc;
+    WinInfo me{};
+    me.pid = uint64_t(getpid());
+    me.base = reinterpret_cast<uint64_t>(win.p);
+    me.device = device;
+    me.ok = cudaIpcGetMemHandle(&me.handle, win.p) == cudaSuccess;
+    cudaGetLastError();
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) std::memcpy(me.uuid, prop.uuid.bytes, 16);
+    std::vector<WinInfo> all(P);
+    if ((rc = allgather_host(&me, all.data(), sizeof(WinInfo), s))) return rc;
+    bool ok = me.ok != 0;
+    std::vector<char*> base(P, nullptr);
+    base[rank] = win.as<char>();
+    for (int q = 0; q < P && ok; ++q) {
+      if (q == rank) continue;
+      if (!all[q].ok || std::memcmp(all[q].uuid, me.uuid, 16) == 0) {
+        ok = false;  // a shared GPU: in-kernel cross-rank waits are not safe there
+        break;
+      }
+      if (all[q].pid == me.pid) {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, device, all[q].device);
+        if (!can) {
+          ok = false;
+          break;
+        }
+        const cudaError_t e = cudaDeviceEnablePeerAccess(all[q].device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ok = false;
+        cudaGetLastError();
+        base[q] = reinterpret_cast<char*>(all[q].base);
+      } else {
+        void* ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, all[q].handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          cudaGetLastError();
+          ok = false;
+          break;
+        }
+        ipc_open.push_back(ptr);
+        base[q] = static_cast<char*>(ptr);
+      }
+    }
+    int mine_ok = ok ? 1 : 0;
+    std::vector<int> oks(P);
+    if ((rc = allgather_host(&mine_ok, oks.data(), sizeof(int), s))) return rc;
+    p2p_checked = true;
+    p2p = true;
+    for (int q = 0; q < P; ++q) p2p = p2p && oks[q];
+    if (!p2p) {
+      close_peers();
+      return OKT_OK;
+    }
+    tab = okt::PeerTab{};
+    tab.P = P;
+    tab.rank = rank;
+    for (int q = 0; q < P; ++q) {
+      tab.hdr[q] = reinterpret_cast<okt::P2PHdr*>(base[q]);
+      for (int p = 0; p < 2; ++p) {
+        tab.L[q][p] = reinterpret_cast<uint64_t*>(base[q] + lay.L[p]);
+        tab.sur_idx[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.sidx[p]);
+        tab.sur_val[q][p] = reinterpret_cast<double*>(base[q] + lay.sval[p]);
+        tab.u_idx[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.uidx[p]);
+        tab.u_val[q][p] = reinterpret_cast<double*>(base[q] + lay.uval[p]);
+      }
+    }
+    if ((rc = ensure(planb, sizeof(okt::P2PPlan)))) return rc;
+    pdone.zero_init = true;
+    if ((rc = ensure(pdone, 64))) return rc;
+    if ((rc = ensure(plt, sizeof(uint32_t) * okt::kP2PMaxP * size_t(S.max_chunks)))) return rc;
+    if ((rc = ensure(tabd, sizeof(okt::PeerTab)))) return rc;
+    if ((rc = ck(cudaMemcpy(tabd.p, &tab, sizeof(okt::PeerTab), cudaMemcpyHostToDevice), "tab"))) return rc;
+    if ((rc = ensure(indexes, 4 * std::max<size_t>(n, 1)))) return rc;
+    win_n = n;
+    return OKT_OK;
+  }
+
+  // Steady iteration on the P2P window (no host round trip until the end).
+  // K1 (with its fused publication, see pub_L) already wrote the local
+  // selection into tab.L[rank][par] and raised L-ready at every peer.
+  okt::PubL pub_L(uint64_t epoch, int par) {
+    okt::PubL pb;
+    pb.tab = tabd.as<okt::PeerTab>();
+    pb.epoch = epoch;
+    pb.par = par;
+    pb.P = P;
+    pb.done = pdone.as<uint32_t>();
+    pb.lt = plt.as<uint32_t>();
+    pb.cuts = d()->cuts;
+    pb.d_off = d()->off;
+    pb.flags = &d()->flags;
+    return pb;
+  }
+
+  int p2p_steady(uint64_t epoch, int par, cudaStream_t s) {
+    okt::P2PPlan* dp = planb.as<okt::P2PPlan>();
+    const okt::PeerTab* dt = tabd.as<okt::PeerTab>();
+    const uint64_t lo = st.cuts[rank], hi = st.cuts[rank + 1];
+    const uint64_t W = hi > lo ? hi - lo : 0;
+    int rc;
+    if ((rc = ensure(mask, ((W + 15) / 16) * 16 + 16)) || (rc = ensure(stage, 4 * std::max<uint64_t>(W, 1) * P)))
+      return rc;
+    tmark(OKT_T_MERGE, s);
+    rc = ck(okt::launch_p2p_scatter(L, dt, P, epoch, par, d()->off, dp, lo, W, mask.as<uint32_t>(),
+                                    stage.as<float>(), &d()->flags, kP2PTimeoutNs), "p2p");
+    okt::PubSur ps;
+    ps.tab = dt;
+    ps.epoch = epoch;
+    ps.par = par;
+    ps.done = pdone.as<uint32_t>() + 1;
+    ps.flags = &d()->flags;
+    if (!rc) rc = ck(okt::launch_region_scan(L, S, P, true, lo, W, mask.as<uint32_t>(), stage.as<float>(),
+                                             &d()->global_th, tab.sur_idx[rank][par], tab.sur_val[rank][par],
+                                             &d()->S, &ps), "region_scan");
+    tmark(OKT_T_ALLGATHER, s);
+    if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, P, epoch, par, &d()->S, dp, &d()->U, &d()->flags,
+                                                kP2PTimeoutNs), "p2p");
+    if (!rc) rc = ck(cudaMemcpyAsync(hplan, dp, sizeof(okt::P2PPlan), cudaMemcpyDeviceToHost, s), "d2h");
+    return rc;
+  }
+
+  // Ledger of a P2P step, from the sizes every rank agreed on (h / hplan valid).
+  void p2p_credit() {
+    std::vector<uint64_t> counts(size_t(P) * P, 0);
+    for (int q = 0; q < P; ++q) {
+      counts[size_t(rank) * P + q] = h->off[q + 1] - h->off[q];
+      counts[size_t(q) * P + rank] = hplan->seg_cnt[q];
+    }
+    okt::plan::ledger_split(ledger[OKT_PHASE_SPLIT], rank, P, counts.data(), st.bucket_size);
+    for (int q = 0; q < P; ++q)
+      if (q != rank) {
+        ledger[OKT_PHASE_SPLIT].bytes_sent += 8 * counts[size_t(rank) * P + q];
+        ledger[OKT_PHASE_SPLIT].bytes_recv += 8 * hplan->seg_cnt[q];
+      }
+    credit_allgather_u32();
+    const std::vector<uint64_t> sizes(hplan->sizes, hplan->sizes + P);
+    const okt::plan::Balance B = okt::plan::balance(rank, P, sizes);
+    if (B.on) {
+      okt::plan::ledger_balance(ledger[OKT_PHASE_BALANCE], B);
+      for (const auto& p : B.sends) ledger[OKT_PHASE_BALANCE].bytes_sent += 12 * (p.b - p.a);
+      for (const auto& p : B.recvs) ledger[OKT_PHASE_BALANCE].bytes_recv += 12 * (p.b - p.a);
+    }
+    credit_allgatherv(OKT_PHASE_ALLGATHERV, B.part_sz, 12);
+  }
+
   // ---- the step ---------------------------------------------------------------------
   int step(const float* g, float* w, size_t n, double alpha, int64_t t, size_t k, bool sgd,
            okt_result* out, cudaStream_t s) {
@@ -553,6 +777,16 @@ struct okt_comm {
 
     const bool thr = (t - 1) % int64_t(st.tau_prime) == 0;
     const bool bnd = (t - 1) % int64_t(st.tau) == 0;
+    if (P > 1 && (rc = setup_p2p(n, s))) return rc;
+    // Steady iterations on distinct GPUs run the device-driven exchange; the
+    // refresh iterations (1 in tau') keep the host-synchronised protocol.
+    const bool use_p2p = p2p && !thr && !bnd && st.regions == P;
+    uint64_t epoch = 0;
+    int par = 0;
+    if (use_p2p) {
+      epoch = ++p2p_epoch;
+      par = int(epoch & 1);
+    }
     const float* acc = g;
     const float* eps_in = nullptr;
     float* eps_out = nullptr;
@@ -598,9 +832,11 @@ struct okt_comm {
                              &d()->flags, nullptr, &ap1), "k1");
     } else {
       tmark(OKT_T_SELECT, s);
+      const okt::PubL pl = use_p2p ? pub_L(epoch, par) : okt::PubL{};
       rc = ck(okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, g, eps_in, eps_out, fa,
-                             n, &d()->local_th, nullptr, okt::OutCoo{coo.as<uint64_t>()}, &d()->m, nullptr,
-                             &d()->flags, nullptr), "k1");
+                             n, &d()->local_th, nullptr,
+                             okt::OutCoo{use_p2p ? tab.L[rank][par] : coo.as<uint64_t>()}, &d()->m, nullptr,
+                             &d()->flags, nullptr, nullptr, use_p2p ? &pl : nullptr), "k1");
     }
     if (rc) return abort_step(rc);
 
@@ -626,6 +862,13 @@ struct okt_comm {
       d_U = &d()->S;
       new_cuts[0] = 0;
       new_cuts[1] = n;
+    } else if (use_p2p) {
+      rc = p2p_steady(epoch, par, s);
+      if (rc) return abort_step(rc);
+      for (int q = 0; q <= P; ++q) new_cuts[q] = st.cuts[q];
+      d_U = &d()->U;
+      ui = tab.u_idx[rank][par];
+      uv = tab.u_val[rank][par];
     } else {
       if (!is_pow2(P)) return set_err(OKT_ERR_CONFIG, "world size must be a power of two");
       // ---- boundaries ----
@@ -703,6 +946,15 @@ struct okt_comm {
       dev_stale = true;
       return set_err(OKT_ERR_NUMERIC, "ok_sparse_allreduce: non-finite input");
     }
+    if (h->flags & 8u) {
+      dev_stale = true;
+      return set_err(OKT_ERR_TRANSPORT, "TransportError: a peer did not reach the exchange (timeout)");
+    }
+    if (h->flags & 16u) {
+      dev_stale = true;
+      return set_err(OKT_ERR_TRANSPORT, "TransportError: a peer failed (non-finite input)");
+    }
+    if (use_p2p) p2p_credit();
     if (h->flags & 2u) {
       dev_stale = true;
       return set_err(OKT_ERR_PROTOCOL, "split_and_reduce: entries outside my region");
@@ -781,6 +1033,7 @@ int init_comm(okt_comm* c) {
   if (e == cudaSuccess) e = c->chunkcap.ensure(64);
   if (e == cudaSuccess) e = cudaMallocHost(&c->h, sizeof(DevScalars));
   if (e == cudaSuccess) e = cudaMallocHost(&c->hup, sizeof(DevScalars));
+  if (e == cudaSuccess) e = cudaMallocHost(&c->hplan, sizeof(okt::P2PPlan));
   if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("init: ") + cudaGetErrorString(e));
   std::memset(c->h, 0, sizeof(DevScalars));
   std::memset(c->hup, 0, sizeof(DevScalars));
@@ -913,6 +1166,8 @@ int okt_comm_destroy(okt_comm* c) {
   if (c->ready_ev) cudaEventDestroy(c->ready_ev);
   if (c->h) cudaFreeHost(c->h);
   if (c->hup) cudaFreeHost(c->hup);
+  if (c->hplan) cudaFreeHost(c->hplan);
+  c->close_peers();
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return OKT_OK;

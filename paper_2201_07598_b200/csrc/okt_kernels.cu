@@ -68,8 +68,9 @@ __global__ void __launch_bounds__(kThreads)
                    const double* __restrict__ sval, const uint32_t* __restrict__ counts,
                    const uint32_t* __restrict__ counts2, uint64_t cap_host, const uint64_t* d_cap,
                    uint64_t* __restrict__ o64, uint32_t* __restrict__ oidx, double* __restrict__ oval,
-                   uint64_t* d_total, uint64_t* d_total2, ApplyArgs ap) {
+                   uint64_t* d_total, uint64_t* d_total2, ApplyArgs ap, PubSur pub) {
   __shared__ uint64_t red[kWarps];
+  __shared__ int s_last;
   const int c = blockIdx.x, G = gridDim.x;
   const uint64_t cnt = counts[c];
   const uint64_t cap = d_cap ? *d_cap : cap_host;
@@ -147,21 +148,46 @@ __global__ void __launch_bounds__(kThreads)
       if (threadIdx.x == 0) *d_total2 = s2;
     }
   }
+  if (pub.tab) {
+    // P2P: the last CTA to finish publishes the survivor count to the peers
+    // once every entry is in place (okt_p2p.cuh).
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(pub.done, 1u) == unsigned(G - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    uint64_t tot = 0;
+    for (int q = threadIdx.x; q < G; q += kThreads) tot += counts[q];
+    tot = block_sum(tot, red);
+    const PeerTab* tab = pub.tab;
+    const int me = tab->rank, P = tab->P;
+    if (threadIdx.x == 0) {
+      tab->hdr[me]->pub[pub.par].S = tot;
+      tab->hdr[me]->pub[pub.par].status = (*pub.flags & (1u | 8u | 16u)) ? 1 : 0;
+      *pub.done = 0;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < P && int(threadIdx.x) != me)
+      st_release_sys(&tab->hdr[threadIdx.x]->flag[kFlagSurReady][me], pub.epoch);
+  }
 }
 
 template <int MODE>
 static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_t cap_host,
                                   const uint64_t* d_cap, bool with2, uint64_t* o64, uint32_t* oidx,
                                   double* oval, uint64_t* d_total, uint64_t* d_total2,
-                                  const ApplyArgs* ap = nullptr) {
+                                  const ApplyArgs* ap = nullptr, const PubSur* pub = nullptr) {
+  const PubSur pb = pub ? *pub : PubSur{};
   if (ap && ap->w)
     compact_kernel<MODE, true><<<G, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts,
                                                         with2 ? S.counts2 : nullptr, cap_host, d_cap, o64, oidx,
-                                                        oval, d_total, d_total2, *ap);
+                                                        oval, d_total, d_total2, *ap, pb);
   else
     compact_kernel<MODE, false><<<G, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts,
                                                          with2 ? S.counts2 : nullptr, cap_host, d_cap, o64, oidx,
-                                                         oval, d_total, d_total2, ApplyArgs{});
+                                                         oval, d_total, d_total2, ApplyArgs{}, pb);
   ++L.launches;
   return cudaGetLastError();
 }
@@ -300,7 +326,7 @@ template <bool ACCUM, bool SELECT, bool HIST, bool DUAL>
 static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float* g, const float* eps_in,
                                float* eps_out, float alpha, uint64_t n, const double* d_th,
                                const double* d_th2, const OutCoo& out, uint64_t* d_m, uint64_t* d_m2,
-                               uint32_t* d_flags, uint32_t* d_hist, const ApplyArgs* ap) {
+                               uint32_t* d_flags, uint32_t* d_hist, const ApplyArgs* ap, const PubL* pub) {
   constexpr int TILE = kJ * 4 * kThreads;
   const uint64_t tiles = (n + TILE - 1) / TILE;
   auto kern = vec ? k1_kernel<ACCUM, SELECT, HIST, true, DUAL> : k1_kernel<ACCUM, SELECT, HIST, false, DUAL>;
@@ -315,6 +341,7 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !SELECT) return e;
   const uint64_t chunk_cap = uint64_t(tpc) * TILE;
+  if (pub) return launch_p2p_compact_L(L, S, G, chunk_cap, out.aos, d_m, *pub);
   if (out.aos)
     return launch_compact<0>(L, S, G, chunk_cap, nullptr, DUAL, out.aos, nullptr, nullptr, d_m, d_m2);
   return launch_compact<1>(L, S, G, chunk_cap, nullptr, DUAL, nullptr, out.idx, out.val, d_m, d_m2, ap);
@@ -323,7 +350,7 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
 cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, const float* eps_in,
                       float* eps_out, float alpha, uint64_t n, const double* d_th, const double* d_th2,
                       const OutCoo& out, uint64_t* d_m, uint64_t* d_m2, uint32_t* d_flags, uint32_t* d_hist,
-                      const ApplyArgs* ap) {
+                      const ApplyArgs* ap, const PubL* pub) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   bool vec = al(g);
   if (mode != K1Mode::kSelect) vec = vec && al(eps_in) && al(eps_out);
@@ -331,17 +358,17 @@ cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, co
   switch (mode) {
     case K1Mode::kSelect:
       return dual ? k1_dispatch<false, true, false, true>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out,
-                                                           d_m, d_m2, d_flags, d_hist, ap)
+                                                           d_m, d_m2, d_flags, d_hist, ap, pub)
                   : k1_dispatch<false, true, false, false>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2,
-                                                            out, d_m, d_m2, d_flags, d_hist, ap);
+                                                            out, d_m, d_m2, d_flags, d_hist, ap, pub);
     case K1Mode::kAccumSelect:
       return dual ? k1_dispatch<true, true, false, true>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out,
-                                                          d_m, d_m2, d_flags, d_hist, ap)
+                                                          d_m, d_m2, d_flags, d_hist, ap, pub)
                   : k1_dispatch<true, true, false, false>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out,
-                                                           d_m, d_m2, d_flags, d_hist, ap);
+                                                           d_m, d_m2, d_flags, d_hist, ap, pub);
     case K1Mode::kAccumHist:
       return k1_dispatch<true, false, true, false>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out, d_m,
-                                                   d_m2, d_flags, d_hist, ap);
+                                                   d_m2, d_flags, d_hist, ap, pub);
   }
   return cudaErrorInvalidValue;
 }
@@ -434,7 +461,7 @@ __global__ void __launch_bounds__(kThreads)
   const int tid = threadIdx.x;
   // A step whose input was non-finite applies nothing (the reference throws
   // before touching the residual or the model).
-  const bool skip = (*d_flags & 1u) != 0;
+  const bool skip = (*d_flags & (1u | 8u | 16u)) != 0;  // own or a peer's failure
   const uint64_t cnt = skip ? 0 : *d_U;
   const float tf = ceil_to_float(*d_local_th);
   const double dP = double(P);
@@ -562,54 +589,101 @@ __device__ __forceinline__ double bracket_sum(const float* st, uint32_t bits) {
   return a[0];
 }
 
+// Thread-contiguous layout: thread t of a tile owns coordinates
+// [t*32, t*32+32) (eight mask words, two 16 B loads), so its selected set is a
+// 32-bit mask and the tile order is (thread, bit): one warp scan + one CTA
+// barrier per tile.  The first values each thread emits are gathered from the
+// staging before the barrier, so a tile costs about one memory round trip.
+constexpr int kRegionCoordsPerThread = 32;
+constexpr int kRegionTile = kThreads * kRegionCoordsPerThread;  // 8192 coordinates
+static_assert(kRegionTile == kRegionTileHost, "staging sized for the region tile");
+
 template <int P, bool FILTER>
 __global__ void __launch_bounds__(kThreads)
     region_scan_kernel(uint64_t lo, uint64_t W, uint32_t tiles, uint32_t tpc, uint32_t* mask,
                        const float* __restrict__ stage, const double* d_gth, uint32_t* __restrict__ sidx,
                        double* __restrict__ sval, uint32_t* counts) {
-  constexpr int C = 4, TILE = kJ * C * kThreads;
-  __shared__ uint32_t tbl[2][32];
-  const int tid = threadIdx.x;
+  __shared__ uint32_t wtot[2][kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double gth = FILTER ? *d_gth : 0.0;
   const uint64_t nwords = (W + 3) / 4;
   const uint32_t t0 = blockIdx.x * tpc, t1 = min(t0 + tpc, tiles);
-  const uint64_t obase = uint64_t(blockIdx.x) * tpc * TILE;
+  const uint64_t obase = uint64_t(blockIdx.x) * tpc * kRegionTile;
   uint32_t running = 0;
   int parity = 0;
   for (uint32_t tile = t0; tile < t1; ++tile, parity ^= 1) {
-    const uint64_t base = uint64_t(tile) * TILE;
-    double val[kJ][C];
-    bool pred[kJ][C];
-    unsigned bal[kJ][C];
+    const uint64_t w0 = uint64_t(tile) * (kRegionTile / 4) + uint64_t(tid) * 8;  // first mask word
+    uint32_t mw[8];
+    if (w0 + 8 <= nwords) {
+      const uint4 a = *reinterpret_cast<const uint4*>(mask + w0);
+      const uint4 b = *reinterpret_cast<const uint4*>(mask + w0 + 4);
+      mw[0] = a.x; mw[1] = a.y; mw[2] = a.z; mw[3] = a.w;
+      mw[4] = b.x; mw[5] = b.y; mw[6] = b.z; mw[7] = b.w;
+    } else {
 #pragma unroll
-    for (int j = 0; j < kJ; ++j) {
-      const uint64_t wi = (base >> 2) + uint64_t(j) * kThreads + tid;
-      const uint32_t mw = wi < nwords ? mask[wi] : 0u;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const uint32_t bits = (mw >> (8 * c)) & 0xffu;
-        val[j][c] = 0.0;
-        bool p = false;
-        if (bits) {
-          val[j][c] = bracket_sum<P>(stage + (wi * 4 + c) * P, bits);
-          p = !FILTER || fabs(val[j][c]) >= gth;
-        }
-        pred[j][c] = p;
-        bal[j][c] = __ballot_sync(0xffffffffu, p);
-      }
-      if (mw) mask[wi] = 0u;
+      for (int j = 0; j < 8; ++j) mw[j] = (w0 + j < nwords) ? mask[w0 + j] : 0u;
     }
-    uint32_t grp[kJ];
-    const uint32_t total = tile_offsets<C>(tbl[parity], bal, grp);
+    uint32_t present = 0;
 #pragma unroll
-    for (int j = 0; j < kJ; ++j) {
+    for (int j = 0; j < 8; ++j)
 #pragma unroll
-      for (int c = 0; c < C; ++c)
-        if (pred[j][c]) {
-          const uint64_t pos = obase + running + grp[j] + rank_in_group<C>(bal, j, c);
-          sidx[pos] = uint32_t(lo + base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C + c);
-          sval[pos] = val[j][c];
-        }
+      for (int c = 0; c < 4; ++c)
+        if ((mw[j] >> (8 * c)) & 0xffu) present |= 1u << (j * 4 + c);
+    const uint64_t c0 = w0 * 4;  // first coordinate (region-relative)
+    auto bits_of = [&](int k) { return (mw[k >> 2] >> (8 * (k & 3))) & 0xffu; };
+    // Values of the first two emitted coordinates stay in registers.
+    uint32_t sel = FILTER ? 0u : present;
+    double v_first[2] = {0.0, 0.0};
+    int k_first[2] = {-1, -1};
+    int kept = 0;
+    for (uint32_t rest = present; rest; rest &= rest - 1) {
+      const int k = __ffs(rest) - 1;
+      const double v = bracket_sum<P>(stage + (c0 + k) * P, bits_of(k));
+      const bool keep = !FILTER || fabs(v) >= gth;
+      if (FILTER && keep) sel |= 1u << k;
+      if (keep && kept < 2) {
+        v_first[kept] = v;
+        k_first[kept] = k;
+        ++kept;
+      } else if (!FILTER && kept >= 2) {
+        break;  // REGION mode: the rest is gathered after the scan
+      }
+    }
+    if (present) {
+      if (w0 + 8 <= nwords) {
+        *reinterpret_cast<uint4*>(mask + w0) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(mask + w0 + 4) = make_uint4(0, 0, 0, 0);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (w0 + j < nwords) mask[w0 + j] = 0u;
+      }
+    }
+    // CTA exclusive scan of the per-thread counts.
+    const uint32_t cnt = __popc(sel);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wtot[parity][warp] = incl;
+    __syncthreads();
+    uint32_t wpre = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t x = wtot[parity][w];
+      wpre += (w < warp) ? x : 0u;
+      total += x;
+    }
+    uint64_t pos = obase + running + wpre + incl - cnt;
+    int emitted = 0;
+    for (uint32_t rest = sel; rest; rest &= rest - 1, ++pos, ++emitted) {
+      const int k = __ffs(rest) - 1;
+      const double v = (emitted < 2 && k_first[emitted] == k) ? v_first[emitted]
+                                                              : bracket_sum<P>(stage + (c0 + k) * P, bits_of(k));
+      sidx[pos] = uint32_t(lo + c0 + k);
+      sval[pos] = v;
     }
     running += total;
   }
@@ -619,32 +693,28 @@ __global__ void __launch_bounds__(kThreads)
 template <int P, bool FILTER>
 static cudaError_t region_scan_dispatch(Launch& L, const Stage& S, uint64_t lo, uint64_t W, uint32_t* mask,
                                         const float* stage, const double* d_gth, uint32_t* out_idx,
-                                        double* out_val, uint64_t* d_count) {
-  constexpr int TILE = kJ * 4 * kThreads;
+                                        double* out_val, uint64_t* d_count, const PubSur* pub) {
+  constexpr int TILE = kRegionTile;
   const uint64_t tiles = (W + TILE - 1) / TILE;
-  if (tiles == 0) {
-    cudaMemsetAsync(d_count, 0, sizeof(uint64_t), L.s);
-    return cudaGetLastError();
-  }
   static int cap = 0;
   if (!cap) cap = resident_ctas(region_scan_kernel<P, FILTER>, kThreads, L.sms);
   const uint32_t G = chunks_for(tiles, cap, S.max_chunks);
-  const uint32_t tpc = uint32_t((tiles + G - 1) / G);
+  const uint32_t tpc = uint32_t(std::max<uint64_t>((tiles + G - 1) / G, 1));
   region_scan_kernel<P, FILTER><<<G, kThreads, 0, L.s>>>(lo, W, uint32_t(tiles), tpc, mask, stage, d_gth, S.sidx,
                                                          S.sval, S.counts);
   ++L.launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_compact<2>(L, S, G, uint64_t(tpc) * TILE, nullptr, false, nullptr, out_idx, out_val, d_count,
-                           nullptr);
+                           nullptr, nullptr, pub);
 }
 
 cudaError_t launch_region_scan(Launch& L, const Stage& S, int P, bool filter, uint64_t lo, uint64_t W,
                                uint32_t* mask, const float* stage, const double* d_gth, uint32_t* out_idx,
-                               double* out_val, uint64_t* d_count) {
-#define OKT_RS(PP)                                                                                     \
-  return filter ? region_scan_dispatch<PP, true>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count) \
-                : region_scan_dispatch<PP, false>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count)
+                               double* out_val, uint64_t* d_count, const PubSur* pub) {
+#define OKT_RS(PP)                                                                                          \
+  return filter ? region_scan_dispatch<PP, true>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count, pub) \
+                : region_scan_dispatch<PP, false>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count, pub)
   switch (P) {
     case 1: OKT_RS(1);
     case 2: OKT_RS(2);

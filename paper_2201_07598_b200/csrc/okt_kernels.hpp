@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "okt_p2p.cuh"
+
 namespace okt {
 
 // Per-comm launch context: stream and launch accounting.
@@ -37,6 +39,7 @@ struct Stage {
 size_t stage_entries(uint64_t count, int tile, int max_chunks);
 constexpr int kK1Tile = 4096;   // K1 / region-scan tile (elements)
 constexpr int kCooTile = 1024;  // O(k) passes tile (entries)
+constexpr int kRegionTileHost = 8192;  // region scan tile (coordinates)
 
 // Output of a compaction: AoS u64 entries or SoA (u32 idx, f64 val).
 struct OutCoo {
@@ -71,7 +74,7 @@ struct Segs {
 cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, const float* eps_in,
                       float* eps_out, float alpha, uint64_t n, const double* d_th, const double* d_th2,
                       const OutCoo& out, uint64_t* d_m, uint64_t* d_m2, uint32_t* d_flags,
-                      uint32_t* d_hist, const ApplyArgs* ap = nullptr);
+                      uint32_t* d_hist, const ApplyArgs* ap = nullptr, const PubL* pub = nullptr);
 
 // K2/K4: exact k-th largest magnitude (k clamped to the element count) by MSD
 // radix select on the IEEE bit patterns; writes the threshold to *d_th_out
@@ -108,7 +111,8 @@ cudaError_t launch_scatter(Launch& L, const Segs& segs, uint64_t lo, uint64_t W,
 // fp64, keep explicit zeros, optionally filter by |sum| >= *d_gth, clear mask.
 cudaError_t launch_region_scan(Launch& L, const Stage& S, int P, bool filter, uint64_t lo, uint64_t W,
                                uint32_t* mask, const float* stage, const double* d_gth,
-                               uint32_t* out_idx, double* out_val, uint64_t* d_count);
+                               uint32_t* out_idx, double* out_val, uint64_t* d_count,
+                               const PubSur* pub = nullptr);
 
 // Small control kernels.
 cudaError_t launch_slice_offsets(Launch& L, const uint64_t* coo, const uint64_t* d_m,
@@ -129,5 +133,19 @@ cudaError_t launch_gen_noise(Launch& L, float* out, uint64_t n, uint64_t noise_k
                              double coef);
 cudaError_t launch_scatter_heavy(Launch& L, const uint32_t* pos, const float* val,
                                  uint64_t count, float* out);
+
+// ---- device-driven multi-GPU exchange (okt_p2p.cu) ----------------------------
+// K1 phase B for the P2P path: compaction into the window's L, slice offsets,
+// publication of (offsets, status) and of the L-ready flag to every peer.
+cudaError_t launch_p2p_compact_L(Launch& L, const Stage& S, uint32_t G, uint64_t chunk_cap, uint64_t* out,
+                                 uint64_t* d_m, const PubL& pub);
+// Waits for every peer's L, then scatters my slices read out of their HBM.
+cudaError_t launch_p2p_scatter(Launch& L, const PeerTab* d_tab, int P, uint64_t epoch, int par,
+                               const uint64_t* d_off, P2PPlan* plan, uint64_t lo, uint64_t W, uint32_t* mask,
+                               float* stage, uint32_t* d_flags, uint64_t timeout_ns);
+// Waits for every rank's survivors, plans (offsets / balance), pulls u.
+cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, int P, uint64_t epoch, int par,
+                                  const uint64_t* d_S, P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags,
+                                  uint64_t timeout_ns);
 
 }  // namespace okt

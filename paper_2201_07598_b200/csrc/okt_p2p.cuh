@@ -1,0 +1,111 @@
+// okt_p2p.cuh — device-driven multi-GPU exchange over NVLink peer memory.
+//
+// Every rank owns one symmetric window (same layout on all ranks) that its
+// peers map: through CUDA IPC across processes, or directly within one
+// process.  Phases hand data over with release/acquire flags instead of host
+// synchronisation:
+//   publish  the producer fences at system scope, then stores
+//            flag[kind][me] = epoch into every peer's window header;
+//   wait     the consumer spins (ld.acquire.sys, bounded by a timeout) on its
+//            own header until every peer's flag reached the epoch, then reads
+//            the peers' published words remotely.
+// Bulk data never moves through a staging copy: the consumer's kernels read
+// the producer's buffers in place over NVLink (pull model), e.g. the region
+// scatter reads each source's COO slice straight out of that source's HBM.
+// Buffers a peer may still read are double-buffered by step parity; a rank can
+// only run one step ahead of a peer (each step waits on every peer), so a
+// parity slot is never rewritten while someone reads it.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace okt {
+
+constexpr int kP2PMaxP = 8;
+enum P2PFlag { kFlagLReady = 0, kFlagSurReady = 1, kFlagBlockReady = 2, kP2PFlagKinds = 4 };
+
+// What a rank publishes for its peers each step (double-buffered by parity).
+struct P2PPub {
+  uint64_t off[kP2PMaxP + 1];  // slice offsets of the local selection L
+  uint64_t status;             // non-zero: this rank's step failed (non-finite input)
+  uint64_t S;                  // survivors of the global threshold
+  uint64_t pad[5];
+};
+
+struct P2PHdr {
+  uint64_t flag[kP2PFlagKinds][kP2PMaxP];  // written by peers
+  P2PPub pub[2];
+};
+
+// Peer table: every rank's window pieces (index = rank), both parities.
+struct PeerTab {
+  P2PHdr* hdr[kP2PMaxP];
+  uint64_t* L[kP2PMaxP][2];
+  uint32_t* sur_idx[kP2PMaxP][2];
+  double* sur_val[kP2PMaxP][2];
+  uint32_t* u_idx[kP2PMaxP][2];
+  double* u_val[kP2PMaxP][2];
+  int P;
+  int rank;
+};
+
+// Device-side plan of the balance + allgatherv phase (local memory).
+struct P2PPlan {
+  uint64_t sizes[kP2PMaxP];
+  uint64_t off[kP2PMaxP + 1];    // stream offsets of each rank's survivors
+  uint64_t block[kP2PMaxP + 1];  // equal blocks when balanced
+  uint64_t total;
+  uint32_t balanced;
+  uint32_t pad;
+  uint64_t seg_off[kP2PMaxP];    // my split slices inside each source's L
+  uint64_t seg_cnt[kP2PMaxP];
+  uint64_t peer_status[kP2PMaxP];
+};
+
+// Fused publication hooks (phase B of a compaction publishes what it wrote).
+struct PubL {  // K1 phase B: local selection L + its slice offsets
+  const PeerTab* tab = nullptr;  // device copy
+  uint64_t epoch = 0;
+  int par = 0;
+  int P = 1;
+  uint32_t* done = nullptr;      // last-CTA counter (self-resetting)
+  uint32_t* lt = nullptr;        // [chunk][kP2PMaxP] entries below each cut
+  const uint64_t* cuts = nullptr;
+  uint64_t* d_off = nullptr;     // local copy of the slice offsets
+  const uint32_t* flags = nullptr;
+};
+struct PubSur {  // region scan phase B: survivors of the global threshold
+  const PeerTab* tab = nullptr;
+  uint64_t epoch = 0;
+  int par = 0;
+  uint32_t* done = nullptr;
+  const uint32_t* flags = nullptr;
+};
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until *p >= epoch; false after `timeout_ns` (a peer died or diverged).
+__device__ __forceinline__ bool wait_flag(const uint64_t* p, uint64_t epoch, uint64_t timeout_ns) {
+  if (ld_acquire_sys(p) >= epoch) return true;
+  const uint64_t t0 = globaltimer_ns();
+  while (true) {
+    __nanosleep(64);
+    if (ld_acquire_sys(p) >= epoch) return true;
+    if (globaltimer_ns() - t0 > timeout_ns) return false;
+  }
+}
+
+}  // namespace okt

@@ -63,21 +63,25 @@ int scenario(const char* name, int P, std::size_t n, std::size_t k, int iters, s
       if (!(ref[r].u == gpu[r].u) || ref[r].indexes != gpu[r].indexes ||
           ref[r].local_selected != gpu[r].local_selected || !same_state(sr[r], sg[r])) {
         std::printf("FAIL %s: t=%lld rank %d result/state differs\n", name, (long long)t, r);
+        okt_oklab::release(&wg.transport);
         return 1;
       }
     }
     if (!same_ledger(wr.ledger, wg.ledger, P)) {
       std::printf("FAIL %s: t=%lld ledger differs\n", name, (long long)t);
+      okt_oklab::release(&wg.transport);
       return 1;
     }
   }
   std::printf("PASS %s\n", name);
+  okt_oklab::release(&wg.transport);
   return 0;
 }
 
 }  // namespace
 
 int main() {
+  std::setvbuf(stdout, nullptr, _IONBF, 0);
   int fails = 0;
   // acceptance.cpp:101-145 (criterion 1), a subset of the 100 instances
   for (int m = 0; m < 12; ++m) {
@@ -112,6 +116,7 @@ int main() {
       OkState s;
       return okt_oklab::ok_sparse_allreduce(ctx, s, f32(test::random_dense(77 + ctx.rank, 32)), 5, 4).u;
     });
+    okt_oklab::release(&wg.transport);
     const bool ok = ref[0] == gpu[0] && ref[1] == gpu[1] && gpu[0].nnz() == 32;
     std::printf("%s off-cycle fallback\n", ok ? "PASS" : "FAIL");
     fails += ok ? 0 : 1;
@@ -125,6 +130,7 @@ int main() {
     try { okt_oklab::ok_sparse_allreduce(ctx, s, DenseGrad{}, 1, 1); } catch (const std::invalid_argument&) { ++ok; }
     try { okt_oklab::ok_sparse_allreduce(ctx, s, DenseGrad(std::vector<double>{1.0}), 0, 1); } catch (const std::invalid_argument&) { ++ok; }
     try { okt_oklab::ok_sparse_allreduce(ctx, s, DenseGrad(std::vector<double>{1.0, std::nan("")}), 1, 1); } catch (const NumericError&) { ++ok; }
+    okt_oklab::release(&w.transport);
     std::printf("%s exception mapping\n", ok == 3 ? "PASS" : "FAIL");
     fails += ok == 3 ? 0 : 1;
   }
