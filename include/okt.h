@@ -175,6 +175,19 @@ int okt_sgd_step(okt_comm* comm, const float* d_grad, float* d_w, size_t n,
                  double alpha, int64_t t, size_t k, okt_result* out,
                  void* stream);
 
+/* Asynchronous forms: enqueue the step on `stream` and return.  On the steady
+ * device-driven iterations (one CUDA graph for P = 1, the NVLink window path
+ * for P > 1) nothing waits on the host until okt_step_wait; other iterations
+ * synchronise internally as the synchronous calls do.  okt_step_wait
+ * finishes the step (state commit, result, error status).  Any other call on
+ * the comm — including the next step — waits for a step still in flight. */
+int okt_sparse_allreduce_async(okt_comm* comm, const float* d_acc, size_t n,
+                               int64_t t, size_t k, void* stream);
+int okt_sgd_step_async(okt_comm* comm, const float* d_grad, float* d_w,
+                       size_t n, double alpha, int64_t t, size_t k,
+                       void* stream);
+int okt_step_wait(okt_comm* comm, okt_result* out);
+
 /* Host-buffer forms of the two hot entry points: the reference's own calling
  * convention (DenseGrad in, SparseGrad out, both in host memory).  The
  * gradient is copied host->device into a comm-owned buffer, the step runs, and
@@ -252,6 +265,7 @@ enum okt_timer {
   OKT_T_ALLGATHER,    /* K5/K6 balance + allgatherv */
   OKT_T_APPLY,        /* K7 residual / model scatter */
   OKT_T_STEP,         /* whole call */
+  OKT_T_K1,           /* the K1 streaming kernel alone (phase A) */
   OKT_T_COUNT
 };
 /* When on, the library records CUDA events around each phase on its stream

@@ -15,9 +15,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libokt.so")
 
 OKT_MAX_WORLD = 8
-OKT_T_COUNT = 8
+OKT_T_COUNT = 9
 TIMER_NAMES = ("select", "threshold", "split", "merge", "global", "allgather",
-               "apply", "step")
+               "apply", "step", "k1")
 
 # Every symbol include/okt.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -28,6 +28,7 @@ EXPORTS = (
     "okt_get_state", "okt_set_state", "okt_set_params", "okt_ledger",
     "okt_ledger_reset", "okt_sparse_allreduce", "okt_residual_reset",
     "okt_residual", "okt_sgd_step", "okt_sparse_allreduce_host",
+    "okt_sparse_allreduce_async", "okt_sgd_step_async", "okt_step_wait",
     "okt_sgd_step_host", "okt_memcpy_h2d", "okt_memcpy_d2h",
     "okt_th_re_evaluate_dense", "okt_th_re_evaluate_sparse",
     "okt_select_by_threshold", "okt_space_repartition",
@@ -106,6 +107,10 @@ def lib() -> ctypes.CDLL:
         "okt_ledger_reset": (c_int, [c_void_p]),
         "okt_sparse_allreduce": (c_int, [c_void_p, c_void_p, c_size_t, c_int64, c_size_t,
                                          P(OktResult), c_void_p]),
+        "okt_sparse_allreduce_async": (c_int, [c_void_p, c_void_p, c_size_t, c_int64, c_size_t, c_void_p]),
+        "okt_sgd_step_async": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_double, c_int64, c_size_t,
+                                       c_void_p]),
+        "okt_step_wait": (c_int, [c_void_p, P(OktResult)]),
         "okt_residual_reset": (c_int, [c_void_p, c_size_t, c_void_p, c_void_p]),
         "okt_residual": (c_int, [c_void_p, P(c_void_p), P(c_size_t)]),
         "okt_sgd_step": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_double, c_int64,

@@ -186,6 +186,18 @@ struct okt_comm {
   std::vector<void*> ipc_open;
   uint64_t p2p_epoch = 0;
   okt::P2PPlan* hplan = nullptr;  // pinned mirror of the device plan
+  // CUDA graph of the steady single-rank step (memset, K1, fused compaction +
+  // apply, scalar readback); per-step pointers come through `ptrsb`.
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    size_t n = 0, k = 0;
+    bool sgd = false, prof = false;
+    uint64_t gen = 0, kernels = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+  } graph1;
+  uint64_t buf_gen = 1;
+  Buf ptrsb;
+  okt::StepPtrs* hptrs = nullptr;
   DevScalars* h = nullptr;   // pinned download mirror
   DevScalars* hup = nullptr; // pinned upload staging
   size_t cap_n = 0;
@@ -194,6 +206,7 @@ struct okt_comm {
 
   // profiling
   bool prof = false;
+  bool graphs_on = std::getenv("OKT_DISABLE_GRAPHS") == nullptr;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   struct Span { int id; cudaEvent_t a, b; };
@@ -278,6 +291,7 @@ struct okt_comm {
     spans.clear();
     ev_used = 0;
     open_id = -1;
+    collect_k1();
   }
 
   // ---- capacity -----------------------------------------------------------------
@@ -300,6 +314,7 @@ struct okt_comm {
     S.s64 = st64.as<uint64_t>();
     S.sidx = stidx.as<uint32_t>();
     S.sval = stval.as<double>();
+    ++buf_gen;  // captured graphs hold these pointers
     if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("reserve: ") + cudaGetErrorString(e));
     cap_n = n;
     return OKT_OK;
@@ -748,9 +763,112 @@ struct okt_comm {
     credit_allgatherv(OKT_PHASE_ALLGATHERV, B.part_sz, 12);
   }
 
+  // Steady single-rank step through one CUDA graph launch.  Returns with the
+  // stream synchronised and h valid.
+  int run_graph_p1(const float* g, const float* eps_in, float* eps_out, float* w, float alpha, size_t n, size_t k,
+                   bool sgd, cudaStream_t s) {
+    int rc;
+    StepGraph& G = graph1;
+    hptrs->g = g;
+    hptrs->eps_in = eps_in;
+    hptrs->eps_out = eps_out;
+    hptrs->w = w;
+    hptrs->alpha = alpha;
+    if (!G.exec || G.n != n || G.k != k || G.sgd != sgd || G.gen != buf_gen || G.prof != prof) {
+      if (G.exec) {
+        cudaGraphExecDestroy(G.exec);
+        G.exec = nullptr;
+      }
+      if (!G.e0) {
+        cudaEventCreate(&G.e0);
+        cudaEventCreate(&G.e1);
+      }
+      if ((rc = ensure(ptrsb, sizeof(okt::StepPtrs)))) return rc;
+      const okt::StepPtrs* dp = ptrsb.as<okt::StepPtrs>();
+      const uint64_t l0 = L.launches;
+      if ((rc = ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture"))) return rc;
+      cudaMemcpyAsync(ptrsb.p, hptrs, sizeof(okt::StepPtrs), cudaMemcpyHostToDevice, s);
+      cudaMemsetAsync(&d()->flags, 0, 4, s);
+      if (prof) cudaEventRecordWithFlags(G.e0, s, cudaEventRecordExternal);
+      okt::ApplyArgs ap;
+      if (sgd) ap = okt::ApplyArgs{nullptr, nullptr, &d()->flags, dp};
+      cudaError_t e = okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, g, eps_in,
+                                     eps_out, alpha, n, &d()->local_th, &d()->global_th,
+                                     okt::OutCoo{nullptr, sur_idx.as<uint32_t>(), sur_val.as<double>()}, &d()->S,
+                                     &d()->m, &d()->flags, nullptr, &ap, nullptr, dp);
+      if (prof) cudaEventRecordWithFlags(G.e1, s, cudaEventRecordExternal);
+      cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t e2 = cudaStreamEndCapture(s, &graph);
+      if (e != cudaSuccess || e2 != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        return ck(e != cudaSuccess ? e : e2, "graph capture");
+      }
+      e = cudaGraphInstantiate(&G.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if ((rc = ck(e, "graph instantiate"))) return rc;
+      G.kernels = L.launches - l0;
+      L.launches = l0;
+      graph1_k1_pairs = k1_used / 2;
+      k1_used = 0;
+      G.n = n;
+      G.k = k;
+      G.sgd = sgd;
+      G.gen = buf_gen;
+      G.prof = prof;
+    }
+    if ((rc = ck(cudaGraphLaunch(G.exec, s), "graph launch"))) return rc;
+    L.launches += G.kernels;
+    if (prof) k1_used = 2 * graph1_k1_pairs;  // the graph re-recorded its K1 events
+    graph_prof_pending = prof;
+    if (defer) return OKT_OK;
+    if ((rc = ck(cudaStreamSynchronize(s), "device"))) return rc;
+    collect_graph_prof();
+    return OKT_OK;
+  }
+  bool graph_prof_pending = false;
+  // K1 phase-A event pairs (profiling); the graph's pairs are reused per launch.
+  std::vector<cudaEvent_t> k1_pool;
+  size_t k1_used = 0;
+  static cudaEvent_t k1_event_cb(void* ctx) {
+    okt_comm* c = static_cast<okt_comm*>(ctx);
+    if (c->k1_used == c->k1_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->k1_pool.push_back(e);
+    }
+    return c->k1_pool[c->k1_used++];
+  }
+  void collect_k1() {
+    for (size_t i = 0; i + 1 < k1_used; i += 2) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, k1_pool[i], k1_pool[i + 1]) == cudaSuccess) {
+        t_ms[OKT_T_K1] += ms;
+        t_calls[OKT_T_K1] += 1;
+      }
+    }
+    cudaGetLastError();
+    k1_used = 0;
+  }
+  size_t graph1_k1_pairs = 0;  // events [0, 2*pairs) belong to the captured graph
+  void collect_graph_prof() {
+    if (!graph_prof_pending) return;
+    graph_prof_pending = false;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, graph1.e0, graph1.e1) == cudaSuccess) {
+      t_ms[OKT_T_SELECT] += ms;
+      t_calls[OKT_T_SELECT] += 1;
+    }
+    cudaGetLastError();
+  }
+
   // ---- the step ---------------------------------------------------------------------
   int step(const float* g, float* w, size_t n, double alpha, int64_t t, size_t k, bool sgd,
            okt_result* out, cudaStream_t s) {
+    if (pending.on) {
+      const int prc = wait_pending(nullptr);
+      if (prc) return prc;
+    }
     if (n == 0 || k < 1 || t < 1)
       return set_err(OKT_ERR_INVALID_ARGUMENT, "ok_sparse_allreduce: empty input, k < 1, or t < 1");
     if (n > 0xffffffffull) return set_err(OKT_ERR_INVALID_ARGUMENT, "n exceeds the u32 index space");
@@ -773,10 +891,11 @@ struct okt_comm {
       cudaEventRecord(step_begin, s);
     }
     if ((rc = upload_state(s))) return rc;
-    if ((rc = ck(cudaMemsetAsync(&d()->flags, 0, 4, s), "memset"))) return rc;
-
     const bool thr = (t - 1) % int64_t(st.tau_prime) == 0;
     const bool bnd = (t - 1) % int64_t(st.tau) == 0;
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    const bool use_graph = P == 1 && !thr && graphs_on && al16(g) && (!sgd || al16(w));
+    if (!use_graph && (rc = ck(cudaMemsetAsync(&d()->flags, 0, 4, s), "memset"))) return rc;
     if (P > 1 && (rc = setup_p2p(n, s))) return rc;
     // Steady iterations on distinct GPUs run the device-driven exchange; the
     // refresh iterations (1 in tau') keep the host-synchronised protocol.
@@ -797,6 +916,21 @@ struct okt_comm {
     }
     uint32_t* hp = hist.as<uint32_t>();
     const float fa = float(alpha);
+    if (use_graph) {
+      if ((rc = run_graph_p1(g, eps_in, eps_out, w, fa, n, k, sgd, s))) return abort_step(rc);
+      if (prof) {
+        cudaEvent_t e = ev_get();
+        cudaEventRecord(e, s);
+        spans.push_back({OKT_T_STEP, step_begin, e});
+      }
+      if (defer_commit(n, t, thr, sgd, std::vector<uint64_t>{0, uint64_t(n)}, sur_idx.as<uint32_t>(),
+                       sur_val.as<double>(), s))
+        return OKT_OK;
+      cudaStreamSynchronize(s);
+      tcollect();
+      return commit_step(n, t, thr, sgd, std::vector<uint64_t>{0, uint64_t(n)}, sur_idx.as<uint32_t>(),
+                         sur_val.as<double>(), out);
+    }
     // P = 1: u is a subset of the local selection, so K7 (w -= u, eps = 0 at u)
     // is fused into the compaction that writes u, and indexes = u.indices.
     okt::ApplyArgs ap1;
@@ -927,21 +1061,75 @@ struct okt_comm {
       cudaEventRecord(e, s);
       spans.push_back({OKT_T_STEP, step_begin, e});
     }
+    if (use_p2p && defer) {
+      cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s);
+      p2p_credit_pending = true;
+      if (defer_commit(n, t, thr, sgd, new_cuts, ui, uv, s)) return OKT_OK;
+    }
     if ((rc = sync(s))) return abort_step(rc);
     tcollect();
+    if (use_p2p) p2p_credit_pending = true;
+    return commit_step(n, t, thr, sgd, new_cuts, ui, uv, out);
+  }
+
+  bool p2p_credit_pending = false;
+  // A step enqueued by okt_sgd_step_async / okt_sparse_allreduce_async whose
+  // readback has not been waited for yet.
+  struct Pending {
+    bool on = false;
+    size_t n = 0;
+    int64_t t = 0;
+    bool thr = false, sgd = false;
+    std::vector<uint64_t> cuts;
+    const uint32_t* ui = nullptr;
+    const double* uv = nullptr;
+    cudaStream_t s = nullptr;
+  } pending;
+  bool defer = false;  // set by the async entry points for the current call
+  bool has_sync_result = false;  // an async call that completed synchronously
+  okt_result last_result{};
+
+  int wait_pending(okt_result* out) {
+    if (!pending.on) return OKT_OK;
+    pending.on = false;
+    const int rc = ck(cudaStreamSynchronize(pending.s), "device");
+    if (rc) return abort_step(rc);
+    tcollect();
+    collect_graph_prof();
+    return commit_step(pending.n, pending.t, pending.thr, pending.sgd, pending.cuts, pending.ui, pending.uv, out);
+  }
+  bool defer_commit(size_t n, int64_t t, bool thr, bool sgd, const std::vector<uint64_t>& cuts, const uint32_t* ui,
+                    const double* uv, cudaStream_t s) {
+    if (!defer) return false;
+    pending = Pending{true, n, t, thr, sgd, cuts, ui, uv, s};
+    return true;
+  }
+  // Error checks + commit of a finished step (h valid, stream synchronised).
+  int commit_step(size_t n, int64_t t, bool thr, bool sgd, const std::vector<uint64_t>& new_cuts,
+                  const uint32_t* ui, const double* uv, okt_result* out) {
+    const bool credit = p2p_credit_pending;
+    p2p_credit_pending = false;
     if (prof) {
-      // Algorithmic bytes: K1 reads g (+ eps) and writes eps and
-      // the m COO entries; refresh iterations add the radix passes over acc.
+      // Algorithmic bytes: K1 reads g (+ eps), writes eps and
+      // emits the COO (8 B per local entry; 12 B per u entry when the
+      // single-rank step emits u directly); refresh iterations add the radix
+      // passes over acc; K7 reads u, gathers acc, updates w and eps.
       const double nn = double(n), mm = double(h->m);
       const double uu = double(P == 1 ? h->S : h->U);
-      double sel = (sgd ? 12.0 * nn : 4.0 * nn) + 8.0 * mm;
-      if (thr && sgd) sel += 4.0 * nn;  // the select-only K1 after the fused accumulate+histogram
+      double sel = (sgd ? 12.0 : 4.0) * nn;
+      if (P == 1 && !thr) {
+        sel += 12.0 * uu;
+      } else {
+        sel += 8.0 * mm;
+        if (thr && sgd) sel += 4.0 * nn;  // the select-only K1 after the fused accumulate+histogram
+      }
       t_bytes[OKT_T_SELECT] += sel;
+      // the streaming kernel alone: reads g (+ eps), writes eps and 8 B per staged entry
+      t_bytes[OKT_T_K1] += (sgd ? 12.0 : 4.0) * nn + 8.0 * ((P == 1 && !thr) ? uu : mm) +
+                           ((thr && sgd) ? 4.0 * nn : 0.0);
       if (thr) t_bytes[OKT_T_THRESHOLD] += (sgd ? 2.0 : 3.0) * 4.0 * nn;
-      // K7: read u (12 B), gather acc (4 B), w read+write (8 B), eps zero (4 B).
-      t_bytes[OKT_T_APPLY] += uu * (sgd ? 28.0 : 16.0);
+      if (P > 1) t_bytes[OKT_T_APPLY] += uu * (sgd ? 28.0 : 16.0);
     }
-
     if (h->flags & 1u) {
       dev_stale = true;
       return set_err(OKT_ERR_NUMERIC, "ok_sparse_allreduce: non-finite input");
@@ -954,7 +1142,7 @@ struct okt_comm {
       dev_stale = true;
       return set_err(OKT_ERR_TRANSPORT, "TransportError: a peer failed (non-finite input)");
     }
-    if (use_p2p) p2p_credit();
+    if (credit) p2p_credit();
     if (h->flags & 2u) {
       dev_stale = true;
       return set_err(OKT_ERR_PROTOCOL, "split_and_reduce: entries outside my region");
@@ -1034,6 +1222,7 @@ int init_comm(okt_comm* c) {
   if (e == cudaSuccess) e = cudaMallocHost(&c->h, sizeof(DevScalars));
   if (e == cudaSuccess) e = cudaMallocHost(&c->hup, sizeof(DevScalars));
   if (e == cudaSuccess) e = cudaMallocHost(&c->hplan, sizeof(okt::P2PPlan));
+  if (e == cudaSuccess) e = cudaMallocHost(&c->hptrs, sizeof(okt::StepPtrs));
   if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("init: ") + cudaGetErrorString(e));
   std::memset(c->h, 0, sizeof(DevScalars));
   std::memset(c->hup, 0, sizeof(DevScalars));
@@ -1167,6 +1356,12 @@ int okt_comm_destroy(okt_comm* c) {
   if (c->h) cudaFreeHost(c->h);
   if (c->hup) cudaFreeHost(c->hup);
   if (c->hplan) cudaFreeHost(c->hplan);
+  if (c->hptrs) cudaFreeHost(c->hptrs);
+  if (c->graph1.exec) cudaGraphExecDestroy(c->graph1.exec);
+  if (c->graph1.e0) {
+    cudaEventDestroy(c->graph1.e0);
+    cudaEventDestroy(c->graph1.e1);
+  }
   c->close_peers();
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
@@ -1188,8 +1383,14 @@ int okt_comm_reserve(okt_comm* c, size_t n) {
   return rc;
 }
 
-int okt_get_state(const okt_comm* c, okt_state* out) {
-  OKT_COMM_CHECK(c);
+int okt_get_state(const okt_comm* cc, okt_state* out) {
+  OKT_COMM_CHECK(cc);
+  okt_comm* c = const_cast<okt_comm*>(cc);
+  if (c->pending.on) {
+    DeviceGuard g(c->device);
+    const int rc = c->wait_pending(nullptr);
+    if (rc) return rc;
+  }
   if (!out) return set_err(OKT_ERR_INVALID_ARGUMENT, "null out");
   *out = c->st;
   return OKT_OK;
@@ -1197,6 +1398,11 @@ int okt_get_state(const okt_comm* c, okt_state* out) {
 
 int okt_set_state(okt_comm* c, const okt_state* in) {
   OKT_COMM_CHECK(c);
+  if (c->pending.on) {
+    DeviceGuard g(c->device);
+    const int rc = c->wait_pending(nullptr);
+    if (rc) return rc;
+  }
   if (!in) return set_err(OKT_ERR_INVALID_ARGUMENT, "null state");
   c->st = *in;
   c->dev_stale = true;
@@ -1212,8 +1418,14 @@ int okt_set_params(okt_comm* c, uint32_t tau, uint32_t tau_prime, uint32_t bucke
   return OKT_OK;
 }
 
-int okt_ledger(const okt_comm* c, int phase, okt_counters* out) {
-  OKT_COMM_CHECK(c);
+int okt_ledger(const okt_comm* cc, int phase, okt_counters* out) {
+  OKT_COMM_CHECK(cc);
+  okt_comm* c = const_cast<okt_comm*>(cc);
+  if (c->pending.on) {
+    DeviceGuard g(c->device);
+    const int rc = c->wait_pending(nullptr);
+    if (rc) return rc;
+  }
   if (phase < 0 || phase >= OKT_PHASE_COUNT || !out) return set_err(OKT_ERR_INVALID_ARGUMENT, "bad phase");
   *out = c->ledger[phase];
   return OKT_OK;
@@ -1234,14 +1446,60 @@ int okt_sparse_allreduce(okt_comm* c, const float* d_acc, size_t n, int64_t t, s
   return c->step(d_acc, nullptr, n, 0.0, t, k, false, out, c->pick(stream));
 }
 
+int okt_sparse_allreduce_async(okt_comm* c, const float* d_acc, size_t n, int64_t t, size_t k, void* stream) {
+  OKT_COMM_CHECK(c);
+  DeviceGuard g(c->device);
+  int rc = c->reserve(n);
+  if (rc) return rc;
+  c->defer = true;
+  c->has_sync_result = false;
+  rc = c->step(d_acc, nullptr, n, 0.0, t, k, false, &c->last_result, c->pick(stream));
+  c->defer = false;
+  c->has_sync_result = rc == OKT_OK && !c->pending.on;
+  return rc;
+}
+
+int okt_sgd_step_async(okt_comm* c, const float* d_grad, float* d_w, size_t n, double alpha, int64_t t, size_t k,
+                       void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!d_w) return set_err(OKT_ERR_INVALID_ARGUMENT, "null model");
+  DeviceGuard g(c->device);
+  int rc = c->reserve(n);
+  if (rc) return rc;
+  c->defer = true;
+  c->has_sync_result = false;
+  rc = c->step(d_grad, d_w, n, alpha, t, k, true, &c->last_result, c->pick(stream));
+  c->defer = false;
+  c->has_sync_result = rc == OKT_OK && !c->pending.on;
+  return rc;
+}
+
+int okt_step_wait(okt_comm* c, okt_result* out) {
+  OKT_COMM_CHECK(c);
+  DeviceGuard g(c->device);
+  if (!c->pending.on) {
+    if (!c->has_sync_result) return set_err(OKT_ERR_INVALID_ARGUMENT, "no step in flight");
+    c->has_sync_result = false;
+    if (out) *out = c->last_result;
+    return OKT_OK;
+  }
+  return c->wait_pending(out);
+}
+
 int okt_residual_reset(okt_comm* c, size_t n, const float* d_init, void* stream) {
   OKT_COMM_CHECK(c);
+  if (c->pending.on && c->wait_pending(nullptr)) return OKT_ERR_INTERNAL;
   DeviceGuard g(c->device);
   return c->residual_reset(n, d_init, c->pick(stream));
 }
 
 int okt_residual(okt_comm* c, float** d_eps, size_t* n) {
   OKT_COMM_CHECK(c);
+  if (c->pending.on) {
+    DeviceGuard g(c->device);
+    const int rc = c->wait_pending(nullptr);
+    if (rc) return rc;
+  }
   if (d_eps) *d_eps = c->eps_n ? c->eps[c->eps_cur].as<float>() : nullptr;
   if (n) *n = c->eps_n;
   return OKT_OK;
@@ -1531,6 +1789,8 @@ int okt_plan_ledger(int rank, int P, int kind, const uint64_t* sizes, uint64_t l
 int okt_set_profiling(okt_comm* c, int on) {
   OKT_COMM_CHECK(c);
   c->prof = on != 0;
+  c->L.k1_event = c->prof ? &okt_comm::k1_event_cb : nullptr;
+  c->L.k1_ctx = c;
   return OKT_OK;
 }
 

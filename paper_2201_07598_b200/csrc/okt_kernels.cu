@@ -71,6 +71,10 @@ __global__ void __launch_bounds__(kThreads)
                    uint64_t* d_total, uint64_t* d_total2, ApplyArgs ap, PubSur pub) {
   __shared__ uint64_t red[kWarps];
   __shared__ int s_last;
+  if (APPLY && ap.ind) {
+    ap.acc = ap.ind->eps_out;
+    ap.w = ap.ind->w;
+  }
   const int c = blockIdx.x, G = gridDim.x;
   const uint64_t cnt = counts[c];
   const uint64_t cap = d_cap ? *d_cap : cap_host;
@@ -180,7 +184,7 @@ static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_
                                   double* oval, uint64_t* d_total, uint64_t* d_total2,
                                   const ApplyArgs* ap = nullptr, const PubSur* pub = nullptr) {
   const PubSur pb = pub ? *pub : PubSur{};
-  if (ap && ap->w)
+  if (ap && (ap->w || ap->ind))
     compact_kernel<MODE, true><<<G, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts,
                                                         with2 ? S.counts2 : nullptr, cap_host, d_cap, o64, oidx,
                                                         oval, d_total, d_total2, *ap, pb);
@@ -200,8 +204,14 @@ __global__ void __launch_bounds__(kThreads)
     k1_kernel(const float* __restrict__ g, const float* eps_in, float* eps_out, float alpha, uint64_t n,
               uint32_t tiles, uint32_t tpc, const double* __restrict__ d_th,
               const double* __restrict__ d_th2, uint64_t* __restrict__ stg, uint32_t* counts,
-              uint32_t* counts2, uint32_t* d_flags, uint32_t* d_hist) {
+              uint32_t* counts2, uint32_t* d_flags, uint32_t* d_hist, const StepPtrs* ind) {
   constexpr int C = 4, TILE = kJ * C * kThreads;
+  if (ind) {
+    g = ind->g;
+    eps_in = ind->eps_in;
+    eps_out = ind->eps_out;
+    alpha = ind->alpha;
+  }
   __shared__ uint32_t tbl[2][32];
   __shared__ uint32_t s_hist[HIST ? 2048 : 1];
   __shared__ uint64_t red[kWarps];
@@ -326,7 +336,8 @@ template <bool ACCUM, bool SELECT, bool HIST, bool DUAL>
 static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float* g, const float* eps_in,
                                float* eps_out, float alpha, uint64_t n, const double* d_th,
                                const double* d_th2, const OutCoo& out, uint64_t* d_m, uint64_t* d_m2,
-                               uint32_t* d_flags, uint32_t* d_hist, const ApplyArgs* ap, const PubL* pub) {
+                               uint32_t* d_flags, uint32_t* d_hist, const ApplyArgs* ap, const PubL* pub,
+                               const StepPtrs* ind) {
   constexpr int TILE = kJ * 4 * kThreads;
   const uint64_t tiles = (n + TILE - 1) / TILE;
   auto kern = vec ? k1_kernel<ACCUM, SELECT, HIST, true, DUAL> : k1_kernel<ACCUM, SELECT, HIST, false, DUAL>;
@@ -335,8 +346,10 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
   if (!cap) cap = resident_ctas(kern, kThreads, L.sms);
   const uint32_t G = chunks_for(tiles, cap, S.max_chunks);
   const uint32_t tpc = uint32_t((tiles + G - 1) / G);
+  if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, cudaEventRecordExternal);
   kern<<<G, kThreads, 0, L.s>>>(g, eps_in, eps_out, alpha, n, uint32_t(tiles), tpc, d_th, d_th2, S.s64, S.counts,
-                                S.counts2, d_flags, d_hist);
+                                S.counts2, d_flags, d_hist, ind);
+  if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, cudaEventRecordExternal);
   ++L.launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !SELECT) return e;
@@ -350,7 +363,7 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
 cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, const float* eps_in,
                       float* eps_out, float alpha, uint64_t n, const double* d_th, const double* d_th2,
                       const OutCoo& out, uint64_t* d_m, uint64_t* d_m2, uint32_t* d_flags, uint32_t* d_hist,
-                      const ApplyArgs* ap, const PubL* pub) {
+                      const ApplyArgs* ap, const PubL* pub, const StepPtrs* ind) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   bool vec = al(g);
   if (mode != K1Mode::kSelect) vec = vec && al(eps_in) && al(eps_out);
@@ -358,17 +371,17 @@ cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, co
   switch (mode) {
     case K1Mode::kSelect:
       return dual ? k1_dispatch<false, true, false, true>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out,
-                                                           d_m, d_m2, d_flags, d_hist, ap, pub)
+                                                           d_m, d_m2, d_flags, d_hist, ap, pub, ind)
                   : k1_dispatch<false, true, false, false>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2,
-                                                            out, d_m, d_m2, d_flags, d_hist, ap, pub);
+                                                            out, d_m, d_m2, d_flags, d_hist, ap, pub, ind);
     case K1Mode::kAccumSelect:
       return dual ? k1_dispatch<true, true, false, true>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out,
-                                                          d_m, d_m2, d_flags, d_hist, ap, pub)
+                                                          d_m, d_m2, d_flags, d_hist, ap, pub, ind)
                   : k1_dispatch<true, true, false, false>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out,
-                                                           d_m, d_m2, d_flags, d_hist, ap, pub);
+                                                           d_m, d_m2, d_flags, d_hist, ap, pub, ind);
     case K1Mode::kAccumHist:
       return k1_dispatch<true, false, true, false>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out, d_m,
-                                                   d_m2, d_flags, d_hist, ap, pub);
+                                                   d_m2, d_flags, d_hist, ap, pub, ind);
   }
   return cudaErrorInvalidValue;
 }

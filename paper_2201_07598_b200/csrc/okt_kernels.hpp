@@ -13,6 +13,10 @@ struct Launch {
   cudaStream_t s = nullptr;
   uint64_t launches = 0;        // kernels launched through this context
   int sms = 148;
+  // Profiling: when set, the K1 streaming kernel (phase A) is bracketed by a
+  // pair of events from this pool (also captured into CUDA graphs).
+  cudaEvent_t (*k1_event)(void* ctx) = nullptr;
+  void* k1_ctx = nullptr;
 };
 
 struct RadixState {
@@ -48,11 +52,23 @@ struct OutCoo {
   double* val = nullptr;
 };
 
+// Per-step pointers read from device memory, so one captured CUDA graph serves
+// every steady step (the graph refreshes this block from pinned host memory).
+struct StepPtrs {
+  const float* g;
+  const float* eps_in;
+  float* eps_out;
+  float* w;
+  float alpha;
+  float pad;
+};
+
 // Fused K7 for the single-rank path (every entry of u is locally selected).
 struct ApplyArgs {
   float* acc = nullptr;   // residual buffer holding acc; zeroed at u's indices
   float* w = nullptr;     // model; w[i] -= u_i
   uint32_t* d_flags = nullptr;
+  const StepPtrs* ind = nullptr;  // when set, acc / w come from here
 };
 
 // Split-phase receive segments for the region scatter (M1): one per source.
@@ -74,7 +90,8 @@ struct Segs {
 cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, const float* eps_in,
                       float* eps_out, float alpha, uint64_t n, const double* d_th, const double* d_th2,
                       const OutCoo& out, uint64_t* d_m, uint64_t* d_m2, uint32_t* d_flags,
-                      uint32_t* d_hist, const ApplyArgs* ap = nullptr, const PubL* pub = nullptr);
+                      uint32_t* d_hist, const ApplyArgs* ap = nullptr, const PubL* pub = nullptr,
+                      const StepPtrs* ind = nullptr);
 
 // K2/K4: exact k-th largest magnitude (k clamped to the element count) by MSD
 // radix select on the IEEE bit patterns; writes the threshold to *d_th_out

@@ -384,3 +384,47 @@ def test_gpu_reproduces_reference_golden(okm, gpus, name):
         prev = led
         for r in range(1, P):
             assert got[r].u == got[0].u
+
+
+# ---- asynchronous entry points (okt_*_async + okt_step_wait) ----
+@pytest.mark.parametrize("P", [1, 2])
+def test_async_steps_match_sync_steps(okm, oracle, gpus, P):
+    import ctypes
+    import torch
+    from paper_2201_07598_b200 import _lib
+    L = _lib.lib()
+    n, k, steps = 50_000, 500, 40
+    worlds = [gpu_world(okm, P, gpus), gpu_world(okm, P, gpus)]
+    for w in worlds:
+        for r in range(P):
+            assert L.okt_set_params(w.ctx(r).comm, 8, 4, 2) == 0
+    grads = {(t, r): torch.from_numpy(oracle.drift(t, 4, n, r + 1).astype(np.float32)).to(f"cuda:{w.devices[r]}")
+             for t in range(1, steps + 1) for r in range(P) for w in worlds[:1]}
+    models = [[torch.zeros(n, dtype=torch.float32, device=f"cuda:{w.devices[r]}") for r in range(P)] for w in worlds]
+
+    def run(wi, asynchronous):
+        w = worlds[wi]
+
+        def body(ctx):
+            torch.cuda.set_device(w.devices[ctx.rank])
+            out = []
+            for t in range(1, steps + 1):
+                g = grads[(t, ctx.rank)].to(f"cuda:{w.devices[ctx.rank]}")
+                res = _lib.OktResult()
+                args = (ctx.comm, ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(models[wi][ctx.rank].data_ptr()),
+                        n, 1.0, t, k)
+                if asynchronous:
+                    assert L.okt_sgd_step_async(*args, None) == 0, L.okt_last_error()
+                    assert L.okt_step_wait(ctx.comm, ctypes.byref(res)) == 0, L.okt_last_error()
+                else:
+                    assert L.okt_sgd_step(*args, ctypes.byref(res), None) == 0, L.okt_last_error()
+                out.append(okm._sparse_from(res.u, n))
+            return out
+        return okm.run_ranks(w, body)
+
+    a = run(0, False)
+    b = run(1, True)
+    for r in range(P):
+        for t in range(steps):
+            assert a[r][t] == b[r][t], (r, t)
+        assert torch.equal(models[0][r].cpu(), models[1][r].cpu())
