@@ -166,7 +166,7 @@ def _cpu_model() -> str:
     return "unknown"
 
 
-def trace_steps(args, rank, stream, step, t0):
+def trace_steps(args, rank, stream, step, t0, step_async=None, wait=None, flush=None):
     """CUPTI timeline of 16 steps: per-kernel device time and the idle gaps
     between them (host launch / sync latency), written next to a chrome trace."""
     import torch
@@ -174,7 +174,13 @@ def trace_steps(args, rank, stream, step, t0):
     os.makedirs(args.trace, exist_ok=True)
     with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
         for i in range(16):
-            step(t0 + 1 + i)
+            if step_async is not None:
+                with torch.cuda.stream(stream):
+                    flush.fill_(i & 0xff)
+                step_async(t0 + 1 + i)
+                wait()
+            else:
+                step(t0 + 1 + i)
         torch.cuda.synchronize()
     prof.export_chrome_trace(os.path.join(args.trace, f"trace_rank{rank}.json"))
     ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
@@ -271,11 +277,9 @@ def run_okt(args):
         step(t)
     barrier()
     if args.trace:
-        trace_steps(args, rank, stream, step, t)
+        trace_steps(args, rank, stream, step, t, step_async, wait, flush)
         t += 16
-    # ---- timed device-resident run
-    L.okt_set_profiling(comm, 1)
-    L.okt_reset_phase_times(comm)
+    # ---- timed device-resident run (no profiling events inside the steps)
     launches0 = ctypes.c_uint64()
     L.okt_kernel_launches(comm, ctypes.byref(launches0))
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -301,7 +305,19 @@ def run_okt(args):
     L.okt_kernel_launches(comm, ctypes.byref(launches1))
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
+    # ---- the same timed loop again with the library's per-phase CUDA events
+    # on its stream (phase breakdown + the K1 roofline)
     from paper_2201_07598_b200._lib import OKT_T_COUNT, TIMER_NAMES
+    L.okt_set_profiling(comm, 1)
+    L.okt_reset_phase_times(comm)
+    barrier()
+    for i in range(args.steps):
+        t += 1
+        with torch.cuda.stream(stream):
+            flush.fill_(i & 0xff)
+        step_async(t)
+        wait()
+    barrier()
     ms_t = (ctypes.c_double * OKT_T_COUNT)()
     calls = (ctypes.c_uint64 * OKT_T_COUNT)()
     byts = (ctypes.c_double * OKT_T_COUNT)()

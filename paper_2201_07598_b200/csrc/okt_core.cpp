@@ -1791,6 +1791,17 @@ int okt_set_profiling(okt_comm* c, int on) {
   c->prof = on != 0;
   c->L.k1_event = c->prof ? &okt_comm::k1_event_cb : nullptr;
   c->L.k1_ctx = c;
+  // Events are created up front: creation is not allowed inside a capture.
+  while (c->prof && c->k1_pool.size() < 16) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    c->k1_pool.push_back(e);
+  }
+  while (c->prof && c->ev_pool.size() < 64) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    c->ev_pool.push_back(e);
+  }
   return OKT_OK;
 }
 

@@ -346,10 +346,15 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
   if (!cap) cap = resident_ctas(kern, kThreads, L.sms);
   const uint32_t G = chunks_for(tiles, cap, S.max_chunks);
   const uint32_t tpc = uint32_t((tiles + G - 1) / G);
-  if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, cudaEventRecordExternal);
+  // Profiling events: inside a stream capture they must be external event
+  // nodes (re-recorded at every graph launch); outside, plain records.
+  cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+  if (L.k1_event) cudaStreamIsCapturing(L.s, &cap_st);
+  const unsigned ev_flags = cap_st == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, ev_flags);
   kern<<<G, kThreads, 0, L.s>>>(g, eps_in, eps_out, alpha, n, uint32_t(tiles), tpc, d_th, d_th2, S.s64, S.counts,
                                 S.counts2, d_flags, d_hist, ind);
-  if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, cudaEventRecordExternal);
+  if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, ev_flags);
   ++L.launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !SELECT) return e;
