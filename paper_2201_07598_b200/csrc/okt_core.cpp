@@ -180,7 +180,9 @@ struct okt_comm {
   okt::Stage S;
   // device-driven multi-GPU exchange (okt_p2p.cuh)
   bool p2p_checked = false, p2p = false;
-  Buf win, planb, boot, tabd, pdone, plt;
+  Buf win, planb, boot, tabd, pdone, plt, selflags;
+  const float* cur_acc = nullptr;  // the step's accumulator / model (P2P fused apply)
+  float* cur_w = nullptr;
   size_t win_n = 0;
   okt::PeerTab tab{};
   std::vector<void*> ipc_open;
@@ -691,6 +693,7 @@ struct okt_comm {
     if ((rc = ensure(tabd, sizeof(okt::PeerTab)))) return rc;
     if ((rc = ck(cudaMemcpy(tabd.p, &tab, sizeof(okt::PeerTab), cudaMemcpyHostToDevice), "tab"))) return rc;
     if ((rc = ensure(indexes, 4 * std::max<size_t>(n, 1)))) return rc;
+    if ((rc = ensure(selflags, std::max<size_t>(n, 1)))) return rc;
     win_n = n;
     return OKT_OK;
   }
@@ -698,11 +701,10 @@ struct okt_comm {
   // Steady iteration on the P2P window (no host round trip until the end).
   // K1 (with its fused publication, see pub_L) already wrote the local
   // selection into tab.L[rank][par] and raised L-ready at every peer.
-  okt::PubL pub_L(uint64_t epoch, int par) {
+  okt::PubL pub_L(const okt::StepPtrs* sp) {
     okt::PubL pb;
     pb.tab = tabd.as<okt::PeerTab>();
-    pb.epoch = epoch;
-    pb.par = par;
+    pb.sp = sp;
     pb.P = P;
     pb.done = pdone.as<uint32_t>();
     pb.lt = plt.as<uint32_t>();
@@ -712,31 +714,105 @@ struct okt_comm {
     return pb;
   }
 
-  int p2p_steady(uint64_t epoch, int par, cudaStream_t s) {
+  // Enqueues a whole steady P2P iteration on `s` (no host synchronisation):
+  // step block refresh, flag reset, K1 (+ slice offsets + L publication),
+  // fused split/scatter, bracket scan (+ survivor publication), allgatherv
+  // pull with the fused apply, indexes, scalar readback.  Per-step values
+  // (pointers, epoch, parity) are read from ptrsb on the device, so the same
+  // sequence is captured once into a CUDA graph.
+  int enqueue_p2p_step(size_t n, size_t k, bool sgd, cudaStream_t s) {
+    const okt::StepPtrs* sp = ptrsb.as<okt::StepPtrs>();
     okt::P2PPlan* dp = planb.as<okt::P2PPlan>();
     const okt::PeerTab* dt = tabd.as<okt::PeerTab>();
     const uint64_t lo = st.cuts[rank], hi = st.cuts[rank + 1];
     const uint64_t W = hi > lo ? hi - lo : 0;
-    int rc;
-    if ((rc = ensure(mask, ((W + 15) / 16) * 16 + 16)) || (rc = ensure(stage, 4 * std::max<uint64_t>(W, 1) * P)))
-      return rc;
+    (void)k;
+    int rc = ck(cudaMemcpyAsync(ptrsb.p, hptrs, sizeof(okt::StepPtrs), cudaMemcpyHostToDevice, s), "h2d");
+    if (!rc) rc = ck(cudaMemsetAsync(&d()->flags, 0, 4, s), "memset");
+    tmark(OKT_T_SELECT, s);
+    const okt::PubL pl = pub_L(sp);
+    if (!rc)
+      rc = ck(okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, hptrs->g, hptrs->eps_in,
+                             hptrs->eps_out, hptrs->alpha, n, &d()->local_th, nullptr,
+                             okt::OutCoo{tab.L[rank][0]}, &d()->m, nullptr, &d()->flags, nullptr, nullptr, &pl, sp),
+              "k1");
     tmark(OKT_T_MERGE, s);
-    rc = ck(okt::launch_p2p_scatter(L, dt, P, epoch, par, d()->off, dp, lo, W, mask.as<uint32_t>(),
-                                    stage.as<float>(), &d()->flags, kP2PTimeoutNs), "p2p");
+    if (!rc) rc = ck(okt::launch_p2p_scatter(L, dt, sp, d()->off, dp, lo, W, mask.as<uint32_t>(), stage.as<float>(),
+                                             &d()->flags, kP2PTimeoutNs), "p2p");
     okt::PubSur ps;
     ps.tab = dt;
-    ps.epoch = epoch;
-    ps.par = par;
+    ps.sp = sp;
     ps.done = pdone.as<uint32_t>() + 1;
     ps.flags = &d()->flags;
     if (!rc) rc = ck(okt::launch_region_scan(L, S, P, true, lo, W, mask.as<uint32_t>(), stage.as<float>(),
-                                             &d()->global_th, tab.sur_idx[rank][par], tab.sur_val[rank][par],
-                                             &d()->S, &ps), "region_scan");
+                                             &d()->global_th, tab.sur_idx[rank][0], tab.sur_val[rank][0], &d()->S,
+                                             &ps), "region_scan");
     tmark(OKT_T_ALLGATHER, s);
-    if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, P, epoch, par, &d()->S, dp, &d()->U, &d()->flags,
-                                                kP2PTimeoutNs), "p2p");
+    okt::P2PApply pa;
+    pa.on = 1;
+    pa.sgd = sgd ? 1 : 0;
+    pa.d_local_th = &d()->local_th;
+    pa.sel = selflags.as<uint8_t>();
+    if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, sp, &d()->S, dp, &d()->U, &d()->flags, kP2PTimeoutNs, pa),
+                     "p2p");
+    tmark(OKT_T_APPLY, s);
+    if (!rc) rc = ck(okt::launch_select_flags(L, S, selflags.as<uint8_t>(), dt, sp, &d()->U, win_n,
+                                              indexes.as<uint32_t>(), &d()->nidx, &d()->flags), "indexes");
+    tstop(s);
     if (!rc) rc = ck(cudaMemcpyAsync(hplan, dp, sizeof(okt::P2PPlan), cudaMemcpyDeviceToHost, s), "d2h");
+    if (!rc) rc = ck(cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s), "d2h");
     return rc;
+  }
+
+  struct P2PGraph {
+    cudaGraphExec_t exec = nullptr;
+    size_t n = 0, k = 0;
+    bool sgd = false;
+    uint64_t lo = 0, W = 0, gen = 0, win = 0, kernels = 0;
+  } graph2;
+
+  // The steady P2P iteration through one graph launch (captured on first use
+  // and whenever the buffers or the owned region change).
+  int launch_p2p_step(size_t n, size_t k, bool sgd, cudaStream_t s) {
+    int rc;
+    const uint64_t lo = st.cuts[rank], hi = st.cuts[rank + 1];
+    const uint64_t W = hi > lo ? hi - lo : 0;
+    if ((rc = ensure(mask, ((W + 15) / 16) * 16 + 16)) || (rc = ensure(stage, 4 * std::max<uint64_t>(W, 1) * P)) ||
+        (rc = ensure(ptrsb, sizeof(okt::StepPtrs))))
+      return rc;
+    if (prof || !graphs_on) return enqueue_p2p_step(n, k, sgd, s);
+    P2PGraph& G = graph2;
+    const uint64_t gen = buf_gen + reinterpret_cast<uintptr_t>(mask.p) + reinterpret_cast<uintptr_t>(stage.p);
+    if (!G.exec || G.n != n || G.k != k || G.sgd != sgd || G.lo != lo || G.W != W || G.gen != gen || G.win != win_n) {
+      if (G.exec) {
+        cudaGraphExecDestroy(G.exec);
+        G.exec = nullptr;
+      }
+      const uint64_t l0 = L.launches;
+      if ((rc = ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture"))) return rc;
+      rc = enqueue_p2p_step(n, k, sgd, s);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t e2 = cudaStreamEndCapture(s, &graph);
+      if (rc || e2 != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc ? rc : ck(e2, "graph capture");
+      }
+      const cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if ((rc = ck(e, "graph instantiate"))) return rc;
+      G.kernels = L.launches - l0;
+      L.launches = l0;
+      G.n = n;
+      G.k = k;
+      G.sgd = sgd;
+      G.lo = lo;
+      G.W = W;
+      G.gen = gen;
+      G.win = win_n;
+    }
+    if ((rc = ck(cudaGraphLaunch(G.exec, s), "graph launch"))) return rc;
+    L.launches += G.kernels;
+    return OKT_OK;
   }
 
   // Ledger of a P2P step, from the sizes every rank agreed on (h / hplan valid).
@@ -895,11 +971,11 @@ struct okt_comm {
     const bool bnd = (t - 1) % int64_t(st.tau) == 0;
     auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
     const bool use_graph = P == 1 && !thr && graphs_on && al16(g) && (!sgd || al16(w));
-    if (!use_graph && (rc = ck(cudaMemsetAsync(&d()->flags, 0, 4, s), "memset"))) return rc;
     if (P > 1 && (rc = setup_p2p(n, s))) return rc;
     // Steady iterations on distinct GPUs run the device-driven exchange; the
     // refresh iterations (1 in tau') keep the host-synchronised protocol.
-    const bool use_p2p = p2p && !thr && !bnd && st.regions == P;
+    const bool use_p2p = p2p && !thr && !bnd && st.regions == P && al16(g) && (!sgd || al16(w));
+    if (!use_graph && !use_p2p && (rc = ck(cudaMemsetAsync(&d()->flags, 0, 4, s), "memset"))) return rc;
     uint64_t epoch = 0;
     int par = 0;
     if (use_p2p) {
@@ -930,6 +1006,27 @@ struct okt_comm {
       tcollect();
       return commit_step(n, t, thr, sgd, std::vector<uint64_t>{0, uint64_t(n)}, sur_idx.as<uint32_t>(),
                          sur_val.as<double>(), out);
+    }
+    if (use_p2p) {
+      hptrs->g = g;
+      hptrs->eps_in = eps_in;
+      hptrs->eps_out = eps_out;
+      hptrs->w = sgd ? w : nullptr;
+      hptrs->alpha = fa;
+      hptrs->epoch = epoch;
+      hptrs->par = par;
+      if ((rc = launch_p2p_step(n, k, sgd, s))) return abort_step(rc);
+      if (prof) {
+        cudaEvent_t e = ev_get();
+        cudaEventRecord(e, s);
+        spans.push_back({OKT_T_STEP, step_begin, e});
+      }
+      const std::vector<uint64_t> cuts(st.cuts, st.cuts + P + 1);
+      p2p_credit_pending = true;
+      if (defer_commit(n, t, thr, sgd, cuts, tab.u_idx[rank][par], tab.u_val[rank][par], s)) return OKT_OK;
+      if ((rc = ck(cudaStreamSynchronize(s), "device"))) return abort_step(rc);
+      tcollect();
+      return commit_step(n, t, thr, sgd, cuts, tab.u_idx[rank][par], tab.u_val[rank][par], out);
     }
     // P = 1: u is a subset of the local selection, so K7 (w -= u, eps = 0 at u)
     // is fused into the compaction that writes u, and indexes = u.indices.
@@ -966,11 +1063,9 @@ struct okt_comm {
                              &d()->flags, nullptr, &ap1), "k1");
     } else {
       tmark(OKT_T_SELECT, s);
-      const okt::PubL pl = use_p2p ? pub_L(epoch, par) : okt::PubL{};
       rc = ck(okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, g, eps_in, eps_out, fa,
-                             n, &d()->local_th, nullptr,
-                             okt::OutCoo{use_p2p ? tab.L[rank][par] : coo.as<uint64_t>()}, &d()->m, nullptr,
-                             &d()->flags, nullptr, nullptr, use_p2p ? &pl : nullptr), "k1");
+                             n, &d()->local_th, nullptr, okt::OutCoo{coo.as<uint64_t>()}, &d()->m, nullptr,
+                             &d()->flags, nullptr), "k1");
     }
     if (rc) return abort_step(rc);
 
@@ -997,7 +1092,7 @@ struct okt_comm {
       new_cuts[0] = 0;
       new_cuts[1] = n;
     } else if (use_p2p) {
-      rc = p2p_steady(epoch, par, s);
+      // (K1 ran inside launch_p2p_step, issued before the K1 section above)
       if (rc) return abort_step(rc);
       for (int q = 0; q <= P; ++q) new_cuts[q] = st.cuts[q];
       d_U = &d()->U;
@@ -1048,8 +1143,8 @@ struct okt_comm {
       uv = u_val.as<double>();
     }
 
-    // ---- K7 (fused into the compaction for P = 1) ----
-    if (P > 1) {
+    // ---- K7 (fused into the compaction for P = 1, into the pull on the P2P path) ----
+    if (P > 1 && !use_p2p) {
       tmark(OKT_T_APPLY, s);
       rc = ck(okt::launch_apply(L, S, ui, uv, d_U, U_bound, const_cast<float*>(acc), sgd, sgd ? w : nullptr, P,
                                 &d()->local_th, indexes.as<uint32_t>(), &d()->nidx, &d()->flags), "apply");

@@ -67,13 +67,17 @@ __global__ void __launch_bounds__(kThreads)
     compact_kernel(const uint64_t* __restrict__ s64, const uint32_t* __restrict__ sidx,
                    const double* __restrict__ sval, const uint32_t* __restrict__ counts,
                    const uint32_t* __restrict__ counts2, uint64_t cap_host, const uint64_t* d_cap,
-                   uint64_t* __restrict__ o64, uint32_t* __restrict__ oidx, double* __restrict__ oval,
+                   uint64_t* __restrict__ o64, uint32_t* oidx, double* oval,
                    uint64_t* d_total, uint64_t* d_total2, ApplyArgs ap, PubSur pub) {
   __shared__ uint64_t red[kWarps];
   __shared__ int s_last;
   if (APPLY && ap.ind) {
     ap.acc = ap.ind->eps_out;
     ap.w = ap.ind->w;
+  }
+  if (MODE == 2 && pub.tab) {  // P2P: survivors go to this step's window slot
+    oidx = pub.tab->sur_idx[pub.tab->rank][pub.sp->par];
+    oval = pub.tab->sur_val[pub.tab->rank][pub.sp->par];
   }
   const int c = blockIdx.x, G = gridDim.x;
   const uint64_t cnt = counts[c];
@@ -165,16 +169,16 @@ __global__ void __launch_bounds__(kThreads)
     for (int q = threadIdx.x; q < G; q += kThreads) tot += counts[q];
     tot = block_sum(tot, red);
     const PeerTab* tab = pub.tab;
-    const int me = tab->rank, P = tab->P;
+    const int me = tab->rank, P = tab->P, par = pub.sp->par;
     if (threadIdx.x == 0) {
-      tab->hdr[me]->pub[pub.par].S = tot;
-      tab->hdr[me]->pub[pub.par].status = (*pub.flags & (1u | 8u | 16u)) ? 1 : 0;
+      tab->hdr[me]->pub[par].S = tot;
+      tab->hdr[me]->pub[par].status = (*pub.flags & (1u | 8u | 16u)) ? 1 : 0;
       *pub.done = 0;
     }
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x < P && int(threadIdx.x) != me)
-      st_release_sys(&tab->hdr[threadIdx.x]->flag[kFlagSurReady][me], pub.epoch);
+      st_release_sys(&tab->hdr[threadIdx.x]->flag[kFlagSurReady][me], pub.sp->epoch);
   }
 }
 
@@ -204,8 +208,18 @@ __global__ void __launch_bounds__(kThreads)
     k1_kernel(const float* __restrict__ g, const float* eps_in, float* eps_out, float alpha, uint64_t n,
               uint32_t tiles, uint32_t tpc, const double* __restrict__ d_th,
               const double* __restrict__ d_th2, uint64_t* __restrict__ stg, uint32_t* counts,
-              uint32_t* counts2, uint32_t* d_flags, uint32_t* d_hist, const StepPtrs* ind) {
+              uint32_t* counts2, uint32_t* d_flags, uint32_t* d_hist, const StepPtrs* ind,
+              const uint64_t* lt_cuts, int lt_P, uint32_t* lt_out) {
   constexpr int C = 4, TILE = kJ * C * kThreads;
+  // P2P: per chunk, the staged position of the first entry at or after each
+  // cut (= entries below the cut), so K1's phase B needs no search.
+  __shared__ uint64_t s_cut[kMaxP];
+  __shared__ uint32_t s_lt[kMaxP], s_below[kMaxP];
+  if (lt_cuts && threadIdx.x < lt_P) {
+    s_cut[threadIdx.x] = lt_cuts[threadIdx.x];
+    s_lt[threadIdx.x] = 0xffffffffu;
+    s_below[threadIdx.x] = 0;
+  }
   if (ind) {
     g = ind->g;
     eps_in = ind->eps_in;
@@ -304,8 +318,28 @@ __global__ void __launch_bounds__(kThreads)
           if (DUAL) mloc += (valid[j][c] && m >= tf_loc) ? 1u : 0u;
           bal[j][c] = __ballot_sync(0xffffffffu, pred[j][c]);
         }
+      // A cut inside this tile: the entries below it are a prefix of the
+      // tile's order, counted here (warp reduce + one smem add per warp).
+      uint32_t cut_mask = 0;
+      if (lt_cuts) {
+        for (int d = 0; d < lt_P; ++d) {
+          const uint64_t cut = s_cut[d];
+          if (cut >= base && cut < base + TILE) {
+            cut_mask |= 1u << d;
+            uint32_t below = 0;
+#pragma unroll
+            for (int j = 0; j < kJ; ++j)
+#pragma unroll
+              for (int c = 0; c < C; ++c)
+                below += (pred[j][c] && base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C + c < cut) ? 1u : 0u;
+            below = __reduce_add_sync(0xffffffffu, below);
+            if ((tid & 31) == 0 && below) atomicAdd(&s_below[d], below);
+          }
+        }
+      }
       uint32_t grp[kJ];
       const uint32_t total = tile_offsets<C>(tbl[parity], bal, grp);
+      if (cut_mask && tid < lt_P && ((cut_mask >> tid) & 1u)) s_lt[tid] = running + s_below[tid];
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
 #pragma unroll
@@ -321,6 +355,15 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   if (SELECT && tid == 0) counts[blockIdx.x] = running;
+  if (lt_cuts) {
+    __syncthreads();
+    if (tid < lt_P) {
+      // no cut inside the chunk: everything or nothing is below it
+      const uint64_t chunk_lo = uint64_t(t0) * TILE;
+      const uint32_t v = s_lt[tid] != 0xffffffffu ? s_lt[tid] : (s_cut[tid] <= chunk_lo ? 0u : running);
+      lt_out[uint64_t(blockIdx.x) * kMaxP + tid] = v;
+    }
+  }
   if (DUAL) {
     const uint64_t s = block_sum(mloc, red);
     if (tid == 0) counts2[blockIdx.x] = uint32_t(s);
@@ -353,7 +396,8 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
   const unsigned ev_flags = cap_st == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, ev_flags);
   kern<<<G, kThreads, 0, L.s>>>(g, eps_in, eps_out, alpha, n, uint32_t(tiles), tpc, d_th, d_th2, S.s64, S.counts,
-                                S.counts2, d_flags, d_hist, ind);
+                                S.counts2, d_flags, d_hist, ind, pub ? pub->cuts : nullptr, pub ? pub->P : 0,
+                                pub ? pub->lt : nullptr);
   if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, ev_flags);
   ++L.launches;
   cudaError_t e = cudaGetLastError();
@@ -548,6 +592,54 @@ cudaError_t launch_apply(Launch& L, const Stage& S, const uint32_t* u_idx, const
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_compact<3>(L, S, G, 0, S.chunk_cap, false, nullptr, out_indexes, nullptr, d_nidx, nullptr);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    select_flags_kernel(const uint8_t* __restrict__ sel, const PeerTab* tab, const StepPtrs* sp, const uint64_t* d_U,
+                        const uint32_t* d_flags, uint32_t* __restrict__ sidx, uint32_t* counts, uint64_t* d_cap) {
+  __shared__ uint32_t tbl[2][32];
+  const uint32_t* __restrict__ u_idx = tab->u_idx[tab->rank][sp->par];
+  const int tid = threadIdx.x;
+  const uint64_t cnt = (*d_flags & (1u | 8u | 16u)) ? 0 : *d_U;
+  const uint64_t tiles = (cnt + kTileK - 1) / kTileK;
+  const uint64_t tpc = (tiles + gridDim.x - 1) / gridDim.x;
+  if (blockIdx.x == 0 && tid == 0) *d_cap = tpc * kTileK;
+  const uint64_t t0 = uint64_t(blockIdx.x) * tpc, t1 = min(t0 + tpc, tiles);
+  const uint64_t obase = uint64_t(blockIdx.x) * tpc * kTileK;
+  uint32_t running = 0;
+  int parity = 0;
+  for (uint64_t tile = t0; tile < t1; ++tile, parity ^= 1) {
+    bool pred[kJ];
+    uint32_t idx[kJ];
+    unsigned bal[kJ][1];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const uint64_t e = tile * kTileK + uint64_t(j) * kThreads + tid;
+      pred[j] = e < cnt && sel[e];
+      idx[j] = pred[j] ? u_idx[e] : 0u;
+      bal[j][0] = __ballot_sync(0xffffffffu, pred[j]);
+    }
+    uint32_t grp[kJ];
+    const uint32_t total = tile_offsets<1>(tbl[parity], bal, grp);
+#pragma unroll
+    for (int j = 0; j < kJ; ++j)
+      if (pred[j]) sidx[obase + running + grp[j] + rank_in_group<1>(bal, j, 0)] = idx[j];
+    running += total;
+  }
+  if (tid == 0) counts[blockIdx.x] = running;
+}
+
+cudaError_t launch_select_flags(Launch& L, const Stage& S, const uint8_t* sel, const PeerTab* d_tab,
+                                const StepPtrs* sp, const uint64_t* d_U, uint64_t bound, uint32_t* out,
+                                uint64_t* d_count, const uint32_t* d_flags) {
+  static int cap = 0;
+  if (!cap) cap = resident_ctas(select_flags_kernel, kThreads, L.sms);
+  const uint32_t G = chunks_for((bound + kTileK - 1) / kTileK, cap, S.max_chunks);
+  select_flags_kernel<<<G, kThreads, 0, L.s>>>(sel, d_tab, sp, d_U, d_flags, S.sidx, S.counts, S.chunk_cap);
+  ++L.launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_compact<3>(L, S, G, 0, S.chunk_cap, false, nullptr, out, nullptr, d_count, nullptr);
 }
 
 // =============================================================================

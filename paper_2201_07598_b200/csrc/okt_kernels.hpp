@@ -52,17 +52,6 @@ struct OutCoo {
   double* val = nullptr;
 };
 
-// Per-step pointers read from device memory, so one captured CUDA graph serves
-// every steady step (the graph refreshes this block from pinned host memory).
-struct StepPtrs {
-  const float* g;
-  const float* eps_in;
-  float* eps_out;
-  float* w;
-  float alpha;
-  float pad;
-};
-
 // Fused K7 for the single-rank path (every entry of u is locally selected).
 struct ApplyArgs {
   float* acc = nullptr;   // residual buffer holding acc; zeroed at u's indices
@@ -157,12 +146,16 @@ cudaError_t launch_scatter_heavy(Launch& L, const uint32_t* pos, const float* va
 cudaError_t launch_p2p_compact_L(Launch& L, const Stage& S, uint32_t G, uint64_t chunk_cap, uint64_t* out,
                                  uint64_t* d_m, const PubL& pub);
 // Waits for every peer's L, then scatters my slices read out of their HBM.
-cudaError_t launch_p2p_scatter(Launch& L, const PeerTab* d_tab, int P, uint64_t epoch, int par,
-                               const uint64_t* d_off, P2PPlan* plan, uint64_t lo, uint64_t W, uint32_t* mask,
-                               float* stage, uint32_t* d_flags, uint64_t timeout_ns);
+cudaError_t launch_p2p_scatter(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, const uint64_t* d_off,
+                               P2PPlan* plan, uint64_t lo, uint64_t W, uint32_t* mask, float* stage,
+                               uint32_t* d_flags, uint64_t timeout_ns);
 // Waits for every rank's survivors, plans (offsets / balance), pulls u.
-cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, int P, uint64_t epoch, int par,
-                                  const uint64_t* d_S, P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags,
-                                  uint64_t timeout_ns);
+cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, const uint64_t* d_S,
+                                  P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns,
+                                  const P2PApply& ap);
+// indexes = {u_idx[j] : sel[j]} in order (the K7 intersection, after a fused apply).
+cudaError_t launch_select_flags(Launch& L, const Stage& S, const uint8_t* sel, const PeerTab* d_tab,
+                                const StepPtrs* sp, const uint64_t* d_U, uint64_t bound, uint32_t* out,
+                                uint64_t* d_count, const uint32_t* d_flags);
 
 }  // namespace okt

@@ -20,28 +20,20 @@ constexpr uint32_t kAbortBits = 1u | 8u | 16u;  // local non-finite, peer timeou
 }
 
 // K1 phase B on the P2P path: copy each chunk to its final position in the
-// window's L and count, per chunk, the entries below every cut (the chunk is
-// sorted, so a binary search).  The last CTA to finish turns the per-chunk
-// counts into the slice offsets, publishes them with this rank's status, and
-// raises L-ready at every peer.
+// window's L.  K1's phase A already counted, per chunk, the entries below
+// every cut; the last CTA to finish turns those counts into the slice
+// offsets, publishes them with this rank's status, and raises L-ready at every
+// peer.
 __global__ void __launch_bounds__(kThreads)
     p2p_compact_L_kernel(const uint64_t* __restrict__ s64, const uint32_t* __restrict__ counts, uint64_t cap,
-                         uint64_t* __restrict__ out, uint64_t* d_m, PubL pb) {
+                         uint64_t* d_m, PubL pb) {
   __shared__ uint64_t red[kWarps];
   __shared__ int s_last;
   const int c = blockIdx.x, G = gridDim.x, tid = threadIdx.x, P = pb.P;
+  const int par = pb.sp->par;
+  uint64_t* __restrict__ out = pb.tab->L[pb.tab->rank][par];
   const uint64_t cnt = counts[c];
   const uint64_t src = uint64_t(c) * cap;
-  if (tid < P) {
-    const uint64_t key = pb.cuts[tid];
-    uint64_t lo = 0, hi = cnt;
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (uint64_t(coo_idx(s64[src + mid])) < key) lo = mid + 1;
-      else hi = mid;
-    }
-    pb.lt[uint64_t(c) * kP2PMaxP + tid] = uint32_t(lo);
-  }
   uint64_t pre = 0;
   for (int q = tid; q < c; q += kThreads) pre += counts[q];
   pre = block_sum(pre, red);
@@ -57,7 +49,7 @@ __global__ void __launch_bounds__(kThreads)
   tot = block_sum(tot, red);
   const PeerTab* tab = pb.tab;
   const int me = tab->rank;
-  P2PPub* mine = &tab->hdr[me]->pub[pb.par];
+  P2PPub* mine = &tab->hdr[me]->pub[par];
   for (int d = 0; d < P; ++d) {
     uint64_t o = 0;
     for (int q = tid; q < G; q += kThreads) o += pb.lt[uint64_t(q) * kP2PMaxP + d];
@@ -76,16 +68,18 @@ __global__ void __launch_bounds__(kThreads)
   }
   __threadfence_system();
   __syncthreads();
-  if (tid < P && tid != me) st_release_sys(&tab->hdr[tid]->flag[kFlagLReady][me], pb.epoch);
+  if (tid < P && tid != me) st_release_sys(&tab->hdr[tid]->flag[kFlagLReady][me], pb.sp->epoch);
 }
 
 // K3 (M1) fused with the split exchange.  Each CTA waits until every peer's
 // L is published, then scatters my region's entries read straight out of the
 // peers' HBM (NVLink) into the presence mask / coordinate-major staging.
 __global__ void __launch_bounds__(kThreads)
-    p2p_scatter_kernel(const PeerTab* __restrict__ tab, uint64_t epoch, int par, const uint64_t* d_off,
+    p2p_scatter_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, const uint64_t* d_off,
                        P2PPlan* plan, uint64_t lo, uint64_t W, uint32_t* mask, float* stage, uint32_t* d_flags,
                        uint64_t timeout_ns) {
+  const uint64_t epoch = sp->epoch;
+  const int par = sp->par;
   __shared__ uint64_t s_start[kP2PMaxP + 1];
   __shared__ const uint64_t* s_ptr[kP2PMaxP];
   __shared__ uint64_t s_cnt[kP2PMaxP];
@@ -153,8 +147,12 @@ __global__ void __launch_bounds__(kThreads)
 // survivors; balanced -> my block from the owners' survivors.  round 1
 // (balanced only) pulls the other blocks from their block owners' u.
 __global__ void __launch_bounds__(kThreads)
-    p2p_pull_kernel(const PeerTab* __restrict__ tab, uint64_t epoch, int par, const uint64_t* d_S, P2PPlan* plan,
-                    uint64_t* d_U, int round, uint32_t* d_flags, uint64_t timeout_ns) {
+    p2p_pull_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, const uint64_t* d_S, P2PPlan* plan,
+                    uint64_t* d_U, int round, uint32_t* d_flags, uint64_t timeout_ns, P2PApply ap) {
+  const uint64_t epoch = sp->epoch;
+  const int par = sp->par;
+  float* acc = ap.on ? (ap.sgd ? sp->eps_out : const_cast<float*>(sp->g)) : nullptr;
+  float* wm = (ap.on && ap.sgd) ? sp->w : nullptr;
   __shared__ uint64_t s_size[kP2PMaxP], s_off[kP2PMaxP + 1], s_blk[kP2PMaxP + 1];
   __shared__ int s_bal, s_abort;
   const int P = tab->P, me = tab->rank, q = threadIdx.x;
@@ -224,26 +222,47 @@ __global__ void __launch_bounds__(kThreads)
   }
   const uint64_t span = b - a;
   const uint64_t stride = uint64_t(gridDim.x) * kThreads;
+  const float tf = acc ? ceil_to_float(*ap.d_local_th) : 0.f;
+  const double dP = double(P);
+  bool bad = false;
   for (uint64_t x = uint64_t(blockIdx.x) * kThreads + threadIdx.x; x < span; x += stride) {
     const uint64_t pos = a + x;
     if (round == 1 && pos >= s_blk[me] && pos < s_blk[me + 1]) continue;  // my own block
     int r = 0;
+    uint32_t i;
+    double v;
     if (round == 0) {
       while (r + 1 < P && pos >= s_off[r + 1]) ++r;
       const uint64_t j = pos - s_off[r];
-      ui[pos] = tab->sur_idx[r][par][j];
-      uv[pos] = tab->sur_val[r][par][j];
+      i = tab->sur_idx[r][par][j];
+      v = tab->sur_val[r][par][j];
     } else {
       while (r + 1 < P && pos >= s_blk[r + 1]) ++r;
-      ui[pos] = tab->u_idx[r][par][pos];
-      uv[pos] = tab->u_val[r][par][pos];
+      i = tab->u_idx[r][par][pos];
+      v = tab->u_val[r][par][pos];
+    }
+    ui[pos] = i;
+    uv[pos] = v;
+    if (acc) {
+      // K7 (oktopk.cpp:299-302, trainer.cpp:437-442, 478-479) on the entry.
+      const float av = acc[i];
+      const bool sel = fabsf(av) >= tf;
+      if (wm) {
+        const float nw = float(double(wm[i]) - v / dP);
+        wm[i] = nw;
+        bad |= (__float_as_uint(nw) & 0x7f800000u) == 0x7f800000u;
+      }
+      if (wm && sel) acc[i] = 0.f;
+      ap.sel[pos] = sel ? 1 : 0;
     }
   }
+  if (acc && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(d_flags, 4u);
 }
 
 // Balanced case only: publish "my block is in u", wait for every other block.
-__global__ void p2p_block_sync_kernel(const PeerTab* __restrict__ tab, uint64_t epoch, const P2PPlan* plan,
+__global__ void p2p_block_sync_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, const P2PPlan* plan,
                                       uint32_t* d_flags, uint64_t timeout_ns) {
+  const uint64_t epoch = sp->epoch;
   const int P = tab->P, me = tab->rank, q = threadIdx.x;
   if (!plan->balanced || (*d_flags & (1u | 8u | 16u))) return;
   __threadfence_system();
@@ -256,29 +275,28 @@ __global__ void p2p_block_sync_kernel(const PeerTab* __restrict__ tab, uint64_t 
 // ---- launchers ----------------------------------------------------------------------------
 cudaError_t launch_p2p_compact_L(Launch& L, const Stage& S, uint32_t G, uint64_t chunk_cap, uint64_t* out,
                                  uint64_t* d_m, const PubL& pub) {
-  p2p_compact_L_kernel<<<G, kThreads, 0, L.s>>>(S.s64, S.counts, chunk_cap, out, d_m, pub);
+  (void)out;  // the window slot of this step's parity, chosen on the device
+  p2p_compact_L_kernel<<<G, kThreads, 0, L.s>>>(S.s64, S.counts, chunk_cap, d_m, pub);
   ++L.launches;
   return cudaGetLastError();
 }
 
-cudaError_t launch_p2p_scatter(Launch& L, const PeerTab* d_tab, int P, uint64_t epoch, int par,
-                               const uint64_t* d_off, P2PPlan* plan, uint64_t lo, uint64_t W, uint32_t* mask,
-                               float* stage, uint32_t* d_flags, uint64_t timeout_ns) {
-  (void)P;
-  p2p_scatter_kernel<<<L.sms * 2, kThreads, 0, L.s>>>(d_tab, epoch, par, d_off, plan, lo, W, mask, stage, d_flags,
+cudaError_t launch_p2p_scatter(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, const uint64_t* d_off,
+                               P2PPlan* plan, uint64_t lo, uint64_t W, uint32_t* mask, float* stage,
+                               uint32_t* d_flags, uint64_t timeout_ns) {
+  p2p_scatter_kernel<<<L.sms * 2, kThreads, 0, L.s>>>(d_tab, sp, d_off, plan, lo, W, mask, stage, d_flags,
                                                       timeout_ns);
   ++L.launches;
   return cudaGetLastError();
 }
 
-cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, int P, uint64_t epoch, int par,
-                                  const uint64_t* d_S, P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags,
-                                  uint64_t timeout_ns) {
-  (void)P;
+cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, const uint64_t* d_S,
+                                  P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns,
+                                  const P2PApply& ap) {
   const int grid = L.sms * 2;
-  p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, epoch, par, d_S, plan, d_U, 0, d_flags, timeout_ns);
-  p2p_block_sync_kernel<<<1, 32, 0, L.s>>>(d_tab, epoch, plan, d_flags, timeout_ns);
-  p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, epoch, par, d_S, plan, d_U, 1, d_flags, timeout_ns);
+  p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, d_S, plan, d_U, 0, d_flags, timeout_ns, ap);
+  p2p_block_sync_kernel<<<1, 32, 0, L.s>>>(d_tab, sp, plan, d_flags, timeout_ns);
+  p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, d_S, plan, d_U, 1, d_flags, timeout_ns, ap);
   L.launches += 3;
   return cudaGetLastError();
 }

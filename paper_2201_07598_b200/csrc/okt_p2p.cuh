@@ -23,6 +23,21 @@
 namespace okt {
 
 constexpr int kP2PMaxP = 8;
+
+// Per-step arguments read from device memory, so one captured CUDA graph
+// serves every steady step (the graph refreshes this block from pinned host
+// memory as its first node).
+struct StepPtrs {
+  const float* g;
+  const float* eps_in;
+  float* eps_out;
+  float* w;
+  float alpha;
+  float pad;
+  uint64_t epoch;  // P2P: flag value of this step
+  int32_t par;     // P2P: parity slot of the window buffers
+  int32_t pad2;
+};
 enum P2PFlag { kFlagLReady = 0, kFlagSurReady = 1, kFlagBlockReady = 2, kP2PFlagKinds = 4 };
 
 // What a rank publishes for its peers each step (double-buffered by parity).
@@ -63,11 +78,18 @@ struct P2PPlan {
   uint64_t peer_status[kP2PMaxP];
 };
 
+// K7 fused into the allgatherv pull: every u entry is touched once.
+struct P2PApply {
+  int on = 0;
+  int sgd = 0;                  // acc = sp->eps_out and w = sp->w; else acc = sp->g
+  const double* d_local_th = nullptr;
+  uint8_t* sel = nullptr;       // per u entry: 1 if in the local selection
+};
+
 // Fused publication hooks (phase B of a compaction publishes what it wrote).
 struct PubL {  // K1 phase B: local selection L + its slice offsets
   const PeerTab* tab = nullptr;  // device copy
-  uint64_t epoch = 0;
-  int par = 0;
+  const StepPtrs* sp = nullptr;  // epoch / parity of the step
   int P = 1;
   uint32_t* done = nullptr;      // last-CTA counter (self-resetting)
   uint32_t* lt = nullptr;        // [chunk][kP2PMaxP] entries below each cut
@@ -77,8 +99,7 @@ struct PubL {  // K1 phase B: local selection L + its slice offsets
 };
 struct PubSur {  // region scan phase B: survivors of the global threshold
   const PeerTab* tab = nullptr;
-  uint64_t epoch = 0;
-  int par = 0;
+  const StepPtrs* sp = nullptr;
   uint32_t* done = nullptr;
   const uint32_t* flags = nullptr;
 };
