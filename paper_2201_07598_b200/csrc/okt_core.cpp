@@ -18,6 +18,7 @@
 // is committed only when the step succeeds, so a failing step leaves the
 // state, the residual and the model as the reference leaves them.
 #include <algorithm>
+#include <cstddef>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -86,8 +87,13 @@ struct DevScalars {
   double th_arg;  // threshold argument of the sub-phase entry points
   double pad0;
   uint64_t m, R, S, U, nidx;
-  uint32_t flags;  // bit0 non-finite input, bit1 out-of-region entry, bit2 non-finite iterate
+  // The P2P steady step refreshes [sp, plan] with one H2D copy per step
+  // (flags and plan zeroed), and reads everything back with one D2H.
+  okt::StepPtrs sp;
+  uint32_t flags;  // bit0 non-finite input, bit1 out-of-region entry, bit2 non-finite iterate,
+                   // bit3 peer timeout, bit4 peer failure
   uint32_t pad1;
+  okt::P2PPlan plan;
   uint64_t cuts[OKT_MAX_WORLD + 1];
   uint64_t off[OKT_MAX_WORLD + 1];
   uint64_t prop[OKT_MAX_WORLD + 1];
@@ -117,19 +123,30 @@ okt_state default_state() {
   return s;
 }
 
-// Symmetric P2P window layout (identical on every rank for a given n).
+// Symmetric P2P window layout (identical on every rank for a given n): per
+// parity, K1's chunked staging + chunk counts + per-chunk cut counts, the
+// region scan's chunked survivors + counts + chunk prefix, and u.
 struct WinLayout {
-  size_t L[2], sidx[2], sval[2], uidx[2], uval[2], bytes;
+  size_t kstg[2], kcnt[2], klt[2], sidx[2], sval[2], scnt[2], spre[2], uidx[2], uval[2], bytes;
 };
-WinLayout win_layout(size_t n) {
+WinLayout win_layout(size_t n, int max_chunks) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t kst = okt::stage_entries(n, okt::kK1Tile, max_chunks);
+  const size_t sst = okt::stage_entries(n, okt::kRegionTileHost, max_chunks);
+  const size_t mc = size_t(max_chunks);
   WinLayout w;
   size_t o = al(sizeof(okt::P2PHdr));
-  for (int p = 0; p < 2; ++p) { w.L[p] = o; o += al(8 * n); }
-  for (int p = 0; p < 2; ++p) { w.sidx[p] = o; o += al(4 * n); }
-  for (int p = 0; p < 2; ++p) { w.sval[p] = o; o += al(8 * n); }
-  for (int p = 0; p < 2; ++p) { w.uidx[p] = o; o += al(4 * n); }
-  for (int p = 0; p < 2; ++p) { w.uval[p] = o; o += al(8 * n); }
+  for (int p = 0; p < 2; ++p) {
+    w.kstg[p] = o; o += al(8 * kst);
+    w.kcnt[p] = o; o += al(4 * mc);
+    w.klt[p] = o; o += al(4 * okt::kP2PMaxP * mc);
+    w.sidx[p] = o; o += al(4 * sst);
+    w.sval[p] = o; o += al(8 * sst);
+    w.scnt[p] = o; o += al(4 * mc);
+    w.spre[p] = o; o += al(8 * (mc + 1));
+    w.uidx[p] = o; o += al(4 * n);
+    w.uval[p] = o; o += al(8 * n);
+  }
   w.bytes = o;
   return w;
 }
@@ -180,14 +197,13 @@ struct okt_comm {
   okt::Stage S;
   // device-driven multi-GPU exchange (okt_p2p.cuh)
   bool p2p_checked = false, p2p = false;
-  Buf win, planb, boot, tabd, pdone, plt, selflags;
+  Buf win, boot, tabd, selflags;
   const float* cur_acc = nullptr;  // the step's accumulator / model (P2P fused apply)
   float* cur_w = nullptr;
   size_t win_n = 0;
   okt::PeerTab tab{};
   std::vector<void*> ipc_open;
   uint64_t p2p_epoch = 0;
-  okt::P2PPlan* hplan = nullptr;  // pinned mirror of the device plan
   // CUDA graph of the steady single-rank step (memset, K1, fused compaction +
   // apply, scalar readback); per-step pointers come through `ptrsb`.
   struct StepGraph {
@@ -613,7 +629,7 @@ struct okt_comm {
     std::vector<int> ones(P);
     close_peers();
     if ((rc = allgather_host(&one, ones.data(), sizeof(int), s))) return rc;  // peers closed my old window
-    const WinLayout lay = win_layout(n);
+    const WinLayout lay = win_layout(n, S.max_chunks);
     win.zero_init = false;
     if (win.p) {
       cudaFree(win.p);
@@ -679,39 +695,23 @@ struct okt_comm {
     for (int q = 0; q < P; ++q) {
       tab.hdr[q] = reinterpret_cast<okt::P2PHdr*>(base[q]);
       for (int p = 0; p < 2; ++p) {
-        tab.L[q][p] = reinterpret_cast<uint64_t*>(base[q] + lay.L[p]);
-        tab.sur_idx[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.sidx[p]);
-        tab.sur_val[q][p] = reinterpret_cast<double*>(base[q] + lay.sval[p]);
+        tab.kstg[q][p] = reinterpret_cast<uint64_t*>(base[q] + lay.kstg[p]);
+        tab.kcnt[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.kcnt[p]);
+        tab.klt[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.klt[p]);
+        tab.sidx[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.sidx[p]);
+        tab.sval[q][p] = reinterpret_cast<double*>(base[q] + lay.sval[p]);
+        tab.scnt[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.scnt[p]);
+        tab.spre[q][p] = reinterpret_cast<uint64_t*>(base[q] + lay.spre[p]);
         tab.u_idx[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.uidx[p]);
         tab.u_val[q][p] = reinterpret_cast<double*>(base[q] + lay.uval[p]);
       }
     }
-    if ((rc = ensure(planb, sizeof(okt::P2PPlan)))) return rc;
-    pdone.zero_init = true;
-    if ((rc = ensure(pdone, 64))) return rc;
-    if ((rc = ensure(plt, sizeof(uint32_t) * okt::kP2PMaxP * size_t(S.max_chunks)))) return rc;
     if ((rc = ensure(tabd, sizeof(okt::PeerTab)))) return rc;
     if ((rc = ck(cudaMemcpy(tabd.p, &tab, sizeof(okt::PeerTab), cudaMemcpyHostToDevice), "tab"))) return rc;
     if ((rc = ensure(indexes, 4 * std::max<size_t>(n, 1)))) return rc;
     if ((rc = ensure(selflags, std::max<size_t>(n, 1)))) return rc;
     win_n = n;
     return OKT_OK;
-  }
-
-  // Steady iteration on the P2P window (no host round trip until the end).
-  // K1 (with its fused publication, see pub_L) already wrote the local
-  // selection into tab.L[rank][par] and raised L-ready at every peer.
-  okt::PubL pub_L(const okt::StepPtrs* sp) {
-    okt::PubL pb;
-    pb.tab = tabd.as<okt::PeerTab>();
-    pb.sp = sp;
-    pb.P = P;
-    pb.done = pdone.as<uint32_t>();
-    pb.lt = plt.as<uint32_t>();
-    pb.cuts = d()->cuts;
-    pb.d_off = d()->off;
-    pb.flags = &d()->flags;
-    return pb;
   }
 
   // Enqueues a whole steady P2P iteration on `s` (no host synchronisation):
@@ -721,45 +721,52 @@ struct okt_comm {
   // (pointers, epoch, parity) are read from ptrsb on the device, so the same
   // sequence is captured once into a CUDA graph.
   int enqueue_p2p_step(size_t n, size_t k, bool sgd, cudaStream_t s) {
-    const okt::StepPtrs* sp = ptrsb.as<okt::StepPtrs>();
-    okt::P2PPlan* dp = planb.as<okt::P2PPlan>();
+    const okt::StepPtrs* sp = &d()->sp;
+    okt::P2PPlan* dp = &d()->plan;
     const okt::PeerTab* dt = tabd.as<okt::PeerTab>();
     const uint64_t lo = st.cuts[rank], hi = st.cuts[rank + 1];
     const uint64_t W = hi > lo ? hi - lo : 0;
     (void)k;
-    int rc = ck(cudaMemcpyAsync(ptrsb.p, hptrs, sizeof(okt::StepPtrs), cudaMemcpyHostToDevice, s), "h2d");
-    if (!rc) rc = ck(cudaMemsetAsync(&d()->flags, 0, 4, s), "memset");
+    // one H2D: the step block, zeroed flags and a zeroed plan
+    const size_t blk = offsetof(DevScalars, plan) + sizeof(okt::P2PPlan) - offsetof(DevScalars, sp);
+    int rc = ck(cudaMemcpyAsync(&d()->sp, &hup->sp, blk, cudaMemcpyHostToDevice, s), "h2d");
     tmark(OKT_T_SELECT, s);
-    const okt::PubL pl = pub_L(sp);
+    okt::K1P2P kp;
+    kp.tab = dt;
+    kp.sp = sp;
+    kp.cuts = d()->cuts;
     if (!rc)
-      rc = ck(okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, hptrs->g, hptrs->eps_in,
-                             hptrs->eps_out, hptrs->alpha, n, &d()->local_th, nullptr,
-                             okt::OutCoo{tab.L[rank][0]}, &d()->m, nullptr, &d()->flags, nullptr, nullptr, &pl, sp),
+      rc = ck(okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, hup->sp.g,
+                             hup->sp.eps_in, hup->sp.eps_out, hup->sp.alpha, n, &d()->local_th, nullptr,
+                             okt::OutCoo{}, &d()->m, nullptr, &d()->flags, nullptr, nullptr, &kp, sp),
               "k1");
     tmark(OKT_T_MERGE, s);
-    if (!rc) rc = ck(okt::launch_p2p_scatter(L, dt, sp, d()->off, dp, lo, W, mask.as<uint32_t>(), stage.as<float>(),
+    if (!rc) rc = ck(okt::launch_p2p_scatter(L, dt, sp, dp, lo, W, mask.as<uint32_t>(), stage.as<float>(),
                                              &d()->flags, kP2PTimeoutNs), "p2p");
-    okt::PubSur ps;
-    ps.tab = dt;
-    ps.sp = sp;
-    ps.done = pdone.as<uint32_t>() + 1;
-    ps.flags = &d()->flags;
+    okt::RSP2P rp;
+    rp.tab = dt;
+    rp.sp = sp;
     if (!rc) rc = ck(okt::launch_region_scan(L, S, P, true, lo, W, mask.as<uint32_t>(), stage.as<float>(),
-                                             &d()->global_th, tab.sur_idx[rank][0], tab.sur_val[rank][0], &d()->S,
-                                             &ps), "region_scan");
+                                             &d()->global_th, nullptr, nullptr, &d()->S, &rp), "region_scan");
     tmark(OKT_T_ALLGATHER, s);
     okt::P2PApply pa;
     pa.on = 1;
     pa.sgd = sgd ? 1 : 0;
     pa.d_local_th = &d()->local_th;
-    pa.sel = selflags.as<uint8_t>();
-    if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, sp, &d()->S, dp, &d()->U, &d()->flags, kP2PTimeoutNs, pa),
+    // oktopk_sgd_step reports no index list (trainer.hpp:123-127): only the
+    // plain allreduce needs the sel flags and the indexes compaction.
+    pa.sel = sgd ? nullptr : selflags.as<uint8_t>();
+    okt::K1Totals kt;
+    kt.d_m = &d()->m;
+    kt.d_off = d()->off;
+    if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, sp, &d()->S, dp, &d()->U, &d()->flags, kP2PTimeoutNs, pa, kt),
                      "p2p");
-    tmark(OKT_T_APPLY, s);
-    if (!rc) rc = ck(okt::launch_select_flags(L, S, selflags.as<uint8_t>(), dt, sp, &d()->U, win_n,
-                                              indexes.as<uint32_t>(), &d()->nidx, &d()->flags), "indexes");
+    if (!sgd) {
+      tmark(OKT_T_APPLY, s);
+      if (!rc) rc = ck(okt::launch_select_flags(L, S, selflags.as<uint8_t>(), dt, sp, &d()->U, win_n,
+                                                indexes.as<uint32_t>(), &d()->nidx, &d()->flags), "indexes");
+    }
     tstop(s);
-    if (!rc) rc = ck(cudaMemcpyAsync(hplan, dp, sizeof(okt::P2PPlan), cudaMemcpyDeviceToHost, s), "d2h");
     if (!rc) rc = ck(cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s), "d2h");
     return rc;
   }
@@ -777,8 +784,7 @@ struct okt_comm {
     int rc;
     const uint64_t lo = st.cuts[rank], hi = st.cuts[rank + 1];
     const uint64_t W = hi > lo ? hi - lo : 0;
-    if ((rc = ensure(mask, ((W + 15) / 16) * 16 + 16)) || (rc = ensure(stage, 4 * std::max<uint64_t>(W, 1) * P)) ||
-        (rc = ensure(ptrsb, sizeof(okt::StepPtrs))))
+    if ((rc = ensure(mask, ((W + 15) / 16) * 16 + 16)) || (rc = ensure(stage, 4 * std::max<uint64_t>(W, 1) * P)))
       return rc;
     if (prof || !graphs_on) return enqueue_p2p_step(n, k, sgd, s);
     P2PGraph& G = graph2;
@@ -815,21 +821,21 @@ struct okt_comm {
     return OKT_OK;
   }
 
-  // Ledger of a P2P step, from the sizes every rank agreed on (h / hplan valid).
+  // Ledger of a P2P step, from the sizes every rank agreed on (h valid).
   void p2p_credit() {
     std::vector<uint64_t> counts(size_t(P) * P, 0);
     for (int q = 0; q < P; ++q) {
       counts[size_t(rank) * P + q] = h->off[q + 1] - h->off[q];
-      counts[size_t(q) * P + rank] = hplan->seg_cnt[q];
+      counts[size_t(q) * P + rank] = h->plan.seg_cnt[q];
     }
     okt::plan::ledger_split(ledger[OKT_PHASE_SPLIT], rank, P, counts.data(), st.bucket_size);
     for (int q = 0; q < P; ++q)
       if (q != rank) {
         ledger[OKT_PHASE_SPLIT].bytes_sent += 8 * counts[size_t(rank) * P + q];
-        ledger[OKT_PHASE_SPLIT].bytes_recv += 8 * hplan->seg_cnt[q];
+        ledger[OKT_PHASE_SPLIT].bytes_recv += 8 * h->plan.seg_cnt[q];
       }
     credit_allgather_u32();
-    const std::vector<uint64_t> sizes(hplan->sizes, hplan->sizes + P);
+    const std::vector<uint64_t> sizes(h->plan.sizes, h->plan.sizes + P);
     const okt::plan::Balance B = okt::plan::balance(rank, P, sizes);
     if (B.on) {
       okt::plan::ledger_balance(ledger[OKT_PHASE_BALANCE], B);
@@ -1008,13 +1014,14 @@ struct okt_comm {
                          sur_val.as<double>(), out);
     }
     if (use_p2p) {
-      hptrs->g = g;
-      hptrs->eps_in = eps_in;
-      hptrs->eps_out = eps_out;
-      hptrs->w = sgd ? w : nullptr;
-      hptrs->alpha = fa;
-      hptrs->epoch = epoch;
-      hptrs->par = par;
+      okt::StepPtrs& sp = hup->sp;
+      sp.g = g;
+      sp.eps_in = eps_in;
+      sp.eps_out = eps_out;
+      sp.w = sgd ? w : nullptr;
+      sp.alpha = fa;
+      sp.epoch = epoch;
+      sp.par = par;
       if ((rc = launch_p2p_step(n, k, sgd, s))) return abort_step(rc);
       if (prof) {
         cudaEvent_t e = ev_get();
@@ -1091,13 +1098,6 @@ struct okt_comm {
       d_U = &d()->S;
       new_cuts[0] = 0;
       new_cuts[1] = n;
-    } else if (use_p2p) {
-      // (K1 ran inside launch_p2p_step, issued before the K1 section above)
-      if (rc) return abort_step(rc);
-      for (int q = 0; q <= P; ++q) new_cuts[q] = st.cuts[q];
-      d_U = &d()->U;
-      ui = tab.u_idx[rank][par];
-      uv = tab.u_val[rank][par];
     } else {
       if (!is_pow2(P)) return set_err(OKT_ERR_CONFIG, "world size must be a power of two");
       // ---- boundaries ----
@@ -1143,8 +1143,8 @@ struct okt_comm {
       uv = u_val.as<double>();
     }
 
-    // ---- K7 (fused into the compaction for P = 1, into the pull on the P2P path) ----
-    if (P > 1 && !use_p2p) {
+    // ---- K7 (fused into the compaction for P = 1; the P2P path returned above) ----
+    if (P > 1) {
       tmark(OKT_T_APPLY, s);
       rc = ck(okt::launch_apply(L, S, ui, uv, d_U, U_bound, const_cast<float*>(acc), sgd, sgd ? w : nullptr, P,
                                 &d()->local_th, indexes.as<uint32_t>(), &d()->nidx, &d()->flags), "apply");
@@ -1156,14 +1156,8 @@ struct okt_comm {
       cudaEventRecord(e, s);
       spans.push_back({OKT_T_STEP, step_begin, e});
     }
-    if (use_p2p && defer) {
-      cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s);
-      p2p_credit_pending = true;
-      if (defer_commit(n, t, thr, sgd, new_cuts, ui, uv, s)) return OKT_OK;
-    }
     if ((rc = sync(s))) return abort_step(rc);
     tcollect();
-    if (use_p2p) p2p_credit_pending = true;
     return commit_step(n, t, thr, sgd, new_cuts, ui, uv, out);
   }
 
@@ -1204,6 +1198,8 @@ struct okt_comm {
                   const uint32_t* ui, const double* uv, okt_result* out) {
     const bool credit = p2p_credit_pending;
     p2p_credit_pending = false;
+    // the P2P EF step produces no index list (oktopk_sgd_step reports none)
+    const bool no_indexes = credit && sgd;
     if (prof) {
       // Algorithmic bytes: K1 reads g (+ eps), writes eps and
       // emits the COO (8 B per local entry; 12 B per u entry when the
@@ -1258,8 +1254,8 @@ struct okt_comm {
       out->u.d_val = uv;
       out->u.nnz = P == 1 ? h->S : h->U;
       out->u.n = n;
-      out->d_indexes = P == 1 ? ui : indexes.as<uint32_t>();
-      out->n_indexes = P == 1 ? h->S : h->nidx;
+      out->d_indexes = P == 1 ? ui : (no_indexes ? nullptr : indexes.as<uint32_t>());
+      out->n_indexes = P == 1 ? h->S : (no_indexes ? 0 : h->nidx);
       out->local_selected = h->m;
     }
     if (h->flags & 4u) return set_err(OKT_ERR_NUMERIC, "oktopk_sgd_step: non-finite iterate");
@@ -1316,7 +1312,6 @@ int init_comm(okt_comm* c) {
   if (e == cudaSuccess) e = c->chunkcap.ensure(64);
   if (e == cudaSuccess) e = cudaMallocHost(&c->h, sizeof(DevScalars));
   if (e == cudaSuccess) e = cudaMallocHost(&c->hup, sizeof(DevScalars));
-  if (e == cudaSuccess) e = cudaMallocHost(&c->hplan, sizeof(okt::P2PPlan));
   if (e == cudaSuccess) e = cudaMallocHost(&c->hptrs, sizeof(okt::StepPtrs));
   if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("init: ") + cudaGetErrorString(e));
   std::memset(c->h, 0, sizeof(DevScalars));
@@ -1450,7 +1445,6 @@ int okt_comm_destroy(okt_comm* c) {
   if (c->ready_ev) cudaEventDestroy(c->ready_ev);
   if (c->h) cudaFreeHost(c->h);
   if (c->hup) cudaFreeHost(c->hup);
-  if (c->hplan) cudaFreeHost(c->hplan);
   if (c->hptrs) cudaFreeHost(c->hptrs);
   if (c->graph1.exec) cudaGraphExecDestroy(c->graph1.exec);
   if (c->graph1.e0) {

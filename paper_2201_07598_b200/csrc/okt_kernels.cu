@@ -68,17 +68,13 @@ __global__ void __launch_bounds__(kThreads)
                    const double* __restrict__ sval, const uint32_t* __restrict__ counts,
                    const uint32_t* __restrict__ counts2, uint64_t cap_host, const uint64_t* d_cap,
                    uint64_t* __restrict__ o64, uint32_t* oidx, double* oval,
-                   uint64_t* d_total, uint64_t* d_total2, ApplyArgs ap, PubSur pub) {
+                   uint64_t* d_total, uint64_t* d_total2, ApplyArgs ap) {
   __shared__ uint64_t red[kWarps];
-  __shared__ int s_last;
   if (APPLY && ap.ind) {
     ap.acc = ap.ind->eps_out;
     ap.w = ap.ind->w;
   }
-  if (MODE == 2 && pub.tab) {  // P2P: survivors go to this step's window slot
-    oidx = pub.tab->sur_idx[pub.tab->rank][pub.sp->par];
-    oval = pub.tab->sur_val[pub.tab->rank][pub.sp->par];
-  }
+
   const int c = blockIdx.x, G = gridDim.x;
   const uint64_t cnt = counts[c];
   const uint64_t cap = d_cap ? *d_cap : cap_host;
@@ -156,46 +152,21 @@ __global__ void __launch_bounds__(kThreads)
       if (threadIdx.x == 0) *d_total2 = s2;
     }
   }
-  if (pub.tab) {
-    // P2P: the last CTA to finish publishes the survivor count to the peers
-    // once every entry is in place (okt_p2p.cuh).
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(pub.done, 1u) == unsigned(G - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    uint64_t tot = 0;
-    for (int q = threadIdx.x; q < G; q += kThreads) tot += counts[q];
-    tot = block_sum(tot, red);
-    const PeerTab* tab = pub.tab;
-    const int me = tab->rank, P = tab->P, par = pub.sp->par;
-    if (threadIdx.x == 0) {
-      tab->hdr[me]->pub[par].S = tot;
-      tab->hdr[me]->pub[par].status = (*pub.flags & (1u | 8u | 16u)) ? 1 : 0;
-      *pub.done = 0;
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x < P && int(threadIdx.x) != me)
-      st_release_sys(&tab->hdr[threadIdx.x]->flag[kFlagSurReady][me], pub.sp->epoch);
-  }
 }
 
 template <int MODE>
 static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_t cap_host,
                                   const uint64_t* d_cap, bool with2, uint64_t* o64, uint32_t* oidx,
                                   double* oval, uint64_t* d_total, uint64_t* d_total2,
-                                  const ApplyArgs* ap = nullptr, const PubSur* pub = nullptr) {
-  const PubSur pb = pub ? *pub : PubSur{};
+                                  const ApplyArgs* ap = nullptr) {
   if (ap && (ap->w || ap->ind))
     compact_kernel<MODE, true><<<G, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts,
                                                         with2 ? S.counts2 : nullptr, cap_host, d_cap, o64, oidx,
-                                                        oval, d_total, d_total2, *ap, pb);
+                                                        oval, d_total, d_total2, *ap);
   else
     compact_kernel<MODE, false><<<G, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts,
                                                          with2 ? S.counts2 : nullptr, cap_host, d_cap, o64, oidx,
-                                                         oval, d_total, d_total2, ApplyArgs{}, pb);
+                                                         oval, d_total, d_total2, ApplyArgs{});
   ++L.launches;
   return cudaGetLastError();
 }
@@ -208,17 +179,28 @@ __global__ void __launch_bounds__(kThreads)
     k1_kernel(const float* __restrict__ g, const float* eps_in, float* eps_out, float alpha, uint64_t n,
               uint32_t tiles, uint32_t tpc, const double* __restrict__ d_th,
               const double* __restrict__ d_th2, uint64_t* __restrict__ stg, uint32_t* counts,
-              uint32_t* counts2, uint32_t* d_flags, uint32_t* d_hist, const StepPtrs* ind,
-              const uint64_t* lt_cuts, int lt_P, uint32_t* lt_out) {
+              uint32_t* counts2, uint32_t* d_flags, uint32_t* d_hist, const StepPtrs* ind, K1P2P p2p) {
   constexpr int C = 4, TILE = kJ * C * kThreads;
-  // P2P: per chunk, the staged position of the first entry at or after each
-  // cut (= entries below the cut), so K1's phase B needs no search.
+  // P2P mode: the chunk-local staging, its counts and, per chunk, the number
+  // of entries below every cut live in this rank's window; peers read each
+  // chunk's slice for their region in place ([lt[c][r], lt[c][r+1])).
   __shared__ uint64_t s_cut[kMaxP];
   __shared__ uint32_t s_lt[kMaxP], s_below[kMaxP];
-  if (lt_cuts && threadIdx.x < lt_P) {
-    s_cut[threadIdx.x] = lt_cuts[threadIdx.x];
-    s_lt[threadIdx.x] = 0xffffffffu;
-    s_below[threadIdx.x] = 0;
+  __shared__ int s_last;
+  // (the P2P path always runs the vectorised, single-threshold variants)
+  const bool p2p_on = VEC && !DUAL && p2p.tab != nullptr;
+  const int lt_P = p2p_on ? p2p.tab->P : 0;
+  uint32_t* lt_out = nullptr;
+  if (p2p_on) {
+    const int me = p2p.tab->rank, par = p2p.sp->par;
+    stg = p2p.tab->kstg[me][par];
+    counts = p2p.tab->kcnt[me][par];
+    lt_out = p2p.tab->klt[me][par];
+    if (threadIdx.x < lt_P) {
+      s_cut[threadIdx.x] = p2p.cuts[threadIdx.x];
+      s_lt[threadIdx.x] = 0xffffffffu;
+      s_below[threadIdx.x] = 0;
+    }
   }
   if (ind) {
     g = ind->g;
@@ -321,7 +303,7 @@ __global__ void __launch_bounds__(kThreads)
       // A cut inside this tile: the entries below it are a prefix of the
       // tile's order, counted here (warp reduce + one smem add per warp).
       uint32_t cut_mask = 0;
-      if (lt_cuts) {
+      if (p2p_on) {
         for (int d = 0; d < lt_P; ++d) {
           const uint64_t cut = s_cut[d];
           if (cut >= base && cut < base + TILE) {
@@ -355,7 +337,7 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   if (SELECT && tid == 0) counts[blockIdx.x] = running;
-  if (lt_cuts) {
+  if (p2p_on) {
     __syncthreads();
     if (tid < lt_P) {
       // no cut inside the chunk: everything or nothing is below it
@@ -373,13 +355,21 @@ __global__ void __launch_bounds__(kThreads)
     for (int i = tid; i < 2048; i += kThreads)
       if (s_hist[i]) atomicAdd(&d_hist[i], s_hist[i]);
   }
+  if (p2p_on && blockIdx.x == 0 && tid == 0) {
+    // Chunk geometry for the peers; the status and the L-ready flags are
+    // published by the next kernel on the stream (the P2P scatter), once
+    // every CTA of this one has finished.
+    P2PPub* pub = &p2p.tab->hdr[p2p.tab->rank]->pub[p2p.sp->par];
+    pub->k1_G = gridDim.x;
+    pub->k1_cap = tpc * TILE;
+  }
 }
 
 template <bool ACCUM, bool SELECT, bool HIST, bool DUAL>
 static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float* g, const float* eps_in,
                                float* eps_out, float alpha, uint64_t n, const double* d_th,
                                const double* d_th2, const OutCoo& out, uint64_t* d_m, uint64_t* d_m2,
-                               uint32_t* d_flags, uint32_t* d_hist, const ApplyArgs* ap, const PubL* pub,
+                               uint32_t* d_flags, uint32_t* d_hist, const ApplyArgs* ap, const K1P2P* p2p,
                                const StepPtrs* ind) {
   constexpr int TILE = kJ * 4 * kThreads;
   const uint64_t tiles = (n + TILE - 1) / TILE;
@@ -396,14 +386,13 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
   const unsigned ev_flags = cap_st == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, ev_flags);
   kern<<<G, kThreads, 0, L.s>>>(g, eps_in, eps_out, alpha, n, uint32_t(tiles), tpc, d_th, d_th2, S.s64, S.counts,
-                                S.counts2, d_flags, d_hist, ind, pub ? pub->cuts : nullptr, pub ? pub->P : 0,
-                                pub ? pub->lt : nullptr);
+                                S.counts2, d_flags, d_hist, ind, p2p ? *p2p : K1P2P{});
   if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, ev_flags);
   ++L.launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !SELECT) return e;
   const uint64_t chunk_cap = uint64_t(tpc) * TILE;
-  if (pub) return launch_p2p_compact_L(L, S, G, chunk_cap, out.aos, d_m, *pub);
+  if (p2p) return cudaSuccess;  // peers consume the chunked staging in place
   if (out.aos)
     return launch_compact<0>(L, S, G, chunk_cap, nullptr, DUAL, out.aos, nullptr, nullptr, d_m, d_m2);
   return launch_compact<1>(L, S, G, chunk_cap, nullptr, DUAL, nullptr, out.idx, out.val, d_m, d_m2, ap);
@@ -412,7 +401,7 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
 cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, const float* eps_in,
                       float* eps_out, float alpha, uint64_t n, const double* d_th, const double* d_th2,
                       const OutCoo& out, uint64_t* d_m, uint64_t* d_m2, uint32_t* d_flags, uint32_t* d_hist,
-                      const ApplyArgs* ap, const PubL* pub, const StepPtrs* ind) {
+                      const ApplyArgs* ap, const K1P2P* pub, const StepPtrs* ind) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   bool vec = al(g);
   if (mode != K1Mode::kSelect) vec = vec && al(eps_in) && al(eps_out);
@@ -711,10 +700,16 @@ static_assert(kRegionTile == kRegionTileHost, "staging sized for the region tile
 template <int P, bool FILTER>
 __global__ void __launch_bounds__(kThreads)
     region_scan_kernel(uint64_t lo, uint64_t W, uint32_t tiles, uint32_t tpc, uint32_t* mask,
-                       const float* __restrict__ stage, const double* d_gth, uint32_t* __restrict__ sidx,
-                       double* __restrict__ sval, uint32_t* counts) {
+                       const float* __restrict__ stage, const double* d_gth, uint32_t* sidx, double* sval,
+                       uint32_t* counts, RSP2P p2p) {
   __shared__ uint32_t wtot[2][kWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (p2p.tab) {  // P2P: the survivors' chunks live in this rank's window
+    const int me = p2p.tab->rank, par = p2p.sp->par;
+    sidx = p2p.tab->sidx[me][par];
+    sval = p2p.tab->sval[me][par];
+    counts = p2p.tab->scnt[me][par];
+  }
   const double gth = FILTER ? *d_gth : 0.0;
   const uint64_t nwords = (W + 3) / 4;
   const uint32_t t0 = blockIdx.x * tpc, t1 = min(t0 + tpc, tiles);
@@ -798,12 +793,19 @@ __global__ void __launch_bounds__(kThreads)
     running += total;
   }
   if (tid == 0) counts[blockIdx.x] = running;
+  if (p2p.tab && blockIdx.x == 0 && tid == 0) {
+    // Chunk geometry for the peers; the chunk prefix, S and the flags are
+    // published by the next kernel on the stream (the P2P pull).
+    P2PPub* pub = &p2p.tab->hdr[p2p.tab->rank]->pub[p2p.sp->par];
+    pub->sur_G = gridDim.x;
+    pub->sur_cap = tpc * kRegionTile;
+  }
 }
 
 template <int P, bool FILTER>
 static cudaError_t region_scan_dispatch(Launch& L, const Stage& S, uint64_t lo, uint64_t W, uint32_t* mask,
                                         const float* stage, const double* d_gth, uint32_t* out_idx,
-                                        double* out_val, uint64_t* d_count, const PubSur* pub) {
+                                        double* out_val, uint64_t* d_count, const RSP2P* p2p) {
   constexpr int TILE = kRegionTile;
   const uint64_t tiles = (W + TILE - 1) / TILE;
   static int cap = 0;
@@ -811,17 +813,17 @@ static cudaError_t region_scan_dispatch(Launch& L, const Stage& S, uint64_t lo, 
   const uint32_t G = chunks_for(tiles, cap, S.max_chunks);
   const uint32_t tpc = uint32_t(std::max<uint64_t>((tiles + G - 1) / G, 1));
   region_scan_kernel<P, FILTER><<<G, kThreads, 0, L.s>>>(lo, W, uint32_t(tiles), tpc, mask, stage, d_gth, S.sidx,
-                                                         S.sval, S.counts);
+                                                         S.sval, S.counts, p2p ? *p2p : RSP2P{});
   ++L.launches;
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || p2p) return e;  // P2P: peers read the chunks in place
   return launch_compact<2>(L, S, G, uint64_t(tpc) * TILE, nullptr, false, nullptr, out_idx, out_val, d_count,
-                           nullptr, nullptr, pub);
+                           nullptr);
 }
 
 cudaError_t launch_region_scan(Launch& L, const Stage& S, int P, bool filter, uint64_t lo, uint64_t W,
                                uint32_t* mask, const float* stage, const double* d_gth, uint32_t* out_idx,
-                               double* out_val, uint64_t* d_count, const PubSur* pub) {
+                               double* out_val, uint64_t* d_count, const RSP2P* pub) {
 #define OKT_RS(PP)                                                                                          \
   return filter ? region_scan_dispatch<PP, true>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count, pub) \
                 : region_scan_dispatch<PP, false>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count, pub)

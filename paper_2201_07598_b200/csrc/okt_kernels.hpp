@@ -79,7 +79,7 @@ struct Segs {
 cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, const float* eps_in,
                       float* eps_out, float alpha, uint64_t n, const double* d_th, const double* d_th2,
                       const OutCoo& out, uint64_t* d_m, uint64_t* d_m2, uint32_t* d_flags,
-                      uint32_t* d_hist, const ApplyArgs* ap = nullptr, const PubL* pub = nullptr,
+                      uint32_t* d_hist, const ApplyArgs* ap = nullptr, const K1P2P* p2p = nullptr,
                       const StepPtrs* ind = nullptr);
 
 // K2/K4: exact k-th largest magnitude (k clamped to the element count) by MSD
@@ -118,7 +118,7 @@ cudaError_t launch_scatter(Launch& L, const Segs& segs, uint64_t lo, uint64_t W,
 cudaError_t launch_region_scan(Launch& L, const Stage& S, int P, bool filter, uint64_t lo, uint64_t W,
                                uint32_t* mask, const float* stage, const double* d_gth,
                                uint32_t* out_idx, double* out_val, uint64_t* d_count,
-                               const PubSur* pub = nullptr);
+                               const RSP2P* p2p = nullptr);
 
 // Small control kernels.
 cudaError_t launch_slice_offsets(Launch& L, const uint64_t* coo, const uint64_t* d_m,
@@ -141,18 +141,13 @@ cudaError_t launch_scatter_heavy(Launch& L, const uint32_t* pos, const float* va
                                  uint64_t count, float* out);
 
 // ---- device-driven multi-GPU exchange (okt_p2p.cu) ----------------------------
-// K1 phase B for the P2P path: compaction into the window's L, slice offsets,
-// publication of (offsets, status) and of the L-ready flag to every peer.
-cudaError_t launch_p2p_compact_L(Launch& L, const Stage& S, uint32_t G, uint64_t chunk_cap, uint64_t* out,
-                                 uint64_t* d_m, const PubL& pub);
 // Waits for every peer's L, then scatters my slices read out of their HBM.
-cudaError_t launch_p2p_scatter(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, const uint64_t* d_off,
-                               P2PPlan* plan, uint64_t lo, uint64_t W, uint32_t* mask, float* stage,
-                               uint32_t* d_flags, uint64_t timeout_ns);
+cudaError_t launch_p2p_scatter(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
+                               uint64_t W, uint32_t* mask, float* stage, uint32_t* d_flags, uint64_t timeout_ns);
 // Waits for every rank's survivors, plans (offsets / balance), pulls u.
 cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, const uint64_t* d_S,
                                   P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns,
-                                  const P2PApply& ap);
+                                  const P2PApply& ap, const K1Totals& totals);
 // indexes = {u_idx[j] : sel[j]} in order (the K7 intersection, after a fused apply).
 cudaError_t launch_select_flags(Launch& L, const Stage& S, const uint8_t* sel, const PeerTab* d_tab,
                                 const StepPtrs* sp, const uint64_t* d_U, uint64_t bound, uint32_t* out,

@@ -42,10 +42,13 @@ enum P2PFlag { kFlagLReady = 0, kFlagSurReady = 1, kFlagBlockReady = 2, kP2PFlag
 
 // What a rank publishes for its peers each step (double-buffered by parity).
 struct P2PPub {
-  uint64_t off[kP2PMaxP + 1];  // slice offsets of the local selection L
-  uint64_t status;             // non-zero: this rank's step failed (non-finite input)
-  uint64_t S;                  // survivors of the global threshold
-  uint64_t pad[5];
+  uint64_t status;   // non-zero: this rank's step failed (non-finite input)
+  uint64_t S;        // survivors of the global threshold
+  uint32_t k1_G;     // K1 chunk geometry: chunks and entries per chunk
+  uint32_t k1_cap;
+  uint32_t sur_G;    // region-scan chunk geometry
+  uint32_t sur_cap;
+  uint64_t pad[4];
 };
 
 struct P2PHdr {
@@ -53,13 +56,19 @@ struct P2PHdr {
   P2PPub pub[2];
 };
 
-// Peer table: every rank's window pieces (index = rank), both parities.
+// Peer table: every rank's window pieces (index = rank), both parities.  The
+// chunked phase-A outputs are consumed in place: no compaction pass sits
+// between a producer and its peers.
 struct PeerTab {
   P2PHdr* hdr[kP2PMaxP];
-  uint64_t* L[kP2PMaxP][2];
-  uint32_t* sur_idx[kP2PMaxP][2];
-  double* sur_val[kP2PMaxP][2];
-  uint32_t* u_idx[kP2PMaxP][2];
+  uint64_t* kstg[kP2PMaxP][2];  // K1 chunk-local staging (AoS u32 idx | f32 val)
+  uint32_t* kcnt[kP2PMaxP][2];  // entries per K1 chunk
+  uint32_t* klt[kP2PMaxP][2];   // [chunk][kP2PMaxP] entries below each cut
+  uint32_t* sidx[kP2PMaxP][2];  // region-scan chunk staging (survivors)
+  double* sval[kP2PMaxP][2];
+  uint32_t* scnt[kP2PMaxP][2];  // survivors per chunk
+  uint64_t* spre[kP2PMaxP][2];  // exclusive prefix of scnt (chunks + 1 entries)
+  uint32_t* u_idx[kP2PMaxP][2]; // allgathered u
   double* u_val[kP2PMaxP][2];
   int P;
   int rank;
@@ -86,22 +95,20 @@ struct P2PApply {
   uint8_t* sel = nullptr;       // per u entry: 1 if in the local selection
 };
 
-// Fused publication hooks (phase B of a compaction publishes what it wrote).
-struct PubL {  // K1 phase B: local selection L + its slice offsets
+// P2P mode of K1 (phase A writes straight into the window and its last CTA
+// publishes) and of the region scan (same, for the survivors).
+struct K1P2P {
   const PeerTab* tab = nullptr;  // device copy
   const StepPtrs* sp = nullptr;  // epoch / parity of the step
-  int P = 1;
-  uint32_t* done = nullptr;      // last-CTA counter (self-resetting)
-  uint32_t* lt = nullptr;        // [chunk][kP2PMaxP] entries below each cut
   const uint64_t* cuts = nullptr;
-  uint64_t* d_off = nullptr;     // local copy of the slice offsets
-  const uint32_t* flags = nullptr;
 };
-struct PubSur {  // region scan phase B: survivors of the global threshold
+struct K1Totals {  // where the local selection size / slice offsets go
+  uint64_t* d_m = nullptr;
+  uint64_t* d_off = nullptr;
+};
+struct RSP2P {
   const PeerTab* tab = nullptr;
   const StepPtrs* sp = nullptr;
-  uint32_t* done = nullptr;
-  const uint32_t* flags = nullptr;
 };
 
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
