@@ -54,7 +54,43 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=32)
     ap.add_argument("--trace", default="", help="directory: dump a CUPTI timeline (torch.profiler) of 16 steps")
-    return ap.parse_args()
+    ap.add_argument("--no-l2-flush", action="store_true", help="diagnostics only: skip the L2 flush between steps")
+    ap.add_argument("--p2p-trace", default="",
+                    help="directory: dump per-CTA globaltimer stamps of the last device-driven (P2P) step")
+    a = ap.parse_args()
+    if a.p2p_trace:
+        os.environ["OKT_P2P_TRACE"] = "1"  # read when the comm maps its peers
+    return a
+
+
+def dump_p2p_trace(L, comm, rank, outdir):
+    """Per-kernel spans of the last P2P step from the CTAs' %globaltimer stamps
+    (okt_debug_p2p_trace), relative to the first K1 CTA start."""
+    import numpy as np
+    kinds, ctas = 5, 2048
+    buf = (ctypes.c_uint64 * (kinds * ctas * 4))()
+    if L.okt_debug_p2p_trace(comm, buf, kinds * ctas * 4):
+        return
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(kinds, ctas, 4).astype(np.int64)
+    used = a[:, :, 0] > 0
+    t0 = a[0, :, 0][used[0]].min() if used[0].any() else 0
+    out = {}
+    for k, nm in enumerate(["k1", "scatter", "region_scan", "pull0", "pull1"]):
+        u = used[k]
+        if not u.any():
+            continue
+        st, wt, en = a[k, u, 0] - t0, a[k, u, 1] - t0, a[k, u, 2] - t0
+        wt = wt[a[k, u, 1] > 0]
+        en = en[a[k, u, 2] > 0]
+        out[nm] = {"ctas": int(u.sum()), "start_min_us": float(st.min()) / 1e3, "start_max_us": float(st.max()) / 1e3,
+                   "waited_min_us": float(wt.min()) / 1e3 if wt.size else None,
+                   "waited_max_us": float(wt.max()) / 1e3 if wt.size else None,
+                   "end_med_us": float(np.median(en)) / 1e3 if en.size else None,
+                   "end_max_us": float(en.max()) / 1e3 if en.size else None}
+    os.makedirs(outdir, exist_ok=True)
+    np.save(os.path.join(outdir, f"p2p_trace_rank{rank}.npy"), a)
+    with open(os.path.join(outdir, f"p2p_trace_rank{rank}.json"), "w") as f:
+        json.dump(out, f, indent=1)
 
 
 def dist_env():
@@ -71,7 +107,7 @@ def workload(args, P):
             "tau": args.tau, "tau_prime": args.tau_prime, "bucket": args.bucket,
             "inputs": f"drifting_gradient_process(t, seed=1, rank_key=r+1), ring of {args.ring} snapshots",
             "parallelism": f"dp{P} (one process per GPU, NCCL/NVLink)" if P > 1 else "single GPU",
-            "l2": "flushed (256 MiB write) before every timed step"}
+            "l2": "not flushed (diagnostic run)" if args.no_l2_flush else "flushed (256 MiB write) before every timed step"}
 
 
 # ---- clocks ----------------------------------------------------------------------
@@ -243,7 +279,7 @@ def run_okt(args):
         assert L.okt_gen_drift(ctypes.c_void_p(buf.data_ptr()), n, i + 1, 1, rank + 1, 0, sp) == 0
     wmodel = torch.zeros(n, dtype=torch.float32, device="cuda")
     assert L.okt_residual_reset(comm, n, None, sp) == 0
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = torch.empty((1 << 20) if args.no_l2_flush else (256 << 20), dtype=torch.uint8, device="cuda")
     res = OktResult()
 
     def barrier():
@@ -305,6 +341,8 @@ def run_okt(args):
     L.okt_kernel_launches(comm, ctypes.byref(launches1))
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
+    if args.p2p_trace:
+        dump_p2p_trace(L, comm, rank, args.p2p_trace)
     # ---- the same timed loop again with the library's per-phase CUDA events
     # on its stream (phase breakdown + the K1 roofline)
     from paper_2201_07598_b200._lib import OKT_T_COUNT, TIMER_NAMES

@@ -278,6 +278,11 @@ int okt_phase_bytes(okt_comm* comm, double* bytes_out /* OKT_T_COUNT */);
 int okt_reset_phase_times(okt_comm* comm);
 /* Number of kernels this comm has launched since creation. */
 int okt_kernel_launches(const okt_comm* comm, uint64_t* out);
+/* Diagnostics: per-CTA %globaltimer stamps (ns) of the last device-driven
+ * (NVLink P2P) step, [5 kernels: K1, scatter, region scan, pull 0, pull 1]
+ * x [2048 CTAs] x [start, after waits, end, 0].  Recorded only when the comm
+ * was set up with OKT_P2P_TRACE in the environment (else OKT_ERR_CONFIG). */
+int okt_debug_p2p_trace(okt_comm* comm, uint64_t* out, size_t n_words);
 
 /* ---- seeded input generators (bit-exact ports of the reference's rng.hpp
  * streams, rounded to fp32; not on the hot path) ---------------------------- */

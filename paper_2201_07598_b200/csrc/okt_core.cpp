@@ -197,7 +197,7 @@ struct okt_comm {
   okt::Stage S;
   // device-driven multi-GPU exchange (okt_p2p.cuh)
   bool p2p_checked = false, p2p = false;
-  Buf win, boot, tabd, selflags;
+  Buf win, boot, tabd, selflags, trbuf;
   const float* cur_acc = nullptr;  // the step's accumulator / model (P2P fused apply)
   float* cur_w = nullptr;
   size_t win_n = 0;
@@ -705,6 +705,12 @@ struct okt_comm {
         tab.u_idx[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.uidx[p]);
         tab.u_val[q][p] = reinterpret_cast<double*>(base[q] + lay.uval[p]);
       }
+    }
+    if (std::getenv("OKT_P2P_TRACE")) {
+      const size_t words = size_t(okt::kTraceKinds) * okt::kTraceCtas * 4;
+      if ((rc = ensure(trbuf, 8 * words))) return rc;
+      if ((rc = ck(cudaMemset(trbuf.p, 0, 8 * words), "memset"))) return rc;
+      tab.trace = trbuf.as<uint64_t>();
     }
     if ((rc = ensure(tabd, sizeof(okt::PeerTab)))) return rc;
     if ((rc = ck(cudaMemcpy(tabd.p, &tab, sizeof(okt::PeerTab), cudaMemcpyHostToDevice), "tab"))) return rc;
@@ -1921,6 +1927,17 @@ int okt_reset_phase_times(okt_comm* c) {
 int okt_kernel_launches(const okt_comm* c, uint64_t* out) {
   OKT_COMM_CHECK(c);
   if (out) *out = c->L.launches;
+  return OKT_OK;
+}
+
+int okt_debug_p2p_trace(okt_comm* c, uint64_t* out, size_t n_words) {
+  OKT_COMM_CHECK(c);
+  if (!c->p2p || !c->tab.trace) return OKT_ERR_CONFIG;
+  const size_t words = std::min(n_words, size_t(okt::kTraceKinds) * okt::kTraceCtas * 4);
+  cudaSetDevice(c->device);
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(out, c->tab.trace, 8 * words, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return OKT_ERR_CUDA;
   return OKT_OK;
 }
 

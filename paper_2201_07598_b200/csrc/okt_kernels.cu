@@ -202,6 +202,8 @@ __global__ void __launch_bounds__(kThreads)
       s_below[threadIdx.x] = 0;
     }
   }
+  uint64_t* const trace = p2p_on ? p2p.tab->trace : nullptr;
+  if (trace && threadIdx.x == 0) trace_stamp(trace, kTrK1, 0);
   if (ind) {
     g = ind->g;
     eps_in = ind->eps_in;
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(kThreads)
     pub->k1_G = gridDim.x;
     pub->k1_cap = tpc * TILE;
   }
+  if (trace && (tid & 31) == 0) trace_stamp(trace, kTrK1, 2);
 }
 
 template <bool ACCUM, bool SELECT, bool HIST, bool DUAL>
@@ -709,6 +712,7 @@ __global__ void __launch_bounds__(kThreads)
     sidx = p2p.tab->sidx[me][par];
     sval = p2p.tab->sval[me][par];
     counts = p2p.tab->scnt[me][par];
+    if (FILTER && tid == 0) trace_stamp(p2p.tab->trace, kTrRegion, 0);
   }
   const double gth = FILTER ? *d_gth : 0.0;
   const uint64_t nwords = (W + 3) / 4;
@@ -800,6 +804,7 @@ __global__ void __launch_bounds__(kThreads)
     pub->sur_G = gridDim.x;
     pub->sur_cap = tpc * kRegionTile;
   }
+  if (FILTER && p2p.tab && lane == 0) trace_stamp(p2p.tab->trace, kTrRegion, 2);
 }
 
 template <int P, bool FILTER>

@@ -38,7 +38,11 @@ __global__ void __launch_bounds__(kThreads)
   const int par = sp->par;
   const int P = tab->P, me = tab->rank, q = threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (q == 0) s_abort = (*d_flags & 1u) ? 1 : 0;
+  uint64_t* const trace = tab->trace;
+  if (q == 0) {
+    s_abort = (*d_flags & 1u) ? 1 : 0;
+    trace_stamp(trace, kTrScatter, 0);
+  }
   if (blockIdx.x == 0 && q == 0) {
     // Publish this rank's K1 output (every K1 CTA finished before this kernel
     // started): status, then L-ready at every peer and at myself.
@@ -68,6 +72,7 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   if (s_abort) return;
   if (q == 0) {
+    trace_stamp(trace, kTrScatter, 1);
     uint32_t acc = 0;
     for (int r = 0; r < P; ++r) {
       s_start[r] = acc;
@@ -110,6 +115,7 @@ __global__ void __launch_bounds__(kThreads)
     }
     if (lane == 0 && b > a) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->seg_cnt[r]), b - a);
   }
+  if (lane == 0) trace_stamp(trace, kTrScatter, 2);
 }
 
 // Allgatherv by pulling.  round 0 waits for every rank's survivors and
@@ -130,7 +136,12 @@ __global__ void __launch_bounds__(kThreads)
   float* wm = (ap.on && ap.sgd) ? sp->w : nullptr;
   const int P = tab->P, me = tab->rank, q = threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (q == 0) s_abort = (*d_flags & (1u | 8u | 16u)) ? 1 : 0;
+  uint64_t* const trace = tab->trace;
+  const int trk = round == 0 ? kTrPull0 : kTrPull1;
+  if (q == 0) {
+    s_abort = (*d_flags & (1u | 8u | 16u)) ? 1 : 0;
+    trace_stamp(trace, trk, 0);
+  }
   __syncthreads();
   if (round == 0 && blockIdx.x == 0) {
     // Publish this rank's survivors (every region-scan CTA finished before
@@ -248,6 +259,7 @@ __global__ void __launch_bounds__(kThreads)
       if (d == P) *lt.d_m = o;
     }
   }
+  if (q == 0) trace_stamp(trace, trk, 1);
   if (s_abort) return;
   const bool bal = s_bal != 0;
   if (round == 1 && !bal) return;
@@ -326,6 +338,7 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   if (acc && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(d_flags, 4u);
+  if (lane == 0) trace_stamp(trace, trk, 2);
 }
 
 // Balanced case only: publish "my block is in u", wait for every other block.

@@ -72,7 +72,12 @@ struct PeerTab {
   double* u_val[kP2PMaxP][2];
   int P;
   int rank;
+  uint64_t* trace;  // diagnostics (OKT_P2P_TRACE): [kTraceKinds][kTraceCtas][4] globaltimer stamps, or null
 };
+// Per-CTA timestamps of the last P2P step (diagnostics only):
+// slot 0 = CTA start, 1 = after its flag waits / prologue, 2 = last warp done.
+enum TraceKind { kTrK1 = 0, kTrScatter = 1, kTrRegion = 2, kTrPull0 = 3, kTrPull1 = 4, kTraceKinds = 5 };
+constexpr int kTraceCtas = 2048;
 
 // Device-side plan of the balance + allgatherv phase (local memory).
 struct P2PPlan {
@@ -123,6 +128,16 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+__device__ __forceinline__ void trace_stamp(uint64_t* tr, int kind, int slot) {
+  if (tr && blockIdx.x < kTraceCtas) {
+    uint64_t* p = tr + (uint64_t(kind) * kTraceCtas + blockIdx.x) * 4 + slot;
+    if (slot == 2)
+      atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)globaltimer_ns());
+    else
+      *p = globaltimer_ns();
+  }
 }
 
 // Spin until *p >= epoch; false after `timeout_ns` (a peer died or diverged).
