@@ -107,7 +107,9 @@ def workload(args, P):
             "tau": args.tau, "tau_prime": args.tau_prime, "bucket": args.bucket,
             "inputs": f"drifting_gradient_process(t, seed=1, rank_key=r+1), ring of {args.ring} snapshots",
             "parallelism": f"dp{P} (one process per GPU, NCCL/NVLink)" if P > 1 else "single GPU",
-            "l2": "not flushed (diagnostic run)" if args.no_l2_flush else "flushed (256 MiB write) before every timed step"}
+            "l2": "not flushed (diagnostic run)" if args.no_l2_flush else
+            "flushed before every timed step, outside the events: 256 MiB write, then a 256 MiB read sweep "
+            "(clean L2: no write-back of the flush buffer inside the step)"}
 
 
 # ---- clocks ----------------------------------------------------------------------
@@ -202,6 +204,21 @@ def _cpu_model() -> str:
     return "unknown"
 
 
+class L2Flush:
+    """Evicts L2 between timed steps: a write of a buffer larger than L2, then
+    a read sweep of another one, so the step starts with L2 holding neither its
+    inputs nor dirty lines whose write-back it would pay for."""
+
+    def __init__(self, nbytes: int):
+        import torch
+        self.w = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        self.r = torch.zeros(nbytes // 8, dtype=torch.int64, device="cuda")
+
+    def fill_(self, v: int):
+        self.w.fill_(v)
+        self.r.sum()
+
+
 def trace_steps(args, rank, stream, step, t0, step_async=None, wait=None, flush=None):
     """CUPTI timeline of 16 steps: per-kernel device time and the idle gaps
     between them (host launch / sync latency), written next to a chrome trace."""
@@ -279,7 +296,7 @@ def run_okt(args):
         assert L.okt_gen_drift(ctypes.c_void_p(buf.data_ptr()), n, i + 1, 1, rank + 1, 0, sp) == 0
     wmodel = torch.zeros(n, dtype=torch.float32, device="cuda")
     assert L.okt_residual_reset(comm, n, None, sp) == 0
-    flush = torch.empty((1 << 20) if args.no_l2_flush else (256 << 20), dtype=torch.uint8, device="cuda")
+    flush = L2Flush(1 << 20 if args.no_l2_flush else 256 << 20)
     res = OktResult()
 
     def barrier():

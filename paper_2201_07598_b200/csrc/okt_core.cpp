@@ -747,7 +747,7 @@ struct okt_comm {
                              okt::OutCoo{}, &d()->m, nullptr, &d()->flags, nullptr, nullptr, &kp, sp),
               "k1");
     tmark(OKT_T_MERGE, s);
-    if (!rc) rc = ck(okt::launch_p2p_scatter(L, dt, sp, dp, lo, W, mask.as<uint32_t>(), stage.as<float>(),
+    if (!rc) rc = ck(okt::launch_p2p_scatter(L, dt, sp, dp, lo, W, n, mask.as<uint32_t>(), stage.as<float>(),
                                              &d()->flags, kP2PTimeoutNs), "p2p");
     okt::RSP2P rp;
     rp.tab = dt;

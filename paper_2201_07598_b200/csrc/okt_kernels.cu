@@ -36,6 +36,17 @@ int resident_ctas(K kernel, int threads, int sms) {
   return per_sm * sms;
 }
 
+// First tile of chunk c when `tiles` tiles are split evenly over G chunks:
+// floor(c * tiles / G), in 32-bit arithmetic whenever the product fits (the
+// 64-bit division is a called subroutine).
+__device__ __forceinline__ uint64_t split_at(uint32_t c, uint64_t tiles, uint32_t G) {
+  const uint64_t m = uint64_t(c) * tiles;
+  return m <= 0xffffffffull ? uint64_t(uint32_t(m) / G) : m / G;
+}
+
+// Same, for launches whose host side checked tiles * G < 2^32.
+__device__ __forceinline__ uint32_t split_at32(uint32_t c, uint32_t tiles, uint32_t G) { return c * tiles / G; }
+
 __device__ __forceinline__ bool nonfinite(float a) {
   return (__float_as_uint(a) & 0x7f800000u) == 0x7f800000u;
 }
@@ -226,8 +237,10 @@ __global__ void __launch_bounds__(kThreads)
   }
   bool bad = false;
   uint32_t running = 0, mloc = 0;
-  const uint32_t t0 = blockIdx.x * tpc;
-  const uint32_t t1 = min(t0 + tpc, tiles);
+  // balanced split: every chunk gets floor or ceil(tiles / G) tiles (the
+  // staging capacity per chunk stays tpc = ceil(tiles / G) tiles)
+  const uint32_t t0 = split_at32(blockIdx.x, tiles, gridDim.x);
+  const uint32_t t1 = split_at32(blockIdx.x + 1, tiles, gridDim.x);
   uint64_t* out = stg + uint64_t(blockIdx.x) * tpc * TILE;
   int parity = 0;
   for (uint32_t tile = t0; tile < t1; ++tile, parity ^= 1) {
@@ -381,6 +394,7 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
   int& cap = vec ? cap_v : cap_s;
   if (!cap) cap = resident_ctas(kern, kThreads, L.sms);
   const uint32_t G = chunks_for(tiles, cap, S.max_chunks);
+  if (uint64_t(tiles) * G > 0xffffffffull) return cudaErrorInvalidValue;  // split_at32's range
   const uint32_t tpc = uint32_t((tiles + G - 1) / G);
   // Profiling events: inside a stream capture they must be external event
   // nodes (re-recorded at every graph launch); outside, plain records.
@@ -445,7 +459,7 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t tiles = (cnt + kTileK - 1) / kTileK;
   const uint64_t tpc = (tiles + gridDim.x - 1) / gridDim.x;
   if (blockIdx.x == 0 && tid == 0) *d_cap = tpc * kTileK;
-  const uint64_t t0 = uint64_t(blockIdx.x) * tpc, t1 = min(t0 + tpc, tiles);
+  const uint64_t t0 = split_at(blockIdx.x, tiles, gridDim.x), t1 = split_at(blockIdx.x + 1, tiles, gridDim.x);
   const uint64_t obase = uint64_t(blockIdx.x) * tpc * kTileK;
   uint32_t running = 0;
   int parity = 0;
@@ -522,7 +536,7 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t tiles = (cnt + kTileK - 1) / kTileK;
   const uint64_t tpc = (tiles + gridDim.x - 1) / gridDim.x;
   if (blockIdx.x == 0 && tid == 0) *d_cap = tpc * kTileK;
-  const uint64_t t0 = uint64_t(blockIdx.x) * tpc, t1 = min(t0 + tpc, tiles);
+  const uint64_t t0 = split_at(blockIdx.x, tiles, gridDim.x), t1 = split_at(blockIdx.x + 1, tiles, gridDim.x);
   const uint64_t obase = uint64_t(blockIdx.x) * tpc * kTileK;
   uint32_t running = 0;
   bool bad = false;
@@ -596,7 +610,7 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t tiles = (cnt + kTileK - 1) / kTileK;
   const uint64_t tpc = (tiles + gridDim.x - 1) / gridDim.x;
   if (blockIdx.x == 0 && tid == 0) *d_cap = tpc * kTileK;
-  const uint64_t t0 = uint64_t(blockIdx.x) * tpc, t1 = min(t0 + tpc, tiles);
+  const uint64_t t0 = split_at(blockIdx.x, tiles, gridDim.x), t1 = split_at(blockIdx.x + 1, tiles, gridDim.x);
   const uint64_t obase = uint64_t(blockIdx.x) * tpc * kTileK;
   uint32_t running = 0;
   int parity = 0;
@@ -691,6 +705,46 @@ __device__ __forceinline__ double bracket_sum(const float* st, uint32_t bits) {
   return a[0];
 }
 
+// All P staged slots of one coordinate in one vector load (the row is
+// P * 4 bytes, aligned to it); absent slots are loaded and ignored.
+template <int P>
+__device__ __forceinline__ void load_slots(const float* __restrict__ st, float (&v)[P]) {
+  if constexpr (P == 1) {
+    v[0] = st[0];
+  } else if constexpr (P == 2) {
+    const float2 x = *reinterpret_cast<const float2*>(st);
+    v[0] = x.x; v[1] = x.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < P; q += 4) {
+      const float4 x = *reinterpret_cast<const float4*>(st + q);
+      v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
+    }
+  }
+}
+// bracket_sum over values already in registers.
+template <int P>
+__device__ __forceinline__ double bracket_regs(const float (&v)[P], uint32_t bits) {
+  double a[P];
+  bool h[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) {
+    h[q] = (bits >> q) & 1u;
+    a[q] = h[q] ? double(v[q]) : 0.0;
+  }
+#pragma unroll
+  for (int s = P >> 1; s >= 1; s >>= 1) {
+#pragma unroll
+    for (int q = 0; q < s; ++q) {
+      if (h[q] && h[q + s]) a[q] = a[q] + a[q + s];
+      else if (h[q + s]) a[q] = a[q + s];
+      h[q] = h[q] || h[q + s];
+    }
+  }
+  return a[0];
+}
+constexpr int kGather = 4;
+
 // Thread-contiguous layout: thread t of a tile owns coordinates
 // [t*32, t*32+32) (eight mask words, two 16 B loads), so its selected set is a
 // 32-bit mask and the tile order is (thread, bit): one warp scan + one CTA
@@ -701,7 +755,7 @@ constexpr int kRegionTile = kThreads * kRegionCoordsPerThread;  // 8192 coordina
 static_assert(kRegionTile == kRegionTileHost, "staging sized for the region tile");
 
 template <int P, bool FILTER>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
     region_scan_kernel(uint64_t lo, uint64_t W, uint32_t tiles, uint32_t tpc, uint32_t* mask,
                        const float* __restrict__ stage, const double* d_gth, uint32_t* sidx, double* sval,
                        uint32_t* counts, RSP2P p2p) {
@@ -716,7 +770,8 @@ __global__ void __launch_bounds__(kThreads)
   }
   const double gth = FILTER ? *d_gth : 0.0;
   const uint64_t nwords = (W + 3) / 4;
-  const uint32_t t0 = blockIdx.x * tpc, t1 = min(t0 + tpc, tiles);
+  const uint32_t t0 = split_at32(blockIdx.x, tiles, gridDim.x);
+  const uint32_t t1 = split_at32(blockIdx.x + 1, tiles, gridDim.x);
   const uint64_t obase = uint64_t(blockIdx.x) * tpc * kRegionTile;
   uint32_t running = 0;
   int parity = 0;
@@ -739,23 +794,45 @@ __global__ void __launch_bounds__(kThreads)
       for (int c = 0; c < 4; ++c)
         if ((mw[j] >> (8 * c)) & 0xffu) present |= 1u << (j * 4 + c);
     const uint64_t c0 = w0 * 4;  // first coordinate (region-relative)
-    auto bits_of = [&](int k) { return (mw[k >> 2] >> (8 * (k & 3))) & 0xffu; };
-    // Values of the first two emitted coordinates stay in registers.
-    uint32_t sel = FILTER ? 0u : present;
-    double v_first[2] = {0.0, 0.0};
-    int k_first[2] = {-1, -1};
-    int kept = 0;
-    for (uint32_t rest = present; rest; rest &= rest - 1) {
-      const int k = __ffs(rest) - 1;
-      const double v = bracket_sum<P>(stage + (c0 + k) * P, bits_of(k));
-      const bool keep = !FILTER || fabs(v) >= gth;
-      if (FILTER && keep) sel |= 1u << k;
-      if (keep && kept < 2) {
-        v_first[kept] = v;
-        k_first[kept] = k;
-        ++kept;
-      } else if (!FILTER && kept >= 2) {
-        break;  // REGION mode: the rest is gathered after the scan
+    auto bits_of = [&](int k) {  // select tree: keeps mw[] in registers
+      const int j = k >> 2;
+      const uint32_t w01 = (j & 1) ? mw[1] : mw[0], w23 = (j & 1) ? mw[3] : mw[2];
+      const uint32_t w45 = (j & 1) ? mw[5] : mw[4], w67 = (j & 1) ? mw[7] : mw[6];
+      const uint32_t w03 = (j & 2) ? w23 : w01, w47 = (j & 2) ? w67 : w45;
+      return (((j & 4) ? w47 : w03) >> (8 * (k & 3))) & 0xffu;
+    };
+    // The first kGather present coordinates: all their stage loads are issued
+    // together (one memory round trip), and their sums stay in registers for
+    // the emit below.  Threads with more present coordinates (rare at top-k
+    // densities) walk the rest one by one.
+    int kk[kGather];
+    double vv[kGather];
+    {
+      uint32_t rest = present;
+#pragma unroll
+      for (int b = 0; b < kGather; ++b) {
+        kk[b] = rest ? __ffs(rest) - 1 : -1;
+        rest &= rest - 1;
+      }
+      float raw[kGather][P];
+#pragma unroll
+      for (int b = 0; b < kGather; ++b)
+        if (kk[b] >= 0) load_slots<P>(stage + (c0 + kk[b]) * P, raw[b]);
+#pragma unroll
+      for (int b = 0; b < kGather; ++b) vv[b] = kk[b] >= 0 ? bracket_regs<P>(raw[b], bits_of(kk[b])) : 0.0;
+    }
+    uint32_t sel = present;
+    if (FILTER) {
+      sel = 0u;
+#pragma unroll
+      for (int b = 0; b < kGather; ++b)
+        if (kk[b] >= 0 && fabs(vv[b]) >= gth) sel |= 1u << kk[b];
+      uint32_t rest = present;
+#pragma unroll
+      for (int b = 0; b < kGather; ++b) rest &= rest - 1;
+      for (; rest; rest &= rest - 1) {
+        const int k = __ffs(rest) - 1;
+        if (fabs(bracket_sum<P>(stage + (c0 + k) * P, bits_of(k))) >= gth) sel |= 1u << k;
       }
     }
     if (present) {
@@ -768,6 +845,7 @@ __global__ void __launch_bounds__(kThreads)
           if (w0 + j < nwords) mask[w0 + j] = 0u;
       }
     }
+    if (FILTER && p2p.tab && lane == 0) trace_stamp(p2p.tab->trace, kTrRegion, 1, true);
     // CTA exclusive scan of the per-thread counts.
     const uint32_t cnt = __popc(sel);
     uint32_t incl = cnt;
@@ -785,12 +863,19 @@ __global__ void __launch_bounds__(kThreads)
       wpre += (w < warp) ? x : 0u;
       total += x;
     }
+    if (FILTER && p2p.tab && lane == 0) trace_stamp(p2p.tab->trace, kTrRegion, 3, true);
     uint64_t pos = obase + running + wpre + incl - cnt;
-    int emitted = 0;
-    for (uint32_t rest = sel; rest; rest &= rest - 1, ++pos, ++emitted) {
+    for (uint32_t rest = sel; rest; rest &= rest - 1, ++pos) {
       const int k = __ffs(rest) - 1;
-      const double v = (emitted < 2 && k_first[emitted] == k) ? v_first[emitted]
-                                                              : bracket_sum<P>(stage + (c0 + k) * P, bits_of(k));
+      double v = 0.0;
+      bool have = false;
+#pragma unroll
+      for (int b = 0; b < kGather; ++b)
+        if (kk[b] == k) {
+          v = vv[b];
+          have = true;
+        }
+      if (!have) v = bracket_sum<P>(stage + (c0 + k) * P, bits_of(k));
       sidx[pos] = uint32_t(lo + c0 + k);
       sval[pos] = v;
     }
@@ -816,6 +901,7 @@ static cudaError_t region_scan_dispatch(Launch& L, const Stage& S, uint64_t lo, 
   static int cap = 0;
   if (!cap) cap = resident_ctas(region_scan_kernel<P, FILTER>, kThreads, L.sms);
   const uint32_t G = chunks_for(tiles, cap, S.max_chunks);
+  if (uint64_t(tiles) * G > 0xffffffffull) return cudaErrorInvalidValue;  // split_at32's range
   const uint32_t tpc = uint32_t(std::max<uint64_t>((tiles + G - 1) / G, 1));
   region_scan_kernel<P, FILTER><<<G, kThreads, 0, L.s>>>(lo, W, uint32_t(tiles), tpc, mask, stage, d_gth, S.sidx,
                                                          S.sval, S.counts, p2p ? *p2p : RSP2P{});

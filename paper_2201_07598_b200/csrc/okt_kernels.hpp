@@ -143,7 +143,8 @@ cudaError_t launch_scatter_heavy(Launch& L, const uint32_t* pos, const float* va
 // ---- device-driven multi-GPU exchange (okt_p2p.cu) ----------------------------
 // Waits for every peer's L, then scatters my slices read out of their HBM.
 cudaError_t launch_p2p_scatter(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
-                               uint64_t W, uint32_t* mask, float* stage, uint32_t* d_flags, uint64_t timeout_ns);
+                               uint64_t W, uint64_t n, uint32_t* mask, float* stage, uint32_t* d_flags,
+                               uint64_t timeout_ns);
 // Waits for every rank's survivors, plans (offsets / balance), pulls u.
 cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, const uint64_t* d_S,
                                   P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns,

@@ -23,76 +23,65 @@ namespace {
 constexpr uint32_t kAbortBits = 1u | 8u | 16u;  // local non-finite, peer timeout, peer failure
 }
 
-// K3 (M1) fused with the split exchange.  Each CTA waits until every peer
-// published its K1 chunks, then one warp per (source, chunk) reads that
-// chunk's slice for my region, [lt[c][me], lt[c][me+1]), straight out of the
-// source's HBM (NVLink) and scatters it into the presence mask /
-// coordinate-major staging.  Order does not matter here: the bracket scan
-// re-derives it from coordinates.
+// K3 (M1) fused with the split exchange.  Work items are (source, chunk,
+// part): only the K1 chunks whose coordinates overlap my region carry entries
+// for me, and each is split into `parts` so every warp of the grid gets a
+// share.  A warp reads its part of the chunk's slice for my region,
+// [lt[c][me], lt[c][me+1]), straight out of the source's HBM (NVLink for a
+// peer) and scatters it into the presence mask / coordinate-major staging.
+// My own chunks need no hand-off, so they are scattered first, while the
+// peers' L-ready flags are in flight.  Order does not matter here: the
+// bracket scan re-derives it from coordinates.
 __global__ void __launch_bounds__(kThreads)
     p2p_scatter_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo, uint64_t W,
-                       uint32_t* mask, float* stage, uint32_t* d_flags, uint64_t timeout_ns) {
-  __shared__ uint32_t s_G[kP2PMaxP], s_cap[kP2PMaxP], s_start[kP2PMaxP + 1];
+                       uint32_t k1_tiles, uint32_t* mask, float* stage, uint32_t* d_flags, uint64_t timeout_ns) {
+  __shared__ uint64_t s_seg[kP2PMaxP];
   __shared__ int s_abort;
   const uint64_t epoch = sp->epoch;
   const int par = sp->par;
   const int P = tab->P, me = tab->rank, q = threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t* const trace = tab->trace;
+  const P2PPub* my_pub = &tab->hdr[me]->pub[par];
+  const uint32_t G = my_pub->k1_G, cap = my_pub->k1_cap;  // same geometry on every rank (same n)
   if (q == 0) {
     s_abort = (*d_flags & 1u) ? 1 : 0;
     trace_stamp(trace, kTrScatter, 0);
   }
+  if (q < P) s_seg[q] = 0;
   if (blockIdx.x == 0 && q == 0) {
     // Publish this rank's K1 output (every K1 CTA finished before this kernel
-    // started): status, then L-ready at every peer and at myself.
+    // started): status, then L-ready at every rank (myself included).
     tab->hdr[me]->pub[par].status = (*d_flags & 1u) ? 1 : 0;
     __threadfence_system();
-    for (int r = 0; r < P; ++r) st_release_sys(&tab->hdr[r]->flag[kFlagLReady][me], epoch);
+    for (int r = 0; r < P; ++r) st_relaxed_sys(&tab->hdr[r]->flag[kFlagLReady][me], epoch);
   }
-  __syncthreads();
-  if (q < P) {
-    uint32_t G = 0, cap = 0;
-    if (!wait_flag(&tab->hdr[me]->flag[kFlagLReady][q], epoch, timeout_ns)) {
-      atomicOr(d_flags, 8u);
-      s_abort = 1;
-    } else {
-      const volatile P2PPub* pub = &tab->hdr[q]->pub[par];
-      G = pub->k1_G;
-      cap = pub->k1_cap;
-      if (q != me && pub->status) {
-        atomicOr(d_flags, 16u);
-        s_abort = 1;
-      }
-      if (blockIdx.x == 0) plan->peer_status[q] = pub->status;
-    }
-    s_G[q] = G;
-    s_cap[q] = cap;
+  // Chunks overlapping [lo, lo + W): chunk c holds tiles
+  // [c * tiles / G, (c + 1) * tiles / G) (k1_kernel's balanced split).
+  constexpr uint64_t T = kK1Tile;
+  uint32_t c_lo = 0, nch = 0;
+  if (W > 0 && G > 0) {
+    const uint64_t tl = lo / T, th = (lo + W - 1) / T;
+    c_lo = uint32_t(((tl + 1) * G + k1_tiles - 1) / k1_tiles - 1);
+    const uint32_t c_hi = uint32_t(((th + 1) * G + k1_tiles - 1) / k1_tiles - 1);
+    nch = c_hi - c_lo + 1;
   }
+  const uint32_t warps_total = gridDim.x * kWarps;
+  const uint32_t parts = max(1u, min(8u, warps_total / max(1u, uint32_t(P) * nch)));
+  const uint32_t per_src = nch * parts;
+  const uint32_t gw = blockIdx.x * kWarps + warp;
   __syncthreads();
-  if (s_abort) return;
-  if (q == 0) {
-    trace_stamp(trace, kTrScatter, 1);
-    uint32_t acc = 0;
-    for (int r = 0; r < P; ++r) {
-      s_start[r] = acc;
-      acc += s_G[r];
-    }
-    s_start[P] = acc;
-  }
-  __syncthreads();
-  const uint32_t items = s_start[P];
-  for (uint32_t it = blockIdx.x * kWarps + warp; it < items; it += gridDim.x * kWarps) {
-    int r = 0;
-    while (r + 1 < P && it >= s_start[r + 1]) ++r;
-    const uint32_t c = it - s_start[r];
+  auto run = [&](int r, uint32_t it) {
+    const uint32_t c = c_lo + it / parts, part = it % parts;
     const uint32_t* lt = tab->klt[r][par] + uint64_t(c) * kP2PMaxP;
-    const uint32_t a = lt[me];
-    const uint32_t b = (me + 1 < P) ? lt[me + 1] : tab->kcnt[r][par][c];
-    const uint64_t* src = tab->kstg[r][par] + uint64_t(c) * s_cap[r];
-    // Every lane issues its (remote) loads for a 256-entry round before any
+    const uint32_t a0 = lt[me];
+    const uint32_t b0 = (me + 1 < P) ? lt[me + 1] : tab->kcnt[r][par][c];
+    const uint32_t len = b0 > a0 ? b0 - a0 : 0;
+    const uint32_t a = a0 + uint32_t(uint64_t(len) * part / parts), b = a0 + uint32_t(uint64_t(len) * (part + 1) / parts);
+    const uint64_t* src = tab->kstg[r][par] + uint64_t(c) * cap;
+    // Every lane issues its (remote) loads for a 128-entry round before any
     // store, so a round costs one NVLink round trip.
-    constexpr int R = 8;
+    constexpr int R = 4;
     for (uint32_t j0 = a; j0 < b; j0 += 32 * R) {
       uint64_t e[R];
 #pragma unroll
@@ -113,8 +102,37 @@ __global__ void __launch_bounds__(kThreads)
         atomicOr(&mask[i >> 2], 1u << (unsigned(i & 3u) * 8u + unsigned(r)));
       }
     }
-    if (lane == 0 && b > a) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->seg_cnt[r]), b - a);
+    if (lane == 0 && b > a) atomicAdd(reinterpret_cast<unsigned long long*>(&s_seg[r]), (unsigned long long)(b - a));
+  };
+  // 1. my own chunks (local HBM, no wait)
+  if (!s_abort)
+    for (uint32_t it = gw; it < per_src; it += warps_total) run(me, it);
+  // 2. wait for every peer's L-ready, then their chunks (NVLink)
+  if (q < P && q != me) {
+    if (!wait_flag(&tab->hdr[me]->flag[kFlagLReady][q], epoch, timeout_ns)) {
+      atomicOr(d_flags, 8u);
+      s_abort = 1;
+    } else {
+      const volatile P2PPub* pub = &tab->hdr[q]->pub[par];
+      const uint64_t st = pub->status;
+      if (st || pub->k1_G != G || pub->k1_cap != cap) {
+        atomicOr(d_flags, 16u);
+        s_abort = 1;
+      }
+      if (blockIdx.x == 0) plan->peer_status[q] = st;
+    }
   }
+  __syncthreads();
+  if (q == 0) trace_stamp(trace, kTrScatter, 1);
+  if (!s_abort) {
+    const uint32_t remote = uint32_t(P - 1) * per_src;
+    for (uint32_t it = gw; it < remote; it += warps_total) {
+      const uint32_t k = it / per_src;
+      run((me + 1 + int(k)) % P, it % per_src);
+    }
+  }
+  __syncthreads();
+  if (q < P && s_seg[q]) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->seg_cnt[q]), (unsigned long long)s_seg[q]);
   if (lane == 0) trace_stamp(trace, kTrScatter, 2);
 }
 
@@ -181,7 +199,7 @@ __global__ void __launch_bounds__(kThreads)
       mine->S = tot;
       mine->status = (*d_flags & (1u | 8u | 16u)) ? 1 : 0;
       __threadfence_system();
-      for (int r = 0; r < P; ++r) st_release_sys(&tab->hdr[r]->flag[kFlagSurReady][me], epoch);
+      for (int r = 0; r < P; ++r) st_relaxed_sys(&tab->hdr[r]->flag[kFlagSurReady][me], epoch);
     }
   }
   if (round == 0) {
@@ -299,14 +317,19 @@ __global__ void __launch_bounds__(kThreads)
   };
   if (round == 0) {
     const uint64_t a = bal ? s_blk[me] : 0, b = bal ? s_blk[me + 1] : s_off[P];
+    // (rank, chunk, part) work items: every chunk split so all warps get a share
     const uint32_t items = s_start[P];
-    for (uint32_t it = blockIdx.x * kWarps + warp; it < items; it += gridDim.x * kWarps) {
+    const uint32_t warps_total = gridDim.x * kWarps;
+    const uint32_t parts = max(1u, min(8u, warps_total / max(1u, items)));
+    for (uint32_t it = blockIdx.x * kWarps + warp; it < items * parts; it += warps_total) {
+      const uint32_t item = it / parts, part = it % parts;
       int r = 0;
-      while (r + 1 < P && it >= s_start[r + 1]) ++r;
-      const uint32_t c = it - s_start[r];
+      while (r + 1 < P && item >= s_start[r + 1]) ++r;
+      const uint32_t c = item - s_start[r];
       const uint64_t base = s_off[r] + tab->spre[r][par][c];
       const uint64_t end = base + tab->scnt[r][par][c];
-      const uint64_t lo = max(base, a), hi = min(end, b);
+      const uint64_t len = end - base;
+      const uint64_t lo = max(base + len * part / parts, a), hi = min(base + len * (part + 1) / parts, b);
       const uint32_t* si = tab->sidx[r][par] + uint64_t(c) * s_cap[r];
       const double* sv = tab->sval[r][par] + uint64_t(c) * s_cap[r];
       for (uint64_t p0 = lo; p0 < hi; p0 += 32 * R) {
@@ -347,17 +370,22 @@ __global__ void p2p_block_sync_kernel(const PeerTab* __restrict__ tab, const Ste
   const uint64_t epoch = sp->epoch;
   const int P = tab->P, me = tab->rank, q = threadIdx.x;
   if (!plan->balanced || (*d_flags & (1u | 8u | 16u))) return;
-  __threadfence_system();
   __syncthreads();
-  if (q < P && q != me) st_release_sys(&tab->hdr[q]->flag[kFlagBlockReady][me], epoch);
+  if (q < P && q != me) {
+    __threadfence_system();
+    st_relaxed_sys(&tab->hdr[q]->flag[kFlagBlockReady][me], epoch);
+  }
   if (q < P && q != me && !wait_flag(&tab->hdr[me]->flag[kFlagBlockReady][q], epoch, timeout_ns))
     atomicOr(d_flags, 8u);
 }
 
 // ---- launchers ----------------------------------------------------------------------------
 cudaError_t launch_p2p_scatter(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
-                               uint64_t W, uint32_t* mask, float* stage, uint32_t* d_flags, uint64_t timeout_ns) {
-  p2p_scatter_kernel<<<L.sms * 2, kThreads, 0, L.s>>>(d_tab, sp, plan, lo, W, mask, stage, d_flags, timeout_ns);
+                               uint64_t W, uint64_t n, uint32_t* mask, float* stage, uint32_t* d_flags,
+                               uint64_t timeout_ns) {
+  const uint32_t k1_tiles = uint32_t((n + kK1Tile - 1) / kK1Tile);
+  p2p_scatter_kernel<<<L.sms * 2, kThreads, 0, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, mask, stage, d_flags,
+                                                      timeout_ns);
   ++L.launches;
   return cudaGetLastError();
 }

@@ -119,6 +119,13 @@ struct RSP2P {
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Publishing to P ranks: one __threadfence_system() (fence.sc.sys), then a
+// relaxed system-scope store per rank — the fence-based release pattern.  A
+// st.release.sys per rank would pay one system fence each (~1.8 us apiece on
+// B200; tools/p2p_lat.cu measures it).
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -130,10 +137,10 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 
-__device__ __forceinline__ void trace_stamp(uint64_t* tr, int kind, int slot) {
+__device__ __forceinline__ void trace_stamp(uint64_t* tr, int kind, int slot, bool max = false) {
   if (tr && blockIdx.x < kTraceCtas) {
     uint64_t* p = tr + (uint64_t(kind) * kTraceCtas + blockIdx.x) * 4 + slot;
-    if (slot == 2)
+    if (slot == 2 || max)
       atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)globaltimer_ns());
     else
       *p = globaltimer_ns();
