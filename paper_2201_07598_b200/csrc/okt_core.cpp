@@ -124,7 +124,7 @@ okt_state default_state() {
 }
 
 // Symmetric P2P window layout (identical on every rank for a given n): per
-// parity, K1's chunked staging + chunk counts + per-chunk cut counts, the
+// parity, K1's per-tile staging + tile counts + per-tile cut counts, the
 // region scan's chunked survivors + counts + chunk prefix, and u.
 struct WinLayout {
   size_t kstg[2], kcnt[2], klt[2], sidx[2], sval[2], scnt[2], spre[2], uidx[2], uval[2], bytes;
@@ -134,12 +134,13 @@ WinLayout win_layout(size_t n, int max_chunks) {
   const size_t kst = okt::stage_entries(n, okt::kK1Tile, max_chunks);
   const size_t sst = okt::stage_entries(n, okt::kRegionTileHost, max_chunks);
   const size_t mc = size_t(max_chunks);
+  const size_t kt = std::max(mc, (n + okt::kK1Tile - 1) / okt::kK1Tile);  // K1 counts are per tile
   WinLayout w;
   size_t o = al(sizeof(okt::P2PHdr));
   for (int p = 0; p < 2; ++p) {
     w.kstg[p] = o; o += al(8 * kst);
-    w.kcnt[p] = o; o += al(4 * mc);
-    w.klt[p] = o; o += al(4 * okt::kP2PMaxP * mc);
+    w.kcnt[p] = o; o += al(4 * kt);
+    w.klt[p] = o; o += al(4 * okt::kP2PMaxP * kt);
     w.sidx[p] = o; o += al(4 * sst);
     w.sval[p] = o; o += al(8 * sst);
     w.scnt[p] = o; o += al(4 * mc);
@@ -192,7 +193,7 @@ struct okt_comm {
   Buf eps[2];
   Buf hgrad;               // staging for the host-buffer entry points
   Buf st64, stidx, stval;  // phase-A compaction staging
-  Buf counts, counts2, chunkcap;
+  Buf counts, counts2, chunkcap, tilectr;
   Buf hist, scal;
   okt::Stage S;
   // device-driven multi-GPU exchange (okt_p2p.cuh)
@@ -204,8 +205,9 @@ struct okt_comm {
   okt::PeerTab tab{};
   std::vector<void*> ipc_open;
   uint64_t p2p_epoch = 0;
-  // CUDA graph of the steady single-rank step (memset, K1, fused compaction +
-  // apply, scalar readback); per-step pointers come through `ptrsb`.
+  // CUDA graph of the steady single-rank step (step block H2D, K1, fused
+  // compaction + apply, scalar readback); per-step pointers are read from the
+  // step block (DevScalars::sp) on the device.
   struct StepGraph {
     cudaGraphExec_t exec = nullptr;
     size_t n = 0, k = 0;
@@ -214,8 +216,6 @@ struct okt_comm {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
   } graph1;
   uint64_t buf_gen = 1;
-  Buf ptrsb;
-  okt::StepPtrs* hptrs = nullptr;
   DevScalars* h = nullptr;   // pinned download mirror
   DevScalars* hup = nullptr; // pinned upload staging
   size_t cap_n = 0;
@@ -319,6 +319,9 @@ struct okt_comm {
     const size_t k1_stage = okt::stage_entries(n, okt::kK1Tile, S.max_chunks);
     const size_t coo_stage = std::max({okt::stage_entries(n, okt::kCooTile, S.max_chunks), k1_stage,
                                        okt::stage_entries(n, okt::kRegionTileHost, S.max_chunks)});
+    const size_t k1_tiles = (n + okt::kK1Tile - 1) / okt::kK1Tile;
+    const size_t ncounts = std::max<size_t>(size_t(S.max_chunks), k1_tiles);
+    if (e == cudaSuccess) e = counts.ensure(4 * ncounts);
     if (e == cudaSuccess) e = coo.ensure(8 * n);
     if (e == cudaSuccess) e = st64.ensure(8 * k1_stage);
     if (e == cudaSuccess) e = stidx.ensure(4 * coo_stage);
@@ -329,6 +332,8 @@ struct okt_comm {
       if (e == cudaSuccess) e = sur_val.ensure(8 * n);
       if (e == cudaSuccess) e = indexes.ensure(4 * n);
     }
+    S.counts = counts.as<uint32_t>();
+    S.max_tiles = ncounts;
     S.s64 = st64.as<uint64_t>();
     S.sidx = stidx.as<uint32_t>();
     S.sval = stval.as<double>();
@@ -724,7 +729,7 @@ struct okt_comm {
   // step block refresh, flag reset, K1 (+ slice offsets + L publication),
   // fused split/scatter, bracket scan (+ survivor publication), allgatherv
   // pull with the fused apply, indexes, scalar readback.  Per-step values
-  // (pointers, epoch, parity) are read from ptrsb on the device, so the same
+  // (pointers, epoch, parity) are read from the step block on the device, so the same
   // sequence is captured once into a CUDA graph.
   int enqueue_p2p_step(size_t n, size_t k, bool sgd, cudaStream_t s) {
     const okt::StepPtrs* sp = &d()->sp;
@@ -857,11 +862,12 @@ struct okt_comm {
                    bool sgd, cudaStream_t s) {
     int rc;
     StepGraph& G = graph1;
-    hptrs->g = g;
-    hptrs->eps_in = eps_in;
-    hptrs->eps_out = eps_out;
-    hptrs->w = w;
-    hptrs->alpha = alpha;
+    hup->sp.g = g;
+    hup->sp.eps_in = eps_in;
+    hup->sp.eps_out = eps_out;
+    hup->sp.w = w;
+    hup->sp.alpha = alpha;
+    hup->flags = 0;
     if (!G.exec || G.n != n || G.k != k || G.sgd != sgd || G.gen != buf_gen || G.prof != prof) {
       if (G.exec) {
         cudaGraphExecDestroy(G.exec);
@@ -871,12 +877,12 @@ struct okt_comm {
         cudaEventCreate(&G.e0);
         cudaEventCreate(&G.e1);
       }
-      if ((rc = ensure(ptrsb, sizeof(okt::StepPtrs)))) return rc;
-      const okt::StepPtrs* dp = ptrsb.as<okt::StepPtrs>();
+      const okt::StepPtrs* dp = &d()->sp;
       const uint64_t l0 = L.launches;
       if ((rc = ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture"))) return rc;
-      cudaMemcpyAsync(ptrsb.p, hptrs, sizeof(okt::StepPtrs), cudaMemcpyHostToDevice, s);
-      cudaMemsetAsync(&d()->flags, 0, 4, s);
+      // one H2D node: the step pointers and zeroed flags
+      cudaMemcpyAsync(&d()->sp, &hup->sp, offsetof(DevScalars, pad1) - offsetof(DevScalars, sp),
+                      cudaMemcpyHostToDevice, s);
       if (prof) cudaEventRecordWithFlags(G.e0, s, cudaEventRecordExternal);
       okt::ApplyArgs ap;
       if (sgd) ap = okt::ApplyArgs{nullptr, nullptr, &d()->flags, dp};
@@ -1316,15 +1322,17 @@ int init_comm(okt_comm* c) {
   if (e == cudaSuccess) e = c->counts.ensure(4 * size_t(c->S.max_chunks));
   if (e == cudaSuccess) e = c->counts2.ensure(4 * size_t(c->S.max_chunks));
   if (e == cudaSuccess) e = c->chunkcap.ensure(64);
+  c->tilectr.zero_init = true;
+  if (e == cudaSuccess) e = c->tilectr.ensure(64);
   if (e == cudaSuccess) e = cudaMallocHost(&c->h, sizeof(DevScalars));
   if (e == cudaSuccess) e = cudaMallocHost(&c->hup, sizeof(DevScalars));
-  if (e == cudaSuccess) e = cudaMallocHost(&c->hptrs, sizeof(okt::StepPtrs));
   if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("init: ") + cudaGetErrorString(e));
   std::memset(c->h, 0, sizeof(DevScalars));
   std::memset(c->hup, 0, sizeof(DevScalars));
   c->S.counts = c->counts.as<uint32_t>();
   c->S.counts2 = c->counts2.as<uint32_t>();
   c->S.chunk_cap = c->chunkcap.as<uint64_t>();
+  c->S.tile_ctr = c->tilectr.as<uint32_t>();
   return c->reserve(4096);
 }
 
@@ -1451,7 +1459,6 @@ int okt_comm_destroy(okt_comm* c) {
   if (c->ready_ev) cudaEventDestroy(c->ready_ev);
   if (c->h) cudaFreeHost(c->h);
   if (c->hup) cudaFreeHost(c->hup);
-  if (c->hptrs) cudaFreeHost(c->hptrs);
   if (c->graph1.exec) cudaGraphExecDestroy(c->graph1.exec);
   if (c->graph1.e0) {
     cudaEventDestroy(c->graph1.e0);
@@ -1625,18 +1632,28 @@ static int copy_result_to_host(okt_comm* c, const okt_result& r, uint32_t* h_idx
   return c->ck(e, "copy result");
 }
 
+// The host gradient is staged into device memory with one H2D copy (copy
+// engine).  Reading a pinned gradient in place from K1 over PCIe was measured
+// slower end to end (1.27 vs 1.22 ms/iter at the VGG size): the copy engine
+// sustains more PCIe read bandwidth than SM-issued loads.
+static const float* host_input(okt_comm* c, const float* h, size_t n, cudaStream_t s, int* rc) {
+  if ((*rc = c->ensure(c->hgrad, 4 * std::max<size_t>(n, 1)))) return nullptr;
+  if (n && (*rc = c->ck(cudaMemcpyAsync(c->hgrad.p, h, 4 * n, cudaMemcpyHostToDevice, s), "h2d"))) return nullptr;
+  return c->hgrad.as<float>();
+}
+
 int okt_sparse_allreduce_host(okt_comm* c, const float* h_acc, size_t n, int64_t t, size_t k, uint32_t* h_u_idx,
                               double* h_u_val, uint32_t* h_indexes, size_t u_cap, okt_result* out, void* stream) {
   OKT_COMM_CHECK(c);
   if (!h_acc) return set_err(OKT_ERR_INVALID_ARGUMENT, "null gradient");
   DeviceGuard g(c->device);
   cudaStream_t s = c->pick(stream);
-  int rc = c->ensure(c->hgrad, 4 * std::max<size_t>(n, 1));
+  int rc;
+  const float* gin = host_input(c, h_acc, n, s, &rc);
   if (rc) return rc;
-  if (n && (rc = c->ck(cudaMemcpyAsync(c->hgrad.p, h_acc, 4 * n, cudaMemcpyHostToDevice, s), "h2d"))) return rc;
   okt_result r{};
   if ((rc = c->reserve(n))) return rc;
-  rc = c->step(c->hgrad.as<float>(), nullptr, n, 0.0, t, k, false, &r, s);
+  rc = c->step(gin, nullptr, n, 0.0, t, k, false, &r, s);
   if (rc) return rc;
   if (out) *out = r;
   return copy_result_to_host(c, r, h_u_idx, h_u_val, h_indexes, u_cap, s);
@@ -1648,12 +1665,12 @@ int okt_sgd_step_host(okt_comm* c, const float* h_grad, float* d_w, size_t n, do
   if (!h_grad || !d_w) return set_err(OKT_ERR_INVALID_ARGUMENT, "null argument");
   DeviceGuard g(c->device);
   cudaStream_t s = c->pick(stream);
-  int rc = c->ensure(c->hgrad, 4 * std::max<size_t>(n, 1));
+  int rc;
+  const float* gin = host_input(c, h_grad, n, s, &rc);
   if (rc) return rc;
-  if (n && (rc = c->ck(cudaMemcpyAsync(c->hgrad.p, h_grad, 4 * n, cudaMemcpyHostToDevice, s), "h2d"))) return rc;
   okt_result r{};
   if ((rc = c->reserve(n))) return rc;
-  rc = c->step(c->hgrad.as<float>(), d_w, n, alpha, t, k, true, &r, s);
+  rc = c->step(gin, d_w, n, alpha, t, k, true, &r, s);
   if (rc) return rc;
   if (out) *out = r;
   return copy_result_to_host(c, r, h_u_idx, h_u_val, nullptr, u_cap, s);

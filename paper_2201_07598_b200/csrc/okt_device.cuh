@@ -80,6 +80,25 @@ __device__ __forceinline__ uint32_t rank_in_group(const unsigned (&bal)[kJ][C], 
 }
 
 // CTA-wide sum of one u32 per thread (all threads get the result).
+// This thread's share of sum_{q < n} p[q * step]: U independent (predicated)
+// loads in flight per round, so a CTA sums thousands of counts in about one
+// memory round trip instead of one per loop iteration.
+template <int U = 16>
+__device__ __forceinline__ uint64_t strided_sum(const uint32_t* p, uint32_t n, uint32_t step = 1) {
+  uint64_t acc = 0;
+  for (uint32_t q0 = 0; q0 < n; q0 += U * kThreads) {
+    uint32_t v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t q = q0 + uint32_t(u) * kThreads + threadIdx.x;
+      v[u] = q < n ? p[uint64_t(q) * step] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += v[u];
+  }
+  return acc;
+}
+
 __device__ __forceinline__ uint64_t block_sum(uint64_t v, uint64_t* red) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

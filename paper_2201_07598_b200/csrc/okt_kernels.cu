@@ -73,26 +73,63 @@ size_t stage_entries(uint64_t count, int tile, int max_chunks) {
 // separate apply pass; `indexes` is then u's index array itself.
 constexpr int kCompactBatch = 2;
 
+// A CTA copies a group of consecutive chunks (up to kThreads; one chunk per
+// CTA for the static-chunk producers, a few tiles for K1's per-tile staging):
+// the group's counts are block-scanned first, so the group's first entries
+// can be loaded while the block reduces the global prefix.
+
 template <int MODE, bool APPLY>
 __global__ void __launch_bounds__(kThreads)
     compact_kernel(const uint64_t* __restrict__ s64, const uint32_t* __restrict__ sidx,
                    const double* __restrict__ sval, const uint32_t* __restrict__ counts,
-                   const uint32_t* __restrict__ counts2, uint64_t cap_host, const uint64_t* d_cap,
-                   uint64_t* __restrict__ o64, uint32_t* oidx, double* oval,
+                   const uint32_t* __restrict__ counts2, uint32_t g2, uint32_t G, uint64_t cap_host,
+                   const uint64_t* d_cap, uint64_t* __restrict__ o64, uint32_t* oidx, double* oval,
                    uint64_t* d_total, uint64_t* d_total2, ApplyArgs ap) {
   __shared__ uint64_t red[kWarps];
+  __shared__ uint32_t s_pre[kThreads + 1];
+  __shared__ uint32_t s_wt[kWarps];
   if (APPLY && ap.ind) {
     ap.acc = ap.ind->eps_out;
     ap.w = ap.ind->w;
   }
-
-  const int c = blockIdx.x, G = gridDim.x;
-  const uint64_t cnt = counts[c];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t c0 = uint32_t(split_at(blockIdx.x, G, gridDim.x));
+  const uint32_t c1 = uint32_t(split_at(blockIdx.x + 1, G, gridDim.x));
+  const int nc = int(c1 - c0);
   const uint64_t cap = d_cap ? *d_cap : cap_host;
-  const uint64_t src = uint64_t(c) * cap;
+  // group prefix (block scan) and this thread's share of the global prefix
+  const uint32_t v = tid < nc ? counts[c0 + tid] : 0u;
+  // CTA 0 (c0 = 0, no prefix) sums all G counts instead: the totals
+  const bool first = blockIdx.x == 0;
+  uint64_t pre = strided_sum(counts, first ? G : c0);
+  uint64_t s2 = (first && counts2) ? strided_sum(counts2, g2) : 0;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_wt[warp] = incl;
+  __syncthreads();
+  uint32_t wpre = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) wpre += (w < warp) ? s_wt[w] : 0u;
+  if (tid < nc) s_pre[tid + 1] = wpre + incl;
+  if (tid == 0) s_pre[0] = 0;
+  __syncthreads();
+  const uint64_t cnt = s_pre[nc];
+  auto src_of = [&](uint64_t j) {  // staging position of the group's j-th entry
+    int lo = 0, hi = nc - 1;          // last k with s_pre[k] <= j
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pre[mid] <= j) lo = mid;
+      else hi = mid - 1;
+    }
+    return uint64_t(c0 + lo) * cap + (j - s_pre[lo]);
+  };
   // The first kCompactBatch entries of each thread are loaded (and, for the
-  // fused apply, their model / residual words gathered) before the chunk
-  // prefix is known: only the output positions depend on it.
+  // fused apply, their model words gathered) before the global prefix is
+  // known: only the output positions depend on it.
   constexpr int B = kCompactBatch;
   uint64_t e64[B];
   uint32_t ei[B];
@@ -100,15 +137,16 @@ __global__ void __launch_bounds__(kThreads)
   float wv[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) {
-    const uint64_t j = threadIdx.x + uint64_t(b) * kThreads;
+    const uint64_t j = tid + uint64_t(b) * kThreads;
     e64[b] = 0;
     ei[b] = 0;
     ev[b] = 0.0;
     wv[b] = 0.f;
     if (j < cnt) {
-      if (MODE == 0 || MODE == 1) e64[b] = s64[src + j];
-      if (MODE == 2 || MODE == 3) ei[b] = sidx[src + j];
-      if (MODE == 2) ev[b] = sval[src + j];
+      const uint64_t sj = src_of(j);
+      if (MODE == 0 || MODE == 1) e64[b] = s64[sj];
+      if (MODE == 2 || MODE == 3) ei[b] = sidx[sj];
+      if (MODE == 2) ev[b] = sval[sj];
       if (MODE == 1) {
         ei[b] = coo_idx(e64[b]);
         ev[b] = double(coo_val(e64[b]));
@@ -116,9 +154,15 @@ __global__ void __launch_bounds__(kThreads)
       if (APPLY) wv[b] = ap.w[ei[b]];
     }
   }
-  uint64_t pre = 0;
-  for (int q = threadIdx.x; q < c; q += kThreads) pre += counts[q];
   pre = block_sum(pre, red);
+  if (first) {
+    if (counts2) s2 = block_sum(s2, red);
+    if (tid == 0) {
+      *d_total = pre;
+      if (counts2) *d_total2 = s2;
+    }
+    pre = 0;
+  }
   const bool skip = APPLY && (*ap.d_flags & 1u);  // non-finite step: touch nothing
   bool bad = false;
   auto emit = [&](uint64_t j, uint64_t e, uint32_t i, double v, float w_old) {
@@ -137,47 +181,51 @@ __global__ void __launch_bounds__(kThreads)
   };
 #pragma unroll
   for (int b = 0; b < B; ++b) {
-    const uint64_t j = threadIdx.x + uint64_t(b) * kThreads;
+    const uint64_t j = tid + uint64_t(b) * kThreads;
     if (j < cnt) emit(j, e64[b], ei[b], ev[b], wv[b]);
   }
-  for (uint64_t j = threadIdx.x + uint64_t(B) * kThreads; j < cnt; j += kThreads) {
+  for (uint64_t j = tid + uint64_t(B) * kThreads; j < cnt; j += kThreads) {
+    const uint64_t sj = src_of(j);
     uint64_t e = 0;
     uint32_t i = 0;
     double v = 0.0;
-    if (MODE == 0 || MODE == 1) e = s64[src + j];
+    if (MODE == 0 || MODE == 1) e = s64[sj];
     if (MODE == 1) {
       i = coo_idx(e);
       v = double(coo_val(e));
     }
-    if (MODE == 2 || MODE == 3) i = sidx[src + j];
-    if (MODE == 2) v = sval[src + j];
+    if (MODE == 2 || MODE == 3) i = sidx[sj];
+    if (MODE == 2) v = sval[sj];
     emit(j, e, i, v, APPLY ? ap.w[i] : 0.f);
   }
-  if (APPLY && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(ap.d_flags, 4u);
-  if (c == G - 1) {
-    if (threadIdx.x == 0) *d_total = pre + cnt;
-    if (counts2) {
-      uint64_t s2 = 0;
-      for (int q = threadIdx.x; q < G; q += kThreads) s2 += counts2[q];
-      s2 = block_sum(s2, red);
-      if (threadIdx.x == 0) *d_total2 = s2;
-    }
-  }
+  if (APPLY && __syncthreads_or(bad) && tid == 0) atomicOr(ap.d_flags, 4u);
 }
 
+// G chunks of `cap` entries (cap_host, or *d_cap when set); counts2: g2
+// partial sums (0 = none).
 template <int MODE>
 static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_t cap_host,
-                                  const uint64_t* d_cap, bool with2, uint64_t* o64, uint32_t* oidx,
+                                  const uint64_t* d_cap, uint32_t g2, uint64_t* o64, uint32_t* oidx,
                                   double* oval, uint64_t* d_total, uint64_t* d_total2,
                                   const ApplyArgs* ap = nullptr) {
-  if (ap && (ap->w || ap->ind))
-    compact_kernel<MODE, true><<<G, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts,
-                                                        with2 ? S.counts2 : nullptr, cap_host, d_cap, o64, oidx,
-                                                        oval, d_total, d_total2, *ap);
+  // one chunk per CTA while the grid fits one wave, then groups of up to
+  // kThreads chunks
+  static int cap_a = 0, cap_p = 0;
+  const bool apply = ap && (ap->w || ap->ind);
+  int& cap = apply ? cap_a : cap_p;
+  if (!cap)
+    cap = apply ? resident_ctas(compact_kernel<MODE, true>, kThreads, L.sms)
+                : resident_ctas(compact_kernel<MODE, false>, kThreads, L.sms);
+  const uint32_t slots = uint32_t(std::min(cap, S.max_chunks));
+  const uint32_t per = std::min<uint32_t>(kThreads, std::max<uint32_t>(1, (G + slots - 1) / slots));
+  const uint32_t GB = std::max<uint32_t>(1, (G + per - 1) / per);
+  const uint32_t* c2 = g2 ? S.counts2 : nullptr;
+  if (apply)
+    compact_kernel<MODE, true><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap,
+                                                         o64, oidx, oval, d_total, d_total2, *ap);
   else
-    compact_kernel<MODE, false><<<G, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts,
-                                                         with2 ? S.counts2 : nullptr, cap_host, d_cap, o64, oidx,
-                                                         oval, d_total, d_total2, ApplyArgs{});
+    compact_kernel<MODE, false><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap,
+                                                          o64, oidx, oval, d_total, d_total2, ApplyArgs{});
   ++L.launches;
   return cudaGetLastError();
 }
@@ -186,18 +234,24 @@ static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_
 // K1: fused accumulate / select / compact (phase A)
 // =============================================================================
 template <bool ACCUM, bool SELECT, bool HIST, bool VEC, bool DUAL>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
     k1_kernel(const float* __restrict__ g, const float* eps_in, float* eps_out, float alpha, uint64_t n,
-              uint32_t tiles, uint32_t tpc, const double* __restrict__ d_th,
+              uint32_t tiles, uint32_t* tile_ctr, const double* __restrict__ d_th,
               const double* __restrict__ d_th2, uint64_t* __restrict__ stg, uint32_t* counts,
               uint32_t* counts2, uint32_t* d_flags, uint32_t* d_hist, const StepPtrs* ind, K1P2P p2p) {
   constexpr int C = 4, TILE = kJ * C * kThreads;
-  // P2P mode: the chunk-local staging, its counts and, per chunk, the number
-  // of entries below every cut live in this rank's window; peers read each
-  // chunk's slice for their region in place ([lt[c][r], lt[c][r+1])).
+  // Tiles are handed out dynamically (a ticket counter; the prefetched next
+  // ticket hides its round trip), so every CTA streams until the input is
+  // exhausted instead of a statically assigned range finishing unevenly.
+  // Each tile compacts its selected entries into its own staging slot
+  // [tile * TILE, ...) with its count in counts[tile]: the tile order is the
+  // coordinate order, whichever CTA ran the tile.
+  // P2P mode: the staging, the counts and, per tile, the number of entries
+  // below every cut live in this rank's window; peers read each tile's slice
+  // for their region in place ([lt[t][r], lt[t][r+1])).
   __shared__ uint64_t s_cut[kMaxP];
-  __shared__ uint32_t s_lt[kMaxP], s_below[kMaxP];
-  __shared__ int s_last;
+  __shared__ uint32_t s_below[2][kMaxP];
+  __shared__ uint32_t s_tile[2];
   // (the P2P path always runs the vectorised, single-threshold variants)
   const bool p2p_on = VEC && !DUAL && p2p.tab != nullptr;
   const int lt_P = p2p_on ? p2p.tab->P : 0;
@@ -209,8 +263,8 @@ __global__ void __launch_bounds__(kThreads)
     lt_out = p2p.tab->klt[me][par];
     if (threadIdx.x < lt_P) {
       s_cut[threadIdx.x] = p2p.cuts[threadIdx.x];
-      s_lt[threadIdx.x] = 0xffffffffu;
-      s_below[threadIdx.x] = 0;
+      s_below[0][threadIdx.x] = 0;
+      s_below[1][threadIdx.x] = 0;
     }
   }
   uint64_t* const trace = p2p_on ? p2p.tab->trace : nullptr;
@@ -236,15 +290,16 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
   }
   bool bad = false;
-  uint32_t running = 0, mloc = 0;
-  // balanced split: every chunk gets floor or ceil(tiles / G) tiles (the
-  // staging capacity per chunk stays tpc = ceil(tiles / G) tiles)
-  const uint32_t t0 = split_at32(blockIdx.x, tiles, gridDim.x);
-  const uint32_t t1 = split_at32(blockIdx.x + 1, tiles, gridDim.x);
-  uint64_t* out = stg + uint64_t(blockIdx.x) * tpc * TILE;
-  int parity = 0;
-  for (uint32_t tile = t0; tile < t1; ++tile, parity ^= 1) {
+  uint32_t mloc = 0;
+  if (tid == 0) s_tile[0] = atomicAdd(&tile_ctr[0], 1u);
+  __syncthreads();
+  for (int parity = 0;; parity ^= 1) {
+    const uint32_t tile = s_tile[parity];
+    if (tile >= tiles) break;
+    // next ticket, read after this tile's barrier
+    if (tid == 0) s_tile[parity ^ 1] = atomicAdd(&tile_ctr[0], 1u);
     const uint64_t base = uint64_t(tile) * TILE;
+    uint64_t* out = stg + base;
     float a[kJ][C];
     bool valid[kJ][C];
     if (VEC && base + TILE <= n) {
@@ -330,35 +385,41 @@ __global__ void __launch_bounds__(kThreads)
               for (int c = 0; c < C; ++c)
                 below += (pred[j][c] && base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C + c < cut) ? 1u : 0u;
             below = __reduce_add_sync(0xffffffffu, below);
-            if ((tid & 31) == 0 && below) atomicAdd(&s_below[d], below);
+            if ((tid & 31) == 0 && below) atomicAdd(&s_below[parity][d], below);
           }
         }
       }
       uint32_t grp[kJ];
       const uint32_t total = tile_offsets<C>(tbl[parity], bal, grp);
-      if (cut_mask && tid < lt_P && ((cut_mask >> tid) & 1u)) s_lt[tid] = running + s_below[tid];
+      if (tid == 0) counts[tile] = total;
+      if (tid < lt_P) {
+        // a cut inside the tile: the count below it; else all or nothing
+        lt_out[uint64_t(tile) * kMaxP + tid] =
+            ((cut_mask >> tid) & 1u) ? s_below[parity][tid] : (s_cut[tid] <= base ? 0u : total);
+        s_below[parity][tid] = 0;  // reused two tiles later, after two barriers
+      }
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
 #pragma unroll
         for (int c = 0; c < C; ++c) {
           if (pred[j][c]) {
-            const uint32_t pos = running + grp[j] + rank_in_group<C>(bal, j, c);
+            const uint32_t pos = grp[j] + rank_in_group<C>(bal, j, c);
             const uint64_t e = base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C + c;
             out[pos] = coo_pack(uint32_t(e), a[j][c]);
           }
         }
       }
-      running += total;
+    } else {
+      __syncthreads();  // orders the next-ticket write (SELECT: inside tile_offsets)
     }
   }
-  if (SELECT && tid == 0) counts[blockIdx.x] = running;
-  if (p2p_on) {
-    __syncthreads();
-    if (tid < lt_P) {
-      // no cut inside the chunk: everything or nothing is below it
-      const uint64_t chunk_lo = uint64_t(t0) * TILE;
-      const uint32_t v = s_lt[tid] != 0xffffffffu ? s_lt[tid] : (s_cut[tid] <= chunk_lo ? 0u : running);
-      lt_out[uint64_t(blockIdx.x) * kMaxP + tid] = v;
+  if (tid == 0) {
+    // the last CTA out re-arms the ticket counter for the next launch
+    __threadfence();
+    if (atomicAdd(&tile_ctr[1], 1u) == gridDim.x - 1) {
+      tile_ctr[0] = 0;
+      tile_ctr[1] = 0;
+      __threadfence();
     }
   }
   if (DUAL) {
@@ -375,8 +436,8 @@ __global__ void __launch_bounds__(kThreads)
     // published by the next kernel on the stream (the P2P scatter), once
     // every CTA of this one has finished.
     P2PPub* pub = &p2p.tab->hdr[p2p.tab->rank]->pub[p2p.sp->par];
-    pub->k1_G = gridDim.x;
-    pub->k1_cap = tpc * TILE;
+    pub->k1_G = tiles;  // chunk = tile
+    pub->k1_cap = TILE;
   }
   if (trace && (tid & 31) == 0) trace_stamp(trace, kTrK1, 2);
 }
@@ -393,26 +454,26 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
   static int cap_v = 0, cap_s = 0;
   int& cap = vec ? cap_v : cap_s;
   if (!cap) cap = resident_ctas(kern, kThreads, L.sms);
-  const uint32_t G = chunks_for(tiles, cap, S.max_chunks);
-  if (uint64_t(tiles) * G > 0xffffffffull) return cudaErrorInvalidValue;  // split_at32's range
-  const uint32_t tpc = uint32_t((tiles + G - 1) / G);
+  const uint32_t G = chunks_for(tiles, cap, S.max_chunks);  // persistent CTAs
+  if (tiles > S.max_tiles) return cudaErrorInvalidValue;         // counts / staging capacity
   // Profiling events: inside a stream capture they must be external event
   // nodes (re-recorded at every graph launch); outside, plain records.
   cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
   if (L.k1_event) cudaStreamIsCapturing(L.s, &cap_st);
   const unsigned ev_flags = cap_st == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, ev_flags);
-  kern<<<G, kThreads, 0, L.s>>>(g, eps_in, eps_out, alpha, n, uint32_t(tiles), tpc, d_th, d_th2, S.s64, S.counts,
-                                S.counts2, d_flags, d_hist, ind, p2p ? *p2p : K1P2P{});
+  kern<<<G, kThreads, 0, L.s>>>(g, eps_in, eps_out, alpha, n, uint32_t(tiles), S.tile_ctr, d_th, d_th2, S.s64,
+                                S.counts, S.counts2, d_flags, d_hist, ind, p2p ? *p2p : K1P2P{});
   if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, ev_flags);
   ++L.launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !SELECT) return e;
-  const uint64_t chunk_cap = uint64_t(tpc) * TILE;
-  if (p2p) return cudaSuccess;  // peers consume the chunked staging in place
+  if (p2p) return cudaSuccess;  // peers consume the per-tile staging in place
+  // chunks = tiles; counts2 holds one partial sum per K1 CTA
   if (out.aos)
-    return launch_compact<0>(L, S, G, chunk_cap, nullptr, DUAL, out.aos, nullptr, nullptr, d_m, d_m2);
-  return launch_compact<1>(L, S, G, chunk_cap, nullptr, DUAL, nullptr, out.idx, out.val, d_m, d_m2, ap);
+    return launch_compact<0>(L, S, uint32_t(tiles), TILE, nullptr, DUAL ? G : 0, out.aos, nullptr, nullptr, d_m, d_m2);
+  return launch_compact<1>(L, S, uint32_t(tiles), TILE, nullptr, DUAL ? G : 0, nullptr, out.idx, out.val, d_m, d_m2,
+                           ap);
 }
 
 cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, const float* eps_in,
@@ -518,7 +579,7 @@ cudaError_t launch_filter(Launch& L, const Stage& S, bool aos, const uint64_t* i
   ++L.launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_compact<2>(L, S, G, 0, S.chunk_cap, false, nullptr, out_idx, out_val, d_cnt_out, nullptr, ap);
+  return launch_compact<2>(L, S, G, 0, S.chunk_cap, 0, nullptr, out_idx, out_val, d_cnt_out, nullptr, ap);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -597,7 +658,7 @@ cudaError_t launch_apply(Launch& L, const Stage& S, const uint32_t* u_idx, const
   ++L.launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_compact<3>(L, S, G, 0, S.chunk_cap, false, nullptr, out_indexes, nullptr, d_nidx, nullptr);
+  return launch_compact<3>(L, S, G, 0, S.chunk_cap, 0, nullptr, out_indexes, nullptr, d_nidx, nullptr);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -645,7 +706,7 @@ cudaError_t launch_select_flags(Launch& L, const Stage& S, const uint8_t* sel, c
   ++L.launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_compact<3>(L, S, G, 0, S.chunk_cap, false, nullptr, out, nullptr, d_count, nullptr);
+  return launch_compact<3>(L, S, G, 0, S.chunk_cap, 0, nullptr, out, nullptr, d_count, nullptr);
 }
 
 // =============================================================================
@@ -774,25 +835,32 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t t1 = split_at32(blockIdx.x + 1, tiles, gridDim.x);
   const uint64_t obase = uint64_t(blockIdx.x) * tpc * kRegionTile;
   uint32_t running = 0;
+  auto load_mask = [&](uint32_t tile, uint32_t (&m)[8]) {
+    const uint64_t w = uint64_t(tile) * (kRegionTile / 4) + uint64_t(tid) * 8;
+    if (w + 8 <= nwords) {
+      const uint4 a = *reinterpret_cast<const uint4*>(mask + w);
+      const uint4 b = *reinterpret_cast<const uint4*>(mask + w + 4);
+      m[0] = a.x; m[1] = a.y; m[2] = a.z; m[3] = a.w;
+      m[4] = b.x; m[5] = b.y; m[6] = b.z; m[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) m[j] = (w + j < nwords) ? mask[w + j] : 0u;
+    }
+  };
+  uint32_t nx[8];  // the next tile's mask words, loaded one tile ahead
+  if (t0 < t1) load_mask(t0, nx);
   int parity = 0;
   for (uint32_t tile = t0; tile < t1; ++tile, parity ^= 1) {
     const uint64_t w0 = uint64_t(tile) * (kRegionTile / 4) + uint64_t(tid) * 8;  // first mask word
     uint32_t mw[8];
-    if (w0 + 8 <= nwords) {
-      const uint4 a = *reinterpret_cast<const uint4*>(mask + w0);
-      const uint4 b = *reinterpret_cast<const uint4*>(mask + w0 + 4);
-      mw[0] = a.x; mw[1] = a.y; mw[2] = a.z; mw[3] = a.w;
-      mw[4] = b.x; mw[5] = b.y; mw[6] = b.z; mw[7] = b.w;
-    } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) mw[j] = (w0 + j < nwords) ? mask[w0 + j] : 0u;
-    }
+    for (int j = 0; j < 8; ++j) mw[j] = nx[j];
+    if (tile + 1 < t1) load_mask(tile + 1, nx);
+    // bit c of nibble j: byte c of word j non-zero (some source present)
     uint32_t present = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if ((mw[j] >> (8 * c)) & 0xffu) present |= 1u << (j * 4 + c);
+      present |= (((__vcmpne4(mw[j], 0u) & 0x01010101u) * 0x01020408u) >> 24) << (4 * j);
     const uint64_t c0 = w0 * 4;  // first coordinate (region-relative)
     auto bits_of = [&](int k) {  // select tree: keeps mw[] in registers
       const int j = k >> 2;
@@ -908,7 +976,7 @@ static cudaError_t region_scan_dispatch(Launch& L, const Stage& S, uint64_t lo, 
   ++L.launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || p2p) return e;  // P2P: peers read the chunks in place
-  return launch_compact<2>(L, S, G, uint64_t(tpc) * TILE, nullptr, false, nullptr, out_idx, out_val, d_count,
+  return launch_compact<2>(L, S, G, uint64_t(tpc) * TILE, nullptr, 0, nullptr, out_idx, out_val, d_count,
                            nullptr);
 }
 

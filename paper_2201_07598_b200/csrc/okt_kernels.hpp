@@ -37,7 +37,9 @@ struct Stage {
   uint32_t* counts = nullptr;   // per-chunk emitted counts
   uint32_t* counts2 = nullptr;  // per-chunk secondary counts (K1 dual threshold)
   uint64_t* chunk_cap = nullptr;  // device-computed chunk capacity (entries)
+  uint32_t* tile_ctr = nullptr;   // K1 tile tickets [next, CTAs done]; zero between launches
   int max_chunks = 0;
+  uint64_t max_tiles = 0;         // counts[] capacity for K1's per-tile counts
 };
 // Staging entries needed for a pass over `count` elements in tiles of `tile`.
 size_t stage_entries(uint64_t count, int tile, int max_chunks);

@@ -23,10 +23,9 @@ namespace {
 constexpr uint32_t kAbortBits = 1u | 8u | 16u;  // local non-finite, peer timeout, peer failure
 }
 
-// K3 (M1) fused with the split exchange.  Work items are (source, chunk,
-// part): only the K1 chunks whose coordinates overlap my region carry entries
-// for me, and each is split into `parts` so every warp of the grid gets a
-// share.  A warp reads its part of the chunk's slice for my region,
+// K3 (M1) fused with the split exchange.  Work items are (source, tile,
+// part): only the K1 tiles overlapping my region carry entries for me, and
+// each is split into `parts` when there are more warps than tiles.  A warp reads its part of the chunk's slice for my region,
 // [lt[c][me], lt[c][me+1]), straight out of the source's HBM (NVLink for a
 // peer) and scatters it into the presence mask / coordinate-major staging.
 // My own chunks need no hand-off, so they are scattered first, while the
@@ -42,8 +41,7 @@ __global__ void __launch_bounds__(kThreads)
   const int P = tab->P, me = tab->rank, q = threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t* const trace = tab->trace;
-  const P2PPub* my_pub = &tab->hdr[me]->pub[par];
-  const uint32_t G = my_pub->k1_G, cap = my_pub->k1_cap;  // same geometry on every rank (same n)
+  const uint32_t G = k1_tiles, cap = kK1Tile;  // same geometry on every rank (same n)
   if (q == 0) {
     s_abort = (*d_flags & 1u) ? 1 : 0;
     trace_stamp(trace, kTrScatter, 0);
@@ -56,15 +54,11 @@ __global__ void __launch_bounds__(kThreads)
     __threadfence_system();
     for (int r = 0; r < P; ++r) st_relaxed_sys(&tab->hdr[r]->flag[kFlagLReady][me], epoch);
   }
-  // Chunks overlapping [lo, lo + W): chunk c holds tiles
-  // [c * tiles / G, (c + 1) * tiles / G) (k1_kernel's balanced split).
-  constexpr uint64_t T = kK1Tile;
+  // K1 chunks are its tiles: the ones overlapping [lo, lo + W).
   uint32_t c_lo = 0, nch = 0;
   if (W > 0 && G > 0) {
-    const uint64_t tl = lo / T, th = (lo + W - 1) / T;
-    c_lo = uint32_t(((tl + 1) * G + k1_tiles - 1) / k1_tiles - 1);
-    const uint32_t c_hi = uint32_t(((th + 1) * G + k1_tiles - 1) / k1_tiles - 1);
-    nch = c_hi - c_lo + 1;
+    c_lo = uint32_t(lo / kK1Tile);
+    nch = uint32_t((lo + W - 1) / kK1Tile) - c_lo + 1;
   }
   const uint32_t warps_total = gridDim.x * kWarps;
   const uint32_t parts = max(1u, min(8u, warps_total / max(1u, uint32_t(P) * nch)));
@@ -269,7 +263,7 @@ __global__ void __launch_bounds__(kThreads)
     const uint32_t* cnt = tab->kcnt[me][par];
     const uint32_t* klt = tab->klt[me][par];
     uint64_t o = 0;
-    for (uint32_t c = threadIdx.x; c < G; c += kThreads) o += (d == P) ? cnt[c] : klt[uint64_t(c) * kP2PMaxP + d];
+    o = (d == P) ? strided_sum(cnt, G) : strided_sum(klt + d, G, kP2PMaxP);
     __shared__ uint64_t red[kWarps];
     o = block_sum(o, red);
     if (threadIdx.x == 0) {
