@@ -1,9 +1,9 @@
 """GPU parity of the host-buffer entry points (okt_sgd_step_host,
 okt_sparse_allreduce_host) — the reference's calling convention: the dense
 gradient lives in host memory (oktopk.hpp:118-120 takes a DenseGrad by
-reference).  A pinned gradient is read by K1 in place over PCIe; a pageable
-one goes through the staging copy; both must give the oracle's trajectory bit
-for bit (exact-sum integer inputs, as in test_sgd_trajectory_exact_sum).
+reference).  Pinned and pageable host gradients must both give the oracle's
+trajectory bit for bit (exact-sum integer inputs, as in
+test_sgd_trajectory_exact_sum).
 """
 import ctypes
 
