@@ -67,7 +67,7 @@ def dump_p2p_trace(L, comm, rank, outdir):
     """Per-kernel spans of the last P2P step from the CTAs' %globaltimer stamps
     (okt_debug_p2p_trace), relative to the first K1 CTA start."""
     import numpy as np
-    kinds, ctas = 5, 2048
+    kinds, ctas = 7, 2048
     buf = (ctypes.c_uint64 * (kinds * ctas * 4))()
     if L.okt_debug_p2p_trace(comm, buf, kinds * ctas * 4):
         return
@@ -75,7 +75,7 @@ def dump_p2p_trace(L, comm, rank, outdir):
     used = a[:, :, 0] > 0
     t0 = a[0, :, 0][used[0]].min() if used[0].any() else 0
     out = {}
-    for k, nm in enumerate(["k1", "scatter", "region_scan", "pull0", "pull1"]):
+    for k, nm in enumerate(["k1", "merge", "unused", "pull0", "pull1", "publish_l", "publish_sur"]):
         u = used[k]
         if not u.any():
             continue
@@ -107,6 +107,8 @@ def workload(args, P):
             "tau": args.tau, "tau_prime": args.tau_prime, "bucket": args.bucket,
             "inputs": f"drifting_gradient_process(t, seed=1, rank_key=r+1), ring of {args.ring} snapshots",
             "parallelism": f"dp{P} (one process per GPU, NCCL/NVLink)" if P > 1 else "single GPU",
+            "rank_alignment": "device barrier (okt_device_barrier, NVLink flags) before each timed step, "
+                              "outside the events" if P > 1 else None,
             "l2": "not flushed (diagnostic run)" if args.no_l2_flush else
             "flushed before every timed step, outside the events: 256 MiB write, then a 256 MiB read sweep "
             "(clean L2: no write-back of the flush buffer inside the step)"}
@@ -345,6 +347,11 @@ def run_okt(args):
         t += 1
         with torch.cuda.stream(stream):
             flush.fill_(i & 0xff)  # evict L2 between timed steps (outside the events)
+        if world > 1:
+            # align the ranks' GPUs (device barrier over NVLink, outside the
+            # events): the step is timed without the host loop's launch skew
+            L.okt_device_barrier(comm, ctypes.c_void_p(stream.cuda_stream))
+        with torch.cuda.stream(stream):
             ev[i][0].record(stream)
         step_async(t)
         with torch.cuda.stream(stream):

@@ -187,6 +187,11 @@ int okt_sgd_step_async(okt_comm* comm, const float* d_grad, float* d_w,
                        size_t n, double alpha, int64_t t, size_t k,
                        void* stream);
 int okt_step_wait(okt_comm* comm, okt_result* out);
+/* Device-side barrier of all ranks, enqueued on `stream` (NULL = the comm's
+ * stream): work enqueued after it starts on every GPU within one NVLink flag
+ * latency of the others (collective; the host does not wait).  Without a
+ * peer-mapped world it is a host barrier. */
+int okt_device_barrier(okt_comm* comm, void* stream);
 
 /* Host-buffer forms of the two hot entry points: the reference's own calling
  * convention (DenseGrad in, SparseGrad out, both in host memory).  The
@@ -279,8 +284,8 @@ int okt_reset_phase_times(okt_comm* comm);
 /* Number of kernels this comm has launched since creation. */
 int okt_kernel_launches(const okt_comm* comm, uint64_t* out);
 /* Diagnostics: per-CTA %globaltimer stamps (ns) of the last device-driven
- * (NVLink P2P) step, [5 kernels: K1, scatter, region scan, pull 0, pull 1]
- * x [2048 CTAs] x [start, after waits, end, 0].  Recorded only when the comm
+ * (NVLink P2P) step, [7 kinds: K1, merge, (unused), pull 0, pull 1, L publish,
+ * survivor publish] x [2048 CTAs] x [start, after waits, end, 0].  Recorded only when the comm
  * was set up with OKT_P2P_TRACE in the environment (else OKT_ERR_CONFIG). */
 int okt_debug_p2p_trace(okt_comm* comm, uint64_t* out, size_t n_words);
 

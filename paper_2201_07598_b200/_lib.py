@@ -28,7 +28,7 @@ EXPORTS = (
     "okt_get_state", "okt_set_state", "okt_set_params", "okt_ledger",
     "okt_ledger_reset", "okt_sparse_allreduce", "okt_residual_reset",
     "okt_residual", "okt_sgd_step", "okt_sparse_allreduce_host",
-    "okt_sparse_allreduce_async", "okt_sgd_step_async", "okt_step_wait",
+    "okt_sparse_allreduce_async", "okt_sgd_step_async", "okt_step_wait", "okt_device_barrier",
     "okt_sgd_step_host", "okt_memcpy_h2d", "okt_memcpy_d2h",
     "okt_th_re_evaluate_dense", "okt_th_re_evaluate_sparse",
     "okt_select_by_threshold", "okt_space_repartition",
@@ -111,6 +111,7 @@ def lib() -> ctypes.CDLL:
         "okt_sgd_step_async": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_double, c_int64, c_size_t,
                                        c_void_p]),
         "okt_step_wait": (c_int, [c_void_p, P(OktResult)]),
+        "okt_device_barrier": (c_int, [c_void_p, c_void_p]),
         "okt_residual_reset": (c_int, [c_void_p, c_size_t, c_void_p, c_void_p]),
         "okt_residual": (c_int, [c_void_p, P(c_void_p), P(c_size_t)]),
         "okt_sgd_step": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_double, c_int64,

@@ -125,14 +125,15 @@ okt_state default_state() {
 
 // Symmetric P2P window layout (identical on every rank for a given n): per
 // parity, K1's per-tile staging + tile counts + per-tile cut counts, the
-// region scan's chunked survivors + counts + chunk prefix, and u.
+// merge kernel's per-tile survivor chunks + counts + chunk prefix, and u.
 struct WinLayout {
   size_t kstg[2], kcnt[2], klt[2], sidx[2], sval[2], scnt[2], spre[2], uidx[2], uval[2], bytes;
 };
 WinLayout win_layout(size_t n, int max_chunks) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t kst = okt::stage_entries(n, okt::kK1Tile, max_chunks);
-  const size_t sst = okt::stage_entries(n, okt::kRegionTileHost, max_chunks);
+  // survivor chunks: one per K1 tile overlapping the region (capacity kK1Tile)
+  const size_t sst = (n + 2 * size_t(okt::kK1Tile) - 1) / okt::kK1Tile * okt::kK1Tile + okt::kK1Tile;
   const size_t mc = size_t(max_chunks);
   const size_t kt = std::max(mc, (n + okt::kK1Tile - 1) / okt::kK1Tile);  // K1 counts are per tile
   WinLayout w;
@@ -143,8 +144,8 @@ WinLayout win_layout(size_t n, int max_chunks) {
     w.klt[p] = o; o += al(4 * okt::kP2PMaxP * kt);
     w.sidx[p] = o; o += al(4 * sst);
     w.sval[p] = o; o += al(8 * sst);
-    w.scnt[p] = o; o += al(4 * mc);
-    w.spre[p] = o; o += al(8 * (mc + 1));
+    w.scnt[p] = o; o += al(4 * (kt + 2));  // one survivor chunk per K1 tile of the region
+    w.spre[p] = o; o += al(8 * (kt + 3));
     w.uidx[p] = o; o += al(4 * n);
     w.uval[p] = o; o += al(8 * n);
   }
@@ -175,6 +176,9 @@ struct okt_comm {
   std::unique_ptr<okt::Transport> tr;
   cudaStream_t own = nullptr;
   cudaEvent_t ready_ev = nullptr;
+  // side branch of the P2P step (K1's totals, off the critical path)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   Launch L;
   okt_state st = default_state();
   bool dev_stale = true;  // device thresholds / cuts must be re-uploaded
@@ -205,6 +209,7 @@ struct okt_comm {
   okt::PeerTab tab{};
   std::vector<void*> ipc_open;
   uint64_t p2p_epoch = 0;
+  uint64_t bar_epoch = 0;  // okt_device_barrier calls (same count on every rank)
   // CUDA graph of the steady single-rank step (step block H2D, K1, fused
   // compaction + apply, scalar readback); per-step pointers are read from the
   // step block (DevScalars::sp) on the device.
@@ -751,14 +756,19 @@ struct okt_comm {
                              hup->sp.eps_in, hup->sp.eps_out, hup->sp.alpha, n, &d()->local_th, nullptr,
                              okt::OutCoo{}, &d()->m, nullptr, &d()->flags, nullptr, nullptr, &kp, sp),
               "k1");
+    // K1's totals (selection size, slice offsets) on a side branch
+    okt::K1Totals kt;
+    kt.d_m = &d()->m;
+    kt.d_off = d()->off;
+    if (!rc) rc = ck(cudaEventRecord(ev_fork, s), "fork");
+    if (!rc) rc = ck(cudaStreamWaitEvent(side, ev_fork, 0), "fork");
+    if (!rc) rc = ck(okt::launch_p2p_totals(L, side, dt, sp, P, kt), "totals");
+    if (!rc) rc = ck(cudaEventRecord(ev_join, side), "join");
     tmark(OKT_T_MERGE, s);
-    if (!rc) rc = ck(okt::launch_p2p_scatter(L, dt, sp, dp, lo, W, n, mask.as<uint32_t>(), stage.as<float>(),
-                                             &d()->flags, kP2PTimeoutNs), "p2p");
-    okt::RSP2P rp;
-    rp.tab = dt;
-    rp.sp = sp;
-    if (!rc) rc = ck(okt::launch_region_scan(L, S, P, true, lo, W, mask.as<uint32_t>(), stage.as<float>(),
-                                             &d()->global_th, nullptr, nullptr, &d()->S, &rp), "region_scan");
+    // split exchange + region merge in one kernel (reads every source's K1
+    // tiles of my region in place)
+    if (!rc) rc = ck(okt::launch_p2p_merge(L, dt, sp, dp, P, lo, W, n, &d()->global_th, &d()->flags, kP2PTimeoutNs),
+                     "p2p");
     tmark(OKT_T_ALLGATHER, s);
     okt::P2PApply pa;
     pa.on = 1;
@@ -767,10 +777,7 @@ struct okt_comm {
     // oktopk_sgd_step reports no index list (trainer.hpp:123-127): only the
     // plain allreduce needs the sel flags and the indexes compaction.
     pa.sel = sgd ? nullptr : selflags.as<uint8_t>();
-    okt::K1Totals kt;
-    kt.d_m = &d()->m;
-    kt.d_off = d()->off;
-    if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, sp, &d()->S, dp, &d()->U, &d()->flags, kP2PTimeoutNs, pa, kt),
+    if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, sp, &d()->S, dp, &d()->U, &d()->flags, kP2PTimeoutNs, pa),
                      "p2p");
     if (!sgd) {
       tmark(OKT_T_APPLY, s);
@@ -778,6 +785,7 @@ struct okt_comm {
                                                 indexes.as<uint32_t>(), &d()->nidx, &d()->flags), "indexes");
     }
     tstop(s);
+    if (!rc) rc = ck(cudaStreamWaitEvent(s, ev_join, 0), "join");
     if (!rc) rc = ck(cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s), "d2h");
     return rc;
   }
@@ -1309,7 +1317,10 @@ int init_comm(okt_comm* c) {
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
   c->L.sms = dev_sms;
   if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ready_ev, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ready_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     return set_err(OKT_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(cudaGetLastError()));
   }
   c->L.s = c->own;
@@ -1457,6 +1468,9 @@ int okt_comm_destroy(okt_comm* c) {
   c->tr.reset();
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->ready_ev) cudaEventDestroy(c->ready_ev);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->h) cudaFreeHost(c->h);
   if (c->hup) cudaFreeHost(c->hup);
   if (c->graph1.exec) cudaGraphExecDestroy(c->graph1.exec);
@@ -1574,6 +1588,23 @@ int okt_sgd_step_async(okt_comm* c, const float* d_grad, float* d_w, size_t n, d
   c->defer = false;
   c->has_sync_result = rc == OKT_OK && !c->pending.on;
   return rc;
+}
+
+int okt_device_barrier(okt_comm* c, void* stream) {
+  OKT_COMM_CHECK(c);
+  DeviceGuard g(c->device);
+  int rc;
+  if ((rc = c->wait_pending(nullptr))) return rc;
+  cudaStream_t s = c->pick(stream);
+  if (c->P == 1) return OKT_OK;
+  if (c->p2p) {
+    c->L.s = s;
+    return c->ck(okt::launch_p2p_barrier(c->L, c->tabd.as<okt::PeerTab>(), ++c->bar_epoch, &c->d()->flags,
+                                         kP2PTimeoutNs), "barrier");
+  }
+  int one = 1;
+  std::vector<int> all(c->P);
+  return c->allgather_host(&one, all.data(), sizeof(int), s);
 }
 
 int okt_step_wait(okt_comm* c, okt_result* out) {

@@ -128,4 +128,28 @@ __device__ __forceinline__ float coo_val(uint64_t e) {
   return __uint_as_float(uint32_t(e >> 32));
 }
 
+// The reference's stride-doubling bracket sum (oktopk.cpp sparse_sum over
+// the P sources of one coordinate; absent sources leave their bracket slot
+// empty) in fp64 over values already in registers; bit r of `bits`: source r
+// present.
+template <int P>
+__device__ __forceinline__ double bracket_regs(const float (&v)[P], uint32_t bits) {
+  double a[P];
+  bool h[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) {
+    h[q] = (bits >> q) & 1u;
+    a[q] = h[q] ? double(v[q]) : 0.0;
+  }
+#pragma unroll
+  for (int s = P >> 1; s >= 1; s >>= 1) {
+#pragma unroll
+    for (int q = 0; q < s; ++q) {
+      if (h[q] && h[q + s]) a[q] = a[q] + a[q + s];
+      else if (h[q + s]) a[q] = a[q + s];
+      h[q] = h[q] || h[q + s];
+    }
+  }
+  return a[0];
+}
 }  // namespace okt

@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
   // (the P2P path always runs the vectorised, single-threshold variants)
   const bool p2p_on = VEC && !DUAL && p2p.tab != nullptr;
   const int lt_P = p2p_on ? p2p.tab->P : 0;
+  const int me_rank = p2p_on ? p2p.tab->rank : 0;
   uint32_t* lt_out = nullptr;
   if (p2p_on) {
     const int me = p2p.tab->rank, par = p2p.sp->par;
@@ -413,15 +414,6 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
       __syncthreads();  // orders the next-ticket write (SELECT: inside tile_offsets)
     }
   }
-  if (tid == 0) {
-    // the last CTA out re-arms the ticket counter for the next launch
-    __threadfence();
-    if (atomicAdd(&tile_ctr[1], 1u) == gridDim.x - 1) {
-      tile_ctr[0] = 0;
-      tile_ctr[1] = 0;
-      __threadfence();
-    }
-  }
   if (DUAL) {
     const uint64_t s = block_sum(mloc, red);
     if (tid == 0) counts2[blockIdx.x] = uint32_t(s);
@@ -431,11 +423,21 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
     for (int i = tid; i < 2048; i += kThreads)
       if (s_hist[i]) atomicAdd(&d_hist[i], s_hist[i]);
   }
+  if (tid == 0) {
+    // the last CTA out re-arms the ticket counter for the next launch
+    __threadfence();
+    if (atomicAdd(&tile_ctr[1], 1u) == gridDim.x - 1) {
+      tile_ctr[0] = 0;
+      tile_ctr[1] = 0;
+      __threadfence();
+    }
+  }
   if (p2p_on && blockIdx.x == 0 && tid == 0) {
     // Chunk geometry for the peers; the status and the L-ready flags are
-    // published by the next kernel on the stream (the P2P scatter), once
-    // every CTA of this one has finished.
-    P2PPub* pub = &p2p.tab->hdr[p2p.tab->rank]->pub[p2p.sp->par];
+    // published by the next kernel on the stream (the P2P scatter) once every
+    // CTA of this one has finished: a system fence issued here, while the grid
+    // still streams, would wait for that traffic to drain (tools/fence_lat.cu).
+    P2PPub* pub = &p2p.tab->hdr[me_rank]->pub[p2p.sp->par];
     pub->k1_G = tiles;  // chunk = tile
     pub->k1_cap = TILE;
   }
@@ -783,27 +785,6 @@ __device__ __forceinline__ void load_slots(const float* __restrict__ st, float (
     }
   }
 }
-// bracket_sum over values already in registers.
-template <int P>
-__device__ __forceinline__ double bracket_regs(const float (&v)[P], uint32_t bits) {
-  double a[P];
-  bool h[P];
-#pragma unroll
-  for (int q = 0; q < P; ++q) {
-    h[q] = (bits >> q) & 1u;
-    a[q] = h[q] ? double(v[q]) : 0.0;
-  }
-#pragma unroll
-  for (int s = P >> 1; s >= 1; s >>= 1) {
-#pragma unroll
-    for (int q = 0; q < s; ++q) {
-      if (h[q] && h[q + s]) a[q] = a[q] + a[q + s];
-      else if (h[q + s]) a[q] = a[q + s];
-      h[q] = h[q] || h[q + s];
-    }
-  }
-  return a[0];
-}
 constexpr int kGather = 4;
 
 // Thread-contiguous layout: thread t of a tile owns coordinates
@@ -819,16 +800,9 @@ template <int P, bool FILTER>
 __global__ void __launch_bounds__(kThreads, 2)
     region_scan_kernel(uint64_t lo, uint64_t W, uint32_t tiles, uint32_t tpc, uint32_t* mask,
                        const float* __restrict__ stage, const double* d_gth, uint32_t* sidx, double* sval,
-                       uint32_t* counts, RSP2P p2p) {
+                       uint32_t* counts) {
   __shared__ uint32_t wtot[2][kWarps];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (p2p.tab) {  // P2P: the survivors' chunks live in this rank's window
-    const int me = p2p.tab->rank, par = p2p.sp->par;
-    sidx = p2p.tab->sidx[me][par];
-    sval = p2p.tab->sval[me][par];
-    counts = p2p.tab->scnt[me][par];
-    if (FILTER && tid == 0) trace_stamp(p2p.tab->trace, kTrRegion, 0);
-  }
   const double gth = FILTER ? *d_gth : 0.0;
   const uint64_t nwords = (W + 3) / 4;
   const uint32_t t0 = split_at32(blockIdx.x, tiles, gridDim.x);
@@ -913,7 +887,6 @@ __global__ void __launch_bounds__(kThreads, 2)
           if (w0 + j < nwords) mask[w0 + j] = 0u;
       }
     }
-    if (FILTER && p2p.tab && lane == 0) trace_stamp(p2p.tab->trace, kTrRegion, 1, true);
     // CTA exclusive scan of the per-thread counts.
     const uint32_t cnt = __popc(sel);
     uint32_t incl = cnt;
@@ -931,7 +904,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       wpre += (w < warp) ? x : 0u;
       total += x;
     }
-    if (FILTER && p2p.tab && lane == 0) trace_stamp(p2p.tab->trace, kTrRegion, 3, true);
     uint64_t pos = obase + running + wpre + incl - cnt;
     for (uint32_t rest = sel; rest; rest &= rest - 1, ++pos) {
       const int k = __ffs(rest) - 1;
@@ -950,20 +922,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     running += total;
   }
   if (tid == 0) counts[blockIdx.x] = running;
-  if (p2p.tab && blockIdx.x == 0 && tid == 0) {
-    // Chunk geometry for the peers; the chunk prefix, S and the flags are
-    // published by the next kernel on the stream (the P2P pull).
-    P2PPub* pub = &p2p.tab->hdr[p2p.tab->rank]->pub[p2p.sp->par];
-    pub->sur_G = gridDim.x;
-    pub->sur_cap = tpc * kRegionTile;
-  }
-  if (FILTER && p2p.tab && lane == 0) trace_stamp(p2p.tab->trace, kTrRegion, 2);
 }
 
 template <int P, bool FILTER>
 static cudaError_t region_scan_dispatch(Launch& L, const Stage& S, uint64_t lo, uint64_t W, uint32_t* mask,
                                         const float* stage, const double* d_gth, uint32_t* out_idx,
-                                        double* out_val, uint64_t* d_count, const RSP2P* p2p) {
+                                        double* out_val, uint64_t* d_count) {
   constexpr int TILE = kRegionTile;
   const uint64_t tiles = (W + TILE - 1) / TILE;
   static int cap = 0;
@@ -972,20 +936,20 @@ static cudaError_t region_scan_dispatch(Launch& L, const Stage& S, uint64_t lo, 
   if (uint64_t(tiles) * G > 0xffffffffull) return cudaErrorInvalidValue;  // split_at32's range
   const uint32_t tpc = uint32_t(std::max<uint64_t>((tiles + G - 1) / G, 1));
   region_scan_kernel<P, FILTER><<<G, kThreads, 0, L.s>>>(lo, W, uint32_t(tiles), tpc, mask, stage, d_gth, S.sidx,
-                                                         S.sval, S.counts, p2p ? *p2p : RSP2P{});
+                                                         S.sval, S.counts);
   ++L.launches;
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || p2p) return e;  // P2P: peers read the chunks in place
+  if (e != cudaSuccess) return e;
   return launch_compact<2>(L, S, G, uint64_t(tpc) * TILE, nullptr, 0, nullptr, out_idx, out_val, d_count,
                            nullptr);
 }
 
 cudaError_t launch_region_scan(Launch& L, const Stage& S, int P, bool filter, uint64_t lo, uint64_t W,
                                uint32_t* mask, const float* stage, const double* d_gth, uint32_t* out_idx,
-                               double* out_val, uint64_t* d_count, const RSP2P* pub) {
+                               double* out_val, uint64_t* d_count) {
 #define OKT_RS(PP)                                                                                          \
-  return filter ? region_scan_dispatch<PP, true>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count, pub) \
-                : region_scan_dispatch<PP, false>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count, pub)
+  return filter ? region_scan_dispatch<PP, true>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count) \
+                : region_scan_dispatch<PP, false>(L, S, lo, W, mask, stage, d_gth, out_idx, out_val, d_count)
   switch (P) {
     case 1: OKT_RS(1);
     case 2: OKT_RS(2);

@@ -119,8 +119,7 @@ cudaError_t launch_scatter(Launch& L, const Segs& segs, uint64_t lo, uint64_t W,
 // fp64, keep explicit zeros, optionally filter by |sum| >= *d_gth, clear mask.
 cudaError_t launch_region_scan(Launch& L, const Stage& S, int P, bool filter, uint64_t lo, uint64_t W,
                                uint32_t* mask, const float* stage, const double* d_gth,
-                               uint32_t* out_idx, double* out_val, uint64_t* d_count,
-                               const RSP2P* p2p = nullptr);
+                               uint32_t* out_idx, double* out_val, uint64_t* d_count);
 
 // Small control kernels.
 cudaError_t launch_slice_offsets(Launch& L, const uint64_t* coo, const uint64_t* d_m,
@@ -143,14 +142,20 @@ cudaError_t launch_scatter_heavy(Launch& L, const uint32_t* pos, const float* va
                                  uint64_t count, float* out);
 
 // ---- device-driven multi-GPU exchange (okt_p2p.cu) ----------------------------
-// Waits for every peer's L, then scatters my slices read out of their HBM.
-cudaError_t launch_p2p_scatter(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
-                               uint64_t W, uint64_t n, uint32_t* mask, float* stage, uint32_t* d_flags,
-                               uint64_t timeout_ns);
+// Split exchange + region merge of the steady P2P step (K1's per-tile staging
+// of every source read in place; survivors chunked into my window).
+cudaError_t launch_p2p_merge(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, int P, uint64_t lo,
+                             uint64_t W, uint64_t n, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns);
 // Waits for every rank's survivors, plans (offsets / balance), pulls u.
-cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, const uint64_t* d_S,
+cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, uint64_t* d_S,
                                   P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns,
-                                  const P2PApply& ap, const K1Totals& totals);
+                                  const P2PApply& ap);
+// Device barrier over the peer flags (okt_device_barrier).
+cudaError_t launch_p2p_barrier(Launch& L, const PeerTab* d_tab, uint64_t epoch, uint32_t* d_flags,
+                               uint64_t timeout_ns);
+// This rank's selection size / slice offsets from K1's tile counts (side stream).
+cudaError_t launch_p2p_totals(Launch& L, cudaStream_t s, const PeerTab* d_tab, const StepPtrs* sp, int P,
+                              const K1Totals& totals);
 // indexes = {u_idx[j] : sel[j]} in order (the K7 intersection, after a fused apply).
 cudaError_t launch_select_flags(Launch& L, const Stage& S, const uint8_t* sel, const PeerTab* d_tab,
                                 const StepPtrs* sp, const uint64_t* d_U, uint64_t bound, uint32_t* out,

@@ -2,20 +2,24 @@
 //
 // Steady Ok-Topk iteration on P ranks, no host round trip and no compaction
 // pass between a producer and its consumers:
-//   K1 phase A (chunked staging + per-chunk cut counts in the window;
-//     its last CTA publishes L-ready)
-//   wait(L ready) -> scatter reads my slice of every chunk of every rank in
-//     place over NVLink -> bracket scan / survivor filter, chunked into the
-//     window (its last CTA writes the chunk prefix and publishes survivors)
-//   wait(survivors) -> plan (offsets, balance) -> pull every chunk to its
-//     position in u, applying K7 on the way
-//     [balanced: pull my block, publish(block), wait, pull the other blocks]
-//   -> indexes.
+//   K1 (per-tile staging + per-tile cut counts in the window; its last CTA
+//     publishes L-ready)
+//   scatter: my own tiles first; CTA 0 waits for every peer's L-ready and
+//     releases the other CTAs; then every peer's tiles, read in place over
+//     NVLink -> bracket scan / survivor filter, chunked into the window (its
+//     last CTA writes the chunk prefix and publishes survivors-ready)
+//   pull: CTA 0 waits for every rank's survivors, plans (offsets, balance),
+//     releases the others; every chunk is pulled to its position in u,
+//     applying K7 on the way [balanced: my block, block sync, the others].
+// Every publish is issued by a CTA running alone at the end of its kernel: a
+// system fence issued while the rest of the grid still streams waits for that
+// traffic to drain.
 #include "okt_device.cuh"
 #include "okt_kernels.hpp"
 #include "okt_p2p.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace okt {
 
@@ -23,93 +27,63 @@ namespace {
 constexpr uint32_t kAbortBits = 1u | 8u | 16u;  // local non-finite, peer timeout, peer failure
 }
 
-// K3 (M1) fused with the split exchange.  Work items are (source, tile,
-// part): only the K1 tiles overlapping my region carry entries for me, and
-// each is split into `parts` when there are more warps than tiles.  A warp reads its part of the chunk's slice for my region,
-// [lt[c][me], lt[c][me+1]), straight out of the source's HBM (NVLink for a
-// peer) and scatters it into the presence mask / coordinate-major staging.
-// My own chunks need no hand-off, so they are scattered first, while the
-// peers' L-ready flags are in flight.  Order does not matter here: the
-// bracket scan re-derives it from coordinates.
-__global__ void __launch_bounds__(kThreads)
-    p2p_scatter_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo, uint64_t W,
-                       uint32_t k1_tiles, uint32_t* mask, float* stage, uint32_t* d_flags, uint64_t timeout_ns) {
-  __shared__ uint64_t s_seg[kP2PMaxP];
+// K3 on the device-driven path: the split exchange and the region merge fused
+// into one kernel, with no random global traffic.  A CTA owns one K1 tile t
+// (4096 coordinates) of my region: after every source's L-ready, it reads
+// each source's compacted entries of tile t (in place: NVLink for a peer —
+// the entries of a tile are contiguous and coordinate-sorted), scatters them
+// into a shared-memory mask / stage, and runs the bracket scan + global
+// threshold filter over the tile from shared memory, writing the tile's
+// survivors as one chunk (capacity 4096) of the survivor staging.  (Random
+// 4-byte global stores — a global-memory scatter — stall every system fence
+// on the GPU for tens of microseconds; tools/p2p_noise.cu.)
+constexpr int kMergeTile = kK1Tile;              // coordinates per CTA tile
+constexpr int kMergePer = kMergeTile / kThreads;  // 16 coordinates per thread in the scan
+
+template <int P>
+__global__ void __launch_bounds__(kThreads, 2)
+    p2p_merge_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo, uint64_t W,
+                     uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* s_mask = sm;                                             // [kMergeTile / 4]: byte per coordinate, bit per source
+  float* s_val = reinterpret_cast<float*>(sm + kMergeTile / 4);      // [P][kMergeTile]
+  __shared__ uint32_t s_wt[kWarps];
+  __shared__ uint32_t s_seg[P];
   __shared__ int s_abort;
   const uint64_t epoch = sp->epoch;
   const int par = sp->par;
-  const int P = tab->P, me = tab->rank, q = threadIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int me = tab->rank, q = threadIdx.x, lane = q & 31, warp = q >> 5;
   uint64_t* const trace = tab->trace;
-  const uint32_t G = k1_tiles, cap = kK1Tile;  // same geometry on every rank (same n)
   if (q == 0) {
     s_abort = (*d_flags & 1u) ? 1 : 0;
-    trace_stamp(trace, kTrScatter, 0);
+    trace_stamp(trace, kTrMerge, 0);
   }
   if (q < P) s_seg[q] = 0;
-  if (blockIdx.x == 0 && q == 0) {
-    // Publish this rank's K1 output (every K1 CTA finished before this kernel
-    // started): status, then L-ready at every rank (myself included).
-    tab->hdr[me]->pub[par].status = (*d_flags & 1u) ? 1 : 0;
-    __threadfence_system();
-    for (int r = 0; r < P; ++r) st_relaxed_sys(&tab->hdr[r]->flag[kFlagLReady][me], epoch);
-  }
-  // K1 chunks are its tiles: the ones overlapping [lo, lo + W).
-  uint32_t c_lo = 0, nch = 0;
-  if (W > 0 && G > 0) {
-    c_lo = uint32_t(lo / kK1Tile);
-    nch = uint32_t((lo + W - 1) / kK1Tile) - c_lo + 1;
-  }
-  const uint32_t warps_total = gridDim.x * kWarps;
-  const uint32_t parts = max(1u, min(8u, warps_total / max(1u, uint32_t(P) * nch)));
-  const uint32_t per_src = nch * parts;
-  const uint32_t gw = blockIdx.x * kWarps + warp;
-  __syncthreads();
-  auto run = [&](int r, uint32_t it) {
-    const uint32_t c = c_lo + it / parts, part = it % parts;
-    const uint32_t* lt = tab->klt[r][par] + uint64_t(c) * kP2PMaxP;
-    const uint32_t a0 = lt[me];
-    const uint32_t b0 = (me + 1 < P) ? lt[me + 1] : tab->kcnt[r][par][c];
-    const uint32_t len = b0 > a0 ? b0 - a0 : 0;
-    const uint32_t a = a0 + uint32_t(uint64_t(len) * part / parts), b = a0 + uint32_t(uint64_t(len) * (part + 1) / parts);
-    const uint64_t* src = tab->kstg[r][par] + uint64_t(c) * cap;
-    // Every lane issues its (remote) loads for a 128-entry round before any
-    // store, so a round costs one NVLink round trip.
-    constexpr int R = 4;
-    for (uint32_t j0 = a; j0 < b; j0 += 32 * R) {
-      uint64_t e[R];
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const uint32_t j = j0 + lane + 32 * k;
-        e[k] = j < b ? src[j] : ~0ull;
-      }
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        if (j0 + lane + 32 * k >= b) continue;
-        const uint64_t idx = coo_idx(e[k]);
-        if (idx < lo || idx - lo >= W) {
-          atomicOr(d_flags, 2u);
-          continue;
-        }
-        const uint64_t i = idx - lo;
-        stage[i * uint64_t(P) + r] = coo_val(e[k]);
-        atomicOr(&mask[i >> 2], 1u << (unsigned(i & 3u) * 8u + unsigned(r)));
-      }
+  const uint64_t hi = lo + W;
+  const uint32_t t_lo = uint32_t(lo / kMergeTile);
+  const uint32_t ntiles = W ? uint32_t((hi - 1) / kMergeTile) - t_lo + 1 : 0;
+  if (blockIdx.x == 0) {
+    // this rank's K1 output: status, then L-ready at every rank (the GPU is
+    // quiet: K1 finished and nobody streams yet)
+    if (q == 0) {
+      P2PPub* pub = &tab->hdr[me]->pub[par];  // (read by this rank's pull)
+      pub->sur_G = ntiles;
+      pub->sur_cap = kMergeTile;
+      trace_stamp(trace, kTrPubL, 0);
     }
-    if (lane == 0 && b > a) atomicAdd(reinterpret_cast<unsigned long long*>(&s_seg[r]), (unsigned long long)(b - a));
-  };
-  // 1. my own chunks (local HBM, no wait)
-  if (!s_abort)
-    for (uint32_t it = gw; it < per_src; it += warps_total) run(me, it);
-  // 2. wait for every peer's L-ready, then their chunks (NVLink)
+    const uint64_t pay[3] = {(*d_flags & 1u) ? 1ull : 0ull, k1_tiles, uint64_t(kK1Tile)};
+    publish_flag(tab->hdr, P, me, kFlagLReady, epoch, pay);
+    if (q == 0) trace_stamp(trace, kTrPubL, 3);
+  }
+  // every source's L-ready (each CTA polls its own flag copy)
   if (q < P && q != me) {
-    if (!wait_flag(&tab->hdr[me]->flag[kFlagLReady][q], epoch, timeout_ns)) {
+    const FlagSlot* f = my_flag(tab->hdr[me], kFlagLReady, q);
+    if (!wait_flag(&f->epoch, epoch, timeout_ns)) {
       atomicOr(d_flags, 8u);
       s_abort = 1;
     } else {
-      const volatile P2PPub* pub = &tab->hdr[q]->pub[par];
-      const uint64_t st = pub->status;
-      if (st || pub->k1_G != G || pub->k1_cap != cap) {
+      const uint64_t st = flag_word(f, 0);
+      if (st || flag_word(f, 1) != k1_tiles || flag_word(f, 2) != uint64_t(kK1Tile)) {
         atomicOr(d_flags, 16u);
         s_abort = 1;
       }
@@ -117,28 +91,121 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   __syncthreads();
-  if (q == 0) trace_stamp(trace, kTrScatter, 1);
-  if (!s_abort) {
-    const uint32_t remote = uint32_t(P - 1) * per_src;
-    for (uint32_t it = gw; it < remote; it += warps_total) {
-      const uint32_t k = it / per_src;
-      run((me + 1 + int(k)) % P, it % per_src);
+  if (q == 0) trace_stamp(trace, kTrMerge, 1);
+  const double gth = *d_gth;
+  uint32_t* const out_idx = tab->sidx[me][par];
+  double* const out_val = tab->sval[me][par];
+  uint32_t* const out_cnt = tab->scnt[me][par];
+  // Tiles of this CTA: j = blockIdx.x + i * gridDim.x.  Two-stage prefetch:
+  // while tile j is merged, the entries of the next tile and the counts of
+  // the one after are in flight (one entry per thread and source per stage;
+  // a source with more than kThreads entries in a tile — dense regions — is
+  // finished by a direct loop).
+  const uint32_t gs = gridDim.x;
+  auto load_counts = [&](uint32_t j, uint32_t (&c)[P]) {
+#pragma unroll
+    for (int r = 0; r < P; ++r) c[r] = (j < ntiles && !s_abort) ? tab->kcnt[r][par][t_lo + j] : 0u;
+  };
+  auto load_entries = [&](uint32_t j, const uint32_t (&c)[P], uint64_t (&e)[P]) {
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+      e[r] = uint32_t(q) < c[r] ? tab->kstg[r][par][uint64_t(t_lo + j) * kMergeTile + q] : ~0ull;
+  };
+  uint32_t cnt0[P], cnt1[P], cnt2[P];
+  uint64_t e0[P], e1[P];
+  load_counts(blockIdx.x, cnt0);
+  load_entries(blockIdx.x, cnt0, e0);
+  load_counts(blockIdx.x + gs, cnt1);
+  for (uint32_t j = blockIdx.x; j < ntiles; j += gs) {
+    const uint32_t t = t_lo + j;
+    const uint64_t base = uint64_t(t) * kMergeTile;
+    load_entries(j + gs, cnt1, e1);
+    load_counts(j + 2 * gs, cnt2);
+    for (int w = q; w < kMergeTile / 4; w += kThreads) s_mask[w] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
+      uint32_t got = 0;
+      auto land = [&](uint64_t ent) {
+        const uint64_t idx = coo_idx(ent);
+        if (idx < lo || idx >= hi) return;  // the region's edge tiles
+        const uint32_t c = uint32_t(idx - base);
+        s_val[r * kMergeTile + c] = coo_val(ent);
+        atomicOr(&s_mask[c >> 2], 1u << ((c & 3u) * 8u + uint32_t(r)));
+        ++got;
+      };
+      if (e0[r] != ~0ull) land(e0[r]);
+      for (uint32_t e = kThreads + q; e < cnt0[r]; e += kThreads) land(tab->kstg[r][par][base + e]);
+      got = __reduce_add_sync(0xffffffffu, got);
+      if (lane == 0 && got) atomicAdd(&s_seg[r], got);
     }
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
+      cnt0[r] = cnt1[r];
+      cnt1[r] = cnt2[r];
+      e0[r] = e1[r];
+    }
+    __syncthreads();
+    // bracket scan + filter over the tile: thread q owns coordinates
+    // [16 q, 16 q + 16) (four mask words)
+    const uint4 mw4 = reinterpret_cast<const uint4*>(s_mask)[q];
+    auto bits_of = [&](int k) {  // source bits of coordinate k (select tree: no local memory)
+      const int j = k >> 2;
+      const uint32_t w = (j & 2) ? ((j & 1) ? mw4.w : mw4.z) : ((j & 1) ? mw4.y : mw4.x);
+      return (w >> (8 * (k & 3))) & 0xffu;
+    };
+    auto nib = [](uint32_t w) { return ((__vcmpne4(w, 0u) & 0x01010101u) * 0x01020408u) >> 24; };
+    const uint32_t present = nib(mw4.x) | (nib(mw4.y) << 4) | (nib(mw4.z) << 8) | (nib(mw4.w) << 12);
+    uint32_t sel = 0;
+    for (uint32_t rest = present; rest; rest &= rest - 1) {
+      const int k = __ffs(rest) - 1;
+      const uint32_t c = uint32_t(q) * kMergePer + uint32_t(k);
+      float v[P];
+#pragma unroll
+      for (int r = 0; r < P; ++r) v[r] = s_val[r * kMergeTile + c];
+      if (fabs(bracket_regs<P>(v, bits_of(k))) >= gth) sel |= 1u << k;
+    }
+    const uint32_t n_sel = __popc(sel);
+    uint32_t incl = n_sel;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    if (lane == 31) s_wt[warp] = incl;
+    __syncthreads();
+    uint32_t wpre = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      wpre += (w < warp) ? s_wt[w] : 0u;
+      total += s_wt[w];
+    }
+    uint64_t pos = uint64_t(j) * kMergeTile + wpre + incl - n_sel;
+    for (uint32_t rest = sel; rest; rest &= rest - 1, ++pos) {
+      const int k = __ffs(rest) - 1;
+      const uint32_t c = uint32_t(q) * kMergePer + uint32_t(k);
+      float v[P];
+#pragma unroll
+      for (int r = 0; r < P; ++r) v[r] = s_val[r * kMergeTile + c];
+      out_idx[pos] = uint32_t(base + c);
+      out_val[pos] = bracket_regs<P>(v, bits_of(k));
+    }
+    if (q == 0) out_cnt[j] = total;
+    __syncthreads();  // s_mask / s_val / s_wt reused by the next tile
   }
-  __syncthreads();
   if (q < P && s_seg[q]) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->seg_cnt[q]), (unsigned long long)s_seg[q]);
-  if (lane == 0) trace_stamp(trace, kTrScatter, 2);
+  if (lane == 0) trace_stamp(trace, kTrMerge, 2);
 }
 
-// Allgatherv by pulling.  round 0 waits for every rank's survivors and
+// Allgatherv by pulling.  round 0: CTA 0 waits for every rank's survivors and
 // derives the plan of balance_and_allgatherv (oktopk.cpp:172-231; identical on
-// all ranks), then one warp per (rank, chunk) copies that chunk's survivors
+// all ranks), then one warp per (rank, chunk, part) copies survivors
 // from the owner's window to their stream position in my u (unbalanced: all
 // of u; balanced: my block).  round 1 (balanced only) pulls the other blocks
 // from their block owners' u.  K7 runs on each entry as it lands.
 __global__ void __launch_bounds__(kThreads)
     p2p_pull_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, uint64_t* d_S, P2PPlan* plan,
-                    uint64_t* d_U, int round, uint32_t* d_flags, uint64_t timeout_ns, P2PApply ap, K1Totals lt) {
+                    uint64_t* d_U, int round, uint32_t* d_flags, uint64_t timeout_ns, P2PApply ap) {
   __shared__ uint64_t s_size[kP2PMaxP], s_off[kP2PMaxP + 1], s_blk[kP2PMaxP + 1];
   __shared__ uint32_t s_G[kP2PMaxP], s_cap[kP2PMaxP], s_start[kP2PMaxP + 1];
   __shared__ int s_bal, s_abort;
@@ -155,60 +222,72 @@ __global__ void __launch_bounds__(kThreads)
     trace_stamp(trace, trk, 0);
   }
   __syncthreads();
-  if (round == 0 && blockIdx.x == 0) {
-    // Publish this rank's survivors (every region-scan CTA finished before
-    // this kernel started): exclusive prefix of the chunk counts (where each
-    // chunk lands in my part of u), S, status, then survivors-ready at every
-    // peer and at myself.
-    P2PPub* mine = &tab->hdr[me]->pub[par];
-    const int G = int(mine->sur_G);
-    const uint32_t* cnt = tab->scnt[me][par];
-    uint64_t* pre = tab->spre[me][par];
-    const int per = (G + kThreads - 1) / kThreads;
-    uint64_t own = 0;
-    for (int c = q * per; c < min(G, (q + 1) * per); ++c) own += cnt[c];
-    uint64_t incl = own;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t x = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += x;
-    }
-    __shared__ uint64_t wsum[kWarps];
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    uint64_t wpre = 0, tot = 0;
-    for (int w = 0; w < kWarps; ++w) {
-      wpre += (w < warp) ? wsum[w] : 0;
-      tot += wsum[w];
-    }
-    uint64_t run = wpre + incl - own;
-    for (int c = q * per; c < min(G, (q + 1) * per); ++c) {
-      pre[c] = run;
-      run += cnt[c];
-    }
-    __syncthreads();
-    if (q == 0) {
-      pre[G] = tot;
-      *d_S = tot;
-      mine->S = tot;
-      mine->status = (*d_flags & (1u | 8u | 16u)) ? 1 : 0;
-      __threadfence_system();
-      for (int r = 0; r < P; ++r) st_relaxed_sys(&tab->hdr[r]->flag[kFlagSurReady][me], epoch);
-    }
-  }
   if (round == 0) {
+    // CTA 0 publishes this rank's survivors (every region-scan CTA finished
+    // before this kernel started; the other CTAs only poll, so the system
+    // fence is cheap): the exclusive prefix of the chunk counts (where each
+    // chunk lands in my part of u), S, status, then survivors-ready at every
+    // rank.
+    if (blockIdx.x == 0) {
+      P2PPub* mine = &tab->hdr[me]->pub[par];
+      const int G = int(mine->sur_G);
+      const uint32_t* cnt = tab->scnt[me][par];
+      uint64_t* pre = tab->spre[me][par];
+      const int per = (G + kThreads - 1) / kThreads;
+      const int c0 = q * per, c1 = min(G, (q + 1) * per);
+      uint64_t own = 0;
+      for (int cb = c0; cb < c1; cb += 8) {  // 8 loads in flight per round
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = cb + u < c1 ? cnt[cb + u] : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) own += v[u];
+      }
+      uint64_t incl = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      __shared__ uint64_t wsum[kWarps];
+      if (lane == 31) wsum[warp] = incl;
+      __syncthreads();
+      uint64_t wpre = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        wpre += (w < warp) ? wsum[w] : 0;
+        tot += wsum[w];
+      }
+      uint64_t run = wpre + incl - own;
+      for (int c = c0; c < c1; ++c) {
+        pre[c] = run;
+        run += cnt[c];
+      }
+      __syncthreads();
+      if (q == 0) {
+        pre[G] = tot;
+        *d_S = tot;
+        trace_stamp(trace, kTrPubSur, 0);
+      }
+      __syncthreads();
+      const uint64_t pay[4] = {(*d_flags & kAbortBits) ? 1ull : 0ull, tot, uint64_t(G), uint64_t(mine->sur_cap)};
+      publish_flag(tab->hdr, P, me, kFlagSurReady, epoch, pay);
+      if (q == 0) trace_stamp(trace, kTrPubSur, 3);
+    }
+    // every CTA: wait on its own flag copies, read the ranks' survivor counts
+    // and geometry, derive the plan (CTA 0 also stores it for round 1 / host)
     if (q < P) {
       uint64_t sz = 0;
       uint32_t G = 0, cap = 0;
-      if (!wait_flag(&tab->hdr[me]->flag[kFlagSurReady][q], epoch, timeout_ns)) {
+      const FlagSlot* f = my_flag(tab->hdr[me], kFlagSurReady, q);
+      if (!wait_flag(&f->epoch, epoch, timeout_ns)) {
         atomicOr(d_flags, 8u);
         s_abort = 1;
       } else {
-        const volatile P2PPub* pub = &tab->hdr[q]->pub[par];
-        sz = pub->S;
-        G = pub->sur_G;
-        cap = pub->sur_cap;
-        if (q != me && pub->status) {
+        sz = flag_word(f, 1);
+        G = uint32_t(flag_word(f, 2));
+        cap = uint32_t(flag_word(f, 3));
+        if (q != me && flag_word(f, 0)) {
           atomicOr(d_flags, 16u);
           s_abort = 1;
         }
@@ -236,7 +315,11 @@ __global__ void __launch_bounds__(kThreads)
       s_blk[0] = 0;
       for (int r = 0; r < P; ++r) s_blk[r + 1] = s_blk[r] + base + (uint64_t(r) < rem ? 1 : 0);
       if (blockIdx.x == 0) {
-        for (int r = 0; r < P; ++r) plan->sizes[r] = s_size[r];
+        for (int r = 0; r < P; ++r) {
+          plan->sizes[r] = s_size[r];
+          plan->sur_G[r] = s_G[r];
+          plan->sur_cap[r] = s_cap[r];
+        }
         for (int r = 0; r <= P; ++r) {
           plan->off[r] = s_off[r];
           plan->block[r] = s_blk[r];
@@ -247,34 +330,39 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
   } else {
+    // round 1: the plan CTA 0 of round 0 stored
     if (q <= P) {
       s_off[q] = plan->off[q];
       s_blk[q] = plan->block[q];
     }
-    if (q == 0) s_bal = int(plan->balanced);
-  }
-  __syncthreads();
-  if (round == 1 && lt.d_m && int(blockIdx.x) <= P) {
-    // Off the critical path: this rank's selection size and slice offsets
-    // (from K1's chunk counts), one CTA per offset, for the result and the
-    // ledger.
-    const int d = blockIdx.x;
-    const uint32_t G = tab->hdr[me]->pub[par].k1_G;
-    const uint32_t* cnt = tab->kcnt[me][par];
-    const uint32_t* klt = tab->klt[me][par];
-    uint64_t o = 0;
-    o = (d == P) ? strided_sum(cnt, G) : strided_sum(klt + d, G, kP2PMaxP);
-    __shared__ uint64_t red[kWarps];
-    o = block_sum(o, red);
-    if (threadIdx.x == 0) {
-      lt.d_off[d] = o;
-      if (d == P) *lt.d_m = o;
+    if (q < P) s_cap[q] = plan->sur_cap[q];
+    if (q == 0) {
+      s_bal = int(plan->balanced);
+      uint32_t items = 0;
+      for (int r = 0; r < P; ++r) {
+        s_start[r] = items;
+        items += plan->sur_G[r];
+      }
+      s_start[P] = items;
     }
   }
+  __syncthreads();
   if (q == 0) trace_stamp(trace, trk, 1);
   if (s_abort) return;
   const bool bal = s_bal != 0;
-  if (round == 1 && !bal) return;
+  if (round == 1) {
+    if (!bal) return;
+    // balanced: CTA 0 publishes "my block of u is complete" (every round-0
+    // CTA finished before this kernel started); every CTA waits for every
+    // peer's block on its own flag copy
+    if (blockIdx.x == 0) publish_flag(tab->hdr, P, me, kFlagBlockReady, sp->epoch);
+    if (q < P && q != me && !wait_flag(&my_flag(tab->hdr[me], kFlagBlockReady, q)->epoch, sp->epoch, timeout_ns)) {
+      atomicOr(d_flags, 8u);
+      s_abort = 1;
+    }
+    __syncthreads();
+    if (s_abort) return;
+  }
   uint32_t* ui = tab->u_idx[me][par];
   double* uv = tab->u_val[me][par];
   const float tf = acc ? ceil_to_float(*ap.d_local_th) : 0.f;
@@ -358,42 +446,106 @@ __global__ void __launch_bounds__(kThreads)
   if (lane == 0) trace_stamp(trace, trk, 2);
 }
 
-// Balanced case only: publish "my block is in u", wait for every other block.
-__global__ void p2p_block_sync_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, const P2PPlan* plan,
-                                      uint32_t* d_flags, uint64_t timeout_ns) {
-  const uint64_t epoch = sp->epoch;
-  const int P = tab->P, me = tab->rank, q = threadIdx.x;
-  if (!plan->balanced || (*d_flags & (1u | 8u | 16u))) return;
-  __syncthreads();
-  if (q < P && q != me) {
-    __threadfence_system();
-    st_relaxed_sys(&tab->hdr[q]->flag[kFlagBlockReady][me], epoch);
+// This rank's selection size and slice offsets from K1's per-tile counts (one
+// CTA per value: d < P the entries below cut d, d = P all), for the result and
+// the ledger.  Runs on a side stream, off the step's critical path.
+__global__ void __launch_bounds__(kThreads)
+    p2p_totals_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, K1Totals lt) {
+  __shared__ uint64_t red[kWarps];
+  const int P = tab->P, me = tab->rank, par = sp->par, d = blockIdx.x;
+  const uint32_t G = tab->hdr[me]->pub[par].k1_G;
+  uint64_t o = (d == P) ? strided_sum(tab->kcnt[me][par], G) : strided_sum(tab->klt[me][par] + d, G, kP2PMaxP);
+  o = block_sum(o, red);
+  if (threadIdx.x == 0) {
+    lt.d_off[d] = o;
+    if (d == P) *lt.d_m = o;
   }
-  if (q < P && q != me && !wait_flag(&tab->hdr[me]->flag[kFlagBlockReady][q], epoch, timeout_ns))
+}
+
+// okt_device_barrier: publish, then wait for every peer (one CTA).
+__global__ void p2p_barrier_kernel(const PeerTab* __restrict__ tab, uint64_t epoch, uint32_t* d_flags,
+                                   uint64_t timeout_ns) {
+  const int P = tab->P, me = tab->rank, q = threadIdx.x;
+  publish_flag(tab->hdr, P, me, kFlagBarrier, epoch);
+  if (q < P && q != me && !wait_flag(&tab->hdr[me]->flag[kFlagBarrier][0][q].epoch, epoch, timeout_ns))
     atomicOr(d_flags, 8u);
 }
 
 // ---- launchers ----------------------------------------------------------------------------
-cudaError_t launch_p2p_scatter(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
-                               uint64_t W, uint64_t n, uint32_t* mask, float* stage, uint32_t* d_flags,
-                               uint64_t timeout_ns) {
-  const uint32_t k1_tiles = uint32_t((n + kK1Tile - 1) / kK1Tile);
-  p2p_scatter_kernel<<<L.sms * 2, kThreads, 0, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, mask, stage, d_flags,
-                                                      timeout_ns);
+template <int P>
+static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
+                                  uint64_t W, uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags,
+                                  uint64_t timeout_ns) {
+  constexpr size_t smem = size_t(kMergeTile) + size_t(P) * kMergeTile * sizeof(float);
+  // the dynamic shared memory opt-in is per device
+  static int caps[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& cap = caps[dev & 63];
+  if (!cap) {
+    cudaFuncSetAttribute(p2p_merge_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_merge_kernel<P>, kThreads, smem) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    cap = per_sm * L.sms;
+  }
+  const uint64_t ntiles = W ? (lo + W - 1) / kMergeTile - lo / kMergeTile + 1 : 0;
+  const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, uint64_t(cap))));
+  p2p_merge_kernel<P><<<grid, kThreads, smem, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
   ++L.launches;
   return cudaGetLastError();
 }
 
-cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, const uint64_t* d_S,
+cudaError_t launch_p2p_merge(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, int P, uint64_t lo,
+                             uint64_t W, uint64_t n, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns) {
+  const uint32_t k1_tiles = uint32_t((n + kK1Tile - 1) / kK1Tile);
+  switch (P) {
+    case 2: return merge_dispatch<2>(L, d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
+    case 4: return merge_dispatch<4>(L, d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
+    case 8: return merge_dispatch<8>(L, d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, uint64_t* d_S,
                                   P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns,
-                                  const P2PApply& ap, const K1Totals& totals) {
-  const int grid = L.sms * 2;
-  p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, const_cast<uint64_t*>(d_S), plan, d_U, 0, d_flags, timeout_ns, ap,
-                                              K1Totals{});
-  p2p_block_sync_kernel<<<1, 32, 0, L.s>>>(d_tab, sp, plan, d_flags, timeout_ns);
-  p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, const_cast<uint64_t*>(d_S), plan, d_U, 1, d_flags, timeout_ns, ap,
-                                              totals);
-  L.launches += 3;
+                                  const P2PApply& ap) {
+  // one wave of as many CTAs as fit (every CTA waits on its own flag copy, so
+  // the whole grid must be resident)
+  static int caps[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& cap = caps[dev & 63];
+  if (!cap) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_pull_kernel, kThreads, 0) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    cap = std::min(per_sm, 4) * L.sms;
+  }
+  const int grid = cap;
+  p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, d_S, plan, d_U, 0, d_flags, timeout_ns, ap);
+  p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, d_S, plan, d_U, 1, d_flags, timeout_ns, ap);
+  L.launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_totals(Launch& L, cudaStream_t s, const PeerTab* d_tab, const StepPtrs* sp, int P,
+                              const K1Totals& totals) {
+  p2p_totals_kernel<<<P + 1, kThreads, 0, s>>>(d_tab, sp, totals);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_barrier(Launch& L, const PeerTab* d_tab, uint64_t epoch, uint32_t* d_flags,
+                               uint64_t timeout_ns) {
+  p2p_barrier_kernel<<<1, kThreads, 0, L.s>>>(d_tab, epoch, d_flags, timeout_ns);
+  ++L.launches;
   return cudaGetLastError();
 }
 

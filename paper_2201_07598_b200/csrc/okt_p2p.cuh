@@ -4,8 +4,8 @@
 // peers map: through CUDA IPC across processes, or directly within one
 // process.  Phases hand data over with release/acquire flags instead of host
 // synchronisation:
-//   publish  the producer fences at system scope, then stores
-//            flag[kind][me] = epoch into every peer's window header;
+//   publish  the producer stores its payload, fences at system scope, then
+//            stores flag[kind][copy][me].epoch into every peer's window header;
 //   wait     the consumer spins (ld.acquire.sys, bounded by a timeout) on its
 //            own header until every peer's flag reached the epoch, then reads
 //            the peers' published words remotely.
@@ -38,7 +38,7 @@ struct StepPtrs {
   int32_t par;     // P2P: parity slot of the window buffers
   int32_t pad2;
 };
-enum P2PFlag { kFlagLReady = 0, kFlagSurReady = 1, kFlagBlockReady = 2, kP2PFlagKinds = 4 };
+enum P2PFlag { kFlagLReady = 0, kFlagSurReady = 1, kFlagBlockReady = 2, kFlagBarrier = 3, kP2PFlagKinds = 4 };
 
 // What a rank publishes for its peers each step (double-buffered by parity).
 struct P2PPub {
@@ -51,8 +51,21 @@ struct P2PPub {
   uint64_t pad[4];
 };
 
+// Flags are replicated: a publisher stores its epoch into kFlagCopies copies
+// (one 128-byte line each) at every rank, and CTA b polls copy b % kFlagCopies
+// — a few hundred CTAs polling a single line contend on one L2 slice and see
+// the flag microseconds apart, and fanning a flag out inside the grid costs a
+// fence that waits for the grid's own traffic.
+// A flag slot carries the words its consumers need (status, counts,
+// geometry) next to the epoch, so a consumer reads them from its own memory
+// instead of every CTA reading the source's header over NVLink.
+constexpr int kFlagCopies = 32, kFlagWords = 7;
+struct FlagSlot {
+  uint64_t epoch;
+  uint64_t v[kFlagWords];  // payload, valid once epoch is observed
+};
 struct P2PHdr {
-  uint64_t flag[kP2PFlagKinds][kP2PMaxP];  // written by peers
+  FlagSlot flag[kP2PFlagKinds][kFlagCopies][kP2PMaxP];  // [kind][copy][source rank], written by the sources
   P2PPub pub[2];
 };
 
@@ -76,7 +89,11 @@ struct PeerTab {
 };
 // Per-CTA timestamps of the last P2P step (diagnostics only):
 // slot 0 = CTA start, 1 = after its flag waits / prologue, 2 = last warp done.
-enum TraceKind { kTrK1 = 0, kTrScatter = 1, kTrRegion = 2, kTrPull0 = 3, kTrPull1 = 4, kTraceKinds = 5 };
+enum TraceKind {
+  kTrK1 = 0, kTrMerge = 1, kTrUnused = 2, kTrPull0 = 3, kTrPull1 = 4,
+  kTrPubL = 5, kTrPubSur = 6,  // CTA 0's publish: [before fence, after fence, after the flag stores]
+  kTraceKinds = 7
+};
 constexpr int kTraceCtas = 2048;
 
 // Device-side plan of the balance + allgatherv phase (local memory).
@@ -90,6 +107,8 @@ struct P2PPlan {
   uint64_t seg_off[kP2PMaxP];    // my split slices inside each source's L
   uint64_t seg_cnt[kP2PMaxP];
   uint64_t peer_status[kP2PMaxP];
+  uint32_t sur_G[kP2PMaxP];      // every rank's region-scan chunk geometry
+  uint32_t sur_cap[kP2PMaxP];
 };
 
 // K7 fused into the allgatherv pull: every u entry is touched once.
@@ -100,8 +119,8 @@ struct P2PApply {
   uint8_t* sel = nullptr;       // per u entry: 1 if in the local selection
 };
 
-// P2P mode of K1 (phase A writes straight into the window and its last CTA
-// publishes) and of the region scan (same, for the survivors).
+// P2P mode of K1: its per-tile staging, counts and cut counts go straight into
+// this rank's window, where the peers' merge kernels read them in place.
 struct K1P2P {
   const PeerTab* tab = nullptr;  // device copy
   const StepPtrs* sp = nullptr;  // epoch / parity of the step
@@ -110,10 +129,6 @@ struct K1P2P {
 struct K1Totals {  // where the local selection size / slice offsets go
   uint64_t* d_m = nullptr;
   uint64_t* d_off = nullptr;
-};
-struct RSP2P {
-  const PeerTab* tab = nullptr;
-  const StepPtrs* sp = nullptr;
 };
 
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
@@ -129,6 +144,14 @@ __device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ uint64_t globaltimer_ns() {
@@ -158,4 +181,37 @@ __device__ __forceinline__ bool wait_flag(const uint64_t* p, uint64_t epoch, uin
   }
 }
 
+// Every thread of the publishing CTA, after a __syncthreads: the payload,
+// then the epoch, into every copy of this rank's slot of flag `kind` at every
+// rank.  Each storing thread fences between its payload and its epoch stores
+// (the fence-based release pattern; the fences run in parallel).
+template <int NPAY>
+__device__ __forceinline__ void publish_flag(P2PHdr* const* hdr, int P, int me, int kind, uint64_t epoch,
+                                             const uint64_t (&pay)[NPAY]) {
+  static_assert(NPAY <= kFlagWords, "flag payload");
+  const int total = P * kFlagCopies;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    FlagSlot* slot = &hdr[i / kFlagCopies]->flag[kind][i % kFlagCopies][me];
+#pragma unroll
+    for (int k = 0; k < NPAY; ++k) st_relaxed_sys(&slot->v[k], pay[k]);
+    __threadfence_system();
+    st_relaxed_sys(&slot->epoch, epoch);
+  }
+}
+// This CTA's copy of source q's slot of flag `kind` in my header.
+__device__ __forceinline__ const FlagSlot* my_flag(const P2PHdr* mine, int kind, int q) {
+  return &mine->flag[kind][blockIdx.x % kFlagCopies][q];
+}
+// Payload word k of a slot whose epoch this thread has acquired.
+__device__ __forceinline__ uint64_t flag_word(const FlagSlot* f, int k) {
+  return *reinterpret_cast<const volatile uint64_t*>(&f->v[k]);
+}
+// Same, without payload.
+__device__ __forceinline__ void publish_flag(P2PHdr* const* hdr, int P, int me, int kind, uint64_t epoch) {
+  const int total = P * kFlagCopies;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    __threadfence_system();
+    st_relaxed_sys(&hdr[i / kFlagCopies]->flag[kind][i % kFlagCopies][me].epoch, epoch);
+  }
+}
 }  // namespace okt

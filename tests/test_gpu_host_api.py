@@ -92,3 +92,19 @@ def test_sparse_allreduce_host_matches_device_call(okm, gpus, pinned):
         assert np.array_equal(h_idx[:U].numpy().view(np.uint32), ref.u.indices)
         assert np.array_equal(h_val[:U].numpy(), ref.u.values)
         assert np.array_equal(h_ind[:int(res.n_indexes)].numpy().view(np.uint32), ref.indexes)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_device_barrier(okm, gpus, P):
+    """okt_device_barrier is collective and leaves the comms usable (peer-mapped
+    worlds run it as a flag kernel, shared-GPU worlds as a host barrier)."""
+    from paper_2201_07598_b200 import _lib
+    L = _lib.lib()
+    w = okm.World(P, [r % gpus for r in range(P)])
+    for _ in range(3):
+        rcs = okm.run_ranks(w, lambda ctx: L.okt_device_barrier(ctx.comm, None))
+        assert rcs == [0] * P
+    g = [np.random.default_rng(r).standard_normal(4096).astype(np.float32) for r in range(P)]
+    st = [okm.OkState() for _ in range(P)]
+    res = okm.run_ranks(w, lambda ctx: okm.ok_sparse_allreduce(ctx, st[ctx.rank], g[ctx.rank], 1, 40))
+    assert all(np.array_equal(r.u.indices, res[0].u.indices) for r in res)
