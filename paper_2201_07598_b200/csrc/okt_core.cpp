@@ -661,13 +661,20 @@ struct okt_comm {
     bool ok = me.ok != 0;
     std::vector<char*> base(P, nullptr);
     base[rank] = win.as<char>();
+    // Test hook: OKT_P2P_ALLOW_SHARED=1 (with OKT_P2P_GRID_DIV >= the ranks per
+    // GPU, so the ranks' spinning kernels fit side by side) runs the
+    // device-driven path with several ranks of one process on one GPU.
+    static const bool allow_shared = std::getenv("OKT_P2P_ALLOW_SHARED") != nullptr;
     for (int q = 0; q < P && ok; ++q) {
       if (q == rank) continue;
-      if (!all[q].ok || std::memcmp(all[q].uuid, me.uuid, 16) == 0) {
+      const bool same_gpu = std::memcmp(all[q].uuid, me.uuid, 16) == 0;
+      if (!all[q].ok || (same_gpu && !(allow_shared && all[q].pid == me.pid))) {
         ok = false;  // a shared GPU: in-kernel cross-rank waits are not safe there
         break;
       }
-      if (all[q].pid == me.pid) {
+      if (same_gpu) {
+        base[q] = reinterpret_cast<char*>(all[q].base);
+      } else if (all[q].pid == me.pid) {
         int can = 0;
         cudaDeviceCanAccessPeer(&can, device, all[q].device);
         if (!can) {

@@ -472,6 +472,13 @@ __global__ void p2p_barrier_kernel(const PeerTab* __restrict__ tab, uint64_t epo
 }
 
 // ---- launchers ----------------------------------------------------------------------------
+// Test hook (see setup_p2p): shrink the spinning kernels' grids so that
+// several ranks sharing one GPU fit side by side.
+static int grid_div() {
+  static const int d = std::getenv("OKT_P2P_GRID_DIV") ? std::max(1, std::atoi(std::getenv("OKT_P2P_GRID_DIV"))) : 1;
+  return d;
+}
+
 template <int P>
 static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
                                   uint64_t W, uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags,
@@ -490,7 +497,7 @@ static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtr
       cudaGetLastError();
       per_sm = 1;
     }
-    cap = per_sm * L.sms;
+    cap = std::max(1, per_sm * L.sms / grid_div());
   }
   const uint64_t ntiles = W ? (lo + W - 1) / kMergeTile - lo / kMergeTile + 1 : 0;
   const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, uint64_t(cap))));
@@ -526,7 +533,7 @@ cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtr
       cudaGetLastError();
       per_sm = 1;
     }
-    cap = std::min(per_sm, 4) * L.sms;
+    cap = std::max(1, std::min(per_sm, 4) * L.sms / grid_div());
   }
   const int grid = cap;
   p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, d_S, plan, d_U, 0, d_flags, timeout_ns, ap);
