@@ -416,7 +416,8 @@ def run_okt(args):
         d2h += 12 * res.u.nnz
     barrier()
     clk = clocks.stop()
-    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev) / e2e_steps
+    e2e_list = [a.elapsed_time(b) for a, b in e2e_ev]
+    e2e_ms = sum(e2e_list) / e2e_steps
     # ---- max over ranks
     mine = torch.tensor([total_ms, e2e_ms, wall], dtype=torch.float64)
     if world > 1:
@@ -443,7 +444,9 @@ def run_okt(args):
                 "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": workload(args, P),
                 "e2e": {"value": e2e_ms, "unit": "ms/iter", "h2d_bytes_per_step": 4 * n,
-                        "d2h_bytes_per_step": int(d2h / e2e_steps)},
+                        "d2h_bytes_per_step": int(d2h / e2e_steps), "steps": e2e_steps,
+                        "ms_min": min(e2e_list), "ms_median": statistics.median(e2e_list), "ms_max": max(e2e_list),
+                        "path": "okt_sgd_step_host: gradient H2D from pinned host memory, step, u D2H"},
                 "gpu_launches": int(launches1.value - launches0.value),
                 "roofline": {"bound": "hbm", "kernel": "k1_kernel (fused residual accumulate + threshold select "
                                                          "+ chunk-local COO compaction; phase A of K1)",

@@ -222,6 +222,10 @@ struct okt_comm {
   } graph1;
   uint64_t buf_gen = 1;
   DevScalars* h = nullptr;   // pinned download mirror
+  okt::HostOut* hfast = nullptr;      // mapped pinned: the steady P = 1 step's scalars
+  okt::HostOut* hfast_dev = nullptr;  // its device address
+  uint64_t p1_seq = 0;
+  bool hfast_pending = false;
   DevScalars* hup = nullptr; // pinned upload staging
   size_t cap_n = 0;
   int eps_cur = 0;
@@ -882,7 +886,10 @@ struct okt_comm {
     hup->sp.eps_out = eps_out;
     hup->sp.w = w;
     hup->sp.alpha = alpha;
+    hup->sp.epoch = ++p1_seq;
+    hup->sp.hflags = &hfast_dev->flags;
     hup->flags = 0;
+    hfast->flags = 0;  // the kernels OR error bits into it
     if (!G.exec || G.n != n || G.k != k || G.sgd != sgd || G.gen != buf_gen || G.prof != prof) {
       if (G.exec) {
         cudaGraphExecDestroy(G.exec);
@@ -899,14 +906,17 @@ struct okt_comm {
       cudaMemcpyAsync(&d()->sp, &hup->sp, offsetof(DevScalars, pad1) - offsetof(DevScalars, sp),
                       cudaMemcpyHostToDevice, s);
       if (prof) cudaEventRecordWithFlags(G.e0, s, cudaEventRecordExternal);
-      okt::ApplyArgs ap;
-      if (sgd) ap = okt::ApplyArgs{nullptr, nullptr, &d()->flags, dp};
+      okt::ApplyArgs ap;  // (acc / w of the fused K7 come from the step block)
+      ap.k7 = sgd;
+      ap.d_flags = &d()->flags;
+      ap.ind = dp;
+      ap.hout = hfast_dev;
       cudaError_t e = okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, g, eps_in,
                                      eps_out, alpha, n, &d()->local_th, &d()->global_th,
                                      okt::OutCoo{nullptr, sur_idx.as<uint32_t>(), sur_val.as<double>()}, &d()->S,
                                      &d()->m, &d()->flags, nullptr, &ap, nullptr, dp);
       if (prof) cudaEventRecordWithFlags(G.e1, s, cudaEventRecordExternal);
-      cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s);
+      // (no D2H node: phase B's last CTA writes m, S and the flags to hfast)
       cudaGraph_t graph = nullptr;
       const cudaError_t e2 = cudaStreamEndCapture(s, &graph);
       if (e != cudaSuccess || e2 != cudaSuccess) {
@@ -930,9 +940,23 @@ struct okt_comm {
     L.launches += G.kernels;
     if (prof) k1_used = 2 * graph1_k1_pairs;  // the graph re-recorded its K1 events
     graph_prof_pending = prof;
-    if (defer) return OKT_OK;
+    if (defer) {
+      hfast_pending = true;  // read by wait_pending after its sync
+      return OKT_OK;
+    }
     if ((rc = ck(cudaStreamSynchronize(s), "device"))) return rc;
+    if ((rc = read_hfast())) return rc;
     collect_graph_prof();
+    return OKT_OK;
+  }
+  // The scalars a steady single-rank graph step hands back through mapped
+  // host memory (into the DevScalars mirror, where commit_step reads them).
+  int read_hfast() {
+    const volatile okt::HostOut* o = hfast;
+    if (o->seq != p1_seq) return set_err(OKT_ERR_INTERNAL, "single-rank step: no scalars from the device");
+    h->m = o->m;
+    h->S = o->S;
+    h->flags = o->flags;  // (bits 0 and 2: the only ones a single-rank step sets)
     return OKT_OK;
   }
   bool graph_prof_pending = false;
@@ -1065,7 +1089,12 @@ struct okt_comm {
     // P = 1: u is a subset of the local selection, so K7 (w -= u, eps = 0 at u)
     // is fused into the compaction that writes u, and indexes = u.indices.
     okt::ApplyArgs ap1;
-    if (sgd && P == 1) ap1 = okt::ApplyArgs{eps_out, w, &d()->flags};
+    if (sgd && P == 1) {
+      ap1.k7 = true;
+      ap1.acc = eps_out;
+      ap1.w = w;
+      ap1.d_flags = &d()->flags;
+    }
 
     // ---- K1 / K2 ----
     if (thr) {
@@ -1208,8 +1237,12 @@ struct okt_comm {
   int wait_pending(okt_result* out) {
     if (!pending.on) return OKT_OK;
     pending.on = false;
-    const int rc = ck(cudaStreamSynchronize(pending.s), "device");
+    int rc = ck(cudaStreamSynchronize(pending.s), "device");
     if (rc) return abort_step(rc);
+    if (hfast_pending) {
+      hfast_pending = false;
+      if ((rc = read_hfast())) return abort_step(rc);
+    }
     tcollect();
     collect_graph_prof();
     return commit_step(pending.n, pending.t, pending.thr, pending.sgd, pending.cuts, pending.ui, pending.uv, out);
@@ -1344,6 +1377,8 @@ int init_comm(okt_comm* c) {
   if (e == cudaSuccess) e = c->tilectr.ensure(64);
   if (e == cudaSuccess) e = cudaMallocHost(&c->h, sizeof(DevScalars));
   if (e == cudaSuccess) e = cudaMallocHost(&c->hup, sizeof(DevScalars));
+  if (e == cudaSuccess) e = cudaHostAlloc(&c->hfast, sizeof(okt::HostOut), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hfast_dev), c->hfast, 0);
   if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("init: ") + cudaGetErrorString(e));
   std::memset(c->h, 0, sizeof(DevScalars));
   std::memset(c->hup, 0, sizeof(DevScalars));
@@ -1480,6 +1515,7 @@ int okt_comm_destroy(okt_comm* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->h) cudaFreeHost(c->h);
   if (c->hup) cudaFreeHost(c->hup);
+  if (c->hfast) cudaFreeHost(c->hfast);
   if (c->graph1.exec) cudaGraphExecDestroy(c->graph1.exec);
   if (c->graph1.e0) {
     cudaEventDestroy(c->graph1.e0);

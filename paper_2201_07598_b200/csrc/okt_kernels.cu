@@ -160,6 +160,11 @@ __global__ void __launch_bounds__(kThreads)
     if (tid == 0) {
       *d_total = pre;
       if (counts2) *d_total2 = s2;
+      if (ap.hout) {  // the step's scalars straight into mapped host memory (no D2H node)
+        ap.hout->m = counts2 ? s2 : 0;
+        ap.hout->S = pre;
+        ap.hout->seq = ap.ind->epoch;
+      }
     }
     pre = 0;
   }
@@ -198,7 +203,10 @@ __global__ void __launch_bounds__(kThreads)
     if (MODE == 2) v = sval[sj];
     emit(j, e, i, v, APPLY ? ap.w[i] : 0.f);
   }
-  if (APPLY && __syncthreads_or(bad) && tid == 0) atomicOr(ap.d_flags, 4u);
+  if (APPLY && __syncthreads_or(bad) && tid == 0) {
+    atomicOr(ap.d_flags, 4u);
+    if (ap.hout) atomicOr_system(ap.ind->hflags, 4u);  // (error path only)
+  }
 }
 
 // G chunks of `cap` entries (cap_host, or *d_cap when set); counts2: g2
@@ -211,7 +219,7 @@ static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_
   // one chunk per CTA while the grid fits one wave, then groups of up to
   // kThreads chunks
   static int cap_a = 0, cap_p = 0;
-  const bool apply = ap && (ap->w || ap->ind);
+  const bool apply = ap && ap->k7;
   int& cap = apply ? cap_a : cap_p;
   if (!cap)
     cap = apply ? resident_ctas(compact_kernel<MODE, true>, kThreads, L.sms)
@@ -220,7 +228,10 @@ static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_
   const uint32_t per = std::min<uint32_t>(kThreads, std::max<uint32_t>(1, (G + slots - 1) / slots));
   const uint32_t GB = std::max<uint32_t>(1, (G + per - 1) / per);
   const uint32_t* c2 = g2 ? S.counts2 : nullptr;
-  if (apply)
+  if (!apply && ap && ap->hout)
+    compact_kernel<MODE, false><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap,
+                                                          o64, oidx, oval, d_total, d_total2, *ap);
+  else if (apply)
     compact_kernel<MODE, true><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap,
                                                          o64, oidx, oval, d_total, d_total2, *ap);
   else
@@ -418,7 +429,10 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
     const uint64_t s = block_sum(mloc, red);
     if (tid == 0) counts2[blockIdx.x] = uint32_t(s);
   }
-  if (__syncthreads_or(bad) && tid == 0) atomicOr(d_flags, 1u);
+  if (__syncthreads_or(bad) && tid == 0) {
+    atomicOr(d_flags, 1u);
+    if (ind && ind->hflags) atomicOr_system(ind->hflags, 1u);  // (error path only)
+  }
   if (HIST) {
     for (int i = tid; i < 2048; i += kThreads)
       if (s_hist[i]) atomicAdd(&d_hist[i], s_hist[i]);

@@ -55,11 +55,23 @@ struct OutCoo {
 };
 
 // Fused K7 for the single-rank path (every entry of u is locally selected).
+// What the host reads after a steady single-rank graph step, written by the
+// kernels straight into mapped pinned memory (no D2H node): phase B's CTA 0
+// writes the counts, and any CTA that detects an error ORs its bit into
+// flags (the host clears flags before each launch).
+struct HostOut {
+  uint64_t seq;  // StepPtrs::epoch of the step that wrote it
+  uint64_t m, S;
+  uint32_t flags, pad;
+};
+
 struct ApplyArgs {
+  bool k7 = false;        // apply K7 at u's entries (P = 1 EF step)
   float* acc = nullptr;   // residual buffer holding acc; zeroed at u's indices
   float* w = nullptr;     // model; w[i] -= u_i
   uint32_t* d_flags = nullptr;
   const StepPtrs* ind = nullptr;  // when set, acc / w come from here
+  HostOut* hout = nullptr;        // when set: the step's scalars go there (ind->hflags: its flags)
 };
 
 // Split-phase receive segments for the region scatter (M1): one per source.

@@ -34,9 +34,10 @@ struct StepPtrs {
   float* w;
   float alpha;
   float pad;
-  uint64_t epoch;  // P2P: flag value of this step
+  uint64_t epoch;  // P2P: flag value of this step; P = 1 graph: step sequence number
   int32_t par;     // P2P: parity slot of the window buffers
   int32_t pad2;
+  uint32_t* hflags;  // P = 1 graph: mapped host word the error bits are ORed into
 };
 enum P2PFlag { kFlagLReady = 0, kFlagSurReady = 1, kFlagBlockReady = 2, kFlagBarrier = 3, kP2PFlagKinds = 4 };
 
