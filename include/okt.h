@@ -283,10 +283,11 @@ int okt_phase_bytes(okt_comm* comm, double* bytes_out /* OKT_T_COUNT */);
 int okt_reset_phase_times(okt_comm* comm);
 /* Number of kernels this comm has launched since creation. */
 int okt_kernel_launches(const okt_comm* comm, uint64_t* out);
-/* Diagnostics: per-CTA %globaltimer stamps (ns) of the last device-driven
- * (NVLink P2P) step, [7 kinds: K1, merge, (unused), pull 0, pull 1, L publish,
- * survivor publish] x [2048 CTAs] x [start, after waits, end, 0].  Recorded only when the comm
- * was set up with OKT_P2P_TRACE in the environment (else OKT_ERR_CONFIG). */
+/* Diagnostics: per-CTA %globaltimer stamps (ns) of the last graph step,
+ * [7 kinds: K1, merge, compact (P = 1), pull 0, pull 1, L publish, survivor
+ * publish] x [2048 CTAs] x [start, after waits, end, extra].  Recorded only
+ * when the comm was created with OKT_P2P_TRACE in the environment (else
+ * OKT_ERR_CONFIG). */
 int okt_debug_p2p_trace(okt_comm* comm, uint64_t* out, size_t n_words);
 
 /* ---- seeded input generators (bit-exact ports of the reference's rng.hpp

@@ -727,12 +727,7 @@ struct okt_comm {
         tab.u_val[q][p] = reinterpret_cast<double*>(base[q] + lay.uval[p]);
       }
     }
-    if (std::getenv("OKT_P2P_TRACE")) {
-      const size_t words = size_t(okt::kTraceKinds) * okt::kTraceCtas * 4;
-      if ((rc = ensure(trbuf, 8 * words))) return rc;
-      if ((rc = ck(cudaMemset(trbuf.p, 0, 8 * words), "memset"))) return rc;
-      tab.trace = trbuf.as<uint64_t>();
-    }
+    tab.trace = trbuf.as<uint64_t>();  // (null unless OKT_P2P_TRACE)
     if ((rc = ensure(tabd, sizeof(okt::PeerTab)))) return rc;
     if ((rc = ck(cudaMemcpy(tabd.p, &tab, sizeof(okt::PeerTab), cudaMemcpyHostToDevice), "tab"))) return rc;
     if ((rc = ensure(indexes, 4 * std::max<size_t>(n, 1)))) return rc;
@@ -888,6 +883,7 @@ struct okt_comm {
     hup->sp.alpha = alpha;
     hup->sp.epoch = ++p1_seq;
     hup->sp.hflags = &hfast_dev->flags;
+    hup->sp.trace = trbuf.as<uint64_t>();
     hup->flags = 0;
     hfast->flags = 0;  // the kernels OR error bits into it
     if (!G.exec || G.n != n || G.k != k || G.sgd != sgd || G.gen != buf_gen || G.prof != prof) {
@@ -911,6 +907,7 @@ struct okt_comm {
       ap.d_flags = &d()->flags;
       ap.ind = dp;
       ap.hout = hfast_dev;
+      ap.trace = trbuf.as<uint64_t>();
       cudaError_t e = okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, g, eps_in,
                                      eps_out, alpha, n, &d()->local_th, &d()->global_th,
                                      okt::OutCoo{nullptr, sur_idx.as<uint32_t>(), sur_val.as<double>()}, &d()->S,
@@ -1386,6 +1383,11 @@ int init_comm(okt_comm* c) {
   c->S.counts2 = c->counts2.as<uint32_t>();
   c->S.chunk_cap = c->chunkcap.as<uint64_t>();
   c->S.tile_ctr = c->tilectr.as<uint32_t>();
+  if (std::getenv("OKT_P2P_TRACE")) {  // diagnostics: per-CTA globaltimer stamps
+    c->trbuf.zero_init = true;
+    if (c->trbuf.ensure(8 * size_t(okt::kTraceKinds) * okt::kTraceCtas * 4) != cudaSuccess)
+      return set_err(OKT_ERR_CUDA, "trace buffer");
+  }
   return c->reserve(4096);
 }
 
@@ -2023,11 +2025,11 @@ int okt_kernel_launches(const okt_comm* c, uint64_t* out) {
 
 int okt_debug_p2p_trace(okt_comm* c, uint64_t* out, size_t n_words) {
   OKT_COMM_CHECK(c);
-  if (!c->p2p || !c->tab.trace) return OKT_ERR_CONFIG;
+  if (!c->trbuf.p) return OKT_ERR_CONFIG;
   const size_t words = std::min(n_words, size_t(okt::kTraceKinds) * okt::kTraceCtas * 4);
   cudaSetDevice(c->device);
   if (cudaDeviceSynchronize() != cudaSuccess ||
-      cudaMemcpy(out, c->tab.trace, 8 * words, cudaMemcpyDeviceToHost) != cudaSuccess)
+      cudaMemcpy(out, c->trbuf.p, 8 * words, cudaMemcpyDeviceToHost) != cudaSuccess)
     return OKT_ERR_CUDA;
   return OKT_OK;
 }

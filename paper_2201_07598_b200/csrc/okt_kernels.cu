@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(kThreads)
     ap.w = ap.ind->w;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) trace_stamp(ap.trace, kTrCompact, 0);
   const uint32_t c0 = uint32_t(split_at(blockIdx.x, G, gridDim.x));
   const uint32_t c1 = uint32_t(split_at(blockIdx.x + 1, G, gridDim.x));
   const int nc = int(c1 - c0);
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(kThreads)
   if (tid < nc) s_pre[tid + 1] = wpre + incl;
   if (tid == 0) s_pre[0] = 0;
   __syncthreads();
+  if (tid == 0) trace_stamp(ap.trace, kTrCompact, 1);
   const uint64_t cnt = s_pre[nc];
   auto src_of = [&](uint64_t j) {  // staging position of the group's j-th entry
     int lo = 0, hi = nc - 1;          // last k with s_pre[k] <= j
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   pre = block_sum(pre, red);
+  if (tid == 0) trace_stamp(ap.trace, kTrCompact, 3);
   if (first) {
     if (counts2) s2 = block_sum(s2, red);
     if (tid == 0) {
@@ -207,6 +210,7 @@ __global__ void __launch_bounds__(kThreads)
     atomicOr(ap.d_flags, 4u);
     if (ap.hout) atomicOr_system(ap.ind->hflags, 4u);  // (error path only)
   }
+  if (lane == 0) trace_stamp(ap.trace, kTrCompact, 2);
 }
 
 // G chunks of `cap` entries (cap_host, or *d_cap when set); counts2: g2
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
       s_below[1][threadIdx.x] = 0;
     }
   }
-  uint64_t* const trace = p2p_on ? p2p.tab->trace : nullptr;
+  uint64_t* const trace = p2p_on ? p2p.tab->trace : (ind ? ind->trace : nullptr);
   if (trace && threadIdx.x == 0) trace_stamp(trace, kTrK1, 0);
   if (ind) {
     g = ind->g;

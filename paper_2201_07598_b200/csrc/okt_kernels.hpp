@@ -72,6 +72,7 @@ struct ApplyArgs {
   uint32_t* d_flags = nullptr;
   const StepPtrs* ind = nullptr;  // when set, acc / w come from here
   HostOut* hout = nullptr;        // when set: the step's scalars go there (ind->hflags: its flags)
+  uint64_t* trace = nullptr;      // diagnostics (OKT_P2P_TRACE): per-CTA stamps, kind kTrCompact
 };
 
 // Split-phase receive segments for the region scatter (M1): one per source.

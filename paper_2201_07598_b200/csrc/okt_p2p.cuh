@@ -38,6 +38,7 @@ struct StepPtrs {
   int32_t par;     // P2P: parity slot of the window buffers
   int32_t pad2;
   uint32_t* hflags;  // P = 1 graph: mapped host word the error bits are ORed into
+  uint64_t* trace;   // diagnostics (OKT_P2P_TRACE): per-CTA stamps, or null
 };
 enum P2PFlag { kFlagLReady = 0, kFlagSurReady = 1, kFlagBlockReady = 2, kFlagBarrier = 3, kP2PFlagKinds = 4 };
 
@@ -91,7 +92,7 @@ struct PeerTab {
 // Per-CTA timestamps of the last P2P step (diagnostics only):
 // slot 0 = CTA start, 1 = after its flag waits / prologue, 2 = last warp done.
 enum TraceKind {
-  kTrK1 = 0, kTrMerge = 1, kTrUnused = 2, kTrPull0 = 3, kTrPull1 = 4,
+  kTrK1 = 0, kTrMerge = 1, kTrCompact = 2, kTrPull0 = 3, kTrPull1 = 4,
   kTrPubL = 5, kTrPubSur = 6,  // CTA 0's publish: [before fence, after fence, after the flag stores]
   kTraceKinds = 7
 };

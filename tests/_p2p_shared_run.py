@@ -49,8 +49,11 @@ for t in range(1, steps + 1):
     for r in range(P):
         assert np.array_equal(got[r][0], u_idx) and np.array_equal(got[r][1], u_val), (t, r, "u")
         assert np.array_equal(d_w[r].cpu().numpy().astype(np.float64), ws[r]), (t, r, "model")
-# the device-driven path really ran (the trace exists only on a mapped world)
-buf = (ctypes.c_uint64 * 4)()
+# the device-driven path really ran: its merge kernel stamped the trace
+kinds, ctas = 7, 2048
 for r in range(P):
-    assert L.okt_debug_p2p_trace(w.ctx(r).comm, buf, 4) == 0, f"rank {r}: P2P path not active"
+    buf = (ctypes.c_uint64 * (kinds * ctas * 4))()
+    assert L.okt_debug_p2p_trace(w.ctx(r).comm, buf, kinds * ctas * 4) == 0
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(kinds, ctas, 4)
+    assert a[1, 0, 0] > 0, f"rank {r}: P2P path not active"
 print("ok", P, G)
