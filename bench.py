@@ -418,11 +418,28 @@ def run_okt(args):
     clk = clocks.stop()
     e2e_list = [a.elapsed_time(b) for a, b in e2e_ev]
     e2e_ms = sum(e2e_list) / e2e_steps
+    # ---- reference point: a dense NCCL allreduce of the same gradient
+    dense_ms = None
+    if world > 1:
+        pg = dist.new_group(backend="nccl")
+        dense = torch.empty(n, dtype=torch.float32, device="cuda")
+        dense.copy_(ring[0])
+        dev_ = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(16)]
+        for i in range(4 + len(dev_)):
+            flush.fill_(i & 0xff)
+            barrier()
+            if i >= 4:
+                dev_[i - 4][0].record()
+            dist.all_reduce(dense, group=pg)
+            if i >= 4:
+                dev_[i - 4][1].record()
+        torch.cuda.synchronize()
+        dense_ms = sum(a.elapsed_time(b) for a, b in dev_) / len(dev_)
     # ---- max over ranks
-    mine = torch.tensor([total_ms, e2e_ms, wall], dtype=torch.float64)
+    mine = torch.tensor([total_ms, e2e_ms, wall, dense_ms or 0.0], dtype=torch.float64)
     if world > 1:
         dist.all_reduce(mine, op=dist.ReduceOp.MAX)
-    total_ms, e2e_ms, wall = mine.tolist()
+    total_ms, e2e_ms, wall, dense_ms = mine.tolist()
     ms_per_step = total_ms / args.steps
     achieved = k1_bytes / (k1_ms * 1e-3) / 1e9 if k1_ms > 0 else None
     peak = None
@@ -460,6 +477,10 @@ def run_okt(args):
                 "phases_ms_per_step": phases,
                 "avg_U": U_sum / args.steps, "avg_local_selected": m_sum / args.steps,
                 "wall_ms_per_step": 1e3 * wall / args.steps,
+                "dense_nccl_allreduce": None if world == 1 else {
+                    "ms": dense_ms, "bytes": 4 * n,
+                    "note": "reference point: torch.distributed NCCL all_reduce of the dense fp32 gradient, "
+                            "device-timed, max over ranks (not the metric)"},
                 "clocks": clk}
     # ---- CPU baseline (rank 0, N = 1 only): the reference itself, bounded sample
     if rank == 0 and P == 1 and not args.no_cpu_baseline:
