@@ -185,7 +185,6 @@ inline oklab::OkAllreduceResult ok_sparse_allreduce(const oklab::WorkerCtx& ctx,
 inline oklab::StepOutcome oktopk_sgd_step(const oklab::WorkerCtx& ctx, oklab::ModelState& model,
                                           oklab::Residual& residual, const oklab::Problem& problem,
                                           std::size_t k, oklab::OkState& ok, oklab::XiProbe* probe = nullptr) {
-  (void)probe;
   detail::Binding* b = nullptr;
   okt_comm* c = detail::comm_for(ctx, &b);
   const std::int64_t t = model.t + 1;
@@ -194,6 +193,11 @@ inline oklab::StepOutcome oktopk_sgd_step(const oklab::WorkerCtx& ctx, oklab::Mo
   const std::size_t n = grad.size();
   if (n != problem.dim() || !grad.all_finite())
     throw oklab::NumericError("oktopk_sgd_step: non-finite or misshaped gradient");
+  if (probe != nullptr) {  // the accumulator as make_accumulator forms it (trainer.cpp:423-435, 471-474)
+    probe->acc = oklab::DenseGrad(n);
+    for (std::size_t i = 0; i < n; ++i) probe->acc[i] = residual.eps[i] + alpha * grad[i];
+    probe->grad = grad;
+  }
   // Residual and model to the device (fp32).
   std::vector<float> eps(residual.eps.values.begin(), residual.eps.values.end());
   std::vector<float> w(model.w.values.begin(), model.w.values.end()), gf(grad.values.begin(), grad.values.end());
