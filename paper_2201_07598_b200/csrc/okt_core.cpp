@@ -93,6 +93,7 @@ struct DevScalars {
   uint32_t flags;  // bit0 non-finite input, bit1 out-of-region entry, bit2 non-finite iterate,
                    // bit3 peer timeout, bit4 peer failure
   uint32_t pad1;
+  uint32_t pflags[2];  // the single-rank graph step's flag words, by step parity
   okt::P2PPlan plan;
   uint64_t cuts[OKT_MAX_WORLD + 1];
   uint64_t off[OKT_MAX_WORLD + 1];
@@ -215,6 +216,8 @@ struct okt_comm {
   // step block (DevScalars::sp) on the device.
   struct StepGraph {
     cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;     // kept: its kernel nodes hold the captured arguments
+    cudaGraphNode_t k1 = nullptr, cb = nullptr;  // K1 and phase B, updated every step
     size_t n = 0, k = 0;
     bool sgd = false, prof = false;
     uint64_t gen = 0, kernels = 0;
@@ -876,52 +879,67 @@ struct okt_comm {
                    bool sgd, cudaStream_t s) {
     int rc;
     StepGraph& G = graph1;
-    hup->sp.g = g;
-    hup->sp.eps_in = eps_in;
-    hup->sp.eps_out = eps_out;
-    hup->sp.w = w;
-    hup->sp.alpha = alpha;
-    hup->sp.epoch = ++p1_seq;
-    hup->sp.hflags = &hfast_dev->flags;
-    hup->sp.trace = trbuf.as<uint64_t>();
-    hup->flags = 0;
-    hfast->flags = 0;  // the kernels OR error bits into it
+    // The step's pointers, α and flag word are kernel arguments, rewritten in
+    // the instantiated graph every step (no H2D node); the flag word
+    // alternates by step parity and phase B clears the next one.
+    const uint64_t seq = ++p1_seq;
+    uint32_t* fl = &d()->pflags[seq & 1];
+    uint32_t* fl_next = &d()->pflags[(seq + 1) & 1];
+    okt::ApplyArgs ap;
+    ap.k7 = sgd;
+    ap.acc = sgd ? eps_out : nullptr;
+    ap.w = sgd ? w : nullptr;
+    ap.d_flags = fl;
+    ap.hout = hfast_dev;
+    ap.seq = seq;
+    ap.d_flags_next = fl_next;
+    ap.trace = trbuf.as<uint64_t>();
+    hfast->bad_iter = 0;
     if (!G.exec || G.n != n || G.k != k || G.sgd != sgd || G.gen != buf_gen || G.prof != prof) {
       if (G.exec) {
         cudaGraphExecDestroy(G.exec);
         G.exec = nullptr;
       }
+      if (G.graph) {
+        cudaGraphDestroy(G.graph);
+        G.graph = nullptr;
+      }
       if (!G.e0) {
         cudaEventCreate(&G.e0);
         cudaEventCreate(&G.e1);
       }
-      const okt::StepPtrs* dp = &d()->sp;
       const uint64_t l0 = L.launches;
       if ((rc = ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture"))) return rc;
-      // one H2D node: the step pointers and zeroed flags
-      cudaMemcpyAsync(&d()->sp, &hup->sp, offsetof(DevScalars, pad1) - offsetof(DevScalars, sp),
-                      cudaMemcpyHostToDevice, s);
       if (prof) cudaEventRecordWithFlags(G.e0, s, cudaEventRecordExternal);
-      okt::ApplyArgs ap;  // (acc / w of the fused K7 come from the step block)
-      ap.k7 = sgd;
-      ap.d_flags = &d()->flags;
-      ap.ind = dp;
-      ap.hout = hfast_dev;
-      ap.trace = trbuf.as<uint64_t>();
       cudaError_t e = okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, g, eps_in,
                                      eps_out, alpha, n, &d()->local_th, &d()->global_th,
                                      okt::OutCoo{nullptr, sur_idx.as<uint32_t>(), sur_val.as<double>()}, &d()->S,
-                                     &d()->m, &d()->flags, nullptr, &ap, nullptr, dp);
+                                     &d()->m, fl, nullptr, &ap, nullptr, nullptr);
       if (prof) cudaEventRecordWithFlags(G.e1, s, cudaEventRecordExternal);
-      // (no D2H node: phase B's last CTA writes m, S and the flags to hfast)
-      cudaGraph_t graph = nullptr;
-      const cudaError_t e2 = cudaStreamEndCapture(s, &graph);
+      // (no D2H node: phase B's CTA 0 writes m, S and the flags to hfast)
+      const cudaError_t e2 = cudaStreamEndCapture(s, &G.graph);
       if (e != cudaSuccess || e2 != cudaSuccess) {
-        if (graph) cudaGraphDestroy(graph);
+        if (G.graph) cudaGraphDestroy(G.graph);
+        G.graph = nullptr;
         return ck(e != cudaSuccess ? e : e2, "graph capture");
       }
-      e = cudaGraphInstantiate(&G.exec, graph, 0);
-      cudaGraphDestroy(graph);
+      // the two kernel nodes: phase B by its function, K1 the other one
+      size_t nn = 0;
+      cudaGraphGetNodes(G.graph, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      cudaGraphGetNodes(G.graph, nodes.data(), &nn);
+      G.k1 = G.cb = nullptr;
+      const void* cfunc = okt::compact_graph_kernel(sgd);
+      for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        cudaGraphNodeGetType(nd, &ty);
+        if (ty != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp{};
+        cudaGraphKernelNodeGetParams(nd, &kp);
+        (kp.func == cfunc ? G.cb : G.k1) = nd;
+      }
+      if (!G.k1 || !G.cb) return set_err(OKT_ERR_INTERNAL, "single-rank graph: kernel nodes not found");
+      e = cudaGraphInstantiate(&G.exec, G.graph, 0);
       if ((rc = ck(e, "graph instantiate"))) return rc;
       G.kernels = L.launches - l0;
       L.launches = l0;
@@ -932,6 +950,28 @@ struct okt_comm {
       G.sgd = sgd;
       G.gen = buf_gen;
       G.prof = prof;
+    } else {
+      // this step's arguments into the instantiated nodes: K1 (g, eps_in,
+      // eps_out, alpha, d_flags = arguments 0-3 and 12) and phase B
+      // (ApplyArgs = argument 14)
+      cudaKernelNodeParams kp{};
+      if ((rc = ck(cudaGraphKernelNodeGetParams(G.k1, &kp), "graph params"))) return rc;
+      void* a1[16];
+      for (int i = 0; i < 16; ++i) a1[i] = kp.kernelParams[i];
+      a1[0] = &g;
+      a1[1] = &eps_in;
+      a1[2] = &eps_out;
+      a1[3] = &alpha;
+      a1[12] = &fl;
+      kp.kernelParams = a1;
+      if ((rc = ck(cudaGraphExecKernelNodeSetParams(G.exec, G.k1, &kp), "graph params"))) return rc;
+      cudaKernelNodeParams cp{};
+      if ((rc = ck(cudaGraphKernelNodeGetParams(G.cb, &cp), "graph params"))) return rc;
+      void* a2[15];
+      for (int i = 0; i < 15; ++i) a2[i] = cp.kernelParams[i];
+      a2[14] = &ap;
+      cp.kernelParams = a2;
+      if ((rc = ck(cudaGraphExecKernelNodeSetParams(G.exec, G.cb, &cp), "graph params"))) return rc;
     }
     if ((rc = ck(cudaGraphLaunch(G.exec, s), "graph launch"))) return rc;
     L.launches += G.kernels;
@@ -953,7 +993,7 @@ struct okt_comm {
     if (o->seq != p1_seq) return set_err(OKT_ERR_INTERNAL, "single-rank step: no scalars from the device");
     h->m = o->m;
     h->S = o->S;
-    h->flags = o->flags;  // (bits 0 and 2: the only ones a single-rank step sets)
+    h->flags = o->flags | (o->bad_iter ? 4u : 0u);  // (bits 0 and 2: all a single-rank step sets)
     return OKT_OK;
   }
   bool graph_prof_pending = false;
@@ -1519,6 +1559,7 @@ int okt_comm_destroy(okt_comm* c) {
   if (c->hup) cudaFreeHost(c->hup);
   if (c->hfast) cudaFreeHost(c->hfast);
   if (c->graph1.exec) cudaGraphExecDestroy(c->graph1.exec);
+  if (c->graph1.graph) cudaGraphDestroy(c->graph1.graph);
   if (c->graph1.e0) {
     cudaEventDestroy(c->graph1.e0);
     cudaEventDestroy(c->graph1.e1);

@@ -93,7 +93,10 @@ __global__ void __launch_bounds__(kThreads)
     ap.w = ap.ind->w;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) trace_stamp(ap.trace, kTrCompact, 0);
+  if (tid == 0) {
+    trace_stamp(ap.trace, kTrCompact, 0);
+    if (blockIdx.x == 0 && ap.d_flags_next) *ap.d_flags_next = 0;  // (nobody uses it during this step)
+  }
   const uint32_t c0 = uint32_t(split_at(blockIdx.x, G, gridDim.x));
   const uint32_t c1 = uint32_t(split_at(blockIdx.x + 1, G, gridDim.x));
   const int nc = int(c1 - c0);
@@ -166,7 +169,8 @@ __global__ void __launch_bounds__(kThreads)
       if (ap.hout) {  // the step's scalars straight into mapped host memory (no D2H node)
         ap.hout->m = counts2 ? s2 : 0;
         ap.hout->S = pre;
-        ap.hout->seq = ap.ind->epoch;
+        ap.hout->flags = *reinterpret_cast<volatile uint32_t*>(ap.d_flags);  // (K1 has finished)
+        ap.hout->seq = ap.seq;
       }
     }
     pre = 0;
@@ -208,9 +212,14 @@ __global__ void __launch_bounds__(kThreads)
   }
   if (APPLY && __syncthreads_or(bad) && tid == 0) {
     atomicOr(ap.d_flags, 4u);
-    if (ap.hout) atomicOr_system(ap.ind->hflags, 4u);  // (error path only)
+    if (ap.hout) *reinterpret_cast<volatile uint32_t*>(&ap.hout->bad_iter) = 1u;  // (error path only)
   }
   if (lane == 0) trace_stamp(ap.trace, kTrCompact, 2);
+}
+
+const void* compact_graph_kernel(bool apply) {
+  return apply ? reinterpret_cast<const void*>(compact_kernel<1, true>)
+               : reinterpret_cast<const void*>(compact_kernel<1, false>);
 }
 
 // G chunks of `cap` entries (cap_host, or *d_cap when set); counts2: g2
@@ -435,7 +444,6 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
   }
   if (__syncthreads_or(bad) && tid == 0) {
     atomicOr(d_flags, 1u);
-    if (ind && ind->hflags) atomicOr_system(ind->hflags, 1u);  // (error path only)
   }
   if (HIST) {
     for (int i = tid; i < 2048; i += kThreads)

@@ -60,9 +60,10 @@ struct OutCoo {
 // writes the counts, and any CTA that detects an error ORs its bit into
 // flags (the host clears flags before each launch).
 struct HostOut {
-  uint64_t seq;  // StepPtrs::epoch of the step that wrote it
+  uint64_t seq;  // the step that wrote it (ApplyArgs::seq)
   uint64_t m, S;
-  uint32_t flags, pad;
+  uint32_t flags;     // K1's error bits of the step
+  uint32_t bad_iter;  // set by phase B on a non-finite model update (the host clears it)
 };
 
 struct ApplyArgs {
@@ -71,9 +72,13 @@ struct ApplyArgs {
   float* w = nullptr;     // model; w[i] -= u_i
   uint32_t* d_flags = nullptr;
   const StepPtrs* ind = nullptr;  // when set, acc / w come from here
-  HostOut* hout = nullptr;        // when set: the step's scalars go there (ind->hflags: its flags)
+  HostOut* hout = nullptr;        // when set: the step's scalars go there
+  uint64_t seq = 0;               // ... tagged with this step number
+  uint32_t* d_flags_next = nullptr;  // when set: CTA 0 clears the next graph step's flag word
   uint64_t* trace = nullptr;      // diagnostics (OKT_P2P_TRACE): per-CTA stamps, kind kTrCompact
 };
+// The single-rank graph's kernels, for per-step parameter updates.
+const void* compact_graph_kernel(bool apply);
 
 // Split-phase receive segments for the region scatter (M1): one per source.
 struct Segs {

@@ -37,7 +37,6 @@ struct StepPtrs {
   uint64_t epoch;  // P2P: flag value of this step; P = 1 graph: step sequence number
   int32_t par;     // P2P: parity slot of the window buffers
   int32_t pad2;
-  uint32_t* hflags;  // P = 1 graph: mapped host word the error bits are ORed into
   uint64_t* trace;   // diagnostics (OKT_P2P_TRACE): per-CTA stamps, or null
 };
 enum P2PFlag { kFlagLReady = 0, kFlagSurReady = 1, kFlagBlockReady = 2, kFlagBarrier = 3, kP2PFlagKinds = 4 };
