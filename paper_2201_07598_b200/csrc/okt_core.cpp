@@ -228,6 +228,10 @@ struct okt_comm {
   okt::HostOut* hfast = nullptr;      // mapped pinned: the steady P = 1 step's scalars
   okt::HostOut* hfast_dev = nullptr;  // its device address
   uint64_t p1_seq = 0;
+  okt::P2PHostOut* hp2p = nullptr;      // mapped pinned: the steady P2P EF step's results
+  okt::P2PHostOut* hp2p_dev = nullptr;
+  bool hp2p_pending = false;
+  uint64_t hp2p_epoch = 0;
   bool hfast_pending = false;
   DevScalars* hup = nullptr; // pinned upload staging
   size_t cap_n = 0;
@@ -771,7 +775,7 @@ struct okt_comm {
     kt.d_off = d()->off;
     if (!rc) rc = ck(cudaEventRecord(ev_fork, s), "fork");
     if (!rc) rc = ck(cudaStreamWaitEvent(side, ev_fork, 0), "fork");
-    if (!rc) rc = ck(okt::launch_p2p_totals(L, side, dt, sp, P, kt), "totals");
+    if (!rc) rc = ck(okt::launch_p2p_totals(L, side, dt, sp, P, kt, sgd ? hp2p_dev : nullptr), "totals");
     if (!rc) rc = ck(cudaEventRecord(ev_join, side), "join");
     tmark(OKT_T_MERGE, s);
     // split exchange + region merge in one kernel (reads every source's K1
@@ -786,7 +790,8 @@ struct okt_comm {
     // oktopk_sgd_step reports no index list (trainer.hpp:123-127): only the
     // plain allreduce needs the sel flags and the indexes compaction.
     pa.sel = sgd ? nullptr : selflags.as<uint8_t>();
-    if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, sp, &d()->S, dp, &d()->U, &d()->flags, kP2PTimeoutNs, pa),
+    if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, sp, &d()->S, dp, &d()->U, &d()->flags, kP2PTimeoutNs, pa,
+                                                sgd ? hp2p_dev : nullptr, S.tile_ctr + 4),
                      "p2p");
     if (!sgd) {
       tmark(OKT_T_APPLY, s);
@@ -795,7 +800,9 @@ struct okt_comm {
     }
     tstop(s);
     if (!rc) rc = ck(cudaStreamWaitEvent(s, ev_join, 0), "join");
-    if (!rc) rc = ck(cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s), "d2h");
+    // EF steps hand their results back through mapped host memory (hp2p); the
+    // plain allreduce (indexes, ...) reads the scalars back with one D2H
+    if (!rc && !sgd) rc = ck(cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s), "d2h");
     return rc;
   }
 
@@ -988,6 +995,24 @@ struct okt_comm {
   }
   // The scalars a steady single-rank graph step hands back through mapped
   // host memory (into the DevScalars mirror, where commit_step reads them).
+  // The results of a steady device-driven EF step, written by its kernels into
+  // mapped host memory (into the DevScalars mirror, where commit_step reads them).
+  int read_hp2p() {
+    if (!hp2p_pending) return OKT_OK;
+    hp2p_pending = false;
+    const volatile okt::P2PHostOut* o = hp2p;
+    if (o->seq_pull != hp2p_epoch || o->seq_tot != hp2p_epoch)
+      return set_err(OKT_ERR_INTERNAL, "device-driven step: no results from the device");
+    h->m = o->m;
+    h->U = o->U;
+    for (int q = 0; q <= P; ++q) h->off[q] = o->off[q];
+    for (int q = 0; q < P; ++q) {
+      h->plan.sizes[q] = o->sizes[q];
+      h->plan.seg_cnt[q] = o->seg_cnt[q];
+    }
+    h->flags = o->flags_early | (o->err_timeout ? 8u : 0u) | (o->err_peer ? 16u : 0u) | (o->err_iter ? 4u : 0u);
+    return OKT_OK;
+  }
   int read_hfast() {
     const volatile okt::HostOut* o = hfast;
     if (o->seq != p1_seq) return set_err(OKT_ERR_INTERNAL, "single-rank step: no scalars from the device");
@@ -1110,6 +1135,11 @@ struct okt_comm {
       sp.alpha = fa;
       sp.epoch = epoch;
       sp.par = par;
+      if (sgd) {  // the kernels set these on an error (the step's results come through hp2p)
+        hp2p->err_timeout = hp2p->err_peer = hp2p->err_iter = 0;
+        hp2p_pending = true;
+        hp2p_epoch = epoch;
+      }
       if ((rc = launch_p2p_step(n, k, sgd, s))) return abort_step(rc);
       if (prof) {
         cudaEvent_t e = ev_get();
@@ -1120,6 +1150,7 @@ struct okt_comm {
       p2p_credit_pending = true;
       if (defer_commit(n, t, thr, sgd, cuts, tab.u_idx[rank][par], tab.u_val[rank][par], s)) return OKT_OK;
       if ((rc = ck(cudaStreamSynchronize(s), "device"))) return abort_step(rc);
+      if ((rc = read_hp2p())) return abort_step(rc);
       tcollect();
       return commit_step(n, t, thr, sgd, cuts, tab.u_idx[rank][par], tab.u_val[rank][par], out);
     }
@@ -1280,6 +1311,7 @@ struct okt_comm {
       hfast_pending = false;
       if ((rc = read_hfast())) return abort_step(rc);
     }
+    if ((rc = read_hp2p())) return abort_step(rc);
     tcollect();
     collect_graph_prof();
     return commit_step(pending.n, pending.t, pending.thr, pending.sgd, pending.cuts, pending.ui, pending.uv, out);
@@ -1361,6 +1393,8 @@ struct okt_comm {
 
   int abort_step(int rc) {
     dev_stale = true;
+    hp2p_pending = false;
+    hfast_pending = false;
     cudaStreamSynchronize(L.s);
     cudaGetLastError();
     spans.clear();
@@ -1416,6 +1450,8 @@ int init_comm(okt_comm* c) {
   if (e == cudaSuccess) e = cudaMallocHost(&c->hup, sizeof(DevScalars));
   if (e == cudaSuccess) e = cudaHostAlloc(&c->hfast, sizeof(okt::HostOut), cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hfast_dev), c->hfast, 0);
+  if (e == cudaSuccess) e = cudaHostAlloc(&c->hp2p, sizeof(okt::P2PHostOut), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hp2p_dev), c->hp2p, 0);
   if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("init: ") + cudaGetErrorString(e));
   std::memset(c->h, 0, sizeof(DevScalars));
   std::memset(c->hup, 0, sizeof(DevScalars));
@@ -1558,6 +1594,7 @@ int okt_comm_destroy(okt_comm* c) {
   if (c->h) cudaFreeHost(c->h);
   if (c->hup) cudaFreeHost(c->hup);
   if (c->hfast) cudaFreeHost(c->hfast);
+  if (c->hp2p) cudaFreeHost(c->hp2p);
   if (c->graph1.exec) cudaGraphExecDestroy(c->graph1.exec);
   if (c->graph1.graph) cudaGraphDestroy(c->graph1.graph);
   if (c->graph1.e0) {

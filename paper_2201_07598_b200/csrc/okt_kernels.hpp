@@ -167,13 +167,13 @@ cudaError_t launch_p2p_merge(Launch& L, const PeerTab* d_tab, const StepPtrs* sp
 // Waits for every rank's survivors, plans (offsets / balance), pulls u.
 cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, uint64_t* d_S,
                                   P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns,
-                                  const P2PApply& ap);
+                                  const P2PApply& ap, P2PHostOut* hout, uint32_t* done);
 // Device barrier over the peer flags (okt_device_barrier).
 cudaError_t launch_p2p_barrier(Launch& L, const PeerTab* d_tab, uint64_t epoch, uint32_t* d_flags,
                                uint64_t timeout_ns);
 // This rank's selection size / slice offsets from K1's tile counts (side stream).
 cudaError_t launch_p2p_totals(Launch& L, cudaStream_t s, const PeerTab* d_tab, const StepPtrs* sp, int P,
-                              const K1Totals& totals);
+                              const K1Totals& totals, P2PHostOut* hout);
 // indexes = {u_idx[j] : sel[j]} in order (the K7 intersection, after a fused apply).
 cudaError_t launch_select_flags(Launch& L, const Stage& S, const uint8_t* sel, const PeerTab* d_tab,
                                 const StepPtrs* sp, const uint64_t* d_U, uint64_t bound, uint32_t* out,

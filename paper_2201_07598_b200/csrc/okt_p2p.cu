@@ -205,7 +205,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 // from their block owners' u.  K7 runs on each entry as it lands.
 __global__ void __launch_bounds__(kThreads)
     p2p_pull_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, uint64_t* d_S, P2PPlan* plan,
-                    uint64_t* d_U, int round, uint32_t* d_flags, uint64_t timeout_ns, P2PApply ap) {
+                    uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns, P2PApply ap, P2PHostOut* hout,
+                    uint32_t* done) {
+  __shared__ int s_last;
   __shared__ uint64_t s_size[kP2PMaxP], s_off[kP2PMaxP + 1], s_blk[kP2PMaxP + 1];
   __shared__ uint32_t s_G[kP2PMaxP], s_cap[kP2PMaxP], s_start[kP2PMaxP + 1];
   __shared__ int s_bal, s_abort;
@@ -216,13 +218,15 @@ __global__ void __launch_bounds__(kThreads)
   const int P = tab->P, me = tab->rank, q = threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t* const trace = tab->trace;
-  const int trk = round == 0 ? kTrPull0 : kTrPull1;
   if (q == 0) {
     s_abort = (*d_flags & (1u | 8u | 16u)) ? 1 : 0;
-    trace_stamp(trace, trk, 0);
+    trace_stamp(trace, kTrPull0, 0);
+    // done[par] counts this step's CTAs through the balanced hand-off; the
+    // previous step cleared it, this one clears the next step's
+    if (blockIdx.x == 0) done[par ^ 1] = 0;
   }
   __syncthreads();
-  if (round == 0) {
+  {
     // CTA 0 publishes this rank's survivors (every region-scan CTA finished
     // before this kernel started; the other CTAs only poll, so the system
     // fence is cheap): the exclusive prefix of the chunk counts (where each
@@ -282,6 +286,7 @@ __global__ void __launch_bounds__(kThreads)
       const FlagSlot* f = my_flag(tab->hdr[me], kFlagSurReady, q);
       if (!wait_flag(&f->epoch, epoch, timeout_ns)) {
         atomicOr(d_flags, 8u);
+        if (hout) hout->err_timeout = 1;
         s_abort = 1;
       } else {
         sz = flag_word(f, 1);
@@ -289,6 +294,7 @@ __global__ void __launch_bounds__(kThreads)
         cap = uint32_t(flag_word(f, 3));
         if (q != me && flag_word(f, 0)) {
           atomicOr(d_flags, 16u);
+          if (hout) hout->err_peer = 1;
           s_abort = 1;
         }
       }
@@ -327,42 +333,22 @@ __global__ void __launch_bounds__(kThreads)
         plan->total = total;
         plan->balanced = uint32_t(s_bal);
         *d_U = s_abort ? 0 : total;
+        if (hout) {  // the step's plan for the host's commit and ledger (mapped memory)
+          hout->U = s_abort ? 0 : total;
+          for (int r = 0; r < P; ++r) {
+            hout->sizes[r] = s_size[r];
+            hout->seg_cnt[r] = *reinterpret_cast<volatile uint64_t*>(&plan->seg_cnt[r]);  // (merge finished)
+          }
+          hout->flags_early = *reinterpret_cast<volatile uint32_t*>(d_flags);
+          hout->seq_pull = epoch;
+        }
       }
-    }
-  } else {
-    // round 1: the plan CTA 0 of round 0 stored
-    if (q <= P) {
-      s_off[q] = plan->off[q];
-      s_blk[q] = plan->block[q];
-    }
-    if (q < P) s_cap[q] = plan->sur_cap[q];
-    if (q == 0) {
-      s_bal = int(plan->balanced);
-      uint32_t items = 0;
-      for (int r = 0; r < P; ++r) {
-        s_start[r] = items;
-        items += plan->sur_G[r];
-      }
-      s_start[P] = items;
     }
   }
   __syncthreads();
-  if (q == 0) trace_stamp(trace, trk, 1);
+  if (q == 0) trace_stamp(trace, kTrPull0, 1);
   if (s_abort) return;
   const bool bal = s_bal != 0;
-  if (round == 1) {
-    if (!bal) return;
-    // balanced: CTA 0 publishes "my block of u is complete" (every round-0
-    // CTA finished before this kernel started); every CTA waits for every
-    // peer's block on its own flag copy
-    if (blockIdx.x == 0) publish_flag(tab->hdr, P, me, kFlagBlockReady, sp->epoch);
-    if (q < P && q != me && !wait_flag(&my_flag(tab->hdr[me], kFlagBlockReady, q)->epoch, sp->epoch, timeout_ns)) {
-      atomicOr(d_flags, 8u);
-      s_abort = 1;
-    }
-    __syncthreads();
-    if (s_abort) return;
-  }
   uint32_t* ui = tab->u_idx[me][par];
   double* uv = tab->u_val[me][par];
   const float tf = acc ? ceil_to_float(*ap.d_local_th) : 0.f;
@@ -397,7 +383,7 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
   };
-  if (round == 0) {
+  {
     const uint64_t a = bal ? s_blk[me] : 0, b = bal ? s_blk[me + 1] : s_off[P];
     // (rank, chunk, part) work items: every chunk split so all warps get a share
     const uint32_t items = s_start[P];
@@ -429,7 +415,31 @@ __global__ void __launch_bounds__(kThreads)
         land_batch(pos, ok, i, v);
       }
     }
-  } else {
+  }
+  if (bal) {
+    // Balanced: the other blocks come from their block owners' u once each
+    // owner's round 0 is complete.  The last CTA of my grid to finish round 0
+    // publishes "my block is complete" (a grid-wide hand-off through a
+    // per-parity counter: every CTA is resident, the grid is one wave);
+    // every CTA waits for every peer's block on its own flag copy.
+    __syncthreads();
+    if (q == 0) {
+      __threadfence();
+      s_last = atomicAdd(&done[par], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      publish_flag(tab->hdr, P, me, kFlagBlockReady, epoch);
+    }
+    if (q < P && q != me && !wait_flag(&my_flag(tab->hdr[me], kFlagBlockReady, q)->epoch, epoch, timeout_ns)) {
+      atomicOr(d_flags, 8u);
+      if (hout) hout->err_timeout = 1;
+      s_abort = 1;
+    }
+    __syncthreads();
+    if (s_abort) return;
+    if (q == 0) trace_stamp(trace, kTrPull1, 0);
     const uint64_t total = s_off[P];
     const uint64_t stride = uint64_t(gridDim.x) * kThreads;
     for (uint64_t pos = uint64_t(blockIdx.x) * kThreads + threadIdx.x; pos < total; pos += stride) {
@@ -442,15 +452,18 @@ __global__ void __launch_bounds__(kThreads)
       land_batch(pa, ok, i, v);
     }
   }
-  if (acc && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(d_flags, 4u);
-  if (lane == 0) trace_stamp(trace, trk, 2);
+  if (acc && __syncthreads_or(bad) && threadIdx.x == 0) {
+    atomicOr(d_flags, 4u);
+    if (hout) hout->err_iter = 1;
+  }
+  if (lane == 0) trace_stamp(trace, kTrPull0, 2);
 }
 
 // This rank's selection size and slice offsets from K1's per-tile counts (one
 // CTA per value: d < P the entries below cut d, d = P all), for the result and
 // the ledger.  Runs on a side stream, off the step's critical path.
 __global__ void __launch_bounds__(kThreads)
-    p2p_totals_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, K1Totals lt) {
+    p2p_totals_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, K1Totals lt, P2PHostOut* hout) {
   __shared__ uint64_t red[kWarps];
   const int P = tab->P, me = tab->rank, par = sp->par, d = blockIdx.x;
   const uint32_t G = tab->hdr[me]->pub[par].k1_G;
@@ -459,6 +472,13 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x == 0) {
     lt.d_off[d] = o;
     if (d == P) *lt.d_m = o;
+    if (hout) {
+      hout->off[d] = o;
+      if (d == P) {
+        hout->m = o;
+        hout->seq_tot = sp->epoch;
+      }
+    }
   }
 }
 
@@ -519,7 +539,7 @@ cudaError_t launch_p2p_merge(Launch& L, const PeerTab* d_tab, const StepPtrs* sp
 
 cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, uint64_t* d_S,
                                   P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns,
-                                  const P2PApply& ap) {
+                                  const P2PApply& ap, P2PHostOut* hout, uint32_t* done) {
   // one wave of as many CTAs as fit (every CTA waits on its own flag copy, so
   // the whole grid must be resident)
   static int caps[64] = {};
@@ -536,15 +556,14 @@ cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtr
     cap = std::max(1, std::min(per_sm, 4) * L.sms / grid_div());
   }
   const int grid = cap;
-  p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, d_S, plan, d_U, 0, d_flags, timeout_ns, ap);
-  p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, d_S, plan, d_U, 1, d_flags, timeout_ns, ap);
-  L.launches += 2;
+  p2p_pull_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, d_S, plan, d_U, d_flags, timeout_ns, ap, hout, done);
+  ++L.launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_p2p_totals(Launch& L, cudaStream_t s, const PeerTab* d_tab, const StepPtrs* sp, int P,
-                              const K1Totals& totals) {
-  p2p_totals_kernel<<<P + 1, kThreads, 0, s>>>(d_tab, sp, totals);
+                              const K1Totals& totals, P2PHostOut* hout) {
+  p2p_totals_kernel<<<P + 1, kThreads, 0, s>>>(d_tab, sp, totals, hout);
   ++L.launches;
   return cudaGetLastError();
 }

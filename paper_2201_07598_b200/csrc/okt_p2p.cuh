@@ -120,6 +120,20 @@ struct P2PApply {
   uint8_t* sel = nullptr;       // per u entry: 1 if in the local selection
 };
 
+// What the host reads after a steady device-driven EF step, written by the
+// kernels straight into mapped pinned memory (no D2H node).  The error words
+// are written (never cleared) by whichever CTA hits the error; the host clears
+// them before each launch.
+struct P2PHostOut {
+  uint64_t seq_pull, seq_tot;   // the step (epoch) that wrote each part
+  uint64_t U, m;
+  uint64_t sizes[kP2PMaxP];     // every rank's survivors (the balance plan's input)
+  uint64_t seg_cnt[kP2PMaxP];   // entries received from each source
+  uint64_t off[kP2PMaxP + 1];   // my selection's slice offsets per destination
+  uint32_t flags_early;         // K1 / merge error bits, as the pull saw them
+  uint32_t err_timeout, err_peer, err_iter;
+};
+
 // P2P mode of K1: its per-tile staging, counts and cut counts go straight into
 // this rank's window, where the peers' merge kernels read them in place.
 struct K1P2P {
