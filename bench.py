@@ -404,6 +404,10 @@ def run_okt(args):
         t += 1
         with torch.cuda.stream(stream):
             flush.fill_(i & 0xff)
+        if world > 1:
+            barrier()  # hosts and GPUs aligned before each timed call (outside the events)
+            L.okt_device_barrier(comm, ctypes.c_void_p(stream.cuda_stream))
+        with torch.cuda.stream(stream):
             e2e_ev[i][0].record(stream)
         rc = L.okt_sgd_step_host(comm, ctypes.c_void_p(hbuf[i % len(hbuf)].data_ptr()),
                                  ctypes.c_void_p(wmodel.data_ptr()), n, 1.0, t, k,
