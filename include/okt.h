@@ -57,7 +57,8 @@ typedef enum okt_status {
   OKT_ERR_CONFIG = 5,           /* ConfigError (non power-of-two P, P > 8) */
   OKT_ERR_CUDA = 6,             /* CUDA runtime failure */
   OKT_ERR_NCCL = 7,             /* NCCL failure */
-  OKT_ERR_INTERNAL = 8
+  OKT_ERR_INTERNAL = 8,
+  OKT_ERR_DECODE = 9            /* DecodeError: a malformed wire image */
 } okt_status;
 
 /* Ledger phases, numbered as oklab::Phase (include/oklab/transport.hpp:15-22). */
@@ -289,6 +290,18 @@ int okt_kernel_launches(const okt_comm* comm, uint64_t* out);
  * when the comm was created with OKT_P2P_TRACE in the environment (else
  * OKT_ERR_CONFIG). */
 int okt_debug_p2p_trace(okt_comm* comm, uint64_t* out, size_t n_words);
+
+/* ---- COO wire codec (proj/core/src/sparse.cpp:275-312) ----------------------
+ * The reference's wire image of a SparseGrad: [nnz u32][indices u32 x nnz]
+ * [values f32 x nnz], little endian, 4 + 8 nnz bytes.  Device buffers, on the
+ * current device; d_out / d_in 4-byte aligned.  Encode rounds each fp64 value
+ * to fp32 (round to nearest).  Decode checks what wire_decode checks — header
+ * present, length 4 + 8 nnz, every index < n and strictly increasing — and
+ * returns OKT_ERR_DECODE otherwise (also when nnz > cap); *nnz_out is set on
+ * success. */
+int okt_wire_encode(const uint32_t* d_idx, const double* d_val, size_t nnz, void* d_out, void* stream);
+int okt_wire_decode(const void* d_in, size_t bytes, size_t n, uint32_t* d_idx, double* d_val, size_t cap,
+                    size_t* nnz_out, void* stream);
 
 /* ---- seeded input generators (bit-exact ports of the reference's rng.hpp
  * streams, rounded to fp32; not on the hot path) ---------------------------- */

@@ -548,3 +548,46 @@ int orc_sgd_step(int P, orc_state* st, const double* const* grad, double* const*
       if (!isfinite(w[r][i])) return -2;
   return 0;
 }
+
+/* ---- COO wire codec (sparse.cpp:260-312) ---------------------------------- */
+static void put_u32(uint8_t* o, uint32_t w) { /* put_u32, sparse.cpp:260-265 */
+  o[0] = (uint8_t)(w & 0xff);
+  o[1] = (uint8_t)((w >> 8) & 0xff);
+  o[2] = (uint8_t)((w >> 16) & 0xff);
+  o[3] = (uint8_t)((w >> 24) & 0xff);
+}
+static uint32_t get_u32(const uint8_t* b) { /* get_u32, sparse.cpp:267-272 */
+  return (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+}
+
+void orc_wire_encode(const uint32_t* idx, const double* val, size_t nnz, uint8_t* out) { /* sparse.cpp:276-285 */
+  put_u32(out, (uint32_t)nnz);
+  for (size_t i = 0; i < nnz; ++i) put_u32(out + 4 + 4 * i, idx[i]);
+  for (size_t i = 0; i < nnz; ++i) {
+    const float f = (float)val[i];
+    uint32_t w;
+    memcpy(&w, &f, 4);
+    put_u32(out + 4 + 4 * nnz + 4 * i, w);
+  }
+}
+
+int orc_wire_decode(const uint8_t* in, size_t bytes, size_t n, uint32_t* idx, double* val, size_t* nnz_out) {
+  /* sparse.cpp:287-310 */
+  if (bytes < 4) return 1;
+  const uint32_t nnz = get_u32(in);
+  if (bytes != 4 + (size_t)8 * nnz) return 1;
+  for (uint32_t i = 0; i < nnz; ++i) {
+    const uint32_t v = get_u32(in + 4 + 4 * (size_t)i);
+    if (v >= n) return 1;
+    if (i > 0 && v <= idx[i - 1]) return 1;
+    idx[i] = v;
+  }
+  for (uint32_t i = 0; i < nnz; ++i) {
+    const uint32_t w = get_u32(in + 4 + 4 * (size_t)nnz + 4 * (size_t)i);
+    float f;
+    memcpy(&f, &w, 4);
+    val[i] = (double)f;
+  }
+  *nnz_out = nnz;
+  return 0;
+}

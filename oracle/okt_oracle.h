@@ -85,6 +85,14 @@ int orc_sgd_step(int P, orc_state* st, const double* const* grad, double* const*
                  size_t n, double alpha, int64_t t, size_t k, orc_counters* ledger, uint32_t* u_idx,
                  double* u_val, size_t* U);
 
+/* COO wire codec (proj/core/src/sparse.cpp:275-312): [nnz u32][indices u32 *
+ * nnz][values f32 * nnz], little endian.  encode writes 4 + 8 nnz bytes;
+ * decode returns 0, or 1 for a malformed buffer (the reference's DecodeError):
+ * short header, length not 4 + 8 nnz, an index >= n, indices not strictly
+ * increasing. */
+void orc_wire_encode(const uint32_t* idx, const double* val, size_t nnz, uint8_t* out);
+int orc_wire_decode(const uint8_t* in, size_t bytes, size_t n, uint32_t* idx, double* val, size_t* nnz);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,7 +4,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
-from ctypes import (POINTER, Structure, c_char_p, c_double, c_int, c_int32, c_int64,
+from ctypes import (POINTER, Structure, c_char_p, c_double, c_int, c_int32, c_int64, c_uint8,
                     c_size_t, c_uint32, c_uint64, c_void_p)
 from typing import List, Sequence
 
@@ -64,6 +64,31 @@ def _ptrs(arrs, ctype):
 class _Common:
     """Shared ok_sparse_allreduce driver for the restatement and the reference."""
     _fn_allreduce = None
+    _fn_wire_enc = None
+    _fn_wire_dec = None
+
+    def wire_encode(self, idx: np.ndarray, val: np.ndarray) -> bytes:
+        """wire_encode (sparse.cpp:275-285): [nnz u32][idx u32][f32 values]."""
+        idx = np.ascontiguousarray(idx, dtype=np.uint32)
+        val = np.ascontiguousarray(val, dtype=np.float64)
+        out = np.zeros(4 + 8 * idx.size, np.uint8)
+        getattr(self.L, self._fn_wire_enc)(*self._wire_enc_args(idx, val, out))
+        return out.tobytes()
+
+    def wire_decode(self, b: bytes, n: int):
+        """wire_decode (sparse.cpp:287-310): (indices, values), or None for a
+        malformed image (DecodeError)."""
+        buf = np.frombuffer(b, np.uint8).copy() if len(b) else np.zeros(1, np.uint8)
+        cap = max(1, len(b) // 4)
+        idx = np.zeros(cap, np.uint32)
+        val = np.zeros(cap, np.float64)
+        nnz = c_size_t(0)
+        rc = getattr(self.L, self._fn_wire_dec)(buf.ctypes.data_as(POINTER(c_uint8)), c_size_t(len(b)), c_size_t(n),
+                                                 idx.ctypes.data_as(POINTER(c_uint32)),
+                                                 val.ctypes.data_as(POINTER(c_double)), ctypes.byref(nnz))
+        if rc:
+            return None
+        return idx[:nnz.value].copy(), val[:nnz.value].copy()
 
     def ok_sparse_allreduce(self, inputs: Sequence[np.ndarray], states: Sequence[OrcState], t: int, k: int,
                             ledger: np.ndarray = None):
@@ -98,6 +123,11 @@ class _Common:
 class Oracle(_Common):
     """The plain-C restatement (okt_oracle.c)."""
 
+    @staticmethod
+    def _wire_enc_args(idx, val, out):
+        return (idx.ctypes.data_as(POINTER(c_uint32)), val.ctypes.data_as(POINTER(c_double)), c_size_t(idx.size),
+                out.ctypes.data_as(POINTER(c_uint8)))
+
     def __init__(self, path: str = ORC_PATH):
         if not os.path.exists(path):
             build()
@@ -119,6 +149,12 @@ class Oracle(_Common):
         L.orc_drift.argtypes = [c_int64, c_uint64, c_size_t, c_uint64, c_int, POINTER(c_double)]
         L.orc_equal_slice_ends.restype = None
         L.orc_equal_slice_ends.argtypes = [c_uint64, c_int, POINTER(c_uint64)]
+        L.orc_wire_encode.restype = None
+        L.orc_wire_encode.argtypes = [POINTER(c_uint32), POINTER(c_double), c_size_t, POINTER(c_uint8)]
+        L.orc_wire_decode.restype = c_int
+        L.orc_wire_decode.argtypes = [POINTER(c_uint8), c_size_t, c_size_t, POINTER(c_uint32), POINTER(c_double),
+                                      POINTER(c_size_t)]
+        self._fn_wire_enc, self._fn_wire_dec = "orc_wire_encode", "orc_wire_decode"
 
     def _call(self, P, g, n, t, k, st, led, u_idx, u_val, U, ix, nix, sel):
         return self.L.orc_ok_sparse_allreduce(
@@ -215,6 +251,12 @@ class Oracle(_Common):
 class Reference(_Common):
     """The reference implementation itself (oracle/_ref/libokref.so)."""
 
+    @staticmethod
+    def _wire_enc_args(idx, val, out):
+        n = int(idx.max()) + 1 if idx.size else 1
+        return (idx.ctypes.data_as(POINTER(c_uint32)), val.ctypes.data_as(POINTER(c_double)), c_size_t(idx.size),
+                c_size_t(n), out.ctypes.data_as(POINTER(c_uint8)))
+
     def __init__(self, path: str = REF_PATH):
         if not os.path.exists(path):
             raise FileNotFoundError(f"{path} not built (needs /root/reference at build time)")
@@ -225,6 +267,12 @@ class Reference(_Common):
         L.okref_th_re_evaluate_dense.argtypes = [POINTER(c_double), c_size_t, c_size_t]
         L.okref_drift_f32.restype = None
         L.okref_drift_f32.argtypes = [c_int64, c_uint64, c_size_t, c_uint64, POINTER(c_double)]
+        L.okref_wire_encode.restype = c_int
+        L.okref_wire_encode.argtypes = [POINTER(c_uint32), POINTER(c_double), c_size_t, c_size_t, POINTER(c_uint8)]
+        L.okref_wire_decode.restype = c_int
+        L.okref_wire_decode.argtypes = [POINTER(c_uint8), c_size_t, c_size_t, POINTER(c_uint32), POINTER(c_double),
+                                        POINTER(c_size_t)]
+        self._fn_wire_enc, self._fn_wire_dec = "okref_wire_encode", "okref_wire_decode"
         L.okref_bench_sgd.restype = c_int
         L.okref_bench_sgd.argtypes = [c_int, c_size_t, c_size_t, c_int, c_int, c_uint32, c_uint32, c_uint32,
                                       c_double, c_uint64, c_int, POINTER(c_double), c_char_p, c_size_t]

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <span>
 #include <thread>
 #include <vector>
 
@@ -255,6 +256,27 @@ int okref_bench_sgd(int P, size_t n, size_t k, int warmup, int iters, uint32_t t
   for (int i = 0; i < iters; ++i)
     ms[i] = std::chrono::duration<double, std::milli>(t1[warmup + i] - t0[warmup + i]).count();
   return 0;
+}
+
+// The reference's COO wire codec (sparse.cpp:275-312) on flat buffers.
+int okref_wire_encode(const uint32_t* idx, const double* val, size_t nnz, size_t n, uint8_t* out) {
+  oklab::SparseGrad sg(n);
+  sg.indices.assign(idx, idx + nnz);
+  sg.values.assign(val, val + nnz);
+  const std::vector<std::uint8_t> b = oklab::wire_encode(sg);
+  std::memcpy(out, b.data(), b.size());
+  return 0;
+}
+int okref_wire_decode(const uint8_t* in, size_t bytes, size_t n, uint32_t* idx, double* val, size_t* nnz) {
+  try {
+    const oklab::SparseGrad sg = oklab::wire_decode(std::span<const std::uint8_t>(in, bytes), n);
+    std::copy(sg.indices.begin(), sg.indices.end(), idx);
+    std::copy(sg.values.begin(), sg.values.end(), val);
+    *nnz = sg.nnz();
+    return 0;
+  } catch (const oklab::DecodeError&) {
+    return 1;
+  }
 }
 
 }  // extern "C"

@@ -34,7 +34,7 @@ EXPORTS = (
     "okt_select_by_threshold", "okt_space_repartition",
     "okt_split_and_reduce", "okt_balance_and_allgatherv",
     "okt_set_profiling", "okt_phase_times", "okt_phase_bytes", "okt_reset_phase_times",
-    "okt_kernel_launches", "okt_debug_p2p_trace", "okt_gen_random_dense", "okt_gen_drift",
+    "okt_kernel_launches", "okt_debug_p2p_trace", "okt_wire_encode", "okt_wire_decode", "okt_gen_random_dense", "okt_gen_drift",
     "okt_plan_cuts", "okt_plan_balance", "okt_plan_ledger",
 )
 
@@ -141,6 +141,9 @@ def lib() -> ctypes.CDLL:
         "okt_phase_bytes": (c_int, [c_void_p, P(c_double)]),
         "okt_reset_phase_times": (c_int, [c_void_p]),
         "okt_kernel_launches": (c_int, [c_void_p, P(c_uint64)]),
+        "okt_wire_encode": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
+        "okt_wire_decode": (c_int, [c_void_p, c_size_t, c_size_t, c_void_p, c_void_p, c_size_t, P(c_size_t),
+                                    c_void_p]),
         "okt_debug_p2p_trace": (c_int, [c_void_p, P(c_uint64), c_size_t]),
         "okt_gen_random_dense": (c_int, [c_void_p, c_size_t, c_uint64, c_void_p]),
         "okt_gen_drift": (c_int, [c_void_p, c_size_t, c_int64, c_uint64, c_uint64, c_int,

@@ -2112,4 +2112,53 @@ int okt_debug_p2p_trace(okt_comm* c, uint64_t* out, size_t n_words) {
   return OKT_OK;
 }
 
+// ---- COO wire codec ------------------------------------------------------------
+int okt_wire_encode(const uint32_t* d_idx, const double* d_val, size_t nnz, void* d_out, void* stream) {
+  if (!d_out || (nnz && (!d_idx || !d_val))) return set_err(OKT_ERR_INVALID_ARGUMENT, "wire_encode: null buffer");
+  if (reinterpret_cast<uintptr_t>(d_out) & 3u) return set_err(OKT_ERR_INVALID_ARGUMENT, "wire_encode: unaligned image");
+  if (nnz > 0xffffffffull) return set_err(OKT_ERR_INVALID_ARGUMENT, "wire_encode: nnz does not fit the u32 header");
+  okt::Launch L;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&L.sms, cudaDevAttrMultiProcessorCount, dev);
+  L.s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = okt::launch_wire_encode(L, d_idx, d_val, nnz, static_cast<uint32_t*>(d_out));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L.s);
+  if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("wire_encode: ") + cudaGetErrorString(e));
+  return OKT_OK;
+}
+
+int okt_wire_decode(const void* d_in, size_t bytes, size_t n, uint32_t* d_idx, double* d_val, size_t cap,
+                    size_t* nnz_out, void* stream) {
+  if (!d_in || !nnz_out) return set_err(OKT_ERR_INVALID_ARGUMENT, "wire_decode: null buffer");
+  if (reinterpret_cast<uintptr_t>(d_in) & 3u) return set_err(OKT_ERR_INVALID_ARGUMENT, "wire_decode: unaligned image");
+  if (bytes < 4) return set_err(OKT_ERR_DECODE, "wire_decode: missing header");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t nnz = 0;
+  cudaError_t e = cudaMemcpyAsync(&nnz, d_in, 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("wire_decode: ") + cudaGetErrorString(e));
+  if (bytes != 4 + 8 * size_t(nnz)) return set_err(OKT_ERR_DECODE, "wire_decode: buffer length does not match nnz header");
+  if (nnz > cap || (nnz && (!d_idx || !d_val)))
+    return set_err(OKT_ERR_DECODE, "wire_decode: output capacity below nnz");
+  okt::Launch L;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&L.sms, cudaDevAttrMultiProcessorCount, dev);
+  L.s = s;
+  uint32_t* d_err = nullptr;
+  e = cudaMallocAsync(reinterpret_cast<void**>(&d_err), 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0, 4, s);
+  if (e == cudaSuccess && nnz)
+    e = okt::launch_wire_decode(L, static_cast<const uint32_t*>(d_in), nnz, n, d_idx, d_val, d_err);
+  uint32_t err = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&err, d_err, 4, cudaMemcpyDeviceToHost, s);
+  if (d_err) cudaFreeAsync(d_err, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("wire_decode: ") + cudaGetErrorString(e));
+  if (err) return set_err(OKT_ERR_DECODE, "wire_decode: index out of range or not strictly increasing");
+  *nnz_out = nnz;
+  return OKT_OK;
+}
+
 }  // extern "C"

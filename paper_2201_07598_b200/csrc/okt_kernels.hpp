@@ -179,4 +179,9 @@ cudaError_t launch_select_flags(Launch& L, const Stage& S, const uint8_t* sel, c
                                 const StepPtrs* sp, const uint64_t* d_U, uint64_t bound, uint32_t* out,
                                 uint64_t* d_count, const uint32_t* d_flags);
 
+// COO wire codec (okt_wire.cu): out / in are the image as u32 words.
+cudaError_t launch_wire_encode(Launch& L, const uint32_t* idx, const double* val, uint64_t nnz, uint32_t* out);
+cudaError_t launch_wire_decode(Launch& L, const uint32_t* in, uint64_t nnz, uint64_t n, uint32_t* idx, double* val,
+                               uint32_t* err);
+
 }  // namespace okt

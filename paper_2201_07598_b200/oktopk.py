@@ -60,7 +60,7 @@ class CudaError(OkError):
 
 
 _ERRORS = {1: InvalidArgument, 2: NumericError, 3: ProtocolError, 4: TransportError,
-           5: ConfigError, 6: CudaError, 7: CudaError, 8: OkError}
+           5: ConfigError, 6: CudaError, 7: CudaError, 8: OkError, 9: DecodeError}
 
 
 def _check(rc: int) -> None:
@@ -398,6 +398,38 @@ def balance_and_allgatherv(ctx: WorkerCtx, region: SparseGrad, global_th: float)
                                                  ctypes.c_void_p(val.data_ptr()), region.nnz(), region.n,
                                                  float(global_th), ctypes.byref(u), None))
     return _sparse_from(u, region.n)
+
+
+def wire_encode(s: SparseGrad, device: int = 0) -> bytes:
+    """oklab::wire_encode (sparse.hpp:126, sparse.cpp:275-285) on the device:
+    [nnz u32][indices u32 x nnz][values f32 x nnz], little endian."""
+    import torch
+    nnz = s.nnz()
+    idx = torch.from_numpy(np.ascontiguousarray(s.indices, dtype=np.uint32).view(np.int32)).to(f"cuda:{device}")
+    val = torch.from_numpy(np.ascontiguousarray(s.values, dtype=np.float64)).to(f"cuda:{device}")
+    out = torch.empty(1 + 2 * nnz, dtype=torch.int32, device=f"cuda:{device}")
+    with torch.cuda.device(device):
+        _check(_lib.lib().okt_wire_encode(ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(val.data_ptr()), nnz,
+                                          ctypes.c_void_p(out.data_ptr()), None))
+    return out.cpu().numpy().view(np.uint8).tobytes()
+
+
+def wire_decode(b: bytes, n: int, device: int = 0) -> SparseGrad:
+    """oklab::wire_decode (sparse.hpp:131, sparse.cpp:287-310) on the device;
+    a malformed image raises DecodeError."""
+    import torch
+    raw = np.frombuffer(bytes(b) + b"\0" * (-len(b) % 4), np.uint8).view(np.int32)
+    img = torch.from_numpy(raw.copy()).to(f"cuda:{device}") if raw.size else torch.zeros(1, dtype=torch.int32,
+                                                                                            device=f"cuda:{device}")
+    cap = max(1, (len(b) - 4) // 8) if len(b) >= 4 else 1
+    idx = torch.empty(cap, dtype=torch.int32, device=f"cuda:{device}")
+    val = torch.empty(cap, dtype=torch.float64, device=f"cuda:{device}")
+    nnz = ctypes.c_size_t(0)
+    with torch.cuda.device(device):
+        _check(_lib.lib().okt_wire_decode(ctypes.c_void_p(img.data_ptr()), len(b), n, ctypes.c_void_p(idx.data_ptr()),
+                                          ctypes.c_void_p(val.data_ptr()), cap, ctypes.byref(nnz), None))
+    m = nnz.value
+    return SparseGrad(n, idx[:m].cpu().numpy().view(np.uint32).copy(), val[:m].cpu().numpy().copy())
 
 
 def ok_sparse_allreduce(ctx: WorkerCtx, state: OkState, g, t: int, k: int) -> OkAllreduceResult:
