@@ -1,19 +1,19 @@
 // okt_p2p.cu — kernels of the device-driven multi-GPU exchange (okt_p2p.cuh).
 //
 // Steady Ok-Topk iteration on P ranks, no host round trip and no compaction
-// pass between a producer and its consumers:
-//   K1 (per-tile staging + per-tile cut counts in the window; its last CTA
-//     publishes L-ready)
-//   scatter: my own tiles first; CTA 0 waits for every peer's L-ready and
-//     releases the other CTAs; then every peer's tiles, read in place over
-//     NVLink -> bracket scan / survivor filter, chunked into the window (its
-//     last CTA writes the chunk prefix and publishes survivors-ready)
-//   pull: CTA 0 waits for every rank's survivors, plans (offsets, balance),
-//     releases the others; every chunk is pulled to its position in u,
-//     applying K7 on the way [balanced: my block, block sync, the others].
-// Every publish is issued by a CTA running alone at the end of its kernel: a
-// system fence issued while the rest of the grid still streams waits for that
-// traffic to drain.
+// pass between a producer and its consumers (one CUDA graph):
+//   K1 (per-tile staging + per-tile cut counts in the window)
+//   merge: CTA 0 publishes L-ready; every CTA waits on its own flag copy, reads
+//     every source's K1 tiles of its region in place (NVLink) and runs the
+//     bracket scan / survivor filter in shared memory; survivors chunked into
+//     the window
+//   pull: CTA 0 publishes the survivor prefix and count; every CTA waits, plans
+//     (offsets, balance) and pulls every chunk to its position in u, applying
+//     K7 on the way [balanced: my block, an in-grid hand-off, the others]
+//   totals (side branch): selection size and slice offsets
+// Every publish is issued at a kernel start, while the rest of the grid only
+// polls: a system fence issued while the grid streams random stores waits for
+// that traffic to drain (tools/fence_lat.cu, tools/p2p_noise.cu).
 #include "okt_device.cuh"
 #include "okt_kernels.hpp"
 #include "okt_p2p.cuh"
@@ -197,12 +197,12 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (lane == 0) trace_stamp(trace, kTrMerge, 2);
 }
 
-// Allgatherv by pulling.  round 0: CTA 0 waits for every rank's survivors and
+// Allgatherv by pulling.  Every CTA waits for every rank's survivors and
 // derives the plan of balance_and_allgatherv (oktopk.cpp:172-231; identical on
-// all ranks), then one warp per (rank, chunk, part) copies survivors
-// from the owner's window to their stream position in my u (unbalanced: all
-// of u; balanced: my block).  round 1 (balanced only) pulls the other blocks
-// from their block owners' u.  K7 runs on each entry as it lands.
+// all ranks), then one warp per (rank, chunk, part) copies survivors from the
+// owner's window to their stream position in my u (unbalanced: all of u;
+// balanced: my block, then — after every owner's block is complete — the
+// other blocks from their owners' u).  K7 runs on each entry as it lands.
 __global__ void __launch_bounds__(kThreads)
     p2p_pull_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, uint64_t* d_S, P2PPlan* plan,
                     uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns, P2PApply ap, P2PHostOut* hout,
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kThreads)
       if (q == 0) trace_stamp(trace, kTrPubSur, 3);
     }
     // every CTA: wait on its own flag copies, read the ranks' survivor counts
-    // and geometry, derive the plan (CTA 0 also stores it for round 1 / host)
+    // and geometry, derive the plan (CTA 0 also stores it for the host)
     if (q < P) {
       uint64_t sz = 0;
       uint32_t G = 0, cap = 0;

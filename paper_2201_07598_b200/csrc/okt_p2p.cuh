@@ -8,10 +8,10 @@
 //            stores flag[kind][copy][me].epoch into every peer's window header;
 //   wait     the consumer spins (ld.acquire.sys, bounded by a timeout) on its
 //            own header until every peer's flag reached the epoch, then reads
-//            the peers' published words remotely.
+//            the payload that came with it from the same slot.
 // Bulk data never moves through a staging copy: the consumer's kernels read
-// the producer's buffers in place over NVLink (pull model), e.g. the region
-// scatter reads each source's COO slice straight out of that source's HBM.
+// the producer's buffers in place over NVLink (pull model), e.g. the merge
+// reads each source's K1 tiles straight out of that source's HBM.
 // Buffers a peer may still read are double-buffered by step parity; a rank can
 // only run one step ahead of a peer (each step waits on every peer), so a
 // parity slot is never rewritten while someone reads it.
