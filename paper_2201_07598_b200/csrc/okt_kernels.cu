@@ -19,6 +19,7 @@
 #include "okt_kernels.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 
 namespace okt {
@@ -231,13 +232,13 @@ static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_
                                   const ApplyArgs* ap = nullptr) {
   // one chunk per CTA while the grid fits one wave, then groups of up to
   // kThreads chunks
-  static int cap_a = 0, cap_p = 0;
+  static std::atomic<int> cap_a{0}, cap_p{0};  // (resident CTAs; benign concurrent first use)
   const bool apply = ap && ap->k7;
-  int& cap = apply ? cap_a : cap_p;
+  std::atomic<int>& cap = apply ? cap_a : cap_p;
   if (!cap)
     cap = apply ? resident_ctas(compact_kernel<MODE, true>, kThreads, L.sms)
                 : resident_ctas(compact_kernel<MODE, false>, kThreads, L.sms);
-  const uint32_t slots = uint32_t(std::min(cap, S.max_chunks));
+  const uint32_t slots = uint32_t(std::min(cap.load(), S.max_chunks));
   const uint32_t per = std::min<uint32_t>(kThreads, std::max<uint32_t>(1, (G + slots - 1) / slots));
   const uint32_t GB = std::max<uint32_t>(1, (G + per - 1) / per);
   const uint32_t* c2 = g2 ? S.counts2 : nullptr;
@@ -479,8 +480,8 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
   constexpr int TILE = kJ * 4 * kThreads;
   const uint64_t tiles = (n + TILE - 1) / TILE;
   auto kern = vec ? k1_kernel<ACCUM, SELECT, HIST, true, DUAL> : k1_kernel<ACCUM, SELECT, HIST, false, DUAL>;
-  static int cap_v = 0, cap_s = 0;
-  int& cap = vec ? cap_v : cap_s;
+  static std::atomic<int> cap_v{0}, cap_s{0};
+  std::atomic<int>& cap = vec ? cap_v : cap_s;
   if (!cap) cap = resident_ctas(kern, kThreads, L.sms);
   const uint32_t G = chunks_for(tiles, cap, S.max_chunks);  // persistent CTAs
   if (tiles > S.max_tiles) return cudaErrorInvalidValue;         // counts / staging capacity
@@ -593,8 +594,8 @@ __global__ void __launch_bounds__(kThreads)
 cudaError_t launch_filter(Launch& L, const Stage& S, bool aos, const uint64_t* in_aos, const uint32_t* in_idx,
                           const double* in_val, const uint64_t* d_cnt_in, uint64_t bound, const double* d_th,
                           uint32_t* out_idx, double* out_val, uint64_t* d_cnt_out, const ApplyArgs* ap) {
-  static int cap_a = 0, cap_s = 0;
-  int& cap = aos ? cap_a : cap_s;
+  static std::atomic<int> cap_a{0}, cap_s{0};
+  std::atomic<int>& cap = aos ? cap_a : cap_s;
   if (!cap) cap = aos ? resident_ctas(filter_kernel<true>, kThreads, L.sms)
                       : resident_ctas(filter_kernel<false>, kThreads, L.sms);
   const uint32_t G = chunks_for((bound + kTileK - 1) / kTileK, cap, S.max_chunks);
@@ -678,7 +679,7 @@ __global__ void __launch_bounds__(kThreads)
 cudaError_t launch_apply(Launch& L, const Stage& S, const uint32_t* u_idx, const double* u_val, const uint64_t* d_U,
                          uint64_t bound, float* acc, bool zero_eps, float* w, int P, const double* d_local_th,
                          uint32_t* out_indexes, uint64_t* d_nidx, uint32_t* d_flags) {
-  static int cap = 0;
+  static std::atomic<int> cap{0};
   if (!cap) cap = resident_ctas(apply_kernel, kThreads, L.sms);
   const uint32_t G = chunks_for((bound + kTileK - 1) / kTileK, cap, S.max_chunks);
   apply_kernel<<<G, kThreads, 0, L.s>>>(u_idx, u_val, d_U, acc, zero_eps ? 1 : 0, w, P, d_local_th, S.sidx, S.counts,
@@ -727,7 +728,7 @@ __global__ void __launch_bounds__(kThreads)
 cudaError_t launch_select_flags(Launch& L, const Stage& S, const uint8_t* sel, const PeerTab* d_tab,
                                 const StepPtrs* sp, const uint64_t* d_U, uint64_t bound, uint32_t* out,
                                 uint64_t* d_count, const uint32_t* d_flags) {
-  static int cap = 0;
+  static std::atomic<int> cap{0};
   if (!cap) cap = resident_ctas(select_flags_kernel, kThreads, L.sms);
   const uint32_t G = chunks_for((bound + kTileK - 1) / kTileK, cap, S.max_chunks);
   select_flags_kernel<<<G, kThreads, 0, L.s>>>(sel, d_tab, sp, d_U, d_flags, S.sidx, S.counts, S.chunk_cap);
@@ -956,7 +957,7 @@ static cudaError_t region_scan_dispatch(Launch& L, const Stage& S, uint64_t lo, 
                                         double* out_val, uint64_t* d_count) {
   constexpr int TILE = kRegionTile;
   const uint64_t tiles = (W + TILE - 1) / TILE;
-  static int cap = 0;
+  static std::atomic<int> cap{0};
   if (!cap) cap = resident_ctas(region_scan_kernel<P, FILTER>, kThreads, L.sms);
   const uint32_t G = chunks_for(tiles, cap, S.max_chunks);
   if (uint64_t(tiles) * G > 0xffffffffull) return cudaErrorInvalidValue;  // split_at32's range

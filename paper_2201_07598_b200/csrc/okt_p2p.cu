@@ -19,6 +19,7 @@
 #include "okt_p2p.cuh"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 namespace okt {
@@ -505,10 +506,10 @@ static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtr
                                   uint64_t timeout_ns) {
   constexpr size_t smem = size_t(kMergeTile) + size_t(P) * kMergeTile * sizeof(float);
   // the dynamic shared memory opt-in is per device
-  static int caps[64] = {};
+  static std::atomic<int> caps[64];  // per device (the dynamic-smem opt-in is per device)
   int dev = 0;
   cudaGetDevice(&dev);
-  int& cap = caps[dev & 63];
+  std::atomic<int>& cap = caps[dev & 63];
   if (!cap) {
     cudaFuncSetAttribute(p2p_merge_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per_sm = 0;
@@ -542,10 +543,10 @@ cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtr
                                   const P2PApply& ap, P2PHostOut* hout, uint32_t* done) {
   // one wave of as many CTAs as fit (every CTA waits on its own flag copy, so
   // the whole grid must be resident)
-  static int caps[64] = {};
+  static std::atomic<int> caps[64];  // per device (the dynamic-smem opt-in is per device)
   int dev = 0;
   cudaGetDevice(&dev);
-  int& cap = caps[dev & 63];
+  std::atomic<int>& cap = caps[dev & 63];
   if (!cap) {
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_pull_kernel, kThreads, 0) != cudaSuccess ||
