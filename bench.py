@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=128)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="okt", choices=["okt", "reference"])
-    ap.add_argument("--n", type=int, default=VGG_N)
+    # (--elements: under torchrun an abbreviation-like "--n" is taken by the launcher)
+    ap.add_argument("--n", "--elements", dest="n", type=int, default=VGG_N)
     ap.add_argument("--density", type=float, default=0.01)
     ap.add_argument("--tau", type=int, default=64)
     ap.add_argument("--tau-prime", type=int, default=32)
@@ -342,6 +343,7 @@ def run_okt(args):
     clocks.start()
     barrier()
     U_sum, m_sum = 0, 0
+    t_first = t + 1
     wall0 = time.perf_counter()
     for i in range(args.steps):
         t += 1
@@ -441,9 +443,15 @@ def run_okt(args):
         dense_ms = sum(a.elapsed_time(b) for a, b in dev_) / len(dev_)
     # ---- max over ranks
     mine = torch.tensor([total_ms, e2e_ms, wall, dense_ms or 0.0], dtype=torch.float64)
+    per_step = torch.tensor(step_ms, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(mine, op=dist.ReduceOp.MAX)
+        dist.all_reduce(per_step, op=dist.ReduceOp.MAX)
     total_ms, e2e_ms, wall, dense_ms = mine.tolist()
+    # steady vs refresh iterations ((t - 1) % tau' == 0 re-evaluates the thresholds)
+    refresh = [(t_first + i - 1) % args.tau_prime == 0 for i in range(args.steps)]
+    st_ms = [v for v, r in zip(per_step.tolist(), refresh) if not r]
+    rf_ms = [v for v, r in zip(per_step.tolist(), refresh) if r]
     ms_per_step = total_ms / args.steps
     achieved = k1_bytes / (k1_ms * 1e-3) / 1e9 if k1_ms > 0 else None
     peak = None
@@ -479,6 +487,11 @@ def run_okt(args):
                              "bytes_formula": "12n + 8e per EF step (read g, eps; write eps; 8 B per staged "
                                               "entry e); refresh steps add a 4n + 8m select pass"},
                 "phases_ms_per_step": phases,
+                "steady_ms": statistics.mean(st_ms) if st_ms else None,
+                "refresh_ms": statistics.mean(rf_ms) if rf_ms else None,
+                "refresh_steps_timed": len(rf_ms),
+                # dense-equivalent bandwidth, comparable to an allreduce's busBw
+                "dense_equivalent_gbs": 2 * 4 * n * (P - 1) / P / (ms_per_step * 1e-3) / 1e9 if P > 1 else None,
                 "avg_U": U_sum / args.steps, "avg_local_selected": m_sum / args.steps,
                 "wall_ms_per_step": 1e3 * wall / args.steps,
                 "dense_nccl_allreduce": None if world == 1 else {
