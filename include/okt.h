@@ -17,6 +17,7 @@
  *   space_repartition     include/oklab/oktopk.hpp:58     okt_space_repartition
  *   split_and_reduce      include/oklab/oktopk.hpp:77     okt_split_and_reduce
  *   balance_and_allgatherv include/oklab/oktopk.hpp:92    okt_balance_and_allgatherv
+ *   topka_allreduce       include/oklab/collectives.hpp    okt_topka_allreduce (Table-1 baseline)
  *   WorkerCtx / Transport include/oklab/transport.hpp:91-122  okt_world / okt_comm
  *   TrafficLedger         include/oklab/transport.hpp:52  okt_ledger
  *   OkState/ThresholdState include/oklab/oktopk.hpp:30, sparse.hpp:56  okt_state
@@ -233,6 +234,16 @@ int okt_split_and_reduce(okt_comm* comm, const float* d_g, size_t n,
 int okt_balance_and_allgatherv(okt_comm* comm, const uint32_t* d_idx,
                                const double* d_val, size_t nnz, size_t n,
                                double global_th, okt_sparse* u, void* stream);
+
+/* ---- Table-1 baseline ------------------------------------------------------
+ * topka_allreduce(ctx, g, k) (collectives.cpp:152-159): exact local top-k of
+ * the fp32 gradient (magnitude-descending, ties toward the smaller index),
+ * allgathered and summed in the reference's stride-doubling order (fp64).
+ * 1 <= k <= n (OKT_ERR_INVALID_ARGUMENT otherwise); a non-finite gradient
+ * fails with OKT_ERR_NUMERIC on its rank and OKT_ERR_TRANSPORT on the others.
+ * `out` points into comm-owned device memory valid until the next call. */
+int okt_topka_allreduce(okt_comm* comm, const float* d_g, size_t n, size_t k,
+                        okt_sparse* out, void* stream);
 
 /* ---- host planning (pure functions, no GPU) ------------------------------
  * The exchange plans every rank derives from the sizes it already agreed on;

@@ -246,6 +246,53 @@ size_t orc_sparse_sum(int P, const uint32_t* const* idx, const double* const* va
   return m;
 }
 
+/* topk_exact (sparse.cpp:43-80): th = k-th largest magnitude; keep every
+ * |g| > th and the first k - #{|g| > th} entries with |g| == th (the
+ * magnitude-descending order breaks ties toward the smaller index), emitted in
+ * coordinate order — the reference sorts the kept positions ascending. */
+size_t orc_topk_exact(const double* g, size_t n, size_t k, uint32_t* idx, double* val) {
+  if (k < 1 || k > n) return 0;
+  const double th = orc_kth_largest_mag(g, n, k);
+  size_t gt = 0;
+  for (size_t i = 0; i < n; ++i) gt += fabs(g[i]) > th;
+  size_t eq_left = k - gt, m = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const double a = fabs(g[i]);
+    int keep = a > th;
+    if (!keep && a == th && eq_left) {
+      keep = 1;
+      --eq_left;
+    }
+    if (keep) {
+      idx[m] = (uint32_t)i;
+      val[m] = g[i];
+      ++m;
+    }
+  }
+  return m;
+}
+
+/* collectives.cpp:152-159: every rank's exact top-k, sparse_allgatherv (which
+ * only moves them), sparse_sum in the stride-doubling order. */
+size_t orc_topka_allreduce(int P, const double* const* g, size_t n, size_t k, uint32_t* out_idx,
+                           double* out_val) {
+  if (P <= 0 || P > ORC_MAX_P || k < 1 || k > n) return 0;
+  uint32_t* pi[ORC_MAX_P];
+  double* pv[ORC_MAX_P];
+  size_t nnz[ORC_MAX_P];
+  for (int q = 0; q < P; ++q) {
+    pi[q] = (uint32_t*)malloc(k * sizeof(uint32_t));
+    pv[q] = (double*)malloc(k * sizeof(double));
+    nnz[q] = orc_topk_exact(g[q], n, k, pi[q], pv[q]);
+  }
+  const size_t m = orc_sparse_sum(P, (const uint32_t* const*)pi, (const double* const*)pv, nnz, out_idx, out_val);
+  for (int q = 0; q < P; ++q) {
+    free(pi[q]);
+    free(pv[q]);
+  }
+  return m;
+}
+
 /* ---- ledger helpers (transport.cpp:71-93, 103-160; collectives.cpp:30-77) ---- */
 static int log2i(int p) {
   int l = 0;

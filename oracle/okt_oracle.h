@@ -64,6 +64,13 @@ void orc_equal_slice_ends(uint64_t n, int P, uint64_t* ends);
 /* sparse.cpp:206-257: stride-doubling union sum of P sorted parts; returns nnz. */
 size_t orc_sparse_sum(int P, const uint32_t* const* idx, const double* const* val, const size_t* nnz,
                       uint32_t* out_idx, double* out_val);
+/* topk_exact (sparse.cpp:43-80) of a dense vector: the k largest magnitudes,
+ * ties toward the smaller index, returned in coordinate order; 1 <= k <= n. */
+size_t orc_topk_exact(const double* g, size_t n, size_t k, uint32_t* idx, double* val);
+/* topka_allreduce (collectives.cpp:152-159) of P dense vectors: sparse_sum of
+ * the P exact top-k parts; out holds up to P*k entries. */
+size_t orc_topka_allreduce(int P, const double* const* g, size_t n, size_t k, uint32_t* out_idx,
+                           double* out_val);
 /* oktopk.cpp:28-61 for all ranks: cuts from each rank's selected indices. */
 void orc_space_repartition(int P, const uint32_t* const* sel, const size_t* m, uint64_t n,
                            uint64_t* cuts, orc_counters* ledger /* P*6, may be NULL */);

@@ -138,6 +138,9 @@ class Oracle(_Common):
         L.orc_select.restype = c_size_t
         L.orc_select.argtypes = [POINTER(c_double), c_size_t, c_double, POINTER(c_uint32), POINTER(c_double)]
         L.orc_sparse_sum.restype = c_size_t
+        L.orc_topk_exact.restype = c_size_t
+        L.orc_topk_exact.argtypes = [POINTER(c_double), c_size_t, c_size_t, POINTER(c_uint32), POINTER(c_double)]
+        L.orc_topka_allreduce.restype = c_size_t
         L.orc_space_repartition.restype = None
         L.orc_ok_sparse_allreduce.restype = c_int
         L.orc_sgd_step.restype = c_int
@@ -205,6 +208,23 @@ class Oracle(_Common):
                                   oi.ctypes.data_as(POINTER(c_uint32)), ov.ctypes.data_as(POINTER(c_double)))
         return oi[:m].copy(), ov[:m].copy()
 
+    def topk_exact(self, g: np.ndarray, k: int):
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        idx = np.empty(max(k, 1), np.uint32)
+        val = np.empty(max(k, 1), np.float64)
+        m = self.L.orc_topk_exact(g.ctypes.data_as(POINTER(c_double)), g.size, k,
+                                  idx.ctypes.data_as(POINTER(c_uint32)), val.ctypes.data_as(POINTER(c_double)))
+        return idx[:m].copy(), val[:m].copy()
+
+    def topka_allreduce(self, inputs: Sequence[np.ndarray], k: int):
+        P = len(inputs)
+        g = [np.ascontiguousarray(x, dtype=np.float64) for x in inputs]
+        oi = np.empty(max(P * k, 1), np.uint32)
+        ov = np.empty(max(P * k, 1), np.float64)
+        m = self.L.orc_topka_allreduce(c_int(P), _ptrs(g, c_double), c_size_t(g[0].size), c_size_t(k),
+                                       oi.ctypes.data_as(POINTER(c_uint32)), ov.ctypes.data_as(POINTER(c_double)))
+        return oi[:m].copy(), ov[:m].copy()
+
     def space_repartition(self, sels: Sequence[np.ndarray], n: int, ledger: np.ndarray = None) -> List[int]:
         P = len(sels)
         s = [np.ascontiguousarray(x, dtype=np.uint32) for x in sels]
@@ -263,6 +283,7 @@ class Reference(_Common):
         L = ctypes.CDLL(path)
         self.L = L
         L.okref_allreduce.restype = c_int
+        L.okref_topka.restype = c_int
         L.okref_th_re_evaluate_dense.restype = c_double
         L.okref_th_re_evaluate_dense.argtypes = [POINTER(c_double), c_size_t, c_size_t]
         L.okref_drift_f32.restype = None
@@ -283,6 +304,19 @@ class Reference(_Common):
             c_int(P), g, c_size_t(n), c_int64(t), c_size_t(k), st, led,
             u_idx.ctypes.data_as(POINTER(c_uint32)), u_val.ctypes.data_as(POINTER(c_double)), ctypes.byref(U),
             ix, nix, sel, self.err, c_size_t(512))
+
+    def topka_allreduce(self, inputs: Sequence[np.ndarray], k: int):
+        P = len(inputs)
+        g = [np.ascontiguousarray(x, dtype=np.float64) for x in inputs]
+        oi = np.empty(max(P * k, 1), np.uint32)
+        ov = np.empty(max(P * k, 1), np.float64)
+        U = c_size_t(0)
+        rc = self.L.okref_topka(c_int(P), _ptrs(g, c_double), c_size_t(g[0].size), c_size_t(k),
+                                oi.ctypes.data_as(POINTER(c_uint32)), ov.ctypes.data_as(POINTER(c_double)),
+                                ctypes.byref(U), self.err, c_size_t(512))
+        if rc:
+            raise RuntimeError(f"okref_topka rc={rc}: {self.err.value.decode(errors='replace')}")
+        return oi[:U.value].copy(), ov[:U.value].copy()
 
     def th_re_evaluate(self, g: np.ndarray, k: int) -> float:
         g = np.ascontiguousarray(g, dtype=np.float64)

@@ -22,6 +22,7 @@
 #include <thread>
 #include <vector>
 
+#include "oklab/collectives.hpp"
 #include "oklab/errors.hpp"
 #include "oklab/inproc.hpp"
 #include "oklab/oktopk.hpp"
@@ -277,6 +278,32 @@ int okref_wire_decode(const uint8_t* in, size_t bytes, size_t n, uint32_t* idx, 
   } catch (const oklab::DecodeError&) {
     return 1;
   }
+}
+
+// One oklab::topka_allreduce on P rank threads (collectives.cpp:152-159).
+int okref_topka(int P, const double* const* g, size_t n, size_t k, uint32_t* u_idx, double* u_val, size_t* U,
+                char* err, size_t errlen) {
+  InprocTransport tr(P, 64);
+  TrafficLedger led(P);
+  std::vector<SparseGrad> res(P);
+  const int rc = run_ranks(
+      tr, P,
+      [&](int r) {
+        WorkerCtx ctx{r, P, &tr, &led};
+        DenseGrad dg(std::vector<double>(g[r], g[r] + n));
+        res[r] = topka_allreduce(ctx, dg, k);
+      },
+      err, errlen);
+  if (rc) return rc;
+  for (int r = 1; r < P; ++r)
+    if (res[r] != res[0]) {
+      std::snprintf(err, errlen, "ranks disagree on u");
+      return 8;
+    }
+  *U = res[0].nnz();
+  std::memcpy(u_idx, res[0].indices.data(), res[0].nnz() * sizeof(uint32_t));
+  std::memcpy(u_val, res[0].values.data(), res[0].nnz() * sizeof(double));
+  return 0;
 }
 
 }  // extern "C"

@@ -194,6 +194,7 @@ struct okt_comm {
   Buf gval;                // gathered region values (refresh)
   Buf u_idx, u_val;        // allgathered result
   Buf sel_idx, sel_val;    // sub-phase outputs
+  Buf tk_aux, tk_parts;    // TopkA: trim chunk counts / gathered exact top-k parts (AoS)
   Buf indexes;
   Buf eps[2];
   Buf hgrad;               // staging for the host-buffer entry points
@@ -2001,6 +2002,148 @@ int okt_balance_and_allgatherv(okt_comm* c, const uint32_t* d_idx, const double*
   u->d_val = c->u_val.as<double>();
   u->nnz = U;
   u->n = n;
+  return OKT_OK;
+}
+
+// ---- Table-1 baseline: TopkA -----------------------------------------------------------
+// topka_allreduce (collectives.cpp:152-159): exact local top-k (topk_exact,
+// sparse.cpp:43-80 — magnitude-descending, ties toward the smaller index),
+// sparse_allgatherv of the P parts, sparse_sum (sparse.cpp:241-257).  On the
+// GPU: K2 radix select of the exact k-th magnitude, K1 select of {|g| >= th},
+// the tie trim (okt_topk.cu), one all-pairs exchange of the k-entry parts and
+// the region merge (scatter + bracket-sum scan) over the whole vector.
+int okt_topka_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt_sparse* out, void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!out) return set_err(OKT_ERR_INVALID_ARGUMENT, "topka_allreduce: null output");
+  if (k < 1 || k > n) return set_err(OKT_ERR_INVALID_ARGUMENT, "topk_exact: k must be in [1, n]");
+  if (n > 0xffffffffull) return set_err(OKT_ERR_INVALID_ARGUMENT, "topka_allreduce: n exceeds 32-bit indices");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  const int P = c->P, rank = c->rank;
+  int rc = c->reserve(n);
+  if (rc) return rc;
+  rc = c->ck(cudaMemsetAsync(&c->d()->flags, 0, 4, s), "memset");
+  if (!rc)
+    rc = c->ck(okt::launch_radix_select(c->L, okt::RadixSrc::kDenseF32, d_g, n, nullptr, n, k, &c->d()->rs,
+                                        c->hist.as<uint32_t>(), &c->d()->th_arg, false), "radix");
+  if (!rc)
+    rc = c->ck(okt::launch_k1(c->L, c->S, okt::K1Mode::kSelect, d_g, nullptr, nullptr, 0.f, n, &c->d()->th_arg,
+                              nullptr, okt::OutCoo{c->coo.as<uint64_t>(), nullptr, nullptr}, &c->d()->m, nullptr,
+                              &c->d()->flags, nullptr), "k1");
+  if (rc || (rc = c->sync(s))) return rc;
+  const bool bad = (c->h->flags & 1u) != 0;
+  const uint64_t m = c->h->m;
+  const float th = float(c->h->th_arg);
+  std::string err;
+  if (P > 1) {
+    // every rank's part size (and health) before any data moves
+    c->hup->small[0] = uint32_t(k);
+    c->hup->small[1] = bad ? 1u : 0u;
+    if ((rc = c->ck(cudaMemcpyAsync(&c->d()->small[0], &c->hup->small[0], 8, cudaMemcpyHostToDevice, s), "h2d")))
+      return rc;
+    rc = c->tr->allgather(&c->d()->small[0], c->d()->small_all, 8, s, err);
+    if (rc) return c->comm_err(rc, err);
+    if ((rc = c->sync(s))) return rc;
+    for (int q = 0; q < P; ++q) {
+      if (c->h->small_all[2 * q + 1]) {
+        if (q == rank) return set_err(OKT_ERR_NUMERIC, "topka_allreduce: non-finite input");
+        return set_err(OKT_ERR_TRANSPORT,
+                       "TransportError: rank " + std::to_string(q) + " failed (non-finite input)");
+      }
+      if (c->h->small_all[2 * q] != uint32_t(k))
+        return set_err(OKT_ERR_PROTOCOL, "topka_allreduce: ranks disagree on k");
+    }
+  } else if (bad) {
+    return set_err(OKT_ERR_NUMERIC, "topka_allreduce: non-finite input");
+  }
+  if (m < k) return set_err(OKT_ERR_INTERNAL, "topka_allreduce: selection smaller than k");
+  // Exact top-k of the selection: all |v| > th, then the first (k - #gt) ties.
+  uint64_t* parts = nullptr;
+  if ((rc = c->ensure(c->tk_parts, 8 * k * size_t(P)))) return rc;
+  parts = c->tk_parts.as<uint64_t>();
+  uint64_t* mine = parts + k * uint64_t(rank);
+  if (P == 1) {
+    if ((rc = c->ensure(c->sel_idx, 4 * k)) || (rc = c->ensure(c->sel_val, 8 * k))) return rc;
+  }
+  if (m == k && P > 1) {
+    rc = c->ck(cudaMemcpyAsync(mine, c->coo.p, 8 * k, cudaMemcpyDeviceToDevice, s), "copy");
+    if (rc) return rc;
+  } else {
+    const uint64_t chunks = (m + okt::kTopkTrimChunk - 1) / okt::kTopkTrimChunk;
+    if ((rc = c->ensure(c->tk_aux, 24 * chunks))) return rc;
+    uint32_t* gt = c->tk_aux.as<uint32_t>();
+    uint32_t* eq = gt + chunks;
+    uint64_t* off = reinterpret_cast<uint64_t*>(c->tk_aux.as<char>() + 8 * chunks);
+    uint64_t* eqb = off + chunks;
+    rc = c->ck(okt::launch_topk_count(c->L, c->coo.as<uint64_t>(), m, th, gt, eq), "topk_count");
+    if (rc) return rc;
+    std::vector<uint32_t> hc(2 * chunks);
+    if ((rc = c->ck(cudaMemcpyAsync(hc.data(), gt, 8 * chunks, cudaMemcpyDeviceToHost, s), "d2h"))) return rc;
+    if ((rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+    uint64_t n_gt = 0;
+    for (uint64_t i = 0; i < chunks; ++i) n_gt += hc[i];
+    if (n_gt >= k) return set_err(OKT_ERR_INTERNAL, "topka_allreduce: threshold above the k-th magnitude");
+    const uint64_t need = k - n_gt;
+    std::vector<uint64_t> ho(2 * chunks);
+    uint64_t pos = 0, eq_seen = 0;
+    for (uint64_t i = 0; i < chunks; ++i) {
+      ho[i] = pos;
+      ho[chunks + i] = eq_seen;
+      const uint64_t keep_eq = eq_seen >= need ? 0 : std::min<uint64_t>(hc[chunks + i], need - eq_seen);
+      pos += hc[i] + keep_eq;
+      eq_seen += hc[chunks + i];
+    }
+    if (pos != k) return set_err(OKT_ERR_INTERNAL, "topka_allreduce: tie trim miscounted");
+    if ((rc = c->ck(cudaMemcpyAsync(off, ho.data(), 16 * chunks, cudaMemcpyHostToDevice, s), "h2d"))) return rc;
+    rc = c->ck(okt::launch_topk_write(c->L, c->coo.as<uint64_t>(), m, th, off, eqb, need,
+                                      P > 1 ? mine : nullptr, P == 1 ? c->sel_idx.as<uint32_t>() : nullptr,
+                                      P == 1 ? c->sel_val.as<double>() : nullptr), "topk_write");
+    if (rc) return rc;
+    // the pageable H2D above has been consumed once the stream passes this point
+    if ((rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  }
+  if (P == 1) {
+    out->d_idx = c->sel_idx.as<uint32_t>();
+    out->d_val = c->sel_val.as<double>();
+    out->nnz = k;
+    out->n = n;
+    return OKT_OK;
+  }
+  // sparse_allgatherv: every part to every peer (one exchange, all pairs).
+  std::vector<Xfer> sends, recvs;
+  for (int q = 0; q < P; ++q) {
+    if (q == rank) continue;
+    sends.push_back({q, mine, 8 * k});
+    recvs.push_back({q, parts + k * uint64_t(q), 8 * k});
+  }
+  rc = c->tr->exchange(sends, recvs, s, err);
+  if (rc) return c->comm_err(rc, err);
+  c->credit_allgatherv(OKT_PHASE_ALLGATHERV, std::vector<uint64_t>(P, k), 12);
+  // sparse_sum: region merge over [0, n) with the P parts as sources.
+  const uint64_t bound = k * uint64_t(P);
+  if ((rc = c->ensure(c->mask, ((n + 15) / 16) * 16 + 16)) || (rc = c->ensure(c->stage, 4 * n * size_t(P))) ||
+      (rc = c->ensure(c->sel_idx, 4 * bound)) || (rc = c->ensure(c->sel_val, 8 * bound)))
+    return rc;
+  okt::Segs segs{};
+  segs.nseg = P;
+  segs.start[0] = 0;
+  for (int q = 0; q < P; ++q) {
+    segs.ptr[q] = parts + k * uint64_t(q);
+    segs.src[q] = q;
+    segs.start[q + 1] = segs.start[q] + k;
+  }
+  rc = c->ck(okt::launch_scatter(c->L, segs, 0, n, P, c->mask.as<uint32_t>(), c->stage.as<float>(),
+                                 &c->d()->flags), "scatter");
+  if (!rc)
+    rc = c->ck(okt::launch_region_scan(c->L, c->S, P, false, 0, n, c->mask.as<uint32_t>(), c->stage.as<float>(),
+                                       nullptr, c->sel_idx.as<uint32_t>(), c->sel_val.as<double>(), &c->d()->R),
+               "region_scan");
+  if (rc || (rc = c->sync(s))) return rc;
+  out->d_idx = c->sel_idx.as<uint32_t>();
+  out->d_val = c->sel_val.as<double>();
+  out->nnz = c->h->R;
+  out->n = n;
   return OKT_OK;
 }
 

@@ -184,4 +184,12 @@ cudaError_t launch_wire_encode(Launch& L, const uint32_t* idx, const double* val
 cudaError_t launch_wire_decode(Launch& L, const uint32_t* in, uint64_t nnz, uint64_t n, uint32_t* idx, double* val,
                                uint32_t* err);
 
+// Exact top-k trim of a threshold selection (okt_topk.cu): chunks of 1024 entries.
+constexpr int kTopkTrimChunk = 1024;
+cudaError_t launch_topk_count(Launch& L, const uint64_t* coo, uint64_t m, float th, uint32_t* gt_cnt,
+                              uint32_t* eq_cnt);
+cudaError_t launch_topk_write(Launch& L, const uint64_t* coo, uint64_t m, float th, const uint64_t* off,
+                              const uint64_t* eq_before, uint64_t need, uint64_t* aos, uint32_t* out_idx,
+                              double* out_val);
+
 }  // namespace okt

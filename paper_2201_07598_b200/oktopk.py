@@ -400,6 +400,16 @@ def balance_and_allgatherv(ctx: WorkerCtx, region: SparseGrad, global_th: float)
     return _sparse_from(u, region.n)
 
 
+def topka_allreduce(ctx: WorkerCtx, g, k: int) -> SparseGrad:
+    """Table-1 baseline TopkA (collectives.cpp:152-159): exact local top-k,
+    sparse_allgatherv, stride-doubling sparse_sum — all on the GPU."""
+    d = _device_f32(g, ctx.device)
+    s = OktSparse()
+    _check(_lib.lib().okt_topka_allreduce(ctx.comm, ctypes.c_void_p(d.data_ptr()), d.numel(), max(int(k), 0),
+                                          ctypes.byref(s), None))
+    return _sparse_from(s, d.numel())
+
+
 def wire_encode(s: SparseGrad, device: int = 0) -> bytes:
     """oklab::wire_encode (sparse.hpp:126, sparse.cpp:275-285) on the device:
     [nnz u32][indices u32 x nnz][values f32 x nnz], little endian."""

@@ -62,6 +62,20 @@ def main():
         g[:256] += 1.0 + 0.001 * r
         return g
     record(ref, "skew_P4.npz", 4, 2048, 64, [1, 2, 3], skew, 2, 1, 4)
+    # topka_allreduce (collectives.cpp:152-159; test_collectives.cpp:167-190)
+    os.makedirs(os.path.join(HERE, "topka"), exist_ok=True)
+    rng = np.random.default_rng(77)
+    topka = {
+        "int_P4": (4, 200, 12, [orc.random_int_dense(900 + r, 200, 1000) for r in range(4)]),
+        "f32_P2": (2, 1000, 37, [f32(orc.random_dense(300 + r, 1000)) for r in range(2)]),
+        "ties_P8": (8, 512, 40, [rng.choice([-1.0, 1.0, 0.5, -0.5, 0.0, 0.25], 512) for _ in range(8)]),
+        "kn_P2": (2, 64, 64, [f32(orc.random_dense(400 + r, 64)) for r in range(2)]),
+        "k1_P1": (1, 300, 1, [f32(orc.random_dense(500, 300))]),
+    }
+    for name, (P, n, k, ins) in topka.items():
+        ui, uv = ref.topka_allreduce(ins, k)
+        np.savez_compressed(os.path.join(HERE, "topka", name + ".npz"), P=P, n=n, k=k, inputs=np.stack(ins),
+                            u_idx=ui, u_val=uv)
     print("golden fixtures written to", HERE)
 
 
