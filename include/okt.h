@@ -17,7 +17,11 @@
  *   space_repartition     include/oklab/oktopk.hpp:58     okt_space_repartition
  *   split_and_reduce      include/oklab/oktopk.hpp:77     okt_split_and_reduce
  *   balance_and_allgatherv include/oklab/oktopk.hpp:92    okt_balance_and_allgatherv
- *   topka_allreduce       include/oklab/collectives.hpp    okt_topka_allreduce (Table-1 baseline)
+ *   topka_allreduce       include/oklab/collectives.hpp:33  okt_topka_allreduce (Table-1 baselines)
+ *   gtopk_allreduce       include/oklab/collectives.hpp:53  okt_gtopk_allreduce
+ *   topkdsa_allreduce     include/oklab/collectives.hpp:45  okt_topkdsa_allreduce
+ *   gaussiank_allreduce   include/oklab/collectives.hpp:70  okt_gaussiank_allreduce
+ *   gaussian_threshold    include/oklab/sparse.hpp:102, collectives.hpp:64  okt_gaussiank_threshold
  *   WorkerCtx / Transport include/oklab/transport.hpp:91-122  okt_world / okt_comm
  *   TrafficLedger         include/oklab/transport.hpp:52  okt_ledger
  *   OkState/ThresholdState include/oklab/oktopk.hpp:30, sparse.hpp:56  okt_state
@@ -241,9 +245,27 @@ int okt_balance_and_allgatherv(okt_comm* comm, const uint32_t* d_idx,
  * allgathered and summed in the reference's stride-doubling order (fp64).
  * 1 <= k <= n (OKT_ERR_INVALID_ARGUMENT otherwise); a non-finite gradient
  * fails with OKT_ERR_NUMERIC on its rank and OKT_ERR_TRANSPORT on the others.
- * `out` points into comm-owned device memory valid until the next call. */
+ * `out` points into comm-owned device memory valid until the next call.
+ * The other Table-1 baselines follow the same contract:
+ *   gtopk_allreduce   collectives.cpp:300-325  log2 P pairwise merge + top-k rounds
+ *   topkdsa_allreduce collectives.cpp:184-297  reduce-scatter with the dense switch,
+ *                                              then allgatherv of the segments
+ *   gaussiank_allreduce collectives.cpp:342-352 Gaussian-fit threshold (0.9
+ *                     rescaling when scale_to_floor), select, allgatherv, sum
+ * okt_gaussiank_threshold returns gaussian_threshold (scale_to_floor = 0, raw)
+ * or gaussiank_scaled_threshold (1); the fp64 moments come from a tree
+ * reduction, within a few ulp of the reference's sequential sums.  Zero-variance
+ * input fails with OKT_ERR_NUMERIC ("DegenerateDistributionError"). */
 int okt_topka_allreduce(okt_comm* comm, const float* d_g, size_t n, size_t k,
                         okt_sparse* out, void* stream);
+int okt_gtopk_allreduce(okt_comm* comm, const float* d_g, size_t n, size_t k,
+                        okt_sparse* out, void* stream);
+int okt_topkdsa_allreduce(okt_comm* comm, const float* d_g, size_t n, size_t k,
+                          okt_sparse* out, void* stream);
+int okt_gaussiank_threshold(okt_comm* comm, const float* d_g, size_t n, size_t k,
+                            int scale_to_floor, double* th, void* stream);
+int okt_gaussiank_allreduce(okt_comm* comm, const float* d_g, size_t n, size_t k,
+                            int scale_to_floor, okt_sparse* out, void* stream);
 
 /* ---- host planning (pure functions, no GPU) ------------------------------
  * The exchange plans every rank derives from the sizes it already agreed on;

@@ -330,6 +330,302 @@ static void credit_allgatherv(orc_counters* L, int P, int ph, const uint64_t* pa
     }
 }
 
+/* ---- remaining Table-1 baselines (collectives.cpp:184-352) ---- */
+static void free_part(part_t* p) {
+  free(p->idx);
+  free(p->val);
+  p->idx = NULL;
+  p->val = NULL;
+  p->nnz = 0;
+}
+
+/* topk_exact of a sparse list (sparse.cpp:82-92): take = min(k, nnz) of its
+ * values, ties toward the smaller position (= smaller index). */
+static part_t topk_sparse(part_t s, size_t k) {
+  part_t o;
+  const size_t take = k < s.nnz ? k : s.nnz;
+  o.idx = (uint32_t*)malloc((take + 1) * sizeof(uint32_t));
+  o.val = (double*)malloc((take + 1) * sizeof(double));
+  uint32_t* pos = (uint32_t*)malloc((take + 1) * sizeof(uint32_t));
+  o.nnz = take ? orc_topk_exact(s.val, s.nnz, take, pos, o.val) : 0;
+  for (size_t i = 0; i < o.nnz; ++i) o.idx[i] = s.idx[pos[i]];
+  free(pos);
+  return o;
+}
+
+static part_t dense_topk(const double* g, size_t n, size_t k) {
+  part_t o;
+  o.idx = (uint32_t*)malloc((k + 1) * sizeof(uint32_t));
+  o.val = (double*)malloc((k + 1) * sizeof(double));
+  o.nnz = orc_topk_exact(g, n, k, o.idx, o.val);
+  return o;
+}
+
+/* gtopk_allreduce (collectives.cpp:300-325) replayed for all ranks: each level
+ * merges the pair (lower rank first) and keeps the exact top-k. */
+size_t orc_gtopk_allreduce(int P, const double* const* g, size_t n, size_t k, uint32_t* out_idx, double* out_val,
+                           orc_counters* ledger) {
+  if (P <= 0 || P > ORC_MAX_P || k < 1 || k > n) return 0;
+  part_t st[ORC_MAX_P], nx[ORC_MAX_P];
+  for (int r = 0; r < P; ++r) st[r] = dense_topk(g[r], n, k);
+  for (int level = 1; level < P; level <<= 1) {
+    for (int r = 0; r < P; ++r) {
+      const int peer = r ^ level, a = r < peer ? r : peer, b = r < peer ? peer : r;
+      credit(ledger, P, r, 0, 1, 2 * st[r].nnz);
+      credit(ledger, P, r, 0, 0, 2 * st[peer].nnz);
+      part_t m = merge_two(st[a], st[b]);
+      nx[r] = topk_sparse(m, k);
+      free_part(&m);
+    }
+    for (int r = 0; r < P; ++r) {
+      free_part(&st[r]);
+      st[r] = nx[r];
+    }
+  }
+  memcpy(out_idx, st[0].idx, st[0].nnz * sizeof(uint32_t));
+  memcpy(out_val, st[0].val, st[0].nnz * sizeof(double));
+  const size_t m = st[0].nnz;
+  for (int r = 0; r < P; ++r) free_part(&st[r]);
+  return m;
+}
+
+/* TopkDSA working set (collectives.cpp:162-182): COO or a dense window. */
+typedef struct {
+  int dense;
+  part_t coo;
+  double* win;
+  uint64_t lo, hi;
+} dsa_t;
+
+static void dsa_densify(dsa_t* w, uint64_t lo, uint64_t hi) {
+  if (w->dense) return;
+  w->win = (double*)calloc(hi - lo + 1, sizeof(double));
+  for (size_t i = 0; i < w->coo.nnz; ++i) w->win[w->coo.idx[i] - lo] = w->coo.val[i];
+  w->lo = lo;
+  w->hi = hi;
+  w->dense = 1;
+  free_part(&w->coo);
+}
+
+static part_t slice_part(part_t s, uint64_t lo, uint64_t hi) { /* sparse_slice, sparse.cpp:190-202 */
+  size_t a = 0, b;
+  while (a < s.nnz && s.idx[a] < lo) ++a;
+  b = a;
+  while (b < s.nnz && s.idx[b] < hi) ++b;
+  part_t o;
+  o.idx = (uint32_t*)malloc((b - a + 1) * sizeof(uint32_t));
+  o.val = (double*)malloc((b - a + 1) * sizeof(double));
+  memcpy(o.idx, s.idx + a, (b - a) * sizeof(uint32_t));
+  memcpy(o.val, s.val + a, (b - a) * sizeof(double));
+  o.nnz = b - a;
+  return o;
+}
+
+/* topkdsa_allreduce (collectives.cpp:184-297) replayed for all ranks in lockstep. */
+size_t orc_topkdsa_allreduce(int P, const double* const* g, size_t n, size_t k, uint32_t* out_idx, double* out_val,
+                             orc_counters* ledger) {
+  if (P <= 0 || P > ORC_MAX_P || k < 1 || k > n) return 0;
+  dsa_t w[ORC_MAX_P];
+  for (int r = 0; r < P; ++r) {
+    memset(&w[r], 0, sizeof(w[r]));
+    w[r].coo = dense_topk(g[r], n, k);
+  }
+  if (P == 1) {
+    memcpy(out_idx, w[0].coo.idx, w[0].coo.nnz * sizeof(uint32_t));
+    memcpy(out_val, w[0].coo.val, w[0].coo.nnz * sizeof(double));
+    const size_t m = w[0].coo.nnz;
+    free_part(&w[0].coo);
+    return m;
+  }
+  uint64_t ends[ORC_MAX_P + 1];
+  orc_equal_slice_ends(n, P, ends);
+  int lo[ORC_MAX_P], hi[ORC_MAX_P];
+  for (int r = 0; r < P; ++r) {
+    lo[r] = 0;
+    hi[r] = P;
+  }
+  for (int mask = P >> 1; mask > 0; mask >>= 1) {
+    /* messages of every rank first: kind, dense half or COO slice */
+    int kind[ORC_MAX_P];
+    double* dmsg[ORC_MAX_P];
+    part_t cmsg[ORC_MAX_P];
+    uint64_t klo[ORC_MAX_P], khi[ORC_MAX_P];
+    for (int r = 0; r < P; ++r) {
+      const int mid = lo[r] + mask;
+      int keep_lo, keep_hi, send_lo, send_hi;
+      if ((r & mask) == 0) {
+        keep_lo = lo[r]; keep_hi = mid; send_lo = mid; send_hi = hi[r];
+      } else {
+        keep_lo = mid; keep_hi = hi[r]; send_lo = lo[r]; send_hi = mid;
+      }
+      const uint64_t s0 = ends[send_lo], s1 = ends[send_hi];
+      klo[r] = ends[keep_lo];
+      khi[r] = ends[keep_hi];
+      kind[r] = w[r].dense;
+      dmsg[r] = NULL;
+      cmsg[r].idx = NULL;
+      cmsg[r].val = NULL;
+      cmsg[r].nnz = 0;
+      if (w[r].dense) {
+        dmsg[r] = (double*)malloc((s1 - s0 + 1) * sizeof(double));
+        memcpy(dmsg[r], w[r].win + (s0 - w[r].lo), (s1 - s0) * sizeof(double));
+        credit(ledger, P, r, 0, 1, s1 - s0);
+      } else {
+        cmsg[r] = slice_part(w[r].coo, s0, s1);
+        credit(ledger, P, r, 0, 1, 2 * cmsg[r].nnz);
+      }
+      lo[r] = keep_lo;
+      hi[r] = keep_hi;
+    }
+    for (int r = 0; r < P; ++r) {
+      const int partner = r ^ mask;
+      const uint64_t k0 = klo[r], k1 = khi[r];
+      credit(ledger, P, r, 0, 0, kind[partner] ? k1 - k0 : 2 * cmsg[partner].nnz);
+      /* restrict to the kept half */
+      if (w[r].dense) {
+        double* kept = (double*)malloc((k1 - k0 + 1) * sizeof(double));
+        memcpy(kept, w[r].win + (k0 - w[r].lo), (k1 - k0) * sizeof(double));
+        free(w[r].win);
+        w[r].win = kept;
+        w[r].lo = k0;
+        w[r].hi = k1;
+      } else {
+        part_t kept = slice_part(w[r].coo, k0, k1);
+        free_part(&w[r].coo);
+        w[r].coo = kept;
+      }
+      if (kind[partner]) {
+        dsa_densify(&w[r], k0, k1);
+        for (uint64_t i = 0; i < k1 - k0; ++i) w[r].win[i] += dmsg[partner][i];
+      } else if (w[r].dense) {
+        const part_t th = cmsg[partner];
+        for (size_t i = 0; i < th.nnz; ++i) w[r].win[th.idx[i] - w[r].lo] += th.val[i];
+      } else {
+        part_t m = r < partner ? merge_two(w[r].coo, cmsg[partner]) : merge_two(cmsg[partner], w[r].coo);
+        free_part(&w[r].coo);
+        w[r].coo = m;
+      }
+      if (!w[r].dense && 2 * w[r].coo.nnz >= k1 - k0) dsa_densify(&w[r], k0, k1);
+    }
+    for (int r = 0; r < P; ++r) {
+      free(dmsg[r]);
+      free_part(&cmsg[r]);
+    }
+  }
+  /* segments, concatenated in rank order; allgatherv ledger */
+  size_t m = 0;
+  uint64_t segn[ORC_MAX_P];
+  for (int r = 0; r < P; ++r) {
+    if (w[r].dense) {
+      segn[r] = 0;
+      for (uint64_t i = 0; i < w[r].hi - w[r].lo; ++i)
+        if (w[r].win[i] != 0.0) {
+          out_idx[m] = (uint32_t)(w[r].lo + i);
+          out_val[m++] = w[r].win[i];
+          ++segn[r];
+        }
+      free(w[r].win);
+    } else {
+      segn[r] = w[r].coo.nnz;
+      memcpy(out_idx + m, w[r].coo.idx, w[r].coo.nnz * sizeof(uint32_t));
+      memcpy(out_val + m, w[r].coo.val, w[r].coo.nnz * sizeof(double));
+      m += w[r].coo.nnz;
+      free_part(&w[r].coo);
+    }
+  }
+  credit_allgatherv(ledger, P, 2, segn);
+  return m;
+}
+
+/* gaussian_threshold (sparse.cpp:167-188): sequential fp64 mean and unbiased
+ * variance, quantile at 1 - k/(2n) (raw, may be negative); with
+ * scale_to_floor, gaussiank_scaled_threshold.  NAN on bad input / zero variance. */
+double orc_inverse_normal_cdf(double p);
+double orc_gaussian_threshold(const double* g, size_t n, size_t k, int scale_to_floor) {
+  if (n < 2 || k < 1 || k > n) return NAN;
+  double mean = 0.0;
+  for (size_t i = 0; i < n; ++i) mean += g[i];
+  mean /= (double)n;
+  double ss = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    const double d = g[i] - mean;
+    ss += d * d;
+  }
+  const double var = ss / (double)(n - 1);
+  if (var == 0.0) return NAN;
+  const double p = 1.0 - (double)k / (2.0 * (double)n);
+  double th = mean + sqrt(var) * orc_inverse_normal_cdf(p);
+  if (scale_to_floor) { /* gaussiank_scaled_threshold, collectives.cpp:327-340 */
+    if (!(th >= 0.0)) th = 0.0;
+    for (;;) {
+      size_t c = 0;
+      for (size_t i = 0; i < n; ++i) c += fabs(g[i]) >= th;
+      if (4 * c > 3 * k) break;
+      th *= 0.9;
+    }
+  }
+  return th;
+}
+
+/* Acklam's quantile approximation + two Halley steps (sparse.cpp:122-165). */
+double orc_inverse_normal_cdf(double p) {
+  static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                             1.383577518672690e+02,  -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                             6.680131188771972e+01,  -1.328068155288572e+01};
+  static const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                             -2.549732539343734e+00, 4.374664141464968e+00,  2.938163982698783e+00};
+  static const double d[] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                             3.754408661907416e+00};
+  double x, q, r;
+  if (p < 0.02425) {
+    q = sqrt(-2.0 * log(p));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  } else if (p <= 1.0 - 0.02425) {
+    q = p - 0.5;
+    r = q * q;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1.0);
+  } else {
+    q = sqrt(-2.0 * log(1.0 - p));
+    x = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  }
+  for (int it = 0; it < 2; ++it) {
+    const double e = 0.5 * erfc(-x / sqrt(2.0)) - p;
+    const double u = e * 2.5066282746310005 * exp(x * x / 2.0);
+    x = x - u / (1.0 + x * u / 2.0);
+  }
+  return x;
+}
+
+/* gaussiank_allreduce (collectives.cpp:342-352): per-rank threshold selection,
+ * allgatherv (ledger), sparse_sum.  out holds up to P*n entries. */
+size_t orc_gaussiank_allreduce(int P, const double* const* g, size_t n, size_t k, int scale_to_floor,
+                               uint32_t* out_idx, double* out_val, orc_counters* ledger) {
+  if (P <= 0 || P > ORC_MAX_P) return 0;
+  uint32_t* pi[ORC_MAX_P];
+  double* pv[ORC_MAX_P];
+  size_t nnz[ORC_MAX_P];
+  uint64_t parts[ORC_MAX_P];
+  for (int q = 0; q < P; ++q) {
+    double th = orc_gaussian_threshold(g[q], n, k, scale_to_floor);
+    if (!(th >= 0.0)) th = 0.0; /* std::max(gaussian_threshold, 0.0) */
+    pi[q] = (uint32_t*)malloc((n + 1) * sizeof(uint32_t));
+    pv[q] = (double*)malloc((n + 1) * sizeof(double));
+    nnz[q] = orc_select(g[q], n, th, pi[q], pv[q]);
+    parts[q] = nnz[q];
+  }
+  if (P > 1) credit_allgatherv(ledger, P, 2, parts);
+  const size_t m = orc_sparse_sum(P, (const uint32_t* const*)pi, (const double* const*)pv, nnz, out_idx, out_val);
+  for (int q = 0; q < P; ++q) {
+    free(pi[q]);
+    free(pv[q]);
+  }
+  return m;
+}
+
 /* ---- space_repartition (oktopk.cpp:28-61) -------------------------------------- */
 void orc_space_repartition(int P, const uint32_t* const* sel, const size_t* m, uint64_t n, uint64_t* cuts,
                            orc_counters* ledger) {

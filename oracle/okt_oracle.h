@@ -71,6 +71,18 @@ size_t orc_topk_exact(const double* g, size_t n, size_t k, uint32_t* idx, double
  * the P exact top-k parts; out holds up to P*k entries. */
 size_t orc_topka_allreduce(int P, const double* const* g, size_t n, size_t k, uint32_t* out_idx,
                            double* out_val);
+/* gtopk_allreduce (collectives.cpp:300-325) / topkdsa_allreduce (:184-297):
+ * rank 0's result (all ranks agree); ledger P*6 counters or NULL. */
+size_t orc_gtopk_allreduce(int P, const double* const* g, size_t n, size_t k, uint32_t* out_idx, double* out_val,
+                           orc_counters* ledger);
+size_t orc_topkdsa_allreduce(int P, const double* const* g, size_t n, size_t k, uint32_t* out_idx, double* out_val,
+                             orc_counters* ledger);
+/* gaussian_threshold / gaussiank_scaled_threshold (sparse.cpp:167-188,
+ * collectives.cpp:327-340); NAN for n < 2, k outside [1, n] or zero variance. */
+double orc_inverse_normal_cdf(double p);
+double orc_gaussian_threshold(const double* g, size_t n, size_t k, int scale_to_floor);
+size_t orc_gaussiank_allreduce(int P, const double* const* g, size_t n, size_t k, int scale_to_floor,
+                               uint32_t* out_idx, double* out_val, orc_counters* ledger);
 /* oktopk.cpp:28-61 for all ranks: cuts from each rank's selected indices. */
 void orc_space_repartition(int P, const uint32_t* const* sel, const size_t* m, uint64_t n,
                            uint64_t* cuts, orc_counters* ledger /* P*6, may be NULL */);

@@ -141,6 +141,11 @@ class Oracle(_Common):
         L.orc_topk_exact.restype = c_size_t
         L.orc_topk_exact.argtypes = [POINTER(c_double), c_size_t, c_size_t, POINTER(c_uint32), POINTER(c_double)]
         L.orc_topka_allreduce.restype = c_size_t
+        L.orc_gtopk_allreduce.restype = c_size_t
+        L.orc_topkdsa_allreduce.restype = c_size_t
+        L.orc_gaussiank_allreduce.restype = c_size_t
+        L.orc_gaussian_threshold.restype = c_double
+        L.orc_gaussian_threshold.argtypes = [POINTER(c_double), c_size_t, c_size_t, c_int]
         L.orc_space_repartition.restype = None
         L.orc_ok_sparse_allreduce.restype = c_int
         L.orc_sgd_step.restype = c_int
@@ -225,6 +230,33 @@ class Oracle(_Common):
                                        oi.ctypes.data_as(POINTER(c_uint32)), ov.ctypes.data_as(POINTER(c_double)))
         return oi[:m].copy(), ov[:m].copy()
 
+    def baseline(self, which: str, inputs: Sequence[np.ndarray], k: int, scale_to_floor: bool = True,
+                 ledger: np.ndarray = None):
+        """gtopk / topkdsa / gaussiank allreduce of P dense inputs (rank 0's result)."""
+        P = len(inputs)
+        g = [np.ascontiguousarray(x, dtype=np.float64) for x in inputs]
+        n = g[0].size
+        cap = max(P * n, 1)
+        oi = np.empty(cap, np.uint32)
+        ov = np.empty(cap, np.float64)
+        led = ledger if ledger is not None else np.zeros((P, 6, 4), np.uint64)
+        lp = led.ctypes.data_as(POINTER(Counters))
+        args = (c_int(P), _ptrs(g, c_double), c_size_t(n), c_size_t(k))
+        outs = (oi.ctypes.data_as(POINTER(c_uint32)), ov.ctypes.data_as(POINTER(c_double)), lp)
+        if which == "gtopk":
+            m = self.L.orc_gtopk_allreduce(*args, *outs)
+        elif which == "topkdsa":
+            m = self.L.orc_topkdsa_allreduce(*args, *outs)
+        elif which == "gaussiank":
+            m = self.L.orc_gaussiank_allreduce(*args, c_int(int(scale_to_floor)), *outs)
+        else:
+            raise ValueError(which)
+        return oi[:m].copy(), ov[:m].copy()
+
+    def gaussian_threshold(self, g: np.ndarray, k: int, scale_to_floor: bool = True) -> float:
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        return self.L.orc_gaussian_threshold(g.ctypes.data_as(POINTER(c_double)), g.size, k, int(scale_to_floor))
+
     def space_repartition(self, sels: Sequence[np.ndarray], n: int, ledger: np.ndarray = None) -> List[int]:
         P = len(sels)
         s = [np.ascontiguousarray(x, dtype=np.uint32) for x in sels]
@@ -284,6 +316,9 @@ class Reference(_Common):
         self.L = L
         L.okref_allreduce.restype = c_int
         L.okref_topka.restype = c_int
+        L.okref_baseline.restype = c_int
+        L.okref_gaussian_threshold.restype = c_double
+        L.okref_gaussian_threshold.argtypes = [POINTER(c_double), c_size_t, c_size_t, c_int]
         L.okref_th_re_evaluate_dense.restype = c_double
         L.okref_th_re_evaluate_dense.argtypes = [POINTER(c_double), c_size_t, c_size_t]
         L.okref_drift_f32.restype = None
@@ -317,6 +352,28 @@ class Reference(_Common):
         if rc:
             raise RuntimeError(f"okref_topka rc={rc}: {self.err.value.decode(errors='replace')}")
         return oi[:U.value].copy(), ov[:U.value].copy()
+
+    def baseline(self, which: str, inputs: Sequence[np.ndarray], k: int, scale_to_floor: bool = True,
+                 ledger: np.ndarray = None):
+        P = len(inputs)
+        g = [np.ascontiguousarray(x, dtype=np.float64) for x in inputs]
+        n = g[0].size
+        cap = max(P * n, 1)
+        oi = np.empty(cap, np.uint32)
+        ov = np.empty(cap, np.float64)
+        U = c_size_t(0)
+        led = ledger if ledger is not None else np.zeros((P, 6, 4), np.uint64)
+        code = {"gtopk": 0, "topkdsa": 1, "gaussiank": 2 if scale_to_floor else 3}[which]
+        rc = self.L.okref_baseline(c_int(code), c_int(P), _ptrs(g, c_double), c_size_t(n), c_size_t(k),
+                                   oi.ctypes.data_as(POINTER(c_uint32)), ov.ctypes.data_as(POINTER(c_double)),
+                                   ctypes.byref(U), led.ctypes.data_as(POINTER(Counters)), self.err, c_size_t(512))
+        if rc:
+            raise RuntimeError(f"okref_baseline rc={rc}: {self.err.value.decode(errors='replace')}")
+        return oi[:U.value].copy(), ov[:U.value].copy()
+
+    def gaussian_threshold(self, g: np.ndarray, k: int, scale_to_floor: bool = True) -> float:
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        return self.L.okref_gaussian_threshold(g.ctypes.data_as(POINTER(c_double)), g.size, k, int(scale_to_floor))
 
     def th_re_evaluate(self, g: np.ndarray, k: int) -> float:
         g = np.ascontiguousarray(g, dtype=np.float64)

@@ -306,4 +306,46 @@ int okref_topka(int P, const double* const* g, size_t n, size_t k, uint32_t* u_i
   return 0;
 }
 
+// gtopk (0) / topkdsa (1) / gaussiank (2, scaled) / gaussiank (3, raw) on P rank threads.
+int okref_baseline(int which, int P, const double* const* g, size_t n, size_t k, uint32_t* u_idx, double* u_val,
+                   size_t* U, okref_counters* ledger, char* err, size_t errlen) {
+  InprocTransport tr(P, 64);
+  TrafficLedger led(P);
+  std::vector<SparseGrad> res(P);
+  const int rc = run_ranks(
+      tr, P,
+      [&](int r) {
+        WorkerCtx ctx{r, P, &tr, &led};
+        DenseGrad dg(std::vector<double>(g[r], g[r] + n));
+        if (which == 0) res[r] = gtopk_allreduce(ctx, dg, k);
+        else if (which == 1) res[r] = topkdsa_allreduce(ctx, dg, k);
+        else res[r] = gaussiank_allreduce(ctx, dg, k, GaussiankOptions{which == 2});
+      },
+      err, errlen);
+  for (int r = 0; r < P && ledger; ++r)
+    for (int ph = 0; ph < kPhaseCount; ++ph) {
+      const auto& c = led.at(r, static_cast<Phase>(ph));
+      okref_counters& o = ledger[r * kPhaseCount + ph];
+      o.words_sent += c.words_sent;
+      o.words_recv += c.words_recv;
+      o.msgs_sent += c.msgs_sent;
+      o.msgs_recv += c.msgs_recv;
+    }
+  if (rc) return rc;
+  for (int r = 1; r < P; ++r)
+    if (res[r] != res[0]) {
+      std::snprintf(err, errlen, "ranks disagree on u");
+      return 8;
+    }
+  *U = res[0].nnz();
+  std::memcpy(u_idx, res[0].indices.data(), res[0].nnz() * sizeof(uint32_t));
+  std::memcpy(u_val, res[0].values.data(), res[0].nnz() * sizeof(double));
+  return 0;
+}
+
+double okref_gaussian_threshold(const double* g, size_t n, size_t k, int scale_to_floor) {
+  DenseGrad dg(std::vector<double>(g, g + n));
+  return scale_to_floor ? gaussiank_scaled_threshold(dg, k) : gaussian_threshold(dg, k);
+}
+
 }  // extern "C"

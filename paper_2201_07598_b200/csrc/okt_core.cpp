@@ -194,7 +194,10 @@ struct okt_comm {
   Buf gval;                // gathered region values (refresh)
   Buf u_idx, u_val;        // allgathered result
   Buf sel_idx, sel_val;    // sub-phase outputs
-  Buf tk_aux, tk_parts;    // TopkA: trim chunk counts / gathered exact top-k parts (AoS)
+  Buf tk_aux, tk_parts;    // baselines: chunk counts / offsets, gathered AoS parts
+  Buf bl_ai, bl_av, bl_bi, bl_bv, bl_ci, bl_cv;  // baselines: SoA working lists
+  Buf bl_ti, bl_tv;        // baselines: merge positions
+  Buf bl_win, bl_win_in, bl_small;  // TopkDSA windows; small scratch
   Buf indexes;
   Buf eps[2];
   Buf hgrad;               // staging for the host-buffer entry points
@@ -2005,22 +2008,83 @@ int okt_balance_and_allgatherv(okt_comm* c, const uint32_t* d_idx, const double*
   return OKT_OK;
 }
 
-// ---- Table-1 baseline: TopkA -----------------------------------------------------------
-// topka_allreduce (collectives.cpp:152-159): exact local top-k (topk_exact,
-// sparse.cpp:43-80 — magnitude-descending, ties toward the smaller index),
-// sparse_allgatherv of the P parts, sparse_sum (sparse.cpp:241-257).  On the
-// GPU: K2 radix select of the exact k-th magnitude, K1 select of {|g| >= th},
-// the tie trim (okt_topk.cu), one all-pairs exchange of the k-entry parts and
-// the region merge (scatter + bracket-sum scan) over the whole vector.
-int okt_topka_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt_sparse* out, void* stream) {
-  OKT_COMM_CHECK(c);
-  if (!out) return set_err(OKT_ERR_INVALID_ARGUMENT, "topka_allreduce: null output");
-  if (k < 1 || k > n) return set_err(OKT_ERR_INVALID_ARGUMENT, "topk_exact: k must be in [1, n]");
-  if (n > 0xffffffffull) return set_err(OKT_ERR_INVALID_ARGUMENT, "topka_allreduce: n exceeds 32-bit indices");
-  DeviceGuard g(c->device);
-  cudaStream_t s = c->pick(stream);
-  c->L.s = s;
-  const int P = c->P, rank = c->rank;
+// ---- Table-1 baselines (collectives.cpp:152-354) ---------------------------------------
+// TopkA, gTopk, TopkDSA and Gaussiank on the GPU: the comparison collectives
+// of the paper's Table 1.  They are host-orchestrated (a sync per exchange
+// round, as the reference's blocking send/recv) and exact against the
+// reference: the same selections, the same combination trees and the same
+// fp64 adds.  Kernels in okt_baselines.cu; exchanges over the comm's
+// transport; ledger credited as the reference's Message words (ints + reals).
+namespace {
+
+struct SpRef {  // a device SoA sparse list
+  uint32_t* idx = nullptr;
+  double* val = nullptr;
+  uint64_t nnz = 0;
+};
+
+// Exclusive prefix of per-chunk counts, uploaded next to them; returns the total.
+int bl_prefix(okt_comm* c, const uint32_t* d_cnt, uint64_t chunks, uint64_t* d_off, uint64_t& total,
+              cudaStream_t s) {
+  std::vector<uint32_t> hc(chunks);
+  int rc = c->ck(cudaMemcpyAsync(hc.data(), d_cnt, 4 * chunks, cudaMemcpyDeviceToHost, s), "d2h");
+  if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  std::vector<uint64_t> ho(chunks);
+  uint64_t pos = 0;
+  for (uint64_t i = 0; i < chunks; ++i) {
+    ho[i] = pos;
+    pos += hc[i];
+  }
+  total = pos;
+  rc = c->ck(cudaMemcpyAsync(d_off, ho.data(), 8 * chunks, cudaMemcpyHostToDevice, s), "h2d");
+  if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  return OKT_OK;
+}
+
+uint64_t bl_chunks(uint64_t m) { return (m + okt::kTopkTrimChunk - 1) / okt::kTopkTrimChunk; }
+
+// topk_exact's trim of a selection whose k-th largest magnitude is th: every
+// |v| > th, then the first k - #gt ties.  Source: AoS f32 (aos_in) or SoA f64.
+int bl_trim(okt_comm* c, const uint64_t* aos_in, const uint32_t* idx_in, const double* val_in, uint64_t m,
+            double th, uint64_t k, uint64_t* aos_out, uint32_t* idx_out, double* val_out, cudaStream_t s) {
+  const uint64_t chunks = bl_chunks(m);
+  int rc = c->ensure(c->tk_aux, 24 * std::max<uint64_t>(chunks, 1));
+  if (rc) return rc;
+  uint32_t* gt = c->tk_aux.as<uint32_t>();
+  uint32_t* eq = gt + chunks;
+  uint64_t* off = reinterpret_cast<uint64_t*>(c->tk_aux.as<char>() + 8 * chunks);
+  uint64_t* eqb = off + chunks;
+  rc = c->ck(okt::launch_topk_count(c->L, aos_in, idx_in, val_in, m, th, gt, eq), "topk_count");
+  if (rc) return rc;
+  std::vector<uint32_t> hc(2 * chunks);
+  if ((rc = c->ck(cudaMemcpyAsync(hc.data(), gt, 8 * chunks, cudaMemcpyDeviceToHost, s), "d2h"))) return rc;
+  if ((rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  uint64_t n_gt = 0;
+  for (uint64_t i = 0; i < chunks; ++i) n_gt += hc[i];
+  if (n_gt >= k) return set_err(OKT_ERR_INTERNAL, "topk_exact: threshold above the k-th magnitude");
+  const uint64_t need = k > n_gt ? k - n_gt : 0;
+  std::vector<uint64_t> ho(2 * chunks);
+  uint64_t pos = 0, eq_seen = 0;
+  for (uint64_t i = 0; i < chunks; ++i) {
+    ho[i] = pos;
+    ho[chunks + i] = eq_seen;
+    const uint64_t keep_eq = eq_seen >= need ? 0 : std::min<uint64_t>(hc[chunks + i], need - eq_seen);
+    pos += hc[i] + keep_eq;
+    eq_seen += hc[chunks + i];
+  }
+  if (pos != k) return set_err(OKT_ERR_INTERNAL, "topk_exact: tie trim miscounted");
+  if ((rc = c->ck(cudaMemcpyAsync(off, ho.data(), 16 * chunks, cudaMemcpyHostToDevice, s), "h2d"))) return rc;
+  rc = c->ck(okt::launch_topk_write(c->L, aos_in, idx_in, val_in, m, th, off, eqb, need, aos_out, idx_out, val_out),
+             "topk_write");
+  if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  return OKT_OK;
+}
+
+// Local exact top-k of a dense fp32 gradient (topk_exact, sparse.cpp:75-80):
+// radix select of the k-th magnitude, K1 select {|g| >= th} into coo, trim.
+// `bad` reports a non-finite gradient (the trim is then skipped).
+int bl_local_topk(okt_comm* c, const float* d_g, uint64_t n, uint64_t k, uint64_t* aos_out, uint32_t* idx_out,
+                  double* val_out, bool& bad, cudaStream_t s) {
   int rc = c->reserve(n);
   if (rc) return rc;
   rc = c->ck(cudaMemsetAsync(&c->d()->flags, 0, 4, s), "memset");
@@ -2032,96 +2096,61 @@ int okt_topka_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt_s
                               nullptr, okt::OutCoo{c->coo.as<uint64_t>(), nullptr, nullptr}, &c->d()->m, nullptr,
                               &c->d()->flags, nullptr), "k1");
   if (rc || (rc = c->sync(s))) return rc;
-  const bool bad = (c->h->flags & 1u) != 0;
-  const uint64_t m = c->h->m;
-  const float th = float(c->h->th_arg);
-  std::string err;
-  if (P > 1) {
-    // every rank's part size (and health) before any data moves
-    c->hup->small[0] = uint32_t(k);
-    c->hup->small[1] = bad ? 1u : 0u;
-    if ((rc = c->ck(cudaMemcpyAsync(&c->d()->small[0], &c->hup->small[0], 8, cudaMemcpyHostToDevice, s), "h2d")))
-      return rc;
-    rc = c->tr->allgather(&c->d()->small[0], c->d()->small_all, 8, s, err);
-    if (rc) return c->comm_err(rc, err);
-    if ((rc = c->sync(s))) return rc;
-    for (int q = 0; q < P; ++q) {
-      if (c->h->small_all[2 * q + 1]) {
-        if (q == rank) return set_err(OKT_ERR_NUMERIC, "topka_allreduce: non-finite input");
-        return set_err(OKT_ERR_TRANSPORT,
-                       "TransportError: rank " + std::to_string(q) + " failed (non-finite input)");
-      }
-      if (c->h->small_all[2 * q] != uint32_t(k))
-        return set_err(OKT_ERR_PROTOCOL, "topka_allreduce: ranks disagree on k");
-    }
-  } else if (bad) {
-    return set_err(OKT_ERR_NUMERIC, "topka_allreduce: non-finite input");
-  }
-  if (m < k) return set_err(OKT_ERR_INTERNAL, "topka_allreduce: selection smaller than k");
-  // Exact top-k of the selection: all |v| > th, then the first (k - #gt) ties.
-  uint64_t* parts = nullptr;
-  if ((rc = c->ensure(c->tk_parts, 8 * k * size_t(P)))) return rc;
-  parts = c->tk_parts.as<uint64_t>();
-  uint64_t* mine = parts + k * uint64_t(rank);
+  bad = (c->h->flags & 1u) != 0;
+  if (bad) return OKT_OK;
+  if (c->h->m < k) return set_err(OKT_ERR_INTERNAL, "topk_exact: selection smaller than k");
+  return bl_trim(c, c->coo.as<uint64_t>(), nullptr, nullptr, c->h->m, c->h->th_arg, k, aos_out, idx_out, val_out,
+                 s);
+}
+
+// Every rank's (count, health) before any data moves; a non-finite rank fails
+// with NumericError, the others with TransportError (the reference's abort).
+int bl_agree(okt_comm* c, const char* who, uint64_t count, bool bad, std::vector<uint64_t>& counts, cudaStream_t s) {
+  const int P = c->P;
+  counts.assign(P, 0);
   if (P == 1) {
-    if ((rc = c->ensure(c->sel_idx, 4 * k)) || (rc = c->ensure(c->sel_val, 8 * k))) return rc;
-  }
-  if (m == k && P > 1) {
-    rc = c->ck(cudaMemcpyAsync(mine, c->coo.p, 8 * k, cudaMemcpyDeviceToDevice, s), "copy");
-    if (rc) return rc;
-  } else {
-    const uint64_t chunks = (m + okt::kTopkTrimChunk - 1) / okt::kTopkTrimChunk;
-    if ((rc = c->ensure(c->tk_aux, 24 * chunks))) return rc;
-    uint32_t* gt = c->tk_aux.as<uint32_t>();
-    uint32_t* eq = gt + chunks;
-    uint64_t* off = reinterpret_cast<uint64_t*>(c->tk_aux.as<char>() + 8 * chunks);
-    uint64_t* eqb = off + chunks;
-    rc = c->ck(okt::launch_topk_count(c->L, c->coo.as<uint64_t>(), m, th, gt, eq), "topk_count");
-    if (rc) return rc;
-    std::vector<uint32_t> hc(2 * chunks);
-    if ((rc = c->ck(cudaMemcpyAsync(hc.data(), gt, 8 * chunks, cudaMemcpyDeviceToHost, s), "d2h"))) return rc;
-    if ((rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
-    uint64_t n_gt = 0;
-    for (uint64_t i = 0; i < chunks; ++i) n_gt += hc[i];
-    if (n_gt >= k) return set_err(OKT_ERR_INTERNAL, "topka_allreduce: threshold above the k-th magnitude");
-    const uint64_t need = k - n_gt;
-    std::vector<uint64_t> ho(2 * chunks);
-    uint64_t pos = 0, eq_seen = 0;
-    for (uint64_t i = 0; i < chunks; ++i) {
-      ho[i] = pos;
-      ho[chunks + i] = eq_seen;
-      const uint64_t keep_eq = eq_seen >= need ? 0 : std::min<uint64_t>(hc[chunks + i], need - eq_seen);
-      pos += hc[i] + keep_eq;
-      eq_seen += hc[chunks + i];
-    }
-    if (pos != k) return set_err(OKT_ERR_INTERNAL, "topka_allreduce: tie trim miscounted");
-    if ((rc = c->ck(cudaMemcpyAsync(off, ho.data(), 16 * chunks, cudaMemcpyHostToDevice, s), "h2d"))) return rc;
-    rc = c->ck(okt::launch_topk_write(c->L, c->coo.as<uint64_t>(), m, th, off, eqb, need,
-                                      P > 1 ? mine : nullptr, P == 1 ? c->sel_idx.as<uint32_t>() : nullptr,
-                                      P == 1 ? c->sel_val.as<double>() : nullptr), "topk_write");
-    if (rc) return rc;
-    // the pageable H2D above has been consumed once the stream passes this point
-    if ((rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
-  }
-  if (P == 1) {
-    out->d_idx = c->sel_idx.as<uint32_t>();
-    out->d_val = c->sel_val.as<double>();
-    out->nnz = k;
-    out->n = n;
+    if (bad) return set_err(OKT_ERR_NUMERIC, std::string(who) + ": non-finite input");
+    counts[0] = count;
     return OKT_OK;
   }
-  // sparse_allgatherv: every part to every peer (one exchange, all pairs).
+  c->hup->small[0] = uint32_t(count);
+  c->hup->small[1] = bad ? 1u : 0u;
+  int rc = c->ck(cudaMemcpyAsync(&c->d()->small[0], &c->hup->small[0], 8, cudaMemcpyHostToDevice, s), "h2d");
+  if (rc) return rc;
+  std::string err;
+  rc = c->tr->allgather(&c->d()->small[0], c->d()->small_all, 8, s, err);
+  if (rc) return c->comm_err(rc, err);
+  if ((rc = c->sync(s))) return rc;
+  for (int q = 0; q < P; ++q) {
+    if (c->h->small_all[2 * q + 1]) {
+      if (q == c->rank) return set_err(OKT_ERR_NUMERIC, std::string(who) + ": non-finite input");
+      return set_err(OKT_ERR_TRANSPORT, "TransportError: rank " + std::to_string(q) + " failed (non-finite input)");
+    }
+    counts[q] = c->h->small_all[2 * q];
+  }
+  return OKT_OK;
+}
+
+// sparse_allgatherv of AoS f32 parts (counts[q] entries each, parts laid out
+// back to back by rank) + sparse_sum (stride-doubling bracket) via the region
+// merge over [0, n).  Result in sel_idx/sel_val.
+int bl_allgather_sum_aos(okt_comm* c, uint64_t n, const std::vector<uint64_t>& counts, okt_sparse* out,
+                         cudaStream_t s) {
+  const int P = c->P, rank = c->rank;
+  std::vector<uint64_t> off(P + 1, 0);
+  for (int q = 0; q < P; ++q) off[q + 1] = off[q] + counts[q];
+  uint64_t* parts = c->tk_parts.as<uint64_t>();
   std::vector<Xfer> sends, recvs;
   for (int q = 0; q < P; ++q) {
     if (q == rank) continue;
-    sends.push_back({q, mine, 8 * k});
-    recvs.push_back({q, parts + k * uint64_t(q), 8 * k});
+    sends.push_back({q, parts + off[rank], 8 * counts[rank]});
+    recvs.push_back({q, parts + off[q], 8 * counts[q]});
   }
-  rc = c->tr->exchange(sends, recvs, s, err);
+  std::string err;
+  int rc = c->tr->exchange(sends, recvs, s, err);
   if (rc) return c->comm_err(rc, err);
-  c->credit_allgatherv(OKT_PHASE_ALLGATHERV, std::vector<uint64_t>(P, k), 12);
-  // sparse_sum: region merge over [0, n) with the P parts as sources.
-  const uint64_t bound = k * uint64_t(P);
+  c->credit_allgatherv(OKT_PHASE_ALLGATHERV, counts, 12);
+  const uint64_t bound = std::max<uint64_t>(off[P], 1);
   if ((rc = c->ensure(c->mask, ((n + 15) / 16) * 16 + 16)) || (rc = c->ensure(c->stage, 4 * n * size_t(P))) ||
       (rc = c->ensure(c->sel_idx, 4 * bound)) || (rc = c->ensure(c->sel_val, 8 * bound)))
     return rc;
@@ -2129,12 +2158,12 @@ int okt_topka_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt_s
   segs.nseg = P;
   segs.start[0] = 0;
   for (int q = 0; q < P; ++q) {
-    segs.ptr[q] = parts + k * uint64_t(q);
+    segs.ptr[q] = parts + off[q];
     segs.src[q] = q;
-    segs.start[q + 1] = segs.start[q] + k;
+    segs.start[q + 1] = off[q + 1];
   }
-  rc = c->ck(okt::launch_scatter(c->L, segs, 0, n, P, c->mask.as<uint32_t>(), c->stage.as<float>(),
-                                 &c->d()->flags), "scatter");
+  rc = c->ck(okt::launch_scatter(c->L, segs, 0, n, P, c->mask.as<uint32_t>(), c->stage.as<float>(), &c->d()->flags),
+             "scatter");
   if (!rc)
     rc = c->ck(okt::launch_region_scan(c->L, c->S, P, false, 0, n, c->mask.as<uint32_t>(), c->stage.as<float>(),
                                        nullptr, c->sel_idx.as<uint32_t>(), c->sel_val.as<double>(), &c->d()->R),
@@ -2145,6 +2174,436 @@ int okt_topka_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt_s
   out->nnz = c->h->R;
   out->n = n;
   return OKT_OK;
+}
+
+// merge_two (sparse.cpp:206-237) of two sorted SoA lists into `o` (capacity
+// a.nnz + b.nnz); returns o.nnz.
+int bl_merge(okt_comm* c, const SpRef& a, const SpRef& b, SpRef& o, cudaStream_t s) {
+  const uint64_t N = a.nnz + b.nnz;
+  int rc;
+  if ((rc = c->ensure(c->bl_ti, 4 * std::max<uint64_t>(N, 1))) || (rc = c->ensure(c->bl_tv, 8 * std::max<uint64_t>(N, 1))))
+    return rc;
+  const uint64_t chunks = bl_chunks(N);
+  if ((rc = c->ensure(c->tk_aux, 24 * std::max<uint64_t>(chunks, 1)))) return rc;
+  uint32_t* cnt = c->tk_aux.as<uint32_t>();
+  uint64_t* off = reinterpret_cast<uint64_t*>(c->tk_aux.as<char>() + 8 * chunks);
+  uint32_t* ti = c->bl_ti.as<uint32_t>();
+  double* tv = c->bl_tv.as<double>();
+  rc = c->ck(okt::launch_merge_rank(c->L, a.idx, a.val, a.nnz, b.idx, b.val, b.nnz, ti, tv), "merge_rank");
+  if (!rc) rc = c->ck(okt::launch_merge_heads(c->L, ti, tv, N, cnt, nullptr, nullptr, nullptr), "merge_count");
+  uint64_t total = 0;
+  if (rc || (rc = bl_prefix(c, cnt, chunks, off, total, s))) return rc;
+  rc = c->ck(okt::launch_merge_heads(c->L, ti, tv, N, nullptr, off, o.idx, o.val), "merge_write");
+  o.nnz = total;
+  return rc;
+}
+
+// One send and one receive with `partner` (the reference's paired send/recv).
+int bl_swap(okt_comm* c, int partner, const std::vector<std::pair<const void*, size_t>>& out,
+            const std::vector<std::pair<void*, size_t>>& in, cudaStream_t s) {
+  std::vector<Xfer> sends, recvs;
+  for (auto& x : out) sends.push_back({partner, const_cast<void*>(x.first), x.second});
+  for (auto& x : in) recvs.push_back({partner, x.first, x.second});
+  std::string err;
+  int rc = c->tr->exchange(sends, recvs, s, err);
+  if (rc) return c->comm_err(rc, err);
+  return OKT_OK;
+}
+
+int bl_check(okt_comm* c, const char* who, const float* d_g, size_t n, size_t k, okt_sparse* out) {
+  (void)c;
+  if (!out || (!d_g && n)) return set_err(OKT_ERR_INVALID_ARGUMENT, std::string(who) + ": null argument");
+  if (k < 1 || k > n) return set_err(OKT_ERR_INVALID_ARGUMENT, "topk_exact: k must be in [1, n]");
+  if (n > 0xffffffffull) return set_err(OKT_ERR_INVALID_ARGUMENT, std::string(who) + ": n exceeds 32-bit indices");
+  return OKT_OK;
+}
+
+void bl_credit_pair(okt_comm* c, int ph, uint64_t sent_words, uint64_t recv_words) {
+  okt::plan::credit(c->ledger[ph], true, sent_words, 1);
+  okt::plan::credit(c->ledger[ph], false, recv_words, 1);
+}
+
+// Acklam's rational approximation of the standard normal quantile, refined by
+// two Halley steps on the erfc-based CDF (the reference's inverse_normal_cdf,
+// sparse.cpp:122-165).
+double inverse_normal_cdf(double p) {
+  static const double A[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                             1.383577518672690e+02,  -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double B[] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                             6.680131188771972e+01,  -1.328068155288572e+01};
+  static const double C[] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                             -2.549732539343734e+00, 4.374664141464968e+00,  2.938163982698783e+00};
+  static const double D[] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                             3.754408661907416e+00};
+  const double plow = 0.02425;
+  auto tail = [&](double q) {
+    return (((((C[0] * q + C[1]) * q + C[2]) * q + C[3]) * q + C[4]) * q + C[5]) /
+           ((((D[0] * q + D[1]) * q + D[2]) * q + D[3]) * q + 1.0);
+  };
+  double x;
+  if (p < plow) {
+    x = tail(std::sqrt(-2.0 * std::log(p)));
+  } else if (p <= 1.0 - plow) {
+    const double q = p - 0.5, r = q * q;
+    x = (((((A[0] * r + A[1]) * r + A[2]) * r + A[3]) * r + A[4]) * r + A[5]) * q /
+        (((((B[0] * r + B[1]) * r + B[2]) * r + B[3]) * r + B[4]) * r + 1.0);
+  } else {
+    x = -tail(std::sqrt(-2.0 * std::log(1.0 - p)));
+  }
+  const double sqrt2pi = 2.5066282746310005;
+  for (int it = 0; it < 2; ++it) {
+    const double e = 0.5 * std::erfc(-x / std::sqrt(2.0)) - p;
+    const double u = e * sqrt2pi * std::exp(x * x / 2.0);
+    x = x - u / (1.0 + x * u / 2.0);
+  }
+  return x;
+}
+
+}  // namespace
+
+// topka_allreduce (collectives.cpp:152-159): exact local top-k, sparse_allgatherv,
+// sparse_sum.
+int okt_topka_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt_sparse* out, void* stream) {
+  OKT_COMM_CHECK(c);
+  int rc = bl_check(c, "topka_allreduce", d_g, n, k, out);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  const int P = c->P;
+  if ((rc = c->ensure(c->tk_parts, 8 * k * size_t(P)))) return rc;
+  if (P == 1 && ((rc = c->ensure(c->sel_idx, 4 * k)) || (rc = c->ensure(c->sel_val, 8 * k)))) return rc;
+  bool bad = false;
+  rc = bl_local_topk(c, d_g, n, k, P > 1 ? c->tk_parts.as<uint64_t>() + k * uint64_t(c->rank) : nullptr,
+                     P == 1 ? c->sel_idx.as<uint32_t>() : nullptr, P == 1 ? c->sel_val.as<double>() : nullptr, bad,
+                     s);
+  if (rc) return rc;
+  std::vector<uint64_t> counts;
+  if ((rc = bl_agree(c, "topka_allreduce", k, bad, counts, s))) return rc;
+  for (int q = 0; q < P; ++q)
+    if (counts[q] != k) return set_err(OKT_ERR_PROTOCOL, "topka_allreduce: ranks disagree on k");
+  if (P == 1) {
+    *out = okt_sparse{c->sel_idx.as<uint32_t>(), c->sel_val.as<double>(), k, n};
+    return OKT_OK;
+  }
+  return bl_allgather_sum_aos(c, n, counts, out, s);
+}
+
+// gtopk_allreduce (collectives.cpp:300-325): log2 P rounds of pairwise
+// exchange; each rank sums its k entries with its partner's (merge_two) and
+// keeps the exact top-k of the sum.  Every list has exactly k entries.
+int okt_gtopk_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt_sparse* out, void* stream) {
+  OKT_COMM_CHECK(c);
+  int rc = bl_check(c, "gtopk_allreduce", d_g, n, k, out);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  const int P = c->P, rank = c->rank;
+  if ((rc = c->ensure(c->bl_ai, 4 * k)) || (rc = c->ensure(c->bl_av, 8 * k)) || (rc = c->ensure(c->bl_bi, 4 * k)) ||
+      (rc = c->ensure(c->bl_bv, 8 * k)) || (rc = c->ensure(c->bl_ci, 8 * k)) || (rc = c->ensure(c->bl_cv, 16 * k)))
+    return rc;
+  SpRef A{c->bl_ai.as<uint32_t>(), c->bl_av.as<double>(), k};
+  SpRef B{c->bl_bi.as<uint32_t>(), c->bl_bv.as<double>(), k};
+  SpRef C{c->bl_ci.as<uint32_t>(), c->bl_cv.as<double>(), 0};
+  bool bad = false;
+  if ((rc = bl_local_topk(c, d_g, n, k, nullptr, A.idx, A.val, bad, s))) return rc;
+  std::vector<uint64_t> counts;
+  if ((rc = bl_agree(c, "gtopk_allreduce", k, bad, counts, s))) return rc;
+  for (int q = 0; q < P; ++q)
+    if (counts[q] != k) return set_err(OKT_ERR_PROTOCOL, "gtopk_allreduce: ranks disagree on k");
+  for (int level = 0; (1 << level) < P; ++level) {
+    const int partner = rank ^ (1 << level);
+    rc = bl_swap(c, partner, {{A.idx, 4 * k}, {A.val, 8 * k}}, {{B.idx, 4 * k}, {B.val, 8 * k}}, s);
+    if (rc) return rc;
+    bl_credit_pair(c, OKT_PHASE_SPLIT, 2 * k, 2 * k);
+    if ((rc = bl_merge(c, A, B, C, s))) return rc;
+    // topk_exact(SparseGrad, k), sparse.cpp:82-92: C.nnz >= k always.
+    rc = c->ck(okt::launch_radix_select(c->L, okt::RadixSrc::kF64, C.val, C.nnz, nullptr, C.nnz, k, &c->d()->rs,
+                                        c->hist.as<uint32_t>(), &c->d()->th_arg, false), "radix");
+    if (rc || (rc = c->sync(s))) return rc;
+    if ((rc = bl_trim(c, nullptr, C.idx, C.val, C.nnz, c->h->th_arg, k, nullptr, A.idx, A.val, s))) return rc;
+  }
+  if ((rc = c->ensure(c->sel_idx, 4 * k)) || (rc = c->ensure(c->sel_val, 8 * k))) return rc;
+  rc = c->ck(cudaMemcpyAsync(c->sel_idx.p, A.idx, 4 * k, cudaMemcpyDeviceToDevice, s), "copy");
+  if (!rc) rc = c->ck(cudaMemcpyAsync(c->sel_val.p, A.val, 8 * k, cudaMemcpyDeviceToDevice, s), "copy");
+  if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  *out = okt_sparse{c->sel_idx.as<uint32_t>(), c->sel_val.as<double>(), k, n};
+  return OKT_OK;
+}
+
+// topkdsa_allreduce (collectives.cpp:184-297): recursive-halving reduce-scatter
+// of the exact local top-k whose working set switches from COO to a dense fp64
+// window once 2·nnz >= the window width, then sparse_allgatherv of the owned
+// segments (disjoint, ascending: concatenation is the sum).
+int okt_topkdsa_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt_sparse* out, void* stream) {
+  OKT_COMM_CHECK(c);
+  int rc = bl_check(c, "topkdsa_allreduce", d_g, n, k, out);
+  if (rc) return rc;
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  const int P = c->P, rank = c->rank;
+  // two COO ping-pong sets of capacity n, a partner COO, two dense windows
+  if ((rc = c->ensure(c->bl_ai, 4 * n)) || (rc = c->ensure(c->bl_av, 8 * n)) || (rc = c->ensure(c->bl_ci, 4 * n)) ||
+      (rc = c->ensure(c->bl_cv, 8 * n)) || (rc = c->ensure(c->bl_bi, 4 * n)) || (rc = c->ensure(c->bl_bv, 8 * n)) ||
+      (rc = c->ensure(c->bl_win, 8 * n)) || (rc = c->ensure(c->bl_win_in, 8 * n)) || (rc = c->ensure(c->bl_small, 64)))
+    return rc;
+  SpRef A{c->bl_ai.as<uint32_t>(), c->bl_av.as<double>(), k};
+  SpRef B{c->bl_bi.as<uint32_t>(), c->bl_bv.as<double>(), 0};
+  bool bad = false;
+  if ((rc = bl_local_topk(c, d_g, n, k, nullptr, A.idx, A.val, bad, s))) return rc;
+  std::vector<uint64_t> counts;
+  if ((rc = bl_agree(c, "topkdsa_allreduce", k, bad, counts, s))) return rc;
+  if (P == 1) {
+    if ((rc = c->ensure(c->sel_idx, 4 * k)) || (rc = c->ensure(c->sel_val, 8 * k))) return rc;
+    rc = c->ck(cudaMemcpyAsync(c->sel_idx.p, A.idx, 4 * k, cudaMemcpyDeviceToDevice, s), "copy");
+    if (!rc) rc = c->ck(cudaMemcpyAsync(c->sel_val.p, A.val, 8 * k, cudaMemcpyDeviceToDevice, s), "copy");
+    if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+    *out = okt_sparse{c->sel_idx.as<uint32_t>(), c->sel_val.as<double>(), k, n};
+    return OKT_OK;
+  }
+  const std::vector<uint64_t> ends = equal_slice_ends(n, P);
+  bool dense = false;
+  double* wbase = nullptr;  // window over [win_lo, win_hi)
+  uint64_t win_lo = 0, win_hi = 0;
+  auto densify = [&](uint64_t lo, uint64_t hi) -> int {  // dsa_densify, collectives.cpp:172-182
+    wbase = c->bl_win.as<double>();
+    int r = c->ck(cudaMemsetAsync(wbase, 0, 8 * (hi - lo), s), "memset");
+    if (!r) r = c->ck(okt::launch_window_scatter(c->L, A.idx, A.val, A.nnz, lo, wbase, false), "densify");
+    win_lo = lo;
+    win_hi = hi;
+    dense = true;
+    A.nnz = 0;
+    return r;
+  };
+  uint64_t* hb = reinterpret_cast<uint64_t*>(&c->hup->prop[0]);  // 4 words of pinned staging
+  int lo = 0, hi = P;
+  for (int mask = P >> 1; mask > 0; mask >>= 1) {
+    const int partner = rank ^ mask, mid = lo + mask;
+    int keep_lo, keep_hi, send_lo, send_hi;
+    if ((rank & mask) == 0) {
+      keep_lo = lo; keep_hi = mid; send_lo = mid; send_hi = hi;
+    } else {
+      keep_lo = mid; keep_hi = hi; send_lo = lo; send_hi = mid;
+    }
+    const uint64_t s0 = ends[send_lo], s1 = ends[send_hi], k0 = ends[keep_lo], k1 = ends[keep_hi];
+    // sparse_slice bounds of the send and keep halves
+    uint64_t a_s0 = 0, a_s1 = 0, a_k0 = 0, a_k1 = 0;
+    if (!dense) {
+      uint64_t* sb = c->bl_small.as<uint64_t>();
+      rc = c->ck(okt::launch_slice_bounds(c->L, A.idx, A.nnz, s0, s1, sb), "slice");
+      if (!rc) rc = c->ck(okt::launch_slice_bounds(c->L, A.idx, A.nnz, k0, k1, sb + 2), "slice");
+      if (!rc) rc = c->ck(cudaMemcpyAsync(hb, sb, 32, cudaMemcpyDeviceToHost, s), "d2h");
+      if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+      a_s0 = hb[0]; a_s1 = hb[1]; a_k0 = hb[2]; a_k1 = hb[3];
+    }
+    // header {kind, count}: 1 = dense half, 0 = COO
+    const uint32_t my_kind = dense ? 1u : 0u;
+    const uint64_t my_cnt = dense ? s1 - s0 : a_s1 - a_s0;
+    c->hup->small[0] = my_kind;
+    c->hup->small[1] = uint32_t(my_cnt);
+    if ((rc = c->ck(cudaMemcpyAsync(&c->d()->small[0], &c->hup->small[0], 8, cudaMemcpyHostToDevice, s), "h2d")))
+      return rc;
+    rc = bl_swap(c, partner, {{&c->d()->small[0], 8}}, {{&c->d()->small_all[0], 8}}, s);
+    if (rc) return rc;
+    if ((rc = c->sync(s))) return rc;
+    const uint32_t th_kind = c->h->small_all[0];
+    const uint64_t th_cnt = c->h->small_all[1];
+    if (th_kind == 1 && th_cnt != k1 - k0) return set_err(OKT_ERR_PROTOCOL, "topkdsa: dense half length mismatch");
+    std::vector<std::pair<const void*, size_t>> outs;
+    std::vector<std::pair<void*, size_t>> ins;
+    if (dense) outs.push_back({wbase + (s0 - win_lo), 8 * my_cnt});
+    else outs = {{A.idx + a_s0, 4 * my_cnt}, {A.val + a_s0, 8 * my_cnt}};
+    if (th_kind == 1) ins.push_back({c->bl_win_in.p, 8 * th_cnt});
+    else ins = {{B.idx, 4 * th_cnt}, {B.val, 8 * th_cnt}};
+    if ((rc = bl_swap(c, partner, outs, ins, s))) return rc;
+    bl_credit_pair(c, OKT_PHASE_SPLIT, dense ? my_cnt : 2 * my_cnt, th_kind == 1 ? th_cnt : 2 * th_cnt);
+    // restrict the working set to the kept half
+    if (dense) {
+      wbase += k0 - win_lo;
+      win_lo = k0;
+      win_hi = k1;
+    } else {
+      A.idx += a_k0;
+      A.val += a_k0;
+      A.nnz = a_k1 - a_k0;
+    }
+    // fold in the partner's contribution
+    if (th_kind == 1) {
+      if (!dense && (rc = densify(k0, k1))) return rc;
+      if ((rc = c->ck(okt::launch_window_add(c->L, wbase, c->bl_win_in.as<double>(), k1 - k0), "window_add")))
+        return rc;
+    } else {
+      B.nnz = th_cnt;
+      if (dense) {
+        if ((rc = c->ck(okt::launch_window_scatter(c->L, B.idx, B.val, B.nnz, win_lo, wbase, true), "scatter_add")))
+          return rc;
+      } else {
+        // lower-rank contribution first (the bracket); the adds commute
+        const bool in_first = A.idx >= c->bl_ai.as<uint32_t>() && A.idx < c->bl_ai.as<uint32_t>() + n;
+        SpRef dst{in_first ? c->bl_ci.as<uint32_t>() : c->bl_ai.as<uint32_t>(),
+                  in_first ? c->bl_cv.as<double>() : c->bl_av.as<double>(), 0};
+        if ((rc = rank < partner ? bl_merge(c, A, B, dst, s) : bl_merge(c, B, A, dst, s))) return rc;
+        A = dst;
+      }
+    }
+    // storage crossover: COO costs two words per entry, the window one per coordinate
+    if (!dense && 2 * A.nnz >= k1 - k0 && (rc = densify(k0, k1))) return rc;
+    lo = keep_lo;
+    hi = keep_hi;
+  }
+  // the owned segment
+  SpRef seg = A;
+  if (dense) {
+    const uint64_t W = win_hi - win_lo, chunks = bl_chunks(W);
+    if ((rc = c->ensure(c->tk_aux, 24 * std::max<uint64_t>(chunks, 1)))) return rc;
+    uint32_t* cnt = c->tk_aux.as<uint32_t>();
+    uint64_t* off = reinterpret_cast<uint64_t*>(c->tk_aux.as<char>() + 8 * chunks);
+    seg = SpRef{c->bl_bi.as<uint32_t>(), c->bl_bv.as<double>(), 0};
+    rc = c->ck(okt::launch_dense_nonzero(c->L, wbase, W, win_lo, cnt, nullptr, nullptr, nullptr), "nz_count");
+    uint64_t total = 0;
+    if (rc || (rc = bl_prefix(c, cnt, chunks, off, total, s))) return rc;
+    if ((rc = c->ck(okt::launch_dense_nonzero(c->L, wbase, W, win_lo, nullptr, off, seg.idx, seg.val), "nz_write")))
+      return rc;
+    seg.nnz = total;
+  }
+  // sparse_allgatherv of the segments, concatenated in rank order
+  std::vector<uint64_t> segn;
+  if ((rc = bl_agree(c, "topkdsa_allreduce", seg.nnz, false, segn, s))) return rc;
+  std::vector<uint64_t> off(P + 1, 0);
+  for (int q = 0; q < P; ++q) off[q + 1] = off[q] + segn[q];
+  const uint64_t U = off[P];
+  if ((rc = c->ensure(c->sel_idx, 4 * std::max<uint64_t>(U, 1))) ||
+      (rc = c->ensure(c->sel_val, 8 * std::max<uint64_t>(U, 1))))
+    return rc;
+  uint32_t* ui = c->sel_idx.as<uint32_t>();
+  double* uv = c->sel_val.as<double>();
+  rc = c->ck(cudaMemcpyAsync(ui + off[rank], seg.idx, 4 * seg.nnz, cudaMemcpyDeviceToDevice, s), "copy");
+  if (!rc) rc = c->ck(cudaMemcpyAsync(uv + off[rank], seg.val, 8 * seg.nnz, cudaMemcpyDeviceToDevice, s), "copy");
+  if (rc) return rc;
+  std::vector<Xfer> sends, recvs;
+  for (int q = 0; q < P; ++q) {
+    if (q == rank) continue;
+    sends.push_back({q, seg.idx, 4 * seg.nnz});
+    sends.push_back({q, seg.val, 8 * seg.nnz});
+    recvs.push_back({q, ui + off[q], 4 * segn[q]});
+    recvs.push_back({q, uv + off[q], 8 * segn[q]});
+  }
+  std::string err;
+  rc = c->tr->exchange(sends, recvs, s, err);
+  if (rc) return c->comm_err(rc, err);
+  c->credit_allgatherv(OKT_PHASE_ALLGATHERV, segn, 12);
+  if ((rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  *out = okt_sparse{ui, uv, U, n};
+  return OKT_OK;
+}
+
+// gaussian_threshold (sparse.cpp:167-188; scale_to_floor = 0, the raw value)
+// or gaussiank_scaled_threshold (collectives.cpp:327-340; 1: clamped at 0 and
+// scaled by 0.9 until more than 3k/4 coordinates pass).  Mean and unbiased
+// variance in fp64 by a fixed-shape tree (the reference sums sequentially: the
+// two agree to a few ulp), the normal quantile at 1 - k/(2n) on the host.
+int okt_gaussiank_threshold(okt_comm* c, const float* d_g, size_t n, size_t k, int scale_to_floor, double* th,
+                            void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!th || (!d_g && n)) return set_err(OKT_ERR_INVALID_ARGUMENT, "gaussian_threshold: null argument");
+  if (n < 2) return set_err(OKT_ERR_INVALID_ARGUMENT, "gaussian_threshold: need n >= 2");
+  if (k < 1 || k > n) return set_err(OKT_ERR_INVALID_ARGUMENT, "gaussian_threshold: k must be in [1, n]");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  int rc;
+  if ((rc = c->ensure(c->bl_small, 8 * 1024 + 64))) return rc;
+  double* partial = c->bl_small.as<double>() + 8;
+  double* dm = c->bl_small.as<double>();
+  rc = c->ck(okt::launch_moments(c->L, d_g, n, partial, dm, dm + 1), "moments");
+  double* hm = reinterpret_cast<double*>(&c->hup->prop[0]);
+  if (!rc) rc = c->ck(cudaMemcpyAsync(hm, dm, 16, cudaMemcpyDeviceToHost, s), "d2h");
+  if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  const double mean = hm[0], var = hm[1];
+  if (!std::isfinite(mean) || !std::isfinite(var))
+    return set_err(OKT_ERR_NUMERIC, "gaussian_threshold: non-finite input");
+  if (var == 0.0) return set_err(OKT_ERR_NUMERIC, "DegenerateDistributionError: gaussian_threshold: zero variance input");
+  const double p = 1.0 - double(k) / (2.0 * double(n));
+  double t = mean + std::sqrt(var) * inverse_normal_cdf(p);
+  if (scale_to_floor) {
+    t = std::max(t, 0.0);
+    auto* hc = reinterpret_cast<unsigned long long*>(&c->hup->prop[2]);
+    auto* dc = reinterpret_cast<unsigned long long*>(dm + 2);
+    for (;;) {
+      rc = c->ck(okt::launch_count_ge(c->L, d_g, n, t, dc), "count_ge");
+      if (!rc) rc = c->ck(cudaMemcpyAsync(hc, dc, 8, cudaMemcpyDeviceToHost, s), "d2h");
+      if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+      if (4 * uint64_t(*hc) > 3 * uint64_t(k)) break;
+      t *= 0.9;
+    }
+  }
+  *th = t;
+  return OKT_OK;
+}
+
+// gaussiank_allreduce (collectives.cpp:342-352): Gaussian-fit threshold,
+// select_by_threshold, sparse_allgatherv, sparse_sum.
+int okt_gaussiank_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, int scale_to_floor, okt_sparse* out,
+                            void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!out) return set_err(OKT_ERR_INVALID_ARGUMENT, "gaussiank_allreduce: null output");
+  if (n > 0xffffffffull) return set_err(OKT_ERR_INVALID_ARGUMENT, "gaussiank_allreduce: n exceeds 32-bit indices");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  const int P = c->P;
+  double th = 0.0;
+  int rc = okt_gaussiank_threshold(c, d_g, n, k, scale_to_floor, &th, stream);
+  // a numeric failure (non-finite or zero-variance input) still joins the
+  // agreement below, so the other ranks fail instead of waiting
+  const bool bad = rc == OKT_ERR_NUMERIC;
+  const std::string why = bad ? std::string(okt_last_error()) : std::string();
+  if (rc && !bad) return rc;
+  th = std::max(th, 0.0);
+  uint64_t m = 0;
+  if (!bad) {
+    if ((rc = c->reserve(n))) return rc;
+    if ((rc = c->upload_f64(&c->d()->th_arg, th, &c->hup->th_arg, s))) return rc;
+    rc = c->ck(okt::launch_k1(c->L, c->S, okt::K1Mode::kSelect, d_g, nullptr, nullptr, 0.f, n, &c->d()->th_arg,
+                              nullptr, okt::OutCoo{c->coo.as<uint64_t>(), nullptr, nullptr}, &c->d()->m, nullptr,
+                              &c->d()->flags, nullptr), "k1");
+    if (rc || (rc = c->sync(s))) return rc;
+    m = c->h->m;
+  }
+  std::vector<uint64_t> counts;
+  if ((rc = bl_agree(c, "gaussiank_allreduce", m, bad, counts, s))) {
+    if (bad && rc == OKT_ERR_NUMERIC) set_err(OKT_ERR_NUMERIC, why);
+    return rc;
+  }
+  uint64_t total = 0;
+  for (int q = 0; q < P; ++q) total += counts[q];
+  if (P == 1) {
+    if ((rc = c->ensure(c->sel_idx, 4 * std::max<uint64_t>(m, 1))) ||
+        (rc = c->ensure(c->sel_val, 8 * std::max<uint64_t>(m, 1))))
+      return rc;
+    const uint64_t chunks = bl_chunks(m);
+    if ((rc = c->ensure(c->tk_aux, 24 * std::max<uint64_t>(chunks, 1)))) return rc;
+    std::vector<uint64_t> ho(chunks);
+    for (uint64_t i = 0; i < chunks; ++i) ho[i] = i * okt::kTopkTrimChunk;
+    uint64_t* off = c->tk_aux.as<uint64_t>();
+    if (chunks && (rc = c->ck(cudaMemcpyAsync(off, ho.data(), 8 * chunks, cudaMemcpyHostToDevice, s), "h2d")))
+      return rc;
+    rc = c->ck(okt::launch_aos_to_soa(c->L, c->coo.as<uint64_t>(), m, off, c->sel_idx.as<uint32_t>(),
+                                      c->sel_val.as<double>()), "aos_to_soa");
+    if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+    *out = okt_sparse{c->sel_idx.as<uint32_t>(), c->sel_val.as<double>(), m, n};
+    return OKT_OK;
+  }
+  // parts back to back by rank
+  if ((rc = c->ensure(c->tk_parts, 8 * std::max<uint64_t>(total, 1)))) return rc;
+  uint64_t my_off = 0;
+  for (int q = 0; q < c->rank; ++q) my_off += counts[q];
+  rc = c->ck(cudaMemcpyAsync(c->tk_parts.as<uint64_t>() + my_off, c->coo.p, 8 * m, cudaMemcpyDeviceToDevice, s),
+             "copy");
+  if (rc) return rc;
+  return bl_allgather_sum_aos(c, n, counts, out, s);
 }
 
 // ---- host planning (no GPU) ------------------------------------------------------------

@@ -184,12 +184,32 @@ cudaError_t launch_wire_encode(Launch& L, const uint32_t* idx, const double* val
 cudaError_t launch_wire_decode(Launch& L, const uint32_t* in, uint64_t nnz, uint64_t n, uint32_t* idx, double* val,
                                uint32_t* err);
 
-// Exact top-k trim of a threshold selection (okt_topk.cu): chunks of 1024 entries.
+// ---- Table-1 baselines (okt_baselines.cu) ----------------------------------------------
+// Order-preserving compactions run in chunks of kTopkTrimChunk entries: a
+// count pass (per-chunk counts), the host's exclusive prefix, a write pass.
 constexpr int kTopkTrimChunk = 1024;
-cudaError_t launch_topk_count(Launch& L, const uint64_t* coo, uint64_t m, float th, uint32_t* gt_cnt,
-                              uint32_t* eq_cnt);
-cudaError_t launch_topk_write(Launch& L, const uint64_t* coo, uint64_t m, float th, const uint64_t* off,
-                              const uint64_t* eq_before, uint64_t need, uint64_t* aos, uint32_t* out_idx,
-                              double* out_val);
+// Exact top-k trim over an AoS f32 (aos != null) or SoA f64 (idx, val) list.
+cudaError_t launch_topk_count(Launch& L, const uint64_t* aos, const uint32_t* idx, const double* val, uint64_t m,
+                              double th, uint32_t* gt_cnt, uint32_t* eq_cnt);
+cudaError_t launch_topk_write(Launch& L, const uint64_t* aos_in, const uint32_t* idx, const double* val, uint64_t m,
+                              double th, const uint64_t* off, const uint64_t* eq_before, uint64_t need,
+                              uint64_t* aos, uint32_t* out_idx, double* out_val);
+// merge_two: positions (tmp of na + nb entries), then heads (off == null: counts).
+cudaError_t launch_merge_rank(Launch& L, const uint32_t* ai, const double* av, uint64_t na, const uint32_t* bi,
+                              const double* bv, uint64_t nb, uint32_t* ti, double* tv);
+cudaError_t launch_merge_heads(Launch& L, const uint32_t* ti, const double* tv, uint64_t N, uint32_t* cnt,
+                               const uint64_t* off, uint32_t* oi, double* ov);
+cudaError_t launch_dense_nonzero(Launch& L, const double* w, uint64_t W, uint64_t lo, uint32_t* cnt,
+                                 const uint64_t* off, uint32_t* oi, double* ov);
+cudaError_t launch_aos_to_soa(Launch& L, const uint64_t* aos, uint64_t m, const uint64_t* off, uint32_t* oi,
+                              double* ov);
+cudaError_t launch_slice_bounds(Launch& L, const uint32_t* idx, uint64_t n, uint64_t lo, uint64_t hi,
+                                uint64_t* out);
+cudaError_t launch_window_scatter(Launch& L, const uint32_t* idx, const double* val, uint64_t nnz, uint64_t lo,
+                                  double* win, bool add);
+cudaError_t launch_window_add(Launch& L, double* win, const double* in, uint64_t W);
+// Gaussiank: mean and unbiased variance (fp64, fixed reduction shape); partial holds 1024 doubles.
+cudaError_t launch_moments(Launch& L, const float* g, uint64_t n, double* partial, double* d_mean, double* d_var);
+cudaError_t launch_count_ge(Launch& L, const float* g, uint64_t n, double th, unsigned long long* cnt);
 
 }  // namespace okt

@@ -410,6 +410,54 @@ def topka_allreduce(ctx: WorkerCtx, g, k: int) -> SparseGrad:
     return _sparse_from(s, d.numel())
 
 
+def gtopk_allreduce(ctx: WorkerCtx, g, k: int) -> SparseGrad:
+    """Table-1 baseline gTopk (collectives.cpp:300-325)."""
+    d = _device_f32(g, ctx.device)
+    s = OktSparse()
+    _check(_lib.lib().okt_gtopk_allreduce(ctx.comm, ctypes.c_void_p(d.data_ptr()), d.numel(), max(int(k), 0),
+                                          ctypes.byref(s), None))
+    return _sparse_from(s, d.numel())
+
+
+def topkdsa_allreduce(ctx: WorkerCtx, g, k: int) -> SparseGrad:
+    """Table-1 baseline TopkDSA (collectives.cpp:184-297): reduce-scatter with the
+    COO -> dense-window switch, then allgatherv of the owned segments."""
+    d = _device_f32(g, ctx.device)
+    s = OktSparse()
+    _check(_lib.lib().okt_topkdsa_allreduce(ctx.comm, ctypes.c_void_p(d.data_ptr()), d.numel(), max(int(k), 0),
+                                            ctypes.byref(s), None))
+    return _sparse_from(s, d.numel())
+
+
+def gaussiank_allreduce(ctx: WorkerCtx, g, k: int, scale_to_floor: bool = True) -> SparseGrad:
+    """Table-1 baseline Gaussiank (collectives.cpp:342-352; GaussiankOptions)."""
+    d = _device_f32(g, ctx.device)
+    s = OktSparse()
+    _check(_lib.lib().okt_gaussiank_allreduce(ctx.comm, ctypes.c_void_p(d.data_ptr()), d.numel(), max(int(k), 0),
+                                              int(bool(scale_to_floor)), ctypes.byref(s), None))
+    return _sparse_from(s, d.numel())
+
+
+def gaussian_threshold(g, k: int, ctx: Optional[WorkerCtx] = None) -> float:
+    """sparse.cpp:167-188 (fp64 moments by a tree reduction: within a few ulp)."""
+    ctx = ctx or _scratch_ctx()
+    d = _device_f32(g, ctx.device)
+    th = ctypes.c_double()
+    _check(_lib.lib().okt_gaussiank_threshold(ctx.comm, ctypes.c_void_p(d.data_ptr()), d.numel(), max(int(k), 0), 0,
+                                              ctypes.byref(th), None))
+    return th.value
+
+
+def gaussiank_scaled_threshold(g, k: int, ctx: Optional[WorkerCtx] = None) -> float:
+    """collectives.cpp:327-340."""
+    ctx = ctx or _scratch_ctx()
+    d = _device_f32(g, ctx.device)
+    th = ctypes.c_double()
+    _check(_lib.lib().okt_gaussiank_threshold(ctx.comm, ctypes.c_void_p(d.data_ptr()), d.numel(), max(int(k), 0), 1,
+                                              ctypes.byref(th), None))
+    return th.value
+
+
 def wire_encode(s: SparseGrad, device: int = 0) -> bytes:
     """oklab::wire_encode (sparse.hpp:126, sparse.cpp:275-285) on the device:
     [nnz u32][indices u32 x nnz][values f32 x nnz], little endian."""

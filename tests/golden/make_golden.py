@@ -76,6 +76,29 @@ def main():
         ui, uv = ref.topka_allreduce(ins, k)
         np.savez_compressed(os.path.join(HERE, "topka", name + ".npz"), P=P, n=n, k=k, inputs=np.stack(ins),
                             u_idx=ui, u_val=uv)
+    # gtopk / topkdsa / gaussiank (collectives.cpp:184-352; test_collectives.cpp:192-350)
+    os.makedirs(os.path.join(HERE, "baselines"), exist_ok=True)
+    rng = np.random.default_rng(78)
+    base = {
+        "gtopk_P2": ("gtopk", 2, 150, 8, True, [f32(orc.random_dense(4400 + 13 * r, 150)) for r in range(2)]),
+        "gtopk_P8": ("gtopk", 8, 150, 8, True, [f32(orc.random_dense(4400 + 13 * r, 150)) for r in range(8)]),
+        "gtopk_ties_P4": ("gtopk", 4, 400, 30, True, [rng.choice([-1.0, 1.0, 0.5, -0.5, 0.0], 400) for _ in range(4)]),
+        "topkdsa_int_P4": ("topkdsa", 4, 120, 10, True, [orc.random_int_dense(7100 + r, 120, 50) for r in range(4)]),
+        "topkdsa_cross_P4": ("topkdsa", 4, 64, 24, True,
+                             [np.abs(orc.random_int_dense(8200 + 3 * r, 64, 9)) + 1.0 for r in range(4)]),
+        "topkdsa_f32_P8": ("topkdsa", 8, 2000, 300, True, [f32(orc.random_dense(9100 + r, 2000)) for r in range(8)]),
+        "topkdsa_cancel_P2": ("topkdsa", 2, 64, 40, True,
+                              [np.where(np.arange(64) % 3 == 0, 1.0, 0.5) * s for s in (1.0, -1.0)]),
+        "gaussiank_int_P4": ("gaussiank", 4, 300, 20, True, [orc.random_int_dense(6600 + r, 300, 500) for r in range(4)]),
+        "gaussiank_f32_P2": ("gaussiank", 2, 4000, 40, True, [f32(orc.random_dense(6700 + r, 4000)) for r in range(2)]),
+        "gaussiank_raw_P2": ("gaussiank", 2, 4000, 40, False, [f32(orc.random_dense(6800 + r, 4000)) for r in range(2)]),
+    }
+    for name, (which, P, n, k, sc, ins) in base.items():
+        led = np.zeros((P, 6, 4), np.uint64)
+        ui, uv = ref.baseline(which, ins, k, sc, led)
+        th = np.array([ref.gaussian_threshold(x, k, sc) for x in ins]) if which == "gaussiank" else np.zeros(0)
+        np.savez_compressed(os.path.join(HERE, "baselines", name + ".npz"), which=which, P=P, n=n, k=k,
+                            scale=sc, inputs=np.stack(ins), u_idx=ui, u_val=uv, ledger=led, th=th)
     print("golden fixtures written to", HERE)
 
 
