@@ -8,6 +8,8 @@
 //
 //   oklab::ok_sparse_allreduce(ctx, state, g, t, k)      (oktopk.hpp:118-120)
 //   oklab::oktopk_sgd_step(ctx, model, res, problem, k, ok) (trainer.hpp:149-152)
+//   oklab::topka_allreduce / topkdsa_allreduce / gtopk_allreduce /
+//   gaussiank_allreduce (collectives.hpp:33-71, the Table-1 baselines)
 //
 // Ranks stay threads of one process over one oklab::Transport (the reference's
 // run_ranks model): the first call of each rank binds it to an okt_comm of a
@@ -26,6 +28,7 @@
 #include <string>
 #include <vector>
 
+#include "oklab/collectives.hpp"
 #include "oklab/errors.hpp"
 #include "oklab/oktopk.hpp"
 #include "oklab/sparse.hpp"
@@ -152,6 +155,41 @@ inline oklab::OkAllreduceResult to_result(const okt_result& r, std::size_t n) {
   return out;
 }
 
+inline oklab::SparseGrad to_sparse(const okt_sparse& u, std::size_t n) {
+  oklab::SparseGrad out(n);
+  out.indices.resize(u.nnz);
+  out.values.resize(u.nnz);
+  if (u.nnz) {
+    check(okt_memcpy_d2h(out.indices.data(), u.d_idx, 4 * u.nnz, nullptr));
+    check(okt_memcpy_d2h(out.values.data(), u.d_val, 8 * u.nnz, nullptr));
+  }
+  return out;
+}
+
+// One baseline call: the fp32 gradient staged on the rank's device, the
+// collective, the ledger credit, the result back as fp64.
+template <class F>
+oklab::SparseGrad run_baseline(const oklab::WorkerCtx& ctx, const oklab::DenseGrad& g, F&& fn) {
+  Binding* b = nullptr;
+  okt_comm* c = comm_for(ctx, &b);
+  int dev = 0;
+  check(okt_comm_info(c, nullptr, nullptr, &dev));
+  cudaSetDevice(dev);
+  std::vector<float> gf(g.values.begin(), g.values.end());
+  float* d_g = nullptr;
+  if (!gf.empty() && cudaMalloc(&d_g, 4 * gf.size()) != cudaSuccess) raise(OKT_ERR_CUDA);
+  struct Free {
+    float* p;
+    ~Free() { if (p) cudaFree(p); }
+  } guard{d_g};
+  if (!gf.empty()) check(okt_memcpy_h2d(d_g, gf.data(), 4 * gf.size(), nullptr));
+  okt_sparse u{};
+  const int rc = fn(c, d_g, gf.size(), &u);
+  credit(ctx, b, c);
+  if (rc != OKT_OK) raise(rc);
+  return to_sparse(u, g.size());
+}
+
 }  // namespace detail
 
 // Releases the device comms bound to `transport` (call before destroying it;
@@ -237,6 +275,29 @@ inline oklab::StepOutcome oktopk_sgd_step(const oklab::WorkerCtx& ctx, oklab::Mo
   out.selected_local = r.local_selected;
   out.selected_global = r.u.nnz;
   return out;
+}
+
+// Drop-ins for the Table-1 baselines (collectives.hpp:33-71).
+inline oklab::SparseGrad topka_allreduce(const oklab::WorkerCtx& ctx, const oklab::DenseGrad& g, std::size_t k) {
+  return detail::run_baseline(ctx, g, [&](okt_comm* c, const float* d, std::size_t n, okt_sparse* u) {
+    return okt_topka_allreduce(c, d, n, k, u, nullptr);
+  });
+}
+inline oklab::SparseGrad gtopk_allreduce(const oklab::WorkerCtx& ctx, const oklab::DenseGrad& g, std::size_t k) {
+  return detail::run_baseline(ctx, g, [&](okt_comm* c, const float* d, std::size_t n, okt_sparse* u) {
+    return okt_gtopk_allreduce(c, d, n, k, u, nullptr);
+  });
+}
+inline oklab::SparseGrad topkdsa_allreduce(const oklab::WorkerCtx& ctx, const oklab::DenseGrad& g, std::size_t k) {
+  return detail::run_baseline(ctx, g, [&](okt_comm* c, const float* d, std::size_t n, okt_sparse* u) {
+    return okt_topkdsa_allreduce(c, d, n, k, u, nullptr);
+  });
+}
+inline oklab::SparseGrad gaussiank_allreduce(const oklab::WorkerCtx& ctx, const oklab::DenseGrad& g, std::size_t k,
+                                             oklab::GaussiankOptions opts = {}) {
+  return detail::run_baseline(ctx, g, [&](okt_comm* c, const float* d, std::size_t n, okt_sparse* u) {
+    return okt_gaussiank_allreduce(c, d, n, k, opts.scale_to_floor ? 1 : 0, u, nullptr);
+  });
 }
 
 }  // namespace okt_oklab

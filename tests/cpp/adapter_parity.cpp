@@ -4,7 +4,9 @@
 // OkAllreduceResult, OkState and ledger row must be identical.
 // Built by oracle/Makefile into oracle/_ref/adapter_parity; run by
 // tests/test_gpu_adapter.py.  Exit code = number of mismatching scenarios.
+#include <cmath>
 #include <cstdio>
+#include <functional>
 #include <vector>
 
 #include "okt_oklab.hpp"
@@ -78,6 +80,26 @@ int scenario(const char* name, int P, std::size_t n, std::size_t k, int iters, s
   return 0;
 }
 
+// One Table-1 baseline on both implementations (same inputs, same ledger).
+int baseline(const char* name, int P, const std::vector<DenseGrad>& in,
+             const std::function<SparseGrad(const WorkerCtx&, const DenseGrad&, bool)>& fn) {
+  World wr(P), wg(P);
+  auto ref = run_ranks(wr, [&](const WorkerCtx& ctx) { return fn(ctx, in[ctx.rank], false); });
+  auto gpu = run_ranks(wg, [&](const WorkerCtx& ctx) { return fn(ctx, in[ctx.rank], true); });
+  okt_oklab::release(&wg.transport);
+  for (int r = 0; r < P; ++r)
+    if (!(ref[r] == gpu[r])) {
+      std::printf("FAIL %s: rank %d result differs\n", name, r);
+      return 1;
+    }
+  if (!same_ledger(wr.ledger, wg.ledger, P)) {
+    std::printf("FAIL %s: ledger differs\n", name);
+    return 1;
+  }
+  std::printf("PASS %s\n", name);
+  return 0;
+}
+
 }  // namespace
 
 int main() {
@@ -133,6 +155,42 @@ int main() {
     okt_oklab::release(&w.transport);
     std::printf("%s exception mapping\n", ok == 3 ? "PASS" : "FAIL");
     fails += ok == 3 ? 0 : 1;
+  }
+  // Table-1 baselines (test_collectives.cpp:167-350 inputs)
+  {
+    auto ins = [](int P, std::size_t n, std::uint64_t seed, int kind) {
+      std::vector<DenseGrad> v;
+      for (int r = 0; r < P; ++r) {
+        DenseGrad g = kind == 0   ? test::random_int_dense(seed + r, n, 1000)
+                      : kind == 2 ? test::random_int_dense(seed + 3 * r, n, 9)
+                                  : f32(test::random_dense(seed + r, n));
+        if (kind == 2)  // test_collectives.cpp:227-231: strictly positive integers
+          for (double& x : g.values) x = std::fabs(x) + 1.0;
+        v.push_back(std::move(g));
+      }
+      return v;
+    };
+    fails += baseline("topka_allreduce", 4, ins(4, 200, 900, 0), [](const WorkerCtx& c, const DenseGrad& g, bool b) {
+      return b ? okt_oklab::topka_allreduce(c, g, 12) : oklab::topka_allreduce(c, g, 12);
+    });
+    fails += baseline("topkdsa_allreduce", 4, ins(4, 120, 7100, 0), [](const WorkerCtx& c, const DenseGrad& g, bool b) {
+      return b ? okt_oklab::topkdsa_allreduce(c, g, 10) : oklab::topkdsa_allreduce(c, g, 10);
+    });
+    fails += baseline("topkdsa crossover", 4, ins(4, 64, 8200, 2), [](const WorkerCtx& c, const DenseGrad& g, bool b) {
+      return b ? okt_oklab::topkdsa_allreduce(c, g, 24) : oklab::topkdsa_allreduce(c, g, 24);
+    });
+    for (int P : {2, 4, 8})
+      fails += baseline("gtopk_allreduce", P, ins(P, 150, 4400, 1), [](const WorkerCtx& c, const DenseGrad& g, bool b) {
+        return b ? okt_oklab::gtopk_allreduce(c, g, 8) : oklab::gtopk_allreduce(c, g, 8);
+      });
+    fails += baseline("gaussiank_allreduce", 4, ins(4, 300, 6600, 0), [](const WorkerCtx& c, const DenseGrad& g, bool b) {
+      return b ? okt_oklab::gaussiank_allreduce(c, g, 20) : oklab::gaussiank_allreduce(c, g, 20);
+    });
+    fails += baseline("gaussiank raw", 2, ins(2, 5000, 6800, 1), [](const WorkerCtx& c, const DenseGrad& g, bool b) {
+      GaussiankOptions o;
+      o.scale_to_floor = false;
+      return b ? okt_oklab::gaussiank_allreduce(c, g, 400, o) : oklab::gaussiank_allreduce(c, g, 400, o);
+    });
   }
   std::printf("%d failing scenarios\n", fails);
   return fails;
