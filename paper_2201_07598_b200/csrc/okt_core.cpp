@@ -1184,9 +1184,20 @@ struct okt_comm {
                                          &d()->local_th, false), "radix");
       }
       tmark(OKT_T_SELECT, s);
-      if (!rc) rc = ck(okt::launch_k1(L, S, okt::K1Mode::kSelect, acc, nullptr, nullptr, 0.f, n, &d()->local_th,
-                                      nullptr, okt::OutCoo{coo.as<uint64_t>()}, &d()->m, nullptr, &d()->flags,
-                                      nullptr), "k1");
+      if (P == 1) {
+        // One rank: the region is the local selection {|acc| >= local_th}, so
+        // its k-th largest magnitude (the global refresh, oktopk.cpp:277-293)
+        // is local_th itself, and u = the local selection comes straight out
+        // of a dual-threshold select over acc, K7 fused as in the steady step.
+        if (!rc) rc = ck(cudaMemcpyAsync(&d()->global_th, &d()->local_th, 8, cudaMemcpyDeviceToDevice, s), "copy");
+        if (!rc) rc = ck(okt::launch_k1(L, S, okt::K1Mode::kSelect, acc, nullptr, nullptr, 0.f, n, &d()->local_th,
+                                        &d()->global_th,
+                                        okt::OutCoo{nullptr, sur_idx.as<uint32_t>(), sur_val.as<double>()},
+                                        &d()->S, &d()->m, &d()->flags, nullptr, &ap1), "k1");
+      } else if (!rc) {
+        rc = ck(okt::launch_k1(L, S, okt::K1Mode::kSelect, acc, nullptr, nullptr, 0.f, n, &d()->local_th, nullptr,
+                               okt::OutCoo{coo.as<uint64_t>()}, &d()->m, nullptr, &d()->flags, nullptr), "k1");
+      }
     } else if (P == 1) {
       // Steady state, one rank: the region is the local selection itself, so
       // u = {|acc| >= max(local_th, global_th)} comes straight out of K1 and
@@ -1211,16 +1222,6 @@ struct okt_comm {
     std::vector<uint64_t> new_cuts(P + 1, 0);
 
     if (P == 1) {
-      if (thr) {
-        // The region is the local selection itself (fp32 values, exact in fp64).
-        tmark(OKT_T_GLOBAL, s);
-        rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kAosF32, coo.p, 0, &d()->m, n, k, &d()->rs, hp,
-                                         &d()->global_th, false), "radix");
-        if (!rc)
-          rc = ck(okt::launch_filter(L, S, true, coo.as<uint64_t>(), nullptr, nullptr, &d()->m, n, &d()->global_th,
-                                     sur_idx.as<uint32_t>(), sur_val.as<double>(), &d()->S, &ap1), "filter");
-        if (rc) return abort_step(rc);
-      }
       ui = sur_idx.as<uint32_t>();
       uv = sur_val.as<double>();
       d_U = &d()->S;
