@@ -1020,6 +1020,28 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t want = prefix >> hi;
   const uint64_t stride = uint64_t(gridDim.x) * kThreads;
   uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
+  if (SRC == 0 && (reinterpret_cast<uintptr_t>(data) & 15u) == 0) {
+    // dense f32: 16-byte loads, two in flight per thread, then the < 4 tail keys
+    const float4* d4 = static_cast<const float4*>(data);
+    const uint64_t n4 = n >> 2;
+    auto one = [&](float v) {
+      const uint64_t key = uint64_t(__float_as_uint(v) & 0x7fffffffu);
+      if ((key >> hi) == want) atomicAdd(&sh[(key >> shift) & (nb - 1)], 1u);
+    };
+    uint64_t j = i;
+    for (; j + stride < n4; j += 2 * stride) {
+      const float4 a = __ldg(d4 + j), b = __ldg(d4 + j + stride);
+      one(a.x); one(a.y); one(a.z); one(a.w);
+      one(b.x); one(b.y); one(b.z); one(b.w);
+    }
+    for (; j < n4; j += stride) {
+      const float4 a = __ldg(d4 + j);
+      one(a.x); one(a.y); one(a.z); one(a.w);
+    }
+    i = 4 * n4 + i;  // tail: keys [4*n4, n)
+    if (i < n) one(static_cast<const float*>(data)[i]);
+    i = n;
+  }
   for (; i + 3 * stride < n; i += 4 * stride) {
     uint64_t k0 = mag_key<SRC>(data, i), k1 = mag_key<SRC>(data, i + stride);
     uint64_t k2 = mag_key<SRC>(data, i + 2 * stride), k3 = mag_key<SRC>(data, i + 3 * stride);
