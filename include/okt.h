@@ -17,7 +17,8 @@
  *   space_repartition     include/oklab/oktopk.hpp:58     okt_space_repartition
  *   split_and_reduce      include/oklab/oktopk.hpp:77     okt_split_and_reduce
  *   balance_and_allgatherv include/oklab/oktopk.hpp:92    okt_balance_and_allgatherv
- *   topka_allreduce       include/oklab/collectives.hpp:33  okt_topka_allreduce (Table-1 baselines)
+ *   dense_allreduce       include/oklab/collectives.hpp:28  okt_dense_allreduce (Table-1 baselines)
+ *   topka_allreduce       include/oklab/collectives.hpp:33  okt_topka_allreduce
  *   gtopk_allreduce       include/oklab/collectives.hpp:53  okt_gtopk_allreduce
  *   topkdsa_allreduce     include/oklab/collectives.hpp:45  okt_topkdsa_allreduce
  *   gaussiank_allreduce   include/oklab/collectives.hpp:70  okt_gaussiank_allreduce
@@ -258,6 +259,12 @@ int okt_balance_and_allgatherv(okt_comm* comm, const uint32_t* d_idx,
  * input fails with OKT_ERR_NUMERIC ("DegenerateDistributionError"). */
 int okt_topka_allreduce(okt_comm* comm, const float* d_g, size_t n, size_t k,
                         okt_sparse* out, void* stream);
+/* dense_allreduce (collectives.cpp:89-150; collectives.hpp:28): the fp32
+ * gradient widened to fp64 and summed by recursive halving / doubling in the
+ * reference's order; *d_out = comm-owned fp64 vector of n, valid until the
+ * next call.  Ranks with different n fail with OKT_ERR_PROTOCOL. */
+int okt_dense_allreduce(okt_comm* comm, const float* d_g, size_t n, double** d_out,
+                        void* stream);
 int okt_gtopk_allreduce(okt_comm* comm, const float* d_g, size_t n, size_t k,
                         okt_sparse* out, void* stream);
 int okt_topkdsa_allreduce(okt_comm* comm, const float* d_g, size_t n, size_t k,

@@ -277,6 +277,30 @@ inline oklab::StepOutcome oktopk_sgd_step(const oklab::WorkerCtx& ctx, oklab::Mo
   return out;
 }
 
+// Drop-in for oklab::dense_allreduce (collectives.hpp:28).
+inline oklab::DenseGrad dense_allreduce(const oklab::WorkerCtx& ctx, const oklab::DenseGrad& g) {
+  detail::Binding* b = nullptr;
+  okt_comm* c = detail::comm_for(ctx, &b);
+  int dev = 0;
+  detail::check(okt_comm_info(c, nullptr, nullptr, &dev));
+  cudaSetDevice(dev);
+  std::vector<float> gf(g.values.begin(), g.values.end());
+  float* d_g = nullptr;
+  if (!gf.empty() && cudaMalloc(&d_g, 4 * gf.size()) != cudaSuccess) detail::raise(OKT_ERR_CUDA);
+  struct Free {
+    float* p;
+    ~Free() { if (p) cudaFree(p); }
+  } guard{d_g};
+  if (!gf.empty()) detail::check(okt_memcpy_h2d(d_g, gf.data(), 4 * gf.size(), nullptr));
+  double* d_out = nullptr;
+  const int rc = okt_dense_allreduce(c, d_g, gf.size(), &d_out, nullptr);
+  detail::credit(ctx, b, c);
+  if (rc != OKT_OK) detail::raise(rc);
+  oklab::DenseGrad out(g.size());
+  if (g.size()) detail::check(okt_memcpy_d2h(out.values.data(), d_out, 8 * g.size(), nullptr));
+  return out;
+}
+
 // Drop-ins for the Table-1 baselines (collectives.hpp:33-71).
 inline oklab::SparseGrad topka_allreduce(const oklab::WorkerCtx& ctx, const oklab::DenseGrad& g, std::size_t k) {
   return detail::run_baseline(ctx, g, [&](okt_comm* c, const float* d, std::size_t n, okt_sparse* u) {

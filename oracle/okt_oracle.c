@@ -389,6 +389,65 @@ size_t orc_gtopk_allreduce(int P, const double* const* g, size_t n, size_t k, ui
   return m;
 }
 
+/* dense_allreduce (collectives.cpp:89-150) replayed for all ranks in lockstep:
+ * recursive-halving reduce-scatter (own slice += partner's), recursive-doubling
+ * allgather; rank 0's result in out (n doubles); ledger phase 4 (dense). */
+void orc_dense_allreduce(int P, const double* const* g, size_t n, double* out, orc_counters* ledger) {
+  if (P <= 0 || P > ORC_MAX_P) return;
+  double* buf[ORC_MAX_P];
+  double* in[ORC_MAX_P];
+  for (int r = 0; r < P; ++r) {
+    buf[r] = (double*)malloc((n + 1) * sizeof(double));
+    in[r] = (double*)malloc((n + 1) * sizeof(double));
+    memcpy(buf[r], g[r], n * sizeof(double));
+  }
+  uint64_t ends[ORC_MAX_P + 1];
+  orc_equal_slice_ends(n, P, ends);
+  int lo[ORC_MAX_P], hi[ORC_MAX_P];
+  for (int r = 0; r < P; ++r) {
+    lo[r] = 0;
+    hi[r] = P;
+  }
+  for (int mask = P >> 1; mask > 0; mask >>= 1) {
+    int klo[ORC_MAX_P], khi[ORC_MAX_P];
+    for (int r = 0; r < P; ++r) { /* messages first: the half each rank gives up */
+      const int mid = lo[r] + mask, low = (r & mask) == 0;
+      const int send_lo = low ? mid : lo[r], send_hi = low ? hi[r] : mid;
+      klo[r] = low ? lo[r] : mid;
+      khi[r] = low ? mid : hi[r];
+      memcpy(in[r ^ mask], buf[r] + ends[send_lo], (ends[send_hi] - ends[send_lo]) * sizeof(double));
+      credit(ledger, P, r, 4, 1, ends[send_hi] - ends[send_lo]);
+    }
+    for (int r = 0; r < P; ++r) {
+      const uint64_t kc = ends[khi[r]] - ends[klo[r]];
+      credit(ledger, P, r, 4, 0, kc);
+      double* dst = buf[r] + ends[klo[r]];
+      for (uint64_t i = 0; i < kc; ++i) dst[i] += in[r][i];
+      lo[r] = klo[r];
+      hi[r] = khi[r];
+    }
+  }
+  for (int mask = 1; mask < P; mask <<= 1) {
+    for (int r = 0; r < P; ++r) { /* every rank's reduced block, then the copies */
+      const int base = r & ~(2 * mask - 1), my_lo = (r & mask) ? base + mask : base;
+      memcpy(in[r] + ends[my_lo], buf[r] + ends[my_lo], (ends[my_lo + mask] - ends[my_lo]) * sizeof(double));
+      credit(ledger, P, r, 4, 1, ends[my_lo + mask] - ends[my_lo]);
+    }
+    for (int r = 0; r < P; ++r) {
+      const int partner = r ^ mask, base = partner & ~(2 * mask - 1);
+      const int their_lo = (partner & mask) ? base + mask : base;
+      const uint64_t tc = ends[their_lo + mask] - ends[their_lo];
+      memcpy(buf[r] + ends[their_lo], in[partner] + ends[their_lo], tc * sizeof(double));
+      credit(ledger, P, r, 4, 0, tc);
+    }
+  }
+  memcpy(out, buf[0], n * sizeof(double));
+  for (int r = 0; r < P; ++r) {
+    free(buf[r]);
+    free(in[r]);
+  }
+}
+
 /* TopkDSA working set (collectives.cpp:162-182): COO or a dense window. */
 typedef struct {
   int dense;

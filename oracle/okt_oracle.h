@@ -71,6 +71,8 @@ size_t orc_topk_exact(const double* g, size_t n, size_t k, uint32_t* idx, double
  * the P exact top-k parts; out holds up to P*k entries. */
 size_t orc_topka_allreduce(int P, const double* const* g, size_t n, size_t k, uint32_t* out_idx,
                            double* out_val);
+/* dense_allreduce (collectives.cpp:89-150): rank 0's fp64 sum in out (n). */
+void orc_dense_allreduce(int P, const double* const* g, size_t n, double* out, orc_counters* ledger);
 /* gtopk_allreduce (collectives.cpp:300-325) / topkdsa_allreduce (:184-297):
  * rank 0's result (all ranks agree); ledger P*6 counters or NULL. */
 size_t orc_gtopk_allreduce(int P, const double* const* g, size_t n, size_t k, uint32_t* out_idx, double* out_val,

@@ -144,6 +144,7 @@ class Oracle(_Common):
         L.orc_gtopk_allreduce.restype = c_size_t
         L.orc_topkdsa_allreduce.restype = c_size_t
         L.orc_gaussiank_allreduce.restype = c_size_t
+        L.orc_dense_allreduce.restype = None
         L.orc_gaussian_threshold.restype = c_double
         L.orc_gaussian_threshold.argtypes = [POINTER(c_double), c_size_t, c_size_t, c_int]
         L.orc_space_repartition.restype = None
@@ -253,6 +254,15 @@ class Oracle(_Common):
             raise ValueError(which)
         return oi[:m].copy(), ov[:m].copy()
 
+    def dense_allreduce(self, inputs: Sequence[np.ndarray], ledger: np.ndarray = None) -> np.ndarray:
+        P = len(inputs)
+        g = [np.ascontiguousarray(x, dtype=np.float64) for x in inputs]
+        out = np.empty(max(g[0].size, 1), np.float64)
+        led = ledger if ledger is not None else np.zeros((P, 6, 4), np.uint64)
+        self.L.orc_dense_allreduce(c_int(P), _ptrs(g, c_double), c_size_t(g[0].size),
+                                   out.ctypes.data_as(POINTER(c_double)), led.ctypes.data_as(POINTER(Counters)))
+        return out[:g[0].size].copy()
+
     def gaussian_threshold(self, g: np.ndarray, k: int, scale_to_floor: bool = True) -> float:
         g = np.ascontiguousarray(g, dtype=np.float64)
         return self.L.orc_gaussian_threshold(g.ctypes.data_as(POINTER(c_double)), g.size, k, int(scale_to_floor))
@@ -317,6 +327,7 @@ class Reference(_Common):
         L.okref_allreduce.restype = c_int
         L.okref_topka.restype = c_int
         L.okref_baseline.restype = c_int
+        L.okref_dense.restype = c_int
         L.okref_gaussian_threshold.restype = c_double
         L.okref_gaussian_threshold.argtypes = [POINTER(c_double), c_size_t, c_size_t, c_int]
         L.okref_th_re_evaluate_dense.restype = c_double
@@ -370,6 +381,18 @@ class Reference(_Common):
         if rc:
             raise RuntimeError(f"okref_baseline rc={rc}: {self.err.value.decode(errors='replace')}")
         return oi[:U.value].copy(), ov[:U.value].copy()
+
+    def dense_allreduce(self, inputs: Sequence[np.ndarray], ledger: np.ndarray = None) -> np.ndarray:
+        P = len(inputs)
+        g = [np.ascontiguousarray(x, dtype=np.float64) for x in inputs]
+        out = np.empty(max(g[0].size, 1), np.float64)
+        led = ledger if ledger is not None else np.zeros((P, 6, 4), np.uint64)
+        rc = self.L.okref_dense(c_int(P), _ptrs(g, c_double), c_size_t(g[0].size),
+                                out.ctypes.data_as(POINTER(c_double)), led.ctypes.data_as(POINTER(Counters)),
+                                self.err, c_size_t(512))
+        if rc:
+            raise RuntimeError(f"okref_dense rc={rc}: {self.err.value.decode(errors='replace')}")
+        return out[:g[0].size].copy()
 
     def gaussian_threshold(self, g: np.ndarray, k: int, scale_to_floor: bool = True) -> float:
         g = np.ascontiguousarray(g, dtype=np.float64)

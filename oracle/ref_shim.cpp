@@ -348,4 +348,36 @@ double okref_gaussian_threshold(const double* g, size_t n, size_t k, int scale_t
   return scale_to_floor ? gaussiank_scaled_threshold(dg, k) : gaussian_threshold(dg, k);
 }
 
+// One oklab::dense_allreduce on P rank threads.
+int okref_dense(int P, const double* const* g, size_t n, double* out, okref_counters* ledger, char* err,
+                size_t errlen) {
+  InprocTransport tr(P, 64);
+  TrafficLedger led(P);
+  std::vector<DenseGrad> res(P);
+  const int rc = run_ranks(
+      tr, P,
+      [&](int r) {
+        WorkerCtx ctx{r, P, &tr, &led};
+        res[r] = dense_allreduce(ctx, DenseGrad(std::vector<double>(g[r], g[r] + n)));
+      },
+      err, errlen);
+  for (int r = 0; r < P && ledger; ++r)
+    for (int ph = 0; ph < kPhaseCount; ++ph) {
+      const auto& c = led.at(r, static_cast<Phase>(ph));
+      okref_counters& o = ledger[r * kPhaseCount + ph];
+      o.words_sent += c.words_sent;
+      o.words_recv += c.words_recv;
+      o.msgs_sent += c.msgs_sent;
+      o.msgs_recv += c.msgs_recv;
+    }
+  if (rc) return rc;
+  for (int r = 1; r < P; ++r)
+    if (res[r].values != res[0].values) {
+      std::snprintf(err, errlen, "ranks disagree");
+      return 8;
+    }
+  std::memcpy(out, res[0].values.data(), n * sizeof(double));
+  return 0;
+}
+
 }  // extern "C"

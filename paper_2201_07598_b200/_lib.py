@@ -32,7 +32,7 @@ EXPORTS = (
     "okt_sgd_step_host", "okt_memcpy_h2d", "okt_memcpy_d2h",
     "okt_th_re_evaluate_dense", "okt_th_re_evaluate_sparse",
     "okt_select_by_threshold", "okt_space_repartition",
-    "okt_split_and_reduce", "okt_balance_and_allgatherv", "okt_topka_allreduce", "okt_gtopk_allreduce",
+    "okt_split_and_reduce", "okt_balance_and_allgatherv", "okt_topka_allreduce", "okt_gtopk_allreduce", "okt_dense_allreduce",
     "okt_topkdsa_allreduce", "okt_gaussiank_threshold", "okt_gaussiank_allreduce",
     "okt_set_profiling", "okt_phase_times", "okt_phase_bytes", "okt_reset_phase_times",
     "okt_kernel_launches", "okt_debug_p2p_trace", "okt_wire_encode", "okt_wire_decode", "okt_gen_random_dense", "okt_gen_drift",
@@ -130,6 +130,7 @@ def lib() -> ctypes.CDLL:
         "okt_th_re_evaluate_sparse": (c_int, [c_void_p, c_void_p, c_size_t, c_size_t,
                                               P(c_double), c_void_p]),
         "okt_topka_allreduce": (c_int, [c_void_p, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p]),
+        "okt_dense_allreduce": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
         "okt_gtopk_allreduce": (c_int, [c_void_p, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p]),
         "okt_topkdsa_allreduce": (c_int, [c_void_p, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p]),
         "okt_gaussiank_threshold": (c_int, [c_void_p, c_void_p, c_size_t, c_size_t, c_int, c_void_p, c_void_p]),

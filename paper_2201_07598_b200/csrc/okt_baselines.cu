@@ -11,6 +11,8 @@
 //    heads of equal-index pairs emit the pair's sum;
 //  * dense fp64 windows of TopkDSA (densify, window += half, COO scatter-add,
 //    nonzero extraction — collectives.cpp:167-297);
+//  * the window adds of the dense fp64 recursive-halving allreduce
+//    (collectives.cpp:89-150);
 //  * Gaussiank moments (sparse.cpp:167-188) with a fixed-shape deterministic
 //    fp64 reduction, and the |v| >= th count of the 0.9 rescaling loop.
 //

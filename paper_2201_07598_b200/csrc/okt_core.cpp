@@ -2262,6 +2262,56 @@ double inverse_normal_cdf(double p) {
 
 }  // namespace
 
+// dense_allreduce (collectives.cpp:89-150): the fp32 gradient widened to fp64,
+// recursive-halving reduce-scatter over equal_slice_ends (own + partner's half,
+// the reference's adds), recursive-doubling allgather of the reduced slices.
+int okt_dense_allreduce(okt_comm* c, const float* d_g, size_t n, double** d_out, void* stream) {
+  OKT_COMM_CHECK(c);
+  if (!d_out || (!d_g && n)) return set_err(OKT_ERR_INVALID_ARGUMENT, "dense_allreduce: null argument");
+  if (n > 0xffffffffull) return set_err(OKT_ERR_INVALID_ARGUMENT, "dense_allreduce: n exceeds 32-bit sizes");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->pick(stream);
+  c->L.s = s;
+  const int P = c->P, rank = c->rank;
+  int rc;
+  if ((rc = c->ensure(c->bl_win, 8 * std::max<size_t>(n, 1))) || (rc = c->ensure(c->bl_win_in, 8 * std::max<size_t>(n, 1))))
+    return rc;
+  double* buf = c->bl_win.as<double>();
+  double* in = c->bl_win_in.as<double>();
+  if ((rc = c->ck(okt::launch_widen_f32(c->L, d_g, n, buf), "widen"))) return rc;
+  std::vector<uint64_t> sizes;
+  if ((rc = bl_agree(c, "dense_allreduce", n, false, sizes, s))) return rc;
+  for (int q = 0; q < P; ++q)
+    if (sizes[q] != n) return set_err(OKT_ERR_PROTOCOL, "ProtocolError: dense_allreduce: length mismatch");
+  if (P > 1) {
+    const std::vector<uint64_t> ends = equal_slice_ends(n, P);
+    int lo = 0, hi = P;
+    for (int mask = P >> 1; mask > 0; mask >>= 1) {
+      const int partner = rank ^ mask, mid = lo + mask;
+      const bool low = (rank & mask) == 0;
+      const int keep_lo = low ? lo : mid, keep_hi = low ? mid : hi, send_lo = low ? mid : lo, send_hi = low ? hi : mid;
+      const uint64_t sc = ends[send_hi] - ends[send_lo], kc = ends[keep_hi] - ends[keep_lo];
+      rc = bl_swap(c, partner, {{buf + ends[send_lo], 8 * sc}}, {{in, 8 * kc}}, s);
+      if (rc) return rc;
+      bl_credit_pair(c, OKT_PHASE_DENSE, sc, kc);
+      if ((rc = c->ck(okt::launch_window_add(c->L, buf + ends[keep_lo], in, kc), "window_add"))) return rc;
+      lo = keep_lo;
+      hi = keep_hi;
+    }
+    for (int mask = 1; mask < P; mask <<= 1) {
+      const int partner = rank ^ mask, base = rank & ~(2 * mask - 1);
+      const int my_lo = (rank & mask) ? base + mask : base, their_lo = (rank & mask) ? base : base + mask;
+      const uint64_t mc = ends[my_lo + mask] - ends[my_lo], tc = ends[their_lo + mask] - ends[their_lo];
+      rc = bl_swap(c, partner, {{buf + ends[my_lo], 8 * mc}}, {{buf + ends[their_lo], 8 * tc}}, s);
+      if (rc) return rc;
+      bl_credit_pair(c, OKT_PHASE_DENSE, mc, tc);
+    }
+  }
+  if ((rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  *d_out = buf;
+  return OKT_OK;
+}
+
 // topka_allreduce (collectives.cpp:152-159): exact local top-k, sparse_allgatherv,
 // sparse_sum.
 int okt_topka_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt_sparse* out, void* stream) {

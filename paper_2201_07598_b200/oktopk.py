@@ -410,6 +410,15 @@ def topka_allreduce(ctx: WorkerCtx, g, k: int) -> SparseGrad:
     return _sparse_from(s, d.numel())
 
 
+def dense_allreduce(ctx: WorkerCtx, g) -> np.ndarray:
+    """Dense fp64 recursive-halving allreduce (collectives.cpp:89-150) of the
+    fp32 gradient; returns the summed vector (float64, host)."""
+    d = _device_f32(g, ctx.device)
+    p = ctypes.c_void_p()
+    _check(_lib.lib().okt_dense_allreduce(ctx.comm, ctypes.c_void_p(d.data_ptr()), d.numel(), ctypes.byref(p), None))
+    return _d2h(p.value, d.numel(), np.float64)
+
+
 def gtopk_allreduce(ctx: WorkerCtx, g, k: int) -> SparseGrad:
     """Table-1 baseline gTopk (collectives.cpp:300-325)."""
     d = _device_f32(g, ctx.device)

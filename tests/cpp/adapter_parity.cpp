@@ -192,6 +192,19 @@ int main() {
       return b ? okt_oklab::gaussiank_allreduce(c, g, 400, o) : oklab::gaussiank_allreduce(c, g, 400, o);
     });
   }
+  // dense_allreduce (collectives.cpp:89-150) on fp32-representable inputs
+  for (int P : {2, 4, 8}) {
+    World wr(P), wg(P);
+    std::vector<DenseGrad> in;
+    for (int r = 0; r < P; ++r) in.push_back(f32(test::random_dense(5100 + r, 1001)));
+    auto ref = run_ranks(wr, [&](const WorkerCtx& c) { return oklab::dense_allreduce(c, in[c.rank]); });
+    auto gpu = run_ranks(wg, [&](const WorkerCtx& c) { return okt_oklab::dense_allreduce(c, in[c.rank]); });
+    okt_oklab::release(&wg.transport);
+    bool ok = same_ledger(wr.ledger, wg.ledger, P);
+    for (int r = 0; r < P; ++r) ok = ok && ref[r].values == gpu[r].values;
+    std::printf("%s dense_allreduce P=%d\n", ok ? "PASS" : "FAIL", P);
+    fails += ok ? 0 : 1;
+  }
   std::printf("%d failing scenarios\n", fails);
   return fails;
 }

@@ -99,6 +99,14 @@ def main():
         th = np.array([ref.gaussian_threshold(x, k, sc) for x in ins]) if which == "gaussiank" else np.zeros(0)
         np.savez_compressed(os.path.join(HERE, "baselines", name + ".npz"), which=which, P=P, n=n, k=k,
                             scale=sc, inputs=np.stack(ins), u_idx=ui, u_val=uv, ledger=led, th=th)
+    # dense_allreduce (collectives.cpp:89-150; test_collectives.cpp dense cases)
+    os.makedirs(os.path.join(HERE, "dense"), exist_ok=True)
+    for name, P, n in (("P2_n9", 2, 9), ("P4_n1001", 4, 1001), ("P8_n4096", 8, 4096), ("P8_n5", 8, 5)):
+        ins = [f32(orc.random_dense(3100 + 7 * r, n) * (1.0 + 1000.0 * (r % 3))) for r in range(P)]
+        led = np.zeros((P, 6, 4), np.uint64)
+        out = ref.dense_allreduce(ins, led)
+        np.savez_compressed(os.path.join(HERE, "dense", name + ".npz"), P=P, n=n, inputs=np.stack(ins), out=out,
+                            ledger=led)
     print("golden fixtures written to", HERE)
 
 

@@ -58,3 +58,16 @@ def test_gaussiank_scaling_stops_at_floor(oracle):
     assert 4 * int(np.sum(np.abs(g) >= sc)) > 3 * k
     if sc < raw:
         assert 4 * int(np.sum(np.abs(g) >= sc / 0.9)) <= 3 * k
+
+
+DENSE = sorted(os.path.basename(p) for p in glob.glob(os.path.join(os.path.dirname(HERE), "dense", "*.npz")))
+
+
+@pytest.mark.parametrize("name", DENSE)
+def test_oracle_dense_reproduces_golden(oracle, name):
+    fx = dict(np.load(os.path.join(os.path.dirname(HERE), "dense", name)))
+    P = int(fx["P"])
+    led = np.zeros((P, 6, 4), np.uint64)
+    out = oracle.dense_allreduce(list(fx["inputs"]), led)
+    assert np.array_equal(out.view(np.uint64), fx["out"].view(np.uint64))
+    assert np.array_equal(led, fx["ledger"])

@@ -136,3 +136,57 @@ def test_baseline_non_finite_fails_everywhere(okm, gpus, which):
         w.destroy()
     assert isinstance(errs[1], okm.NumericError)
     assert isinstance(errs[0], okm.TransportError)
+
+
+# ---- dense fp64 recursive-halving allreduce (collectives.cpp:89-150) ----
+DENSE_DIR = os.path.join(os.path.dirname(HERE), "dense")
+DENSE = sorted(os.path.basename(p) for p in glob.glob(os.path.join(DENSE_DIR, "*.npz")))
+
+
+def run_dense(okm, gpus, inputs):
+    P = len(inputs)
+    w = okm.World(P, [r % gpus for r in range(P)])
+    try:
+        got = okm.run_ranks(w, lambda ctx: okm.dense_allreduce(ctx, np.asarray(inputs[ctx.rank], np.float32)))
+        led = ledger_array(okm, w, P)
+    finally:
+        w.destroy()
+    for r in range(1, P):
+        assert np.array_equal(got[r].view(np.uint64), got[0].view(np.uint64))
+    return got[0], led
+
+
+@pytest.mark.parametrize("name", DENSE)
+def test_dense_golden(okm, gpus, name):
+    fx = dict(np.load(os.path.join(DENSE_DIR, name)))
+    out, led = run_dense(okm, gpus, list(fx["inputs"]))
+    assert np.array_equal(out.view(np.uint64), fx["out"].view(np.uint64))
+    assert np.array_equal(led, fx["ledger"])
+
+
+@pytest.mark.parametrize("P,n", [(1, 1000), (2, 1_000_003), (4, 3_000_000), (8, 999_999)])
+def test_dense_matches_oracle(okm, gpus, oracle, P, n):
+    rng = np.random.default_rng(P + n)
+    ins = [(rng.standard_normal(n) * 10.0 ** float(r)).astype(np.float32).astype(np.float64) for r in range(P)]
+    out, led = run_dense(okm, gpus, ins)
+    oled = np.zeros((P, 6, 4), np.uint64)
+    want = oracle.dense_allreduce(ins, oled)
+    assert np.array_equal(out.view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(led, oled)
+
+
+def test_dense_length_mismatch_is_protocol_error(okm, gpus):
+    # test_collectives.cpp: ranks with 8 and 9 elements -> ProtocolError
+    w = okm.World(2, [r % gpus for r in range(2)])
+    errs = [None, None]
+
+    def body(ctx):
+        try:
+            okm.dense_allreduce(ctx, np.ones(8 + ctx.rank, np.float32))
+        except okm.OkError as e:
+            errs[ctx.rank] = e
+    try:
+        okm.run_ranks(w, body)
+    finally:
+        w.destroy()
+    assert all(isinstance(e, okm.ProtocolError) for e in errs), errs
