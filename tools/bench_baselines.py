@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """Table-1 comparison on B200: Ok-Topk (ok_sparse_allreduce, steady + refresh
 steps in their natural proportion) against the GPU baselines TopkA, gTopk,
-TopkDSA and Gaussiank and a dense fp32 NCCL allreduce, on the same inputs.
+TopkDSA and Gaussiank, the reference's fp64 dense allreduce (dense64) and a dense
+fp32 NCCL allreduce, on the same inputs.
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/bench_baselines.py \
         [--elements n] [--density d] [--steps K] [--warmup W] [--algos a,b,..]
@@ -34,7 +35,7 @@ def main():
     ap.add_argument("--density", type=float, default=0.01)
     ap.add_argument("--steps", type=int, default=32)
     ap.add_argument("--warmup", type=int, default=4)
-    ap.add_argument("--algos", default="oktopk,topka,gtopk,topkdsa,gaussiank,dense")
+    ap.add_argument("--algos", default="oktopk,topka,gtopk,topkdsa,gaussiank,dense64,dense")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -79,6 +80,12 @@ def main():
             rc = L.okt_sgd_step(comm, g, ctypes.c_void_p(wmodel.data_ptr()), n, 1.0, t, k, ctypes.byref(res), sp)
         elif algo == "gaussiank":
             rc = L.okt_gaussiank_allreduce(comm, g, n, k, 1, ctypes.byref(out), sp)
+        elif algo == "dense64":  # the reference's fp64 recursive-halving dense allreduce
+            p = ctypes.c_void_p()
+            rc = L.okt_dense_allreduce(comm, g, n, ctypes.byref(p), sp)
+            if rc:
+                raise SystemExit(f"dense64 failed: {L.okt_last_error().decode()}")
+            return n
         elif algo == "dense":
             with torch.cuda.stream(stream):
                 dense.copy_(ring[(t - 1) % len(ring)])
