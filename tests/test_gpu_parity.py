@@ -428,3 +428,29 @@ def test_async_steps_match_sync_steps(okm, oracle, gpus, P):
         for t in range(steps):
             assert a[r][t] == b[r][t], (r, t)
         assert torch.equal(models[0][r].cpu(), models[1][r].cpu())
+
+
+# ---- shape and value edge cases (sizes off the 16-byte / tile grid, k >= n,
+# all-zero and tie-heavy inputs, cancelling ranks), several iterations each so
+# the steady path (graph at P = 1, P2P or host-synced at P > 1) runs too ----
+def _edge_inputs(kind, n, seed):
+    rng = np.random.default_rng(seed)
+    if kind == "normal":
+        return lambda t, r: rng.standard_normal(n) * (1 + t)
+    if kind == "zeros":
+        return lambda t, r: np.zeros(n)
+    if kind == "ties":
+        return lambda t, r: rng.choice([-2.0, -1.0, 0.0, 1.0, 2.0], n)
+    if kind == "cancel":  # ranks pair up with opposite signs: explicit zeros in the regions
+        base = {t: rng.standard_normal(n) for t in range(1, 8)}
+        return lambda t, r: base[t] * (1.0 if r % 2 == 0 else -1.0)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("n,k,kind", [
+    (1, 1, "normal"), (3, 2, "normal"), (4097, 40, "normal"), (8195, 9000, "normal"), (5000, 5000, "ties"),
+    (6000, 60, "zeros"), (20_003, 200, "ties"), (12_289, 120, "cancel"),
+])
+def test_edge_shapes_match_oracle(okm, oracle, gpus, P, n, k, kind):
+    run_both(okm, oracle, P, gpus, _edge_inputs(kind, n, 17 * n + k), range(1, 7), k, tau=4, tau_prime=2)
