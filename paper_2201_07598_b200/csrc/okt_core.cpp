@@ -362,8 +362,12 @@ struct okt_comm {
     cap_n = n;
     return OKT_OK;
   }
+  // Data-dependent capacities (region, survivor, receive and gather buffers):
+  // the first allocation takes 2x headroom, so the drift of the counts between
+  // refresh iterations does not land a cudaFree / cudaMalloc pair (a device
+  // synchronisation) inside a later step.
   int ensure(Buf& b, size_t bytes) {
-    const cudaError_t e = b.ensure(bytes);
+    const cudaError_t e = b.ensure(b.p ? bytes : 2 * bytes);
     if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
     return OKT_OK;
   }
