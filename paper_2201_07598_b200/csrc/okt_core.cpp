@@ -362,15 +362,16 @@ struct okt_comm {
     cap_n = n;
     return OKT_OK;
   }
-  // Data-dependent capacities (region, survivor, receive and gather buffers):
-  // the first allocation takes 2x headroom, so the drift of the counts between
-  // refresh iterations does not land a cudaFree / cudaMalloc pair (a device
-  // synchronisation) inside a later step.
   int ensure(Buf& b, size_t bytes) {
-    const cudaError_t e = b.ensure(b.p ? bytes : 2 * bytes);
+    const cudaError_t e = b.ensure(bytes);
     if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
     return OKT_OK;
   }
+  // Data-dependent capacities of the step (region, survivor, receive and
+  // gather buffers, the region staging): the first allocation takes 2x
+  // headroom, so the drift of the counts between refresh iterations does not
+  // land a cudaFree / cudaMalloc pair (a device synchronisation) in a later step.
+  int ensure_dd(Buf& b, size_t bytes) { return ensure(b, b.p ? bytes : 2 * bytes); }
 
   int sync(cudaStream_t s) {
     cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s);
@@ -480,7 +481,7 @@ struct okt_comm {
       roff[q + 1] = roff[q] + (q == rank ? 0 : rcnt[q]);
       if (q != rank) in_total += rcnt[q];
     }
-    if ((rc = ensure(rbuf, 8 * std::max<uint64_t>(in_total, 1)))) return rc;
+    if ((rc = ensure_dd(rbuf, 8 * std::max<uint64_t>(in_total, 1)))) return rc;
     std::vector<Xfer> sends, recvs;
     uint64_t* cooP = coo.as<uint64_t>();
     uint64_t* rb = rbuf.as<uint64_t>();
@@ -495,10 +496,10 @@ struct okt_comm {
     // K3: region merge.
     tmark(OKT_T_MERGE, s);
     const uint64_t bound = in_total + scnt[rank];
-    if ((rc = ensure(mask, ((W + 15) / 16) * 16 + 16))) return rc;
-    if ((rc = ensure(stage, 4 * std::max<uint64_t>(W, 1) * P))) return rc;
-    if ((rc = ensure(out_idx, 4 * std::max<uint64_t>(bound, 1)))) return rc;
-    if ((rc = ensure(out_val, 8 * std::max<uint64_t>(bound, 1)))) return rc;
+    if ((rc = ensure_dd(mask, ((W + 15) / 16) * 16 + 16))) return rc;
+    if ((rc = ensure_dd(stage, 4 * std::max<uint64_t>(W, 1) * P))) return rc;
+    if ((rc = ensure_dd(out_idx, 4 * std::max<uint64_t>(bound, 1)))) return rc;
+    if ((rc = ensure_dd(out_val, 8 * std::max<uint64_t>(bound, 1)))) return rc;
     okt::Segs segs{};
     segs.nseg = 0;
     segs.start[0] = 0;
@@ -541,7 +542,7 @@ struct okt_comm {
       goff[q + 1] = goff[q] + parts[q];
     }
     const uint64_t total = goff[P];
-    if ((rc = ensure(gval, 8 * std::max<uint64_t>(total, 1)))) return rc;
+    if ((rc = ensure_dd(gval, 8 * std::max<uint64_t>(total, 1)))) return rc;
     double* gv = gval.as<double>();
     if (parts[rank]) {
       rc = ck(cudaMemcpyAsync(gv + goff[rank], reg_val.p, 8 * parts[rank], cudaMemcpyDeviceToDevice, s),
@@ -578,8 +579,8 @@ struct okt_comm {
     const okt::plan::Balance B = okt::plan::balance(rank, P, sizes);
     const uint64_t total = B.total;
     U = total;
-    if ((rc = ensure(u_idx, 4 * std::max<uint64_t>(total, 1)))) return rc;
-    if ((rc = ensure(u_val, 8 * std::max<uint64_t>(total, 1)))) return rc;
+    if ((rc = ensure_dd(u_idx, 4 * std::max<uint64_t>(total, 1)))) return rc;
+    if ((rc = ensure_dd(u_val, 8 * std::max<uint64_t>(total, 1)))) return rc;
     uint32_t* ui = u_idx.as<uint32_t>();
     double* uv = u_val.as<double>();
     const uint32_t* si = sur_idx.as<uint32_t>();
@@ -827,7 +828,7 @@ struct okt_comm {
     int rc;
     const uint64_t lo = st.cuts[rank], hi = st.cuts[rank + 1];
     const uint64_t W = hi > lo ? hi - lo : 0;
-    if ((rc = ensure(mask, ((W + 15) / 16) * 16 + 16)) || (rc = ensure(stage, 4 * std::max<uint64_t>(W, 1) * P)))
+    if ((rc = ensure_dd(mask, ((W + 15) / 16) * 16 + 16)) || (rc = ensure_dd(stage, 4 * std::max<uint64_t>(W, 1) * P)))
       return rc;
     if (prof || !graphs_on) return enqueue_p2p_step(n, k, sgd, s);
     P2PGraph& G = graph2;
@@ -1255,8 +1256,8 @@ struct okt_comm {
         tmark(OKT_T_GLOBAL, s);
         rc = refresh_global_dev(k, bound, s);
         if (!rc) {
-          if ((rc = ensure(sur_idx, 4 * std::max<uint64_t>(bound, 1))) ||
-              (rc = ensure(sur_val, 8 * std::max<uint64_t>(bound, 1))))
+          if ((rc = ensure_dd(sur_idx, 4 * std::max<uint64_t>(bound, 1))) ||
+              (rc = ensure_dd(sur_val, 8 * std::max<uint64_t>(bound, 1))))
             return abort_step(rc);
           rc = ck(okt::launch_filter(L, S, false, nullptr, reg_idx.as<uint32_t>(), reg_val.as<double>(), &d()->R,
                                      bound, &d()->global_th, sur_idx.as<uint32_t>(), sur_val.as<double>(),
@@ -1268,7 +1269,7 @@ struct okt_comm {
       uint64_t U = 0;
       rc = balance_allgatherv_dev(s, U);
       if (rc) return abort_step(rc);
-      if ((rc = ensure(indexes, 4 * std::max<uint64_t>(U, 1)))) return abort_step(rc);
+      if ((rc = ensure_dd(indexes, 4 * std::max<uint64_t>(U, 1)))) return abort_step(rc);
       if ((rc = upload_u64(&d()->U, U, &hup->U, s))) return abort_step(rc);
       U_bound = U;
       d_U = &d()->U;
