@@ -94,6 +94,7 @@ struct DevScalars {
                    // bit3 peer timeout, bit4 peer failure
   uint32_t pad1;
   uint32_t pflags[2];  // the single-rank graph step's flag words, by step parity
+  uint32_t p2pflags[2];  // the argument-fed P2P step's flag words, by step parity
   okt::P2PPlan plan;
   uint64_t cuts[OKT_MAX_WORLD + 1];
   uint64_t off[OKT_MAX_WORLD + 1];
@@ -752,6 +753,21 @@ struct okt_comm {
     return OKT_OK;
   }
 
+  // K1's P2P arguments for this step (hup->sp holds the step block).
+  okt::K1P2P k1p2p_args(bool argfed) {
+    okt::K1P2P kp;
+    kp.tab = tabd.as<okt::PeerTab>();
+    kp.sp = &d()->sp;
+    kp.cuts = d()->cuts;
+    if (argfed) {
+      kp.par_v = hup->sp.par;
+      kp.sp_out = &d()->sp;
+      kp.plan_zero = &d()->plan;
+      kp.spv = hup->sp;
+    }
+    return kp;
+  }
+
   // Enqueues a whole steady P2P iteration on `s` (no host synchronisation):
   // step block refresh, flag reset, K1 (+ slice offsets + L publication),
   // fused split/scatter, bracket scan (+ survivor publication), allgatherv
@@ -765,18 +781,25 @@ struct okt_comm {
     const uint64_t lo = st.cuts[rank], hi = st.cuts[rank + 1];
     const uint64_t W = hi > lo ? hi - lo : 0;
     (void)k;
-    // one H2D: the step block, zeroed flags and a zeroed plan
-    const size_t blk = offsetof(DevScalars, plan) + sizeof(okt::P2PPlan) - offsetof(DevScalars, sp);
-    int rc = ck(cudaMemcpyAsync(&d()->sp, &hup->sp, blk, cudaMemcpyHostToDevice, s), "h2d");
+    // EF steps are argument-fed: the step block rides in K1's arguments (K1's
+    // CTA 0 stores it and clears the plan; the flag word alternates by parity
+    // and the pull clears the next one), so the step starts with K1 — no H2D
+    // node.  The plain allreduce keeps one H2D of the step block, zeroed flags
+    // and a zeroed plan.
+    const bool argfed = sgd;
+    const int par = hup->sp.par;
+    uint32_t* fl = argfed ? &d()->p2pflags[par] : &d()->flags;
+    int rc = OKT_OK;
+    if (!argfed) {
+      const size_t blk = offsetof(DevScalars, plan) + sizeof(okt::P2PPlan) - offsetof(DevScalars, sp);
+      rc = ck(cudaMemcpyAsync(&d()->sp, &hup->sp, blk, cudaMemcpyHostToDevice, s), "h2d");
+    }
     tmark(OKT_T_SELECT, s);
-    okt::K1P2P kp;
-    kp.tab = dt;
-    kp.sp = sp;
-    kp.cuts = d()->cuts;
+    okt::K1P2P kp = k1p2p_args(argfed);
     if (!rc)
       rc = ck(okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, hup->sp.g,
                              hup->sp.eps_in, hup->sp.eps_out, hup->sp.alpha, n, &d()->local_th, nullptr,
-                             okt::OutCoo{}, &d()->m, nullptr, &d()->flags, nullptr, nullptr, &kp, sp),
+                             okt::OutCoo{}, &d()->m, nullptr, fl, nullptr, nullptr, &kp, argfed ? nullptr : sp),
               "k1");
     // K1's totals (selection size, slice offsets) on a side branch
     okt::K1Totals kt;
@@ -789,17 +812,17 @@ struct okt_comm {
     tmark(OKT_T_MERGE, s);
     // split exchange + region merge in one kernel (reads every source's K1
     // tiles of my region in place)
-    if (!rc) rc = ck(okt::launch_p2p_merge(L, dt, sp, dp, P, lo, W, n, &d()->global_th, &d()->flags, kP2PTimeoutNs),
-                     "p2p");
+    if (!rc) rc = ck(okt::launch_p2p_merge(L, dt, sp, dp, P, lo, W, n, &d()->global_th, fl, kP2PTimeoutNs), "p2p");
     tmark(OKT_T_ALLGATHER, s);
     okt::P2PApply pa;
     pa.on = 1;
+    pa.flags2 = argfed ? d()->p2pflags : nullptr;
     pa.sgd = sgd ? 1 : 0;
     pa.d_local_th = &d()->local_th;
     // oktopk_sgd_step reports no index list (trainer.hpp:123-127): only the
     // plain allreduce needs the sel flags and the indexes compaction.
     pa.sel = sgd ? nullptr : selflags.as<uint8_t>();
-    if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, sp, &d()->S, dp, &d()->U, &d()->flags, kP2PTimeoutNs, pa,
+    if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, sp, &d()->S, dp, &d()->U, fl, kP2PTimeoutNs, pa,
                                                 sgd ? hp2p_dev : nullptr, S.tile_ctr + 4),
                      "p2p");
     if (!sgd) {
@@ -820,6 +843,8 @@ struct okt_comm {
     size_t n = 0, k = 0;
     bool sgd = false;
     uint64_t lo = 0, W = 0, gen = 0, win = 0, kernels = 0;
+    cudaGraph_t graph = nullptr;  // kept: its kernel nodes are patched per launch (argument-fed steps)
+    cudaGraphNode_t k1 = nullptr, merge = nullptr, pull = nullptr;
   } graph2;
 
   // The steady P2P iteration through one graph launch (captured on first use
@@ -847,8 +872,36 @@ struct okt_comm {
         if (graph) cudaGraphDestroy(graph);
         return rc ? rc : ck(e2, "graph capture");
       }
+      G.k1 = G.merge = G.pull = nullptr;
+      if (sgd) {  // the nodes whose arguments change per step (K1: the kernel that is none of the others)
+        size_t nn = 0;
+        cudaGraphGetNodes(graph, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(graph, nodes.data(), &nn);
+        const void* fm = okt::p2p_merge_func(P);
+        const void* fp = okt::p2p_pull_func();
+        const void* ft = okt::p2p_totals_func();
+        for (cudaGraphNode_t nd : nodes) {
+          cudaGraphNodeType ty;
+          cudaGraphNodeGetType(nd, &ty);
+          if (ty != cudaGraphNodeTypeKernel) continue;
+          cudaKernelNodeParams kp{};
+          cudaGraphKernelNodeGetParams(nd, &kp);
+          if (kp.func == fm) G.merge = nd;
+          else if (kp.func == fp) G.pull = nd;
+          else if (kp.func != ft) G.k1 = nd;
+        }
+      }
       const cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
-      cudaGraphDestroy(graph);
+      if (sgd && (!G.k1 || !G.merge || !G.pull)) {
+        if (e == cudaSuccess) cudaGraphExecDestroy(G.exec);
+        G.exec = nullptr;
+        cudaGraphDestroy(graph);
+        return set_err(OKT_ERR_INTERNAL, "P2P step graph: kernel nodes not found");
+      }
+      // (the node handles stay valid for exec updates while the graph lives)
+      if (G.graph) cudaGraphDestroy(G.graph);
+      G.graph = graph;
       if ((rc = ck(e, "graph instantiate"))) return rc;
       G.kernels = L.launches - l0;
       L.launches = l0;
@@ -859,10 +912,33 @@ struct okt_comm {
       G.W = W;
       G.gen = gen;
       G.win = win_n;
+    } else if (sgd) {
+      // this step's arguments into the instantiated nodes: K1 (g, eps_in,
+      // eps_out, alpha, the flag word, K1P2P = arguments 0-3, 12, 15), the
+      // merge's and the pull's flag word (arguments 7 and 5)
+      uint32_t* fl = &d()->p2pflags[hup->sp.par];
+      okt::K1P2P kp = k1p2p_args(true);
+      if ((rc = patch_node(G.exec, G.k1, 16, {{0, &hup->sp.g}, {1, &hup->sp.eps_in}, {2, &hup->sp.eps_out},
+                                              {3, &hup->sp.alpha}, {12, &fl}, {15, &kp}})) ||
+          (rc = patch_node(G.exec, G.merge, 9, {{7, &fl}})) || (rc = patch_node(G.exec, G.pull, 10, {{5, &fl}})))
+        return rc;
     }
     if ((rc = ck(cudaGraphLaunch(G.exec, s), "graph launch"))) return rc;
     L.launches += G.kernels;
     return OKT_OK;
+  }
+
+  // Rewrites some arguments of an instantiated kernel node (index -> value).
+  int patch_node(cudaGraphExec_t exec, cudaGraphNode_t nd, int nargs,
+                 std::initializer_list<std::pair<int, void*>> args) {
+    cudaKernelNodeParams kp{};
+    int rc = ck(cudaGraphKernelNodeGetParams(nd, &kp), "graph params");
+    if (rc) return rc;
+    void* a[24];
+    for (int i = 0; i < nargs && i < 24; ++i) a[i] = kp.kernelParams[i];
+    for (const auto& x : args) a[x.first] = x.second;
+    kp.kernelParams = a;
+    return ck(cudaGraphExecKernelNodeSetParams(exec, nd, &kp), "graph params");
   }
 
   // Ledger of a P2P step, from the sizes every rank agreed on (h valid).
@@ -1607,6 +1683,8 @@ int okt_comm_destroy(okt_comm* c) {
   if (c->hp2p) cudaFreeHost(c->hp2p);
   if (c->graph1.exec) cudaGraphExecDestroy(c->graph1.exec);
   if (c->graph1.graph) cudaGraphDestroy(c->graph1.graph);
+  if (c->graph2.exec) cudaGraphExecDestroy(c->graph2.exec);
+  if (c->graph2.graph) cudaGraphDestroy(c->graph2.graph);
   if (c->graph1.e0) {
     cudaEventDestroy(c->graph1.e0);
     cudaEventDestroy(c->graph1.e1);

@@ -282,8 +282,16 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
   const int lt_P = p2p_on ? p2p.tab->P : 0;
   const int me_rank = p2p_on ? p2p.tab->rank : 0;
   uint32_t* lt_out = nullptr;
+  const int p2p_par = p2p_on ? (p2p.par_v >= 0 ? p2p.par_v : p2p.sp->par) : 0;
+  if (p2p_on && p2p.sp_out && blockIdx.x == 0) {
+    // argument-fed step: publish the step block for the later kernels of the
+    // step (they start after this grid) and clear the plan
+    if (threadIdx.x == 0) *p2p.sp_out = p2p.spv;
+    uint32_t* pz = reinterpret_cast<uint32_t*>(p2p.plan_zero);
+    for (int i = threadIdx.x; i < int(sizeof(P2PPlan) / 4); i += blockDim.x) pz[i] = 0u;
+  }
   if (p2p_on) {
-    const int me = p2p.tab->rank, par = p2p.sp->par;
+    const int me = p2p.tab->rank, par = p2p_par;
     stg = p2p.tab->kstg[me][par];
     counts = p2p.tab->kcnt[me][par];
     lt_out = p2p.tab->klt[me][par];
@@ -464,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
     // published by the next kernel on the stream (the P2P scatter) once every
     // CTA of this one has finished: a system fence issued here, while the grid
     // still streams, would wait for that traffic to drain (tools/fence_lat.cu).
-    P2PPub* pub = &p2p.tab->hdr[me_rank]->pub[p2p.sp->par];
+    P2PPub* pub = &p2p.tab->hdr[me_rank]->pub[p2p_par];
     pub->k1_G = tiles;  // chunk = tile
     pub->k1_cap = TILE;
   }

@@ -164,6 +164,10 @@ cudaError_t launch_scatter_heavy(Launch& L, const uint32_t* pos, const float* va
 // of every source read in place; survivors chunked into my window).
 cudaError_t launch_p2p_merge(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, int P, uint64_t lo,
                              uint64_t W, uint64_t n, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns);
+// The P2P kernels, for per-step parameter updates of the instantiated step graph.
+const void* p2p_merge_func(int P);
+const void* p2p_pull_func();
+const void* p2p_totals_func();
 // Waits for every rank's survivors, plans (offsets / balance), pulls u.
 cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, uint64_t* d_S,
                                   P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns,

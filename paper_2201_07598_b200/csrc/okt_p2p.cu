@@ -224,7 +224,10 @@ __global__ void __launch_bounds__(kThreads)
     trace_stamp(trace, kTrPull0, 0);
     // done[par] counts this step's CTAs through the balanced hand-off; the
     // previous step cleared it, this one clears the next step's
-    if (blockIdx.x == 0) done[par ^ 1] = 0;
+    if (blockIdx.x == 0) {
+      done[par ^ 1] = 0;
+      if (ap.flags2) ap.flags2[par ^ 1] = 0;  // the next argument-fed step's flag word
+    }
   }
   __syncthreads();
   {
@@ -575,5 +578,16 @@ cudaError_t launch_p2p_barrier(Launch& L, const PeerTab* d_tab, uint64_t epoch, 
   ++L.launches;
   return cudaGetLastError();
 }
+
+const void* p2p_merge_func(int P) {
+  switch (P) {
+    case 2: return reinterpret_cast<const void*>(p2p_merge_kernel<2>);
+    case 4: return reinterpret_cast<const void*>(p2p_merge_kernel<4>);
+    case 8: return reinterpret_cast<const void*>(p2p_merge_kernel<8>);
+  }
+  return nullptr;
+}
+const void* p2p_pull_func() { return reinterpret_cast<const void*>(p2p_pull_kernel); }
+const void* p2p_totals_func() { return reinterpret_cast<const void*>(p2p_totals_kernel); }
 
 }  // namespace okt

@@ -115,6 +115,7 @@ struct P2PPlan {
 // K7 fused into the allgatherv pull: every u entry is touched once.
 struct P2PApply {
   int on = 0;
+  uint32_t* flags2 = nullptr;   // argument-fed step: the per-parity flag words; CTA 0 clears flags2[par ^ 1]
   int sgd = 0;                  // acc = sp->eps_out and w = sp->w; else acc = sp->g
   const double* d_local_th = nullptr;
   uint8_t* sel = nullptr;       // per u entry: 1 if in the local selection
@@ -140,6 +141,13 @@ struct K1P2P {
   const PeerTab* tab = nullptr;  // device copy
   const StepPtrs* sp = nullptr;  // epoch / parity of the step
   const uint64_t* cuts = nullptr;
+  // Argument-fed step (EF steps; no H2D node): the step block travels here by
+  // value, K1's CTA 0 stores it at sp_out for the later kernels and zeroes the
+  // plan; par_v replaces sp->par inside K1.
+  int par_v = -1;
+  StepPtrs* sp_out = nullptr;
+  P2PPlan* plan_zero = nullptr;
+  StepPtrs spv{};
 };
 struct K1Totals {  // where the local selection size / slice offsets go
   uint64_t* d_m = nullptr;
