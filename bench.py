@@ -255,6 +255,25 @@ def trace_steps(args, rank, stream, step, t0, step_async=None, wait=None, flush=
 
 
 # ---- our arm ------------------------------------------------------------------------
+def bind_to_gpu_cpus(gpu: int) -> str:
+    """Pin this rank to the CPU cores local to its GPU (NVML's affinity mask),
+    so its pinned host buffers are first-touched on the GPU's NUMA node — the
+    usual one-process-per-GPU deployment.  Returns a description for the JSON."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return f"bound to the GPU-local cores ({len(cpus)} of {os.cpu_count()})"
+    except Exception as e:  # no NVML affinity: leave the scheduler's placement
+        return f"unbound ({type(e).__name__})"
+    return "unbound"
+
+
 def run_okt(args):
     import torch
     import torch.distributed as dist
@@ -267,6 +286,7 @@ def run_okt(args):
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
+    affinity = bind_to_gpu_cpus(local)
     L = lib()
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -484,7 +504,7 @@ def run_okt(args):
                 "e2e": {"value": e2e_ms, "unit": "ms/iter", "h2d_bytes_per_step": 4 * n,
                         "d2h_bytes_per_step": int(d2h / e2e_steps), "steps": e2e_steps,
                         "ms_min": min(e2e_list), "ms_median": statistics.median(e2e_list), "ms_max": max(e2e_list),
-                        "path": "okt_sgd_step_host: gradient H2D from pinned host memory, step, u D2H"},
+                        "path": "okt_sgd_step_host: gradient H2D from pinned host memory, step, u D2H", "cpu_affinity": affinity},
                 "gpu_launches": int(launches1.value - launches0.value),
                 "roofline": {"bound": "hbm", "kernel": "k1_kernel (fused residual accumulate + threshold select "
                                                          "+ chunk-local COO compaction; phase A of K1)",
