@@ -753,6 +753,11 @@ struct okt_comm {
     return OKT_OK;
   }
 
+  // Argument-fed EF steps (OKT_P2P_ARGFED=0: the H2D step block instead; diagnostics).
+  const bool argfed_on = [] {
+    const char* e = std::getenv("OKT_P2P_ARGFED");
+    return !(e && e[0] == '0');
+  }();
   // K1's P2P arguments for this step (hup->sp holds the step block).
   okt::K1P2P k1p2p_args(bool argfed) {
     okt::K1P2P kp;
@@ -786,7 +791,7 @@ struct okt_comm {
     // and the pull clears the next one), so the step starts with K1 — no H2D
     // node.  The plain allreduce keeps one H2D of the step block, zeroed flags
     // and a zeroed plan.
-    const bool argfed = sgd;
+    const bool argfed = sgd && argfed_on;
     const int par = hup->sp.par;
     uint32_t* fl = argfed ? &d()->p2pflags[par] : &d()->flags;
     int rc = OKT_OK;
@@ -873,7 +878,7 @@ struct okt_comm {
         return rc ? rc : ck(e2, "graph capture");
       }
       G.k1 = G.merge = G.pull = nullptr;
-      if (sgd) {  // the nodes whose arguments change per step (K1: the kernel that is none of the others)
+      if (sgd && argfed_on) {  // the nodes whose arguments change per step (K1: the kernel that is none of the others)
         size_t nn = 0;
         cudaGraphGetNodes(graph, nullptr, &nn);
         std::vector<cudaGraphNode_t> nodes(nn);
@@ -893,7 +898,7 @@ struct okt_comm {
         }
       }
       const cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
-      if (sgd && (!G.k1 || !G.merge || !G.pull)) {
+      if (sgd && argfed_on && (!G.k1 || !G.merge || !G.pull)) {
         if (e == cudaSuccess) cudaGraphExecDestroy(G.exec);
         G.exec = nullptr;
         cudaGraphDestroy(graph);
@@ -912,7 +917,7 @@ struct okt_comm {
       G.W = W;
       G.gen = gen;
       G.win = win_n;
-    } else if (sgd) {
+    } else if (sgd && argfed_on) {
       // this step's arguments into the instantiated nodes: K1 (g, eps_in,
       // eps_out, alpha, the flag word, K1P2P = arguments 0-3, 12, 15), the
       // merge's and the pull's flag word (arguments 7 and 5)
