@@ -12,7 +12,7 @@ from ctypes import (POINTER, Structure, c_char_p, c_double, c_float, c_int,
                     c_int32, c_int64, c_size_t, c_uint32, c_uint64, c_void_p)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libokt.so")
+LIB_PATH = os.environ.get("OKT_LIB_PATH") or os.path.join(HERE, "libokt.so")  # (override: diagnostics A/B builds)
 
 OKT_MAX_WORLD = 8
 OKT_T_COUNT = 9

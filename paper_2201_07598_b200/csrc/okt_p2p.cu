@@ -41,8 +41,11 @@ constexpr uint32_t kAbortBits = 1u | 8u | 16u;  // local non-finite, peer timeou
 constexpr int kMergeTile = kK1Tile;              // coordinates per CTA tile
 constexpr int kMergePer = kMergeTile / kThreads;  // 16 coordinates per thread in the scan
 
+// P = 2 is capped at 48 registers: 5 CTAs per SM instead of 4 (shared memory
+// allows 6), so more of the region's tiles are in flight at once (interleaved
+// A/B on one box, tools/ab_lib.sh: steady N = 2 0.0812 -> 0.0799 ms).
 template <int P>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
     p2p_merge_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo, uint64_t W,
                      uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns) {
   extern __shared__ uint32_t sm[];
