@@ -163,6 +163,7 @@ struct WinInfo {
   unsigned char uuid[16];
   int32_t device;
   int32_t ok;
+  uint64_t layout_bytes;  // peers compute offsets from their own layout: it must match
 };
 
 constexpr uint64_t kP2PTimeoutNs = 20ull * 1000 * 1000 * 1000;
@@ -202,6 +203,7 @@ struct okt_comm {
   Buf indexes;
   Buf eps[2];
   Buf hgrad;               // staging for the host-buffer entry points
+  Buf galign;              // 16-byte aligned copy of a misaligned gradient (P2P step)
   Buf st64, stidx, stval;  // phase-A compaction staging
   Buf counts, counts2, chunkcap, tilectr;
   Buf hist, scal;
@@ -376,9 +378,15 @@ struct okt_comm {
 
   int sync(cudaStream_t s) {
     cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s);
-    const cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return set_err(OKT_ERR_CUDA, std::string("device: ") + cudaGetErrorString(e));
-    return OKT_OK;
+    return wait_stream(s);
+  }
+  // Host wait on a stream that may hold collectives: bounded on the NCCL
+  // transport (a dead peer -> TransportError after the deadline, never a hang).
+  int wait_stream(cudaStream_t s) {
+    std::string err;
+    const int rc = tr ? tr->wait(s, err) : ck(cudaStreamSynchronize(s), "device");
+    if (rc && tr) return set_err(rc, err);
+    return rc;
   }
   int ck(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return OKT_OK;
@@ -638,7 +646,7 @@ struct okt_comm {
     rc = tr->allgather(b + bytes * P, b, bytes, s, err);
     if (rc) return comm_err(rc, err);
     if ((rc = ck(cudaMemcpyAsync(all, b, bytes * P, cudaMemcpyDeviceToHost, s), "d2h"))) return rc;
-    return ck(cudaStreamSynchronize(s), "sync");
+    return wait_stream(s);
   }
 
   void close_peers() {
@@ -673,6 +681,7 @@ struct okt_comm {
     me.pid = uint64_t(getpid());
     me.base = reinterpret_cast<uint64_t>(win.p);
     me.device = device;
+    me.layout_bytes = lay.bytes;
     me.ok = cudaIpcGetMemHandle(&me.handle, win.p) == cudaSuccess;
     cudaGetLastError();
     cudaDeviceProp prop;
@@ -689,6 +698,10 @@ struct okt_comm {
     for (int q = 0; q < P && ok; ++q) {
       if (q == rank) continue;
       const bool same_gpu = std::memcmp(all[q].uuid, me.uuid, 16) == 0;
+      if (all[q].layout_bytes != me.layout_bytes) {
+        ok = false;  // asymmetric windows (e.g. GPUs with different SM counts): host-synchronised path
+        break;
+      }
       if (!all[q].ok || (same_gpu && !(allow_shared && all[q].pid == me.pid))) {
         ok = false;  // a shared GPU: in-kernel cross-rank waits are not safe there
         break;
@@ -1181,9 +1194,18 @@ struct okt_comm {
     auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
     const bool use_graph = P == 1 && !thr && graphs_on && al16(g) && (!sgd || al16(w));
     if (P > 1 && (rc = setup_p2p(n, s))) return rc;
+    // The path choice must be the same on every rank, so it may not depend on
+    // rank-local pointer alignment: a gradient that is not 16-byte aligned
+    // (the vectorised K1 of the device-driven step needs it) is staged into an
+    // aligned buffer first.  (The model is only scattered: any alignment.)
+    if (P > 1 && p2p && !al16(g)) {
+      if ((rc = ensure(galign, 4 * n))) return rc;
+      if ((rc = ck(cudaMemcpyAsync(galign.p, g, 4 * n, cudaMemcpyDeviceToDevice, s), "stage"))) return rc;
+      g = galign.as<float>();
+    }
     // Steady iterations on distinct GPUs run the device-driven exchange; the
     // refresh iterations (1 in tau') keep the host-synchronised protocol.
-    const bool use_p2p = p2p && !thr && !bnd && st.regions == P && al16(g) && (!sgd || al16(w));
+    const bool use_p2p = p2p && !thr && !bnd && st.regions == P;
     if (!use_graph && !use_p2p && (rc = ck(cudaMemsetAsync(&d()->flags, 0, 4, s), "memset"))) return rc;
     uint64_t epoch = 0;
     int par = 0;
@@ -1458,10 +1480,12 @@ struct okt_comm {
       dev_stale = true;
       return set_err(OKT_ERR_PROTOCOL, "split_and_reduce: entries outside my region");
     }
-    // Commit.
-    st.local_th = h->local_th;
-    st.global_th = h->global_th;
+    // Commit.  Thresholds change only on refresh iterations (oktopk.cpp:258-293);
+    // a steady step leaves them alone.  (The steady graph / P2P steps refresh
+    // only part of the mirror h, so its threshold words may be stale there.)
     if (thr) {
+      st.local_th = h->local_th;
+      st.global_th = h->global_th;
       st.last_local_eval = t;
       st.last_global_eval = t;
     }
@@ -1486,7 +1510,11 @@ struct okt_comm {
     dev_stale = true;
     hp2p_pending = false;
     hfast_pending = false;
-    cudaStreamSynchronize(L.s);
+    {
+      std::string e2;  // (bounded: an aborted NCCL comm has ended its kernels)
+      if (tr) tr->wait(L.s, e2);
+      else cudaStreamSynchronize(L.s);
+    }
     cudaGetLastError();
     spans.clear();
     ev_used = 0;
@@ -1662,8 +1690,13 @@ int okt_comm_init_nccl(okt_comm** out, int rank, int P, int device, const void* 
   ncclUniqueId id;
   std::memcpy(&id, uid, sizeof(id));
   ncclComm_t nc = nullptr;
-  const ncclResult_t r = ncclCommInitRank(&nc, P, id, rank);
+  // Non-blocking communicator: every later wait on it is bounded (okt_transport.hpp).
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  cfg.blocking = 0;
+  ncclResult_t r = ncclCommInitRankConfig(&nc, P, id, rank, &cfg);
+  if (r == ncclInProgress) r = okt::NcclTransport::settle(nc, std::max(120000L, okt::NcclTransport::timeout_from_env()));
   if (r != ncclSuccess) {
+    if (nc) ncclCommAbort(nc);
     delete c;
     return set_err(OKT_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   }
@@ -2117,7 +2150,7 @@ int bl_prefix(okt_comm* c, const uint32_t* d_cnt, uint64_t chunks, uint64_t* d_o
               cudaStream_t s) {
   std::vector<uint32_t> hc(chunks);
   int rc = c->ck(cudaMemcpyAsync(hc.data(), d_cnt, 4 * chunks, cudaMemcpyDeviceToHost, s), "d2h");
-  if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  if (rc || (rc = c->wait_stream(s))) return rc;
   std::vector<uint64_t> ho(chunks);
   uint64_t pos = 0;
   for (uint64_t i = 0; i < chunks; ++i) {
@@ -2126,7 +2159,7 @@ int bl_prefix(okt_comm* c, const uint32_t* d_cnt, uint64_t chunks, uint64_t* d_o
   }
   total = pos;
   rc = c->ck(cudaMemcpyAsync(d_off, ho.data(), 8 * chunks, cudaMemcpyHostToDevice, s), "h2d");
-  if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  if (rc || (rc = c->wait_stream(s))) return rc;
   return OKT_OK;
 }
 
@@ -2147,7 +2180,7 @@ int bl_trim(okt_comm* c, const uint64_t* aos_in, const uint32_t* idx_in, const d
   if (rc) return rc;
   std::vector<uint32_t> hc(2 * chunks);
   if ((rc = c->ck(cudaMemcpyAsync(hc.data(), gt, 8 * chunks, cudaMemcpyDeviceToHost, s), "d2h"))) return rc;
-  if ((rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  if ((rc = c->wait_stream(s))) return rc;
   uint64_t n_gt = 0;
   for (uint64_t i = 0; i < chunks; ++i) n_gt += hc[i];
   if (n_gt >= k) return set_err(OKT_ERR_INTERNAL, "topk_exact: threshold above the k-th magnitude");
@@ -2165,7 +2198,7 @@ int bl_trim(okt_comm* c, const uint64_t* aos_in, const uint32_t* idx_in, const d
   if ((rc = c->ck(cudaMemcpyAsync(off, ho.data(), 16 * chunks, cudaMemcpyHostToDevice, s), "h2d"))) return rc;
   rc = c->ck(okt::launch_topk_write(c->L, aos_in, idx_in, val_in, m, th, off, eqb, need, aos_out, idx_out, val_out),
              "topk_write");
-  if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  if (rc || (rc = c->wait_stream(s))) return rc;
   return OKT_OK;
 }
 
@@ -2395,7 +2428,7 @@ int okt_dense_allreduce(okt_comm* c, const float* d_g, size_t n, double** d_out,
       bl_credit_pair(c, OKT_PHASE_DENSE, mc, tc);
     }
   }
-  if ((rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  if ((rc = c->wait_stream(s))) return rc;
   *d_out = buf;
   return OKT_OK;
 }
@@ -2466,7 +2499,7 @@ int okt_gtopk_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt_s
   if ((rc = c->ensure(c->sel_idx, 4 * k)) || (rc = c->ensure(c->sel_val, 8 * k))) return rc;
   rc = c->ck(cudaMemcpyAsync(c->sel_idx.p, A.idx, 4 * k, cudaMemcpyDeviceToDevice, s), "copy");
   if (!rc) rc = c->ck(cudaMemcpyAsync(c->sel_val.p, A.val, 8 * k, cudaMemcpyDeviceToDevice, s), "copy");
-  if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  if (rc || (rc = c->wait_stream(s))) return rc;
   *out = okt_sparse{c->sel_idx.as<uint32_t>(), c->sel_val.as<double>(), k, n};
   return OKT_OK;
 }
@@ -2498,7 +2531,7 @@ int okt_topkdsa_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt
     if ((rc = c->ensure(c->sel_idx, 4 * k)) || (rc = c->ensure(c->sel_val, 8 * k))) return rc;
     rc = c->ck(cudaMemcpyAsync(c->sel_idx.p, A.idx, 4 * k, cudaMemcpyDeviceToDevice, s), "copy");
     if (!rc) rc = c->ck(cudaMemcpyAsync(c->sel_val.p, A.val, 8 * k, cudaMemcpyDeviceToDevice, s), "copy");
-    if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+    if (rc || (rc = c->wait_stream(s))) return rc;
     *out = okt_sparse{c->sel_idx.as<uint32_t>(), c->sel_val.as<double>(), k, n};
     return OKT_OK;
   }
@@ -2534,7 +2567,7 @@ int okt_topkdsa_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt
       rc = c->ck(okt::launch_slice_bounds(c->L, A.idx, A.nnz, s0, s1, sb), "slice");
       if (!rc) rc = c->ck(okt::launch_slice_bounds(c->L, A.idx, A.nnz, k0, k1, sb + 2), "slice");
       if (!rc) rc = c->ck(cudaMemcpyAsync(hb, sb, 32, cudaMemcpyDeviceToHost, s), "d2h");
-      if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+      if (rc || (rc = c->wait_stream(s))) return rc;
       a_s0 = hb[0]; a_s1 = hb[1]; a_k0 = hb[2]; a_k1 = hb[3];
     }
     // header {kind, count}: 1 = dense half, 0 = COO
@@ -2633,7 +2666,7 @@ int okt_topkdsa_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, okt
   rc = c->tr->exchange(sends, recvs, s, err);
   if (rc) return c->comm_err(rc, err);
   c->credit_allgatherv(OKT_PHASE_ALLGATHERV, segn, 12);
-  if ((rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  if ((rc = c->wait_stream(s))) return rc;
   *out = okt_sparse{ui, uv, U, n};
   return OKT_OK;
 }
@@ -2659,7 +2692,7 @@ int okt_gaussiank_threshold(okt_comm* c, const float* d_g, size_t n, size_t k, i
   rc = c->ck(okt::launch_moments(c->L, d_g, n, partial, dm, dm + 1), "moments");
   double* hm = reinterpret_cast<double*>(&c->hup->prop[0]);
   if (!rc) rc = c->ck(cudaMemcpyAsync(hm, dm, 16, cudaMemcpyDeviceToHost, s), "d2h");
-  if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+  if (rc || (rc = c->wait_stream(s))) return rc;
   const double mean = hm[0], var = hm[1];
   if (!std::isfinite(mean) || !std::isfinite(var))
     return set_err(OKT_ERR_NUMERIC, "gaussian_threshold: non-finite input");
@@ -2673,7 +2706,7 @@ int okt_gaussiank_threshold(okt_comm* c, const float* d_g, size_t n, size_t k, i
     for (;;) {
       rc = c->ck(okt::launch_count_ge(c->L, d_g, n, t, dc), "count_ge");
       if (!rc) rc = c->ck(cudaMemcpyAsync(hc, dc, 8, cudaMemcpyDeviceToHost, s), "d2h");
-      if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+      if (rc || (rc = c->wait_stream(s))) return rc;
       if (4 * uint64_t(*hc) > 3 * uint64_t(k)) break;
       t *= 0.9;
     }
@@ -2731,7 +2764,7 @@ int okt_gaussiank_allreduce(okt_comm* c, const float* d_g, size_t n, size_t k, i
       return rc;
     rc = c->ck(okt::launch_aos_to_soa(c->L, c->coo.as<uint64_t>(), m, off, c->sel_idx.as<uint32_t>(),
                                       c->sel_val.as<double>()), "aos_to_soa");
-    if (rc || (rc = c->ck(cudaStreamSynchronize(s), "sync"))) return rc;
+    if (rc || (rc = c->wait_stream(s))) return rc;
     *out = okt_sparse{c->sel_idx.as<uint32_t>(), c->sel_val.as<double>(), m, n};
     return OKT_OK;
   }

@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
     trace_stamp(trace, kTrMerge, 0);
   }
   if (q < P) s_seg[q] = 0;
+  __syncthreads();  // s_abort / s_seg initialised before any thread may set them
   const uint64_t hi = lo + W;
   const uint32_t t_lo = uint32_t(lo / kMergeTile);
   const uint32_t ntiles = W ? uint32_t((hi - 1) / kMergeTile) - t_lo + 1 : 0;

@@ -11,8 +11,12 @@
 // Both expose the same two collectives the Ok-Topk phases need.
 #pragma once
 
+#include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
+#include <thread>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -40,6 +44,15 @@ class Transport {
   // recv holds P slots of `bytes`; slot r receives rank r's send buffer.
   virtual int allgather(const void* send, void* recv, size_t bytes, cudaStream_t s,
                         std::string& err) = 0;
+  // Waits for everything enqueued on `s` (collectives included).  A transport
+  // whose peers can die under it bounds the wait: TransportError, never a hang.
+  virtual int wait(cudaStream_t s, std::string& err) {
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) return OKT_OK;
+    err = std::string("device: ") + cudaGetErrorString(e);
+    cudaGetLastError();
+    return OKT_ERR_CUDA;
+  }
 };
 
 }  // namespace okt
@@ -168,39 +181,99 @@ class LocalTransport final : public Transport {
   cudaEvent_t ev_;
 };
 
+// Non-blocking NCCL communicator (ncclConfig_t::blocking = 0): every call
+// returns at once, and every host wait on the library's stream is bounded.  A
+// peer that dies (or never arrives) inside a collective leaves the NCCL kernel
+// spinning; after the deadline (OKT_NCCL_TIMEOUT_MS, default 60 s) the comm is
+// aborted (ncclCommAbort ends the kernels) and the call reports
+// TransportError — the role the reference's InprocTransport::close() plays
+// for its blocked waiters (proj/core/src/inproc.cpp:54-61).
 class NcclTransport final : public Transport {
  public:
-  explicit NcclTransport(ncclComm_t c) : c_(c) {}
+  explicit NcclTransport(ncclComm_t c) : c_(c), timeout_ms_(timeout_from_env()) {}
   ~NcclTransport() override {
     if (c_) ncclCommDestroy(c_);
   }
+  static long timeout_from_env() {
+    const char* e = std::getenv("OKT_NCCL_TIMEOUT_MS");
+    return e ? std::max(1L, std::atol(e)) : 60000L;
+  }
+  // Polls a non-blocking comm until its pending call completed (init, group end).
+  static ncclResult_t settle(ncclComm_t c, long timeout_ms) {
+    const auto t0 = std::chrono::steady_clock::now();
+    ncclResult_t st = ncclInProgress;
+    for (;;) {
+      if (ncclCommGetAsyncError(c, &st) != ncclSuccess) return ncclSystemError;
+      if (st != ncclInProgress) return st;
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(timeout_ms)) return ncclInProgress;
+      std::this_thread::yield();
+    }
+  }
   int exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s,
                std::string& err) override {
+    if (!c_) return dead(err);
     ncclResult_t r = ncclGroupStart();
     for (const Xfer& x : sends)
-      if (r == ncclSuccess && x.bytes) r = ncclSend(x.ptr, x.bytes, ncclUint8, x.peer, c_, s);
+      if (ok(r) && x.bytes) r = ncclSend(x.ptr, x.bytes, ncclUint8, x.peer, c_, s);
     for (const Xfer& x : recvs)
-      if (r == ncclSuccess && x.bytes) r = ncclRecv(x.ptr, x.bytes, ncclUint8, x.peer, c_, s);
+      if (ok(r) && x.bytes) r = ncclRecv(x.ptr, x.bytes, ncclUint8, x.peer, c_, s);
     const ncclResult_t r2 = ncclGroupEnd();
-    if (r == ncclSuccess) r = r2;
-    if (r != ncclSuccess) {
-      err = std::string("nccl send/recv: ") + ncclGetErrorString(r);
-      return OKT_ERR_NCCL;
-    }
-    return OKT_OK;
+    if (ok(r)) r = r2;
+    return finish(r, "nccl send/recv", err);
   }
   int allgather(const void* send, void* recv, size_t bytes, cudaStream_t s,
                 std::string& err) override {
-    const ncclResult_t r = ncclAllGather(send, recv, bytes, ncclUint8, c_, s);
-    if (r != ncclSuccess) {
-      err = std::string("ncclAllGather: ") + ncclGetErrorString(r);
-      return OKT_ERR_NCCL;
+    if (!c_) return dead(err);
+    return finish(ncclAllGather(send, recv, bytes, ncclUint8, c_, s), "ncclAllGather", err);
+  }
+  int wait(cudaStream_t s, std::string& err) override {
+    if (!c_) return dead(err);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t spin = 0;; ++spin) {
+      const cudaError_t e = cudaStreamQuery(s);
+      if (e == cudaSuccess) return OKT_OK;
+      if (e != cudaErrorNotReady) {
+        err = std::string("device: ") + cudaGetErrorString(e);
+        cudaGetLastError();
+        return OKT_ERR_CUDA;
+      }
+      ncclResult_t st = ncclSuccess;
+      if ((spin & 63) == 0 && ncclCommGetAsyncError(c_, &st) == ncclSuccess && st != ncclSuccess &&
+          st != ncclInProgress) {
+        abort_comm();
+        err = std::string("TransportError: NCCL: ") + ncclGetErrorString(st);
+        return OKT_ERR_TRANSPORT;
+      }
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(timeout_ms_)) {
+        abort_comm();
+        err = "TransportError: a peer did not complete the collective within " + std::to_string(timeout_ms_) +
+              " ms (communicator aborted)";
+        return OKT_ERR_TRANSPORT;
+      }
+      if (spin > 20000) std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
-    return OKT_OK;
   }
 
  private:
+  static bool ok(ncclResult_t r) { return r == ncclSuccess || r == ncclInProgress; }
+  int finish(ncclResult_t r, const char* what, std::string& err) {
+    if (r == ncclInProgress) r = settle(c_, timeout_ms_);
+    if (r == ncclSuccess) return OKT_OK;
+    abort_comm();
+    err = std::string("TransportError: ") + what + ": " +
+          (r == ncclInProgress ? "timed out" : ncclGetErrorString(r));
+    return OKT_ERR_TRANSPORT;
+  }
+  void abort_comm() {
+    if (c_) ncclCommAbort(c_);
+    c_ = nullptr;
+  }
+  static int dead(std::string& err) {
+    err = "TransportError: the NCCL communicator was aborted by an earlier failure";
+    return OKT_ERR_TRANSPORT;
+  }
   ncclComm_t c_;
+  long timeout_ms_;
 };
 
 }  // namespace okt
