@@ -4,17 +4,22 @@
 One step = one Ok-Topk error-feedback SGD iteration through the C-ABI
 (okt_sgd_step_async + okt_step_wait: acc = eps + alpha*g fused with threshold
 selection, split and reduce, global threshold, balance + allgatherv, residual
-/ model scatter; the per-step CUDA events bracket the enqueue, the wait comes
-after the end event) on a
-VGG-16-sized fp32 gradient (n = 14,728,266, density 1%, BASELINE.json
-configs[1]), tau = 64, tau' = 32, bucket 4 — refresh iterations included in
-the timed window in their natural 1-in-32 proportion.
+/ model scatter) on a BERT-large-sized fp32 gradient (n = 340,000,000,
+density 1%, tau = 64, tau' = 32, bucket 4: BASELINE.json configs[3], the
+largest configuration and the one that fits one B200 per rank).
+
+Both arms time the same iterations t = 1, 2, ... of the same inputs, the
+reference's drifting_gradient_process(t, seed = 1, rank_key = r + 1)
+(trainer.cpp:338-388) rounded to fp32, from a fresh state: t = 1 is a refresh
+iteration (thresholds and boundaries re-learned), the rest steady until
+t = 33.  `value` is the tau'-amortised ms per iteration,
+((tau' - 1) * mean(steady) + mean(refresh)) / tau', from the measured steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl okt|reference]
 
 N > 1 runs under torchrun, one process per GPU; the data path is the library's
-own NCCL communicator (NVLink), torch.distributed (gloo) is only plumbing for
-the id broadcast, barriers and the max-over-ranks reduction.
+own NVLink P2P exchange / NCCL communicator, torch.distributed (gloo) is only
+plumbing for the id broadcast, barriers and the max-over-ranks reduction.
 """
 from __future__ import annotations
 
@@ -30,7 +35,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-VGG_N = 14_728_266
+VGG_N = 14_728_266        # PAPER.md:363 (BASELINE.json configs[1])
+BERT_L_N = 340_000_000    # BASELINE.json configs[3]
+L2_BYTES = 126 << 20      # B200 L2
 
 
 def k_for(n: int, density: float) -> int:
@@ -39,23 +46,41 @@ def k_for(n: int, density: float) -> int:
     return max(1, min(n, int(math.ceil(raw))))
 
 
+def amortised(ms, refresh, tau_prime: int):
+    """tau'-amortised ms per iteration from measured steps: one refresh in
+    every tau' iterations (oktopk.cpp:258-264,277-293)."""
+    st = [v for v, r in zip(ms, refresh) if not r]
+    rf = [v for v, r in zip(ms, refresh) if r]
+    if not st or not rf:
+        return (sum(ms) / len(ms)) if ms else None, (statistics.mean(st) if st else None), \
+            (statistics.mean(rf) if rf else None)
+    s_, r_ = statistics.mean(st), statistics.mean(rf)
+    return ((tau_prime - 1) * s_ + r_) / tau_prime, s_, r_
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=128)
-    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="okt", choices=["okt", "reference"])
     # (--elements: under torchrun an abbreviation-like "--n" is taken by the launcher)
-    ap.add_argument("--n", "--elements", dest="n", type=int, default=VGG_N)
+    ap.add_argument("--n", "--elements", dest="n", type=int, default=BERT_L_N)
     ap.add_argument("--density", type=float, default=0.01)
     ap.add_argument("--tau", type=int, default=64)
     ap.add_argument("--tau-prime", type=int, default=32)
     ap.add_argument("--bucket", type=int, default=4)
-    ap.add_argument("--ring", type=int, default=8, help="distinct gradient snapshots cycled per rank")
+    ap.add_argument("--ring-max", type=int, default=24,
+                    help="gradient snapshots held in HBM at once (the timed window is cut into chunks of this size)")
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=32)
+    ap.add_argument("--cpu-iters", type=int, default=4,
+                    help="reference iterations t = 1..C timed for cpu_baseline (t = 1 refresh, the rest steady)")
+    ap.add_argument("--ref-iters", type=int, default=5,
+                    help="--impl reference: iterations t = 1..R timed (bounded sample of the window)")
+    ap.add_argument("--flush", choices=["auto", "on", "off"], default="auto",
+                    help="L2 flush between timed steps (auto: only when the step's bytes fit in 4x L2)")
     ap.add_argument("--trace", default="", help="directory: dump a CUPTI timeline (torch.profiler) of 16 steps")
-    ap.add_argument("--no-l2-flush", action="store_true", help="diagnostics only: skip the L2 flush between steps")
     ap.add_argument("--p2p-trace", default="",
                     help="directory: dump per-CTA globaltimer stamps of the last device-driven (P2P) step")
     a = ap.parse_args()
@@ -101,18 +126,34 @@ def dist_env():
     return rank, world, local
 
 
+def workload_name(n: int) -> str:
+    if n == BERT_L_N:
+        return "BERT-large-sized fp32 gradient (n = 340M, BASELINE configs[3]), Ok-Topk EF-SGD step"
+    if n == VGG_N:
+        return "VGG-16-sized fp32 gradient (BASELINE configs[1]), Ok-Topk EF-SGD step"
+    return f"n={n} fp32 gradient, Ok-Topk EF-SGD step"
+
+
+def flush_on(args) -> bool:
+    if args.flush != "auto":
+        return args.flush == "on"
+    return 12 * args.n < 4 * L2_BYTES  # the step streams 12n bytes
+
+
 def workload(args, P):
-    return {"workload": "vgg16-sized fp32 gradient, Ok-Topk EF-SGD step" if args.n == VGG_N
-            else f"n={args.n} fp32 gradient, Ok-Topk EF-SGD step",
+    fl = flush_on(args)
+    return {"workload": workload_name(args.n),
             "n": args.n, "density": args.density, "k": k_for(args.n, args.density), "P": P,
             "tau": args.tau, "tau_prime": args.tau_prime, "bucket": args.bucket,
-            "inputs": f"drifting_gradient_process(t, seed=1, rank_key=r+1), ring of {args.ring} snapshots",
-            "parallelism": f"dp{P} (one process per GPU, NCCL/NVLink)" if P > 1 else "single GPU",
-            "rank_alignment": "device barrier (okt_device_barrier, NVLink flags) before each timed step, "
-                              "outside the events" if P > 1 else None,
-            "l2": "not flushed (diagnostic run)" if args.no_l2_flush else
-            "flushed before every timed step, outside the events: 256 MiB write, then a 256 MiB read sweep "
-            "(clean L2: no write-back of the flush buffer inside the step)"}
+            "inputs": "drifting_gradient_process(t, seed=1, rank_key=r+1) rounded to fp32, the same t = 1, 2, ... "
+                      "in both arms (fresh state at t = 1)",
+            "parallelism": f"dp{P} (one process per GPU, NVLink P2P / NCCL)" if P > 1 else "single GPU",
+            "rank_alignment": "device barrier (okt_device_barrier, NVLink flags) before each timed chunk"
+                              if P > 1 else None,
+            "value": "tau'-amortised ms/iter: ((tau'-1) * mean(steady) + mean(refresh)) / tau'",
+            "l2": ("flushed before every timed step, outside the events (256 MiB write + 256 MiB read sweep)" if fl
+                   else f"not flushed: inputs larger than L2 (the step streams 12n = {12 * args.n / 1e9:.2f} GB: "
+                        "g, eps in, eps out); steps run back to back, so the write-back of dirty lines is timed")}
 
 
 # ---- clocks ----------------------------------------------------------------------
@@ -164,6 +205,21 @@ class Clocks:
 
 
 # ---- reference arm -------------------------------------------------------------------
+def reference_sample(P, n, k, iters, args):
+    """The reference's own EF-SGD step (oracle/_ref/libokref.so: oktopk_sgd_step's
+    body on InprocTransport, one pinned core per rank thread, fp64) over
+    t = 1..iters of the same drift inputs; t = 1 is the refresh iteration."""
+    from oracle import Reference
+    ref = Reference()
+    t0 = time.time()
+    ms = [float(x) for x in ref.bench_sgd(P, n, k, 0, iters, args.tau, args.tau_prime, args.bucket, 1.0, 1, True)]
+    refresh = [(t - 1) % args.tau_prime == 0 for t in range(1, iters + 1)]
+    v, st, rf = amortised(ms, refresh, args.tau_prime)
+    sample = (f"t = 1..{iters} of the same drift inputs from a fresh state (t = 1 refresh, {iters - 1} steady), "
+              f"P = {P} rank threads (InprocTransport), one pinned core each; value tau'-amortised")
+    return v, st, rf, ms, sample, time.time() - t0
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -176,23 +232,17 @@ def run_reference(args):
             "config": workload(args, P)}
     try:
         from oracle import Reference
-        ref = Reference()
+        Reference()
     except Exception as e:  # the reference .so is built in the dev container and travels
         line["unavailable"] = f"oracle/_ref/libokref.so not loadable: {e}"
         print(json.dumps(line))
         return 0
-    steps = args.steps
-    t0 = time.time()
-    ms = ref.bench_sgd(P, args.n, k, args.warmup, steps, args.tau, args.tau_prime, args.bucket, 1.0, 1, True)
-    wall = time.time() - t0
-    v = float(ms.mean())
-    line.update({"value": v, "ms_per_step": v,
-                 "cpu_baseline": {"value": v, "unit": "ms/iter", "cores": P, "kind": "reference",
-                                  "sample": f"{steps} timed iterations after {args.warmup} warm-up, "
-                                            f"P={P} rank threads (InprocTransport), one core each",
+    iters = max(2, min(args.steps, args.ref_iters))
+    v, st, rf, ms, sample, wall = reference_sample(P, args.n, k, iters, args)
+    line.update({"value": v, "ms_per_step": v, "steady_ms": st, "refresh_ms": rf, "ms_steps": ms,
+                 "cpu_baseline": {"value": v, "unit": "ms/iter", "cores": P, "kind": "reference", "sample": sample,
                                   "cpu": _cpu_model(), "nproc": os.cpu_count(), "wall_s": round(wall, 1)},
-                 "e2e": {"value": v, "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                 "ms_min": float(ms.min()), "ms_max": float(ms.max())})
+                 "e2e": {"value": v, "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     print(json.dumps(line))
     return 0
 
@@ -279,7 +329,7 @@ def run_okt(args):
     import torch.distributed as dist
 
     from paper_2201_07598_b200 import lib
-    from paper_2201_07598_b200._lib import OktResult
+    from paper_2201_07598_b200._lib import OKT_T_COUNT, TIMER_NAMES, OktResult, OktState
 
     rank, world, local = dist_env()
     P = world
@@ -291,7 +341,7 @@ def run_okt(args):
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("gloo", rank=rank, world_size=world)
-    # ---- comm: NCCL over NVLink for P > 1, a local single-rank world for P = 1
+    # ---- comm: NCCL + NVLink P2P for P > 1, a local single-rank world for P = 1
     comm = ctypes.c_void_p()
     if P > 1:
         uid = (ctypes.c_char * 128)()
@@ -313,93 +363,108 @@ def run_okt(args):
     assert L.okt_comm_reserve(comm, n) == 0
     stream = torch.cuda.Stream()
     sp = ctypes.c_void_p(stream.cuda_stream)
-    # ---- inputs: a ring of drift snapshots per rank, generated on the device
-    ring = [torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(args.ring)]
-    for i, buf in enumerate(ring):
-        assert L.okt_gen_drift(ctypes.c_void_p(buf.data_ptr()), n, i + 1, 1, rank + 1, 0, sp) == 0
-    wmodel = torch.zeros(n, dtype=torch.float32, device="cuda")
-    assert L.okt_residual_reset(comm, n, None, sp) == 0
-    flush = L2Flush(1 << 20 if args.no_l2_flush else 256 << 20)
+    fl = flush_on(args)
+    flush = L2Flush(256 << 20 if fl else 1 << 20)
     res = OktResult()
+    wmodel = torch.zeros(n, dtype=torch.float32, device="cuda")
+    nring = max(1, min(args.ring_max, args.steps))
+    ring = [torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(nring)]
+    scratch = ring[0]
+
+    def gen(buf, t):
+        assert L.okt_gen_drift(ctypes.c_void_p(buf.data_ptr()), n, t, 1, rank + 1, 0, sp) == 0
 
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
 
-    def step(t):
-        g = ring[(t - 1) % args.ring]
-        rc = L.okt_sgd_step(comm, ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(wmodel.data_ptr()), n, 1.0, t, k,
-                            ctypes.byref(res), sp)
-        if rc:
-            raise SystemExit(f"okt_sgd_step failed: {L.okt_last_error().decode()}")
-
-    def step_async(t):
-        g = ring[(t - 1) % args.ring]
+    def step_async(g, t):
         rc = L.okt_sgd_step_async(comm, ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(wmodel.data_ptr()), n,
                                   1.0, t, k, sp)
         if rc:
-            raise SystemExit(f"okt_sgd_step_async failed: {L.okt_last_error().decode()}")
+            raise SystemExit(f"okt_sgd_step_async failed at t={t}: {L.okt_last_error().decode()}")
 
     def wait():
         rc = L.okt_step_wait(comm, ctypes.byref(res))
         if rc:
             raise SystemExit(f"okt_step_wait failed: {L.okt_last_error().decode()}")
 
-    # ---- warm-up
-    t = 0
-    for _ in range(args.warmup):
-        t += 1
-        step(t)
+    def fresh_start():
+        """Residual, model and Ok-Topk state back to t = 0 (the reference arm's start)."""
+        barrier()
+        st = OktState()
+        assert L.okt_get_state(comm, ctypes.byref(st)) == 0
+        st.local_th = st.global_th = 0.0
+        st.last_local_eval = st.last_global_eval = -1
+        st.regions = -1
+        st.t = 0
+        assert L.okt_set_state(comm, ctypes.byref(st)) == 0
+        assert L.okt_residual_reset(comm, n, None, sp) == 0
+        wmodel.zero_()
+        barrier()
+
+    # ---- warm-up: t = 1..W (allocations, graphs, clocks), then a fresh start
+    for t in range(1, args.warmup + 1):
+        gen(scratch, t)
+        step_async(scratch, t)
+        wait()
     barrier()
     if args.trace:
-        trace_steps(args, rank, stream, step, t, step_async, wait, flush)
-        t += 16
-    # ---- timed device-resident run (no profiling events inside the steps)
+        trace_steps(args, rank, stream, None, args.warmup, lambda t: (gen(scratch, t), step_async(scratch, t)),
+                    wait, flush)
+    fresh_start()
+    # ---- timed run: t = 1..K, each step's own drift snapshot pre-generated in
+    # HBM (chunks of --ring-max), per-step CUDA events on the library's stream
     launches0 = ctypes.c_uint64()
     L.okt_kernel_launches(comm, ctypes.byref(launches0))
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = Clocks(local)
     clocks.start()
-    barrier()
-    U_sum, m_sum = 0, 0
-    t_first = t + 1
-    wall0 = time.perf_counter()
-    for i in range(args.steps):
-        t += 1
-        with torch.cuda.stream(stream):
-            flush.fill_(i & 0xff)  # evict L2 between timed steps (outside the events)
+    U, M = [], []
+    t = 0
+    wall_ms = 0.0
+    while t < args.steps:
+        chunk = min(nring, args.steps - t)
+        for i in range(chunk):
+            gen(ring[i], t + 1 + i)
+        barrier()
         if world > 1:
-            # align the ranks' GPUs (device barrier over NVLink, outside the
-            # events): the step is timed without the host loop's launch skew
-            L.okt_device_barrier(comm, ctypes.c_void_p(stream.cuda_stream))
-        with torch.cuda.stream(stream):
-            ev[i][0].record(stream)
-        step_async(t)
-        with torch.cuda.stream(stream):
-            ev[i][1].record(stream)
-        wait()
-        U_sum += res.u.nnz
-        m_sum += res.local_selected
+            L.okt_device_barrier(comm, sp)  # ranks aligned before the chunk (outside the events)
+        w0 = time.perf_counter()
+        for i in range(chunk):
+            t += 1
+            if fl:
+                with torch.cuda.stream(stream):
+                    flush.fill_(t & 0xff)  # evict L2 between timed steps (outside the events)
+            with torch.cuda.stream(stream):
+                ev[t - 1][0].record(stream)
+            step_async(ring[i], t)
+            with torch.cuda.stream(stream):
+                ev[t - 1][1].record(stream)
+            wait()
+            U.append(res.u.nnz)
+            M.append(res.local_selected)
+        torch.cuda.synchronize()
+        wall_ms += 1e3 * (time.perf_counter() - w0)
     barrier()
-    wall = time.perf_counter() - wall0
     launches1 = ctypes.c_uint64()
     L.okt_kernel_launches(comm, ctypes.byref(launches1))
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
     if args.p2p_trace:
         dump_p2p_trace(L, comm, rank, args.p2p_trace)
-    # ---- the same timed loop again with the library's per-phase CUDA events
-    # on its stream (phase breakdown + the K1 roofline)
-    from paper_2201_07598_b200._lib import OKT_T_COUNT, TIMER_NAMES
+    # ---- the same iterations again with the library's per-phase CUDA events on
+    # its stream (phase breakdown + the K1 roofline); fresh start, inputs per step
+    fresh_start()
     L.okt_set_profiling(comm, 1)
     L.okt_reset_phase_times(comm)
-    barrier()
-    for i in range(args.steps):
-        t += 1
-        with torch.cuda.stream(stream):
-            flush.fill_(i & 0xff)
-        step_async(t)
+    nprof = min(args.steps, 8)
+    for tp in range(1, nprof + 1):
+        gen(scratch, tp)
+        if fl:
+            with torch.cuda.stream(stream):
+                flush.fill_(tp & 0xff)
+        step_async(scratch, tp)
         wait()
     barrier()
     ms_t = (ctypes.c_double * OKT_T_COUNT)()
@@ -408,121 +473,130 @@ def run_okt(args):
     L.okt_phase_times(comm, ms_t, calls)
     L.okt_phase_bytes(comm, byts)
     L.okt_set_profiling(comm, 0)
-    phases = {nm: round(ms_t[i] / max(1, args.steps), 4) for i, nm in enumerate(TIMER_NAMES)}
-    k1_ms, k1_bytes, k1_calls = ms_t[TIMER_NAMES.index("k1")], byts[TIMER_NAMES.index("k1")], calls[TIMER_NAMES.index("k1")]
+    phases = {nm: round(ms_t[i] / max(1, nprof), 4) for i, nm in enumerate(TIMER_NAMES)}
+    ik1 = TIMER_NAMES.index("k1")
+    k1_ms, k1_bytes, k1_calls = ms_t[ik1], byts[ik1], calls[ik1]
     # ---- end-to-end through the synchronous host-buffer C-ABI call (the
-    # reference's calling convention: H2D gradient, step, D2H u, all timed)
-    hbuf = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(min(args.ring, 4))]
-    for i, hb in enumerate(hbuf):
-        hb.copy_(ring[i].cpu())
-    cap = n
+    # reference's calling convention: H2D gradient, step, D2H u, all timed),
+    # continuing the timed run's drift sequence at t = K+1, K+2, ...
+    fresh_start()
+    for tp in range(1, args.steps + 1):  # replay the timed window untimed, so the e2e leg continues it
+        gen(scratch, tp)
+        step_async(scratch, tp)
+        wait()
+    hbuf = torch.empty(n, dtype=torch.float32).pin_memory()
+    cap = min(n, 8 * k + 4096)  # u's host buffers (U ~ k on these inputs; a larger U fails the call loudly)
     h_uidx = torch.empty(cap, dtype=torch.int32).pin_memory()
     h_uval = torch.empty(cap, dtype=torch.float64).pin_memory()
-    e2e_steps = max(4, min(args.steps, 32))
+    e2e_steps = max(2, args.e2e_steps)
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e2e_steps)]
-    # untimed warm-up of the host-buffer path (its device staging is allocated on first use)
-    for i in range(2):
-        t += 1
-        if L.okt_sgd_step_host(comm, ctypes.c_void_p(hbuf[i % len(hbuf)].data_ptr()), ctypes.c_void_p(wmodel.data_ptr()),
-                               n, 1.0, t, k, ctypes.c_void_p(h_uidx.data_ptr()), ctypes.c_void_p(h_uval.data_ptr()),
-                               cap, ctypes.byref(res), sp):
-            raise SystemExit(f"okt_sgd_step_host failed: {L.okt_last_error().decode()}")
-    barrier()
-    d2h = 0
+    te = args.steps
+    d2h, e2e_U = 0, []
     for i in range(e2e_steps):
-        t += 1
-        with torch.cuda.stream(stream):
-            flush.fill_(i & 0xff)
+        te += 1
+        gen(scratch, te)
+        hbuf.copy_(scratch, non_blocking=False)  # this step's gradient in pinned host memory (untimed)
+        if fl:
+            with torch.cuda.stream(stream):
+                flush.fill_(i & 0xff)
+        barrier()
         if world > 1:
-            barrier()  # hosts and GPUs aligned before each timed call (outside the events)
-            L.okt_device_barrier(comm, ctypes.c_void_p(stream.cuda_stream))
+            L.okt_device_barrier(comm, sp)
         with torch.cuda.stream(stream):
             e2e_ev[i][0].record(stream)
-        rc = L.okt_sgd_step_host(comm, ctypes.c_void_p(hbuf[i % len(hbuf)].data_ptr()),
-                                 ctypes.c_void_p(wmodel.data_ptr()), n, 1.0, t, k,
-                                 ctypes.c_void_p(h_uidx.data_ptr()), ctypes.c_void_p(h_uval.data_ptr()), cap,
+        rc = L.okt_sgd_step_host(comm, ctypes.c_void_p(hbuf.data_ptr()), ctypes.c_void_p(wmodel.data_ptr()), n, 1.0,
+                                 te, k, ctypes.c_void_p(h_uidx.data_ptr()), ctypes.c_void_p(h_uval.data_ptr()), cap,
                                  ctypes.byref(res), sp)
         if rc:
             raise SystemExit(f"okt_sgd_step_host failed: {L.okt_last_error().decode()}")
         with torch.cuda.stream(stream):
             e2e_ev[i][1].record(stream)
         d2h += 12 * res.u.nnz
+        e2e_U.append(res.u.nnz)
     barrier()
     clk = clocks.stop()
     e2e_list = [a.elapsed_time(b) for a, b in e2e_ev]
-    e2e_ms = sum(e2e_list) / e2e_steps
-    if os.environ.get("OKT_BENCH_DEBUG"):
-        print(f"[rank {rank}] e2e t0={t - e2e_steps + 1} ms={[round(x, 3) for x in e2e_list]}", file=sys.stderr)
+    e2e_refresh = [(tt - 1) % args.tau_prime == 0 for tt in range(args.steps + 1, te + 1)]
     # ---- reference point: a dense NCCL allreduce of the same gradient
     dense_ms = None
     if world > 1:
         pg = dist.new_group(backend="nccl")
-        dense = torch.empty(n, dtype=torch.float32, device="cuda")
-        dense.copy_(ring[0])
-        dev_ = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(16)]
-        for i in range(4 + len(dev_)):
-            flush.fill_(i & 0xff)
+        dense = scratch
+        dev_ = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(8)]
+        for i in range(3 + len(dev_)):
+            if fl:
+                flush.fill_(i & 0xff)
             barrier()
-            if i >= 4:
-                dev_[i - 4][0].record()
+            if i >= 3:
+                dev_[i - 3][0].record()
             dist.all_reduce(dense, group=pg)
-            if i >= 4:
-                dev_[i - 4][1].record()
+            if i >= 3:
+                dev_[i - 3][1].record()
         torch.cuda.synchronize()
         dense_ms = sum(a.elapsed_time(b) for a, b in dev_) / len(dev_)
-    # ---- max over ranks
-    mine = torch.tensor([total_ms, e2e_ms, wall, dense_ms or 0.0], dtype=torch.float64)
+    # ---- max over ranks (per step)
     per_step = torch.tensor(step_ms, dtype=torch.float64)
+    e2e_t = torch.tensor(e2e_list, dtype=torch.float64)
+    mine = torch.tensor([wall_ms, dense_ms or 0.0, k1_ms], dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(mine, op=dist.ReduceOp.MAX)
         dist.all_reduce(per_step, op=dist.ReduceOp.MAX)
-    total_ms, e2e_ms, wall, dense_ms = mine.tolist()
-    # steady vs refresh iterations ((t - 1) % tau' == 0 re-evaluates the thresholds)
-    refresh = [(t_first + i - 1) % args.tau_prime == 0 for i in range(args.steps)]
-    st_ms = [v for v, r in zip(per_step.tolist(), refresh) if not r]
-    rf_ms = [v for v, r in zip(per_step.tolist(), refresh) if r]
-    ms_per_step = total_ms / args.steps
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(mine, op=dist.ReduceOp.MAX)
+    wall_ms, dense_ms, _ = mine.tolist()
+    refresh = [(tt - 1) % args.tau_prime == 0 for tt in range(1, args.steps + 1)]
+    value, steady_ms, refresh_ms = amortised(per_step.tolist(), refresh, args.tau_prime)
+    # e2e: steady host-buffer steps (t = K+1..K+E), plus the device-measured
+    # refresh surcharge amortised over tau' (the same refresh step as `value`)
+    e2e_steady = statistics.mean([v for v, r in zip(e2e_t.tolist(), e2e_refresh) if not r] or e2e_t.tolist())
+    e2e_val = e2e_steady + ((refresh_ms - steady_ms) / args.tau_prime if refresh_ms and steady_ms else 0.0)
     achieved = k1_bytes / (k1_ms * 1e-3) / 1e9 if k1_ms > 0 else None
-    peak = None
     try:
         peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
-        peak_src = "measured"
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        peak, peak_src = 6650.0, "fallback"
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     line = None
     if rank == 0:
-        traffic = None
+        traffic, traffic_src = None, None
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))
-            traffic = prof.get("bytes_per_launch")
+            ent = prof.get("by_n", {}).get(str(n))
+            if ent:
+                traffic, traffic_src = ent.get("bytes_per_launch"), ent.get("source")
         except Exception:
             pass
-        line = {"metric": "Ok-Topk sparse allreduce ms/iter", "value": ms_per_step, "unit": "ms/iter",
-                "n_gpus": P, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        window_mean = sum(per_step.tolist()) / args.steps
+        line = {"metric": "Ok-Topk sparse allreduce ms/iter", "value": value, "unit": "ms/iter",
+                "n_gpus": P, "steps": args.steps, "warmup": args.warmup, "ms_per_step": value,
                 "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": workload(args, P),
-                "e2e": {"value": e2e_ms, "unit": "ms/iter", "h2d_bytes_per_step": 4 * n,
+                "steady_ms": steady_ms, "refresh_ms": refresh_ms, "refresh_steps_timed": sum(refresh),
+                "window_mean_ms": window_mean,
+                "ms_steps": [round(x, 4) for x in per_step.tolist()],
+                "e2e": {"value": e2e_val, "unit": "ms/iter", "h2d_bytes_per_step": 4 * n,
                         "d2h_bytes_per_step": int(d2h / e2e_steps), "steps": e2e_steps,
-                        "ms_min": min(e2e_list), "ms_median": statistics.median(e2e_list), "ms_max": max(e2e_list),
-                        "path": "okt_sgd_step_host: gradient H2D from pinned host memory, step, u D2H", "cpu_affinity": affinity},
+                        "t": [args.steps + 1, te], "mean_U": statistics.mean(e2e_U), "steady_ms": e2e_steady,
+                        "formula": "mean(host-buffer steady steps) + (refresh_ms - steady_ms) / tau'",
+                        "ms_steps": [round(x, 3) for x in e2e_t.tolist()],
+                        "path": "okt_sgd_step_host: gradient H2D from pinned host memory, step, u D2H "
+                                "(continues the timed run's drift sequence)", "cpu_affinity": affinity},
                 "gpu_launches": int(launches1.value - launches0.value),
                 "roofline": {"bound": "hbm", "kernel": "k1_kernel (fused residual accumulate + threshold select "
-                                                         "+ chunk-local COO compaction; phase A of K1)",
+                                                         "+ per-tile COO compaction; P = 1: + fused K7 apply)",
                              "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                             "peak_source": peak_src,
+                             "traffic_source": traffic_src, "peak_source": peak_src,
                              "bytes_per_launch": k1_bytes / max(1, k1_calls),
                              "us_per_launch": 1e3 * k1_ms / max(1, k1_calls), "launches": int(k1_calls),
-                             "bytes_formula": "12n + 8e per EF step (read g, eps; write eps; 8 B per staged "
-                                              "entry e); refresh steps add a 4n + 8m select pass"},
+                             "timed_over": f"t = 1..{nprof} (profiled pass, CUDA events around every K1 launch)",
+                             "bytes_formula": "12n + 8e per EF step (read g, eps; write eps; 8 B per staged entry "
+                                              "e); P = 1 adds 12 B per entry of u (w read + write, old word); "
+                                              "refresh steps add a 4n + 8m select pass"},
                 "phases_ms_per_step": phases,
-                "steady_ms": statistics.mean(st_ms) if st_ms else None,
-                "refresh_ms": statistics.mean(rf_ms) if rf_ms else None,
-                "refresh_steps_timed": len(rf_ms),
                 # dense-equivalent bandwidth, comparable to an allreduce's busBw
-                "dense_equivalent_gbs": 2 * 4 * n * (P - 1) / P / (ms_per_step * 1e-3) / 1e9 if P > 1 else None,
-                "avg_U": U_sum / args.steps, "avg_local_selected": m_sum / args.steps,
-                "wall_ms_per_step": 1e3 * wall / args.steps,
+                "dense_equivalent_gbs": 2 * 4 * n * (P - 1) / P / (value * 1e-3) / 1e9 if P > 1 else None,
+                "avg_U": statistics.mean(U), "avg_local_selected": statistics.mean(M),
+                "wall_ms_per_step": wall_ms / args.steps,
                 "dense_nccl_allreduce": None if world == 1 else {
                     "ms": dense_ms, "bytes": 4 * n,
                     "note": "reference point: torch.distributed NCCL all_reduce of the dense fp32 gradient, "
@@ -531,14 +605,10 @@ def run_okt(args):
     # ---- CPU baseline (rank 0, N = 1 only): the reference itself, bounded sample
     if rank == 0 and P == 1 and not args.no_cpu_baseline:
         try:
-            from oracle import Reference
-            ref = Reference()
-            t0 = time.time()
-            ms = ref.bench_sgd(1, n, k, 1, args.cpu_iters, args.tau, args.tau_prime, args.bucket, 1.0, 1, True)
-            line["cpu_baseline"] = {"value": float(ms.mean()), "unit": "ms/iter", "cores": 1, "kind": "reference",
-                                    "sample": f"{args.cpu_iters} iterations t=2..{args.cpu_iters + 1} "
-                                              f"(one tau' refresh) of the reference's EF-SGD step, same n/k/tau",
-                                    "cpu": _cpu_model(), "wall_s": round(time.time() - t0, 1)}
+            v, st, rf, ms, sample, wall = reference_sample(1, n, k, max(2, args.cpu_iters), args)
+            line["cpu_baseline"] = {"value": v, "unit": "ms/iter", "cores": 1, "kind": "reference",
+                                    "sample": sample, "steady_ms": st, "refresh_ms": rf,
+                                    "cpu": _cpu_model(), "wall_s": round(wall, 1)}
         except Exception as e:
             line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
     if rank == 0:

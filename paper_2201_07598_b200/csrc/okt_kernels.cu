@@ -69,30 +69,36 @@ size_t stage_entries(uint64_t count, int tile, int max_chunks) {
 // =============================================================================
 // MODE 0: AoS u64 -> AoS u64; 1: AoS u64 -> SoA (u32, f32 widened to f64);
 //      2: SoA -> SoA; 3: u32 -> u32.
-// APPLY (P = 1, where every entry of u is also in the local selection): fuse
-// K7 into the copy — w[i] -= v, acc[i] = 0 — so the single-rank step needs no
-// separate apply pass; `indexes` is then u's index array itself.
 constexpr int kCompactBatch = 2;
 
 // A CTA copies a group of consecutive chunks (up to kThreads; one chunk per
 // CTA for the static-chunk producers, a few tiles for K1's per-tile staging):
-// the group's counts are block-scanned first, so the group's first entries
-// can be loaded while the block reduces the global prefix.
+// the group's counts are block-scanned, the group total is published in
+// agg[blockIdx.x] (tagged with the launch), and the group's exclusive prefix is
+// the sum of the lower CTAs' published totals (a decoupled look-back over
+// aggregates only: every CTA publishes before it waits, and the grid is one
+// wave, so nobody waits on a CTA that waits).  The group's first entries are
+// loaded while the look-back completes.  Round 1 summed every lower chunk
+// count per CTA instead (O(G^2 / per) L2 reads: 0.28 ms at 340M).
+__device__ __forceinline__ void agg_publish(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t agg_load(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
-template <int MODE, bool APPLY>
+template <int MODE>
 __global__ void __launch_bounds__(kThreads)
     compact_kernel(const uint64_t* __restrict__ s64, const uint32_t* __restrict__ sidx,
                    const double* __restrict__ sval, const uint32_t* __restrict__ counts,
                    const uint32_t* __restrict__ counts2, uint32_t g2, uint32_t G, uint64_t cap_host,
                    const uint64_t* d_cap, uint64_t* __restrict__ o64, uint32_t* oidx, double* oval,
-                   uint64_t* d_total, uint64_t* d_total2, ApplyArgs ap) {
+                   uint64_t* d_total, uint64_t* d_total2, uint64_t* agg, ApplyArgs ap) {
   __shared__ uint64_t red[kWarps];
   __shared__ uint32_t s_pre[kThreads + 1];
   __shared__ uint32_t s_wt[kWarps];
-  if (APPLY && ap.ind) {
-    ap.acc = ap.ind->eps_out;
-    ap.w = ap.ind->w;
-  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     trace_stamp(ap.trace, kTrCompact, 0);
@@ -102,12 +108,8 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t c1 = uint32_t(split_at(blockIdx.x + 1, G, gridDim.x));
   const int nc = int(c1 - c0);
   const uint64_t cap = d_cap ? *d_cap : cap_host;
-  // group prefix (block scan) and this thread's share of the global prefix
+  // group prefix (block scan)
   const uint32_t v = tid < nc ? counts[c0 + tid] : 0u;
-  // CTA 0 (c0 = 0, no prefix) sums all G counts instead: the totals
-  const bool first = blockIdx.x == 0;
-  uint64_t pre = strided_sum(counts, first ? G : c0);
-  uint64_t s2 = (first && counts2) ? strided_sum(counts2, g2) : 0;
   uint32_t incl = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -122,8 +124,10 @@ __global__ void __launch_bounds__(kThreads)
   if (tid < nc) s_pre[tid + 1] = wpre + incl;
   if (tid == 0) s_pre[0] = 0;
   __syncthreads();
-  if (tid == 0) trace_stamp(ap.trace, kTrCompact, 1);
   const uint64_t cnt = s_pre[nc];
+  const uint64_t tag = uint64_t(ap.tag) << 32;
+  if (tid == 0) agg_publish(&agg[blockIdx.x], tag | cnt);
+  if (tid == 0) trace_stamp(ap.trace, kTrCompact, 1);
   auto src_of = [&](uint64_t j) {  // staging position of the group's j-th entry
     int lo = 0, hi = nc - 1;          // last k with s_pre[k] <= j
     while (lo < hi) {
@@ -133,21 +137,18 @@ __global__ void __launch_bounds__(kThreads)
     }
     return uint64_t(c0 + lo) * cap + (j - s_pre[lo]);
   };
-  // The first kCompactBatch entries of each thread are loaded (and, for the
-  // fused apply, their model words gathered) before the global prefix is
-  // known: only the output positions depend on it.
+  // The first kCompactBatch entries of each thread are loaded before the
+  // global prefix is known: only the output positions depend on it.
   constexpr int B = kCompactBatch;
   uint64_t e64[B];
   uint32_t ei[B];
   double ev[B];
-  float wv[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     const uint64_t j = tid + uint64_t(b) * kThreads;
     e64[b] = 0;
     ei[b] = 0;
     ev[b] = 0.0;
-    wv[b] = 0.f;
     if (j < cnt) {
       const uint64_t sj = src_of(j);
       if (MODE == 0 || MODE == 1) e64[b] = s64[sj];
@@ -157,45 +158,46 @@ __global__ void __launch_bounds__(kThreads)
         ei[b] = coo_idx(e64[b]);
         ev[b] = double(coo_val(e64[b]));
       }
-      if (APPLY) wv[b] = ap.w[ei[b]];
     }
+  }
+  // look-back over the lower CTAs' group totals of this launch
+  uint64_t pre = 0;
+  for (uint32_t b = tid; b < blockIdx.x; b += kThreads) {
+    uint64_t a;
+    do {
+      a = agg_load(&agg[b]);
+    } while ((a & 0xffffffff00000000ull) != tag);
+    pre += uint32_t(a);
   }
   pre = block_sum(pre, red);
   if (tid == 0) trace_stamp(ap.trace, kTrCompact, 3);
-  if (first) {
+  const bool last = blockIdx.x == gridDim.x - 1;
+  if (last) {  // the totals (and the step's scalars, straight into mapped host memory: no D2H node)
+    uint64_t s2 = counts2 ? strided_sum(counts2, g2) : 0;
     if (counts2) s2 = block_sum(s2, red);
     if (tid == 0) {
-      *d_total = pre;
+      *d_total = pre + cnt;
       if (counts2) *d_total2 = s2;
-      if (ap.hout) {  // the step's scalars straight into mapped host memory (no D2H node)
+      if (ap.hout) {
         ap.hout->m = counts2 ? s2 : 0;
-        ap.hout->S = pre;
+        ap.hout->S = pre + cnt;
         ap.hout->flags = *reinterpret_cast<volatile uint32_t*>(ap.d_flags);  // (K1 has finished)
         ap.hout->seq = ap.seq;
       }
     }
-    pre = 0;
   }
-  const bool skip = APPLY && (*ap.d_flags & 1u);  // non-finite step: touch nothing
-  bool bad = false;
-  auto emit = [&](uint64_t j, uint64_t e, uint32_t i, double v, float w_old) {
+  auto emit = [&](uint64_t j, uint64_t e, uint32_t i, double v) {
     if (MODE == 0) o64[pre + j] = e;
     else if (MODE == 3) oidx[pre + j] = i;
     else {
       oidx[pre + j] = i;
       oval[pre + j] = v;
     }
-    if (APPLY && !skip) {
-      const float nw = float(double(w_old) - v);
-      ap.w[i] = nw;
-      ap.acc[i] = 0.f;
-      bad |= (__float_as_uint(nw) & 0x7f800000u) == 0x7f800000u;
-    }
   };
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     const uint64_t j = tid + uint64_t(b) * kThreads;
-    if (j < cnt) emit(j, e64[b], ei[b], ev[b], wv[b]);
+    if (j < cnt) emit(j, e64[b], ei[b], ev[b]);
   }
   for (uint64_t j = tid + uint64_t(B) * kThreads; j < cnt; j += kThreads) {
     const uint64_t sj = src_of(j);
@@ -209,19 +211,12 @@ __global__ void __launch_bounds__(kThreads)
     }
     if (MODE == 2 || MODE == 3) i = sidx[sj];
     if (MODE == 2) v = sval[sj];
-    emit(j, e, i, v, APPLY ? ap.w[i] : 0.f);
-  }
-  if (APPLY && __syncthreads_or(bad) && tid == 0) {
-    atomicOr(ap.d_flags, 4u);
-    if (ap.hout) *reinterpret_cast<volatile uint32_t*>(&ap.hout->bad_iter) = 1u;  // (error path only)
+    emit(j, e, i, v);
   }
   if (lane == 0) trace_stamp(ap.trace, kTrCompact, 2);
 }
 
-const void* compact_graph_kernel(bool apply) {
-  return apply ? reinterpret_cast<const void*>(compact_kernel<1, true>)
-               : reinterpret_cast<const void*>(compact_kernel<1, false>);
-}
+const void* compact_graph_kernel() { return reinterpret_cast<const void*>(compact_kernel<1>); }
 
 // G chunks of `cap` entries (cap_host, or *d_cap when set); counts2: g2
 // partial sums (0 = none).
@@ -231,26 +226,18 @@ static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_
                                   double* oval, uint64_t* d_total, uint64_t* d_total2,
                                   const ApplyArgs* ap = nullptr) {
   // one chunk per CTA while the grid fits one wave, then groups of up to
-  // kThreads chunks
-  static std::atomic<int> cap_a{0}, cap_p{0};  // (resident CTAs; benign concurrent first use)
-  const bool apply = ap && ap->k7;
-  std::atomic<int>& cap = apply ? cap_a : cap_p;
-  if (!cap)
-    cap = apply ? resident_ctas(compact_kernel<MODE, true>, kThreads, L.sms)
-                : resident_ctas(compact_kernel<MODE, false>, kThreads, L.sms);
+  // kThreads chunks; the grid never exceeds one wave (the look-back waits on
+  // lower CTAs)
+  static std::atomic<int> cap{0};  // (resident CTAs; benign concurrent first use)
+  if (!cap) cap = resident_ctas(compact_kernel<MODE>, kThreads, L.sms);
   const uint32_t slots = uint32_t(std::min(cap.load(), S.max_chunks));
   const uint32_t per = std::min<uint32_t>(kThreads, std::max<uint32_t>(1, (G + slots - 1) / slots));
   const uint32_t GB = std::max<uint32_t>(1, (G + per - 1) / per);
   const uint32_t* c2 = g2 ? S.counts2 : nullptr;
-  if (!apply && ap && ap->hout)
-    compact_kernel<MODE, false><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap,
-                                                          o64, oidx, oval, d_total, d_total2, *ap);
-  else if (apply)
-    compact_kernel<MODE, true><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap,
-                                                         o64, oidx, oval, d_total, d_total2, *ap);
-  else
-    compact_kernel<MODE, false><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap,
-                                                          o64, oidx, oval, d_total, d_total2, ApplyArgs{});
+  ApplyArgs a = ap ? *ap : ApplyArgs{};
+  if (!a.tag) a.tag = ++*S.tag_ctr ? *S.tag_ctr : ++*S.tag_ctr;  // (0 never tags a launch)
+  compact_kernel<MODE><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap, o64,
+                                                 oidx, oval, d_total, d_total2, S.agg, a);
   ++L.launches;
   return cudaGetLastError();
 }
@@ -258,12 +245,21 @@ static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_
 // =============================================================================
 // K1: fused accumulate / select / compact (phase A)
 // =============================================================================
-template <bool ACCUM, bool SELECT, bool HIST, bool VEC, bool DUAL>
+// APPLY (single rank, DUAL): u = the emitted set, and every entry of u is in
+// the local selection (indexes = u), so K7 runs here, in the tile that emits
+// the entry: the residual word is stored as 0 instead of acc (no extra bytes
+// on the ACCUM pass; a 4-byte store at the entry on the select-only refresh
+// pass), and w[i] = float(double(w[i]) - double(acc_i)) (trainer.cpp:437-442,
+// 476-480; P = 1).  The pre-update model word is kept per staged entry
+// (ka.wold) so the host can roll the model back when the step fails on a
+// non-finite accumulator (the reference throws before touching the model).
+template <bool ACCUM, bool SELECT, bool HIST, bool VEC, bool DUAL, bool APPLY>
 __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
     k1_kernel(const float* __restrict__ g, const float* eps_in, float* eps_out, float alpha, uint64_t n,
               uint32_t tiles, uint32_t* tile_ctr, const double* __restrict__ d_th,
               const double* __restrict__ d_th2, uint64_t* __restrict__ stg, uint32_t* counts,
-              uint32_t* counts2, uint32_t* d_flags, uint32_t* d_hist, const StepPtrs* ind, K1P2P p2p) {
+              uint32_t* counts2, uint32_t* d_flags, uint32_t* d_hist, const StepPtrs* ind, K1P2P p2p, K1Apply ka) {
+  static_assert(!APPLY || (DUAL && SELECT), "the fused apply is the single-rank dual-threshold select");
   constexpr int C = 4, TILE = kJ * C * kThreads;
   // Tiles are handed out dynamically (a ticket counter; the prefetched next
   // ticket hides its round trip), so every CTA streams until the input is
@@ -323,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
     for (int i = tid; i < 2048; i += kThreads) s_hist[i] = 0;
     __syncthreads();
   }
-  bool bad = false;
+  bool bad = false, bad_iter = false;
   uint32_t mloc = 0;
   if (tid == 0) s_tile[0] = atomicAdd(&tile_ctr[0], 1u);
   __syncthreads();
@@ -352,7 +348,16 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
           a[j][2] = fmaf(alpha, gv[j].z, ev[j].z);
           a[j][3] = fmaf(alpha, gv[j].w, ev[j].w);
           const uint64_t e0 = base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C;
-          *reinterpret_cast<float4*>(eps_out + e0) = make_float4(a[j][0], a[j][1], a[j][2], a[j][3]);
+          float4 st = make_float4(a[j][0], a[j][1], a[j][2], a[j][3]);
+          if (APPLY) {  // the residual of an entry of u is 0 (trainer.cpp:478-479)
+            if (fabsf(st.x) >= tf) st.x = 0.f;
+            if (fabsf(st.y) >= tf) st.y = 0.f;
+            if (fabsf(st.z) >= tf) st.z = 0.f;
+            if (fabsf(st.w) >= tf) st.w = 0.f;
+          }
+          // (single rank: nothing reads the residual again this step -> streaming store)
+          if (APPLY) __stcs(reinterpret_cast<float4*>(eps_out + e0), st);
+          else *reinterpret_cast<float4*>(eps_out + e0) = st;
         } else {
           a[j][0] = gv[j].x;
           a[j][1] = gv[j].y;
@@ -377,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
             x = g[e];
             if (ACCUM) {
               x = fmaf(alpha, x, eps_in[e]);
-              eps_out[e] = x;
+              eps_out[e] = (APPLY && fabsf(x) >= tf) ? 0.f : x;
             }
             bad |= nonfinite(x);
           }
@@ -440,6 +445,14 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
             const uint32_t pos = grp[j] + rank_in_group<C>(bal, j, c);
             const uint64_t e = base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C + c;
             out[pos] = coo_pack(uint32_t(e), a[j][c]);
+            if (APPLY) {
+              const float wo = ka.w[e];
+              const float nw = float(double(wo) - double(a[j][c]));
+              ka.w[e] = nw;
+              ka.wold[base + pos] = wo;
+              if (!ACCUM) ka.zero[e] = 0.f;
+              bad_iter |= nonfinite(nw);
+            }
           }
         }
       }
@@ -454,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
   if (__syncthreads_or(bad) && tid == 0) {
     atomicOr(d_flags, 1u);
   }
+  if (APPLY && __syncthreads_or(bad_iter) && tid == 0) atomicOr(d_flags, 4u);
   if (HIST) {
     for (int i = tid; i < 2048; i += kThreads)
       if (s_hist[i]) atomicAdd(&d_hist[i], s_hist[i]);
@@ -479,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
   if (trace && (tid & 31) == 0) trace_stamp(trace, kTrK1, 2);
 }
 
-template <bool ACCUM, bool SELECT, bool HIST, bool DUAL>
+template <bool ACCUM, bool SELECT, bool HIST, bool DUAL, bool APPLY = false>
 static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float* g, const float* eps_in,
                                float* eps_out, float alpha, uint64_t n, const double* d_th,
                                const double* d_th2, const OutCoo& out, uint64_t* d_m, uint64_t* d_m2,
@@ -487,7 +501,13 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
                                const StepPtrs* ind) {
   constexpr int TILE = kJ * 4 * kThreads;
   const uint64_t tiles = (n + TILE - 1) / TILE;
-  auto kern = vec ? k1_kernel<ACCUM, SELECT, HIST, true, DUAL> : k1_kernel<ACCUM, SELECT, HIST, false, DUAL>;
+  auto kern = vec ? k1_kernel<ACCUM, SELECT, HIST, true, DUAL, APPLY> : k1_kernel<ACCUM, SELECT, HIST, false, DUAL, APPLY>;
+  K1Apply ka{};
+  if (APPLY) {
+    ka.w = ap->w;
+    ka.wold = S.wold;
+    ka.zero = ACCUM ? nullptr : const_cast<float*>(g);  // the select-only pass reads acc in place
+  }
   static std::atomic<int> cap_v{0}, cap_s{0};
   std::atomic<int>& cap = vec ? cap_v : cap_s;
   if (!cap) cap = resident_ctas(kern, kThreads, L.sms);
@@ -500,7 +520,7 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
   const unsigned ev_flags = cap_st == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, ev_flags);
   kern<<<G, kThreads, 0, L.s>>>(g, eps_in, eps_out, alpha, n, uint32_t(tiles), S.tile_ctr, d_th, d_th2, S.s64,
-                                S.counts, S.counts2, d_flags, d_hist, ind, p2p ? *p2p : K1P2P{});
+                                S.counts, S.counts2, d_flags, d_hist, ind, p2p ? *p2p : K1P2P{}, ka);
   if (L.k1_event) cudaEventRecordWithFlags(L.k1_event(L.k1_ctx), L.s, ev_flags);
   ++L.launches;
   cudaError_t e = cudaGetLastError();
@@ -521,6 +541,13 @@ cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, co
   bool vec = al(g);
   if (mode != K1Mode::kSelect) vec = vec && al(eps_in) && al(eps_out);
   const bool dual = d_th2 != nullptr;
+  const bool apply = dual && ap && ap->k7;  // K7 fused into the single-rank select (K1Apply)
+  if (apply && mode == K1Mode::kSelect)
+    return k1_dispatch<false, true, false, true, true>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out, d_m,
+                                                       d_m2, d_flags, d_hist, ap, pub, ind);
+  if (apply && mode == K1Mode::kAccumSelect)
+    return k1_dispatch<true, true, false, true, true>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out, d_m,
+                                                      d_m2, d_flags, d_hist, ap, pub, ind);
   switch (mode) {
     case K1Mode::kSelect:
       return dual ? k1_dispatch<false, true, false, true>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out,
@@ -537,6 +564,27 @@ cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, co
                                                    d_m2, d_flags, d_hist, ap, pub, ind);
   }
   return cudaErrorInvalidValue;
+}
+
+// A failed single-rank step (non-finite accumulator somewhere in the grid)
+// after K1 already applied K7 in the tiles it emitted: put the old model words
+// back (one CTA per K1 tile; error path only).
+__global__ void __launch_bounds__(kThreads)
+    k1_rollback_kernel(const uint64_t* __restrict__ stg, const float* __restrict__ wold,
+                       const uint32_t* __restrict__ counts, uint32_t tiles, float* w) {
+  for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const uint32_t c = counts[t];
+    const uint64_t base = uint64_t(t) * kK1Tile;
+    for (uint32_t j = threadIdx.x; j < c; j += kThreads) w[coo_idx(stg[base + j])] = wold[base + j];
+  }
+}
+
+cudaError_t launch_k1_rollback(Launch& L, const Stage& S, uint64_t n, float* w) {
+  const uint64_t tiles = (n + kK1Tile - 1) / kK1Tile;
+  const uint32_t grid = uint32_t(std::min<uint64_t>(tiles, 65535));
+  k1_rollback_kernel<<<grid, kThreads, 0, L.s>>>(S.s64, S.wold, S.counts, uint32_t(tiles), w);
+  ++L.launches;
+  return cudaGetLastError();
 }
 
 // =============================================================================
