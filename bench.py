@@ -582,16 +582,16 @@ def run_okt(args):
                                 "(continues the timed run's drift sequence)", "cpu_affinity": affinity},
                 "gpu_launches": int(launches1.value - launches0.value),
                 "roofline": {"bound": "hbm", "kernel": "k1_kernel (fused residual accumulate + threshold select "
-                                                         "+ per-tile COO compaction; P = 1: + fused K7 apply)",
+                                                         "+ per-tile COO compaction; P = 1: + residual zeroing)",
                              "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                              "traffic_source": traffic_src, "peak_source": peak_src,
                              "bytes_per_launch": k1_bytes / max(1, k1_calls),
                              "us_per_launch": 1e3 * k1_ms / max(1, k1_calls), "launches": int(k1_calls),
                              "timed_over": f"t = 1..{nprof} (profiled pass, CUDA events around every K1 launch)",
-                             "bytes_formula": "12n + 8e per EF step (read g, eps; write eps; 8 B per staged entry "
-                                              "e); P = 1 adds 12 B per entry of u (w read + write, old word); "
-                                              "refresh steps add a 4n + 8m select pass"},
+                             "bytes_formula": "12n + 8e per EF step (read g, eps; write eps - P = 1: stored as 0 "
+                                              "at u's entries -; 8 B per staged entry e); refresh steps add a "
+                                              "4n + 8m select pass"},
                 "phases_ms_per_step": phases,
                 # dense-equivalent bandwidth, comparable to an allreduce's busBw
                 "dense_equivalent_gbs": 2 * 4 * n * (P - 1) / P / (value * 1e-3) / 1e9 if P > 1 else None,

@@ -206,9 +206,8 @@ struct okt_comm {
   Buf galign;              // 16-byte aligned copy of a misaligned gradient (P2P step)
   Buf st64, stidx, stval;  // phase-A compaction staging
   Buf counts, counts2, chunkcap, tilectr;
-  Buf wold, agg;           // fused single-rank apply: pre-update model words; phase-B look-back totals
+  Buf agg;                 // phase-B look-back: per-CTA group totals
   uint32_t compact_tag = 0;  // phase-B launch tags (Stage::tag_ctr)
-  float* applied_w = nullptr;  // model a fused-apply K1 changed this step (rolled back if the step fails)
   Buf hist, scal;
   okt::Stage S;
   // device-driven multi-GPU exchange (okt_p2p.cuh)
@@ -352,7 +351,6 @@ struct okt_comm {
     if (e == cudaSuccess) e = st64.ensure(8 * k1_stage);
     if (e == cudaSuccess) e = stidx.ensure(4 * coo_stage);
     if (e == cudaSuccess) e = stval.ensure(8 * coo_stage);
-    if (e == cudaSuccess && P == 1) e = wold.ensure(4 * k1_stage);
     agg.zero_init = true;
     if (e == cudaSuccess) e = agg.ensure(8 * (size_t(S.max_chunks) + k1_tiles / 256 + 2));
     if (e == cudaSuccess && P == 1) {
@@ -366,7 +364,6 @@ struct okt_comm {
     S.s64 = st64.as<uint64_t>();
     S.sidx = stidx.as<uint32_t>();
     S.sval = stval.as<double>();
-    S.wold = wold.as<float>();
     S.agg = agg.as<uint64_t>();
     S.tag_ctr = &compact_tag;
     ++buf_gen;  // captured graphs hold these pointers
@@ -1014,10 +1011,6 @@ struct okt_comm {
     ap.d_flags_next = fl_next;
     ap.trace = trbuf.as<uint64_t>();
     ap.tag = ++compact_tag ? compact_tag : ++compact_tag;
-    okt::K1Apply ka;  // K1's argument 16 (the fused K7)
-    ka.w = sgd ? w : nullptr;
-    ka.wold = S.wold;
-    applied_w = sgd ? w : nullptr;
     hfast->bad_iter = 0;
     if (!G.exec || G.n != n || G.k != k || G.sgd != sgd || G.gen != buf_gen || G.prof != prof) {
       if (G.exec) {
@@ -1053,7 +1046,7 @@ struct okt_comm {
       std::vector<cudaGraphNode_t> nodes(nn);
       cudaGraphGetNodes(G.graph, nodes.data(), &nn);
       G.k1 = G.cb = nullptr;
-      const void* cfunc = okt::compact_graph_kernel();
+      const void* cfunc = okt::compact_graph_kernel(sgd);
       for (cudaGraphNode_t nd : nodes) {
         cudaGraphNodeType ty;
         cudaGraphNodeGetType(nd, &ty);
@@ -1076,10 +1069,9 @@ struct okt_comm {
       G.prof = prof;
     } else {
       // this step's arguments into the instantiated nodes: K1 (g, eps_in,
-      // eps_out, alpha, d_flags, K1Apply = arguments 0-3, 12 and 16) and
-      // phase B (ApplyArgs = argument 15)
-      if ((rc = patch_node(G.exec, G.k1, 17, {{0, &g}, {1, &eps_in}, {2, &eps_out}, {3, &alpha}, {12, &fl},
-                                              {16, &ka}})) ||
+      // eps_out, alpha, d_flags = arguments 0-3 and 12) and phase B
+      // (ApplyArgs = argument 15: model pointer, flag words, tag)
+      if ((rc = patch_node(G.exec, G.k1, 17, {{0, &g}, {1, &eps_in}, {2, &eps_out}, {3, &alpha}, {12, &fl}})) ||
           (rc = patch_node(G.exec, G.cb, 16, {{15, &ap}})))
         return rc;
     }
@@ -1269,13 +1261,11 @@ struct okt_comm {
     // P = 1: u is a subset of the local selection, so K7 (w -= u, eps = 0 at u)
     // is fused into the compaction that writes u, and indexes = u.indices.
     okt::ApplyArgs ap1;
-    applied_w = nullptr;
-    if (sgd && P == 1) {  // K7 fused into the emitting K1 (K1Apply)
+    if (sgd && P == 1) {  // K7 fused: residual zero in K1, model update in phase B
       ap1.k7 = true;
       ap1.acc = eps_out;
       ap1.w = w;
       ap1.d_flags = &d()->flags;
-      applied_w = w;
     }
 
     // ---- K1 / K2 ----
@@ -1452,9 +1442,8 @@ struct okt_comm {
       const double nn = double(n), mm = double(h->m);
       const double uu = double(P == 1 ? h->S : h->U);
       double sel = (sgd ? 12.0 : 4.0) * nn;
-      // single-rank EF step: K7 fused into K1 (w read + write, old word kept: 12 B per entry of u)
-      const double k7 = (P == 1 && sgd) ? 12.0 * uu : 0.0;
-      sel += k7;
+      // single-rank EF step: the model half of K7 in phase B (w read + write: 8 B per entry of u)
+      sel += (P == 1 && sgd) ? 8.0 * uu : 0.0;
       if (P == 1 && !thr) {
         sel += 12.0 * uu;
       } else {
@@ -1464,20 +1453,12 @@ struct okt_comm {
       t_bytes[OKT_T_SELECT] += sel;
       // the streaming kernel alone: reads g (+ eps), writes eps and 8 B per staged entry
       t_bytes[OKT_T_K1] += (sgd ? 12.0 : 4.0) * nn + 8.0 * ((P == 1 && !thr) ? uu : mm) +
-                           ((thr && sgd) ? 4.0 * nn : 0.0) + k7;
+                           ((thr && sgd) ? 4.0 * nn : 0.0);
       if (thr) t_bytes[OKT_T_THRESHOLD] += (sgd ? 2.0 : 3.0) * 4.0 * nn;
       if (P > 1) t_bytes[OKT_T_APPLY] += uu * (sgd ? 28.0 : 16.0);
     }
     if (h->flags & 1u) {
       dev_stale = true;
-      if (applied_w) {  // the fused single-rank K7 already ran in K1: restore the model
-        const cudaError_t e = okt::launch_k1_rollback(L, S, n, applied_w);
-        applied_w = nullptr;
-        if (e != cudaSuccess || cudaStreamSynchronize(L.s) != cudaSuccess) {
-          cudaGetLastError();
-          return set_err(OKT_ERR_CUDA, "model rollback after a non-finite step failed");
-        }
-      }
       return set_err(OKT_ERR_NUMERIC, "ok_sparse_allreduce: non-finite input");
     }
     if (h->flags & 8u) {

@@ -69,7 +69,7 @@ size_t stage_entries(uint64_t count, int tile, int max_chunks) {
 // =============================================================================
 // MODE 0: AoS u64 -> AoS u64; 1: AoS u64 -> SoA (u32, f32 widened to f64);
 //      2: SoA -> SoA; 3: u32 -> u32.
-constexpr int kCompactBatch = 2;
+constexpr int kCompactBatch = 4;
 
 // A CTA copies a group of consecutive chunks (up to kThreads; one chunk per
 // CTA for the static-chunk producers, a few tiles for K1's per-tile staging):
@@ -89,7 +89,13 @@ __device__ __forceinline__ uint64_t agg_load(const uint64_t* p) {
   return v;
 }
 
-template <int MODE>
+// APPLY (P = 1 EF step, MODE 1): the model half of K7 on every entry of u,
+// w[i] = float(double(w[i]) - v) (trainer.cpp:437-442, P = 1; K1 already
+// zeroed the residual); skipped when K1 met a non-finite accumulator (the
+// reference throws before touching the model).  Entries go in batches of
+// kCompactBatch per thread: staging loads, then the model gathers, then the
+// stores, so every random access of the batch is in flight together.
+template <int MODE, bool APPLY>
 __global__ void __launch_bounds__(kThreads)
     compact_kernel(const uint64_t* __restrict__ s64, const uint32_t* __restrict__ sidx,
                    const double* __restrict__ sval, const uint32_t* __restrict__ counts,
@@ -137,29 +143,37 @@ __global__ void __launch_bounds__(kThreads)
     }
     return uint64_t(c0 + lo) * cap + (j - s_pre[lo]);
   };
-  // The first kCompactBatch entries of each thread are loaded before the
-  // global prefix is known: only the output positions depend on it.
   constexpr int B = kCompactBatch;
   uint64_t e64[B];
   uint32_t ei[B];
   double ev[B];
+  float wv[B];
+  auto load_batch = [&](uint64_t j0) {
 #pragma unroll
-  for (int b = 0; b < B; ++b) {
-    const uint64_t j = tid + uint64_t(b) * kThreads;
-    e64[b] = 0;
-    ei[b] = 0;
-    ev[b] = 0.0;
-    if (j < cnt) {
-      const uint64_t sj = src_of(j);
-      if (MODE == 0 || MODE == 1) e64[b] = s64[sj];
-      if (MODE == 2 || MODE == 3) ei[b] = sidx[sj];
-      if (MODE == 2) ev[b] = sval[sj];
+    for (int b = 0; b < B; ++b) {
+      const uint64_t j = j0 + uint64_t(b) * kThreads;
+      e64[b] = 0;
+      ei[b] = 0;
+      ev[b] = 0.0;
+      if (j < cnt) {
+        const uint64_t sj = src_of(j);
+        if (MODE == 0 || MODE == 1) e64[b] = s64[sj];
+        if (MODE == 2 || MODE == 3) ei[b] = sidx[sj];
+        if (MODE == 2) ev[b] = sval[sj];
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
       if (MODE == 1) {
         ei[b] = coo_idx(e64[b]);
         ev[b] = double(coo_val(e64[b]));
       }
+      wv[b] = (APPLY && j0 + uint64_t(b) * kThreads < cnt) ? ap.w[ei[b]] : 0.f;
     }
-  }
+  };
+  // The first batch is loaded before the global prefix is known: only the
+  // output positions depend on it.
+  load_batch(tid);
   // look-back over the lower CTAs' group totals of this launch
   uint64_t pre = 0;
   for (uint32_t b = tid; b < blockIdx.x; b += kThreads) {
@@ -186,37 +200,39 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
   }
-  auto emit = [&](uint64_t j, uint64_t e, uint32_t i, double v) {
-    if (MODE == 0) o64[pre + j] = e;
-    else if (MODE == 3) oidx[pre + j] = i;
-    else {
-      oidx[pre + j] = i;
-      oval[pre + j] = v;
-    }
-  };
+  const bool skip = APPLY && (*ap.d_flags & 1u);  // non-finite step: the model stays as it was
+  bool bad = false;
+  for (uint64_t j0 = tid;; j0 += uint64_t(B) * kThreads) {
 #pragma unroll
-  for (int b = 0; b < B; ++b) {
-    const uint64_t j = tid + uint64_t(b) * kThreads;
-    if (j < cnt) emit(j, e64[b], ei[b], ev[b]);
-  }
-  for (uint64_t j = tid + uint64_t(B) * kThreads; j < cnt; j += kThreads) {
-    const uint64_t sj = src_of(j);
-    uint64_t e = 0;
-    uint32_t i = 0;
-    double v = 0.0;
-    if (MODE == 0 || MODE == 1) e = s64[sj];
-    if (MODE == 1) {
-      i = coo_idx(e);
-      v = double(coo_val(e));
+    for (int b = 0; b < B; ++b) {
+      const uint64_t j = j0 + uint64_t(b) * kThreads;
+      if (j >= cnt) continue;
+      if (MODE == 0) o64[pre + j] = e64[b];
+      else if (MODE == 3) oidx[pre + j] = ei[b];
+      else {
+        oidx[pre + j] = ei[b];
+        oval[pre + j] = ev[b];
+      }
+      if (APPLY && !skip) {
+        const float nw = float(double(wv[b]) - ev[b]);
+        ap.w[ei[b]] = nw;
+        bad |= nonfinite(nw);
+      }
     }
-    if (MODE == 2 || MODE == 3) i = sidx[sj];
-    if (MODE == 2) v = sval[sj];
-    emit(j, e, i, v);
+    if (j0 + uint64_t(B) * kThreads >= cnt) break;
+    load_batch(j0 + uint64_t(B) * kThreads);
+  }
+  if (APPLY && __syncthreads_or(bad) && tid == 0) {
+    atomicOr(ap.d_flags, 4u);
+    if (ap.hout) *reinterpret_cast<volatile uint32_t*>(&ap.hout->bad_iter) = 1u;  // (error path only)
   }
   if (lane == 0) trace_stamp(ap.trace, kTrCompact, 2);
 }
 
-const void* compact_graph_kernel() { return reinterpret_cast<const void*>(compact_kernel<1>); }
+const void* compact_graph_kernel(bool apply) {
+  return apply ? reinterpret_cast<const void*>(compact_kernel<1, true>)
+               : reinterpret_cast<const void*>(compact_kernel<1, false>);
+}
 
 // G chunks of `cap` entries (cap_host, or *d_cap when set); counts2: g2
 // partial sums (0 = none).
@@ -229,15 +245,19 @@ static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_
   // kThreads chunks; the grid never exceeds one wave (the look-back waits on
   // lower CTAs)
   static std::atomic<int> cap{0};  // (resident CTAs; benign concurrent first use)
-  if (!cap) cap = resident_ctas(compact_kernel<MODE>, kThreads, L.sms);
+  if (!cap) cap = resident_ctas(compact_kernel<MODE, true>, kThreads, L.sms);
   const uint32_t slots = uint32_t(std::min(cap.load(), S.max_chunks));
   const uint32_t per = std::min<uint32_t>(kThreads, std::max<uint32_t>(1, (G + slots - 1) / slots));
   const uint32_t GB = std::max<uint32_t>(1, (G + per - 1) / per);
   const uint32_t* c2 = g2 ? S.counts2 : nullptr;
   ApplyArgs a = ap ? *ap : ApplyArgs{};
   if (!a.tag) a.tag = ++*S.tag_ctr ? *S.tag_ctr : ++*S.tag_ctr;  // (0 never tags a launch)
-  compact_kernel<MODE><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap, o64,
-                                                 oidx, oval, d_total, d_total2, S.agg, a);
+  if (MODE == 1 && a.k7)
+    compact_kernel<MODE, true><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap,
+                                                         o64, oidx, oval, d_total, d_total2, S.agg, a);
+  else
+    compact_kernel<MODE, false><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap,
+                                                          o64, oidx, oval, d_total, d_total2, S.agg, a);
   ++L.launches;
   return cudaGetLastError();
 }
@@ -246,13 +266,14 @@ static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_
 // K1: fused accumulate / select / compact (phase A)
 // =============================================================================
 // APPLY (single rank, DUAL): u = the emitted set, and every entry of u is in
-// the local selection (indexes = u), so K7 runs here, in the tile that emits
-// the entry: the residual word is stored as 0 instead of acc (no extra bytes
-// on the ACCUM pass; a 4-byte store at the entry on the select-only refresh
-// pass), and w[i] = float(double(w[i]) - double(acc_i)) (trainer.cpp:437-442,
-// 476-480; P = 1).  The pre-update model word is kept per staged entry
-// (ka.wold) so the host can roll the model back when the step fails on a
-// non-finite accumulator (the reference throws before touching the model).
+// the local selection (indexes = u), so the residual half of K7 runs here, in
+// the tile that emits the entry: the residual word is stored as 0 instead of
+// acc (trainer.cpp:478-479; no extra bytes on the ACCUM pass, a 4-byte store
+// per entry on the select-only refresh pass).  The residual buffer written
+// here is committed only when the step succeeds.  The model half (w -= u)
+// stays in phase B, after the whole grid's finiteness is known: a model
+// update inside K1 put a dependent DRAM round trip into every tile and
+// slowed K1 from 0.60 to 1.02 ms at n = 340M (round-2 launch list).
 template <bool ACCUM, bool SELECT, bool HIST, bool VEC, bool DUAL, bool APPLY>
 __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
     k1_kernel(const float* __restrict__ g, const float* eps_in, float* eps_out, float alpha, uint64_t n,
@@ -319,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
     for (int i = tid; i < 2048; i += kThreads) s_hist[i] = 0;
     __syncthreads();
   }
-  bool bad = false, bad_iter = false;
+  bool bad = false;
   uint32_t mloc = 0;
   if (tid == 0) s_tile[0] = atomicAdd(&tile_ctr[0], 1u);
   __syncthreads();
@@ -445,14 +466,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
             const uint32_t pos = grp[j] + rank_in_group<C>(bal, j, c);
             const uint64_t e = base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C + c;
             out[pos] = coo_pack(uint32_t(e), a[j][c]);
-            if (APPLY) {
-              const float wo = ka.w[e];
-              const float nw = float(double(wo) - double(a[j][c]));
-              ka.w[e] = nw;
-              ka.wold[base + pos] = wo;
-              if (!ACCUM) ka.zero[e] = 0.f;
-              bad_iter |= nonfinite(nw);
-            }
+            if (APPLY && !ACCUM) ka.zero[e] = 0.f;
           }
         }
       }
@@ -467,7 +481,6 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
   if (__syncthreads_or(bad) && tid == 0) {
     atomicOr(d_flags, 1u);
   }
-  if (APPLY && __syncthreads_or(bad_iter) && tid == 0) atomicOr(d_flags, 4u);
   if (HIST) {
     for (int i = tid; i < 2048; i += kThreads)
       if (s_hist[i]) atomicAdd(&d_hist[i], s_hist[i]);
@@ -503,11 +516,7 @@ static cudaError_t k1_dispatch(Launch& L, const Stage& S, bool vec, const float*
   const uint64_t tiles = (n + TILE - 1) / TILE;
   auto kern = vec ? k1_kernel<ACCUM, SELECT, HIST, true, DUAL, APPLY> : k1_kernel<ACCUM, SELECT, HIST, false, DUAL, APPLY>;
   K1Apply ka{};
-  if (APPLY) {
-    ka.w = ap->w;
-    ka.wold = S.wold;
-    ka.zero = ACCUM ? nullptr : const_cast<float*>(g);  // the select-only pass reads acc in place
-  }
+  if (APPLY) ka.zero = ACCUM ? nullptr : const_cast<float*>(g);  // the select-only pass reads acc in place
   static std::atomic<int> cap_v{0}, cap_s{0};
   std::atomic<int>& cap = vec ? cap_v : cap_s;
   if (!cap) cap = resident_ctas(kern, kThreads, L.sms);
@@ -564,27 +573,6 @@ cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, co
                                                    d_m2, d_flags, d_hist, ap, pub, ind);
   }
   return cudaErrorInvalidValue;
-}
-
-// A failed single-rank step (non-finite accumulator somewhere in the grid)
-// after K1 already applied K7 in the tiles it emitted: put the old model words
-// back (one CTA per K1 tile; error path only).
-__global__ void __launch_bounds__(kThreads)
-    k1_rollback_kernel(const uint64_t* __restrict__ stg, const float* __restrict__ wold,
-                       const uint32_t* __restrict__ counts, uint32_t tiles, float* w) {
-  for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const uint32_t c = counts[t];
-    const uint64_t base = uint64_t(t) * kK1Tile;
-    for (uint32_t j = threadIdx.x; j < c; j += kThreads) w[coo_idx(stg[base + j])] = wold[base + j];
-  }
-}
-
-cudaError_t launch_k1_rollback(Launch& L, const Stage& S, uint64_t n, float* w) {
-  const uint64_t tiles = (n + kK1Tile - 1) / kK1Tile;
-  const uint32_t grid = uint32_t(std::min<uint64_t>(tiles, 65535));
-  k1_rollback_kernel<<<grid, kThreads, 0, L.s>>>(S.s64, S.wold, S.counts, uint32_t(tiles), w);
-  ++L.launches;
-  return cudaGetLastError();
 }
 
 // =============================================================================

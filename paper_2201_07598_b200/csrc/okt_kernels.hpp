@@ -42,7 +42,6 @@ struct Stage {
   uint64_t max_tiles = 0;         // counts[] capacity for K1's per-tile counts
   uint64_t* agg = nullptr;        // phase B: per-CTA group totals (tag << 32 | count), >= max_chunks words
   uint32_t* tag_ctr = nullptr;    // host counter tagging phase-B launches (never 0)
-  float* wold = nullptr;          // fused single-rank apply: pre-update model word per staged K1 entry
 };
 // Staging entries needed for a pass over `count` elements in tiles of `tile`.
 size_t stage_entries(uint64_t count, int tile, int max_chunks);
@@ -81,16 +80,12 @@ struct ApplyArgs {
   uint64_t* trace = nullptr;      // diagnostics (OKT_P2P_TRACE): per-CTA stamps, kind kTrCompact
   uint32_t tag = 0;               // phase-B launch tag (0: the launcher takes the next from Stage::tag_ctr)
 };
-// K1's fused single-rank apply (K1 argument 16).
+// K1's fused single-rank residual zeroing (K1 argument 16).
 struct K1Apply {
-  float* w = nullptr;     // model: w[i] = float(double(w[i]) - double(acc_i)) at every emitted i
-  float* wold = nullptr;  // pre-update model word at the entry's staging position (rollback)
   float* zero = nullptr;  // select-only pass: the acc buffer, zeroed at every emitted i
 };
 // The single-rank graph's phase-B kernel, for per-step parameter updates.
-const void* compact_graph_kernel();
-// Restores the model words a fused-apply K1 changed (a failed single-rank step).
-cudaError_t launch_k1_rollback(Launch& L, const Stage& S, uint64_t n, float* w);
+const void* compact_graph_kernel(bool apply);
 
 // Split-phase receive segments for the region scatter (M1): one per source.
 struct Segs {

@@ -196,10 +196,11 @@ def test_nccl_dead_peer_is_a_transport_error(gpus):
 
 @pytest.mark.parametrize("t_bad", [6, 9])  # a steady step (single-rank graph) and a refresh (tau' = 4)
 def test_single_rank_nonfinite_step_leaves_model_and_residual(okm, oracle, t_bad):
-    """K7 is fused into K1 at P = 1, so the tiles K1 finished before it met
-    the non-finite accumulator have already updated the model: the failed
-    step must put it back (trainer.cpp:466-488 throws before touching it),
-    and the trajectory then continues exactly like the oracle's."""
+    """At P = 1 K7 is fused into the select (residual zero in K1, model
+    update in phase B): a step that meets a non-finite accumulator late in
+    the grid must leave the model and the residual as they were
+    (trainer.cpp:466-488 throws before touching them), and the trajectory
+    then continues exactly like the oracle's."""
     import torch
     n, k = 300_000, 3_000
     w = okm.World(1, [0])
@@ -216,7 +217,7 @@ def test_single_rank_nonfinite_step_leaves_model_and_residual(okm, oracle, t_bad
                 w_before = model.w.cpu().numpy().copy()
                 eps_before = res.eps(ctx)
                 bad = g.copy()
-                bad[n - 7] = np.inf  # in the last tile: every earlier tile was applied
+                bad[n - 7] = np.inf  # in the last K1 tile
                 with pytest.raises(okm.NumericError):
                     okm.oktopk_sgd_step(ctx, model, res, bad, k, st)
                 assert np.array_equal(model.w.cpu().numpy(), w_before), "model changed by a failed step"
