@@ -250,6 +250,11 @@ struct okt_comm {
   // profiling
   bool prof = false;
   bool graphs_on = std::getenv("OKT_DISABLE_GRAPHS") == nullptr;
+  // Steady single-rank step: direct launches (default) or the captured graph (OKT_P1_GRAPH=1).
+  bool p1_direct = [] {
+    const char* e = std::getenv("OKT_P1_GRAPH");
+    return !(e && e[0] == '1');
+  }();
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   struct Span { int id; cudaEvent_t a, b; };
@@ -1012,7 +1017,21 @@ struct okt_comm {
     ap.trace = trbuf.as<uint64_t>();
     ap.tag = ++compact_tag ? compact_tag : ++compact_tag;
     hfast->bad_iter = 0;
-    if (!G.exec || G.n != n || G.k != k || G.sgd != sgd || G.gen != buf_gen || G.prof != prof) {
+    if (p1_direct) {
+      // The same two kernels launched directly, arguments and all (no graph):
+      // at n = 340M cudaGraphLaunch of the parameter-patched graph took 34 us
+      // of host time (+ 2 x 8 us patching) while the GPU waited (CUPTI trace,
+      // round 2); two cudaLaunchKernel calls take a few us and the second one
+      // is queued while K1 runs.
+      tmark(OKT_T_SELECT, s);
+      rc = ck(okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, g, eps_in, eps_out, alpha,
+                             n, &d()->local_th, &d()->global_th,
+                             okt::OutCoo{nullptr, sur_idx.as<uint32_t>(), sur_val.as<double>()}, &d()->S, &d()->m, fl,
+                             nullptr, &ap, nullptr, nullptr),
+              "k1");
+      tstop(s);
+      if (rc) return rc;
+    } else if (!G.exec || G.n != n || G.k != k || G.sgd != sgd || G.gen != buf_gen || G.prof != prof) {
       if (G.exec) {
         cudaGraphExecDestroy(G.exec);
         G.exec = nullptr;
@@ -1075,10 +1094,12 @@ struct okt_comm {
           (rc = patch_node(G.exec, G.cb, 16, {{15, &ap}})))
         return rc;
     }
-    if ((rc = ck(cudaGraphLaunch(G.exec, s), "graph launch"))) return rc;
-    L.launches += G.kernels;
-    if (prof) k1_used = 2 * graph1_k1_pairs;  // the graph re-recorded its K1 events
-    graph_prof_pending = prof;
+    if (!p1_direct) {
+      if ((rc = ck(cudaGraphLaunch(G.exec, s), "graph launch"))) return rc;
+      L.launches += G.kernels;
+      if (prof) k1_used = 2 * graph1_k1_pairs;  // the graph re-recorded its K1 events
+      graph_prof_pending = prof;
+    }
     if (defer) {
       hfast_pending = true;  // read by wait_pending after its sync
       return OKT_OK;
@@ -1184,7 +1205,7 @@ struct okt_comm {
     const bool thr = (t - 1) % int64_t(st.tau_prime) == 0;
     const bool bnd = (t - 1) % int64_t(st.tau) == 0;
     auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-    const bool use_graph = P == 1 && !thr && graphs_on && al16(g) && (!sgd || al16(w));
+    const bool use_graph = P == 1 && !thr && (p1_direct || (graphs_on && al16(g) && (!sgd || al16(w))));
     if (P > 1 && (rc = setup_p2p(n, s))) return rc;
     // The path choice must be the same on every rank, so it may not depend on
     // rank-local pointer alignment: a gradient that is not 16-byte aligned
