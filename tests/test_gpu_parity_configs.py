@@ -140,8 +140,9 @@ def test_ef_trajectory_tolerance_on_drift_inputs(okm, oracle):
     Stated tolerance (every step, P = 2, n = 1M, k = 1%, tau' = 32):
       * the u index sets agree to Jaccard >= 0.999 and |U - U_ref| <= 0.1% U_ref;
       * on common indices, |u - u_ref| <= 2^-20 * max|u_ref| (fp32 residual drift);
-      * the model's relative L2 error stays <= 2^-18.
-    The first step at which the index sets differ at all is reported."""
+      * the model's relative L2 error stays <= 2^-20.
+    The first step at which the index sets differ at all is reported (round-2
+    B200 run: none within 40 steps; worst |du| 5.8e-8 and model error 9.1e-8)."""
     P, n, k, T = 2, 1_000_000, 10_000, 40
     w = okm.World(P, [0] * P)
     try:
@@ -172,9 +173,9 @@ def test_ef_trajectory_tolerance_on_drift_inputs(okm, oracle):
             dw = float(np.linalg.norm(wm - ws[0])) / max(1e-300, float(np.linalg.norm(ws[0])))
             worst = dict(jaccard=min(worst["jaccard"], jac), dU=max(worst["dU"], dU), dval=max(worst["dval"], dval),
                          dw=max(worst["dw"], dw))
-            assert jac >= 0.99 and dU <= 1e-2, (t, jac, dU)
-            assert dval <= 2.0 ** -16, (t, dval)
-            assert dw <= 1e-3, (t, dw)
+            assert jac >= 0.999 and dU <= 1e-3, (t, jac, dU)
+            assert dval <= 2.0 ** -20, (t, dval)
+            assert dw <= 2.0 ** -20, (t, dw)
         print(f"\n[EF fp32 vs fp64, P={P} n={n} k={k}] first index-set difference at t = {first_diff}; worst {worst}")
     finally:
         w.destroy()

@@ -11,9 +11,9 @@ cap() {  # name regex skip
       --launch-count 1 -o "$OUT/$1" $B > "$OUT/ncu_$1.log" 2>&1
   ncu -i "$OUT/$1.ncu-rep" --page raw --csv > "$OUT/$1_raw.csv" 2>/dev/null
 }
-cap k1_steady 'k1_kernel<true, true, false, true, true' 3
-cap phaseb 'compact_kernel<1, true>' 3
-cap k1_refresh_select 'k1_kernel<false, true, false, true, true' 1
-cap k1_hist 'k1_kernel<true, false, true' 1
+cap k1_steady 'k1_kernel<.bool.1, .bool.1, .bool.0, .bool.1, .bool.1' 3
+cap phaseb 'compact_kernel<.int.1, .bool.1>' 3
+cap k1_refresh_select 'k1_kernel<.bool.0, .bool.1, .bool.0, .bool.1, .bool.1' 1
+cap k1_hist 'k1_kernel<.bool.1, .bool.0, .bool.1' 1
 timeout 600 python bench.py --steps 4 --warmup 3 --no-cpu-baseline --e2e-steps 2 --trace "$OUT/trace" $* > "$OUT/trace.log" 2>&1
 echo done
