@@ -943,11 +943,11 @@ struct okt_comm {
       G.win = win_n;
     } else if (sgd && argfed_on) {
       // this step's arguments into the instantiated nodes: K1 (g, eps_in,
-      // eps_out, alpha, the flag word, K1P2P = arguments 0-3, 12, 15), the
-      // merge's and the pull's flag word (arguments 7 and 5)
+      // eps_out, alpha, the flag word, K1P2P = arguments 0-3, 12, 15 of 17),
+      // the merge's and the pull's flag word (arguments 7 and 5)
       uint32_t* fl = &d()->p2pflags[hup->sp.par];
       okt::K1P2P kp = k1p2p_args(true);
-      if ((rc = patch_node(G.exec, G.k1, 16, {{0, &hup->sp.g}, {1, &hup->sp.eps_in}, {2, &hup->sp.eps_out},
+      if ((rc = patch_node(G.exec, G.k1, kK1Args, {{0, &hup->sp.g}, {1, &hup->sp.eps_in}, {2, &hup->sp.eps_out},
                                               {3, &hup->sp.alpha}, {12, &fl}, {15, &kp}})) ||
           (rc = patch_node(G.exec, G.merge, 9, {{7, &fl}})) || (rc = patch_node(G.exec, G.pull, 10, {{5, &fl}})))
         return rc;
@@ -958,6 +958,9 @@ struct okt_comm {
   }
 
   // Rewrites some arguments of an instantiated kernel node (index -> value).
+  // Kernel parameter counts of the patched nodes (okt_kernels.cu: k1_kernel,
+  // compact_kernel; okt_p2p.cu: p2p_merge_kernel, p2p_pull_kernel).
+  static constexpr int kK1Args = 17, kCompactArgs = 16;
   int patch_node(cudaGraphExec_t exec, cudaGraphNode_t nd, int nargs,
                  std::initializer_list<std::pair<int, void*>> args) {
     cudaKernelNodeParams kp{};
@@ -1090,8 +1093,8 @@ struct okt_comm {
       // this step's arguments into the instantiated nodes: K1 (g, eps_in,
       // eps_out, alpha, d_flags = arguments 0-3 and 12) and phase B
       // (ApplyArgs = argument 15: model pointer, flag words, tag)
-      if ((rc = patch_node(G.exec, G.k1, 17, {{0, &g}, {1, &eps_in}, {2, &eps_out}, {3, &alpha}, {12, &fl}})) ||
-          (rc = patch_node(G.exec, G.cb, 16, {{15, &ap}})))
+      if ((rc = patch_node(G.exec, G.k1, kK1Args, {{0, &g}, {1, &eps_in}, {2, &eps_out}, {3, &alpha}, {12, &fl}})) ||
+          (rc = patch_node(G.exec, G.cb, kCompactArgs, {{15, &ap}})))
         return rc;
     }
     if (!p1_direct) {

@@ -40,6 +40,27 @@ constexpr uint32_t kAbortBits = 1u | 8u | 16u;  // local non-finite, peer timeou
 // on the GPU for tens of microseconds; tools/p2p_noise.cu.)
 constexpr int kMergeTile = kK1Tile;              // coordinates per CTA tile
 constexpr int kMergePer = kMergeTile / kThreads;  // 16 coordinates per thread in the scan
+constexpr int kMergeStages = 4;                   // tiles of entries in flight per CTA
+constexpr int kMergeRing = 128;                   // entries per source per ring stage
+constexpr int kMergeCntCap = 256;                 // tiles whose counts are staged at once
+
+template <int P>
+constexpr size_t merge_smem() {  // mask bytes, values [P][tile], ring [S][P][kMergeRing], counts
+  return size_t(kMergeTile) + size_t(P) * kMergeTile * sizeof(float) +
+         size_t(kMergeStages) * P * kMergeRing * sizeof(uint64_t) + size_t(kMergeCntCap) * P * sizeof(uint32_t);
+}
+
+// 16-byte async copy, L2 only (.cg: no L1 line of a peer's buffer survives
+// into a later step that reuses the same parity slot).
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // P = 2 is capped at 48 registers: 5 CTAs per SM instead of 4 (shared memory
 // allows 6), so more of the region's tiles are in flight at once (interleaved
@@ -101,102 +122,116 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
   uint32_t* const out_idx = tab->sidx[me][par];
   double* const out_val = tab->sval[me][par];
   uint32_t* const out_cnt = tab->scnt[me][par];
-  // Tiles of this CTA: j = blockIdx.x + i * gridDim.x.  Two-stage prefetch:
-  // while tile j is merged, the entries of the next tile and the counts of
-  // the one after are in flight (one entry per thread and source per stage;
-  // a source with more than kThreads entries in a tile — dense regions — is
-  // finished by a direct loop).
+  // Tiles of this CTA: j = blockIdx.x + i * gridDim.x, i < my_n.  Their
+  // per-source counts are staged in shared memory first (all loads in flight
+  // at once), then a kMergeStages-deep cp.async ring keeps the entries of the
+  // next tiles of every source in flight over NVLink while a tile is merged
+  // (the first kMergeRing entries of a tile per source; a denser tile's rest
+  // is read directly).  Round 1 kept one tile in flight: 6.8 us per tile at
+  // n = 340M, P = 4, almost all of it NVLink latency.
+  uint64_t* const ring = reinterpret_cast<uint64_t*>(s_val + P * kMergeTile);    // [S][P][kMergeRing]
+  uint32_t* const s_cnt = reinterpret_cast<uint32_t*>(ring + kMergeStages * P * kMergeRing);  // [kMergeCntCap][P]
   const uint32_t gs = gridDim.x;
-  auto load_counts = [&](uint32_t j, uint32_t (&c)[P]) {
-#pragma unroll
-    for (int r = 0; r < P; ++r) c[r] = (j < ntiles && !s_abort) ? tab->kcnt[r][par][t_lo + j] : 0u;
-  };
-  auto load_entries = [&](uint32_t j, const uint32_t (&c)[P], uint64_t (&e)[P]) {
-#pragma unroll
-    for (int r = 0; r < P; ++r)
-      e[r] = uint32_t(q) < c[r] ? tab->kstg[r][par][uint64_t(t_lo + j) * kMergeTile + q] : ~0ull;
-  };
-  uint32_t cnt0[P], cnt1[P], cnt2[P];
-  uint64_t e0[P], e1[P];
-  load_counts(blockIdx.x, cnt0);
-  load_entries(blockIdx.x, cnt0, e0);
-  load_counts(blockIdx.x + gs, cnt1);
-  for (uint32_t j = blockIdx.x; j < ntiles; j += gs) {
-    const uint32_t t = t_lo + j;
-    const uint64_t base = uint64_t(t) * kMergeTile;
-    load_entries(j + gs, cnt1, e1);
-    load_counts(j + 2 * gs, cnt2);
-    for (int w = q; w < kMergeTile / 4; w += kThreads) s_mask[w] = 0;
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < P; ++r) {
-      uint32_t got = 0;
-      auto land = [&](uint64_t ent) {
-        const uint64_t idx = coo_idx(ent);
-        if (idx < lo || idx >= hi) return;  // the region's edge tiles
-        const uint32_t c = uint32_t(idx - base);
-        s_val[r * kMergeTile + c] = coo_val(ent);
-        atomicOr(&s_mask[c >> 2], 1u << ((c & 3u) * 8u + uint32_t(r)));
-        ++got;
-      };
-      if (e0[r] != ~0ull) land(e0[r]);
-      for (uint32_t e = kThreads + q; e < cnt0[r]; e += kThreads) land(tab->kstg[r][par][base + e]);
-      got = __reduce_add_sync(0xffffffffu, got);
-      if (lane == 0 && got) atomicAdd(&s_seg[r], got);
-    }
-#pragma unroll
-    for (int r = 0; r < P; ++r) {
-      cnt0[r] = cnt1[r];
-      cnt1[r] = cnt2[r];
-      e0[r] = e1[r];
+  const uint32_t my_n = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gs + 1 : 0;
+  for (uint32_t i0 = 0; i0 < my_n; i0 += kMergeCntCap) {
+    const uint32_t ni = min(my_n - i0, uint32_t(kMergeCntCap));
+    for (uint32_t x = q; x < ni * P; x += kThreads) {
+      const uint32_t i = x / P;
+      const int r = int(x % P);
+      s_cnt[x] = s_abort ? 0u : tab->kcnt[r][par][t_lo + blockIdx.x + (i0 + i) * gs];
     }
     __syncthreads();
-    // bracket scan + filter over the tile: thread q owns coordinates
-    // [16 q, 16 q + 16) (four mask words)
-    const uint4 mw4 = reinterpret_cast<const uint4*>(s_mask)[q];
-    auto bits_of = [&](int k) {  // source bits of coordinate k (select tree: no local memory)
-      const int j = k >> 2;
-      const uint32_t w = (j & 2) ? ((j & 1) ? mw4.w : mw4.z) : ((j & 1) ? mw4.y : mw4.x);
-      return (w >> (8 * (k & 3))) & 0xffu;
+    auto issue = [&](uint32_t i) {  // ring stage i % S <- tile i's first entries, every source
+      if (i < ni) {
+        const uint64_t base = uint64_t(t_lo + blockIdx.x + (i0 + i) * gs) * kMergeTile;
+        uint64_t* slot = ring + (i % kMergeStages) * (P * kMergeRing);
+        // entry pairs (16 B; a tile's staging slot starts 16-byte aligned and
+        // holds kMergeTile entries, so the odd count's partner is in bounds)
+        for (int x = q; x < P * kMergeRing / 2; x += kThreads) {
+          const int r = x / (kMergeRing / 2), e = 2 * (x % (kMergeRing / 2));
+          if (uint32_t(e) < s_cnt[i * P + r]) cp_async16(slot + r * kMergeRing + e, tab->kstg[r][par] + base + e);
+        }
+      }
+      cp_async_commit();  // (empty groups keep the group count uniform)
     };
-    auto nib = [](uint32_t w) { return ((__vcmpne4(w, 0u) & 0x01010101u) * 0x01020408u) >> 24; };
-    const uint32_t present = nib(mw4.x) | (nib(mw4.y) << 4) | (nib(mw4.z) << 8) | (nib(mw4.w) << 12);
-    uint32_t sel = 0;
-    for (uint32_t rest = present; rest; rest &= rest - 1) {
-      const int k = __ffs(rest) - 1;
-      const uint32_t c = uint32_t(q) * kMergePer + uint32_t(k);
-      float v[P];
 #pragma unroll
-      for (int r = 0; r < P; ++r) v[r] = s_val[r * kMergeTile + c];
-      if (fabs(bracket_regs<P>(v, bits_of(k))) >= gth) sel |= 1u << k;
-    }
-    const uint32_t n_sel = __popc(sel);
-    uint32_t incl = n_sel;
+    for (int st = 0; st < kMergeStages - 1; ++st) issue(uint32_t(st));
+    for (uint32_t i = 0; i < ni; ++i) {
+      cp_async_wait<kMergeStages - 2>();
+      for (int w = q; w < kMergeTile / 4; w += kThreads) s_mask[w] = 0;
+      __syncthreads();  // stage i landed everywhere; the slot of tile i - 1 is free
+      issue(i + kMergeStages - 1);
+      const uint32_t j = blockIdx.x + (i0 + i) * gs;
+      const uint32_t t = t_lo + j;
+      const uint64_t base = uint64_t(t) * kMergeTile;
+      const uint64_t* slot = ring + (i % kMergeStages) * (P * kMergeRing);
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += x;
+      for (int r = 0; r < P; ++r) {
+        uint32_t got = 0;
+        auto land = [&](uint64_t ent) {
+          const uint64_t idx = coo_idx(ent);
+          if (idx < lo || idx >= hi) return;  // the region's edge tiles
+          const uint32_t c = uint32_t(idx - base);
+          s_val[r * kMergeTile + c] = coo_val(ent);
+          atomicOr(&s_mask[c >> 2], 1u << ((c & 3u) * 8u + uint32_t(r)));
+          ++got;
+        };
+        const uint32_t cr = s_cnt[i * P + r];
+        for (uint32_t e = q; e < cr; e += kThreads)
+          land(e < uint32_t(kMergeRing) ? slot[r * kMergeRing + e] : tab->kstg[r][par][base + e]);
+        got = __reduce_add_sync(0xffffffffu, got);
+        if (lane == 0 && got) atomicAdd(&s_seg[r], got);
+      }
+      __syncthreads();
+      // bracket scan + filter over the tile: thread q owns coordinates
+      // [16 q, 16 q + 16) (four mask words)
+      const uint4 mw4 = reinterpret_cast<const uint4*>(s_mask)[q];
+      auto bits_of = [&](int k) {  // source bits of coordinate k (select tree: no local memory)
+        const int jj = k >> 2;
+        const uint32_t w = (jj & 2) ? ((jj & 1) ? mw4.w : mw4.z) : ((jj & 1) ? mw4.y : mw4.x);
+        return (w >> (8 * (k & 3))) & 0xffu;
+      };
+      auto nib = [](uint32_t w) { return ((__vcmpne4(w, 0u) & 0x01010101u) * 0x01020408u) >> 24; };
+      const uint32_t present = nib(mw4.x) | (nib(mw4.y) << 4) | (nib(mw4.z) << 8) | (nib(mw4.w) << 12);
+      uint32_t sel = 0;
+      for (uint32_t rest = present; rest; rest &= rest - 1) {
+        const int k = __ffs(rest) - 1;
+        const uint32_t c = uint32_t(q) * kMergePer + uint32_t(k);
+        float v[P];
+#pragma unroll
+        for (int r = 0; r < P; ++r) v[r] = s_val[r * kMergeTile + c];
+        if (fabs(bracket_regs<P>(v, bits_of(k))) >= gth) sel |= 1u << k;
+      }
+      const uint32_t n_sel = __popc(sel);
+      uint32_t incl = n_sel;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      if (lane == 31) s_wt[warp] = incl;
+      __syncthreads();
+      uint32_t wpre = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        wpre += (w < warp) ? s_wt[w] : 0u;
+        total += s_wt[w];
+      }
+      uint64_t pos = uint64_t(j) * kMergeTile + wpre + incl - n_sel;
+      for (uint32_t rest = sel; rest; rest &= rest - 1, ++pos) {
+        const int k = __ffs(rest) - 1;
+        const uint32_t c = uint32_t(q) * kMergePer + uint32_t(k);
+        float v[P];
+#pragma unroll
+        for (int r = 0; r < P; ++r) v[r] = s_val[r * kMergeTile + c];
+        out_idx[pos] = uint32_t(base + c);
+        out_val[pos] = bracket_regs<P>(v, bits_of(k));
+      }
+      if (q == 0) out_cnt[j] = total;
+      __syncthreads();  // s_mask / s_val / s_wt / the ring slot reused by later tiles
     }
-    if (lane == 31) s_wt[warp] = incl;
+    cp_async_wait<0>();
     __syncthreads();
-    uint32_t wpre = 0, total = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      wpre += (w < warp) ? s_wt[w] : 0u;
-      total += s_wt[w];
-    }
-    uint64_t pos = uint64_t(j) * kMergeTile + wpre + incl - n_sel;
-    for (uint32_t rest = sel; rest; rest &= rest - 1, ++pos) {
-      const int k = __ffs(rest) - 1;
-      const uint32_t c = uint32_t(q) * kMergePer + uint32_t(k);
-      float v[P];
-#pragma unroll
-      for (int r = 0; r < P; ++r) v[r] = s_val[r * kMergeTile + c];
-      out_idx[pos] = uint32_t(base + c);
-      out_val[pos] = bracket_regs<P>(v, bits_of(k));
-    }
-    if (q == 0) out_cnt[j] = total;
-    __syncthreads();  // s_mask / s_val / s_wt reused by the next tile
   }
   if (q < P && s_seg[q]) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->seg_cnt[q]), (unsigned long long)s_seg[q]);
   if (lane == 0) trace_stamp(trace, kTrMerge, 2);
@@ -511,7 +546,7 @@ template <int P>
 static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
                                   uint64_t W, uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags,
                                   uint64_t timeout_ns) {
-  constexpr size_t smem = size_t(kMergeTile) + size_t(P) * kMergeTile * sizeof(float);
+  constexpr size_t smem = merge_smem<P>();
   // the dynamic shared memory opt-in is per device
   static std::atomic<int> caps[64];  // per device (the dynamic-smem opt-in is per device)
   int dev = 0;
