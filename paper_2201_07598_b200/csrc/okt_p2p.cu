@@ -50,6 +50,11 @@ constexpr size_t merge_smem() {  // mask bytes, values [P][tile], ring [S][P][kM
          size_t(kMergeStages) * P * kMergeRing * sizeof(uint64_t) + size_t(kMergeCntCap) * P * sizeof(uint32_t);
 }
 
+// First tile of span c when `tiles` tiles are split evenly over G spans.
+__host__ __device__ __forceinline__ uint32_t span_at(uint32_t c, uint32_t tiles, uint32_t G) {
+  return uint32_t(uint64_t(c) * tiles / G);
+}
+
 // 16-byte async copy, L2 only (.cg: no L1 line of a peer's buffer survives
 // into a later step that reuses the same parity slot).
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
@@ -93,8 +98,8 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
     // quiet: K1 finished and nobody streams yet)
     if (q == 0) {
       P2PPub* pub = &tab->hdr[me]->pub[par];  // (read by this rank's pull)
-      pub->sur_G = ntiles;
-      pub->sur_cap = kMergeTile;
+      pub->sur_G = gridDim.x;  // one survivor chunk per CTA
+      pub->sur_tiles = ntiles;
       trace_stamp(trace, kTrPubL, 0);
     }
     const uint64_t pay[3] = {(*d_flags & 1u) ? 1ull : 0ull, k1_tiles, uint64_t(kK1Tile)};
@@ -122,7 +127,10 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
   uint32_t* const out_idx = tab->sidx[me][par];
   double* const out_val = tab->sval[me][par];
   uint32_t* const out_cnt = tab->scnt[me][par];
-  // Tiles of this CTA: j = blockIdx.x + i * gridDim.x, i < my_n.  Their
+  // This CTA's tiles: the contiguous span [j0, j0 + my_n) of the region, and
+  // its survivors: one contiguous chunk at j0 * kMergeTile (the span's
+  // capacity), count in out_cnt[blockIdx.x] — a few hundred large chunks per
+  // rank for the pull instead of one small chunk per tile.  The span's
   // per-source counts are staged in shared memory first (all loads in flight
   // at once), then a kMergeStages-deep cp.async ring keeps the entries of the
   // next tiles of every source in flight over NVLink while a tile is merged
@@ -131,19 +139,21 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
   // n = 340M, P = 4, almost all of it NVLink latency.
   uint64_t* const ring = reinterpret_cast<uint64_t*>(s_val + P * kMergeTile);    // [S][P][kMergeRing]
   uint32_t* const s_cnt = reinterpret_cast<uint32_t*>(ring + kMergeStages * P * kMergeRing);  // [kMergeCntCap][P]
-  const uint32_t gs = gridDim.x;
-  const uint32_t my_n = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gs + 1 : 0;
+  const uint32_t j0 = span_at(blockIdx.x, ntiles, gridDim.x);
+  const uint32_t my_n = span_at(blockIdx.x + 1, ntiles, gridDim.x) - j0;
+  const uint64_t out_base = uint64_t(j0) * kMergeTile;
+  uint32_t running = 0;  // survivors of this CTA so far (block-uniform)
   for (uint32_t i0 = 0; i0 < my_n; i0 += kMergeCntCap) {
     const uint32_t ni = min(my_n - i0, uint32_t(kMergeCntCap));
     for (uint32_t x = q; x < ni * P; x += kThreads) {
       const uint32_t i = x / P;
       const int r = int(x % P);
-      s_cnt[x] = s_abort ? 0u : tab->kcnt[r][par][t_lo + blockIdx.x + (i0 + i) * gs];
+      s_cnt[x] = s_abort ? 0u : tab->kcnt[r][par][t_lo + j0 + i0 + i];
     }
     __syncthreads();
     auto issue = [&](uint32_t i) {  // ring stage i % S <- tile i's first entries, every source
       if (i < ni) {
-        const uint64_t base = uint64_t(t_lo + blockIdx.x + (i0 + i) * gs) * kMergeTile;
+        const uint64_t base = uint64_t(t_lo + j0 + i0 + i) * kMergeTile;
         uint64_t* slot = ring + (i % kMergeStages) * (P * kMergeRing);
         // entry pairs (16 B; a tile's staging slot starts 16-byte aligned and
         // holds kMergeTile entries, so the odd count's partner is in bounds)
@@ -161,8 +171,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
       for (int w = q; w < kMergeTile / 4; w += kThreads) s_mask[w] = 0;
       __syncthreads();  // stage i landed everywhere; the slot of tile i - 1 is free
       issue(i + kMergeStages - 1);
-      const uint32_t j = blockIdx.x + (i0 + i) * gs;
-      const uint32_t t = t_lo + j;
+      const uint32_t t = t_lo + j0 + i0 + i;
       const uint64_t base = uint64_t(t) * kMergeTile;
       const uint64_t* slot = ring + (i % kMergeStages) * (P * kMergeRing);
 #pragma unroll
@@ -217,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
         wpre += (w < warp) ? s_wt[w] : 0u;
         total += s_wt[w];
       }
-      uint64_t pos = uint64_t(j) * kMergeTile + wpre + incl - n_sel;
+      uint64_t pos = out_base + running + wpre + incl - n_sel;
       for (uint32_t rest = sel; rest; rest &= rest - 1, ++pos) {
         const int k = __ffs(rest) - 1;
         const uint32_t c = uint32_t(q) * kMergePer + uint32_t(k);
@@ -227,12 +236,13 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
         out_idx[pos] = uint32_t(base + c);
         out_val[pos] = bracket_regs<P>(v, bits_of(k));
       }
-      if (q == 0) out_cnt[j] = total;
+      running += total;
       __syncthreads();  // s_mask / s_val / s_wt / the ring slot reused by later tiles
     }
     cp_async_wait<0>();
     __syncthreads();
   }
+  if (q == 0) out_cnt[blockIdx.x] = running;
   if (q < P && s_seg[q]) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->seg_cnt[q]), (unsigned long long)s_seg[q]);
   if (lane == 0) trace_stamp(trace, kTrMerge, 2);
 }
@@ -249,7 +259,7 @@ __global__ void __launch_bounds__(kThreads)
                     uint32_t* done) {
   __shared__ int s_last;
   __shared__ uint64_t s_size[kP2PMaxP], s_off[kP2PMaxP + 1], s_blk[kP2PMaxP + 1];
-  __shared__ uint32_t s_G[kP2PMaxP], s_cap[kP2PMaxP], s_start[kP2PMaxP + 1];
+  __shared__ uint32_t s_G[kP2PMaxP], s_tiles[kP2PMaxP], s_start[kP2PMaxP + 1];
   __shared__ int s_bal, s_abort;
   const uint64_t epoch = sp->epoch;
   const int par = sp->par;
@@ -317,7 +327,7 @@ __global__ void __launch_bounds__(kThreads)
         trace_stamp(trace, kTrPubSur, 0);
       }
       __syncthreads();
-      const uint64_t pay[4] = {(*d_flags & kAbortBits) ? 1ull : 0ull, tot, uint64_t(G), uint64_t(mine->sur_cap)};
+      const uint64_t pay[4] = {(*d_flags & kAbortBits) ? 1ull : 0ull, tot, uint64_t(G), uint64_t(mine->sur_tiles)};
       publish_flag(tab->hdr, P, me, kFlagSurReady, epoch, pay);
       if (q == 0) trace_stamp(trace, kTrPubSur, 3);
     }
@@ -343,7 +353,7 @@ __global__ void __launch_bounds__(kThreads)
       }
       s_size[q] = sz;
       s_G[q] = G;
-      s_cap[q] = cap;
+      s_tiles[q] = cap;
     }
     __syncthreads();
     if (q == 0) {
@@ -367,7 +377,7 @@ __global__ void __launch_bounds__(kThreads)
         for (int r = 0; r < P; ++r) {
           plan->sizes[r] = s_size[r];
           plan->sur_G[r] = s_G[r];
-          plan->sur_cap[r] = s_cap[r];
+          plan->sur_tiles[r] = s_tiles[r];
         }
         for (int r = 0; r <= P; ++r) {
           plan->off[r] = s_off[r];
@@ -431,7 +441,8 @@ __global__ void __launch_bounds__(kThreads)
     // (rank, chunk, part) work items: every chunk split so all warps get a share
     const uint32_t items = s_start[P];
     const uint32_t warps_total = gridDim.x * kWarps;
-    const uint32_t parts = max(1u, min(8u, warps_total / max(1u, items)));
+    // (a chunk is one merge CTA's span: thousands of entries at large n)
+    const uint32_t parts = max(1u, min(64u, warps_total / max(1u, items)));
     for (uint32_t it = blockIdx.x * kWarps + warp; it < items * parts; it += warps_total) {
       const uint32_t item = it / parts, part = it % parts;
       int r = 0;
@@ -441,8 +452,9 @@ __global__ void __launch_bounds__(kThreads)
       const uint64_t end = base + tab->scnt[r][par][c];
       const uint64_t len = end - base;
       const uint64_t lo = max(base + len * part / parts, a), hi = min(base + len * (part + 1) / parts, b);
-      const uint32_t* si = tab->sidx[r][par] + uint64_t(c) * s_cap[r];
-      const double* sv = tab->sval[r][par] + uint64_t(c) * s_cap[r];
+      const uint64_t cbase = uint64_t(span_at(c, s_tiles[r], s_G[r])) * kMergeTile;
+      const uint32_t* si = tab->sidx[r][par] + cbase;
+      const double* sv = tab->sval[r][par] + cbase;
       for (uint64_t p0 = lo; p0 < hi; p0 += 32 * R) {
         uint64_t pos[R];
         bool ok[R];

@@ -47,8 +47,8 @@ struct P2PPub {
   uint64_t S;        // survivors of the global threshold
   uint32_t k1_G;     // K1 chunk geometry: chunks and entries per chunk
   uint32_t k1_cap;
-  uint32_t sur_G;    // region-scan chunk geometry
-  uint32_t sur_cap;
+  uint32_t sur_G;     // survivor chunks: one per merge CTA (its contiguous span of tiles)
+  uint32_t sur_tiles; // merge tiles of the region (chunk c starts at split(c) * kK1Tile)
   uint64_t pad[4];
 };
 
@@ -108,8 +108,8 @@ struct P2PPlan {
   uint64_t seg_off[kP2PMaxP];    // my split slices inside each source's L
   uint64_t seg_cnt[kP2PMaxP];
   uint64_t peer_status[kP2PMaxP];
-  uint32_t sur_G[kP2PMaxP];      // every rank's region-scan chunk geometry
-  uint32_t sur_cap[kP2PMaxP];
+  uint32_t sur_G[kP2PMaxP];      // every rank's survivor chunk geometry (chunks, region tiles)
+  uint32_t sur_tiles[kP2PMaxP];
 };
 
 // K7 fused into the allgatherv pull: every u entry is touched once.
