@@ -51,8 +51,14 @@ constexpr size_t merge_smem() {  // mask bytes, values [P][tile], ring [S][P][kM
 }
 
 // First tile of span c when `tiles` tiles are split evenly over G spans.
-__host__ __device__ __forceinline__ uint32_t span_at(uint32_t c, uint32_t tiles, uint32_t G) {
-  return uint32_t(uint64_t(c) * tiles / G);
+// (floor(c * tiles / G) without the 64-bit division subroutine: the product
+// is < 2^53, so the double quotient is within one of the answer; fix it up.)
+__device__ __forceinline__ uint32_t span_at(uint32_t c, uint32_t tiles, uint32_t G) {
+  const uint64_t m = uint64_t(c) * tiles;
+  uint64_t qv = uint64_t(double(m) / double(G));
+  if (qv * G > m) --qv;
+  else if ((qv + 1) * G <= m) ++qv;
+  return uint32_t(qv);
 }
 
 // 16-byte async copy, L2 only (.cg: no L1 line of a peer's buffer survives
