@@ -453,13 +453,28 @@ def run_okt(args):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     if args.p2p_trace:
         dump_p2p_trace(L, comm, rank, args.p2p_trace)
-    # ---- the same iterations again with the library's per-phase CUDA events on
-    # its stream (phase breakdown + the K1 roofline); fresh start, inputs per step
+    # ---- steady iterations t = 2..1+nprof again with the library's per-phase
+    # CUDA events on its stream (phase breakdown, the K1 roofline, and the
+    # bytes each phase received over NVLink per unit time); fresh start
+    from paper_2201_07598_b200._lib import OktCounters
+
+    def ledger_bytes():
+        out = []
+        for ph in range(6):
+            c = OktCounters()
+            L.okt_ledger(comm, ph, ctypes.byref(c))
+            out.append(c.bytes_recv)
+        return out
+
     fresh_start()
+    gen(scratch, 1)
+    step_async(scratch, 1)
+    wait()
+    nprof = max(1, min(args.steps - 1, 8))
     L.okt_set_profiling(comm, 1)
     L.okt_reset_phase_times(comm)
-    nprof = min(args.steps, 8)
-    for tp in range(1, nprof + 1):
+    lb0 = ledger_bytes()
+    for tp in range(2, nprof + 2):
         gen(scratch, tp)
         if fl:
             with torch.cuda.stream(stream):
@@ -467,6 +482,7 @@ def run_okt(args):
         step_async(scratch, tp)
         wait()
     barrier()
+    lb1 = ledger_bytes()
     ms_t = (ctypes.c_double * OKT_T_COUNT)()
     calls = (ctypes.c_uint64 * OKT_T_COUNT)()
     byts = (ctypes.c_double * OKT_T_COUNT)()
@@ -474,6 +490,21 @@ def run_okt(args):
     L.okt_phase_bytes(comm, byts)
     L.okt_set_profiling(comm, 0)
     phases = {nm: round(ms_t[i] / max(1, nprof), 4) for i, nm in enumerate(TIMER_NAMES)}
+    # NVLink: bytes received per steady step in the split exchange (merge
+    # kernel: the peers' K1 entries of my region) and in balance + allgatherv
+    # (pull kernel: the peers' survivors), over each phase's device time
+    nvl = None
+    if P > 1:
+        dsplit = (lb1[0] - lb0[0]) / nprof                          # OKT_PHASE_SPLIT
+        dgath = ((lb1[1] - lb0[1]) + (lb1[2] - lb0[2])) / nprof     # OKT_PHASE_BALANCE + OKT_PHASE_ALLGATHERV
+        tm, ta = phases.get("merge") or 0.0, phases.get("allgather") or 0.0
+        nvl = {"peak_gbs_per_direction": 900.0,
+               "merge": {"bytes_recv_per_step": dsplit, "ms": tm,
+                         "gbs": dsplit / (tm * 1e-3) / 1e9 if tm > 0 else None},
+               "pull": {"bytes_recv_per_step": dgath, "ms": ta,
+                        "gbs": dgath / (ta * 1e-3) / 1e9 if ta > 0 else None},
+               "note": "rank 0, steady device-driven steps t = 2..1+nprof; bytes from the ledger (8 B per split "
+                       "entry, 12 B per u entry), time = the phase's CUDA events (kernel incl. its flag waits)"}
     ik1 = TIMER_NAMES.index("k1")
     k1_ms, k1_bytes, k1_calls = ms_t[ik1], byts[ik1], calls[ik1]
     # ---- end-to-end through the synchronous host-buffer C-ABI call (the
@@ -588,11 +619,12 @@ def run_okt(args):
                              "traffic_source": traffic_src, "peak_source": peak_src,
                              "bytes_per_launch": k1_bytes / max(1, k1_calls),
                              "us_per_launch": 1e3 * k1_ms / max(1, k1_calls), "launches": int(k1_calls),
-                             "timed_over": f"t = 1..{nprof} (profiled pass, CUDA events around every K1 launch)",
+                             "timed_over": f"steady t = 2..{nprof + 1} (profiled pass, CUDA events around every K1 launch)",
                              "bytes_formula": "12n + 8e per EF step (read g, eps; write eps - P = 1: stored as 0 "
                                               "at u's entries -; 8 B per staged entry e); refresh steps add a "
                                               "4n + 8m select pass"},
                 "phases_ms_per_step": phases,
+                "nvlink": nvl,
                 # dense-equivalent bandwidth, comparable to an allreduce's busBw
                 "dense_equivalent_gbs": 2 * 4 * n * (P - 1) / P / (value * 1e-3) / 1e9 if P > 1 else None,
                 "avg_U": statistics.mean(U), "avg_local_selected": statistics.mean(M),
