@@ -571,6 +571,9 @@ cudaError_t launch_k1(Launch& L, const Stage& S, K1Mode mode, const float* g, co
     case K1Mode::kAccumHist:
       return k1_dispatch<true, false, true, false>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out, d_m,
                                                    d_m2, d_flags, d_hist, ap, pub, ind);
+    case K1Mode::kAccumSelectHist:
+      return k1_dispatch<true, true, true, false>(L, S, vec, g, eps_in, eps_out, alpha, n, d_th, d_th2, out, d_m,
+                                                  d_m2, d_flags, d_hist, ap, pub, ind);
   }
   return cudaErrorInvalidValue;
 }

@@ -26,7 +26,7 @@ struct RadixState {
   uint32_t pad;
 };
 
-enum class K1Mode { kSelect, kAccumSelect, kAccumHist };
+enum class K1Mode { kSelect, kAccumSelect, kAccumHist, kAccumSelectHist };
 enum class RadixSrc { kDenseF32, kAosF32, kF64 };
 
 // Phase-A staging of the two-phase compactions (okt_device.cuh).
@@ -100,6 +100,7 @@ struct Segs {
 //   kSelect       acc = g,                       emit {|acc| >= th}
 //   kAccumSelect  acc = fma(alpha, g, eps_in) -> eps_out, emit {|acc| >= th}
 //   kAccumHist    acc = fma(alpha, g, eps_in) -> eps_out, radix pass-0 histogram
+//   kAccumSelectHist  both: emit {|acc| >= th} (refresh candidates) + the histogram
 // With d_th2 (dual threshold) the emitted set is {|acc| >= max(th, th2)} and
 // *d_m2 receives |{|acc| >= th}| (P = 1 steady state: u straight from K1).
 // Sets bit 0 of *d_flags on any non-finite accumulator.
