@@ -476,6 +476,9 @@ def run_okt(args):
     lb0 = ledger_bytes()
     for tp in range(2, nprof + 2):
         gen(scratch, tp)
+        barrier()
+        if world > 1:
+            L.okt_device_barrier(comm, sp)  # (host-side generation skews the ranks: align them first)
         if fl:
             with torch.cuda.stream(stream):
                 flush.fill_(tp & 0xff)

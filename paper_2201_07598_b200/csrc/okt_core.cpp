@@ -213,6 +213,7 @@ struct okt_comm {
   // device-driven multi-GPU exchange (okt_p2p.cuh)
   bool p2p_checked = false, p2p = false;
   Buf win, boot, tabd, selflags, trbuf;
+  Buf ubits[2];  // EF P2P steps: u membership bitmaps by step parity (zero between uses)
   const float* cur_acc = nullptr;  // the step's accumulator / model (P2P fused apply)
   float* cur_w = nullptr;
   size_t win_n = 0;
@@ -778,6 +779,15 @@ struct okt_comm {
     if ((rc = ck(cudaMemcpy(tabd.p, &tab, sizeof(okt::PeerTab), cudaMemcpyHostToDevice), "tab"))) return rc;
     if ((rc = ensure(indexes, 4 * std::max<size_t>(n, 1)))) return rc;
     if ((rc = ensure(selflags, std::max<size_t>(n, 1)))) return rc;
+    for (Buf& b : ubits) {
+      b.zero_init = true;
+      if (b.p && b.cap < 4 * ((n + 127) / 128 * 4)) {
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+      }
+      if ((rc = ensure(b, 4 * ((n + 127) / 128 * 4)))) return rc;  // (whole uint4 words)
+    }
     win_n = n;
     return OKT_OK;
   }
@@ -830,6 +840,7 @@ struct okt_comm {
     }
     tmark(OKT_T_SELECT, s);
     okt::K1P2P kp = k1p2p_args(argfed);
+    kp.zero_sel = sgd ? 1 : 0;
     if (!rc)
       rc = ck(okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, hup->sp.g,
                              hup->sp.eps_in, hup->sp.eps_out, hup->sp.alpha, n, &d()->local_th, nullptr,
@@ -856,10 +867,18 @@ struct okt_comm {
     // oktopk_sgd_step reports no index list (trainer.hpp:123-127): only the
     // plain allreduce needs the sel flags and the indexes compaction.
     pa.sel = sgd ? nullptr : selflags.as<uint8_t>();
+    if (sgd) {
+      pa.ubits[0] = ubits[0].as<uint32_t>();
+      pa.ubits[1] = ubits[1].as<uint32_t>();
+    }
     if (!rc) rc = ck(okt::launch_p2p_allgatherv(L, dt, sp, &d()->S, dp, &d()->U, fl, kP2PTimeoutNs, pa,
                                                 sgd ? hp2p_dev : nullptr, S.tile_ctr + 4),
                      "p2p");
-    if (!sgd) {
+    if (sgd) {
+      tmark(OKT_T_APPLY, s);
+      if (!rc) rc = ck(okt::launch_p2p_restore(L, dt, sp, ubits[0].as<uint32_t>(), ubits[1].as<uint32_t>(), n,
+                                               argfed ? d()->p2pflags : nullptr, fl), "restore");
+    } else {
       tmark(OKT_T_APPLY, s);
       if (!rc) rc = ck(okt::launch_select_flags(L, S, selflags.as<uint8_t>(), dt, sp, &d()->U, win_n,
                                                 indexes.as<uint32_t>(), &d()->nidx, &d()->flags), "indexes");
@@ -915,6 +934,7 @@ struct okt_comm {
         const void* fm = okt::p2p_merge_func(P);
         const void* fp = okt::p2p_pull_func();
         const void* ft = okt::p2p_totals_func();
+        const void* fr = okt::p2p_restore_func();
         for (cudaGraphNode_t nd : nodes) {
           cudaGraphNodeType ty;
           cudaGraphNodeGetType(nd, &ty);
@@ -923,7 +943,7 @@ struct okt_comm {
           cudaGraphKernelNodeGetParams(nd, &kp);
           if (kp.func == fm) G.merge = nd;
           else if (kp.func == fp) G.pull = nd;
-          else if (kp.func != ft) G.k1 = nd;
+          else if (kp.func != ft && kp.func != fr) G.k1 = nd;
         }
       }
       const cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
@@ -952,6 +972,7 @@ struct okt_comm {
       // the merge's and the pull's flag word (arguments 7 and 5)
       uint32_t* fl = &d()->p2pflags[hup->sp.par];
       okt::K1P2P kp = k1p2p_args(true);
+      kp.zero_sel = 1;
       if ((rc = patch_node(G.exec, G.k1, kK1Args, {{0, &hup->sp.g}, {1, &hup->sp.eps_in}, {2, &hup->sp.eps_out},
                                               {3, &hup->sp.alpha}, {12, &fl}, {15, &kp}})) ||
           (rc = patch_node(G.exec, G.merge, 9, {{7, &fl}})) || (rc = patch_node(G.exec, G.pull, 10, {{5, &fl}})))
@@ -1761,7 +1782,7 @@ int okt_comm_init_nccl(okt_comm** out, int rank, int P, int device, const void* 
   ncclComm_t nc = nullptr;
   // Non-blocking communicator: every later wait on it is bounded (okt_transport.hpp).
   ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
-  cfg.blocking = 0;
+  cfg.blocking = std::getenv("OKT_NCCL_BLOCKING") ? 1 : 0;  // (diagnostics A/B: a blocking communicator)
   ncclResult_t r = ncclCommInitRankConfig(&nc, P, id, rank, &cfg);
   if (r == ncclInProgress) r = okt::NcclTransport::settle(nc, std::max(120000L, okt::NcclTransport::timeout_from_env()));
   if (r != ncclSuccess) {

@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
           a[j][3] = fmaf(alpha, gv[j].w, ev[j].w);
           const uint64_t e0 = base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C;
           float4 st = make_float4(a[j][0], a[j][1], a[j][2], a[j][3]);
-          if (APPLY) {  // the residual of an entry of u is 0 (trainer.cpp:478-479)
+          if (APPLY || (p2p_on && p2p.zero_sel)) {  // the residual of an entry of u / the local selection is 0
             if (fabsf(st.x) >= tf) st.x = 0.f;
             if (fabsf(st.y) >= tf) st.y = 0.f;
             if (fabsf(st.z) >= tf) st.z = 0.f;

@@ -176,6 +176,10 @@ cudaError_t launch_p2p_merge(Launch& L, const PeerTab* d_tab, const StepPtrs* sp
 const void* p2p_merge_func(int P);
 const void* p2p_pull_func();
 const void* p2p_totals_func();
+const void* p2p_restore_func();
+// EF steps after the pull: acc back at the local entries outside u; clears the next step's u bitmap.
+cudaError_t launch_p2p_restore(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, uint32_t* ub0, uint32_t* ub1,
+                               uint64_t n, const uint32_t* flags2, const uint32_t* d_flags);
 // Waits for every rank's survivors, plans (offsets / balance), pulls u.
 cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, uint64_t* d_S,
                                   P2PPlan* plan, uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns,

@@ -61,6 +61,16 @@ __device__ __forceinline__ uint32_t span_at(uint32_t c, uint32_t tiles, uint32_t
   return uint32_t(qv);
 }
 
+// floor(len * p / q) for q <= 64 (no 64-bit division subroutine).
+__device__ __forceinline__ uint64_t frac_at(uint64_t len, uint32_t p, uint32_t q) {
+  if (len < (1ull << 26)) return uint32_t(len) * p / q;
+  const uint64_t m = len * p;
+  uint64_t v = uint64_t(double(m) / double(q));
+  if (v * q > m) --v;
+  else if ((v + 1) * q <= m) ++v;
+  return v;
+}
+
 // 16-byte async copy, L2 only (.cg: no L1 line of a peer's buffer survives
 // into a later step that reuses the same parity slot).
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
@@ -259,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
 // owner's window to their stream position in my u (unbalanced: all of u;
 // balanced: my block, then — after every owner's block is complete — the
 // other blocks from their owners' u).  K7 runs on each entry as it lands.
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
     p2p_pull_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, uint64_t* d_S, P2PPlan* plan,
                     uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns, P2PApply ap, P2PHostOut* hout,
                     uint32_t* done) {
@@ -271,6 +281,7 @@ __global__ void __launch_bounds__(kThreads)
   const int par = sp->par;
   float* acc = ap.on ? (ap.sgd ? sp->eps_out : const_cast<float*>(sp->g)) : nullptr;
   float* wm = (ap.on && ap.sgd) ? sp->w : nullptr;
+  uint32_t* const ubits = (ap.on && ap.sgd) ? (sp->par ? ap.ubits[1] : ap.ubits[0]) : nullptr;
   const int P = tab->P, me = tab->rank, q = threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t* const trace = tab->trace;
@@ -421,7 +432,7 @@ __global__ void __launch_bounds__(kThreads)
     float av[R], wv[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      av[k] = (acc && ok[k]) ? acc[i[k]] : 0.f;
+      av[k] = (acc && !ubits && ok[k]) ? acc[i[k]] : 0.f;
       wv[k] = (wm && ok[k]) ? wm[i[k]] : 0.f;
     }
 #pragma unroll
@@ -429,7 +440,14 @@ __global__ void __launch_bounds__(kThreads)
       if (!ok[k]) continue;
       ui[pos[k]] = i[k];
       uv[pos[k]] = v[k];
-      if (acc) {
+      if (ubits) {
+        // EF step: the residual was settled by K1 (local selection stored as
+        // 0) and is fixed up by the restore kernel; mark u's entry
+        atomicOr(&ubits[i[k] >> 5], 1u << (i[k] & 31u));
+        const float nw = float(double(wv[k]) - v[k] / dP);
+        wm[i[k]] = nw;
+        bad |= (__float_as_uint(nw) & 0x7f800000u) == 0x7f800000u;
+      } else if (acc) {
         // K7 (oktopk.cpp:299-302, trainer.cpp:437-442, 478-479) on the entry.
         const bool sel = fabsf(av[k]) >= tf;
         if (wm) {
@@ -457,7 +475,7 @@ __global__ void __launch_bounds__(kThreads)
       const uint64_t base = s_off[r] + tab->spre[r][par][c];
       const uint64_t end = base + tab->scnt[r][par][c];
       const uint64_t len = end - base;
-      const uint64_t lo = max(base + len * part / parts, a), hi = min(base + len * (part + 1) / parts, b);
+      const uint64_t lo = max(base + frac_at(len, part, parts), a), hi = min(base + frac_at(len, part + 1, parts), b);
       const uint64_t cbase = uint64_t(span_at(c, s_tiles[r], s_G[r])) * kMergeTile;
       const uint32_t* si = tab->sidx[r][par] + cbase;
       const double* sv = tab->sval[r][par] + cbase;
@@ -541,6 +559,46 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
   }
+}
+
+// EF steps, after the pull: the residual of every locally selected entry
+// outside u goes back to acc (K1 stored 0 for the whole local selection), so
+// eps ends as acc zeroed at indexes = local selection ∩ u (trainer.cpp:
+// 476-480, oktopk.cpp:299-302).  One warp per K1 tile of my staging; the u
+// bitmap of the next step is cleared on the way.
+__global__ void __launch_bounds__(kThreads)
+    p2p_restore_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, uint32_t* ub0, uint32_t* ub1,
+                       uint64_t nwords, const uint32_t* flags2, const uint32_t* d_flags) {
+  const int me = tab->rank, par = sp->par;
+  const uint32_t* ub = par ? ub1 : ub0;
+  uint32_t* ub_next = par ? ub0 : ub1;
+  const uint64_t gt = uint64_t(blockIdx.x) * kThreads + threadIdx.x, gstride = uint64_t(gridDim.x) * kThreads;
+  for (uint64_t w = gt; w < (nwords >> 2); w += gstride) reinterpret_cast<uint4*>(ub_next)[w] = make_uint4(0, 0, 0, 0);
+  for (uint64_t w = (nwords & ~uint64_t(3)) + gt; w < nwords; w += gstride) ub_next[w] = 0u;
+  const uint32_t fl = flags2 ? flags2[par] : *d_flags;
+  if (fl & kAbortBits) return;  // a failed step commits nothing
+  float* eps = sp->eps_out;
+  const uint32_t G = tab->hdr[me]->pub[par].k1_G;
+  const uint32_t* cnt = tab->kcnt[me][par];
+  const uint64_t* stg = tab->kstg[me][par];
+  const int lane = threadIdx.x & 31;
+  const uint64_t wid = gt >> 5, wstride = gstride >> 5;
+  for (uint64_t t = wid; t < G; t += wstride) {
+    const uint32_t c = cnt[t];
+    for (uint32_t j = lane; j < c; j += 32) {
+      const uint64_t e = stg[t * kK1Tile + j];
+      const uint32_t i = coo_idx(e);
+      if (!((ub[i >> 5] >> (i & 31u)) & 1u)) eps[i] = coo_val(e);
+    }
+  }
+}
+
+cudaError_t launch_p2p_restore(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, uint32_t* ub0, uint32_t* ub1,
+                               uint64_t n, const uint32_t* flags2, const uint32_t* d_flags) {
+  const int grid = L.sms * 4;
+  p2p_restore_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, ub0, ub1, (n + 31) / 32, flags2, d_flags);
+  ++L.launches;
+  return cudaGetLastError();
 }
 
 // okt_device_barrier: publish, then wait for every peer (one CTA).
@@ -646,5 +704,6 @@ const void* p2p_merge_func(int P) {
 }
 const void* p2p_pull_func() { return reinterpret_cast<const void*>(p2p_pull_kernel); }
 const void* p2p_totals_func() { return reinterpret_cast<const void*>(p2p_totals_kernel); }
+const void* p2p_restore_func() { return reinterpret_cast<const void*>(p2p_restore_kernel); }
 
 }  // namespace okt

@@ -119,6 +119,12 @@ struct P2PApply {
   int sgd = 0;                  // acc = sp->eps_out and w = sp->w; else acc = sp->g
   const double* d_local_th = nullptr;
   uint8_t* sel = nullptr;       // per u entry: 1 if in the local selection
+  // EF steps: u membership bitmaps (1 bit per coordinate, one per parity).
+  // The pull sets u's bits and leaves the residual alone (K1 already zeroed
+  // the local selection); the restore kernel then puts acc back at the local
+  // entries outside u — indexes = local selection ∩ u (oktopk.cpp:299-302)
+  // without a random gather of acc per entry of u.
+  uint32_t* ubits[2] = {nullptr, nullptr};
 };
 
 // What the host reads after a steady device-driven EF step, written by the
@@ -148,6 +154,9 @@ struct K1P2P {
   StepPtrs* sp_out = nullptr;
   P2PPlan* plan_zero = nullptr;
   StepPtrs spv{};
+  // EF steps: store the residual of every locally selected entry as 0 (the
+  // restore kernel puts acc back where the entry did not make it into u).
+  int zero_sel = 0;
 };
 struct K1Totals {  // where the local selection size / slice offsets go
   uint64_t* d_m = nullptr;

@@ -152,6 +152,8 @@ def _dead_peer_worker(rank, port, q):
         dist.barrier()
         if rank == 1:
             q.put((rank, "exited", None))
+            q.close()
+            q.join_thread()  # (os._exit skips the queue's feeder thread)
             os._exit(0)  # the peer dies before the t = 5 refresh
         time.sleep(0.5)
         t0 = time.time()
@@ -164,6 +166,8 @@ def _dead_peer_worker(rank, port, q):
                              ctypes.byref(res), None)
         dt2 = time.time() - t1
         q.put((rank, (rc, dt, err, rc2, dt2), None))
+        q.close()
+        q.join_thread()
         os._exit(0)  # (no collective teardown with a dead peer)
     except Exception:
         import traceback
