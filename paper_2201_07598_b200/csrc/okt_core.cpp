@@ -1782,7 +1782,13 @@ int okt_comm_init_nccl(okt_comm** out, int rank, int P, int device, const void* 
   ncclComm_t nc = nullptr;
   // Non-blocking communicator: every later wait on it is bounded (okt_transport.hpp).
   ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
-  cfg.blocking = std::getenv("OKT_NCCL_BLOCKING") ? 1 : 0;  // (diagnostics A/B: a blocking communicator)
+  // Blocking by default: a non-blocking communicator made every
+  // host-synchronised refresh 3-5x slower (VGG N = 2: 1.8-2.7 vs 0.56 ms per
+  // refresh; round-2 A/B).  The waits on the stream stay bounded either way
+  // (NcclTransport::wait aborts the communicator at the deadline); only a
+  // peer dying inside an enqueue call itself (first-use connection setup)
+  // needs OKT_NCCL_NONBLOCKING=1.
+  cfg.blocking = std::getenv("OKT_NCCL_NONBLOCKING") ? 0 : 1;
   ncclResult_t r = ncclCommInitRankConfig(&nc, P, id, rank, &cfg);
   if (r == ncclInProgress) r = okt::NcclTransport::settle(nc, std::max(120000L, okt::NcclTransport::timeout_from_env()));
   if (r != ncclSuccess) {

@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
             x = g[e];
             if (ACCUM) {
               x = fmaf(alpha, x, eps_in[e]);
-              eps_out[e] = (APPLY && fabsf(x) >= tf) ? 0.f : x;
+              eps_out[e] = ((APPLY || (p2p_on && p2p.zero_sel)) && fabsf(x) >= tf) ? 0.f : x;
             }
             bad |= nonfinite(x);
           }

@@ -181,13 +181,15 @@ class LocalTransport final : public Transport {
   cudaEvent_t ev_;
 };
 
-// Non-blocking NCCL communicator (ncclConfig_t::blocking = 0): every call
-// returns at once, and every host wait on the library's stream is bounded.  A
+// NCCL communicator with bounded host waits: every wait on the library's
+// stream polls it against a deadline (OKT_NCCL_TIMEOUT_MS, default 60 s).  A
 // peer that dies (or never arrives) inside a collective leaves the NCCL kernel
-// spinning; after the deadline (OKT_NCCL_TIMEOUT_MS, default 60 s) the comm is
-// aborted (ncclCommAbort ends the kernels) and the call reports
-// TransportError — the role the reference's InprocTransport::close() plays
-// for its blocked waiters (proj/core/src/inproc.cpp:54-61).
+// spinning; at the deadline the comm is aborted (ncclCommAbort ends the
+// kernels) and the call reports TransportError — the role the reference's
+// InprocTransport::close() plays for its blocked waiters
+// (proj/core/src/inproc.cpp:54-61).  The communicator is blocking by default
+// (okt_comm_init_nccl); calls that return ncclInProgress on a non-blocking
+// one (OKT_NCCL_NONBLOCKING=1) are settled against the same deadline.
 class NcclTransport final : public Transport {
  public:
   explicit NcclTransport(ncclComm_t c) : c_(c), timeout_ms_(timeout_from_env()) {}
