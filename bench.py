@@ -101,7 +101,7 @@ def dump_p2p_trace(L, comm, rank, outdir):
     used = a[:, :, 0] > 0
     t0 = a[0, :, 0][used[0]].min() if used[0].any() else 0
     out = {}
-    for k, nm in enumerate(["k1", "merge", "compact", "pull0", "pull1", "publish_l", "publish_sur"]):
+    for k, nm in enumerate(["k1", "merge", "compact_or_restore", "pull0", "pull1", "publish_l", "publish_sur"]):
         u = used[k]
         if not u.any():
             continue

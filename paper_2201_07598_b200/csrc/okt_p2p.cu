@@ -40,14 +40,15 @@ constexpr uint32_t kAbortBits = 1u | 8u | 16u;  // local non-finite, peer timeou
 // on the GPU for tens of microseconds; tools/p2p_noise.cu.)
 constexpr int kMergeTile = kK1Tile;              // coordinates per CTA tile
 constexpr int kMergePer = kMergeTile / kThreads;  // 16 coordinates per thread in the scan
-constexpr int kMergeStages = 4;                   // tiles of entries in flight per CTA
+template <int P>
+__host__ __device__ constexpr int merge_stages() { return P <= 4 ? 6 : 4; }  // tiles of entries in flight per CTA
 constexpr int kMergeRing = 128;                   // entries per source per ring stage
 constexpr int kMergeCntCap = 256;                 // tiles whose counts are staged at once
 
 template <int P>
-constexpr size_t merge_smem() {  // mask bytes, values [P][tile], ring [S][P][kMergeRing], counts
+__host__ __device__ constexpr size_t merge_smem() {  // mask bytes, values [P][tile], ring [S][P][kMergeRing], counts
   return size_t(kMergeTile) + size_t(P) * kMergeTile * sizeof(float) +
-         size_t(kMergeStages) * P * kMergeRing * sizeof(uint64_t) + size_t(kMergeCntCap) * P * sizeof(uint32_t);
+         size_t(merge_stages<P>()) * P * kMergeRing * sizeof(uint64_t) + size_t(kMergeCntCap) * P * sizeof(uint32_t);
 }
 
 // First tile of span c when `tiles` tiles are split evenly over G spans.
@@ -148,17 +149,19 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
   // capacity), count in out_cnt[blockIdx.x] — a few hundred large chunks per
   // rank for the pull instead of one small chunk per tile.  The span's
   // per-source counts are staged in shared memory first (all loads in flight
-  // at once), then a kMergeStages-deep cp.async ring keeps the entries of the
+  // at once), then a kS-deep cp.async ring keeps the entries of the
   // next tiles of every source in flight over NVLink while a tile is merged
   // (the first kMergeRing entries of a tile per source; a denser tile's rest
   // is read directly).  Round 1 kept one tile in flight: 6.8 us per tile at
   // n = 340M, P = 4, almost all of it NVLink latency.
   uint64_t* const ring = reinterpret_cast<uint64_t*>(s_val + P * kMergeTile);    // [S][P][kMergeRing]
-  uint32_t* const s_cnt = reinterpret_cast<uint32_t*>(ring + kMergeStages * P * kMergeRing);  // [kMergeCntCap][P]
+  constexpr int kS = merge_stages<P>();
+  uint32_t* const s_cnt = reinterpret_cast<uint32_t*>(ring + kS * P * kMergeRing);  // [kMergeCntCap][P]
   const uint32_t j0 = span_at(blockIdx.x, ntiles, gridDim.x);
   const uint32_t my_n = span_at(blockIdx.x + 1, ntiles, gridDim.x) - j0;
   const uint64_t out_base = uint64_t(j0) * kMergeTile;
   uint32_t running = 0;  // survivors of this CTA so far (block-uniform)
+  for (int w = q; w < kMergeTile / 16; w += kThreads) reinterpret_cast<uint4*>(s_mask)[w] = make_uint4(0, 0, 0, 0);
   for (uint32_t i0 = 0; i0 < my_n; i0 += kMergeCntCap) {
     const uint32_t ni = min(my_n - i0, uint32_t(kMergeCntCap));
     for (uint32_t x = q; x < ni * P; x += kThreads) {
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
     auto issue = [&](uint32_t i) {  // ring stage i % S <- tile i's first entries, every source
       if (i < ni) {
         const uint64_t base = uint64_t(t_lo + j0 + i0 + i) * kMergeTile;
-        uint64_t* slot = ring + (i % kMergeStages) * (P * kMergeRing);
+        uint64_t* slot = ring + (i % kS) * (P * kMergeRing);
         // entry pairs (16 B; a tile's staging slot starts 16-byte aligned and
         // holds kMergeTile entries, so the odd count's partner is in bounds)
         for (int x = q; x < P * kMergeRing / 2; x += kThreads) {
@@ -181,15 +184,14 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
       cp_async_commit();  // (empty groups keep the group count uniform)
     };
 #pragma unroll
-    for (int st = 0; st < kMergeStages - 1; ++st) issue(uint32_t(st));
+    for (int st = 0; st < kS - 1; ++st) issue(uint32_t(st));
     for (uint32_t i = 0; i < ni; ++i) {
-      cp_async_wait<kMergeStages - 2>();
-      for (int w = q; w < kMergeTile / 4; w += kThreads) s_mask[w] = 0;
-      __syncthreads();  // stage i landed everywhere; the slot of tile i - 1 is free
-      issue(i + kMergeStages - 1);
+      cp_async_wait<kS - 2>();
+      __syncthreads();  // stage i landed everywhere; the slot of tile i - 1 is free; tile i - 1 is emitted
+      issue(i + kS - 1);
       const uint32_t t = t_lo + j0 + i0 + i;
       const uint64_t base = uint64_t(t) * kMergeTile;
-      const uint64_t* slot = ring + (i % kMergeStages) * (P * kMergeRing);
+      const uint64_t* slot = ring + (i % kS) * (P * kMergeRing);
 #pragma unroll
       for (int r = 0; r < P; ++r) {
         uint32_t got = 0;
@@ -211,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
       // bracket scan + filter over the tile: thread q owns coordinates
       // [16 q, 16 q + 16) (four mask words)
       const uint4 mw4 = reinterpret_cast<const uint4*>(s_mask)[q];
+      reinterpret_cast<uint4*>(s_mask)[q] = make_uint4(0, 0, 0, 0);  // (this thread's words: clear for the next tile)
       auto bits_of = [&](int k) {  // source bits of coordinate k (select tree: no local memory)
         const int jj = k >> 2;
         const uint32_t w = (jj & 2) ? ((jj & 1) ? mw4.w : mw4.z) : ((jj & 1) ? mw4.y : mw4.x);
@@ -253,7 +256,8 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
         out_val[pos] = bracket_regs<P>(v, bits_of(k));
       }
       running += total;
-      __syncthreads();  // s_mask / s_val / s_wt / the ring slot reused by later tiles
+      // (no barrier here: the next tile's first barrier separates this emit
+      // from its scatter; s_wt is rewritten only after its second one)
     }
     cp_async_wait<0>();
     __syncthreads();
@@ -570,6 +574,7 @@ __global__ void __launch_bounds__(kThreads)
     p2p_restore_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, uint32_t* ub0, uint32_t* ub1,
                        uint64_t nwords, const uint32_t* flags2, const uint32_t* d_flags) {
   const int me = tab->rank, par = sp->par;
+  if (threadIdx.x == 0) trace_stamp(tab->trace, kTrCompact, 0);  // (diagnostics: the restore uses the compact slot)
   const uint32_t* ub = par ? ub1 : ub0;
   uint32_t* ub_next = par ? ub0 : ub1;
   const uint64_t gt = uint64_t(blockIdx.x) * kThreads + threadIdx.x, gstride = uint64_t(gridDim.x) * kThreads;
@@ -591,6 +596,7 @@ __global__ void __launch_bounds__(kThreads)
       if (!((ub[i >> 5] >> (i & 31u)) & 1u)) eps[i] = coo_val(e);
     }
   }
+  if (lane == 0) trace_stamp(tab->trace, kTrCompact, 2);
 }
 
 cudaError_t launch_p2p_restore(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, uint32_t* ub0, uint32_t* ub1,
