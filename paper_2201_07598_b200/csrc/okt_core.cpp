@@ -1332,7 +1332,7 @@ struct okt_comm {
         // radix passes and a second select pass over all n (at n = 340M:
         // 0.39 + 0.43 ms).  Otherwise the dense passes below run as before
         // (pass 0's histogram came out of the same K1 pass).
-        const bool cand = P == 1 && cand_on && st.local_th > 0.0 && std::isfinite(st.local_th);
+        const bool cand = cand_on && st.local_th > 0.0 && std::isfinite(st.local_th);
         if (cand) {
           if (!rc) rc = upload_f64(&d()->th_arg, 0.5 * st.local_th, &hup->th_arg, s);
           if (!rc) rc = ck(okt::launch_k1(L, S, okt::K1Mode::kAccumSelectHist, g, eps_in, eps_out, fa, n,
@@ -1340,12 +1340,23 @@ struct okt_comm {
                                           &d()->flags, hp), "k1");
           if (!rc) rc = sync(s);
           if (rc) return abort_step(rc);
-          if (h->flags & 1u) {
+          if (P == 1 && (h->flags & 1u)) {  // (P > 1: the split's counts exchange tells every rank)
             dev_stale = true;
             return set_err(OKT_ERR_NUMERIC, "ok_sparse_allreduce: non-finite input");
           }
           const uint64_t C = h->R;
-          if (C >= k) {
+          if (C >= k && P > 1) {
+            // the local selection {|acc| >= local_th} = the qualifying candidates, as AoS for the split
+            tmark(OKT_T_THRESHOLD, s);
+            rc = ck(cudaMemsetAsync(hp, 0, 2048 * sizeof(uint32_t), s), "memset");
+            if (!rc) rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kAosF32, coo.p, 0, &d()->R, C, k, &d()->rs,
+                                                      hp, &d()->local_th, false), "radix");
+            tmark(OKT_T_SELECT, s);
+            if (!rc) rc = ck(okt::launch_filter(L, S, true, coo.as<uint64_t>(), nullptr, nullptr, &d()->R, C,
+                                                &d()->local_th, nullptr, nullptr, &d()->m, nullptr,
+                                                coo.as<uint64_t>()), "filter");
+            sel_done = true;
+          } else if (C >= k) {
             tmark(OKT_T_THRESHOLD, s);
             rc = ck(cudaMemsetAsync(hp, 0, 2048 * sizeof(uint32_t), s), "memset");
             if (!rc) rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kAosF32, coo.p, 0, &d()->R, C, k, &d()->rs,
@@ -1380,6 +1391,7 @@ struct okt_comm {
       }
       if (!sel_done) tmark(OKT_T_SELECT, s);
       if (sel_done) {
+        // (the candidate path produced u (P = 1) or the local selection (P > 1))
       } else if (P == 1) {
         // One rank: the region is the local selection {|acc| >= local_th}, so
         // its k-th largest magnitude (the global refresh, oktopk.cpp:277-293)

@@ -68,7 +68,7 @@ size_t stage_entries(uint64_t count, int tile, int max_chunks) {
 // Phase B: chunk prefix + copy to final positions
 // =============================================================================
 // MODE 0: AoS u64 -> AoS u64; 1: AoS u64 -> SoA (u32, f32 widened to f64);
-//      2: SoA -> SoA; 3: u32 -> u32.
+//      2: SoA -> SoA; 3: u32 -> u32; 4: SoA (u32, f64 holding an f32) -> AoS u64.
 constexpr int kCompactBatch = 4;
 
 // A CTA copies a group of consecutive chunks (up to kThreads; one chunk per
@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(kThreads)
       if (j < cnt) {
         const uint64_t sj = src_of(j);
         if (MODE == 0 || MODE == 1) e64[b] = s64[sj];
-        if (MODE == 2 || MODE == 3) ei[b] = sidx[sj];
-        if (MODE == 2) ev[b] = sval[sj];
+        if (MODE == 2 || MODE == 3 || MODE == 4) ei[b] = sidx[sj];
+        if (MODE == 2 || MODE == 4) ev[b] = sval[sj];
       }
     }
 #pragma unroll
@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(kThreads)
       const uint64_t j = j0 + uint64_t(b) * kThreads;
       if (j >= cnt) continue;
       if (MODE == 0) o64[pre + j] = e64[b];
+      else if (MODE == 4) o64[pre + j] = coo_pack(ei[b], float(ev[b]));
       else if (MODE == 3) oidx[pre + j] = ei[b];
       else {
         oidx[pre + j] = ei[b];
@@ -640,7 +641,8 @@ __global__ void __launch_bounds__(kThreads)
 
 cudaError_t launch_filter(Launch& L, const Stage& S, bool aos, const uint64_t* in_aos, const uint32_t* in_idx,
                           const double* in_val, const uint64_t* d_cnt_in, uint64_t bound, const double* d_th,
-                          uint32_t* out_idx, double* out_val, uint64_t* d_cnt_out, const ApplyArgs* ap) {
+                          uint32_t* out_idx, double* out_val, uint64_t* d_cnt_out, const ApplyArgs* ap,
+                          uint64_t* out_aos) {
   static std::atomic<int> cap_a{0}, cap_s{0};
   std::atomic<int>& cap = aos ? cap_a : cap_s;
   if (!cap) cap = aos ? resident_ctas(filter_kernel<true>, kThreads, L.sms)
@@ -655,6 +657,7 @@ cudaError_t launch_filter(Launch& L, const Stage& S, bool aos, const uint64_t* i
   ++L.launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (out_aos) return launch_compact<4>(L, S, G, 0, S.chunk_cap, 0, out_aos, nullptr, nullptr, d_cnt_out, nullptr, ap);
   return launch_compact<2>(L, S, G, 0, S.chunk_cap, 0, nullptr, out_idx, out_val, d_cnt_out, nullptr, ap);
 }
 

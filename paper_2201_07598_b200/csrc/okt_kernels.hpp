@@ -123,12 +123,14 @@ cudaError_t launch_radix_init(Launch& L, RadixState* d_rs, uint64_t k, uint64_t 
                               const uint64_t* d_n);
 
 // Survivor filter: {(i, v) : |v| >= *d_th} of a COO list whose length lives in
-// device memory.  Input is AoS (u32 idx, f32 val) or SoA (u32, f64).
+// device memory.  Input is AoS (u32 idx, f32 val) or SoA (u32, f64); output SoA, or AoS when out_aos
+// (f32 values only).
 cudaError_t launch_filter(Launch& L, const Stage& S, bool aos, const uint64_t* in_aos,
                           const uint32_t* in_idx, const double* in_val,
                           const uint64_t* d_cnt_in, uint64_t bound, const double* d_th,
                           uint32_t* out_idx, double* out_val, uint64_t* d_cnt_out,
-                          const ApplyArgs* ap = nullptr);
+                          const ApplyArgs* ap = nullptr,
+                          uint64_t* out_aos = nullptr);
 
 // K7: for each (i, v) of u: sel = |acc[i]| >= local_th; if w: w[i] -= v / P;
 // if zero_eps && sel: acc[i] = 0; emit i into indexes when sel.
