@@ -113,6 +113,12 @@ def dump_p2p_trace(L, comm, rank, outdir):
                    "waited_max_us": float(wt.max()) / 1e3 if wt.size else None,
                    "end_med_us": float(np.median(en)) / 1e3 if en.size else None,
                    "end_max_us": float(en.max()) / 1e3 if en.size else None}
+    # merge-kernel phase sums per CTA (ns, thread 0: ring wait / scatter / scan / emit), in kind 4's slots
+    ph = a[4][(a[4] > 0).any(axis=1)]
+    if ph.size and "merge" in out:
+        out["merge_phase_us_median_per_cta"] = {nm: float(np.median(ph[:, i])) / 1e3
+                                                for i, nm in enumerate(["wait", "scatter", "scan", "emit"])}
+        out.pop("pull1", None)
     os.makedirs(outdir, exist_ok=True)
     np.save(os.path.join(outdir, f"p2p_trace_rank{rank}.npy"), a)
     with open(os.path.join(outdir, f"p2p_trace_rank{rank}.json"), "w") as f:

@@ -402,7 +402,7 @@ struct okt_comm {
   int wait_stream(cudaStream_t s) {
     std::string err;
     const int rc = tr ? tr->wait(s, err) : ck(cudaStreamSynchronize(s), "device");
-    if (rc && tr) return set_err(rc, err);
+    if (rc && tr) return comm_err(rc, err);
     return rc;
   }
   int ck(cudaError_t e, const char* what) {
@@ -436,9 +436,14 @@ struct okt_comm {
   }
 
   int comm_err(int rc, const std::string& err) {
+    if (rc == OKT_ERR_TRANSPORT) dead = true;  // a closed world / aborted communicator stays failed
     if (rc == OKT_ERR_TRANSPORT && world) return set_err(rc, "TransportError: " + err);
     return set_err(rc, err);
   }
+  // Set by a transport failure (world closed, NCCL communicator aborted, a
+  // peer that timed out): every later collective call fails at once with
+  // TransportError, as calls on a closed InprocTransport do (inproc.cpp:54-61).
+  bool dead = false;
 
   // ---- phases -----------------------------------------------------------------------
   // space_repartition from a selected index list (oktopk.cpp:28-61).  Cuts land
@@ -1211,6 +1216,7 @@ struct okt_comm {
     }
     if (n == 0 || k < 1 || t < 1)
       return set_err(OKT_ERR_INVALID_ARGUMENT, "ok_sparse_allreduce: empty input, k < 1, or t < 1");
+    if (dead && P > 1) return set_err(OKT_ERR_TRANSPORT, "TransportError: the transport failed earlier (peer lost)");
     if (n > 0xffffffffull) return set_err(OKT_ERR_INVALID_ARGUMENT, "n exceeds the u32 index space");
     if (st.tau == 0 || st.tau_prime == 0)
       return set_err(OKT_ERR_INVALID_ARGUMENT, "tau and tau_prime must be >= 1");
@@ -1571,6 +1577,7 @@ struct okt_comm {
     }
     if (h->flags & 8u) {
       dev_stale = true;
+      dead = true;
       return set_err(OKT_ERR_TRANSPORT, "TransportError: a peer did not reach the exchange (timeout)");
     }
     if (h->flags & 16u) {

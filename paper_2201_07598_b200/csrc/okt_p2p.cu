@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
   const uint32_t my_n = span_at(blockIdx.x + 1, ntiles, gridDim.x) - j0;
   const uint64_t out_base = uint64_t(j0) * kMergeTile;
   uint32_t running = 0;  // survivors of this CTA so far (block-uniform)
+  uint64_t ph_acc[4] = {0, 0, 0, 0};  // diagnostics (trace on): ns in wait / scatter / scan / emit, thread 0
   for (int w = q; w < kMergeTile / 16; w += kThreads) reinterpret_cast<uint4*>(s_mask)[w] = make_uint4(0, 0, 0, 0);
   for (uint32_t i0 = 0; i0 < my_n; i0 += kMergeCntCap) {
     const uint32_t ni = min(my_n - i0, uint32_t(kMergeCntCap));
@@ -186,8 +187,11 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
 #pragma unroll
     for (int st = 0; st < kS - 1; ++st) issue(uint32_t(st));
     for (uint32_t i = 0; i < ni; ++i) {
+      uint64_t ph0 = 0;
+      if (trace && q == 0) ph0 = globaltimer_ns();
       cp_async_wait<kS - 2>();
       __syncthreads();  // stage i landed everywhere; the slot of tile i - 1 is free; tile i - 1 is emitted
+      if (trace && q == 0) ph_acc[0] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
       issue(i + kS - 1);
       const uint32_t t = t_lo + j0 + i0 + i;
       const uint64_t base = uint64_t(t) * kMergeTile;
@@ -210,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
         if (lane == 0 && got) atomicAdd(&s_seg[r], got);
       }
       __syncthreads();
+      if (trace && q == 0) ph_acc[1] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
       // bracket scan + filter over the tile: thread q owns coordinates
       // [16 q, 16 q + 16) (four mask words)
       const uint4 mw4 = reinterpret_cast<const uint4*>(s_mask)[q];
@@ -239,6 +244,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
       }
       if (lane == 31) s_wt[warp] = incl;
       __syncthreads();
+      if (trace && q == 0) ph_acc[2] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
       uint32_t wpre = 0, total = 0;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) {
@@ -256,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
         out_val[pos] = bracket_regs<P>(v, bits_of(k));
       }
       running += total;
+      if (trace && q == 0) ph_acc[3] += globaltimer_ns() - ph0;
       // (no barrier here: the next tile's first barrier separates this emit
       // from its scatter; s_wt is rewritten only after its second one)
     }
@@ -263,6 +270,10 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
     __syncthreads();
   }
   if (q == 0) out_cnt[blockIdx.x] = running;
+  if (trace && q == 0 && blockIdx.x < kTraceCtas) {  // (the balanced pull's slots: free on merge-traced steps)
+    uint64_t* tp = trace + (uint64_t(kTrPull1) * kTraceCtas + blockIdx.x) * 4;
+    for (int x = 0; x < 4; ++x) tp[x] = ph_acc[x];
+  }
   if (q < P && s_seg[q]) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->seg_cnt[q]), (unsigned long long)s_seg[q]);
   if (lane == 0) trace_stamp(trace, kTrMerge, 2);
 }
@@ -353,12 +364,14 @@ __global__ void __launch_bounds__(kThreads, 3)
       if (q == 0) trace_stamp(trace, kTrPubSur, 3);
     }
     // every CTA: wait on its own flag copies, read the ranks' survivor counts
-    // and geometry, derive the plan (CTA 0 also stores it for the host)
+    // and geometry, derive the plan (CTA 0 also stores it for the host).  A
+    // step that already failed (its merge timed out on a dead peer) does not
+    // wait again: its own abort status went out with the publication above.
     if (q < P) {
       uint64_t sz = 0;
       uint32_t G = 0, cap = 0;
       const FlagSlot* f = my_flag(tab->hdr[me], kFlagSurReady, q);
-      if (!wait_flag(&f->epoch, epoch, timeout_ns)) {
+      if (!wait_flag(&f->epoch, epoch, s_abort ? 0 : timeout_ns)) {
         atomicOr(d_flags, 8u);
         if (hout) hout->err_timeout = 1;
         s_abort = 1;
@@ -586,14 +599,41 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t G = tab->hdr[me]->pub[par].k1_G;
   const uint32_t* cnt = tab->kcnt[me][par];
   const uint64_t* stg = tab->kstg[me][par];
+  // A warp takes kRT tiles per round and keeps their loads in flight together
+  // (counts, then two entries per lane and tile, then the bitmap words): three
+  // memory round trips per round instead of three per tile.
+  constexpr int kRT = 4;
   const int lane = threadIdx.x & 31;
   const uint64_t wid = gt >> 5, wstride = gstride >> 5;
-  for (uint64_t t = wid; t < G; t += wstride) {
-    const uint32_t c = cnt[t];
-    for (uint32_t j = lane; j < c; j += 32) {
-      const uint64_t e = stg[t * kK1Tile + j];
-      const uint32_t i = coo_idx(e);
-      if (!((ub[i >> 5] >> (i & 31u)) & 1u)) eps[i] = coo_val(e);
+  for (uint64_t t0 = wid * kRT; t0 < G; t0 += wstride * kRT) {
+    uint32_t c[kRT];
+#pragma unroll
+    for (int x = 0; x < kRT; ++x) c[x] = t0 + x < G ? cnt[t0 + x] : 0u;
+    uint64_t e[kRT][2];
+#pragma unroll
+    for (int x = 0; x < kRT; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        const uint32_t j = lane + 32u * y;
+        e[x][y] = j < c[x] ? stg[(t0 + x) * kK1Tile + j] : ~0ull;
+      }
+    uint32_t bw[kRT][2];
+#pragma unroll
+    for (int x = 0; x < kRT; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) bw[x][y] = e[x][y] != ~0ull ? ub[coo_idx(e[x][y]) >> 5] : ~0u;
+#pragma unroll
+    for (int x = 0; x < kRT; ++x) {
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        const uint32_t i = coo_idx(e[x][y]);
+        if (e[x][y] != ~0ull && !((bw[x][y] >> (i & 31u)) & 1u)) eps[i] = coo_val(e[x][y]);
+      }
+      for (uint32_t j = 64 + lane; j < c[x]; j += 32) {  // a dense tile's rest
+        const uint64_t ee = stg[(t0 + x) * kK1Tile + j];
+        const uint32_t i = coo_idx(ee);
+        if (!((ub[i >> 5] >> (i & 31u)) & 1u)) eps[i] = coo_val(ee);
+      }
     }
   }
   if (lane == 0) trace_stamp(tab->trace, kTrCompact, 2);
@@ -601,7 +641,7 @@ __global__ void __launch_bounds__(kThreads)
 
 cudaError_t launch_p2p_restore(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, uint32_t* ub0, uint32_t* ub1,
                                uint64_t n, const uint32_t* flags2, const uint32_t* d_flags) {
-  const int grid = L.sms * 4;
+  const int grid = L.sms * 8;
   p2p_restore_kernel<<<grid, kThreads, 0, L.s>>>(d_tab, sp, ub0, ub1, (n + 31) / 32, flags2, d_flags);
   ++L.launches;
   return cudaGetLastError();
