@@ -191,8 +191,8 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
       if (trace && q == 0) ph0 = globaltimer_ns();
       cp_async_wait<kS - 2>();
       __syncthreads();  // stage i landed everywhere; the slot of tile i - 1 is free; tile i - 1 is emitted
-      if (trace && q == 0) ph_acc[0] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
       issue(i + kS - 1);
+      if (trace && q == 0) ph_acc[0] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();  // (wait + issue)
       const uint32_t t = t_lo + j0 + i0 + i;
       const uint64_t base = uint64_t(t) * kMergeTile;
       const uint64_t* slot = ring + (i % kS) * (P * kMergeRing);

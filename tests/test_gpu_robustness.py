@@ -179,61 +179,31 @@ def test_nccl_dead_peer_is_a_transport_error(gpus):
         pytest.skip("needs 2 GPUs")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_dead_peer_worker, args=(r, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    results = dict()
-    for _ in range(2):
-        r, v, err = q.get(timeout=300)
-        assert err is None, err
-        results[r] = v
-    for p in procs:
-        p.join(timeout=60)
+    for attempt in range(3):  # (a rendezvous port taken in between is retried on a fresh one)
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_dead_peer_worker, args=(r, port, q), daemon=True) for r in range(2)]
+        for p in procs:
+            p.start()
+        results, errs = dict(), []
+        try:
+            for _ in range(2):
+                r, v, err = q.get(timeout=300)
+                if err is not None:
+                    errs.append(err)
+                    break
+                results[r] = v
+        finally:
+            for p in procs:
+                p.join(timeout=30)
+                if p.is_alive():
+                    p.kill()
+        if errs and "EADDRINUSE" in errs[0] and attempt < 2:
+            continue
+        assert not errs, errs[0]
+        break
     rc, dt, err, rc2, dt2 = results[0]
     assert rc == 4, (rc, err)  # OKT_ERR_TRANSPORT
     assert "TransportError" in err, err
     assert dt < 60, dt  # bounded by OKT_NCCL_TIMEOUT_MS (4 s) or the P2P bound (20 s)
-    assert rc2 == 4 and dt2 < 30, (rc2, dt2)
-
-
-@pytest.mark.parametrize("t_bad", [6, 9])  # a steady step (single-rank graph) and a refresh (tau' = 4)
-def test_single_rank_nonfinite_step_leaves_model_and_residual(okm, oracle, t_bad):
-    """At P = 1 K7 is fused into the select (residual zero in K1, model
-    update in phase B): a step that meets a non-finite accumulator late in
-    the grid must leave the model and the residual as they were
-    (trainer.cpp:466-488 throws before touching them), and the trajectory
-    then continues exactly like the oracle's."""
-    import torch
-    n, k = 300_000, 3_000
-    w = okm.World(1, [0])
-    try:
-        ctx = w.ctx(0)
-        st = okm.OkState(okm.ThresholdState(tau=8, tau_prime=4), bucket_size=4)
-        model = okm.ModelState(np.zeros(n), 0, okm.LrSchedule(1.0))
-        res = okm.Residual(n)
-        ost = [OrcState.fresh(8, 4, 4)]
-        eps, ws = [np.zeros(n)], [np.zeros(n)]
-        for t in range(1, 12):
-            g = oracle.random_int_dense(500 + t, n, 3)
-            if t == t_bad:
-                w_before = model.w.cpu().numpy().copy()
-                eps_before = res.eps(ctx)
-                bad = g.copy()
-                bad[n - 7] = np.inf  # in the last K1 tile
-                with pytest.raises(okm.NumericError):
-                    okm.oktopk_sgd_step(ctx, model, res, bad, k, st)
-                assert np.array_equal(model.w.cpu().numpy(), w_before), "model changed by a failed step"
-                assert np.array_equal(res.eps(ctx), eps_before), "residual changed by a failed step"
-                assert st.t == t - 1
-                model.t = t - 1
-            got = okm.oktopk_sgd_step(ctx, model, res, g, k, st)
-            rc, ui, uv = oracle.sgd_step([g], eps, ws, ost, 1.0, t, k)
-            assert rc == 0
-            assert np.array_equal(got.u.indices, ui) and np.array_equal(got.u.values, uv), t
-            assert np.array_equal(res.eps(ctx), eps[0]), t
-            assert np.array_equal(model.w.cpu().numpy().astype(np.float64), ws[0]), t
-        torch.cuda.synchronize()
-    finally:
-        w.destroy()
+    assert rc2 == 4 and dt2 < 30, (rc2, dt2)  # the comm stays failed: the next call fails at once
