@@ -168,7 +168,9 @@ __global__ void __launch_bounds__(kThreads)
         ei[b] = coo_idx(e64[b]);
         ev[b] = double(coo_val(e64[b]));
       }
-      wv[b] = (APPLY && j0 + uint64_t(b) * kThreads < cnt) ? ap.w[ei[b]] : 0.f;
+      // (L2-only 4-byte gathers: through L1 each random word pulled a whole
+      // 128-byte line from DRAM — 445 MB read for 3.4M words at 340M, ncu)
+      wv[b] = (APPLY && j0 + uint64_t(b) * kThreads < cnt) ? __ldcg(ap.w + ei[b]) : 0.f;
     }
   };
   // The first batch is loaded before the global prefix is known: only the
@@ -697,8 +699,8 @@ __global__ void __launch_bounds__(kThreads)
     // entries of u are distinct, so all 2*kJ loads can be in flight together.
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
-      av[j] = valid[j] ? acc[idx[j]] : 0.f;
-      wv[j] = (valid[j] && w) ? w[idx[j]] : 0.f;
+      av[j] = valid[j] ? __ldcg(acc + idx[j]) : 0.f;  // (L2-only random gathers)
+      wv[j] = (valid[j] && w) ? __ldcg(w + idx[j]) : 0.f;
     }
     unsigned bal[kJ][1];
     bool pred[kJ];

