@@ -367,6 +367,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t my_n = span_at(gw + 1, ntiles, nchunks) - j0;
   const uint64_t out_base = uint64_t(j0) * kMergeTile;
   uint32_t running = 0;
+  uint64_t ph_acc[4] = {0, 0, 0, 0};  // diagnostics (trace on): ns in wait+issue / scatter / scan / emit, lane 0
   uint32_t seg[P];
 #pragma unroll
   for (int r = 0; r < P; ++r) seg[r] = 0;
@@ -391,9 +392,12 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
     for (int st = 0; st < S - 1; ++st) issue(uint32_t(st));
     for (uint32_t i = 0; i < ni; ++i) {
+      uint64_t ph0 = 0;
+      if (trace && lane == 0) ph0 = globaltimer_ns();
       cp_async_wait<S - 2>();
       __syncwarp();
       issue(i + S - 1);
+      if (trace && lane == 0) ph_acc[0] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
       const uint32_t t = t_lo + j0 + i0 + i;
       const uint64_t base = uint64_t(t) * kMergeTile;
       const uint64_t* slot = ring + (i % S) * (P * R);
@@ -431,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         }
         __syncwarp();
+        if (trace && lane == 0) ph_acc[1] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
         // scan: lane owns coordinates [lane * 32 * WPL, (lane + 1) * 32 * WPL) of the sub-tile
         uint32_t pw[P][WPL], pres[WPL];
 #pragma unroll
@@ -496,6 +501,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           if (lane >= o) incl += y;
         }
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (trace && lane == 0) ph_acc[2] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
         if (nsel) {
           uint64_t pos = out_base + running + incl - nsel;
 #pragma unroll
@@ -515,12 +521,17 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         running += total;
         __syncwarp();
+        if (trace && lane == 0) ph_acc[3] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
       }
     }
     cp_async_wait<0>();
     __syncwarp();
   }
   if (lane == 0) out_cnt[gw] = running;
+  if (trace && q == 0 && blockIdx.x < kTraceCtas) {  // warp 0's phase sums (the balanced pull's slots)
+    uint64_t* tp = trace + (uint64_t(kTrPull1) * kTraceCtas + blockIdx.x) * 4;
+    for (int x = 0; x < 4; ++x) tp[x] = ph_acc[x];
+  }
 #pragma unroll
   for (int r = 0; r < P; ++r) {
     const uint32_t g = __reduce_add_sync(0xffffffffu, seg[r]);
@@ -537,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 // owner's window to their stream position in my u (unbalanced: all of u;
 // balanced: my block, then — after every owner's block is complete — the
 // other blocks from their owners' u).  K7 runs on each entry as it lands.
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 3)
     p2p_pull_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, uint64_t* d_S, P2PPlan* plan,
                     uint64_t* d_U, uint32_t* d_flags, uint64_t timeout_ns, P2PApply ap, P2PHostOut* hout,
                     uint32_t* done) {
@@ -702,8 +713,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     float av[R], wv[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      av[k] = (acc && !ubits && ok[k]) ? __ldcg(acc + i[k]) : 0.f;  // (L2-only random gathers)
-      wv[k] = (wm && ok[k]) ? __ldcg(wm + i[k]) : 0.f;
+      av[k] = (acc && !ubits && ok[k]) ? acc[i[k]] : 0.f;
+      wv[k] = (wm && ok[k]) ? wm[i[k]] : 0.f;
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
