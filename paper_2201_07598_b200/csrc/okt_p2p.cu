@@ -278,270 +278,6 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
   if (lane == 0) trace_stamp(trace, kTrMerge, 2);
 }
 
-// The same merge with one WARP per contiguous span of K1 tiles and no block
-// barriers after the prologue (the default; OKT_MERGE_CTA=1 selects the
-// block-synchronous kernel above).  The block kernel spends ~250
-// instructions per thread per tile on fixed work (ring issue, mask clear,
-// scatter, scan, scans of counts, emit) — 1.7 us per 4096-coordinate tile at
-// four CTAs per SM, whatever the density (round-2 per-phase trace at 340M,
-// P = 2).  Here a warp merges a tile in NS sub-tiles of SUB coordinates held
-// as P presence bit-planes: the scatter sets a bit per entry, the scan reads
-// each lane's plane words, and a coordinate's value is found in its source's
-// sorted ring list by a popcount rank — no per-coordinate value array, so a
-// warp needs ~5-10 KB of shared memory and many warps run independently.
-template <int P>
-struct MergeCfg {
-  static constexpr int NS = P == 2 ? 2 : 4;        // sub-tiles per K1 tile
-  static constexpr int SUB = kMergeTile / NS;      // coordinates per sub-tile (2048 / 1024)
-  static constexpr int WPL = SUB / 1024;           // plane words per lane (2 / 1)
-  static constexpr int S = P == 2 ? 4 : 3;         // ring stages (tiles in flight per warp)
-  static constexpr int R = P == 8 ? 48 : 64;       // ring entries per source and stage
-};
-template <int P>
-__host__ __device__ constexpr size_t merge_warp_bytes() {
-  return size_t(MergeCfg<P>::S) * P * MergeCfg<P>::R * sizeof(uint64_t) +
-         size_t(P) * (MergeCfg<P>::SUB / 32) * sizeof(uint32_t);
-}
-
-template <int P>
-__global__ void __launch_bounds__(kThreads, 2)
-    p2p_merge_warp_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
-                          uint64_t W, uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns) {
-  using C = MergeCfg<P>;
-  constexpr int NS = C::NS, SUB = C::SUB, WPL = C::WPL, S = C::S, R = C::R;
-  extern __shared__ uint64_t smw[];
-  __shared__ uint32_t s_seg[P];
-  __shared__ int s_abort;
-  const uint64_t epoch = sp->epoch;
-  const int par = sp->par;
-  const int me = tab->rank, q = threadIdx.x, lane = q & 31, warp = q >> 5;
-  uint64_t* const trace = tab->trace;
-  if (q == 0) {
-    s_abort = (*d_flags & 1u) ? 1 : 0;
-    trace_stamp(trace, kTrMerge, 0);
-  }
-  if (q < P) s_seg[q] = 0;
-  __syncthreads();
-  const uint64_t hi = lo + W;
-  const uint32_t t_lo = uint32_t(lo / kMergeTile);
-  const uint32_t ntiles = W ? uint32_t((hi - 1) / kMergeTile) - t_lo + 1 : 0;
-  const uint32_t nchunks = gridDim.x * kWarps;  // one survivor chunk per warp
-  if (blockIdx.x == 0) {
-    if (q == 0) {
-      P2PPub* pub = &tab->hdr[me]->pub[par];  // (read by this rank's pull)
-      pub->sur_G = nchunks;
-      pub->sur_tiles = ntiles;
-      trace_stamp(trace, kTrPubL, 0);
-    }
-    const uint64_t pay[3] = {(*d_flags & 1u) ? 1ull : 0ull, k1_tiles, uint64_t(kK1Tile)};
-    publish_flag(tab->hdr, P, me, kFlagLReady, epoch, pay);
-    if (q == 0) trace_stamp(trace, kTrPubL, 3);
-  }
-  if (q < P && q != me) {
-    const FlagSlot* f = my_flag(tab->hdr[me], kFlagLReady, q);
-    if (!wait_flag(&f->epoch, epoch, timeout_ns)) {
-      atomicOr(d_flags, 8u);
-      s_abort = 1;
-    } else {
-      const uint64_t st = flag_word(f, 0);
-      if (st || flag_word(f, 1) != k1_tiles || flag_word(f, 2) != uint64_t(kK1Tile)) {
-        atomicOr(d_flags, 16u);
-        s_abort = 1;
-      }
-      if (blockIdx.x == 0) plan->peer_status[q] = st;
-    }
-  }
-  __syncthreads();
-  if (q == 0) trace_stamp(trace, kTrMerge, 1);
-  const bool abort = s_abort != 0;
-  const double gth = *d_gth;
-  uint32_t* const out_idx = tab->sidx[me][par];
-  double* const out_val = tab->sval[me][par];
-  uint32_t* const out_cnt = tab->scnt[me][par];
-  // this warp's shared memory: the ring [S][P][R], then the planes [P][SUB / 32]
-  uint64_t* const ring = smw + size_t(warp) * (merge_warp_bytes<P>() / 8);
-  uint32_t* const plane = reinterpret_cast<uint32_t*>(ring + S * P * R);
-  for (int w = lane; w < P * SUB / 32; w += 32) plane[w] = 0u;
-  const uint32_t gw = blockIdx.x * kWarps + warp;
-  const uint32_t j0 = span_at(gw, ntiles, nchunks);
-  const uint32_t my_n = span_at(gw + 1, ntiles, nchunks) - j0;
-  const uint64_t out_base = uint64_t(j0) * kMergeTile;
-  uint32_t running = 0;
-  uint64_t ph_acc[4] = {0, 0, 0, 0};  // diagnostics (trace on): ns in wait+issue / scatter / scan / emit, lane 0
-  uint32_t seg[P];
-#pragma unroll
-  for (int r = 0; r < P; ++r) seg[r] = 0;
-  for (uint32_t i0 = 0; i0 < my_n; i0 += 32) {
-    const uint32_t ni = min(my_n - i0, 32u);
-    uint32_t cnt[P];  // lane l: the counts of tile i0 + l
-#pragma unroll
-    for (int r = 0; r < P; ++r)
-      cnt[r] = (uint32_t(lane) < ni && !abort) ? tab->kcnt[r][par][t_lo + j0 + i0 + lane] : 0u;
-    auto issue = [&](uint32_t i) {  // ring stage i % S <- tile i's first R entries of every source (16-byte pairs)
-      if (i < ni) {
-        const uint64_t base = uint64_t(t_lo + j0 + i0 + i) * kMergeTile;
-        uint64_t* slot = ring + (i % S) * (P * R);
-#pragma unroll
-        for (int r = 0; r < P; ++r) {
-          const uint32_t c = min(__shfl_sync(0xffffffffu, cnt[r], int(i)), uint32_t(R));
-          for (uint32_t e = 2 * lane; e < c; e += 64) cp_async16(slot + r * R + e, tab->kstg[r][par] + base + e);
-        }
-      }
-      cp_async_commit();
-    };
-#pragma unroll
-    for (int st = 0; st < S - 1; ++st) issue(uint32_t(st));
-    for (uint32_t i = 0; i < ni; ++i) {
-      uint64_t ph0 = 0;
-      if (trace && lane == 0) ph0 = globaltimer_ns();
-      cp_async_wait<S - 2>();
-      __syncwarp();
-      issue(i + S - 1);
-      if (trace && lane == 0) ph_acc[0] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
-      const uint32_t t = t_lo + j0 + i0 + i;
-      const uint64_t base = uint64_t(t) * kMergeTile;
-      const uint64_t* slot = ring + (i % S) * (P * R);
-      uint32_t c_t[P], lb[P];
-#pragma unroll
-      for (int r = 0; r < P; ++r) {
-        c_t[r] = __shfl_sync(0xffffffffu, cnt[r], int(i));
-        lb[r] = 0;
-      }
-      auto entry = [&](int r, uint32_t e) {
-        return e < uint32_t(R) ? slot[r * R + e] : tab->kstg[r][par][base + e];
-      };
-      for (int s = 0; s < NS; ++s) {
-        const uint64_t sub0 = base + uint64_t(s) * SUB;
-        // scatter: source r's entries of this sub-tile are the next run of its sorted list
-        uint32_t lbs[P];
-#pragma unroll
-        for (int r = 0; r < P; ++r) {
-          lbs[r] = lb[r];
-          for (;;) {
-            const uint32_t e = lb[r] + uint32_t(lane);
-            bool in = false;
-            uint32_t c = 0;
-            if (e < c_t[r]) {
-              const uint64_t idx = coo_idx(entry(r, e));
-              if (idx < sub0 + SUB) {
-                in = true;
-                c = uint32_t(idx - sub0);
-              }
-            }
-            const unsigned b = __ballot_sync(0xffffffffu, in);
-            if (in) atomicOr(&plane[r * (SUB / 32) + (c >> 5)], 1u << (c & 31u));
-            lb[r] += __popc(b);
-            if (b != 0xffffffffu) break;
-          }
-        }
-        __syncwarp();
-        if (trace && lane == 0) ph_acc[1] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
-        // scan: lane owns coordinates [lane * 32 * WPL, (lane + 1) * 32 * WPL) of the sub-tile
-        uint32_t pw[P][WPL], pres[WPL];
-#pragma unroll
-        for (int x = 0; x < WPL; ++x) pres[x] = 0u;
-#pragma unroll
-        for (int r = 0; r < P; ++r)
-#pragma unroll
-          for (int x = 0; x < WPL; ++x) {
-            uint32_t* wp = &plane[r * (SUB / 32) + lane * WPL + x];
-            pw[r][x] = *wp;
-            *wp = 0u;  // (cleared for the next sub-tile; the next scatter follows a __syncwarp)
-            pres[x] |= pw[r][x];
-          }
-        uint32_t rb[P];  // rank of this lane's first coordinate in each source's sub-tile run
-#pragma unroll
-        for (int r = 0; r < P; ++r) {
-          uint32_t c = 0;
-#pragma unroll
-          for (int x = 0; x < WPL; ++x) c += __popc(pw[r][x]);
-          uint32_t incl = c;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-          }
-          rb[r] = lbs[r] + incl - c;
-        }
-        const uint64_t lane0 = sub0 + uint64_t(lane) * 32 * WPL;  // coordinate of this lane's first slot
-        // value of the coordinate at (word x, bit k): source r's entry rank = rb + set bits before it
-        auto bracket_at = [&](int x, int k, uint32_t& bits) {
-          float v[P];
-#pragma unroll
-          for (int r = 0; r < P; ++r) {
-            v[r] = 0.f;
-            if ((pw[r][x] >> k) & 1u) {
-              uint32_t rk = rb[r] + __popc(pw[r][x] & ((1u << k) - 1u));
-#pragma unroll
-              for (int y = 0; y < WPL; ++y)
-                if (y < x) rk += __popc(pw[r][y]);
-              v[r] = coo_val(entry(r, rk));
-              bits |= 1u << r;
-            }
-          }
-          return bracket_regs<P>(v, bits);
-        };
-        uint32_t nsel = 0;
-#pragma unroll
-        for (int x = 0; x < WPL; ++x)
-          for (uint32_t rest = pres[x]; rest; rest &= rest - 1) {
-            const int k = __ffs(rest) - 1;
-            const uint64_t coord = lane0 + uint64_t(x) * 32 + uint64_t(k);
-            if (coord < lo || coord >= hi) continue;  // the region's edge tiles
-            uint32_t bits = 0;
-            const double sum = bracket_at(x, k, bits);
-#pragma unroll
-            for (int r = 0; r < P; ++r) seg[r] += (bits >> r) & 1u;
-            if (fabs(sum) >= gth) ++nsel;
-          }
-        uint32_t incl = nsel;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        if (trace && lane == 0) ph_acc[2] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
-        if (nsel) {
-          uint64_t pos = out_base + running + incl - nsel;
-#pragma unroll
-          for (int x = 0; x < WPL; ++x)
-            for (uint32_t rest = pres[x]; rest; rest &= rest - 1) {
-              const int k = __ffs(rest) - 1;
-              const uint64_t coord = lane0 + uint64_t(x) * 32 + uint64_t(k);
-              if (coord < lo || coord >= hi) continue;
-              uint32_t bits = 0;
-              const double sum = bracket_at(x, k, bits);
-              if (fabs(sum) >= gth) {
-                out_idx[pos] = uint32_t(coord);
-                out_val[pos] = sum;
-                ++pos;
-              }
-            }
-        }
-        running += total;
-        __syncwarp();
-        if (trace && lane == 0) ph_acc[3] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
-      }
-    }
-    cp_async_wait<0>();
-    __syncwarp();
-  }
-  if (lane == 0) out_cnt[gw] = running;
-  if (trace && q == 0 && blockIdx.x < kTraceCtas) {  // warp 0's phase sums (the balanced pull's slots)
-    uint64_t* tp = trace + (uint64_t(kTrPull1) * kTraceCtas + blockIdx.x) * 4;
-    for (int x = 0; x < 4; ++x) tp[x] = ph_acc[x];
-  }
-#pragma unroll
-  for (int r = 0; r < P; ++r) {
-    const uint32_t g = __reduce_add_sync(0xffffffffu, seg[r]);
-    if (lane == 0 && g) atomicAdd(&s_seg[r], g);
-  }
-  __syncthreads();
-  if (q < P && s_seg[q]) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->seg_cnt[q]), (unsigned long long)s_seg[q]);
-  if (lane == 0) trace_stamp(trace, kTrMerge, 2);
-}
-
 // Allgatherv by pulling.  Every CTA waits for every rank's survivors and
 // derives the plan of balance_and_allgatherv (oktopk.cpp:172-231; identical on
 // all ranks), then one warp per (rank, chunk, part) copies survivors from the
@@ -932,26 +668,24 @@ template <int P>
 static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
                                   uint64_t W, uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags,
                                   uint64_t timeout_ns) {
-  static const bool cta_kernel = std::getenv("OKT_MERGE_CTA") != nullptr;  // (diagnostics A/B)
-  const size_t smem = cta_kernel ? merge_smem<P>() : kWarps * merge_warp_bytes<P>();
-  auto kern = cta_kernel ? p2p_merge_kernel<P> : p2p_merge_warp_kernel<P>;
+  constexpr size_t smem = merge_smem<P>();
   static std::atomic<int> caps[64];  // per device (the dynamic-smem opt-in is per device)
   int dev = 0;
   cudaGetDevice(&dev);
   std::atomic<int>& cap = caps[dev & 63];
   if (!cap) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(p2p_merge_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess || per_sm < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_merge_kernel<P>, kThreads, smem) != cudaSuccess ||
+        per_sm < 1) {
       cudaGetLastError();
       per_sm = 1;
     }
     cap = std::max(1, per_sm * L.sms / grid_div());
   }
   const uint64_t ntiles = W ? (lo + W - 1) / kMergeTile - lo / kMergeTile + 1 : 0;
-  const uint64_t units = cta_kernel ? ntiles : (ntiles + kWarps - 1) / kWarps;  // (a warp per span)
-  const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(units, uint64_t(cap))));
-  kern<<<grid, kThreads, smem, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
+  const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, uint64_t(cap))));
+  p2p_merge_kernel<P><<<grid, kThreads, smem, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
   ++L.launches;
   return cudaGetLastError();
 }
@@ -1006,14 +740,10 @@ cudaError_t launch_p2p_barrier(Launch& L, const PeerTab* d_tab, uint64_t epoch, 
 }
 
 const void* p2p_merge_func(int P) {
-  static const bool cta_kernel = std::getenv("OKT_MERGE_CTA") != nullptr;
   switch (P) {
-    case 2: return cta_kernel ? reinterpret_cast<const void*>(p2p_merge_kernel<2>)
-                              : reinterpret_cast<const void*>(p2p_merge_warp_kernel<2>);
-    case 4: return cta_kernel ? reinterpret_cast<const void*>(p2p_merge_kernel<4>)
-                              : reinterpret_cast<const void*>(p2p_merge_warp_kernel<4>);
-    case 8: return cta_kernel ? reinterpret_cast<const void*>(p2p_merge_kernel<8>)
-                              : reinterpret_cast<const void*>(p2p_merge_warp_kernel<8>);
+    case 2: return reinterpret_cast<const void*>(p2p_merge_kernel<2>);
+    case 4: return reinterpret_cast<const void*>(p2p_merge_kernel<4>);
+    case 8: return reinterpret_cast<const void*>(p2p_merge_kernel<8>);
   }
   return nullptr;
 }
