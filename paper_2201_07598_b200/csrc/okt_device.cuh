@@ -17,6 +17,27 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Device-side invariant checks of the debug build (make DEBUG_CHECKS=1 ->
+// libokt_checked.so): an out-of-range position or count traps the kernel with
+// a message.  compute-sanitizer is refused on the GPU pool these kernels are
+// tested on, so the checked build plus the oracle comparisons stand in for
+// memcheck; in the product build the macro is empty.
+#ifdef OKT_DEBUG_CHECKS
+#include <cstdio>
+#define OKT_DCHECK(cond, what, a, b)                                                                      \
+  do {                                                                                                    \
+    if (!(cond)) {                                                                                        \
+      printf("OKT_DCHECK failed: %s (%llu, %llu) block %d thread %d\n", what, (unsigned long long)(a),    \
+             (unsigned long long)(b), int(blockIdx.x), int(threadIdx.x));                                 \
+      __trap();                                                                                           \
+    }                                                                                                     \
+  } while (0)
+#else
+#define OKT_DCHECK(cond, what, a, b) \
+  do {                               \
+  } while (0)
+#endif
+
 namespace okt {
 
 constexpr int kMaxP = 8;                     // ranks per world (one HGX box)

@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(kThreads)
       if (s_pre[mid] <= j) lo = mid;
       else hi = mid - 1;
     }
+    OKT_DCHECK(j - s_pre[lo] < cap, "compact: entry beyond its chunk", j - s_pre[lo], cap);
     return uint64_t(c0 + lo) * cap + (j - s_pre[lo]);
   };
   constexpr int B = kCompactBatch;
@@ -467,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
         for (int c = 0; c < C; ++c) {
           if (pred[j][c]) {
             const uint32_t pos = grp[j] + rank_in_group<C>(bal, j, c);
+            OKT_DCHECK(pos < uint32_t(TILE), "k1: staged position beyond the tile", pos, tile);
             const uint64_t e = base + uint64_t(j) * (C * kThreads) + uint64_t(tid) * C + c;
             out[pos] = coo_pack(uint32_t(e), a[j][c]);
             if (APPLY && !ACCUM) ka.zero[e] = 0.f;

@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
         uint32_t got = 0;
         auto land = [&](uint64_t ent) {
           const uint64_t idx = coo_idx(ent);
+          OKT_DCHECK(idx >= base && idx < base + kMergeTile, "merge: a source's tile entry outside its tile", idx, base);
           if (idx < lo || idx >= hi) return;  // the region's edge tiles
           const uint32_t c = uint32_t(idx - base);
           s_val[r * kMergeTile + c] = coo_val(ent);
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
           ++got;
         };
         const uint32_t cr = s_cnt[i * P + r];
+        OKT_DCHECK(cr <= uint32_t(kMergeTile), "merge: tile count above the tile", cr, r);
         for (uint32_t e = q; e < cr; e += kThreads)
           land(e < uint32_t(kMergeRing) ? slot[r * kMergeRing + e] : tab->kstg[r][par][base + e]);
         got = __reduce_add_sync(0xffffffffu, got);
@@ -258,6 +260,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
         float v[P];
 #pragma unroll
         for (int r = 0; r < P; ++r) v[r] = s_val[r * kMergeTile + c];
+        OKT_DCHECK(pos < out_base + uint64_t(my_n) * kMergeTile, "merge: survivor beyond the CTA's chunk", pos, out_base);
         out_idx[pos] = uint32_t(base + c);
         out_val[pos] = bracket_regs<P>(v, bits_of(k));
       }
@@ -492,6 +495,7 @@ __global__ void __launch_bounds__(kThreads, 3)
       const uint64_t base = s_off[r] + tab->spre[r][par][c];
       const uint64_t end = base + tab->scnt[r][par][c];
       const uint64_t len = end - base;
+      OKT_DCHECK(end <= s_off[r + 1], "pull: chunk beyond its rank's survivors", end, s_off[r + 1]);
       const uint64_t lo = max(base + frac_at(len, part, parts), a), hi = min(base + frac_at(len, part + 1, parts), b);
       const uint64_t cbase = uint64_t(span_at(c, s_tiles[r], s_G[r])) * kMergeTile;
       const uint32_t* si = tab->sidx[r][par] + cbase;
@@ -608,7 +612,10 @@ __global__ void __launch_bounds__(kThreads)
   for (uint64_t t0 = wid * kRT; t0 < G; t0 += wstride * kRT) {
     uint32_t c[kRT];
 #pragma unroll
-    for (int x = 0; x < kRT; ++x) c[x] = t0 + x < G ? cnt[t0 + x] : 0u;
+    for (int x = 0; x < kRT; ++x) {
+      c[x] = t0 + x < G ? cnt[t0 + x] : 0u;
+      OKT_DCHECK(c[x] <= uint32_t(kK1Tile), "restore: tile count above the tile", c[x], t0 + x);
+    }
     uint64_t e[kRT][2];
 #pragma unroll
     for (int x = 0; x < kRT; ++x)
