@@ -154,8 +154,8 @@ def workload(args, P):
             "inputs": "drifting_gradient_process(t, seed=1, rank_key=r+1) rounded to fp32, the same t = 1, 2, ... "
                       "in both arms (fresh state at t = 1)",
             "parallelism": f"dp{P} (one process per GPU, NVLink P2P / NCCL)" if P > 1 else "single GPU",
-            "rank_alignment": "device barrier (okt_device_barrier, NVLink flags) before each timed chunk"
-                              if P > 1 else None,
+            "rank_alignment": "device barrier (okt_device_barrier, NVLink flags) before each timed step, outside "
+                              "the events" if P > 1 else None,
             "value": "tau'-amortised ms/iter: ((tau'-1) * mean(steady) + mean(refresh)) / tau'",
             "l2": ("flushed before every timed step, outside the events (256 MiB write + 256 MiB read sweep)" if fl
                    else f"not flushed: inputs larger than L2 (the step streams 12n = {12 * args.n / 1e9:.2f} GB: "
@@ -443,6 +443,11 @@ def run_okt(args):
             if fl:
                 with torch.cuda.stream(stream):
                     flush.fill_(t & 0xff)  # evict L2 between timed steps (outside the events)
+            if world > 1 and i:
+                # the ranks' GPUs aligned before every step, outside the events: the
+                # step is timed without the hosts' launch skew (the device barrier
+                # is enqueued on the stream, the host does not wait for it)
+                L.okt_device_barrier(comm, sp)
             with torch.cuda.stream(stream):
                 ev[t - 1][0].record(stream)
             step_async(ring[i], t)
