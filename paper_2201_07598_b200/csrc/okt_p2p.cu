@@ -47,7 +47,7 @@ constexpr int kMergeCntCap = 256;                 // tiles whose counts are stag
 
 template <int P>
 __host__ __device__ constexpr size_t merge_smem() {  // mask bytes, values [P][tile], ring [S][P][kMergeRing], counts
-  return size_t(kMergeTile) + size_t(P) * kMergeTile * sizeof(uint16_t) +
+  return size_t(kMergeTile) + size_t(P) * kMergeTile * sizeof(float) +
          size_t(merge_stages<P>()) * P * kMergeRing * sizeof(uint64_t) + size_t(kMergeCntCap) * P * sizeof(uint32_t);
 }
 
@@ -84,20 +84,16 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Occupancy by P (registers x shared memory with the 2-byte position map):
-// 4 CTAs per SM at P = 2, 3 at P = 4, 2 at P = 8 (the 4-byte value stage of
-// round 1 fit 4 / 2 / 1: at P = 4 the merge ran 6.5 us per tile per CTA,
-// 0.53 ms at 340M — round-2 trace).
+// P = 2 is capped at 48 registers: 5 CTAs per SM instead of 4 (shared memory
+// allows 6), so more of the region's tiles are in flight at once (interleaved
+// A/B on one box, tools/ab_lib.sh: steady N = 2 0.0812 -> 0.0799 ms).
 template <int P>
-__global__ void __launch_bounds__(kThreads, P == 2 ? 4 : (P == 4 ? 3 : 2))
+__global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
     p2p_merge_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo, uint64_t W,
                      uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns) {
   extern __shared__ uint32_t sm[];
   uint32_t* s_mask = sm;                                             // [kMergeTile / 4]: byte per coordinate, bit per source
-  // [P][kMergeTile]: the entry's position in its source's tile list (ring slot
-  // when < kMergeRing, else the source's staging) — 2 bytes per coordinate
-  // instead of a 4-byte value stage, so more CTAs fit per SM
-  uint16_t* s_map = reinterpret_cast<uint16_t*>(sm + kMergeTile / 4);
+  float* s_val = reinterpret_cast<float*>(sm + kMergeTile / 4);      // [P][kMergeTile]
   __shared__ uint32_t s_wt[kWarps];
   __shared__ uint32_t s_seg[P];
   __shared__ int s_abort;
@@ -158,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : (P == 4 ? 3 : 2))
   // (the first kMergeRing entries of a tile per source; a denser tile's rest
   // is read directly).  Round 1 kept one tile in flight: 6.8 us per tile at
   // n = 340M, P = 4, almost all of it NVLink latency.
-  uint64_t* const ring = reinterpret_cast<uint64_t*>(s_map + P * kMergeTile);    // [S][P][kMergeRing]
+  uint64_t* const ring = reinterpret_cast<uint64_t*>(s_val + P * kMergeTile);    // [S][P][kMergeRing]
   constexpr int kS = merge_stages<P>();
   uint32_t* const s_cnt = reinterpret_cast<uint32_t*>(ring + kS * P * kMergeRing);  // [kMergeCntCap][P]
   const uint32_t j0 = span_at(blockIdx.x, ntiles, gridDim.x);
@@ -200,27 +196,22 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : (P == 4 ? 3 : 2))
       const uint32_t t = t_lo + j0 + i0 + i;
       const uint64_t base = uint64_t(t) * kMergeTile;
       const uint64_t* slot = ring + (i % kS) * (P * kMergeRing);
-      // (only called for a source whose presence bit is set at c)
-      auto value_at = [&](int r, uint32_t c) {
-        const uint32_t e = s_map[r * kMergeTile + c];
-        return coo_val(e < uint32_t(kMergeRing) ? slot[r * kMergeRing + e] : tab->kstg[r][par][base + e]);
-      };
 #pragma unroll
       for (int r = 0; r < P; ++r) {
         uint32_t got = 0;
-        auto land = [&](uint64_t ent, uint32_t e) {
+        auto land = [&](uint64_t ent) {
           const uint64_t idx = coo_idx(ent);
           OKT_DCHECK(idx >= base && idx < base + kMergeTile, "merge: a source's tile entry outside its tile", idx, base);
           if (idx < lo || idx >= hi) return;  // the region's edge tiles
           const uint32_t c = uint32_t(idx - base);
-          s_map[r * kMergeTile + c] = uint16_t(e);
+          s_val[r * kMergeTile + c] = coo_val(ent);
           atomicOr(&s_mask[c >> 2], 1u << ((c & 3u) * 8u + uint32_t(r)));
           ++got;
         };
         const uint32_t cr = s_cnt[i * P + r];
         OKT_DCHECK(cr <= uint32_t(kMergeTile), "merge: tile count above the tile", cr, r);
         for (uint32_t e = q; e < cr; e += kThreads)
-          land(e < uint32_t(kMergeRing) ? slot[r * kMergeRing + e] : tab->kstg[r][par][base + e], e);
+          land(e < uint32_t(kMergeRing) ? slot[r * kMergeRing + e] : tab->kstg[r][par][base + e]);
         got = __reduce_add_sync(0xffffffffu, got);
         if (lane == 0 && got) atomicAdd(&s_seg[r], got);
       }
@@ -242,10 +233,9 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : (P == 4 ? 3 : 2))
         const int k = __ffs(rest) - 1;
         const uint32_t c = uint32_t(q) * kMergePer + uint32_t(k);
         float v[P];
-        const uint32_t bits = bits_of(k);
 #pragma unroll
-        for (int r = 0; r < P; ++r) v[r] = ((bits >> r) & 1u) ? value_at(r, c) : 0.f;
-        if (fabs(bracket_regs<P>(v, bits)) >= gth) sel |= 1u << k;
+        for (int r = 0; r < P; ++r) v[r] = s_val[r * kMergeTile + c];
+        if (fabs(bracket_regs<P>(v, bits_of(k))) >= gth) sel |= 1u << k;
       }
       const uint32_t n_sel = __popc(sel);
       uint32_t incl = n_sel;
@@ -268,12 +258,11 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : (P == 4 ? 3 : 2))
         const int k = __ffs(rest) - 1;
         const uint32_t c = uint32_t(q) * kMergePer + uint32_t(k);
         float v[P];
-        const uint32_t bits = bits_of(k);
 #pragma unroll
-        for (int r = 0; r < P; ++r) v[r] = ((bits >> r) & 1u) ? value_at(r, c) : 0.f;
+        for (int r = 0; r < P; ++r) v[r] = s_val[r * kMergeTile + c];
         OKT_DCHECK(pos < out_base + uint64_t(my_n) * kMergeTile, "merge: survivor beyond the CTA's chunk", pos, out_base);
         out_idx[pos] = uint32_t(base + c);
-        out_val[pos] = bracket_regs<P>(v, bits);
+        out_val[pos] = bracket_regs<P>(v, bits_of(k));
       }
       running += total;
       if (trace && q == 0) ph_acc[3] += globaltimer_ns() - ph0;
