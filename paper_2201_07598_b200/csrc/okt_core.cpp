@@ -1655,6 +1655,14 @@ int init_comm(okt_comm* c) {
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
   c->L.sms = dev_sms;
+  // L2 fetch granularity (diagnostics A/B, OKT_L2_FETCH_BYTES = 32 / 64 / 128):
+  // the scatter kernels' random 4-byte accesses pull whole lines from DRAM
+  // (phase B at 340M read 446 MB for 3.4M model words, ncu).  A device-wide
+  // limit, so it is only set when asked for.
+  if (const char* e = std::getenv("OKT_L2_FETCH_BYTES")) {
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(std::atoi(e)));
+    cudaGetLastError();
+  }
   if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ready_ev, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
