@@ -1374,9 +1374,8 @@ struct okt_comm {
                                                 &d()->S), "filter");
             if (!rc) rc = ck(cudaMemcpyAsync(&d()->m, &d()->S, 8, cudaMemcpyDeviceToDevice, s), "copy");
             tmark(OKT_T_APPLY, s);
-            if (!rc) rc = ck(okt::launch_apply(L, S, sur_idx.as<uint32_t>(), sur_val.as<double>(), &d()->S, C,
-                                               eps_out, true, w, 1, &d()->local_th, indexes.as<uint32_t>(),
-                                               &d()->nidx, &d()->flags), "apply");
+            if (!rc) rc = ck(okt::launch_apply_u(L, sur_idx.as<uint32_t>(), sur_val.as<double>(), &d()->S, C, eps_out,
+                                                 w, &d()->flags), "apply");
             sel_done = true;
           } else {
             tmark(OKT_T_THRESHOLD, s);

@@ -665,6 +665,50 @@ cudaError_t launch_filter(Launch& L, const Stage& S, bool aos, const uint64_t* i
   return launch_compact<2>(L, S, G, 0, S.chunk_cap, 0, nullptr, out_idx, out_val, d_cnt_out, nullptr, ap);
 }
 
+// K7 where every entry of u is in the local selection (one rank: indexes = u):
+// eps[i] = 0 and w[i] -= v for each entry, with no gather of acc to test the
+// selection and no index list to compact (the caller's indexes are u's).
+__global__ void __launch_bounds__(kThreads)
+    apply_u_kernel(const uint32_t* __restrict__ u_idx, const double* __restrict__ u_val, const uint64_t* d_U,
+                   float* acc, float* w, uint32_t* d_flags) {
+  if (*d_flags & 1u) return;  // a non-finite step touches nothing
+  const uint64_t cnt = *d_U;
+  constexpr int B = 4;
+  const uint64_t stride = uint64_t(gridDim.x) * kThreads;
+  bool bad = false;
+  for (uint64_t e0 = uint64_t(blockIdx.x) * kThreads + threadIdx.x; e0 < cnt; e0 += B * stride) {
+    uint32_t i[B];
+    double v[B];
+    float wv[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const uint64_t e = e0 + uint64_t(b) * stride;
+      i[b] = e < cnt ? u_idx[e] : 0u;
+      v[b] = e < cnt ? u_val[e] : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) wv[b] = e0 + uint64_t(b) * stride < cnt ? w[i[b]] : 0.f;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      if (e0 + uint64_t(b) * stride >= cnt) continue;
+      const float nw = float(double(wv[b]) - v[b]);
+      w[i[b]] = nw;
+      acc[i[b]] = 0.f;
+      bad |= nonfinite(nw);
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(d_flags, 4u);
+}
+
+cudaError_t launch_apply_u(Launch& L, const uint32_t* u_idx, const double* u_val, const uint64_t* d_U, uint64_t bound,
+                           float* acc, float* w, uint32_t* d_flags) {
+  const uint64_t want = (bound + kThreads * 4 - 1) / (kThreads * 4);
+  const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(L.sms) * 8)));
+  apply_u_kernel<<<grid, kThreads, 0, L.s>>>(u_idx, u_val, d_U, acc, w, d_flags);
+  ++L.launches;
+  return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(kThreads)
     apply_kernel(const uint32_t* __restrict__ u_idx, const double* __restrict__ u_val, const uint64_t* d_U,
                  float* acc, int zero_eps, float* w, int P, const double* d_local_th,

@@ -132,6 +132,9 @@ cudaError_t launch_filter(Launch& L, const Stage& S, bool aos, const uint64_t* i
                           const ApplyArgs* ap = nullptr,
                           uint64_t* out_aos = nullptr);
 
+// K7 when indexes = u (one rank): eps[i] = 0, w[i] -= v for every entry of u.
+cudaError_t launch_apply_u(Launch& L, const uint32_t* u_idx, const double* u_val, const uint64_t* d_U, uint64_t bound,
+                           float* acc, float* w, uint32_t* d_flags);
 // K7: for each (i, v) of u: sel = |acc[i]| >= local_th; if w: w[i] -= v / P;
 // if zero_eps && sel: acc[i] = 0; emit i into indexes when sel.
 cudaError_t launch_apply(Launch& L, const Stage& S, const uint32_t* u_idx, const double* u_val,
