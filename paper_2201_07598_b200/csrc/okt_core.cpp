@@ -1655,9 +1655,10 @@ int init_comm(okt_comm* c) {
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
   c->L.sms = dev_sms;
   // L2 fetch granularity (diagnostics A/B, OKT_L2_FETCH_BYTES = 32 / 64 / 128):
-  // the scatter kernels' random 4-byte accesses pull whole lines from DRAM
-  // (phase B at 340M read 446 MB for 3.4M model words, ncu).  A device-wide
-  // limit, so it is only set when asked for.
+  // the scatter kernels' random 4-byte accesses pull ~128 bytes each from DRAM
+  // (phase B at 340M reads 446 MB for 3.4M model words, ncu).  Measured: no
+  // effect at 32 or 64 (tools/ab_l2fetch.sh, profiles/r02_l2fetch_ab.txt), so
+  // it is only set when asked for.
   if (const char* e = std::getenv("OKT_L2_FETCH_BYTES")) {
     cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(std::atoi(e)));
     cudaGetLastError();
