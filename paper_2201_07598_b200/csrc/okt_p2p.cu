@@ -72,6 +72,34 @@ __device__ __forceinline__ uint64_t frac_at(uint64_t len, uint32_t p, uint32_t q
   return v;
 }
 
+// TMA bulk copies into the ring, completion tracked by one mbarrier per stage.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W;\n"
+      "}\n" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // 16-byte async copy, L2 only (.cg: no L1 line of a peer's buffer survives
 // into a later step that reuses the same parity slot).
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
@@ -149,11 +177,13 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
   // capacity), count in out_cnt[blockIdx.x] — a few hundred large chunks per
   // rank for the pull instead of one small chunk per tile.  The span's
   // per-source counts are staged in shared memory first (all loads in flight
-  // at once), then a kS-deep cp.async ring keeps the entries of the
-  // next tiles of every source in flight over NVLink while a tile is merged
-  // (the first kMergeRing entries of a tile per source; a denser tile's rest
-  // is read directly).  Round 1 kept one tile in flight: 6.8 us per tile at
-  // n = 340M, P = 4, almost all of it NVLink latency.
+  // at once), then a kS-deep ring of TMA bulk copies (cp.async.bulk, one per
+  // source and tile, issued by one thread, completion counted in bytes on the
+  // stage's mbarrier) keeps the entries of the next tiles of every source in
+  // flight over NVLink while a tile is merged (the first kMergeRing entries of
+  // a tile per source; a denser tile's rest is read directly).  Round 1 kept
+  // one tile in flight: 6.8 us per tile at n = 340M, P = 4, almost all of it
+  // NVLink latency.
   uint64_t* const ring = reinterpret_cast<uint64_t*>(s_val + P * kMergeTile);    // [S][P][kMergeRing]
   constexpr int kS = merge_stages<P>();
   uint32_t* const s_cnt = reinterpret_cast<uint32_t*>(ring + kS * P * kMergeRing);  // [kMergeCntCap][P]
@@ -163,6 +193,12 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
   uint32_t running = 0;  // survivors of this CTA so far (block-uniform)
   uint64_t ph_acc[4] = {0, 0, 0, 0};  // diagnostics (trace on): ns in wait / scatter / scan / emit, thread 0
   for (int w = q; w < kMergeTile / 16; w += kThreads) reinterpret_cast<uint4*>(s_mask)[w] = make_uint4(0, 0, 0, 0);
+  __shared__ __align__(8) uint64_t s_mbar[8];  // one per ring stage
+  if (q == 0) {
+    for (int st = 0; st < kS; ++st) mbar_init(&s_mbar[st], 1);
+    fence_proxy_async_smem();  // (the initialised barriers, visible to the copy engine)
+  }
+  uint32_t ph_bits = 0;  // the parity each stage's barrier completes next (every thread tracks it)
   for (uint32_t i0 = 0; i0 < my_n; i0 += kMergeCntCap) {
     const uint32_t ni = min(my_n - i0, uint32_t(kMergeCntCap));
     for (uint32_t x = q; x < ni * P; x += kThreads) {
@@ -171,26 +207,35 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
       s_cnt[x] = s_abort ? 0u : tab->kcnt[r][par][t_lo + j0 + i0 + i];
     }
     __syncthreads();
-    auto issue = [&](uint32_t i) {  // ring stage i % S <- tile i's first entries, every source
-      if (i < ni) {
+    auto issue = [&](uint32_t i) {  // ring stage i % S <- tile i's first entries, every source (thread 0)
+      if (i < ni && q == 0) {
         const uint64_t base = uint64_t(t_lo + j0 + i0 + i) * kMergeTile;
         uint64_t* slot = ring + (i % kS) * (P * kMergeRing);
-        // entry pairs (16 B; a tile's staging slot starts 16-byte aligned and
-        // holds kMergeTile entries, so the odd count's partner is in bounds)
-        for (int x = q; x < P * kMergeRing / 2; x += kThreads) {
-          const int r = x / (kMergeRing / 2), e = 2 * (x % (kMergeRing / 2));
-          if (uint32_t(e) < s_cnt[i * P + r]) cp_async16(slot + r * kMergeRing + e, tab->kstg[r][par] + base + e);
+        uint64_t* mb = &s_mbar[i % kS];
+        // whole 16-byte pairs of entries (a tile's staging slot starts 16-byte
+        // aligned and holds kMergeTile entries, so an odd count's partner is in bounds)
+        uint32_t bytes[P], total = 0;
+#pragma unroll
+        for (int r = 0; r < P; ++r) {
+          const uint32_t c = min(s_cnt[i * P + r], uint32_t(kMergeRing));
+          bytes[r] = ((c + 1u) & ~1u) * 8u;
+          total += bytes[r];
         }
+        fence_proxy_async_smem();  // the slot's earlier generic reads before the copy engine's writes
+        mbar_expect_tx(mb, total);
+#pragma unroll
+        for (int r = 0; r < P; ++r)
+          if (bytes[r]) bulk_g2s(slot + r * kMergeRing, tab->kstg[r][par] + base, bytes[r], mb);
       }
-      cp_async_commit();  // (empty groups keep the group count uniform)
     };
 #pragma unroll
     for (int st = 0; st < kS - 1; ++st) issue(uint32_t(st));
     for (uint32_t i = 0; i < ni; ++i) {
       uint64_t ph0 = 0;
       if (trace && q == 0) ph0 = globaltimer_ns();
-      cp_async_wait<kS - 2>();
-      __syncthreads();  // stage i landed everywhere; the slot of tile i - 1 is free; tile i - 1 is emitted
+      mbar_wait(&s_mbar[i % kS], (ph_bits >> (i % kS)) & 1u);  // stage i landed
+      ph_bits ^= 1u << (i % kS);
+      __syncthreads();  // the slot of tile i - 1 is free; tile i - 1 is emitted
       issue(i + kS - 1);
       if (trace && q == 0) ph_acc[0] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();  // (wait + issue)
       const uint32_t t = t_lo + j0 + i0 + i;
@@ -269,7 +314,6 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
       // (no barrier here: the next tile's first barrier separates this emit
       // from its scatter; s_wt is rewritten only after its second one)
     }
-    cp_async_wait<0>();
     __syncthreads();
   }
   if (q == 0) out_cnt[blockIdx.x] = running;
