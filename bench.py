@@ -555,7 +555,10 @@ def run_okt(args):
         step_async(scratch, tp)
         wait()
     hbuf = torch.empty(n, dtype=torch.float32).pin_memory()
-    cap = min(n, 8 * k + 4096)  # u's host buffers (U ~ k on these inputs; a larger U fails the call loudly)
+    # u's host buffers: U ~ k after a refresh, but between refreshes the EF
+    # residual of unselected heavy slots grows past the threshold (at 0.1 %
+    # density U reached ~10 k by t = 20); a U beyond the buffers fails loudly
+    cap = min(n, 40 * k + 4096)
     h_uidx = torch.empty(cap, dtype=torch.int32).pin_memory()
     h_uval = torch.empty(cap, dtype=torch.float64).pin_memory()
     e2e_steps = max(2, args.e2e_steps)

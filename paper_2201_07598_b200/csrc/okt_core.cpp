@@ -1654,6 +1654,7 @@ int init_comm(okt_comm* c) {
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
   c->L.sms = dev_sms;
+  okt::preload_kernels();
   // L2 fetch granularity (diagnostics A/B, OKT_L2_FETCH_BYTES = 32 / 64 / 128):
   // the scatter kernels' random 4-byte accesses pull ~128 bytes each from DRAM
   // (phase B at 340M reads 446 MB for 3.4M model words, ncu).  Measured: no

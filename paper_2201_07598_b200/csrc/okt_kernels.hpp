@@ -182,6 +182,9 @@ const void* p2p_merge_func(int P);
 const void* p2p_pull_func();
 const void* p2p_totals_func();
 const void* p2p_restore_func();
+// Loads the path's kernels now (lazy module loading would load each at its first launch).
+void preload_kernels();
+void preload_p2p_kernels();
 // EF steps after the pull: acc back at the local entries outside u; clears the next step's u bitmap.
 cudaError_t launch_p2p_restore(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, uint32_t* ub0, uint32_t* ub1,
                                uint64_t n, const uint32_t* flags2, const uint32_t* d_flags);

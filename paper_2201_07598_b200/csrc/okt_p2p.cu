@@ -802,4 +802,16 @@ const void* p2p_pull_func() { return reinterpret_cast<const void*>(p2p_pull_kern
 const void* p2p_totals_func() { return reinterpret_cast<const void*>(p2p_totals_kernel); }
 const void* p2p_restore_func() { return reinterpret_cast<const void*>(p2p_restore_kernel); }
 
+// (see preload_kernels in okt_kernels.cu)
+void preload_p2p_kernels() {
+  cudaFuncAttributes a;
+  for (const void* f : {reinterpret_cast<const void*>(p2p_merge_kernel<2>),
+                        reinterpret_cast<const void*>(p2p_merge_kernel<4>),
+                        reinterpret_cast<const void*>(p2p_merge_kernel<8>),
+                        reinterpret_cast<const void*>(p2p_pull_kernel), reinterpret_cast<const void*>(p2p_totals_kernel),
+                        reinterpret_cast<const void*>(p2p_restore_kernel),
+                        reinterpret_cast<const void*>(p2p_barrier_kernel)})
+    cudaFuncGetAttributes(&a, f);
+}
+
 }  // namespace okt
