@@ -191,6 +191,12 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
   const uint32_t my_n = span_at(blockIdx.x + 1, ntiles, gridDim.x) - j0;
   const uint64_t out_base = uint64_t(j0) * kMergeTile;
   uint32_t running = 0;  // survivors of this CTA so far (block-uniform)
+  // entries received from each source (the ledger's split words), per thread:
+  // reduced once at the end instead of a warp reduce + shared atomic per
+  // source and tile
+  uint32_t seg_mine[P];
+#pragma unroll
+  for (int r = 0; r < P; ++r) seg_mine[r] = 0;
   uint64_t ph_acc[4] = {0, 0, 0, 0};  // diagnostics (trace on): ns in wait / scatter / scan / emit, thread 0
   for (int w = q; w < kMergeTile / 16; w += kThreads) reinterpret_cast<uint4*>(s_mask)[w] = make_uint4(0, 0, 0, 0);
   __shared__ __align__(8) uint64_t s_mbar[8];  // one per ring stage
@@ -243,7 +249,6 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
       const uint64_t* slot = ring + (i % kS) * (P * kMergeRing);
 #pragma unroll
       for (int r = 0; r < P; ++r) {
-        uint32_t got = 0;
         auto land = [&](uint64_t ent) {
           const uint64_t idx = coo_idx(ent);
           OKT_DCHECK(idx >= base && idx < base + kMergeTile, "merge: a source's tile entry outside its tile", idx, base);
@@ -251,14 +256,12 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
           const uint32_t c = uint32_t(idx - base);
           s_val[r * kMergeTile + c] = coo_val(ent);
           atomicOr(&s_mask[c >> 2], 1u << ((c & 3u) * 8u + uint32_t(r)));
-          ++got;
+          ++seg_mine[r];
         };
         const uint32_t cr = s_cnt[i * P + r];
         OKT_DCHECK(cr <= uint32_t(kMergeTile), "merge: tile count above the tile", cr, r);
         for (uint32_t e = q; e < cr; e += kThreads)
           land(e < uint32_t(kMergeRing) ? slot[r * kMergeRing + e] : tab->kstg[r][par][base + e]);
-        got = __reduce_add_sync(0xffffffffu, got);
-        if (lane == 0 && got) atomicAdd(&s_seg[r], got);
       }
       __syncthreads();
       if (trace && q == 0) ph_acc[1] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();
@@ -321,6 +324,12 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
     uint64_t* tp = trace + (uint64_t(kTrPull1) * kTraceCtas + blockIdx.x) * 4;
     for (int x = 0; x < 4; ++x) tp[x] = ph_acc[x];
   }
+#pragma unroll
+  for (int r = 0; r < P; ++r) {
+    const uint32_t g = __reduce_add_sync(0xffffffffu, seg_mine[r]);
+    if (lane == 0 && g) atomicAdd(&s_seg[r], g);
+  }
+  __syncthreads();
   if (q < P && s_seg[q]) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->seg_cnt[q]), (unsigned long long)s_seg[q]);
   if (lane == 0) trace_stamp(trace, kTrMerge, 2);
 }
