@@ -115,7 +115,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // P = 2 is capped at 48 registers: 5 CTAs per SM instead of 4 (shared memory
 // allows 6), so more of the region's tiles are in flight at once (interleaved
 // A/B on one box, tools/ab_lib.sh: steady N = 2 0.0812 -> 0.0799 ms).
-template <int P>
+template <int P, bool TMA>
 __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
     p2p_merge_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo, uint64_t W,
                      uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns) {
@@ -213,8 +213,20 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
       s_cnt[x] = s_abort ? 0u : tab->kcnt[r][par][t_lo + j0 + i0 + i];
     }
     __syncthreads();
-    auto issue = [&](uint32_t i) {  // ring stage i % S <- tile i's first entries, every source (thread 0)
-      if (i < ni && q == 0) {
+    auto issue = [&](uint32_t i) {  // ring stage i % S <- tile i's first entries, every source
+      if constexpr (!TMA) {
+        // cp.async (LDGSTS) by every thread: 16-byte pairs of entries
+        if (i < ni) {
+          const uint64_t base = uint64_t(t_lo + j0 + i0 + i) * kMergeTile;
+          uint64_t* slot = ring + (i % kS) * (P * kMergeRing);
+          for (int x = q; x < P * kMergeRing / 2; x += kThreads) {
+            const int r = x / (kMergeRing / 2), e = 2 * (x % (kMergeRing / 2));
+            if (uint32_t(e) < s_cnt[i * P + r]) cp_async16(slot + r * kMergeRing + e, tab->kstg[r][par] + base + e);
+          }
+        }
+        cp_async_commit();  // (empty groups keep the group count uniform)
+      } else if (i < ni && q == 0) {
+        // TMA bulk copies issued by thread 0, completion on the stage's mbarrier
         const uint64_t base = uint64_t(t_lo + j0 + i0 + i) * kMergeTile;
         uint64_t* slot = ring + (i % kS) * (P * kMergeRing);
         uint64_t* mb = &s_mbar[i % kS];
@@ -239,8 +251,12 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
     for (uint32_t i = 0; i < ni; ++i) {
       uint64_t ph0 = 0;
       if (trace && q == 0) ph0 = globaltimer_ns();
-      mbar_wait(&s_mbar[i % kS], (ph_bits >> (i % kS)) & 1u);  // stage i landed
-      ph_bits ^= 1u << (i % kS);
+      if constexpr (TMA) {
+        mbar_wait(&s_mbar[i % kS], (ph_bits >> (i % kS)) & 1u);  // stage i landed
+        ph_bits ^= 1u << (i % kS);
+      } else {
+        cp_async_wait<kS - 2>();
+      }
       __syncthreads();  // the slot of tile i - 1 is free; tile i - 1 is emitted
       issue(i + kS - 1);
       if (trace && q == 0) ph_acc[0] += globaltimer_ns() - ph0, ph0 = globaltimer_ns();  // (wait + issue)
@@ -317,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
       // (no barrier here: the next tile's first barrier separates this emit
       // from its scatter; s_wt is rewritten only after its second one)
     }
+    if constexpr (!TMA) cp_async_wait<0>();
     __syncthreads();
   }
   if (q == 0) out_cnt[blockIdx.x] = running;
@@ -724,19 +741,30 @@ static int grid_div() {
   return d;
 }
 
+// The merge ring's copies: cp.async (LDGSTS, default) or TMA bulk copies
+// (OKT_MERGE_TMA=1).  Per-tile copies are ~330 bytes per source at 1 %
+// density; as TMA bulk copies from the peers they arrived too slowly to keep
+// the ring ahead (N = 4, 340M: the merge waited 364 us of 504 on its barriers).
+static bool merge_tma() {
+  static const bool on = std::getenv("OKT_MERGE_TMA") != nullptr;
+  return on;
+}
+
 template <int P>
 static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
                                   uint64_t W, uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags,
                                   uint64_t timeout_ns) {
   constexpr size_t smem = merge_smem<P>();
+  auto kern = merge_tma() ? p2p_merge_kernel<P, true> : p2p_merge_kernel<P, false>;
   static std::atomic<int> caps[64];  // per device (the dynamic-smem opt-in is per device)
   int dev = 0;
   cudaGetDevice(&dev);
   std::atomic<int>& cap = caps[dev & 63];
   if (!cap) {
-    cudaFuncSetAttribute(p2p_merge_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(p2p_merge_kernel<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(p2p_merge_kernel<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_merge_kernel<P>, kThreads, smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess ||
         per_sm < 1) {
       cudaGetLastError();
       per_sm = 1;
@@ -745,7 +773,7 @@ static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtr
   }
   const uint64_t ntiles = W ? (lo + W - 1) / kMergeTile - lo / kMergeTile + 1 : 0;
   const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, uint64_t(cap))));
-  p2p_merge_kernel<P><<<grid, kThreads, smem, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
+  kern<<<grid, kThreads, smem, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
   ++L.launches;
   return cudaGetLastError();
 }
@@ -801,9 +829,12 @@ cudaError_t launch_p2p_barrier(Launch& L, const PeerTab* d_tab, uint64_t epoch, 
 
 const void* p2p_merge_func(int P) {
   switch (P) {
-    case 2: return reinterpret_cast<const void*>(p2p_merge_kernel<2>);
-    case 4: return reinterpret_cast<const void*>(p2p_merge_kernel<4>);
-    case 8: return reinterpret_cast<const void*>(p2p_merge_kernel<8>);
+    case 2: return merge_tma() ? reinterpret_cast<const void*>(p2p_merge_kernel<2, true>)
+                               : reinterpret_cast<const void*>(p2p_merge_kernel<2, false>);
+    case 4: return merge_tma() ? reinterpret_cast<const void*>(p2p_merge_kernel<4, true>)
+                               : reinterpret_cast<const void*>(p2p_merge_kernel<4, false>);
+    case 8: return merge_tma() ? reinterpret_cast<const void*>(p2p_merge_kernel<8, true>)
+                               : reinterpret_cast<const void*>(p2p_merge_kernel<8, false>);
   }
   return nullptr;
 }
@@ -814,9 +845,12 @@ const void* p2p_restore_func() { return reinterpret_cast<const void*>(p2p_restor
 // (see preload_kernels in okt_kernels.cu)
 void preload_p2p_kernels() {
   cudaFuncAttributes a;
-  for (const void* f : {reinterpret_cast<const void*>(p2p_merge_kernel<2>),
-                        reinterpret_cast<const void*>(p2p_merge_kernel<4>),
-                        reinterpret_cast<const void*>(p2p_merge_kernel<8>),
+  for (const void* f : {reinterpret_cast<const void*>(p2p_merge_kernel<2, false>),
+                        reinterpret_cast<const void*>(p2p_merge_kernel<4, false>),
+                        reinterpret_cast<const void*>(p2p_merge_kernel<8, false>),
+                        reinterpret_cast<const void*>(p2p_merge_kernel<2, true>),
+                        reinterpret_cast<const void*>(p2p_merge_kernel<4, true>),
+                        reinterpret_cast<const void*>(p2p_merge_kernel<8, true>),
                         reinterpret_cast<const void*>(p2p_pull_kernel), reinterpret_cast<const void*>(p2p_totals_kernel),
                         reinterpret_cast<const void*>(p2p_restore_kernel),
                         reinterpret_cast<const void*>(p2p_barrier_kernel)})
