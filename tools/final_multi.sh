@@ -6,6 +6,11 @@ set -u
 OUT=${1:-gpurun_out/final_multi}
 MAXG=${2:-4}
 mkdir -p "$OUT"
+timeout 900 python bench.py > "$OUT/bench_n1.log" 2>&1
+timeout 900 python bench.py --impl reference > "$OUT/ref_n1.log" 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -c 300 --csv --log-file "$OUT/launches_n1.csv" python bench.py --steps 6 --warmup 3 --no-cpu-baseline \
+    --e2e-steps 2 > "$OUT/ncu_list.log" 2>&1
 N=2
 while [ "$N" -le "$MAXG" ]; do
   TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1"
