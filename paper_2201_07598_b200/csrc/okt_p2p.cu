@@ -41,8 +41,18 @@ constexpr uint32_t kAbortBits = 1u | 8u | 16u;  // local non-finite, peer timeou
 constexpr int kMergeTile = kK1Tile;              // coordinates per CTA tile
 constexpr int kMergePer = kMergeTile / kThreads;  // 16 coordinates per thread in the scan
 template <int P>
-__host__ __device__ constexpr int merge_stages() { return P <= 4 ? 6 : 4; }  // tiles of entries in flight per CTA
-constexpr int kMergeRing = 128;                   // entries per source per ring stage
+// tiles of entries in flight per CTA (OKT_MERGE_STAGES_* at build time, A/B)
+#ifndef OKT_MERGE_STAGES_SMALL
+#define OKT_MERGE_STAGES_SMALL 12
+#endif
+#ifndef OKT_MERGE_STAGES_P8
+#define OKT_MERGE_STAGES_P8 6
+#endif
+__host__ __device__ constexpr int merge_stages() { return P <= 4 ? OKT_MERGE_STAGES_SMALL : OKT_MERGE_STAGES_P8; }
+#ifndef OKT_MERGE_RING
+#define OKT_MERGE_RING 96
+#endif
+constexpr int kMergeRing = OKT_MERGE_RING;        // entries per source per ring stage (a denser tile's rest: direct)
 constexpr int kMergeCntCap = 256;                 // tiles whose counts are staged at once
 
 template <int P>
@@ -116,7 +126,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // allows 6), so more of the region's tiles are in flight at once (interleaved
 // A/B on one box, tools/ab_lib.sh: steady N = 2 0.0812 -> 0.0799 ms).
 template <int P, bool TMA>
-__global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
+__global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
     p2p_merge_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo, uint64_t W,
                      uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns) {
   extern __shared__ uint32_t sm[];
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 5 : 2)
   for (int r = 0; r < P; ++r) seg_mine[r] = 0;
   uint64_t ph_acc[4] = {0, 0, 0, 0};  // diagnostics (trace on): ns in wait / scatter / scan / emit, thread 0
   for (int w = q; w < kMergeTile / 16; w += kThreads) reinterpret_cast<uint4*>(s_mask)[w] = make_uint4(0, 0, 0, 0);
-  __shared__ __align__(8) uint64_t s_mbar[8];  // one per ring stage
+  __shared__ __align__(8) uint64_t s_mbar[32];  // one per ring stage
   if (q == 0) {
     for (int st = 0; st < kS; ++st) mbar_init(&s_mbar[st], 1);
     fence_proxy_async_smem();  // (the initialised barriers, visible to the copy engine)
