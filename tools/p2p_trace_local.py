@@ -17,7 +17,7 @@ from paper_2201_07598_b200 import oktopk as ok  # noqa: E402
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 out = sys.argv[3] if len(sys.argv) > 3 else "gpurun_out/p2p_local"
-n = 14_728_266
+n = int(os.environ.get("OKT_N", "14728266"))
 k = n // 100
 L = _lib.lib()
 w = ok.World(P, list(range(P)))
@@ -46,3 +46,14 @@ for r in range(P):
     a = np.frombuffer(buf, dtype=np.uint64).reshape(kinds, ctas, 4).astype(np.int64)
     np.save(os.path.join(out, f"p2p_trace_rank{r}.npy"), a)
     print("rank", r, "trace rc", rc, "U", U[r])
+    used = a[1, :, 0] > 0
+    t0 = a[0, :, 0][a[0, :, 0] > 0].min()
+    for kind, nm in ((0, "k1"), (1, "merge"), (3, "pull"), (2, "restore")):
+        u = a[kind, :, 0] > 0
+        if u.any():
+            print(f"  {nm}: start {(a[kind, u, 0].min() - t0) / 1e3:.1f} us, end {(a[kind, u, 2].max() - t0) / 1e3:.1f} us,"
+                  f" waited {(a[kind, u, 1].max() - t0) / 1e3:.1f} us")
+    ph = a[4][(a[4] > 0).any(axis=1)]
+    if ph.size:
+        print("  merge phases (median per CTA, us):", [round(float(np.median(ph[:, i])) / 1e3, 1) for i in range(4)])
+
