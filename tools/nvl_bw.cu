@@ -6,6 +6,7 @@
 // bulk copies.  Prints GB/s per pattern.
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e_)); return 1; } } while (0)
@@ -36,6 +37,25 @@ __global__ void rd_pieces_ldg(const uint4* __restrict__ src, int pieces, float* 
     for (int u = 0; u < 4; ++u) {
       const int pp = p + u * nwarps;
       v[u] = (pp < pieces && lane < 21) ? src[size_t(pp) * 2048 + lane] : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += v[u].x;
+  }
+  if (acc == 12345u) out[0] = float(acc);
+}
+// CTA-span order: CTA b walks pieces [b * span, (b + 1) * span) (the merge's
+// contiguous tile spans); 8 warps take consecutive pieces of the span
+__global__ void rd_pieces_span(const uint4* __restrict__ src, int pieces, float* out) {
+  uint32_t acc = 0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int span = (pieces + gridDim.x - 1) / gridDim.x;
+  const int p0 = blockIdx.x * span, p1 = min(pieces, p0 + span);
+  for (int p = p0 + w; p < p1; p += nw * 4) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int pp = p + u * nw;
+      v[u] = (pp < p1 && lane < 21) ? src[size_t(pp) * 2048 + lane] : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc += v[u].x;
@@ -96,11 +116,11 @@ __global__ void rd_pieces_tma(const uint4* __restrict__ src, int pieces, float* 
   if (acc == 12345u) out[0] = float(acc);
 }
 
-int main() {
+int main(int argc, char** argv) {
   int n = 0;
   cudaGetDeviceCount(&n);
   if (n < 2) { printf("needs 2 GPUs\n"); return 0; }
-  const size_t bytes = size_t(1) << 30;
+  const size_t bytes = size_t(argc > 1 ? atoi(argv[1]) : 1) << 30;  // GiB per buffer
   void *b0, *b1;
   float* out;
   CK(cudaSetDevice(1));
@@ -132,6 +152,7 @@ int main() {
   timeit("remote write, coalesced 16 B stores", double(bytes), [&] { wr_coalesced<<<sms * 8, 256>>>((float4*)b1, n4); });
   const int pieces = int(bytes / 32768);
   timeit("remote 336 B pieces / 32 KB slot, LDG", double(pieces) * 336, [&] { rd_pieces_ldg<<<sms * 8, 256>>>((const uint4*)b1, pieces, out); });
+  timeit("remote 336 B pieces, CTA-span order, LDG", double(pieces) * 336, [&] { rd_pieces_span<<<sms * 2, 256>>>((const uint4*)b1, pieces, out); });
   timeit("remote 336 B pieces / 32 KB slot, LDGSTS", double(pieces) * 336, [&] { rd_pieces_ldgsts<<<sms * 8, 256>>>((const uint4*)b1, pieces, out); });
   timeit("remote 336 B pieces / 32 KB slot, TMA bulk", double(pieces) * 336, [&] { rd_pieces_tma<<<sms * 8, 32>>>((const uint4*)b1, pieces, out); });
   timeit("local 336 B pieces / 32 KB slot, LDG", double(pieces) * 336, [&] { rd_pieces_ldg<<<sms * 8, 256>>>((const uint4*)b0, pieces, out); });
