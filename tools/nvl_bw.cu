@@ -155,6 +155,52 @@ int main(int argc, char** argv) {
   timeit("remote 336 B pieces, CTA-span order, LDG", double(pieces) * 336, [&] { rd_pieces_span<<<sms * 2, 256>>>((const uint4*)b1, pieces, out); });
   timeit("remote 336 B pieces / 32 KB slot, LDGSTS", double(pieces) * 336, [&] { rd_pieces_ldgsts<<<sms * 8, 256>>>((const uint4*)b1, pieces, out); });
   timeit("remote 336 B pieces / 32 KB slot, TMA bulk", double(pieces) * 336, [&] { rd_pieces_tma<<<sms * 8, 32>>>((const uint4*)b1, pieces, out); });
+  // both GPUs at once: GPU 0 reads GPU 1's buffer while GPU 1 reads GPU 0's (the merge's all-to-all)
+  {
+    CK(cudaSetDevice(1));
+    CK(cudaDeviceEnablePeerAccess(0, 0));
+    float* out1;
+    CK(cudaMalloc(&out1, 64));
+    cudaStream_t s1;
+    cudaStreamCreate(&s1);
+    CK(cudaSetDevice(0));
+    cudaStream_t s0;
+    cudaStreamCreate(&s0);
+    auto both = [&](bool pieces_mode) {
+      for (int r = 0; r < 5; ++r) {
+        CK(cudaSetDevice(0));
+        if (pieces_mode) rd_pieces_ldg<<<sms * 8, 256, 0, s0>>>((const uint4*)b1, pieces, out);
+        else rd_coalesced<<<sms * 8, 256, 0, s0>>>((const float4*)b1, n4, out);
+        CK(cudaSetDevice(1));
+        if (pieces_mode) rd_pieces_ldg<<<sms * 8, 256, 0, s1>>>((const uint4*)b0, pieces, out1);
+        else rd_coalesced<<<sms * 8, 256, 0, s1>>>((const float4*)b0, n4, out1);
+      }
+      CK(cudaSetDevice(0));
+      return 0;
+    };
+    for (int mode = 0; mode < 2; ++mode) {
+      both(mode);
+      CK(cudaSetDevice(1));
+      cudaDeviceSynchronize();
+      CK(cudaSetDevice(0));
+      cudaDeviceSynchronize();
+      cudaEvent_t a0, a1;
+      cudaEventCreate(&a0);
+      cudaEventCreate(&a1);
+      cudaEventRecord(a0, s0);
+      both(mode);
+      cudaEventRecord(a1, s0);
+      cudaEventSynchronize(a1);
+      CK(cudaSetDevice(1));
+      cudaDeviceSynchronize();
+      CK(cudaSetDevice(0));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a0, a1);
+      const double moved = mode ? double(pieces) * 336 : double(bytes);
+      printf("%-44s %8.1f GB/s per GPU\n", mode ? "BOTH ways at once: 336 B pieces, LDG" : "BOTH ways at once: coalesced reads",
+             moved * 5 / (ms * 1e-3) / 1e9);
+    }
+  }
   timeit("local 336 B pieces / 32 KB slot, LDG", double(pieces) * 336, [&] { rd_pieces_ldg<<<sms * 8, 256>>>((const uint4*)b0, pieces, out); });
   timeit("local 336 B pieces / 32 KB slot, TMA bulk", double(pieces) * 336, [&] { rd_pieces_tma<<<sms * 8, 32>>>((const uint4*)b0, pieces, out); });
   return 0;
