@@ -1049,7 +1049,8 @@ struct okt_comm {
     ap.seq = seq;
     ap.d_flags_next = fl_next;
     ap.trace = trbuf.as<uint64_t>();
-    ap.tag = ++compact_tag ? compact_tag : ++compact_tag;
+    ap.tag = ++compact_tag;  // (patched into the graph every step: a fresh tag per launch)
+    if (ap.tag < 2) ap.tag = compact_tag = 2;
     hfast->bad_iter = 0;
     if (p1_direct) {
       // The same two kernels launched directly, arguments and all (no graph):

@@ -255,7 +255,21 @@ static cudaError_t launch_compact(Launch& L, const Stage& S, uint32_t G, uint64_
   const uint32_t GB = std::max<uint32_t>(1, (G + per - 1) / per);
   const uint32_t* c2 = g2 ? S.counts2 : nullptr;
   ApplyArgs a = ap ? *ap : ApplyArgs{};
-  if (!a.tag) a.tag = ++*S.tag_ctr ? *S.tag_ctr : ++*S.tag_ctr;  // (0 never tags a launch)
+  if (!a.tag) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(L.s, &cs);
+    if (cs == cudaStreamCaptureStatusActive) {
+      // captured into a graph, the launch's arguments (its tag) repeat at every
+      // replay: clear the look-back words in the graph first and use tag 1
+      // (the counter below starts at 2, so no direct launch reuses it)
+      const cudaError_t e = cudaMemsetAsync(S.agg, 0, sizeof(uint64_t) * GB, L.s);
+      if (e != cudaSuccess) return e;
+      a.tag = 1;
+    } else {
+      a.tag = ++*S.tag_ctr;
+      if (a.tag < 2) a.tag = *S.tag_ctr = 2;  // (0 never tags a launch; 1 is the graphs')
+    }
+  }
   if (MODE == 1 && a.k7)
     compact_kernel<MODE, true><<<GB, kThreads, 0, L.s>>>(S.s64, S.sidx, S.sval, S.counts, c2, g2, G, cap_host, d_cap,
                                                          o64, oidx, oval, d_total, d_total2, S.agg, a);
