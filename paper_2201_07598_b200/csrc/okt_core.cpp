@@ -1331,16 +1331,22 @@ struct okt_comm {
       if (sgd) {
         tmark(OKT_T_SELECT, s);
         rc = ck(okt::launch_radix_init(L, &d()->rs, k, n, nullptr), "radix_init");
-        // Refresh candidates (single rank): thresholds drift slowly between
-        // refreshes, so K1's accumulate pass also emits every entry with
+        // Refresh candidates: thresholds drift slowly between refreshes, so a
+        // warm refresh's K1 accumulate pass also emits every entry with
         // |acc| >= local_th_old / 2.  When at least k entries qualify, the
-        // k-th largest is among them: the exact radix select, the survivor
-        // selection and K7 then run over the candidates, instead of two more
-        // radix passes and a second select pass over all n (at n = 340M:
-        // 0.39 + 0.43 ms).  Otherwise the dense passes below run as before
-        // (pass 0's histogram came out of the same K1 pass).
-        const bool cand = cand_on && st.local_th > 0.0 && std::isfinite(st.local_th);
-        if (cand) {
+        // k-th largest is among them: the exact radix select, the local
+        // selection / survivor selection and K7 then run over the candidates,
+        // instead of two more radix passes and a second select pass over all n
+        // (at n = 340M: 0.39 + 0.43 ms).  Otherwise the dense passes run as
+        // before (pass 0's histogram came out of the same K1 pass).
+        // Cold refresh (no previous threshold): pass 0's histogram picks the
+        // top-11-bit bin holding the k-th largest, and a select-only K1 pass
+        // over acc emits everything at or above that bin as the candidates —
+        // instead of two more radix passes and a second select pass.
+        const bool warm = cand_on && st.local_th > 0.0 && std::isfinite(st.local_th);
+        bool have_cand = false;  // candidates in coo (AoS) with count d()->R, at least k of them
+        uint64_t C_bound = n;    // (grid sizing of the candidate kernels)
+        if (warm) {
           if (!rc) rc = upload_f64(&d()->th_arg, 0.5 * st.local_th, &hup->th_arg, s);
           if (!rc) rc = ck(okt::launch_k1(L, S, okt::K1Mode::kAccumSelectHist, g, eps_in, eps_out, fa, n,
                                           &d()->th_arg, nullptr, okt::OutCoo{coo.as<uint64_t>()}, &d()->R, nullptr,
@@ -1351,33 +1357,9 @@ struct okt_comm {
             dev_stale = true;
             return set_err(OKT_ERR_NUMERIC, "ok_sparse_allreduce: non-finite input");
           }
-          const uint64_t C = h->R;
-          if (C >= k && P > 1) {
-            // the local selection {|acc| >= local_th} = the qualifying candidates, as AoS for the split
-            tmark(OKT_T_THRESHOLD, s);
-            rc = ck(cudaMemsetAsync(hp, 0, 2048 * sizeof(uint32_t), s), "memset");
-            if (!rc) rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kAosF32, coo.p, 0, &d()->R, C, k, &d()->rs,
-                                                      hp, &d()->local_th, false), "radix");
-            tmark(OKT_T_SELECT, s);
-            if (!rc) rc = ck(okt::launch_filter(L, S, true, coo.as<uint64_t>(), nullptr, nullptr, &d()->R, C,
-                                                &d()->local_th, nullptr, nullptr, &d()->m, nullptr,
-                                                coo.as<uint64_t>()), "filter");
-            sel_done = true;
-          } else if (C >= k) {
-            tmark(OKT_T_THRESHOLD, s);
-            rc = ck(cudaMemsetAsync(hp, 0, 2048 * sizeof(uint32_t), s), "memset");
-            if (!rc) rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kAosF32, coo.p, 0, &d()->R, C, k, &d()->rs,
-                                                      hp, &d()->local_th, false), "radix");
-            tmark(OKT_T_SELECT, s);
-            if (!rc) rc = ck(cudaMemcpyAsync(&d()->global_th, &d()->local_th, 8, cudaMemcpyDeviceToDevice, s), "copy");
-            if (!rc) rc = ck(okt::launch_filter(L, S, true, coo.as<uint64_t>(), nullptr, nullptr, &d()->R, C,
-                                                &d()->local_th, sur_idx.as<uint32_t>(), sur_val.as<double>(),
-                                                &d()->S), "filter");
-            if (!rc) rc = ck(cudaMemcpyAsync(&d()->m, &d()->S, 8, cudaMemcpyDeviceToDevice, s), "copy");
-            tmark(OKT_T_APPLY, s);
-            if (!rc) rc = ck(okt::launch_apply_u(L, sur_idx.as<uint32_t>(), sur_val.as<double>(), &d()->S, C, eps_out,
-                                                 w, &d()->flags), "apply");
-            sel_done = true;
+          if (h->R >= k) {
+            have_cand = true;
+            C_bound = h->R;
           } else {
             tmark(OKT_T_THRESHOLD, s);
             rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kDenseF32, acc, n, nullptr, n, k, &d()->rs, hp,
@@ -1387,8 +1369,41 @@ struct okt_comm {
           if (!rc) rc = ck(okt::launch_k1(L, S, okt::K1Mode::kAccumHist, g, eps_in, eps_out, fa, n, nullptr, nullptr,
                                           okt::OutCoo{}, nullptr, nullptr, &d()->flags, hp), "k1");
           tmark(OKT_T_THRESHOLD, s);
-          if (!rc) rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kDenseF32, acc, n, nullptr, n, k, &d()->rs,
-                                                    hp, &d()->local_th, true), "radix");
+          if (cand_on) {
+            if (!rc) rc = ck(okt::launch_radix_pass0_floor(L, &d()->rs, hp, &d()->th_arg), "radix");
+            tmark(OKT_T_SELECT, s);
+            if (!rc) rc = ck(okt::launch_k1(L, S, okt::K1Mode::kSelect, acc, nullptr, nullptr, 0.f, n, &d()->th_arg,
+                                            nullptr, okt::OutCoo{coo.as<uint64_t>()}, &d()->R, nullptr, &d()->flags,
+                                            nullptr), "k1");
+            have_cand = true;
+          } else if (!rc) {
+            rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kDenseF32, acc, n, nullptr, n, k, &d()->rs, hp,
+                                             &d()->local_th, true), "radix");
+          }
+        }
+        if (have_cand) {
+          // the exact k-th largest among the candidates, then the local
+          // selection (P > 1, AoS for the split) or u with K7 (P = 1)
+          tmark(OKT_T_THRESHOLD, s);
+          if (!rc) rc = ck(cudaMemsetAsync(hp, 0, 2048 * sizeof(uint32_t), s), "memset");
+          if (!rc) rc = ck(okt::launch_radix_select(L, okt::RadixSrc::kAosF32, coo.p, 0, &d()->R, C_bound, k,
+                                                    &d()->rs, hp, &d()->local_th, false), "radix");
+          tmark(OKT_T_SELECT, s);
+          if (P > 1) {
+            if (!rc) rc = ck(okt::launch_filter(L, S, true, coo.as<uint64_t>(), nullptr, nullptr, &d()->R, C_bound,
+                                                &d()->local_th, nullptr, nullptr, &d()->m, nullptr,
+                                                coo.as<uint64_t>()), "filter");
+          } else {
+            if (!rc) rc = ck(cudaMemcpyAsync(&d()->global_th, &d()->local_th, 8, cudaMemcpyDeviceToDevice, s), "copy");
+            if (!rc) rc = ck(okt::launch_filter(L, S, true, coo.as<uint64_t>(), nullptr, nullptr, &d()->R, C_bound,
+                                                &d()->local_th, sur_idx.as<uint32_t>(), sur_val.as<double>(),
+                                                &d()->S), "filter");
+            if (!rc) rc = ck(cudaMemcpyAsync(&d()->m, &d()->S, 8, cudaMemcpyDeviceToDevice, s), "copy");
+            tmark(OKT_T_APPLY, s);
+            if (!rc) rc = ck(okt::launch_apply_u(L, sur_idx.as<uint32_t>(), sur_val.as<double>(), &d()->S, C_bound,
+                                                 eps_out, w, &d()->flags), "apply");
+          }
+          sel_done = true;
         }
       } else {
         tmark(OKT_T_THRESHOLD, s);

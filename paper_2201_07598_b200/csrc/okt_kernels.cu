@@ -1228,6 +1228,20 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// After pass 0's histogram of dense f32 magnitudes: pick the top-11-bit bin
+// holding the kk-th largest and write the bin's smallest magnitude to *d_floor
+// (every value at or above it is a candidate; at least kk of them exist).
+__global__ void radix_floor_kernel(const RadixState* rs, double* d_floor) {
+  *d_floor = rs->active ? double(__uint_as_float(uint32_t(rs->prefix))) : 0.0;
+}
+
+cudaError_t launch_radix_pass0_floor(Launch& L, RadixState* d_rs, uint32_t* d_hist, double* d_floor) {
+  radix_pick_kernel<<<1, 1024, 0, L.s>>>(d_rs, d_hist, 20, 11, 0, 0, nullptr);
+  radix_floor_kernel<<<1, 1, 0, L.s>>>(d_rs, d_floor);
+  L.launches += 2;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_radix_init(Launch& L, RadixState* d_rs, uint64_t k, uint64_t n_host,
                               const uint64_t* d_n) {
   radix_init_kernel<<<1, 1, 0, L.s>>>(d_rs, k, n_host, d_n);
@@ -1495,6 +1509,7 @@ void preload_kernels() {
   touch(reinterpret_cast<const void*>(radix_hist_kernel<1>));
   touch(reinterpret_cast<const void*>(radix_hist_kernel<2>));
   touch(reinterpret_cast<const void*>(radix_pick_kernel));
+  touch(reinterpret_cast<const void*>(radix_floor_kernel));
   touch(reinterpret_cast<const void*>(slice_offsets_kernel));
   touch(reinterpret_cast<const void*>(proposals_kernel));
   touch(reinterpret_cast<const void*>(cuts_kernel));

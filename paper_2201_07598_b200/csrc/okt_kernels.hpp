@@ -118,6 +118,9 @@ cudaError_t launch_radix_select(Launch& L, RadixSrc src, const void* data,
                                 uint64_t n_host, const uint64_t* d_n, uint64_t n_bound,
                                 uint64_t k, RadixState* d_rs, uint32_t* d_hist,
                                 double* d_th_out, bool hist0_done);
+// After a fused pass-0 histogram: the pass-0 pick, then the smallest magnitude
+// of the chosen bin into *d_floor (the cold refresh's candidate threshold).
+cudaError_t launch_radix_pass0_floor(Launch& L, RadixState* d_rs, uint32_t* d_hist, double* d_floor);
 // Zero-initialises the radix state before a fused pass-0 histogram.
 cudaError_t launch_radix_init(Launch& L, RadixState* d_rs, uint64_t k, uint64_t n_host,
                               const uint64_t* d_n);
