@@ -105,6 +105,8 @@ struct DevScalars {
   uint32_t small[2];
   uint32_t small_all[2 * OKT_MAX_WORLD];
   okt::RadixState rs;
+  uint32_t merge_ctr[2];  // the P2P merge's span tickets (its last CTA re-arms them)
+  uint64_t k1_tot[okt::kP2PMaxP + 1];  // P2P K1's totals accumulators (its last CTA publishes and clears them)
 };
 
 bool is_pow2(int v) { return v >= 1 && (v & (v - 1)) == 0; }
@@ -179,9 +181,6 @@ struct okt_comm {
   std::unique_ptr<okt::Transport> tr;
   cudaStream_t own = nullptr;
   cudaEvent_t ready_ev = nullptr;
-  // side branch of the P2P step (K1's totals, off the critical path)
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   Launch L;
   okt_state st = default_state();
   bool dev_stale = true;  // device thresholds / cuts must be re-uploaded
@@ -814,6 +813,9 @@ struct okt_comm {
       kp.plan_zero = &d()->plan;
       kp.spv = hup->sp;
     }
+    kp.tot_acc = d()->k1_tot;
+    kp.d_off = d()->off;
+    kp.d_m = &d()->m;
     return kp;
   }
 
@@ -846,23 +848,19 @@ struct okt_comm {
     tmark(OKT_T_SELECT, s);
     okt::K1P2P kp = k1p2p_args(argfed);
     kp.zero_sel = sgd ? 1 : 0;
+    kp.hout = sgd ? hp2p_dev : nullptr;  // (K1's last CTA: selection size and slice offsets)
     if (!rc)
       rc = ck(okt::launch_k1(L, S, sgd ? okt::K1Mode::kAccumSelect : okt::K1Mode::kSelect, hup->sp.g,
                              hup->sp.eps_in, hup->sp.eps_out, hup->sp.alpha, n, &d()->local_th, nullptr,
                              okt::OutCoo{}, &d()->m, nullptr, fl, nullptr, nullptr, &kp, argfed ? nullptr : sp),
               "k1");
-    // K1's totals (selection size, slice offsets) on a side branch
-    okt::K1Totals kt;
-    kt.d_m = &d()->m;
-    kt.d_off = d()->off;
-    if (!rc) rc = ck(cudaEventRecord(ev_fork, s), "fork");
-    if (!rc) rc = ck(cudaStreamWaitEvent(side, ev_fork, 0), "fork");
-    if (!rc) rc = ck(okt::launch_p2p_totals(L, side, dt, sp, P, kt, sgd ? hp2p_dev : nullptr), "totals");
-    if (!rc) rc = ck(cudaEventRecord(ev_join, side), "join");
+    // (K1's totals — selection size, slice offsets — come from K1's last CTA:
+    // a side-stream kernel for them held SMs the merge's CTAs then waited for)
     tmark(OKT_T_MERGE, s);
     // split exchange + region merge in one kernel (reads every source's K1
     // tiles of my region in place)
-    if (!rc) rc = ck(okt::launch_p2p_merge(L, dt, sp, dp, P, lo, W, n, &d()->global_th, fl, kP2PTimeoutNs), "p2p");
+    if (!rc) rc = ck(okt::launch_p2p_merge(L, dt, sp, dp, P, lo, W, n, &d()->global_th, fl, kP2PTimeoutNs,
+                                                  d()->merge_ctr), "p2p");
     tmark(OKT_T_ALLGATHER, s);
     okt::P2PApply pa;
     pa.on = 1;
@@ -889,7 +887,6 @@ struct okt_comm {
                                                 indexes.as<uint32_t>(), &d()->nidx, &d()->flags), "indexes");
     }
     tstop(s);
-    if (!rc) rc = ck(cudaStreamWaitEvent(s, ev_join, 0), "join");
     // EF steps hand their results back through mapped host memory (hp2p); the
     // plain allreduce (indexes, ...) reads the scalars back with one D2H
     if (!rc && !sgd) rc = ck(cudaMemcpyAsync(h, d(), sizeof(DevScalars), cudaMemcpyDeviceToHost, s), "d2h");
@@ -938,7 +935,6 @@ struct okt_comm {
         cudaGraphGetNodes(graph, nodes.data(), &nn);
         const void* fm = okt::p2p_merge_func(P);
         const void* fp = okt::p2p_pull_func();
-        const void* ft = okt::p2p_totals_func();
         const void* fr = okt::p2p_restore_func();
         for (cudaGraphNode_t nd : nodes) {
           cudaGraphNodeType ty;
@@ -948,7 +944,7 @@ struct okt_comm {
           cudaGraphKernelNodeGetParams(nd, &kp);
           if (kp.func == fm) G.merge = nd;
           else if (kp.func == fp) G.pull = nd;
-          else if (kp.func != ft && kp.func != fr) G.k1 = nd;
+          else if (kp.func != fr) G.k1 = nd;
         }
       }
       const cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
@@ -978,9 +974,10 @@ struct okt_comm {
       uint32_t* fl = &d()->p2pflags[hup->sp.par];
       okt::K1P2P kp = k1p2p_args(true);
       kp.zero_sel = 1;
+      kp.hout = hp2p_dev;
       if ((rc = patch_node(G.exec, G.k1, kK1Args, {{0, &hup->sp.g}, {1, &hup->sp.eps_in}, {2, &hup->sp.eps_out},
                                               {3, &hup->sp.alpha}, {12, &fl}, {15, &kp}})) ||
-          (rc = patch_node(G.exec, G.merge, 9, {{7, &fl}})) || (rc = patch_node(G.exec, G.pull, 10, {{5, &fl}})))
+          (rc = patch_node(G.exec, G.merge, 11, {{7, &fl}})) || (rc = patch_node(G.exec, G.pull, 10, {{5, &fl}})))
         return rc;
     }
     if ((rc = ck(cudaGraphLaunch(G.exec, s), "graph launch"))) return rc;
@@ -1681,10 +1678,7 @@ int init_comm(okt_comm* c) {
     cudaGetLastError();
   }
   if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ready_ev, cudaEventDisableTiming) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ready_ev, cudaEventDisableTiming) != cudaSuccess) {
     return set_err(OKT_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(cudaGetLastError()));
   }
   c->L.s = c->own;
@@ -1852,9 +1846,6 @@ int okt_comm_destroy(okt_comm* c) {
   c->tr.reset();
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->ready_ev) cudaEventDestroy(c->ready_ev);
-  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-  if (c->ev_join) cudaEventDestroy(c->ev_join);
-  if (c->side) cudaStreamDestroy(c->side);
   if (c->h) cudaFreeHost(c->h);
   if (c->hup) cudaFreeHost(c->hup);
   if (c->hfast) cudaFreeHost(c->hfast);

@@ -360,6 +360,11 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
   }
   bool bad = false;
   uint32_t mloc = 0;
+  // P2P: this CTA's share of the totals, slot d < P (below cut d) kept by
+  // thread d, slot kMaxP (all) by thread 0 (in shared memory: K1's P2P
+  // variant is at its 64-register cap; < 2^32 — fewer entries than n < 2^32)
+  __shared__ uint32_t s_tot[kMaxP + 1];
+  if (tid <= kMaxP) s_tot[tid] = 0;  // (each slot read and written by one thread only)
   if (tid == 0) s_tile[0] = atomicAdd(&tile_ctr[0], 1u);
   __syncthreads();
   for (int parity = 0;; parity ^= 1) {
@@ -472,8 +477,10 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
       if (tid == 0) counts[tile] = total;
       if (tid < lt_P) {
         // a cut inside the tile: the count below it; else all or nothing
-        lt_out[uint64_t(tile) * kMaxP + tid] =
-            ((cut_mask >> tid) & 1u) ? s_below[parity][tid] : (s_cut[tid] <= base ? 0u : total);
+        const uint32_t below = ((cut_mask >> tid) & 1u) ? s_below[parity][tid] : (s_cut[tid] <= base ? 0u : total);
+        lt_out[uint64_t(tile) * kMaxP + tid] = below;
+        s_tot[tid] += below;
+        if (tid == 0) s_tot[kMaxP] += total;
         s_below[parity][tid] = 0;  // reused two tiles later, after two barriers
       }
 #pragma unroll
@@ -497,6 +504,11 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
     const uint64_t s = block_sum(mloc, red);
     if (tid == 0) counts2[blockIdx.x] = uint32_t(s);
   }
+  if (p2p_on && p2p.tot_acc && tid < lt_P) {
+    if (s_tot[tid]) atomicAdd(reinterpret_cast<unsigned long long*>(&p2p.tot_acc[tid]), (unsigned long long)s_tot[tid]);
+    if (tid == 0 && s_tot[kMaxP])
+      atomicAdd(reinterpret_cast<unsigned long long*>(&p2p.tot_acc[kMaxP]), (unsigned long long)s_tot[kMaxP]);
+  }
   if (__syncthreads_or(bad) && tid == 0) {
     atomicOr(d_flags, 1u);
   }
@@ -510,6 +522,20 @@ __global__ void __launch_bounds__(kThreads, VEC ? 4 : 3)
     if (atomicAdd(&tile_ctr[1], 1u) == gridDim.x - 1) {
       tile_ctr[0] = 0;
       tile_ctr[1] = 0;
+      if (p2p_on && p2p.tot_acc) {
+        // every CTA's counts are in: publish the totals (and clear them)
+        const uint64_t all = atomicExch(reinterpret_cast<unsigned long long*>(&p2p.tot_acc[kMaxP]), 0ull);
+        for (int d = 0; d <= lt_P; ++d) {
+          const uint64_t o = d < lt_P ? atomicExch(reinterpret_cast<unsigned long long*>(&p2p.tot_acc[d]), 0ull) : all;
+          p2p.d_off[d] = o;
+          if (p2p.hout) p2p.hout->off[d] = o;
+        }
+        *p2p.d_m = all;
+        if (p2p.hout) {
+          p2p.hout->m = all;
+          p2p.hout->seq_tot = p2p.par_v >= 0 ? p2p.spv.epoch : p2p.sp->epoch;
+        }
+      }
       __threadfence();
     }
   }
@@ -1473,13 +1499,25 @@ cudaError_t launch_scatter_heavy(Launch& L, const uint32_t* pos, const float* va
 // loading a kernel is loaded at its first launch: the first warm refresh of a
 // run (the candidate path, t = tau' + 1) paid 13.6 ms for it at n = 1M
 // (round-2 sweep).  cudaFuncGetAttributes loads a function without running it.
+int carveout_pref() {
+  static const int v = [] {
+    const char* e = std::getenv("OKT_CARVEOUT");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
+}
+
 void preload_kernels() {
   static std::atomic<bool> done[64];  // per device: a module is loaded per context
   int dev = 0;
   cudaGetDevice(&dev);
   if (done[dev & 63].exchange(true)) return;
   cudaFuncAttributes a;
-  auto touch = [&](const void* f) { cudaFuncGetAttributes(&a, f); };
+  const int co = carveout_pref();
+  auto touch = [&](const void* f) {
+    cudaFuncGetAttributes(&a, f);
+    if (co >= 0) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, co);
+  };
 #define OKT_K1(A, S, H, D, AP)                                                   \
   touch(reinterpret_cast<const void*>(k1_kernel<A, S, H, true, D, AP>));         \
   touch(reinterpret_cast<const void*>(k1_kernel<A, S, H, false, D, AP>))

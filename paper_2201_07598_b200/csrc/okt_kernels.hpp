@@ -179,13 +179,15 @@ cudaError_t launch_scatter_heavy(Launch& L, const uint32_t* pos, const float* va
 // Split exchange + region merge of the steady P2P step (K1's per-tile staging
 // of every source read in place; survivors chunked into my window).
 cudaError_t launch_p2p_merge(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, int P, uint64_t lo,
-                             uint64_t W, uint64_t n, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns);
+                             uint64_t W, uint64_t n, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns,
+                             uint32_t* ctr);  // ctr: 2 words, zero before the first launch (re-armed by the kernel)
 // The P2P kernels, for per-step parameter updates of the instantiated step graph.
 const void* p2p_merge_func(int P);
 const void* p2p_pull_func();
-const void* p2p_totals_func();
 const void* p2p_restore_func();
 // Loads the path's kernels now (lazy module loading would load each at its first launch).
+// OKT_CARVEOUT=<0..100>: preferred shared-memory carveout for every kernel (-1: the driver default).
+int carveout_pref();
 void preload_kernels();
 void preload_p2p_kernels();
 // EF steps after the pull: acc back at the local entries outside u; clears the next step's u bitmap.
@@ -198,9 +200,6 @@ cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtr
 // Device barrier over the peer flags (okt_device_barrier).
 cudaError_t launch_p2p_barrier(Launch& L, const PeerTab* d_tab, uint64_t epoch, uint32_t* d_flags,
                                uint64_t timeout_ns);
-// This rank's selection size / slice offsets from K1's tile counts (side stream).
-cudaError_t launch_p2p_totals(Launch& L, cudaStream_t s, const PeerTab* d_tab, const StepPtrs* sp, int P,
-                              const K1Totals& totals, P2PHostOut* hout);
 // indexes = {u_idx[j] : sel[j]} in order (the K7 intersection, after a fused apply).
 cudaError_t launch_select_flags(Launch& L, const Stage& S, const uint8_t* sel, const PeerTab* d_tab,
                                 const StepPtrs* sp, const uint64_t* d_U, uint64_t bound, uint32_t* out,

@@ -2,7 +2,8 @@
 //
 // Steady Ok-Topk iteration on P ranks, no host round trip and no compaction
 // pass between a producer and its consumers (one CUDA graph):
-//   K1 (per-tile staging + per-tile cut counts in the window)
+//   K1 (per-tile staging + per-tile cut counts in the window; its last CTA
+//     publishes the selection size and slice offsets)
 //   merge: CTA 0 publishes L-ready; every CTA waits on its own flag copy, reads
 //     every source's K1 tiles of its region in place (NVLink) and runs the
 //     bracket scan / survivor filter in shared memory; survivors chunked into
@@ -10,7 +11,6 @@
 //   pull: CTA 0 publishes the survivor prefix and count; every CTA waits, plans
 //     (offsets, balance) and pulls every chunk to its position in u, applying
 //     K7 on the way [balanced: my block, an in-grid hand-off, the others]
-//   totals (side branch): selection size and slice offsets
 // Every publish is issued at a kernel start, while the rest of the grid only
 // polls: a system fence issued while the grid streams random stores waits for
 // that traffic to drain (tools/fence_lat.cu, tools/p2p_noise.cu).
@@ -53,7 +53,11 @@ __host__ __device__ constexpr int merge_stages() { return P <= 4 ? OKT_MERGE_STA
 #define OKT_MERGE_RING 96
 #endif
 constexpr int kMergeRing = OKT_MERGE_RING;        // entries per source per ring stage (a denser tile's rest: direct)
-constexpr int kMergeCntCap = 256;                 // tiles whose counts are staged at once
+constexpr int kMergeCntCap = 256;
+#ifndef OKT_MERGE_SPLIT_DEFAULT
+#define OKT_MERGE_SPLIT_DEFAULT 0
+#endif
+constexpr int kMergeSplit = OKT_MERGE_SPLIT_DEFAULT;  // survivor spans per merge CTA, ticketed (0: one, static)                 // tiles whose counts are staged at once
 
 template <int P>
 __host__ __device__ constexpr size_t merge_smem() {  // mask bytes, values [P][tile], ring [S][P][kMergeRing], counts
@@ -128,7 +132,8 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int P, bool TMA>
 __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
     p2p_merge_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo, uint64_t W,
-                     uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns) {
+                     uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns,
+                     uint32_t split, uint32_t* ctr) {
   extern __shared__ uint32_t sm[];
   uint32_t* s_mask = sm;                                             // [kMergeTile / 4]: byte per coordinate, bit per source
   float* s_val = reinterpret_cast<float*>(sm + kMergeTile / 4);      // [P][kMergeTile]
@@ -148,12 +153,15 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
   const uint64_t hi = lo + W;
   const uint32_t t_lo = uint32_t(lo / kMergeTile);
   const uint32_t ntiles = W ? uint32_t((hi - 1) / kMergeTile) - t_lo + 1 : 0;
+  // survivor chunks: `split` per CTA, handed out by a ticket counter
+  // (split 0: one span per CTA, span = blockIdx.x, no tickets)
+  const uint32_t Gc = split ? max(1u, min(ntiles, gridDim.x * split)) : gridDim.x;
   if (blockIdx.x == 0) {
     // this rank's K1 output: status, then L-ready at every rank (the GPU is
     // quiet: K1 finished and nobody streams yet)
     if (q == 0) {
       P2PPub* pub = &tab->hdr[me]->pub[par];  // (read by this rank's pull)
-      pub->sur_G = gridDim.x;  // one survivor chunk per CTA
+      pub->sur_G = Gc;
       pub->sur_tiles = ntiles;
       trace_stamp(trace, kTrPubL, 0);
     }
@@ -182,10 +190,13 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
   uint32_t* const out_idx = tab->sidx[me][par];
   double* const out_val = tab->sval[me][par];
   uint32_t* const out_cnt = tab->scnt[me][par];
-  // This CTA's tiles: the contiguous span [j0, j0 + my_n) of the region, and
-  // its survivors: one contiguous chunk at j0 * kMergeTile (the span's
-  // capacity), count in out_cnt[blockIdx.x] — a few hundred large chunks per
-  // rank for the pull instead of one small chunk per tile.  The span's
+  // The region's tiles in Gc contiguous spans (a few per CTA), taken by
+  // ticket: the tiles are not equally dense (the later, heavier spans of a
+  // region took 1.3x as long as the first ones at BERT-L, N = 2), and a few
+  // CTAs start late behind the side stream's kernels.  Span c's survivors:
+  // one contiguous chunk at j0 * kMergeTile (the span's capacity), count in
+  // out_cnt[c] — a few hundred large chunks per rank for the pull instead of
+  // one small chunk per tile.  The span's
   // per-source counts are staged in shared memory first (all loads in flight
   // at once), then a kS-deep ring of TMA bulk copies (cp.async.bulk, one per
   // source and tile, issued by one thread, completion counted in bytes on the
@@ -197,10 +208,8 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
   uint64_t* const ring = reinterpret_cast<uint64_t*>(s_val + P * kMergeTile);    // [S][P][kMergeRing]
   constexpr int kS = merge_stages<P>();
   uint32_t* const s_cnt = reinterpret_cast<uint32_t*>(ring + kS * P * kMergeRing);  // [kMergeCntCap][P]
-  const uint32_t j0 = span_at(blockIdx.x, ntiles, gridDim.x);
-  const uint32_t my_n = span_at(blockIdx.x + 1, ntiles, gridDim.x) - j0;
-  const uint64_t out_base = uint64_t(j0) * kMergeTile;
-  uint32_t running = 0;  // survivors of this CTA so far (block-uniform)
+  __shared__ uint32_t s_tk[2];
+  if (q == 0) s_tk[0] = split ? atomicAdd(&ctr[0], 1u) : blockIdx.x;
   // entries received from each source (the ledger's split words), per thread:
   // reduced once at the end instead of a warp reduce + shared atomic per
   // source and tile
@@ -215,6 +224,20 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
     fence_proxy_async_smem();  // (the initialised barriers, visible to the copy engine)
   }
   uint32_t ph_bits = 0;  // the parity each stage's barrier completes next (every thread tracks it)
+  __syncthreads();
+  for (int tpar = 0;; tpar ^= 1) {
+  const uint32_t cidx = s_tk[tpar];
+  if (cidx >= Gc) break;
+  if (trace && q == 0 && tpar == 0 && blockIdx.x < kTraceCtas) {  // diagnostics: SM and first span of the CTA
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    trace[(uint64_t(kTrMerge) * kTraceCtas + blockIdx.x) * 4 + 3] = (uint64_t(smid) << 32) | cidx;
+  }
+  if (q == 0) s_tk[tpar ^ 1] = split ? atomicAdd(&ctr[0], 1u) : Gc;  // (read after this span's barriers)
+  const uint32_t j0 = span_at(cidx, ntiles, Gc);
+  const uint32_t my_n = span_at(cidx + 1, ntiles, Gc) - j0;
+  const uint64_t out_base = uint64_t(j0) * kMergeTile;
+  uint32_t running = 0;  // survivors of this span so far (block-uniform)
   for (uint32_t i0 = 0; i0 < my_n; i0 += kMergeCntCap) {
     const uint32_t ni = min(my_n - i0, uint32_t(kMergeCntCap));
     for (uint32_t x = q; x < ni * P; x += kThreads) {
@@ -346,7 +369,18 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
     if constexpr (!TMA) cp_async_wait<0>();
     __syncthreads();
   }
-  if (q == 0) out_cnt[blockIdx.x] = running;
+  if (q == 0) out_cnt[cidx] = running;
+  __syncthreads();  // (an empty span has no barrier of its own)
+  }
+  if (split && q == 0) {
+    // the last CTA out re-arms the ticket counter for the next launch
+    __threadfence();
+    if (atomicAdd(&ctr[1], 1u) == gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+      __threadfence();
+    }
+  }
   if (trace && q == 0 && blockIdx.x < kTraceCtas) {  // (the balanced pull's slots: free on merge-traced steps)
     uint64_t* tp = trace + (uint64_t(kTrPull1) * kTraceCtas + blockIdx.x) * 4;
     for (int x = 0; x < 4; ++x) tp[x] = ph_acc[x];
@@ -639,29 +673,6 @@ __global__ void __launch_bounds__(kThreads, 3)
   if (lane == 0) trace_stamp(trace, kTrPull0, 2);
 }
 
-// This rank's selection size and slice offsets from K1's per-tile counts (one
-// CTA per value: d < P the entries below cut d, d = P all), for the result and
-// the ledger.  Runs on a side stream, off the step's critical path.
-__global__ void __launch_bounds__(kThreads)
-    p2p_totals_kernel(const PeerTab* __restrict__ tab, const StepPtrs* sp, K1Totals lt, P2PHostOut* hout) {
-  __shared__ uint64_t red[kWarps];
-  const int P = tab->P, me = tab->rank, par = sp->par, d = blockIdx.x;
-  const uint32_t G = tab->hdr[me]->pub[par].k1_G;
-  uint64_t o = (d == P) ? strided_sum(tab->kcnt[me][par], G) : strided_sum(tab->klt[me][par] + d, G, kP2PMaxP);
-  o = block_sum(o, red);
-  if (threadIdx.x == 0) {
-    lt.d_off[d] = o;
-    if (d == P) *lt.d_m = o;
-    if (hout) {
-      hout->off[d] = o;
-      if (d == P) {
-        hout->m = o;
-        hout->seq_tot = sp->epoch;
-      }
-    }
-  }
-}
-
 // EF steps, after the pull: the residual of every locally selected entry
 // outside u goes back to acc (K1 stored 0 for the whole local selection), so
 // eps ends as acc zeroed at indexes = local selection ∩ u (trainer.cpp:
@@ -763,7 +774,7 @@ static bool merge_tma() {
 template <int P>
 static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, uint64_t lo,
                                   uint64_t W, uint32_t k1_tiles, const double* d_gth, uint32_t* d_flags,
-                                  uint64_t timeout_ns) {
+                                  uint64_t timeout_ns, uint32_t* ctr) {
   constexpr size_t smem = merge_smem<P>();
   auto kern = merge_tma() ? p2p_merge_kernel<P, true> : p2p_merge_kernel<P, false>;
   static std::atomic<int> caps[64];  // per device (the dynamic-smem opt-in is per device)
@@ -783,18 +794,24 @@ static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtr
   }
   const uint64_t ntiles = W ? (lo + W - 1) / kMergeTile - lo / kMergeTile + 1 : 0;
   const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, uint64_t(cap))));
-  kern<<<grid, kThreads, smem, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
+  static const uint32_t split = [] {  // survivor spans per CTA (OKT_MERGE_SPLIT)
+    const char* e = std::getenv("OKT_MERGE_SPLIT");
+    const int v = e ? std::atoi(e) : kMergeSplit;
+    return uint32_t(std::max(0, std::min(v, 64)));
+  }();
+  kern<<<grid, kThreads, smem, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns, split, ctr);
   ++L.launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_p2p_merge(Launch& L, const PeerTab* d_tab, const StepPtrs* sp, P2PPlan* plan, int P, uint64_t lo,
-                             uint64_t W, uint64_t n, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns) {
+                             uint64_t W, uint64_t n, const double* d_gth, uint32_t* d_flags, uint64_t timeout_ns,
+                             uint32_t* ctr) {
   const uint32_t k1_tiles = uint32_t((n + kK1Tile - 1) / kK1Tile);
   switch (P) {
-    case 2: return merge_dispatch<2>(L, d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
-    case 4: return merge_dispatch<4>(L, d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
-    case 8: return merge_dispatch<8>(L, d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns);
+    case 2: return merge_dispatch<2>(L, d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns, ctr);
+    case 4: return merge_dispatch<4>(L, d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns, ctr);
+    case 8: return merge_dispatch<8>(L, d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns, ctr);
   }
   return cudaErrorInvalidValue;
 }
@@ -823,13 +840,6 @@ cudaError_t launch_p2p_allgatherv(Launch& L, const PeerTab* d_tab, const StepPtr
   return cudaGetLastError();
 }
 
-cudaError_t launch_p2p_totals(Launch& L, cudaStream_t s, const PeerTab* d_tab, const StepPtrs* sp, int P,
-                              const K1Totals& totals, P2PHostOut* hout) {
-  p2p_totals_kernel<<<P + 1, kThreads, 0, s>>>(d_tab, sp, totals, hout);
-  ++L.launches;
-  return cudaGetLastError();
-}
-
 cudaError_t launch_p2p_barrier(Launch& L, const PeerTab* d_tab, uint64_t epoch, uint32_t* d_flags,
                                uint64_t timeout_ns) {
   p2p_barrier_kernel<<<1, kThreads, 0, L.s>>>(d_tab, epoch, d_flags, timeout_ns);
@@ -849,7 +859,6 @@ const void* p2p_merge_func(int P) {
   return nullptr;
 }
 const void* p2p_pull_func() { return reinterpret_cast<const void*>(p2p_pull_kernel); }
-const void* p2p_totals_func() { return reinterpret_cast<const void*>(p2p_totals_kernel); }
 const void* p2p_restore_func() { return reinterpret_cast<const void*>(p2p_restore_kernel); }
 
 // (see preload_kernels in okt_kernels.cu)
@@ -861,10 +870,13 @@ void preload_p2p_kernels() {
                         reinterpret_cast<const void*>(p2p_merge_kernel<2, true>),
                         reinterpret_cast<const void*>(p2p_merge_kernel<4, true>),
                         reinterpret_cast<const void*>(p2p_merge_kernel<8, true>),
-                        reinterpret_cast<const void*>(p2p_pull_kernel), reinterpret_cast<const void*>(p2p_totals_kernel),
+                        reinterpret_cast<const void*>(p2p_pull_kernel),
                         reinterpret_cast<const void*>(p2p_restore_kernel),
                         reinterpret_cast<const void*>(p2p_barrier_kernel)})
+  {
     cudaFuncGetAttributes(&a, f);
+    if (carveout_pref() >= 0) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pref());
+  }
 }
 
 }  // namespace okt

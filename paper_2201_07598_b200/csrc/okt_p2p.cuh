@@ -47,7 +47,7 @@ struct P2PPub {
   uint64_t S;        // survivors of the global threshold
   uint32_t k1_G;     // K1 chunk geometry: chunks and entries per chunk
   uint32_t k1_cap;
-  uint32_t sur_G;     // survivor chunks: one per merge CTA (its contiguous span of tiles)
+  uint32_t sur_G;     // survivor chunks: contiguous spans of the region's tiles (a few per merge CTA)
   uint32_t sur_tiles; // merge tiles of the region (chunk c starts at split(c) * kK1Tile)
   uint64_t pad[4];
 };
@@ -157,10 +157,14 @@ struct K1P2P {
   // EF steps: store the residual of every locally selected entry as 0 (the
   // restore kernel puts acc back where the entry did not make it into u).
   int zero_sel = 0;
-};
-struct K1Totals {  // where the local selection size / slice offsets go
-  uint64_t* d_m = nullptr;
+  // This rank's selection size and slice offsets (the entries below cut d, d <
+  // P; all, d = P), for the result and the ledger: every CTA adds its tiles'
+  // counts into tot_acc (kP2PMaxP + 1 words, zero before the first launch),
+  // and the last CTA out publishes them to d_off / d_m (and hout) and re-arms.
+  uint64_t* tot_acc = nullptr;
   uint64_t* d_off = nullptr;
+  uint64_t* d_m = nullptr;
+  struct P2PHostOut* hout = nullptr;
 };
 
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {

@@ -1,10 +1,17 @@
 #!/usr/bin/env bash
-# Interleaved A/B of a diagnostics switch on one box:  tools/ab_env.sh N REPS VAR
-# (runs bench.py with VAR unset, then VAR=0)
-N=${1:-2}; R=${2:-2}; V=${3:-OKT_P2P_PULL_SPEC}
-run() { env $3 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port $1 \
-  bench.py --gpus $N --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$2', $N, round(d['ms_per_step'],4), round(d['steady_ms'],4))"; }
-for i in $(seq 1 $R); do
-  run $((29800 + i)) on ""
-  run $((29850 + i)) off "$V=0"
+# A/B of one environment switch at N GPUs: the BERT-L bench line and per-CTA P2P traces per value.
+# usage: tools/ab_env.sh OUTDIR N VAR "v1 v2 ..." [extra bench args]     (v = none: VAR unset)
+set -u
+OUT=${1:-gpurun_out/ab}; N=${2:-2}; VAR=$3; VALS=$4
+shift 4
+mkdir -p "$OUT"
+TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1"
+port=29541; i=0
+for v in $VALS; do
+  i=$((i+1)); tag="${i}_$v"
+  if [ "$v" = none ]; then unset "$VAR"; else export "$VAR=$v"; fi
+  timeout 600 $TR --master-port $port bench.py --gpus $N --no-cpu-baseline --e2e-steps 2 "$@" > "$OUT/bench_n${N}_$tag.log" 2>&1; port=$((port+1))
+  timeout 600 $TR --master-port $port bench.py --gpus $N --steps 12 --no-cpu-baseline --e2e-steps 2 \
+    --p2p-trace "$OUT/p2p_n${N}_$tag" "$@" > "$OUT/trace_n${N}_$tag.log" 2>&1; port=$((port+1))
 done
+echo done
