@@ -120,6 +120,28 @@ __device__ __forceinline__ uint64_t strided_sum(const uint32_t* p, uint32_t n, u
   return acc;
 }
 
+// A random 4-byte gather of a model / residual word (one per u entry): L2
+// only, with the 64-byte L2 prefetch-size hint.  Without a hint each such
+// gather pulled 128 B from DRAM (ncu at n = 340M, 3.4M gathers: phase B read
+// 445 MB in 161 us; with .L2::64B 275 MB in 144 us).  OKT_RAND_LD (A/B
+// builds): 0 no hint, 1 .L2::64B, 2 .L2::128B, 3 .L2::256B (487 MB).
+#ifndef OKT_RAND_LD
+#define OKT_RAND_LD 1
+#endif
+__device__ __forceinline__ float ld_rand(const float* p) {
+  float v;
+#if OKT_RAND_LD == 1
+  asm("ld.global.cg.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+#elif OKT_RAND_LD == 2
+  asm("ld.global.cg.L2::128B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+#elif OKT_RAND_LD == 3
+  asm("ld.global.cg.L2::256B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+#else
+  v = __ldcg(p);
+#endif
+  return v;
+}
+
 __device__ __forceinline__ uint64_t block_sum(uint64_t v, uint64_t* red) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kThreads)
       }
       // (L2-only 4-byte gathers: through L1 each random word pulled a whole
       // 128-byte line from DRAM — 445 MB read for 3.4M words at 340M, ncu)
-      wv[b] = (APPLY && j0 + uint64_t(b) * kThreads < cnt) ? __ldcg(ap.w + ei[b]) : 0.f;
+      wv[b] = (APPLY && j0 + uint64_t(b) * kThreads < cnt) ? ld_rand(ap.w + ei[b]) : 0.f;
     }
   };
   // The first batch is loaded before the global prefix is known: only the
@@ -727,7 +727,7 @@ __global__ void __launch_bounds__(kThreads)
       v[b] = e < cnt ? u_val[e] : 0.0;
     }
 #pragma unroll
-    for (int b = 0; b < B; ++b) wv[b] = e0 + uint64_t(b) * stride < cnt ? w[i[b]] : 0.f;
+    for (int b = 0; b < B; ++b) wv[b] = e0 + uint64_t(b) * stride < cnt ? ld_rand(w + i[b]) : 0.f;
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       if (e0 + uint64_t(b) * stride >= cnt) continue;
@@ -785,8 +785,8 @@ __global__ void __launch_bounds__(kThreads)
     // entries of u are distinct, so all 2*kJ loads can be in flight together.
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
-      av[j] = valid[j] ? __ldcg(acc + idx[j]) : 0.f;  // (L2-only random gathers)
-      wv[j] = (valid[j] && w) ? __ldcg(w + idx[j]) : 0.f;
+      av[j] = valid[j] ? ld_rand(acc + idx[j]) : 0.f;  // (L2-only random gathers)
+      wv[j] = (valid[j] && w) ? ld_rand(w + idx[j]) : 0.f;
     }
     unsigned bal[kJ][1];
     bool pred[kJ];

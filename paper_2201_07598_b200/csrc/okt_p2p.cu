@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       av[k] = (acc && !ubits && ok[k]) ? acc[i[k]] : 0.f;
-      wv[k] = (wm && ok[k]) ? wm[i[k]] : 0.f;
+      wv[k] = (wm && ok[k]) ? ld_rand(wm + i[k]) : 0.f;
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
