@@ -14,9 +14,3 @@ timeout 900 $TR --master-port 29512 bench.py --gpus $N --elements 14728266 --p2p
 timeout 1200 $TR --master-port 29513 tools/parity_configs_nccl.py --elements 14728266 --density 0.01 --iters 34 \
     --out "$OUT/parity_vgg_n$N.jsonl" > "$OUT/parity_vgg_n$N.log" 2>&1
 echo done
-# A/B: refresh cost with a blocking NCCL communicator (diagnostics)
-OKT_NCCL_BLOCKING=1 timeout 900 $TR --master-port 29514 bench.py --gpus $N --elements 14728266 --steps 40 \
-    > "$OUT/bench_vgg_n${N}_blocking.log" 2>&1
-timeout 900 $TR --master-port 29515 bench.py --gpus $N --elements 14728266 --steps 40 \
-    > "$OUT/bench_vgg_n${N}_s40.log" 2>&1
-echo done2
