@@ -107,6 +107,7 @@ struct DevScalars {
   okt::RadixState rs;
   uint32_t merge_ctr[2];  // the P2P merge's span tickets (its last CTA re-arms them)
   uint64_t k1_tot[okt::kP2PMaxP + 1];  // P2P K1's totals accumulators (its last CTA publishes and clears them)
+  okt::RadixState rs_sample;  // the cold refresh's sampled candidate threshold
 };
 
 bool is_pow2(int v) { return v >= 1 && (v & (v - 1)) == 0; }
@@ -208,6 +209,7 @@ struct okt_comm {
   Buf agg;                 // phase-B look-back: per-CTA group totals
   uint32_t compact_tag = 0;  // phase-B launch tags (Stage::tag_ctr)
   Buf hist, scal;
+  Buf shist;  // the cold refresh's sample histogram (2048 words)
   okt::Stage S;
   // device-driven multi-GPU exchange (okt_p2p.cuh)
   bool p2p_checked = false, p2p = false;
@@ -255,6 +257,33 @@ struct okt_comm {
     const char* e = std::getenv("OKT_REFRESH_CANDIDATES");
     return !(e && e[0] == '0');
   }();
+  bool refresh_dense_select = true;  // (bytes model) this refresh ran a select-only pass over all of acc
+  // Cold refresh candidates from a sampled threshold, for n >= 2^25 (below
+  // that its five small launches cost more than the select-only pass over acc
+  // it saves: +21 us at n = 14.7M, -137 us at 340M); OKT_COLD_SAMPLE=0: never
+  // (the pass-0 histogram's bin floor and a select-only pass over acc), =1: for every n.
+  int cold_sample_mode = [] {
+    const char* e = std::getenv("OKT_COLD_SAMPLE");
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  bool cold_sample_for(uint64_t n) const {
+    return cold_sample_mode > 0 || (cold_sample_mode < 0 && n >= (uint64_t(1) << 25));
+  }
+  // Sample geometry of a cold refresh: 1 coordinate in 2^s_log2 so that about
+  // E = 1024..2048 samples lie at or above the k-th largest, and the sample
+  // rank q = 1.25 E + 4 sqrt(E): the floor of q's bin then has >= k entries
+  // above it in the whole vector unless the sample is off by ~8 standard
+  // deviations (and then the step falls back to the dense passes).
+  static bool sample_plan(uint64_t n, uint64_t k, uint32_t* s_log2, uint64_t* q) {
+    if (k < 4096 || k >= n) return false;
+    uint32_t s = 0;
+    while (s < 10 && (k >> (s + 1)) >= 1024) ++s;
+    const uint64_t m = (n + (uint64_t(1) << s) - 1) >> s;
+    const double E = double(k) * double(m) / double(n);
+    *s_log2 = s;
+    *q = uint64_t(std::ceil(1.25 * E + 4.0 * std::sqrt(E)));
+    return *q < m;
+  }
   // Steady single-rank step: direct launches (default) or the captured graph (OKT_P1_GRAPH=1).
   bool p1_direct = [] {
     const char* e = std::getenv("OKT_P1_GRAPH");
@@ -1340,11 +1369,24 @@ struct okt_comm {
         // top-11-bit bin holding the k-th largest, and a select-only K1 pass
         // over acc emits everything at or above that bin as the candidates —
         // instead of two more radix passes and a second select pass.
+        // Cold refresh with a large k: the candidate threshold from a strided
+        // sample of acc (a few MB read) instead of pass 0 over all of acc
+        // followed by a second, select-only pass over it (0.40 ms at 340M); the
+        // accumulate pass then emits the candidates as in a warm refresh.
         const bool warm = cand_on && st.local_th > 0.0 && std::isfinite(st.local_th);
+        uint32_t s_log2 = 0;
+        uint64_t s_q = 0;
+        const bool sampled = !warm && cand_on && cold_sample_for(n) && sample_plan(n, k, &s_log2, &s_q);
         bool have_cand = false;  // candidates in coo (AoS) with count d()->R, at least k of them
         uint64_t C_bound = n;    // (grid sizing of the candidate kernels)
-        if (warm) {
-          if (!rc) rc = upload_f64(&d()->th_arg, 0.5 * st.local_th, &hup->th_arg, s);
+        refresh_dense_select = !(warm || sampled);
+        if (warm || sampled) {
+          if (warm) {
+            if (!rc) rc = upload_f64(&d()->th_arg, 0.5 * st.local_th, &hup->th_arg, s);
+          } else if (!rc) {
+            rc = ck(okt::launch_sample_floor(L, g, eps_in, fa, n, s_log2, s_q, &d()->rs_sample, shist.as<uint32_t>(),
+                                             &d()->th_arg), "sample");
+          }
           if (!rc) rc = ck(okt::launch_k1(L, S, okt::K1Mode::kAccumSelectHist, g, eps_in, eps_out, fa, n,
                                           &d()->th_arg, nullptr, okt::OutCoo{coo.as<uint64_t>()}, &d()->R, nullptr,
                                           &d()->flags, hp), "k1");
@@ -1574,12 +1616,12 @@ struct okt_comm {
         sel += 12.0 * uu;
       } else {
         sel += 8.0 * mm;
-        if (thr && sgd) sel += 4.0 * nn;  // the select-only K1 after the fused accumulate+histogram
+        if (thr && sgd && refresh_dense_select) sel += 4.0 * nn;  // the select-only K1 after the accumulate pass
       }
       t_bytes[OKT_T_SELECT] += sel;
       // the streaming kernel alone: reads g (+ eps), writes eps and 8 B per staged entry
       t_bytes[OKT_T_K1] += (sgd ? 12.0 : 4.0) * nn + 8.0 * ((P == 1 && !thr) ? uu : mm) +
-                           ((thr && sgd) ? 4.0 * nn : 0.0);
+                           ((thr && sgd && refresh_dense_select) ? 4.0 * nn : 0.0);
       if (thr) t_bytes[OKT_T_THRESHOLD] += (sgd ? 2.0 : 3.0) * 4.0 * nn;
       if (P > 1) t_bytes[OKT_T_APPLY] += uu * (sgd ? 28.0 : 16.0);
     }
@@ -1687,6 +1729,7 @@ int init_comm(okt_comm* c) {
   c->mask.zero_init = true;
   c->S.max_chunks = dev_sms * 8;
   cudaError_t e = c->hist.ensure(2048 * 4);
+  if (e == cudaSuccess) e = c->shist.ensure(2048 * 4);
   if (e == cudaSuccess) e = c->scal.ensure(sizeof(DevScalars));
   if (e == cudaSuccess) e = c->counts.ensure(4 * size_t(c->S.max_chunks));
   if (e == cudaSuccess) e = c->counts2.ensure(4 * size_t(c->S.max_chunks));

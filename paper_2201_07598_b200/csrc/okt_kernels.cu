@@ -1268,6 +1268,52 @@ cudaError_t launch_radix_pass0_floor(Launch& L, RadixState* d_rs, uint32_t* d_hi
   return cudaGetLastError();
 }
 
+// Sampled pass-0 histogram for the cold refresh's candidate threshold: the
+// same accumulate arithmetic as K1 (fmaf(alpha, g, eps)), the same 2048 bins
+// of the top 11 magnitude bits, over one coordinate per 2^s_log2 block.
+__global__ void __launch_bounds__(kThreads)
+    sample_hist_kernel(const float* __restrict__ g, const float* __restrict__ eps, float alpha, uint64_t n,
+                       uint32_t s_log2, uint64_t m, uint32_t* d_hist) {
+  __shared__ uint32_t s_hist[2048];
+  for (int i = threadIdx.x; i < 2048; i += kThreads) s_hist[i] = 0;
+  __syncthreads();
+  const uint64_t mask = (uint64_t(1) << s_log2) - 1;
+  const uint64_t stride = uint64_t(gridDim.x) * kThreads;
+  constexpr int U = 4;
+  for (uint64_t j0 = uint64_t(blockIdx.x) * kThreads + threadIdx.x; j0 < m; j0 += U * stride) {
+    float gv[U], ev[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t j = j0 + uint64_t(u) * stride;
+      const uint64_t i = (j << s_log2) + ((j * 40503u) & mask);
+      ok[u] = j < m && i < n;
+      gv[u] = ok[u] ? __ldcs(g + i) : 0.f;
+      ev[u] = ok[u] ? __ldcs(eps + i) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) atomicAdd(&s_hist[(__float_as_uint(fmaf(alpha, gv[u], ev[u])) & 0x7fffffffu) >> 20], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += kThreads)
+    if (s_hist[i]) atomicAdd(&d_hist[i], s_hist[i]);
+}
+
+cudaError_t launch_sample_floor(Launch& L, const float* g, const float* eps, float alpha, uint64_t n,
+                                uint32_t s_log2, uint64_t q, RadixState* d_rs, uint32_t* d_hist, double* d_floor) {
+  const uint64_t m = (n + (uint64_t(1) << s_log2) - 1) >> s_log2;
+  cudaError_t e = cudaMemsetAsync(d_hist, 0, 2048 * sizeof(uint32_t), L.s);
+  if (e != cudaSuccess) return e;
+  if ((e = launch_radix_init(L, d_rs, q, m, nullptr)) != cudaSuccess) return e;
+  const uint64_t want = (m + 4 * kThreads - 1) / (4 * kThreads);
+  const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(L.sms) * 4)));
+  sample_hist_kernel<<<grid, kThreads, 0, L.s>>>(g, eps, alpha, n, s_log2, m, d_hist);
+  ++L.launches;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return launch_radix_pass0_floor(L, d_rs, d_hist, d_floor);
+}
+
 cudaError_t launch_radix_init(Launch& L, RadixState* d_rs, uint64_t k, uint64_t n_host,
                               const uint64_t* d_n) {
   radix_init_kernel<<<1, 1, 0, L.s>>>(d_rs, k, n_host, d_n);
@@ -1548,6 +1594,7 @@ void preload_kernels() {
   touch(reinterpret_cast<const void*>(radix_hist_kernel<2>));
   touch(reinterpret_cast<const void*>(radix_pick_kernel));
   touch(reinterpret_cast<const void*>(radix_floor_kernel));
+  touch(reinterpret_cast<const void*>(sample_hist_kernel));
   touch(reinterpret_cast<const void*>(slice_offsets_kernel));
   touch(reinterpret_cast<const void*>(proposals_kernel));
   touch(reinterpret_cast<const void*>(cuts_kernel));

@@ -121,6 +121,12 @@ cudaError_t launch_radix_select(Launch& L, RadixSrc src, const void* data,
 // After a fused pass-0 histogram: the pass-0 pick, then the smallest magnitude
 // of the chosen bin into *d_floor (the cold refresh's candidate threshold).
 cudaError_t launch_radix_pass0_floor(Launch& L, RadixState* d_rs, uint32_t* d_hist, double* d_floor);
+// Cold refresh candidates: the pass-0 bin floor of a strided sample of
+// |eps + alpha * g| (1 in 2^s_log2 coordinates, one pseudo-random pick per
+// block) at sample rank q (from the top), into *d_floor.  d_hist: 2048 words,
+// zeroed here; d_rs: a RadixState of its own.
+cudaError_t launch_sample_floor(Launch& L, const float* g, const float* eps, float alpha, uint64_t n,
+                                uint32_t s_log2, uint64_t q, RadixState* d_rs, uint32_t* d_hist, double* d_floor);
 // Zero-initialises the radix state before a fused pass-0 histogram.
 cudaError_t launch_radix_init(Launch& L, RadixState* d_rs, uint64_t k, uint64_t n_host,
                               const uint64_t* d_n);
