@@ -154,8 +154,16 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
   const uint32_t t_lo = uint32_t(lo / kMergeTile);
   const uint32_t ntiles = W ? uint32_t((hi - 1) / kMergeTile) - t_lo + 1 : 0;
   // survivor chunks: `split` per CTA, handed out by a ticket counter
-  // (split 0: one span per CTA, span = blockIdx.x, no tickets)
+  // (split 0: one span per CTA, span = blockIdx.x, no tickets; bits 8+ of the
+  // argument: a diagnostic permutation of that static assignment)
+  const uint32_t perm = split >> 8;
+  split &= 0xffu;
   const uint32_t Gc = split ? max(1u, min(ntiles, gridDim.x * split)) : gridDim.x;
+  uint32_t span0 = blockIdx.x;
+  if (perm == 1) span0 = gridDim.x - 1 - blockIdx.x;  // reversed
+  else if (perm == 2 && gridDim.x % 148 == 0)         // the CTAs of one SM (b, b + 148, ...) on adjacent spans
+    span0 = (blockIdx.x % 148) * (gridDim.x / 148) + blockIdx.x / 148;
+  else if (perm == 3) span0 = uint32_t((uint64_t(blockIdx.x) * 7919u) % gridDim.x);  // scattered (7919 prime)
   if (blockIdx.x == 0) {
     // this rank's K1 output: status, then L-ready at every rank (the GPU is
     // quiet: K1 finished and nobody streams yet)
@@ -209,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
   constexpr int kS = merge_stages<P>();
   uint32_t* const s_cnt = reinterpret_cast<uint32_t*>(ring + kS * P * kMergeRing);  // [kMergeCntCap][P]
   __shared__ uint32_t s_tk[2];
-  if (q == 0) s_tk[0] = split ? atomicAdd(&ctr[0], 1u) : blockIdx.x;
+  if (q == 0) s_tk[0] = split ? atomicAdd(&ctr[0], 1u) : span0;
   // entries received from each source (the ledger's split words), per thread:
   // reduced once at the end instead of a warp reduce + shared atomic per
   // source and tile
@@ -797,7 +805,9 @@ static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtr
   static const uint32_t split = [] {  // survivor spans per CTA (OKT_MERGE_SPLIT)
     const char* e = std::getenv("OKT_MERGE_SPLIT");
     const int v = e ? std::atoi(e) : kMergeSplit;
-    return uint32_t(std::max(0, std::min(v, 64)));
+    const char* pe = std::getenv("OKT_MERGE_PERM");  // (diagnostics: permuted static spans)
+    const int pm = pe ? std::atoi(pe) : 0;
+    return uint32_t(std::max(0, std::min(v, 64))) | (uint32_t(std::max(0, std::min(pm, 3))) << 8);
   }();
   kern<<<grid, kThreads, smem, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns, split, ctr);
   ++L.launches;
