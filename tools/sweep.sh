@@ -15,8 +15,10 @@ run_cfg() {  # name n density steps cpu_iters ring
   local name=$1 n=$2 dens=$3 steps=$4 cpui=$5 ring=$6 N=1
   while [ "$N" -le "$MAXG" ]; do
     if [ "$N" -eq 1 ]; then
+      local cpu="--cpu-iters $cpui"
+      [ -n "${SWEEP_NO_CPU:-}" ] && cpu="--no-cpu-baseline"  # (SWEEP_NO_CPU=1: skip the reference's CPU leg)
       timeout 1500 python bench.py --elements "$n" --density "$dens" --steps "$steps" --warmup 3 --ring-max "$ring" \
-          --cpu-iters "$cpui" --e2e-steps 3 > "$OUT/${name}_n$N.log" 2>&1
+          $cpu --e2e-steps 3 > "$OUT/${name}_n$N.log" 2>&1
     else
       timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$N" --master-addr 127.0.0.1 \
           --master-port $((29850 + N)) bench.py --gpus "$N" --elements "$n" --density "$dens" --steps "$steps" \
