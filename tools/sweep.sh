@@ -12,7 +12,7 @@ MAXG=${2:-1}
 shift 2 || true
 mkdir -p "$OUT"
 run_cfg() {  # name n density steps cpu_iters ring
-  local name=$1 n=$2 dens=$3 steps=$4 cpui=$5 ring=$6 N=1
+  local name=$1 n=$2 dens=$3 steps=$4 cpui=$5 ring=$6 N=${SWEEP_MIN_N:-1}  # (SWEEP_MIN_N: first N of the doubling)
   while [ "$N" -le "$MAXG" ]; do
     if [ "$N" -eq 1 ]; then
       local cpu="--cpu-iters $cpui"
