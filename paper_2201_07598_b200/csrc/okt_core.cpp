@@ -132,7 +132,7 @@ okt_state default_state() {
 // parity, K1's per-tile staging + tile counts + per-tile cut counts, the
 // merge kernel's per-tile survivor chunks + counts + chunk prefix, and u.
 struct WinLayout {
-  size_t kstg[2], kcnt[2], klt[2], sidx[2], sval[2], scnt[2], spre[2], uidx[2], uval[2], bytes;
+  size_t kstg[2], kcnt[2], klt[2], sidx[2], sval[2], scnt[2], spre[2], sbeg[2], uidx[2], uval[2], bytes;
 };
 WinLayout win_layout(size_t n, int max_chunks) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -151,6 +151,7 @@ WinLayout win_layout(size_t n, int max_chunks) {
     w.sval[p] = o; o += al(8 * sst);
     w.scnt[p] = o; o += al(4 * (kt + 2));  // one survivor chunk per K1 tile of the region
     w.spre[p] = o; o += al(8 * (kt + 3));
+    w.sbeg[p] = o; o += al(4 * (kt + 2));  // first region tile of each survivor chunk
     w.uidx[p] = o; o += al(4 * n);
     w.uval[p] = o; o += al(8 * n);
   }
@@ -803,6 +804,7 @@ struct okt_comm {
         tab.sval[q][p] = reinterpret_cast<double*>(base[q] + lay.sval[p]);
         tab.scnt[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.scnt[p]);
         tab.spre[q][p] = reinterpret_cast<uint64_t*>(base[q] + lay.spre[p]);
+        tab.sbeg[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.sbeg[p]);
         tab.u_idx[q][p] = reinterpret_cast<uint32_t*>(base[q] + lay.uidx[p]);
         tab.u_val[q][p] = reinterpret_cast<double*>(base[q] + lay.uval[p]);
       }

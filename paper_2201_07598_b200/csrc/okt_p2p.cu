@@ -57,6 +57,7 @@ constexpr int kMergeCntCap = 256;
 #ifndef OKT_MERGE_SPLIT_DEFAULT
 #define OKT_MERGE_SPLIT_DEFAULT 0
 #endif
+constexpr int kMergeBalD = 2;  // merge span weights by SM round: 16 - 2 r (16 : 14 : 12 at 3 CTAs per SM)
 constexpr int kMergeSplit = OKT_MERGE_SPLIT_DEFAULT;  // survivor spans per merge CTA, ticketed (0: one, static)                 // tiles whose counts are staged at once
 
 template <int P>
@@ -156,7 +157,8 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
   // survivor chunks: `split` per CTA, handed out by a ticket counter
   // (split 0: one span per CTA, span = blockIdx.x, no tickets; bits 8+ of the
   // argument: a diagnostic permutation of that static assignment)
-  const uint32_t perm = split >> 8;
+  const uint32_t perm = (split >> 8) & 0xffu;
+  const uint32_t bal_d = (split >> 16) & 0xffu, bal_cps = split >> 24;  // static span weights by SM round, see below
   split &= 0xffu;
   const uint32_t Gc = split ? max(1u, min(ntiles, gridDim.x * split)) : gridDim.x;
   uint32_t span0 = blockIdx.x;
@@ -216,6 +218,34 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
   uint64_t* const ring = reinterpret_cast<uint64_t*>(s_val + P * kMergeTile);    // [S][P][kMergeRing]
   constexpr int kS = merge_stages<P>();
   uint32_t* const s_cnt = reinterpret_cast<uint32_t*>(ring + kS * P * kMergeRing);  // [kMergeCntCap][P]
+  // Static spans sized by the CTA's round on its SM: the merge CTAs of one SM
+  // (blocks b, b + R, b + 2R, ... with R = grid / CTAs per SM) do not progress
+  // equally — the SM's warp scheduler favours the older CTA, so with equal
+  // spans at BERT-L N = 2 the first CTA of every SM finished at 135 us and
+  // the third at 174 us, whatever data the spans held (reversed / permuted
+  // span orders moved the slow CTAs with the block index, not with the
+  // span), and the SM ran short-handed meanwhile.  CTA b in round r gets a
+  // span weighted 16 - d r (d = bal_d), so an SM's CTAs finish together.
+  __shared__ uint32_t s_bnd[2];
+  bool wbal = false;
+  // (Only at >= 3 CTAs per SM, P = 2: at P = 4, two per SM, the rounds differed
+  // by 4 %, within the spread of the spans' own costs.)
+  if (!split && perm == 0 && bal_d && bal_cps >= 3 && gridDim.x % bal_cps == 0 && ntiles) {
+    const uint32_t R = gridDim.x / bal_cps;
+    auto f = [&](uint32_t r) -> uint64_t { return uint64_t(max(1, 16 - int(bal_d) * int(r))); };
+    auto C = [&](uint32_t b) -> uint64_t {  // summed weights of blocks < b
+      const uint32_t r = b / R, rem = b % R;
+      uint64_t c = 0;
+      for (uint32_t i = 0; i < r; ++i) c += uint64_t(R) * f(i);
+      return c + uint64_t(rem) * (r < bal_cps ? f(r) : 0);
+    };
+    if (q < 2) {
+      const uint64_t Ct = C(gridDim.x);
+      s_bnd[q] = uint32_t(uint64_t(ntiles) * C(blockIdx.x + uint32_t(q)) / Ct);
+    }
+    wbal = true;
+    __syncthreads();
+  }
   __shared__ uint32_t s_tk[2];
   if (q == 0) s_tk[0] = split ? atomicAdd(&ctr[0], 1u) : span0;
   // entries received from each source (the ledger's split words), per thread:
@@ -242,8 +272,9 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
     trace[(uint64_t(kTrMerge) * kTraceCtas + blockIdx.x) * 4 + 3] = (uint64_t(smid) << 32) | cidx;
   }
   if (q == 0) s_tk[tpar ^ 1] = split ? atomicAdd(&ctr[0], 1u) : Gc;  // (read after this span's barriers)
-  const uint32_t j0 = span_at(cidx, ntiles, Gc);
-  const uint32_t my_n = span_at(cidx + 1, ntiles, Gc) - j0;
+  const uint32_t j0 = wbal ? s_bnd[0] : span_at(cidx, ntiles, Gc);
+  const uint32_t my_n = (wbal ? s_bnd[1] : span_at(cidx + 1, ntiles, Gc)) - j0;
+  if (q == 0) tab->sbeg[me][par][cidx] = j0;  // (the pull finds the chunk's survivors there)
   const uint64_t out_base = uint64_t(j0) * kMergeTile;
   uint32_t running = 0;  // survivors of this span so far (block-uniform)
   for (uint32_t i0 = 0; i0 < my_n; i0 += kMergeCntCap) {
@@ -619,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 3)
       const uint64_t len = end - base;
       OKT_DCHECK(end <= s_off[r + 1], "pull: chunk beyond its rank's survivors", end, s_off[r + 1]);
       const uint64_t lo = max(base + frac_at(len, part, parts), a), hi = min(base + frac_at(len, part + 1, parts), b);
-      const uint64_t cbase = uint64_t(span_at(c, s_tiles[r], s_G[r])) * kMergeTile;
+      const uint64_t cbase = uint64_t(tab->sbeg[r][par][c]) * kMergeTile;  // (the merge's span start)
       const uint32_t* si = tab->sidx[r][par] + cbase;
       const double* sv = tab->sval[r][par] + cbase;
       for (uint64_t p0 = lo; p0 < hi; p0 += 32 * R) {
@@ -807,9 +838,14 @@ static cudaError_t merge_dispatch(Launch& L, const PeerTab* d_tab, const StepPtr
     const int v = e ? std::atoi(e) : kMergeSplit;
     const char* pe = std::getenv("OKT_MERGE_PERM");  // (diagnostics: permuted static spans)
     const int pm = pe ? std::atoi(pe) : 0;
-    return uint32_t(std::max(0, std::min(v, 64))) | (uint32_t(std::max(0, std::min(pm, 3))) << 8);
+    // static spans weighted 16 - d r by the CTA's round r on its SM (OKT_MERGE_BAL=d, default kMergeBalD; 0: equal)
+    const char* be = std::getenv("OKT_MERGE_BAL");
+    const int bd = be ? std::atoi(be) : kMergeBalD;
+    return uint32_t(std::max(0, std::min(v, 64))) | (uint32_t(std::max(0, std::min(pm, 3))) << 8) |
+           (uint32_t(std::max(0, std::min(bd, 15))) << 16);
   }();
-  kern<<<grid, kThreads, smem, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns, split, ctr);
+  const uint32_t cps = uint32_t(std::min(15, std::max(1, cap.load() / std::max(1, L.sms)))) << 24;  // CTAs per SM
+  kern<<<grid, kThreads, smem, L.s>>>(d_tab, sp, plan, lo, W, k1_tiles, d_gth, d_flags, timeout_ns, split | cps, ctr);
   ++L.launches;
   return cudaGetLastError();
 }

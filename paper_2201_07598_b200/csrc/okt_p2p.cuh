@@ -82,6 +82,7 @@ struct PeerTab {
   double* sval[kP2PMaxP][2];
   uint32_t* scnt[kP2PMaxP][2];  // survivors per chunk
   uint64_t* spre[kP2PMaxP][2];  // exclusive prefix of scnt (chunks + 1 entries)
+  uint32_t* sbeg[kP2PMaxP][2];  // first region tile of each survivor chunk (the merge's span)
   uint32_t* u_idx[kP2PMaxP][2]; // allgathered u
   double* u_val[kP2PMaxP][2];
   int P;
