@@ -200,13 +200,12 @@ __global__ void __launch_bounds__(kThreads, P == 2 ? 4 : 2)
   uint32_t* const out_idx = tab->sidx[me][par];
   double* const out_val = tab->sval[me][par];
   uint32_t* const out_cnt = tab->scnt[me][par];
-  // The region's tiles in Gc contiguous spans (a few per CTA), taken by
-  // ticket: the tiles are not equally dense (the later, heavier spans of a
-  // region took 1.3x as long as the first ones at BERT-L, N = 2), and a few
-  // CTAs start late behind the side stream's kernels.  Span c's survivors:
-  // one contiguous chunk at j0 * kMergeTile (the span's capacity), count in
-  // out_cnt[c] — a few hundred large chunks per rank for the pull instead of
-  // one small chunk per tile.  The span's
+  // The region's tiles in Gc contiguous spans: one per CTA (default; sized
+  // by the CTA's round on its SM, below), or `split` per CTA taken by ticket
+  // (OKT_MERGE_SPLIT; slower, DESIGN 7.5).  Span c's survivors: one
+  // contiguous chunk at j0 * kMergeTile (the span's capacity), count in
+  // out_cnt[c], start j0 in sbeg[c] — a few hundred large chunks per rank for
+  // the pull instead of one small chunk per tile.  The span's
   // per-source counts are staged in shared memory first (all loads in flight
   // at once), then a kS-deep ring of TMA bulk copies (cp.async.bulk, one per
   // source and tile, issued by one thread, completion counted in bytes on the
