@@ -69,7 +69,10 @@ size_t stage_entries(uint64_t count, int tile, int max_chunks) {
 // =============================================================================
 // MODE 0: AoS u64 -> AoS u64; 1: AoS u64 -> SoA (u32, f32 widened to f64);
 //      2: SoA -> SoA; 3: u32 -> u32; 4: SoA (u32, f64 holding an f32) -> AoS u64.
-constexpr int kCompactBatch = 4;
+#ifndef OKT_COMPACT_BATCH
+#define OKT_COMPACT_BATCH 4
+#endif
+constexpr int kCompactBatch = OKT_COMPACT_BATCH;
 
 // A CTA copies a group of consecutive chunks (up to kThreads; one chunk per
 // CTA for the static-chunk producers, a few tiles for K1's per-tile staging):
